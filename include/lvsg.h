@@ -1,0 +1,203 @@
+/*
+ * lvsg — B200-native drop-in for the reference `lvs` per-frame
+ * reconstruct + render path (Quark, arXiv 2411.16680).
+ *
+ * C ABI: plain structs, pointers and sizes; no exceptions cross it; every
+ * entry point returns an lvsg_status. Each function cites the reference
+ * interface it replaces (paths relative to the reference's proj/ tree).
+ *
+ * Layouts (identical to the reference's Tensor<float> row-major layouts):
+ *   image        [H, W, 3]              HWC fp32       (network.hpp:369-381)
+ *   LDM depth    [L, Ho, Wo]            fp32, metres   (ldm.hpp:14-21)
+ *   LDM density  [L, Ho, Wo]            fp32 in [0,1]
+ *   LDM blend    [L, Ho, Wo, M]         fp32, post-softmax
+ *   rgb          [Ho, Wo, 3]            fp32           (ldm.hpp:193-199)
+ *   weights      build_params order     (network.hpp:244-317); conv
+ *                [Cout,Cin,3,3], linear [in,out] (tape.hpp:700-706)
+ */
+#ifndef LVSG_H_
+#define LVSG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error classes of the reference (tensor.hpp:15-25, io.hpp:18-31; CLI exit
+ * codes main.cpp:670-693). >= 10: device / runtime failures. */
+typedef enum {
+  LVSG_OK = 0,
+  LVSG_ERR_DIM = 1,      /* DimError: shape / contract violation            */
+  LVSG_ERR_NUMERIC = 2,  /* NumericError: NaN / Inf                          */
+  LVSG_ERR_IO = 3,       /* IoError                                          */
+  LVSG_ERR_CUDA = 10,    /* CUDA runtime failure                             */
+  LVSG_ERR_NO_DEVICE = 11,
+  LVSG_ERR_NCCL = 12,
+  LVSG_ERR_INTERNAL = 13
+} lvsg_status;
+
+/* StepConfig (network.hpp:38-44). `blocks` is the reference block grammar:
+ * comma-separated Bp | U | Lc | A<h> | C (network.hpp:30-36). */
+typedef struct {
+  int64_t in_layers, layers, height, width, pyramid_level;
+  const char* blocks;
+} lvsg_step_config;
+
+/* ModelConfig (network.hpp:46-59). */
+typedef struct {
+  const lvsg_step_config* steps;
+  int64_t num_steps;
+  int64_t channels, views, pyramid_levels;
+  double upsample, near_depth, far_depth;
+  int32_t ablate_render, ablate_attention, ablate_rays, direct_rgb;
+} lvsg_model_config;
+
+/* Camera (camera.hpp:14-41): pinhole, z-depth, texel centres at +0.5;
+ * cam_from_world is a row-major 4x4. */
+typedef struct {
+  double fx, fy, cx, cy;
+  int64_t width, height;
+  double cam_from_world[16];
+} lvsg_camera;
+
+/* Frustum (camera.hpp:54-59). */
+typedef struct {
+  lvsg_camera camera;
+  double near_depth, far_depth;
+} lvsg_frustum;
+
+/* One resolved step of plan_forward (network.hpp:62-72). */
+typedef struct {
+  int64_t in_layers, layers, in_height, in_width, height, width;
+  int32_t doubled;
+  int64_t level, feat_h, feat_w, render_h, render_w, collapse_count, num_tokens;
+} lvsg_step_plan;
+
+#define LVSG_MAX_STEPS 32
+#define LVSG_MAX_LEVELS 16
+
+/* ForwardPlan (network.hpp:74-78). */
+typedef struct {
+  int64_t num_levels;
+  int64_t pyramid_h[LVSG_MAX_LEVELS], pyramid_w[LVSG_MAX_LEVELS];
+  int64_t num_steps;
+  lvsg_step_plan steps[LVSG_MAX_STEPS];
+  int64_t out_height, out_width;
+} lvsg_plan;
+
+/* Optional LDM / diagnostics outputs of lvsg_forward (ForwardResult,
+ * network.hpp:551-558). Any pointer may be NULL. Host pointers. */
+typedef struct {
+  float* depth;        /* [L,Ho,Wo]   */
+  float* density;      /* [L,Ho,Wo]   */
+  float* blend;        /* [L,Ho,Wo,M] */
+  float* blend_logits; /* [L,H,W,M] pre-softmax, volume resolution */
+  float* volume;       /* [L,H,W,C] final feature volume V         */
+} lvsg_ldm_out;
+
+typedef struct lvsg_ctx lvsg_ctx;
+
+/* ---- configuration (pure host, no device) ------------------------------ */
+
+/* ModelConfig::validate (network.cpp:45-103). */
+lvsg_status lvsg_validate_config(const lvsg_model_config* cfg, char* err, size_t err_len);
+/* plan_forward (network.cpp:105-151). */
+lvsg_status lvsg_plan_forward(const lvsg_model_config* cfg, int64_t image_h, int64_t image_w,
+                              lvsg_plan* out, char* err, size_t err_len);
+/* Parameter list of build_params (network.hpp:244-317): count, then per
+ * index the shape (rank <= 4). */
+lvsg_status lvsg_param_count(const lvsg_model_config* cfg, int64_t* count, int64_t* total_numel);
+lvsg_status lvsg_param_shape(const lvsg_model_config* cfg, int64_t index, int32_t* rank,
+                             int64_t dims[4]);
+/* init_param_store<float>(cfg, seed) (network.hpp:354-362), bit-exact:
+ * mt19937_64 + Box-Muller (rng.hpp:14-51). `out` holds total_numel floats,
+ * tensors concatenated in build_params order. */
+lvsg_status lvsg_init_param_store(const lvsg_model_config* cfg, uint64_t seed, float* out);
+
+/* ---- context ------------------------------------------------------------ */
+
+/* Creates a context bound to CUDA device `device`: validates cfg, owns the
+ * device weights, one CUDA stream and the per-frame scratch arena. */
+lvsg_status lvsg_create(const lvsg_model_config* cfg, int32_t device, lvsg_ctx** out);
+void lvsg_destroy(lvsg_ctx* ctx);
+/* Message of the last failure on this context (or of lvsg_create when ctx
+ * is NULL). */
+const char* lvsg_last_error(const lvsg_ctx* ctx);
+
+/* bind_params(cfg, store) (network.hpp:330-339): `count` tensors in
+ * build_params order with their shapes (ranks[i], dims concatenated). Shape
+ * mismatches and wrong counts -> LVSG_ERR_DIM. */
+lvsg_status lvsg_load_weights(lvsg_ctx* ctx, int64_t count, const float* const* tensors,
+                              const int32_t* ranks, const int64_t* dims);
+/* init_params(cfg, seed) on the host, uploaded (network.hpp:321-328). */
+lvsg_status lvsg_init_weights(lvsg_ctx* ctx, uint64_t seed);
+
+/* forward() (network.hpp:562-603) on host buffers: M images [H,W,3] (the
+ * encoder resolution), M cameras, target frustum. The LDM stays resident on
+ * the device for lvsg_render; `out` (optional) receives host copies. */
+lvsg_status lvsg_forward(lvsg_ctx* ctx, int64_t views, const float* const* images, int64_t height,
+                         int64_t width, const lvsg_camera* cams, const lvsg_frustum* target,
+                         const lvsg_ldm_out* out);
+/* render_target() (ldm.hpp:193-199) of the resident LDM against M images
+ * [Hr,Wr,3] with their own cameras (the render resolution may differ from
+ * the encoder's). rgb_out: host [Ho,Wo,3]. */
+lvsg_status lvsg_render(lvsg_ctx* ctx, int64_t views, const float* const* images, int64_t height,
+                        int64_t width, const lvsg_camera* cams, float* rgb_out);
+/* forward() + render_target() in one call (the CLI forward-demo path,
+ * main.cpp:533-541). */
+lvsg_status lvsg_forward_render(lvsg_ctx* ctx, int64_t views, const float* const* enc_images,
+                                int64_t enc_h, int64_t enc_w, const lvsg_camera* enc_cams,
+                                const float* const* render_images, int64_t render_h,
+                                int64_t render_w, const lvsg_camera* render_cams,
+                                const lvsg_frustum* target, float* rgb_out);
+
+/* Device-resident variant: enc_images [M,He,We,3] and render_images
+ * [M,Hr,Wr,3] are contiguous DEVICE buffers, rgb_out a DEVICE buffer
+ * [Ho,Wo,3]; work is enqueued on `stream` (cudaStream_t, NULL = the
+ * context's stream) and the call returns without synchronising. */
+lvsg_status lvsg_forward_render_device(lvsg_ctx* ctx, int64_t views, const float* enc_images,
+                                       int64_t enc_h, int64_t enc_w, const lvsg_camera* enc_cams,
+                                       const float* render_images, int64_t render_h,
+                                       int64_t render_w, const lvsg_camera* render_cams,
+                                       const lvsg_frustum* target, float* rgb_out, void* stream);
+
+/* Row-band render for output sharding across GPUs: renders
+ * output rows [row0,row1) of the resident LDM into rgb_out (device,
+ * [row1-row0, Wo, 3]). Bit-identical to the same rows of a full render. */
+lvsg_status lvsg_render_rows_device(lvsg_ctx* ctx, int64_t views, const float* render_images,
+                                    int64_t render_h, int64_t render_w,
+                                    const lvsg_camera* render_cams, int64_t row0, int64_t row1,
+                                    float* rgb_out, void* stream);
+
+/* Synchronise the context stream; returns the first asynchronous error. */
+lvsg_status lvsg_synchronize(lvsg_ctx* ctx);
+
+/* Per-frame kernel-launch count of the last forward_render (for the bench's
+ * gpu_launches claim) and the CUDA stream the context enqueues on. */
+int64_t lvsg_last_launch_count(const lvsg_ctx* ctx);
+void* lvsg_stream(lvsg_ctx* ctx);
+
+/* ---- stage entry points (per-stage parity, SURVEY.md §7 hard part 2) -----
+ * DEVICE pointers, run on the context stream and synchronised. */
+
+/* geo::world_points (geometry.hpp:84-129): depth [L,H,W] -> points
+ * [L,H,W,3]. Out-of-range depth -> LVSG_ERR_DIM (checked on the device). */
+lvsg_status lvsg_stage_world_points(lvsg_ctx* ctx, const lvsg_frustum* fr, const float* depth,
+                                    int64_t L, int64_t H, int64_t W, float* points);
+/* geo::footprint + CamPod::to_cam over points [P,3] (geometry.hpp:34-79,
+ * :152-160): x0,x1,y0,y1 (int32, 4 per point), valid (uint8), fx,fy (f64). */
+lvsg_status lvsg_stage_footprints(lvsg_ctx* ctx, const lvsg_camera* cam, const float* points,
+                                  int64_t P, int32_t* taps, uint8_t* valid, double* fracs);
+/* geo::gather_backproject (geometry.hpp:138-224): image [Hi,Wi,C], points
+ * [P,3] -> values [P,C] (zero where invalid) and mask [P]. */
+lvsg_status lvsg_stage_gather(lvsg_ctx* ctx, const lvsg_camera* cam, const float* image,
+                              int64_t Hi, int64_t Wi, int64_t C, const float* points, int64_t P,
+                              float* values, float* mask);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LVSG_H_ */

@@ -1,0 +1,119 @@
+"""ModelConfig / StepConfig mirror of the reference (network.hpp:38-59) and the
+presets the benchmarks and tests run on.
+
+The validation and planning rules themselves live in the native host library
+(csrc/host.cpp: `lvsg_validate_config`, `lvsg_plan_forward`, restating
+network.cpp:8-151); this module only carries the values across the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field, replace
+from typing import List
+
+from . import capi
+
+
+@dataclass
+class StepConfig:
+    """network.hpp:38-44."""
+
+    in_layers: int
+    layers: int
+    height: int
+    width: int
+    pyramid_level: int
+    blocks: str
+
+
+@dataclass
+class ModelConfig:
+    """network.hpp:46-59 (`near`/`far` keep the reference names)."""
+
+    steps: List[StepConfig] = field(default_factory=list)
+    channels: int = 0
+    views: int = 0
+    pyramid_levels: int = 0
+    upsample: float = 1.0
+    near: float = 0.0
+    far: float = 0.0
+    ablate_render: bool = False
+    ablate_attention: bool = False
+    ablate_rays: bool = False
+    direct_rgb: bool = False
+
+    def with_views(self, m: int) -> "ModelConfig":
+        return replace(self, views=m, steps=list(self.steps))
+
+    # --- C ABI ---------------------------------------------------------------
+    def to_c(self) -> "CConfig":
+        return CConfig(self)
+
+
+class CConfig:
+    """Owns the ctypes storage behind an lvsg_model_config."""
+
+    def __init__(self, cfg: ModelConfig):
+        n = len(cfg.steps)
+        self._blocks = [s.blocks.encode() for s in cfg.steps]
+        self._steps = (capi.StepConfig * max(n, 1))()
+        for i, s in enumerate(cfg.steps):
+            self._steps[i] = capi.StepConfig(s.in_layers, s.layers, s.height, s.width,
+                                             s.pyramid_level, self._blocks[i])
+        self.c = capi.ModelConfigC(
+            ctypes.cast(self._steps, ctypes.POINTER(capi.StepConfig)), n, cfg.channels,
+            cfg.views, cfg.pyramid_levels, float(cfg.upsample), float(cfg.near), float(cfg.far),
+            int(cfg.ablate_render), int(cfg.ablate_attention), int(cfg.ablate_rays),
+            int(cfg.direct_rgb))
+
+    @property
+    def ptr(self):
+        return ctypes.byref(self.c)
+
+
+def nano_config() -> ModelConfig:
+    """network.cpp:153-168."""
+    return ModelConfig(
+        steps=[StepConfig(8, 8, 8, 8, 2, "Bp,A2,C"),
+               StepConfig(8, 8, 8, 8, 2, "U,A2,C,C"),
+               StepConfig(8, 8, 16, 16, 1, "U,A2,C"),
+               StepConfig(8, 4, 32, 32, 0, "Lc,U,A1,C")],
+        channels=8, views=4, pyramid_levels=3, upsample=2.0, near=1.0, far=6.0)
+
+
+def full_scale_config() -> ModelConfig:
+    """network.cpp:170-187 (Table 6 schedule, 1080p output from 576x960 input)."""
+    return ModelConfig(
+        steps=[StepConfig(24, 24, 36, 64, 3, "Bp,A4,C,C,A4,C,C,A4,C,C"),
+               StepConfig(24, 24, 36, 64, 3, "U,A4,C,C,A4,C,C,A4,C,C"),
+               StepConfig(24, 24, 72, 128, 2, "U,A4,C,C,A4,C,C,A4,C,C"),
+               StepConfig(24, 24, 72, 128, 2, "U,A4,C,A4,C"),
+               StepConfig(24, 12, 144, 256, 1, "Lc,U,A2,C,A2,C"),
+               StepConfig(12, 6, 288, 512, 0, "Lc,U,A1,C,A1,C")],
+        channels=32, views=8, pyramid_levels=4, upsample=3.75, near=0.5, far=100.0)
+
+
+def config1() -> ModelConfig:
+    """BASELINE config 1: 4 views 256^2, C=32, Bp + 2 U&F steps."""
+    return ModelConfig(
+        steps=[StepConfig(8, 8, 32, 32, 2, "Bp,A4,C,C"),
+               StepConfig(8, 8, 64, 64, 1, "U,A2,C"),
+               StepConfig(8, 4, 64, 64, 1, "Lc,U,A1,C")],
+        channels=32, views=4, pyramid_levels=3, upsample=4.0, near=1.0, far=20.0)
+
+
+def micro_config() -> ModelConfig:
+    """tests/test_network.cpp:27-40 (2 views, C=4)."""
+    return ModelConfig(
+        steps=[StepConfig(2, 2, 4, 4, 1, "Bp,A1,C"), StepConfig(2, 2, 8, 8, 0, "U,A1,C")],
+        channels=4, views=2, pyramid_levels=2, upsample=1.0, near=1.0, far=5.0)
+
+
+def scaled_full_config(div: int = 4) -> ModelConfig:
+    """full_scale_config with every volume extent divided by `div` (same
+    schedule, layers, channels and views; 1/div^2 of the texels). Used as the
+    bounded CPU-baseline sample of config 2 (encoder input 576/div x 960/div)."""
+    base = full_scale_config()
+    steps = [StepConfig(s.in_layers, s.layers, s.height // div, s.width // div, s.pyramid_level,
+                        s.blocks) for s in base.steps]
+    return replace(base, steps=steps)
