@@ -196,6 +196,18 @@ lvsg_status lvsg_stage_gather(lvsg_ctx* ctx, const lvsg_camera* cam, const float
                               int64_t Hi, int64_t Wi, int64_t C, const float* points, int64_t P,
                               float* values, float* mask);
 
+/* ---- synthetic inputs (host; the benchmarks' generator) -----------------
+ * RigSpec::cameras / ::target (scenes.cpp:40-60): rows*cols cameras, row
+ * major; target may be NULL. */
+lvsg_status lvsg_rig_cameras(int64_t rows, int64_t cols, double baseline, int64_t width,
+                             int64_t height, double focal, lvsg_camera* cams,
+                             lvsg_camera* target);
+/* make_scene(seed, planes, scene_fr) + oracle_render per camera, f64 -> f32
+ * (scenes.cpp:62-171). images: views contiguous [H_m, W_m, 3] blocks. */
+lvsg_status lvsg_scene_images(uint64_t seed, int64_t planes, const lvsg_frustum* scene_fr,
+                              int64_t views, const lvsg_camera* cams, float* images, char* err,
+                              size_t err_len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -98,7 +98,7 @@ SYMBOLS = [
     "lvsg_load_weights", "lvsg_init_weights", "lvsg_forward", "lvsg_render",
     "lvsg_forward_render", "lvsg_forward_render_device", "lvsg_render_rows_device",
     "lvsg_synchronize", "lvsg_last_launch_count", "lvsg_stream", "lvsg_stage_world_points",
-    "lvsg_stage_footprints", "lvsg_stage_gather",
+    "lvsg_stage_footprints", "lvsg_stage_gather", "lvsg_rig_cameras", "lvsg_scene_images",
 ]
 
 
@@ -144,5 +144,9 @@ def lib() -> ctypes.CDLL:
     L.lvsg_stage_world_points.argtypes = [vp, P(FrustumC), vp, c_i64, c_i64, c_i64, vp]
     L.lvsg_stage_footprints.argtypes = [vp, P(CameraC), vp, c_i64, vp, vp, vp]
     L.lvsg_stage_gather.argtypes = [vp, P(CameraC), vp, c_i64, c_i64, c_i64, vp, c_i64, vp, vp]
+    L.lvsg_rig_cameras.argtypes = [c_i64, c_i64, c_f64, c_i64, c_i64, c_f64, P(CameraC),
+                                   P(CameraC)]
+    L.lvsg_scene_images.argtypes = [ctypes.c_uint64, c_i64, P(FrustumC), c_i64, P(CameraC), vp,
+                                    ctypes.c_char_p, ctypes.c_size_t]
     _lib = L
     return L

@@ -1,0 +1,138 @@
+// conv3x3 on channel-last fp32 maps: SIMT implicit GEMM.
+//
+// Semantics: kernels_ref.hpp:72-96 (y = b + sum_{ci,di,dj} w*x with zero
+// padding), accumulated in the reference's (ci, dy, dx) order starting from
+// the bias, with FFMA (fp32-accurate; see SURVEY.md §7 hard part 2 for why the
+// solve path stays fp32 at 1080p).
+//
+// Tiling: one CTA = 8x32 output pixels x 32 output channels, 128 threads.
+// Warp w owns couts [8w, 8w+8); lane (r = lane/4, q = lane%4) owns the 8
+// pixels of row r, columns [8q, 8q+8). Input channels stream through shared
+// memory 8 at a time as a (8+2)x(32+2) halo tile (row pitch 36 floats so every
+// lane's 8-wide window is 16-byte aligned and conflict-free); the 9x8x32
+// weight slab is read with warp-broadcast LDS.128.
+#include "kernels.h"
+
+namespace lvsg {
+namespace {
+
+constexpr int TH = 8, TW = 32, CK = 8, HP = TH + 2, WP = 36, COT = 32;
+constexpr int NT = 128;
+
+__device__ __forceinline__ float load_src(const ConvArgs& a, int b, int pix, int ch) {
+  // channel -> source (concat_last order)
+  int c = ch;
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    if (s < a.nsrc) {
+      const ConvSrc& S = a.src[s];
+      if (c < S.C) return __ldg(S.ptr + (long long)b * S.bstride + (long long)pix * S.pstride + c);
+      c -= S.C;
+    }
+  }
+  return 0.f;
+}
+
+__global__ void __launch_bounds__(NT) conv3x3_kernel(const ConvArgs a) {
+  __shared__ __align__(16) float s_in[CK * HP * WP];
+  __shared__ __align__(16) float s_w[9 * CK * COT];
+
+  const int tiles_x = (a.W + TW - 1) / TW;
+  const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+  const int x0 = tx * TW, y0 = ty * TH;
+  const int co_base = blockIdx.y * COT;
+  const int b = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int r = lane >> 2, q = lane & 3;
+  const int cw = co_base + warp * 8;  // first cout of this warp
+
+  float acc[8][8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int co = cw + c;
+    const float bv = (a.bias && co < a.Cout) ? __ldg(a.bias + co) : 0.f;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) acc[p][c] = bv;
+  }
+
+  const int HW = a.H * a.W;
+  for (int c0 = 0; c0 < a.Cin; c0 += CK) {
+    __syncthreads();
+    // stage the input halo tile: element e -> (pixel, channel-in-chunk)
+    for (int e = tid; e < HP * (TW + 2) * CK; e += NT) {
+      const int ch = e % CK, pix = e / CK;
+      const int hy = pix / (TW + 2), hx = pix % (TW + 2);
+      const int gy = y0 - 1 + hy, gx = x0 - 1 + hx, gc = c0 + ch;
+      float v = 0.f;
+      if (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W && gc < a.Cin) {
+        const int gp = gy * a.W + gx;
+        v = load_src(a, b, gp, gc);
+        if (a.rinv) v = fm(fm(v, __ldg(a.rinv + (long long)b * HW + gp)), __ldg(a.gain + gc));
+      }
+      s_in[(ch * HP + hy) * WP + hx] = v;
+    }
+    // stage the weight slab [tap][ci][co]
+    for (int e = tid; e < 9 * CK * COT; e += NT) {
+      const int tap = e % 9, rest = e / 9;
+      const int ci = rest % CK, co = rest / CK;
+      const int gci = c0 + ci, gco = co_base + co;
+      float v = 0.f;
+      if (gci < a.Cin && gco < a.Cout) v = __ldg(a.w + ((long long)gco * a.Cin + gci) * 9 + tap);
+      s_w[(tap * CK + ci) * COT + co] = v;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int ci = 0; ci < CK; ++ci) {
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy) {
+        const float* row = s_in + (ci * HP + r + dy) * WP + 8 * q;
+        const float4 v0 = *reinterpret_cast<const float4*>(row);
+        const float4 v1 = *reinterpret_cast<const float4*>(row + 4);
+        const float2 v2 = *reinterpret_cast<const float2*>(row + 8);
+        const float xin[10] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w, v2.x, v2.y};
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+          const float* wr = s_w + ((dy * 3 + dx) * CK + ci) * COT + warp * 8;
+          const float4 wa = *reinterpret_cast<const float4*>(wr);
+          const float4 wb = *reinterpret_cast<const float4*>(wr + 4);
+          const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+          for (int p = 0; p < 8; ++p)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[p][c] = fmaf(xin[p + dx], wv[c], acc[p][c]);
+        }
+      }
+    }
+  }
+
+  // epilogue: GELU, residual, store
+  const int gy = y0 + r;
+  if (gy >= a.H) return;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int gx = x0 + 8 * q + p;
+    if (gx >= a.W) continue;
+    const long long pix = (long long)gy * a.W + gx;
+    float* o = a.out + (long long)b * a.out_bstride + pix * a.out_pstride;
+    const float* rs = a.resid ? a.resid + (long long)b * a.res_bstride + pix * a.res_pstride : nullptr;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int co = cw + c;
+      if (co >= a.Cout) continue;
+      float y = acc[p][c];
+      if (a.gelu) y = gelu_ref(y);
+      if (rs) y = fa(rs[co], y);
+      o[co] = y;
+    }
+  }
+}
+
+}  // namespace
+
+void conv3x3(const ConvArgs& a, cudaStream_t st) {
+  const int tiles = ((a.W + TW - 1) / TW) * ((a.H + TH - 1) / TH);
+  dim3 grid(tiles, (a.Cout + COT - 1) / COT, a.B);
+  conv3x3_kernel<<<grid, NT, 0, st>>>(a);
+}
+
+}  // namespace lvsg

@@ -1,0 +1,769 @@
+// Memory-bound lvsg kernels: layout/elementwise, ray encodings, the Stage-1
+// reprojection gather, the render-to-input-view splat, and the per-texel
+// One-to-many attention / blend-logit / layer-collapse MLPs.
+#include <cfloat>
+
+#include "kernels.h"
+
+namespace lvsg {
+namespace {
+
+constexpr int kMaxM = 32;  // views handled per texel in registers
+
+inline int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
+
+// ----------------------------------------------------------------------------
+// elementwise / layout
+// ----------------------------------------------------------------------------
+
+__global__ void fill_rows_kernel(float* out, const float* row, int64_t rows, int C) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows * C) return;
+  // matmul(ones[P,1], f[1,C]) == 0 + 1*f (network.hpp:466-467)
+  out[i] = fa(0.f, fm(1.f, row[i % C]));
+}
+
+__global__ void fill_layers_kernel(float* out, const float* per_layer, int L, int64_t P) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= L * P) return;
+  out[i] = per_layer[i / P];
+}
+
+__global__ void fill_anchor_depths_kernel(float* out, int L, int64_t P, double inv_span,
+                                          double inv_far) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= L * P) return;
+  const int l = int(i / P);
+  const float a = __double2float_rn(dd(double(l) + 0.5, double(L)));
+  out[i] = __double2float_rn(dd(1.0, da(dm(double(a), inv_span), inv_far)));
+}
+
+// mean_pool2 (tape.hpp:816-836): ((a+b)+c+d)*0.25, channel-last.
+__global__ void mean_pool2_kernel(const float* in, float* out, int B, int H, int W, int C) {
+  const int Ho = H / 2, Wo = W / 2;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)B * Ho * Wo * C;
+  if (i >= n) return;
+  const int c = int(i % C);
+  int64_t t = i / C;
+  const int x = int(t % Wo);
+  t /= Wo;
+  const int y = int(t % Ho);
+  const int b = int(t / Ho);
+  const float* s = in + (int64_t)b * H * W * C;
+  const float v00 = s[((int64_t)(2 * y) * W + 2 * x) * C + c];
+  const float v01 = s[((int64_t)(2 * y) * W + 2 * x + 1) * C + c];
+  const float v10 = s[((int64_t)(2 * y + 1) * W + 2 * x) * C + c];
+  const float v11 = s[((int64_t)(2 * y + 1) * W + 2 * x + 1) * C + c];
+  out[i] = fm(fa(fa(fa(v00, v01), v10), v11), 0.25f);
+}
+
+__global__ void resize_hwc_kernel(const float* in, float* out, int B, int H, int W, int C, int Ho,
+                                  int Wo) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)B * Ho * Wo * C;
+  if (i >= n) return;
+  const int c = int(i % C);
+  int64_t t = i / C;
+  const int x = int(t % Wo);
+  t /= Wo;
+  const int y = int(t % Ho);
+  const int b = int(t / Ho);
+  int y0, y1, x0, x1;
+  float fy, fx;
+  resize_tap(y, H, Ho, y0, y1, fy);
+  resize_tap(x, W, Wo, x0, x1, fx);
+  const float* s = in + (int64_t)b * H * W * C;
+  out[i] = lerp2(s[((int64_t)y0 * W + x0) * C + c], s[((int64_t)y0 * W + x1) * C + c],
+                 s[((int64_t)y1 * W + x0) * C + c], s[((int64_t)y1 * W + x1) * C + c], fx, fy);
+}
+
+// One warp per row: rinv = 1 / sqrt(sum(x^2)/C + 1e-6).
+__global__ void rms_rinv_kernel(const float* x, float* rinv, int64_t rows, int C) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  float s = 0.f;
+  for (int c = lane; c < C; c += 32) {
+    const float v = x[row * C + c];
+    s = fmaf(v, v, s);
+  }
+  s = warp_sum(s);
+  if (lane == 0) rinv[row] = __fdiv_rn(1.0f, __fsqrt_rn(fa(__fdiv_rn(s, float(C)), 1e-6f)));
+}
+
+// ----------------------------------------------------------------------------
+// ray encodings
+// ----------------------------------------------------------------------------
+
+// ray_plane_delta + ray_encoding_base (geometry.hpp:343-391): [M, h, w, 32].
+__global__ void ray_base_kernel(const RayBaseCam* cams, RayBaseArgs a, float* base) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)a.M * a.h * a.w) return;
+  const int j = int(i % a.w);
+  const int ii = int((i / a.w) % a.h);
+  const int m = int(i / ((int64_t)a.w * a.h));
+  const RayBaseCam& g = cams[m];
+  const double d0 = dd(ds(double(j) + 0.5, g.cx), g.fx);
+  const double d1 = dd(ds(double(ii) + 0.5, g.cy), g.fy);
+  double dw[3], d[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    dw[r] = da(da(dm(g.Rwc_in[r * 3 + 0], d0), dm(g.Rwc_in[r * 3 + 1], d1)), dm(g.Rwc_in[r * 3 + 2], 1.0));
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    d[r] = da(da(dm(a.Rcw_t[r * 3 + 0], dw[0]), dm(a.Rcw_t[r * 3 + 1], dw[1])), dm(a.Rcw_t[r * 3 + 2], dw[2]));
+  const double dz = d[2] >= 0 ? fmax(d[2], 1e-6) : fmin(d[2], -1e-6);
+  const double sx = ds(g.o[0], dm(dd(d[0], dz), g.o[2]));
+  const double sy = ds(g.o[1], dm(dd(d[1], dz), g.o[2]));
+  const double e[2] = {tanh(dd(dm(dm(a.tfx, sx), a.inv_span), a.half_w)),
+                       tanh(dd(dm(dm(a.tfy, sy), a.inv_span), a.half_h))};
+  float* out = base + i * 32;
+#pragma unroll
+  for (int comp = 0; comp < 2; ++comp)
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+      const double arg = dm(3.141592653589793 * double(1 << o), e[comp]);
+      double sv, cv;
+      sincos(arg, &sv, &cv);
+      out[comp * 16 + 2 * o] = __double2float_rn(sv);
+      out[comp * 16 + 2 * o + 1] = __double2float_rn(cv);
+    }
+}
+
+// rays_k[p, c] = sum_f resize(base)[p, f] * proj[f, c] (network.hpp:405-411).
+__global__ void ray_project_kernel(const float* base, int M, int hK, int wK, int Hk, int Wk,
+                                   const float* proj, int C, float* out) {
+  extern __shared__ float s_proj[];
+  for (int e = threadIdx.x; e < 32 * C; e += blockDim.x) s_proj[e] = proj[e];
+  __syncthreads();
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)M * Hk * Wk) return;
+  const int x = int(i % Wk);
+  const int y = int((i / Wk) % Hk);
+  const int m = int(i / ((int64_t)Wk * Hk));
+  const float* b = base + (int64_t)m * hK * wK * 32;
+  float f[32];
+  if (Hk == hK && Wk == wK) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) f[k] = b[((int64_t)y * wK + x) * 32 + k];
+  } else {
+    int y0, y1, x0, x1;
+    float fy, fx;
+    resize_tap(y, hK, Hk, y0, y1, fy);
+    resize_tap(x, wK, Wk, x0, x1, fx);
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      f[k] = lerp2(b[((int64_t)y0 * wK + x0) * 32 + k], b[((int64_t)y0 * wK + x1) * 32 + k],
+                   b[((int64_t)y1 * wK + x0) * 32 + k], b[((int64_t)y1 * wK + x1) * 32 + k], fx, fy);
+  }
+  float* o = out + i * C;
+  for (int c = 0; c < C; ++c) {
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) acc = fmaf(f[k], s_proj[k * C + c], acc);
+    o[c] = acc;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Stage 1: reprojection + bilinear feature gather
+// ----------------------------------------------------------------------------
+
+// One thread per (texel, view, 4-channel group). The world point and the
+// footprint are recomputed per group (f64, bit-exact order); the four taps
+// are read as float4 (HWC, 16-byte aligned when C % 4 == 0).
+template <bool kVec4>
+__global__ void gather_stack_kernel(const float* __restrict__ feats, int M, int Hf, int Wf, int C,
+                                    const DevCam* __restrict__ cams, DevRayCam rc,
+                                    const float* __restrict__ depth, int L, int H, int W,
+                                    float* __restrict__ deltas) {
+  const int G = kVec4 ? C / 4 : C;
+  const int64_t total = (int64_t)L * H * W * M * G;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int g = int(i % G);
+  int64_t t = i / G;
+  const int m = int(t % M);
+  const int64_t p = t / M;
+  const int j = int(p % W);
+  const int ii = int((p / W) % H);
+  float pt[3];
+  world_point(rc, ii, j, __ldg(depth + p), pt);
+  const DevCam cam = cams[m];
+  const Footprint f = project_footprint(cam, pt);
+  float* o = deltas + (p * M + m) * C;
+  if (!f.valid) {
+    if (kVec4)
+      reinterpret_cast<float4*>(o)[g] = make_float4(0.f, 0.f, 0.f, 0.f);
+    else
+      o[g] = 0.f;
+    return;
+  }
+  double w[4];
+  bilinear_weights(f, w);
+  const float* img = feats + (int64_t)m * Hf * Wf * C;
+  const float* i00 = img + ((int64_t)f.y0 * Wf + f.x0) * C;
+  const float* i10 = img + ((int64_t)f.y0 * Wf + f.x1) * C;
+  const float* i01 = img + ((int64_t)f.y1 * Wf + f.x0) * C;
+  const float* i11 = img + ((int64_t)f.y1 * Wf + f.x1) * C;
+  if (kVec4) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(i00) + g);
+    const float4 b = __ldg(reinterpret_cast<const float4*>(i10) + g);
+    const float4 c = __ldg(reinterpret_cast<const float4*>(i01) + g);
+    const float4 d = __ldg(reinterpret_cast<const float4*>(i11) + g);
+    reinterpret_cast<float4*>(o)[g] =
+        make_float4(blend4(w, a.x, b.x, c.x, d.x), blend4(w, a.y, b.y, c.y, d.y),
+                    blend4(w, a.z, b.z, c.z, d.z), blend4(w, a.w, b.w, c.w, d.w));
+  } else {
+    o[g] = blend4(w, __ldg(i00 + g), __ldg(i10 + g), __ldg(i01 + g), __ldg(i11 + g));
+  }
+}
+
+// ----------------------------------------------------------------------------
+// render_to_input_view: decode, splat, composite
+// ----------------------------------------------------------------------------
+
+// One thread per texel: a = sigmoid(V w_a) [Ca], sigma, depth, world point.
+__global__ void decode_payload_kernel(const float* __restrict__ V, int L, int H, int W, int C,
+                                      const float* __restrict__ w_appear, int Ca,
+                                      const float* __restrict__ w_sigma,
+                                      const float* __restrict__ w_depth, DepthAct act, DevRayCam rc,
+                                      float* payload, float* depth, float* points) {
+  extern __shared__ float s_w[];  // [C, Ca+2]: appear | sigma | depth
+  const int K2 = Ca + 2;
+  for (int e = threadIdx.x; e < C * K2; e += blockDim.x) {
+    const int k = e / K2, c = e % K2;
+    s_w[e] = c < Ca ? w_appear[k * Ca + c] : (c == Ca ? w_sigma[k] : w_depth[k]);
+  }
+  __syncthreads();
+  const int64_t P = (int64_t)L * H * W;
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const float* v = V + p * C;
+  float* pay = payload + p * (Ca + 1);
+  // matmul order: k ascending from 0 (kernels_ref.hpp:40-48)
+  for (int c = 0; c < Ca + 2; ++c) {
+    float acc = 0.f;
+    for (int k = 0; k < C; ++k) acc = fmaf(v[k], s_w[k * K2 + c], acc);
+    if (c < Ca + 1) {
+      pay[c] = sigmoid_ref(acc);
+    } else {
+      const int l = int(p / ((int64_t)H * W));
+      const float d = activate_depth(acc, l, act);
+      depth[p] = d;
+      const int j = int(p % W), i = int((p / W) % H);
+      float pt[3];
+      world_point(rc, i, j, d, pt);
+      points[p * 3 + 0] = pt[0];
+      points[p * 3 + 1] = pt[1];
+      points[p * 3 + 2] = pt[2];
+    }
+  }
+}
+
+// One warp per (texel, view): lanes stride the K payload channels + weight.
+__global__ void splat_kernel(const float* __restrict__ payload, const float* __restrict__ points,
+                             int L, int PL, int K, const DevCam* __restrict__ cams, int M, int Hv,
+                             int Wv, float* acc) {
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t P = (int64_t)L * PL;
+  if (wid >= P * M) return;
+  const int m = int(wid % M);
+  const int64_t p = wid / M;
+  const int l = int(p / PL);
+  const float pt[3] = {points[p * 3], points[p * 3 + 1], points[p * 3 + 2]};
+  const Footprint f = project_footprint(cams[m], pt);
+  if (!f.valid) return;
+  double w[4];
+  bilinear_weights(f, w);
+  const int64_t base = (int64_t)m * L * Hv * Wv + (int64_t)l * Hv * Wv;
+  const int64_t tap[4] = {base + (int64_t)f.y0 * Wv + f.x0, base + (int64_t)f.y0 * Wv + f.x1,
+                          base + (int64_t)f.y1 * Wv + f.x0, base + (int64_t)f.y1 * Wv + f.x1};
+  for (int c = lane; c < K + 1; c += 32) {
+    const float val = c < K ? payload[p * K + c] : 1.0f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float wk = __double2float_rn(w[k]);
+      atomicAdd(acc + tap[k] * (K + 1) + c, c < K ? fm(wk, val) : wk);
+    }
+  }
+}
+
+// One thread per (view pixel, output channel): normalise by max(wsum,1e-4)
+// then composite back to front (geometry.hpp:317-326; ldm.hpp:98-115).
+__global__ void splat_composite_kernel(const float* __restrict__ acc, int M, int L, int Hv, int Wv,
+                                       int K, float* out) {
+  const int64_t PV = (int64_t)Hv * Wv;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)M * PV * K) return;
+  const int c = int(i % K);
+  const int64_t t = i / K;
+  const int64_t pix = t % PV;
+  const int m = int(t / PV);
+  const int Ca = K - 1;
+  float o = 0.f;
+  for (int l = 0; l < L; ++l) {
+    const float* a = acc + (((int64_t)m * L + l) * PV + pix) * (K + 1);
+    const float ws = a[K];
+    const float n = __fdiv_rn(1.0f, ws > 1e-4f ? ws : 1e-4f);
+    const float s = fm(a[Ca], n);
+    const float v = c < Ca ? fm(a[c], n) : 1.0f;
+    o = fa(fm(v, s), fm(fsb(1.0f, s), o));
+  }
+  out[i] = o;
+}
+
+// ----------------------------------------------------------------------------
+// Stage 2: One-to-many attention, blend logits, layer collapse
+// ----------------------------------------------------------------------------
+
+// One thread per texel. Weights in shared memory (broadcast reads). Per head
+// i: s = n W_q[i]; logits_m = <s, Δ_m>/sqrt(C); softmax over views (max,
+// exp, sum, *1/sum as tape.hpp:390-404); head = sum_m w_m Δ_m; the output
+// projection accumulates head by head (== cat W_O with k ascending).
+template <int C, int M>
+__global__ void __launch_bounds__(128) attend_kernel(float* V, const float* __restrict__ D,
+                                                     int64_t P, int heads,
+                                                     const float* __restrict__ wq,
+                                                     const float* __restrict__ wo,
+                                                     const float* __restrict__ gain,
+                                                     int zero_scores) {
+  extern __shared__ __align__(16) float smem[];
+  float* s_wq = smem;                    // [heads][C][C]
+  float* s_wo = smem + heads * C * C;    // [heads*C][C]
+  for (int e = threadIdx.x; e < heads * C * C; e += blockDim.x) {
+    s_wq[e] = wq[e];
+    s_wo[e] = wo[e];
+  }
+  __syncthreads();
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  float n[C];
+  {
+    const float4* vr = reinterpret_cast<const float4*>(V + p * C);
+    float ms = 0.f;
+#pragma unroll
+    for (int k = 0; k < C / 4; ++k) {
+      const float4 t = vr[k];
+      n[4 * k] = t.x, n[4 * k + 1] = t.y, n[4 * k + 2] = t.z, n[4 * k + 3] = t.w;
+    }
+#pragma unroll
+    for (int k = 0; k < C; ++k) ms = fmaf(n[k], n[k], ms);
+    const float r = __fdiv_rn(1.0f, __fsqrt_rn(fa(__fdiv_rn(ms, float(C)), 1e-6f)));
+#pragma unroll
+    for (int k = 0; k < C; ++k) n[k] = fm(fm(n[k], r), __ldg(gain + k));
+  }
+  const float inv_temp = __double2float_rn(1.0 / sqrt(double(C)));
+  const float* d = D + p * (int64_t)M * C;
+  float out[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) out[c] = 0.f;
+  float w[M];
+  for (int h = 0; h < heads; ++h) {
+    if (zero_scores) {
+      const float u = __fdiv_rn(1.0f, float(M));
+#pragma unroll
+      for (int m = 0; m < M; ++m) w[m] = u;
+    } else {
+      float s[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) s[c] = 0.f;
+      const float* wh = s_wq + h * C * C;
+#pragma unroll 4
+      for (int k = 0; k < C; ++k) {
+        const float nk = n[k];
+#pragma unroll
+        for (int c4 = 0; c4 < C / 4; ++c4) {
+          const float4 wv = reinterpret_cast<const float4*>(wh + k * C)[c4];
+          s[4 * c4] = fmaf(nk, wv.x, s[4 * c4]);
+          s[4 * c4 + 1] = fmaf(nk, wv.y, s[4 * c4 + 1]);
+          s[4 * c4 + 2] = fmaf(nk, wv.z, s[4 * c4 + 2]);
+          s[4 * c4 + 3] = fmaf(nk, wv.w, s[4 * c4 + 3]);
+        }
+      }
+      float mx = -FLT_MAX;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const float4* dm4 = reinterpret_cast<const float4*>(d + m * C);
+        float acc = 0.f;
+#pragma unroll
+        for (int c4 = 0; c4 < C / 4; ++c4) {
+          const float4 t = __ldg(dm4 + c4);
+          acc = fmaf(s[4 * c4], t.x, acc);
+          acc = fmaf(s[4 * c4 + 1], t.y, acc);
+          acc = fmaf(s[4 * c4 + 2], t.z, acc);
+          acc = fmaf(s[4 * c4 + 3], t.w, acc);
+        }
+        w[m] = fm(acc, inv_temp);
+        mx = m == 0 ? w[m] : fmaxf(mx, w[m]);
+      }
+      float sum = 0.f;
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        w[m] = expf(fsb(w[m], mx));
+        sum = fa(sum, w[m]);
+      }
+      const float inv = __fdiv_rn(1.0f, sum);
+#pragma unroll
+      for (int m = 0; m < M; ++m) w[m] = fm(w[m], inv);
+    }
+    float hd[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) hd[c] = 0.f;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const float4* dm4 = reinterpret_cast<const float4*>(d + m * C);
+      const float wm = w[m];
+#pragma unroll
+      for (int c4 = 0; c4 < C / 4; ++c4) {
+        const float4 t = __ldg(dm4 + c4);
+        hd[4 * c4] = fmaf(wm, t.x, hd[4 * c4]);
+        hd[4 * c4 + 1] = fmaf(wm, t.y, hd[4 * c4 + 1]);
+        hd[4 * c4 + 2] = fmaf(wm, t.z, hd[4 * c4 + 2]);
+        hd[4 * c4 + 3] = fmaf(wm, t.w, hd[4 * c4 + 3]);
+      }
+    }
+    const float* wo_h = s_wo + h * C * C;
+#pragma unroll 4
+    for (int k = 0; k < C; ++k) {
+      const float hk = hd[k];
+#pragma unroll
+      for (int c4 = 0; c4 < C / 4; ++c4) {
+        const float4 wv = reinterpret_cast<const float4*>(wo_h + k * C)[c4];
+        out[4 * c4] = fmaf(hk, wv.x, out[4 * c4]);
+        out[4 * c4 + 1] = fmaf(hk, wv.y, out[4 * c4 + 1]);
+        out[4 * c4 + 2] = fmaf(hk, wv.z, out[4 * c4 + 2]);
+        out[4 * c4 + 3] = fmaf(hk, wv.w, out[4 * c4 + 3]);
+      }
+    }
+  }
+  float4* vw = reinterpret_cast<float4*>(V + p * C);
+#pragma unroll
+  for (int k = 0; k < C / 4; ++k) {
+    float4 t = vw[k];
+    t.x = fa(t.x, out[4 * k]);
+    t.y = fa(t.y, out[4 * k + 1]);
+    t.z = fa(t.z, out[4 * k + 2]);
+    t.w = fa(t.w, out[4 * k + 3]);
+    vw[k] = t;
+  }
+}
+
+// Generic-C fallback of the same arithmetic (small channel counts in tests).
+__global__ void attend_generic_kernel(float* V, const float* __restrict__ D, int64_t P, int C,
+                                      int M, int heads, const float* __restrict__ wq,
+                                      const float* __restrict__ wo, const float* __restrict__ gain,
+                                      int zero_scores, float* scratch) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  float* n = scratch + p * 4 * C;
+  float* s = n + C;
+  float* hd = s + C;
+  float* out = hd + C;
+  const float* v = V + p * C;
+  float ms = 0.f;
+  for (int k = 0; k < C; ++k) ms = fmaf(v[k], v[k], ms);
+  const float r = __fdiv_rn(1.0f, __fsqrt_rn(fa(__fdiv_rn(ms, float(C)), 1e-6f)));
+  for (int k = 0; k < C; ++k) n[k] = fm(fm(v[k], r), gain[k]), out[k] = 0.f;
+  const float inv_temp = __double2float_rn(1.0 / sqrt(double(C)));
+  const float* d = D + p * (int64_t)M * C;
+  float w[kMaxM];
+  for (int h = 0; h < heads; ++h) {
+    if (zero_scores) {
+      for (int m = 0; m < M; ++m) w[m] = __fdiv_rn(1.0f, float(M));
+    } else {
+      for (int c = 0; c < C; ++c) {
+        float acc = 0.f;
+        for (int k = 0; k < C; ++k) acc = fmaf(n[k], wq[(h * C + k) * C + c], acc);
+        s[c] = acc;
+      }
+      float mx = 0.f;
+      for (int m = 0; m < M; ++m) {
+        float acc = 0.f;
+        for (int c = 0; c < C; ++c) acc = fmaf(s[c], d[m * C + c], acc);
+        w[m] = fm(acc, inv_temp);
+        mx = m == 0 ? w[m] : fmaxf(mx, w[m]);
+      }
+      float sum = 0.f;
+      for (int m = 0; m < M; ++m) w[m] = expf(fsb(w[m], mx)), sum = fa(sum, w[m]);
+      const float inv = __fdiv_rn(1.0f, sum);
+      for (int m = 0; m < M; ++m) w[m] = fm(w[m], inv);
+    }
+    for (int c = 0; c < C; ++c) {
+      float acc = 0.f;
+      for (int m = 0; m < M; ++m) acc = fmaf(w[m], d[m * C + c], acc);
+      hd[c] = acc;
+    }
+    for (int c = 0; c < C; ++c) {
+      float acc = out[c];
+      for (int k = 0; k < C; ++k) acc = fmaf(hd[k], wo[(h * C + k) * C + c], acc);
+      out[c] = acc;
+    }
+  }
+  for (int c = 0; c < C; ++c) V[p * C + c] = fa(V[p * C + c], out[c]);
+}
+
+__global__ void blend_logits_kernel(const float* __restrict__ V, const float* __restrict__ D,
+                                    int64_t P, int C, int M, const float* __restrict__ bw,
+                                    const float* __restrict__ gain, float* logits) {
+  extern __shared__ float s_bw[];
+  for (int e = threadIdx.x; e < C * C; e += blockDim.x) s_bw[e] = bw[e];
+  __syncthreads();
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const float* v = V + p * C;
+  float ms = 0.f;
+  for (int k = 0; k < C; ++k) ms = fmaf(v[k], v[k], ms);
+  const float r = __fdiv_rn(1.0f, __fsqrt_rn(fa(__fdiv_rn(ms, float(C)), 1e-6f)));
+  const float inv_temp = __double2float_rn(1.0 / sqrt(double(C)));
+  float q[64];
+  const int Cq = C <= 64 ? C : 64;
+  for (int c = 0; c < Cq; ++c) {
+    float acc = 0.f;
+    for (int k = 0; k < C; ++k) acc = fmaf(fm(fm(v[k], r), gain[k]), s_bw[k * C + c], acc);
+    q[c] = acc;
+  }
+  const float* d = D + p * (int64_t)M * C;
+  for (int m = 0; m < M; ++m) {
+    float acc = 0.f;
+    for (int c = 0; c < Cq; ++c) acc = fmaf(q[c], d[m * C + c], acc);
+    logits[p * M + m] = fm(acc, inv_temp);
+  }
+}
+
+// layer_collapse per texel: cat = [a, b]; h = gelu(cat W1 + b1);
+// out = (a+b)*0.5 + (h W2 + b2). W2 accumulates in 16-column chunks of h so
+// the k order stays ascending.
+__global__ void layer_collapse_kernel(const float* __restrict__ V, int L2, int64_t PL, int C,
+                                      const float* __restrict__ w1, const float* __restrict__ b1,
+                                      const float* __restrict__ w2, const float* __restrict__ b2,
+                                      float* out) {
+  extern __shared__ float smem[];
+  float* s_w1 = smem;                 // [2C][2C]
+  float* s_w2 = smem + 4 * C * C;     // [2C][C]
+  for (int e = threadIdx.x; e < 4 * C * C; e += blockDim.x) s_w1[e] = w1[e];
+  for (int e = threadIdx.x; e < 2 * C * C; e += blockDim.x) s_w2[e] = w2[e];
+  __syncthreads();
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)L2 * PL) return;
+  const int64_t l = t / PL, q = t % PL;
+  const float* a = V + ((2 * l) * PL + q) * C;
+  const float* b = V + ((2 * l + 1) * PL + q) * C;
+  float r[64];
+  for (int c = 0; c < C; ++c) r[c] = 0.f;
+  for (int j0 = 0; j0 < 2 * C; j0 += 16) {
+    float hc[16];
+    for (int jj = 0; jj < 16 && j0 + jj < 2 * C; ++jj) {
+      const int j = j0 + jj;
+      float acc = 0.f;
+      for (int k = 0; k < C; ++k) acc = fmaf(a[k], s_w1[k * 2 * C + j], acc);
+      for (int k = 0; k < C; ++k) acc = fmaf(b[k], s_w1[(C + k) * 2 * C + j], acc);
+      hc[jj] = gelu_ref(fa(acc, b1[j]));
+    }
+    for (int jj = 0; jj < 16 && j0 + jj < 2 * C; ++jj) {
+      const float hv = hc[jj];
+      const float* wr = s_w2 + (j0 + jj) * C;
+      for (int c = 0; c < C; ++c) r[c] = fmaf(hv, wr[c], r[c]);
+    }
+  }
+  float* o = out + t * C;
+  for (int c = 0; c < C; ++c) o[c] = fa(fm(fa(a[c], b[c]), 0.5f), fa(r[c], b2[c]));
+}
+
+__global__ void decode_scalar_kernel(const float* __restrict__ V, int64_t P, int C,
+                                     const float* __restrict__ w, float* out, int64_t PL,
+                                     DepthAct act, int do_act) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const float* v = V + p * C;
+  float acc = 0.f;
+  for (int k = 0; k < C; ++k) acc = fmaf(v[k], __ldg(w + k), acc);
+  out[p] = do_act ? activate_depth(acc, int(p / PL), act) : acc;
+}
+
+// ----------------------------------------------------------------------------
+// stage entry points
+// ----------------------------------------------------------------------------
+
+__global__ void stage_world_points_kernel(DevRayCam rc, const float* depth, int L, int H, int W,
+                                          float* points, double lo, double hi, int* bad) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= (int64_t)L * H * W) return;
+  const float d = depth[p];
+  const double dv = double(d);
+  if (dv < lo || dv > hi) atomicOr(bad, 1);
+  float pt[3];
+  world_point(rc, int((p / W) % H), int(p % W), d, pt);
+  points[p * 3] = pt[0];
+  points[p * 3 + 1] = pt[1];
+  points[p * 3 + 2] = pt[2];
+}
+
+__global__ void stage_footprints_kernel(DevCam cam, const float* points, int64_t P, int32_t* taps,
+                                        uint8_t* valid, double* fracs) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const float pt[3] = {points[p * 3], points[p * 3 + 1], points[p * 3 + 2]};
+  const Footprint f = project_footprint(cam, pt);
+  taps[p * 4] = f.x0;
+  taps[p * 4 + 1] = f.x1;
+  taps[p * 4 + 2] = f.y0;
+  taps[p * 4 + 3] = f.y1;
+  valid[p] = f.valid ? 1 : 0;
+  fracs[p * 2] = f.fx;
+  fracs[p * 2 + 1] = f.fy;
+}
+
+__global__ void stage_gather_kernel(DevCam cam, const float* image, int Hi, int Wi, int C,
+                                    const float* points, int64_t P, float* values, float* mask) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  const float pt[3] = {points[p * 3], points[p * 3 + 1], points[p * 3 + 2]};
+  const Footprint f = project_footprint(cam, pt);
+  float* o = values + p * C;
+  if (mask) mask[p] = f.valid ? 1.f : 0.f;
+  if (!f.valid) {
+    for (int c = 0; c < C; ++c) o[c] = 0.f;
+    return;
+  }
+  double w[4];
+  bilinear_weights(f, w);
+  for (int c = 0; c < C; ++c)
+    o[c] = blend4(w, image[((int64_t)f.y0 * Wi + f.x0) * C + c], image[((int64_t)f.y0 * Wi + f.x1) * C + c],
+                  image[((int64_t)f.y1 * Wi + f.x0) * C + c], image[((int64_t)f.y1 * Wi + f.x1) * C + c]);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+
+void fill_rows(float* out, const float* row, int64_t rows, int C, cudaStream_t st) {
+  fill_rows_kernel<<<blocks_for(rows * C, 256), 256, 0, st>>>(out, row, rows, C);
+}
+void fill_layers(float* out, const float* per_layer, int L, int64_t P, cudaStream_t st) {
+  fill_layers_kernel<<<blocks_for(L * P, 256), 256, 0, st>>>(out, per_layer, L, P);
+}
+void fill_anchor_depths(float* out, int L, int64_t P, double inv_span, double inv_far,
+                        cudaStream_t st) {
+  fill_anchor_depths_kernel<<<blocks_for(L * P, 256), 256, 0, st>>>(out, L, P, inv_span, inv_far);
+}
+void mean_pool2(const float* in, float* out, int B, int H, int W, int C, cudaStream_t st) {
+  const int64_t n = (int64_t)B * (H / 2) * (W / 2) * C;
+  mean_pool2_kernel<<<blocks_for(n, 256), 256, 0, st>>>(in, out, B, H, W, C);
+}
+void resize_hwc(const float* in, float* out, int B, int H, int W, int C, int Ho, int Wo,
+                cudaStream_t st) {
+  const int64_t n = (int64_t)B * Ho * Wo * C;
+  if (H == Ho && W == Wo) {
+    cudaMemcpyAsync(out, in, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+    return;
+  }
+  resize_hwc_kernel<<<blocks_for(n, 256), 256, 0, st>>>(in, out, B, H, W, C, Ho, Wo);
+}
+void rms_rinv(const float* x, float* rinv, int64_t rows, int C, cudaStream_t st) {
+  rms_rinv_kernel<<<blocks_for(rows * 32, 256), 256, 0, st>>>(x, rinv, rows, C);
+}
+void ray_base(const RayBaseCam* cams_dev, const RayBaseArgs& a, float* base, cudaStream_t st) {
+  const int64_t n = (int64_t)a.M * a.h * a.w;
+  ray_base_kernel<<<blocks_for(n, 128), 128, 0, st>>>(cams_dev, a, base);
+}
+void ray_project(const float* base, int M, int hK, int wK, int Hk, int Wk, const float* proj,
+                 int C, float* out, cudaStream_t st) {
+  const int64_t n = (int64_t)M * Hk * Wk;
+  ray_project_kernel<<<blocks_for(n, 128), 128, 32 * C * sizeof(float), st>>>(base, M, hK, wK, Hk,
+                                                                               Wk, proj, C, out);
+}
+void gather_stack(const float* feats, int M, int Hf, int Wf, int C, const DevCam* cams_dev,
+                  const DevRayCam& rc, const float* depth, int L, int H, int W, float* deltas,
+                  cudaStream_t st) {
+  const bool v4 = C % 4 == 0;
+  const int64_t n = (int64_t)L * H * W * M * (v4 ? C / 4 : C);
+  if (v4)
+    gather_stack_kernel<true><<<blocks_for(n, 256), 256, 0, st>>>(feats, M, Hf, Wf, C, cams_dev, rc,
+                                                                  depth, L, H, W, deltas);
+  else
+    gather_stack_kernel<false><<<blocks_for(n, 256), 256, 0, st>>>(feats, M, Hf, Wf, C, cams_dev,
+                                                                   rc, depth, L, H, W, deltas);
+}
+void decode_payload(const float* V, int L, int H, int W, int C, const float* w_appear, int Ca,
+                    const float* w_sigma, const float* w_depth, const DepthAct& act,
+                    const DevRayCam& rc, float* payload, float* depth, float* points,
+                    cudaStream_t st) {
+  const int64_t P = (int64_t)L * H * W;
+  decode_payload_kernel<<<blocks_for(P, 128), 128, C * (Ca + 2) * sizeof(float), st>>>(
+      V, L, H, W, C, w_appear, Ca, w_sigma, w_depth, act, rc, payload, depth, points);
+}
+void splat(const float* payload, const float* points, int L, int PL, int K, const DevCam* cams_dev,
+           int M, int Hv, int Wv, float* acc, cudaStream_t st) {
+  const int64_t warps = (int64_t)L * PL * M;
+  splat_kernel<<<blocks_for(warps * 32, 256), 256, 0, st>>>(payload, points, L, PL, K, cams_dev, M,
+                                                            Hv, Wv, acc);
+}
+void splat_composite(const float* acc, int M, int L, int Hv, int Wv, int K, float* out,
+                     cudaStream_t st) {
+  const int64_t n = (int64_t)M * Hv * Wv * K;
+  splat_composite_kernel<<<blocks_for(n, 256), 256, 0, st>>>(acc, M, L, Hv, Wv, K, out);
+}
+
+void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
+            const float* const* wq_heads, const float* wo, const float* gain, int zero_scores,
+            cudaStream_t st) {
+  (void)wq_heads;
+  const size_t smem = 2 * size_t(heads) * C * C * sizeof(float);
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    kern<<<blocks_for(P, 128), 128, smem, st>>>(V, deltas, P, heads, wq, wo, gain, zero_scores);
+  };
+  if (C == 32 && M == 8 && smem <= 200 * 1024) {
+    launch(attend_kernel<32, 8>);
+  } else if (C == 32 && M == 16 && smem <= 200 * 1024) {
+    launch(attend_kernel<32, 16>);
+  } else if (C == 32 && M == 4 && smem <= 200 * 1024) {
+    launch(attend_kernel<32, 4>);
+  } else {
+    // scratch: 4C floats per texel, carved from the caller-visible heap
+    float* scratch = nullptr;
+    cudaMallocAsync(&scratch, size_t(P) * 4 * C * sizeof(float), st);
+    attend_generic_kernel<<<blocks_for(P, 128), 128, 0, st>>>(V, deltas, P, C, M, heads, wq, wo,
+                                                              gain, zero_scores, scratch);
+    cudaFreeAsync(scratch, st);
+  }
+}
+void blend_logits(const float* V, const float* deltas, int64_t P, int C, int M,
+                  const float* blend_w, const float* gain, float* logits, cudaStream_t st) {
+  blend_logits_kernel<<<blocks_for(P, 128), 128, C * C * sizeof(float), st>>>(V, deltas, P, C, M,
+                                                                              blend_w, gain, logits);
+}
+void layer_collapse(const float* V, int L, int64_t PL, int C, const float* w1, const float* b1,
+                    const float* w2, const float* b2, float* out, cudaStream_t st) {
+  const int L2 = L / 2;
+  layer_collapse_kernel<<<blocks_for(L2 * PL, 128), 128, 6 * C * C * sizeof(float), st>>>(
+      V, L2, PL, C, w1, b1, w2, b2, out);
+}
+void decode_scalar(const float* V, int64_t P, int C, const float* w, float* out, int L,
+                   int64_t PL, const DepthAct* act, cudaStream_t st) {
+  (void)L;
+  decode_scalar_kernel<<<blocks_for(P, 256), 256, 0, st>>>(V, P, C, w, out, PL,
+                                                           act ? *act : DepthAct{}, act ? 1 : 0);
+}
+void stage_world_points(const DevRayCam& rc, const float* depth, int L, int H, int W,
+                        float* points, double lo, double hi, int* bad, cudaStream_t st) {
+  const int64_t n = (int64_t)L * H * W;
+  stage_world_points_kernel<<<blocks_for(n, 256), 256, 0, st>>>(rc, depth, L, H, W, points, lo, hi,
+                                                                bad);
+}
+void stage_footprints(const DevCam& cam, const float* points, int64_t P, int32_t* taps,
+                      uint8_t* valid, double* fracs, cudaStream_t st) {
+  stage_footprints_kernel<<<blocks_for(P, 256), 256, 0, st>>>(cam, points, P, taps, valid, fracs);
+}
+void stage_gather(const DevCam& cam, const float* image, int Hi, int Wi, int C,
+                  const float* points, int64_t P, float* values, float* mask, cudaStream_t st) {
+  stage_gather_kernel<<<blocks_for(P, 256), 256, 0, st>>>(cam, image, Hi, Wi, C, points, P, values,
+                                                          mask);
+}
+
+}  // namespace lvsg

@@ -1,0 +1,140 @@
+// Launchers for the lvsg device kernels. All tensors are fp32, channel-last
+// (HWC) unless stated; all launches are asynchronous on `st`.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace lvsg {
+
+// ---- conv3x3 (kernels_ref.hpp:72-96 semantics, zero padding) -------------
+// Input = channel concatenation of up to 3 sources, each [B, H, W, C_i] with
+// pixel stride `pstride` floats and batch stride `bstride` floats. Optional
+// per-pixel rms-norm transform on the input (x * rinv[b,pix]) * gain[c]
+// (fusing conv_mlp_residual's rms_norm, attention.hpp:262-266). Epilogue:
+// + bias, optional GELU, optional residual (out = resid + y; may alias out).
+struct ConvSrc {
+  const float* ptr;
+  int C;
+  int pstride;
+  long long bstride;
+};
+struct ConvArgs {
+  ConvSrc src[3];
+  int nsrc;
+  int Cin, Cout, H, W, B;
+  const float* w;     // [Cout, Cin, 3, 3]
+  const float* bias;  // [Cout] or null
+  const float* rinv;  // [B, H, W] or null
+  const float* gain;  // [Cin] (with rinv)
+  int gelu;
+  float* out;
+  int out_pstride;
+  long long out_bstride;
+  const float* resid;  // or null
+  int res_pstride;
+  long long res_bstride;
+};
+void conv3x3(const ConvArgs& a, cudaStream_t st);
+
+// ---- elementwise / layout ------------------------------------------------
+void fill_rows(float* out, const float* row, int64_t rows, int C, cudaStream_t st);
+void fill_layers(float* out, const float* per_layer, int L, int64_t P, cudaStream_t st);
+// depth[l, :] = T(1 / (double(T((l+0.5)/L)) * inv_span + inv_far)) (network.hpp:469-475)
+void fill_anchor_depths(float* out, int L, int64_t P, double inv_span, double inv_far,
+                        cudaStream_t st);
+void mean_pool2(const float* in, float* out, int B, int H, int W, int C, cudaStream_t st);
+// resize_bilinear of [B,H,W,C] (tape.hpp:858-917, per channel).
+void resize_hwc(const float* in, float* out, int B, int H, int W, int C, int Ho, int Wo,
+                cudaStream_t st);
+// rms_norm reciprocal per row: rinv = 1/sqrt(mean(x^2)+1e-6) (tape.hpp:779-785).
+void rms_rinv(const float* x, float* rinv, int64_t rows, int C, cudaStream_t st);
+
+// ---- encoder ray encodings (geometry.hpp:343-391, network.hpp:397-413) -----
+struct RayBaseCam {
+  double Rwc_in[9];  // grid camera R^T
+  double o[3];       // input centre in the target frame
+  double fx, fy, cx, cy;  // grid camera intrinsics
+};
+struct RayBaseArgs {
+  double Rcw_t[9];
+  double tfx, tfy, inv_span, half_w, half_h;
+  int h, w, M;
+};
+void ray_base(const RayBaseCam* cams_dev, const RayBaseArgs& a, float* base, cudaStream_t st);
+// rays_k = resize(base -> Hk,Wk) @ ray_proj [32,C]
+void ray_project(const float* base, int M, int hK, int wK, int Hk, int Wk, const float* proj,
+                 int C, float* out, cudaStream_t st);
+
+// ---- geometry --------------------------------------------------------------
+// Δ[p, m, :] = gather of feats[m] ([M, Hf, Wf, C]) at world_point(p) through
+// cams[m] (backproject_stack, network.hpp:421-436; invalid -> 0).
+void gather_stack(const float* feats, int M, int Hf, int Wf, int C, const DevCam* cams_dev,
+                  const DevRayCam& rc, const float* depth, int L, int H, int W, float* deltas,
+                  cudaStream_t st);
+
+// render_to_input_view decode (ldm.hpp:229-235): payload [P, Ca+1] =
+// [sigmoid(V w_a), sigmoid(V w_sigma)], depth [P] = activate(V w_depth) and
+// world points [P,3].
+void decode_payload(const float* V, int L, int H, int W, int C, const float* w_appear, int Ca,
+                    const float* w_sigma, const float* w_depth, const DepthAct& da,
+                    const DevRayCam& rc, float* payload, float* depth, float* points,
+                    cudaStream_t st);
+// splat_accumulate (geometry.hpp:230-264) of payload [L*H*W, K] into every
+// view: acc [M, L, Hv, Wv, K+1] (atomics; zeroed by the caller).
+void splat(const float* payload, const float* points, int L, int PL, int K, const DevCam* cams_dev,
+           int M, int Hv, int Wv, float* acc, cudaStream_t st);
+// normalise (splat_project) + over_composite colour and alpha
+// (ldm.hpp:236-243): acc -> out [M, Hv, Wv, K] (K-1 colour + alpha).
+void splat_composite(const float* acc, int M, int L, int Hv, int Wv, int K, float* out,
+                     cudaStream_t st);
+
+// ---- attention / fusion ----------------------------------------------------
+// V += OTM(rms_norm(V), Δ) (attention.hpp:207-252), in place.
+void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
+            const float* const* wq_heads, const float* wo, const float* gain, int zero_scores,
+            cudaStream_t st);
+// logits [P, M] = <rms_norm(V,g) W_blend, Δ_m> / sqrt(C) (network.hpp:539-549).
+void blend_logits(const float* V, const float* deltas, int64_t P, int C, int M,
+                  const float* blend_w, const float* gain, float* logits, cudaStream_t st);
+// layer_collapse (network.hpp:440-455): V [L,H,W,C] -> out [L/2,H,W,C].
+void layer_collapse(const float* V, int L, int64_t PL, int C, const float* w1, const float* b1,
+                    const float* w2, const float* b2, float* out, cudaStream_t st);
+// out[p] = V[p,:] . w (decode_linear with K = 1), optionally activated depth.
+void decode_scalar(const float* V, int64_t P, int C, const float* w, float* out, int L,
+                   int64_t PL, const DepthAct* act, cudaStream_t st);
+
+// ---- Stage 3 + 4 ------------------------------------------------------------
+struct RenderArgs {
+  const float* pre_d;   // [L,H,W]
+  const float* pre_s;   // [L,H,W]
+  const float* logits;  // [L,H,W,M]
+  int L, H, W, M, Ho, Wo;
+  int row0, row1;  // output rows rendered (row band)
+  DepthAct act;
+  DevRayCam rc;           // target camera re-digitised to (Wo, Ho)
+  const DevCam* cams;     // [M] render cameras (device)
+  const float* images;    // [M, Hr, Wr, 3]
+  int Hr, Wr;
+  float* rgb;             // [row1-row0, Wo, 3]
+  float near_depth, far_depth;
+  int* bad_depth;         // set when a depth leaves [near-slack, far+slack]
+  double slack_lo, slack_hi;
+};
+// upsample_activate + render_target fused (ldm.hpp:193-199, :249-271).
+void render_fused(const RenderArgs& a, cudaStream_t st);
+// upsample_activate only (materialised LDM for lvsg_forward outputs).
+void upsample_activate(const RenderArgs& a, float* depth, float* density, float* blend,
+                       cudaStream_t st);
+
+// ---- stage entry points (per-stage parity) ----------------------------------
+void stage_world_points(const DevRayCam& rc, const float* depth, int L, int H, int W,
+                        float* points, double lo, double hi, int* bad, cudaStream_t st);
+void stage_footprints(const DevCam& cam, const float* points, int64_t P, int32_t* taps,
+                      uint8_t* valid, double* fracs, cudaStream_t st);
+void stage_gather(const DevCam& cam, const float* image, int Hi, int Wi, int C,
+                  const float* points, int64_t P, float* values, float* mask, cudaStream_t st);
+
+}  // namespace lvsg

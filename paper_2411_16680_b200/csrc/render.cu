@@ -1,0 +1,156 @@
+// Stage 3 + Stage 4 fused: bilinear x s upsample of the LDM pre-activation
+// maps, activation (Eq. 4 depth, sigmoid density, softmax blend over views),
+// per-layer reprojection into every input view with the 4-tap f64 colour
+// gather, beta renormalisation over valid views, and back-to-front
+// over-compositing into the output frame. The activated 1080p LDM is never
+// materialised.
+//
+// Reference semantics: upsample_activate (ldm.hpp:249-271), resize_bilinear
+// (tape.hpp:858-917), render_target -> world_points + blended_layer_colors +
+// over_composite (ldm.hpp:98-199, geometry.hpp:84-171).
+#include "kernels.h"
+
+namespace lvsg {
+namespace {
+
+constexpr int kMaxViews = 32;
+
+struct Taps {
+  int y0, y1, x0, x1;
+  float fy, fx;
+};
+
+__device__ __forceinline__ float sample(const float* map, int W, const Taps& t) {
+  return lerp2(__ldg(map + t.y0 * W + t.x0), __ldg(map + t.y0 * W + t.x1),
+               __ldg(map + t.y1 * W + t.x0), __ldg(map + t.y1 * W + t.x1), t.fx, t.fy);
+}
+
+// Activated LDM sample of layer l at output pixel: depth, sigma, beta[M].
+__device__ __forceinline__ void ldm_sample(const RenderArgs& a, int l, const Taps& t, float& depth,
+                                           float& sigma, float* beta) {
+  const int64_t plane = (int64_t)a.H * a.W;
+  depth = activate_depth(sample(a.pre_d + l * plane, a.W, t), l, a.act);
+  sigma = sigmoid_ref(sample(a.pre_s + l * plane, a.W, t));
+  const float* lg = a.logits + l * plane * a.M;
+  const int M = a.M;
+  float mx = 0.f;
+  for (int m = 0; m < M; ++m) {
+    const float v = lerp2(__ldg(lg + ((int64_t)t.y0 * a.W + t.x0) * M + m),
+                          __ldg(lg + ((int64_t)t.y0 * a.W + t.x1) * M + m),
+                          __ldg(lg + ((int64_t)t.y1 * a.W + t.x0) * M + m),
+                          __ldg(lg + ((int64_t)t.y1 * a.W + t.x1) * M + m), t.fx, t.fy);
+    beta[m] = v;
+    mx = m == 0 ? v : fmaxf(mx, v);
+  }
+  float sum = 0.f;
+  for (int m = 0; m < M; ++m) {
+    beta[m] = expf(fsb(beta[m], mx));
+    sum = fa(sum, beta[m]);
+  }
+  const float inv = __fdiv_rn(1.0f, sum);
+  for (int m = 0; m < M; ++m) beta[m] = fm(beta[m], inv);
+}
+
+__device__ __forceinline__ Taps taps_for(const RenderArgs& a, int i, int j) {
+  Taps t;
+  resize_tap(i, a.H, a.Ho, t.y0, t.y1, t.fy);
+  resize_tap(j, a.W, a.Wo, t.x0, t.x1, t.fx);
+  return t;
+}
+
+// One thread per output pixel of the row band.
+__global__ void __launch_bounds__(128) render_fused_kernel(const RenderArgs a) {
+  extern __shared__ DevCam s_cams[];
+  for (int m = threadIdx.x; m < a.M; m += blockDim.x) s_cams[m] = a.cams[m];
+  __syncthreads();
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int rows = a.row1 - a.row0;
+  if (idx >= (int64_t)rows * a.Wo) return;
+  const int i = a.row0 + int(idx / a.Wo), j = int(idx % a.Wo);
+  const Taps t = taps_for(a, i, j);
+  const int M = a.M;
+  float o[3] = {0.f, 0.f, 0.f};
+  float beta[kMaxViews];
+  int bad = 0;
+  const int64_t img_stride = (int64_t)a.Hr * a.Wr * 3;
+  for (int l = 0; l < a.L; ++l) {
+    float depth, sigma;
+    ldm_sample(a, l, t, depth, sigma, beta);
+    const double dv = double(depth);
+    bad |= (dv < a.slack_lo || dv > a.slack_hi);
+    float pt[3];
+    world_point(a.rc, i, j, depth, pt);
+    // blended_layer_colors: beta * mask, wsum (k ascending from 0), 1/(wsum+1e-8)
+    float col[kMaxViews][3];
+    float wsum = 0.f;
+    for (int m = 0; m < M; ++m) {
+      const Footprint f = project_footprint(s_cams[m], pt);
+      if (f.valid) {
+        double w[4];
+        bilinear_weights(f, w);
+        const float* img = a.images + m * img_stride;
+        const float* p00 = img + ((int64_t)f.y0 * a.Wr + f.x0) * 3;
+        const float* p10 = img + ((int64_t)f.y0 * a.Wr + f.x1) * 3;
+        const float* p01 = img + ((int64_t)f.y1 * a.Wr + f.x0) * 3;
+        const float* p11 = img + ((int64_t)f.y1 * a.Wr + f.x1) * 3;
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+          col[m][k] = blend4(w, __ldg(p00 + k), __ldg(p10 + k), __ldg(p01 + k), __ldg(p11 + k));
+        beta[m] = fm(beta[m], 1.0f);
+      } else {
+        col[m][0] = col[m][1] = col[m][2] = 0.f;
+        beta[m] = fm(beta[m], 0.0f);
+      }
+      wsum = fa(wsum, fm(beta[m], 1.0f));
+    }
+    const float r = __fdiv_rn(1.0f, fa(wsum, 1e-8f));
+    float rgb[3] = {0.f, 0.f, 0.f};
+    for (int m = 0; m < M; ++m) {
+      const float b = fm(beta[m], r);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) rgb[k] = fa(rgb[k], fm(b, col[m][k]));
+    }
+    // over_composite: o = v*a + (1-a)*o, layer 0 (far) first
+#pragma unroll
+    for (int k = 0; k < 3; ++k) o[k] = fa(fm(rgb[k], sigma), fm(fsb(1.0f, sigma), o[k]));
+  }
+  if (bad && a.bad_depth) atomicOr(a.bad_depth, 1);
+  float* out = a.rgb + idx * 3;
+  out[0] = o[0];
+  out[1] = o[1];
+  out[2] = o[2];
+}
+
+__global__ void upsample_activate_kernel(const RenderArgs a, float* depth, float* density,
+                                         float* blend) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t plane = (int64_t)a.Ho * a.Wo;
+  if (idx >= plane * a.L) return;
+  const int l = int(idx / plane);
+  const int64_t pix = idx % plane;
+  const int i = int(pix / a.Wo), j = int(pix % a.Wo);
+  const Taps t = taps_for(a, i, j);
+  float beta[kMaxViews];
+  float d, s;
+  ldm_sample(a, l, t, d, s, beta);
+  depth[idx] = d;
+  density[idx] = s;
+  for (int m = 0; m < a.M; ++m) blend[idx * a.M + m] = beta[m];
+}
+
+inline int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
+
+}  // namespace
+
+void render_fused(const RenderArgs& a, cudaStream_t st) {
+  const int64_t n = (int64_t)(a.row1 - a.row0) * a.Wo;
+  render_fused_kernel<<<blocks_for(n, 128), 128, a.M * sizeof(DevCam), st>>>(a);
+}
+
+void upsample_activate(const RenderArgs& a, float* depth, float* density, float* blend,
+                       cudaStream_t st) {
+  const int64_t n = (int64_t)a.L * a.Ho * a.Wo;
+  upsample_activate_kernel<<<blocks_for(n, 128), 128, 0, st>>>(a, depth, density, blend);
+}
+
+}  // namespace lvsg

@@ -1,0 +1,1080 @@
+// liblvsg runtime: context (device weights, stream, scratch arena), the
+// per-frame orchestration of forward() + render_target() on the device, and
+// the C ABI of include/lvsg.h.
+//
+// Orchestration mirrors lvs::forward (network.hpp:562-603):
+//   encode_inputs            network.hpp:368-417
+//   initialize               network.hpp:459-493
+//   layer_collapse           network.hpp:440-455
+//   update_block             network.hpp:500-535
+//   fusion_block             attention.hpp:275-281
+//   decode_blend_logits      network.hpp:539-549
+//   upsample_activate        ldm.hpp:249-271      (fused into the render)
+//   render_target            ldm.hpp:193-199
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host.h"
+#include "kernels.h"
+
+namespace lvsg {
+
+int64_t g_launches = 0;  // incremented by every kernel launcher
+
+namespace {
+
+#define CUDA_OK(x)                                                                       \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess)                                                               \
+      throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));                  \
+  } while (0)
+
+// ---- camera conversions (host, f64, reference operation order) -------------
+
+DevCam dev_cam(const lvsg_camera& c) {
+  DevCam d;
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j) d.R[i * 3 + j] = c.cam_from_world[i * 4 + j];
+    d.t[i] = c.cam_from_world[i * 4 + 3];
+  }
+  d.fx = c.fx;
+  d.fy = c.fy;
+  d.cx = c.cx;
+  d.cy = c.cy;
+  d.W = int(c.width);
+  d.H = int(c.height);
+  return d;
+}
+
+void center_of(const lvsg_camera& c, double o[3]) {
+  const double* m = c.cam_from_world;
+  for (int r = 0; r < 3; ++r) {
+    double acc = (-m[0 * 4 + r]) * m[0 * 4 + 3];
+    acc += (-m[1 * 4 + r]) * m[1 * 4 + 3];
+    acc += (-m[2 * 4 + r]) * m[2 * 4 + 3];
+    o[r] = acc;
+  }
+}
+
+// world_points camera: the frustum camera re-digitised to (W, H).
+DevRayCam ray_cam(const lvsg_camera& c0, int64_t W, int64_t H) {
+  lvsg_camera c = camera_scaled(c0, W, H);
+  DevRayCam r;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) r.Rwc[i * 3 + j] = c.cam_from_world[j * 4 + i];
+  center_of(c, r.c);
+  r.fx = c.fx;
+  r.fy = c.fy;
+  r.cx = c.cx;
+  r.cy = c.cy;
+  return r;
+}
+
+DepthAct depth_act(int64_t L, const lvsg_frustum& fr) {
+  DepthAct a;
+  a.L = int(L);
+  a.s_half_over_L = float(0.5 / double(L));
+  a.s_span = float(1.0 / fr.near_depth - 1.0 / fr.far_depth);
+  a.s_inv_far = float(1.0 / fr.far_depth);
+  return a;
+}
+
+// ---- device arena ----------------------------------------------------------
+
+struct Buf {
+  float* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t count) {
+    if (count <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    CUDA_OK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(float)));
+    n = count;
+  }
+  ~Buf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct ConvPairW {
+  const float *w1, *b1, *w2, *b2;
+};
+struct MlpW {
+  const float *gain, *w1, *b1, *w2, *b2;
+};
+struct FusionW {
+  int heads;
+  const float *wq, *wo, *gain;
+  std::vector<MlpW> mlps;
+};
+struct StepW {
+  std::vector<ConvPairW> collapse;  // w1 b1 w2 b2 of each Lc
+  const float *stem_w = nullptr, *stem_b = nullptr;
+  int64_t stem_cin = 0;
+  ConvPairW r1{}, r2{};
+  std::vector<FusionW> fusions;
+};
+struct NetW {
+  const float* init_feature;
+  const float *stem_w, *stem_b;
+  std::vector<ConvPairW> lvl_r1, lvl_r2;
+  std::vector<const float*> ray_proj;
+  const float *w_sigma, *w_depth, *w_appear, *blend_w, *blend_gain;
+  std::vector<StepW> steps;
+};
+
+}  // namespace
+}  // namespace lvsg
+
+struct lvsg_ctx {
+  lvsg::Config cfg;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  std::vector<lvsg::ParamSpec> layout;
+  int64_t total_params = 0;
+  lvsg::Buf weights;
+  bool have_weights = false;
+  lvsg::NetW W;
+
+  // per-resolution plan
+  int64_t He = 0, We = 0;
+  lvsg::Plan plan;
+
+  // arena
+  lvsg::Buf enc_in, ren_in, rgb, enc_x, enc_t, ray_base;
+  std::vector<lvsg::Buf> feats, rays;
+  lvsg::Buf V0, V1, deltas, t1, rinv, uh, ut, uu, payload, depth_in, points, depth_out, acc, fb,
+      fbr, pre_d, pre_s, logits, anchors, ldm_d, ldm_s, ldm_b;
+  lvsg::Buf cams_dev;  // DevCam / RayBaseCam tables
+  int* bad_flag = nullptr;
+  void* pinned = nullptr;  // camera staging
+  size_t pinned_bytes = 0;
+  cudaEvent_t staging_done = nullptr;
+
+  // resident forward result (for lvsg_render)
+  bool have_ldm = false;
+  int64_t L = 0, H = 0, Wd = 0, M = 0;
+  lvsg_frustum target{};
+  float* V = nullptr;
+  int64_t launches = 0;
+};
+
+namespace lvsg {
+namespace {
+
+thread_local std::string g_create_err;
+
+void bind_weights(lvsg_ctx* c) {
+  const Config& cfg = c->cfg;
+  const int64_t C = cfg.channels, Ca = cfg.appear_channels();
+  const float* cur = c->weights.p;
+  auto take = [&](int64_t n) {
+    const float* p = cur;
+    cur += n;
+    return p;
+  };
+  auto pair = [&] {
+    ConvPairW p;
+    p.w1 = take(C * C * 9);
+    p.b1 = take(C);
+    p.w2 = take(C * C * 9);
+    p.b2 = take(C);
+    return p;
+  };
+  NetW& W = c->W;
+  W = NetW{};
+  W.init_feature = take(C);
+  W.stem_w = take(C * 27);
+  W.stem_b = take(C);
+  for (int64_t k = 0; k < cfg.pyramid_levels; ++k) {
+    W.lvl_r1.push_back(pair());
+    W.lvl_r2.push_back(pair());
+    W.ray_proj.push_back(take(32 * C));
+  }
+  W.w_sigma = take(C);
+  W.w_depth = take(C);
+  W.w_appear = take(C * Ca);
+  W.blend_w = take(C * C);
+  W.blend_gain = take(C);
+  for (const Step& st : cfg.steps) {
+    StepW sw;
+    for (const Token& t : parse_blocks(st.blocks)) {
+      switch (t.kind) {
+        case Tok::collapse: {
+          ConvPairW p;
+          p.w1 = take(4 * C * C);
+          p.b1 = take(2 * C);
+          p.w2 = take(2 * C * C);
+          p.b2 = take(C);
+          sw.collapse.push_back(p);
+          break;
+        }
+        case Tok::backproject:
+        case Tok::update: {
+          sw.stem_cin = t.kind == Tok::update ? 2 * C + Ca + 1 : 2 * C;
+          sw.stem_w = take(C * sw.stem_cin * 9);
+          sw.stem_b = take(C);
+          sw.r1 = pair();
+          sw.r2 = pair();
+          break;
+        }
+        case Tok::attend: {
+          FusionW f;
+          f.heads = int(t.heads);
+          f.wq = take(t.heads * C * C);
+          f.wo = take(t.heads * C * C);
+          f.gain = take(C);
+          sw.fusions.push_back(f);
+          break;
+        }
+        case Tok::conv: {
+          MlpW m;
+          m.gain = take(C);
+          m.w1 = take(C * C * 9);
+          m.b1 = take(C);
+          m.w2 = take(C * C * 9);
+          m.b2 = take(C);
+          sw.fusions.back().mlps.push_back(m);
+          break;
+        }
+      }
+    }
+    W.steps.push_back(std::move(sw));
+  }
+}
+
+// Sizes every arena buffer for encoder input (He, We); no allocation after.
+void ensure_plan(lvsg_ctx* c, int64_t He, int64_t We) {
+  if (c->He == He && c->We == We) return;
+  const Config& cfg = c->cfg;
+  Plan plan = plan_forward(cfg, He, We);
+  const int64_t M = cfg.views, C = cfg.channels, Ca = cfg.appear_channels(), K = cfg.pyramid_levels;
+  c->enc_x.ensure(size_t(M * He * We * C));
+  c->enc_t.ensure(size_t(M * He * We * C));
+  c->feats.resize(size_t(K));
+  c->rays.resize(size_t(K));
+  for (int64_t k = 0; k < K; ++k) {
+    size_t n = size_t(M * plan.pyramid[size_t(k)].first * plan.pyramid[size_t(k)].second * C);
+    c->feats[size_t(k)].ensure(n);
+    c->rays[size_t(k)].ensure(n);
+  }
+  c->ray_base.ensure(size_t(M * plan.pyramid.back().first * plan.pyramid.back().second * 32));
+  size_t maxV = 0, maxD = 0, maxU = 0, maxAcc = 0, maxFb = 0, maxIn = 0;
+  for (const StepPlan& sp : plan.steps) {
+    maxV = std::max({maxV, size_t(sp.in_layers * sp.in_height * sp.in_width),
+                     size_t(sp.layers * sp.height * sp.width)});
+    maxIn = std::max(maxIn, size_t(sp.layers * sp.in_height * sp.in_width));
+    maxD = std::max(maxD, size_t(sp.layers * sp.height * sp.width * M * C));
+    maxU = std::max(maxU, size_t(M * sp.feat_h * sp.feat_w));
+    maxAcc = std::max(maxAcc, size_t(M * sp.layers * sp.render_h * sp.render_w * (Ca + 2)));
+    maxFb = std::max(maxFb, size_t(M * sp.render_h * sp.render_w * (Ca + 1)));
+  }
+  c->V0.ensure(maxV * C);
+  c->V1.ensure(maxV * C);
+  c->deltas.ensure(maxD);
+  c->t1.ensure(maxV * C);
+  c->rinv.ensure(maxV);
+  c->uh.ensure(maxU * C);
+  c->ut.ensure(maxU * C);
+  c->uu.ensure(maxU * C);
+  c->payload.ensure(maxIn * (Ca + 1));
+  c->depth_in.ensure(maxIn);
+  c->points.ensure(maxIn * 3);
+  c->depth_out.ensure(maxV);
+  c->acc.ensure(maxAcc);
+  c->fb.ensure(maxFb);
+  c->fbr.ensure(maxU * (Ca + 1));
+  const StepPlan& last = plan.steps.back();
+  const size_t Pf = size_t(last.layers * last.height * last.width);
+  c->pre_d.ensure(Pf);
+  c->pre_s.ensure(Pf);
+  c->logits.ensure(Pf * M);
+  int64_t maxL = 0;
+  for (const Step& s : cfg.steps) maxL = std::max(maxL, s.layers);
+  c->anchors.ensure(size_t(maxL));
+  // camera tables: per step (update cams + render cams) + ray base cams
+  size_t cam_bytes = (plan.steps.size() * 2 + 2) * size_t(M) * sizeof(DevCam) + size_t(M) * sizeof(RayBaseCam);
+  c->cams_dev.ensure((cam_bytes + sizeof(float) - 1) / sizeof(float));
+  if (c->pinned_bytes < cam_bytes) {
+    if (c->pinned) cudaFreeHost(c->pinned);
+    CUDA_OK(cudaMallocHost(&c->pinned, cam_bytes));
+    c->pinned_bytes = cam_bytes;
+  }
+  c->plan = std::move(plan);
+  c->He = He;
+  c->We = We;
+}
+
+ConvArgs conv_args(int B, int H, int W, int Cin, int Cout, const float* w, const float* b,
+                   float* out) {
+  ConvArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.B = B;
+  a.H = H;
+  a.W = W;
+  a.Cin = Cin;
+  a.Cout = Cout;
+  a.w = w;
+  a.bias = b;
+  a.out = out;
+  a.out_pstride = Cout;
+  a.out_bstride = (long long)H * W * Cout;
+  return a;
+}
+
+void add_src(ConvArgs& a, const float* p, int C, int H, int W) {
+  a.src[a.nsrc] = ConvSrc{p, C, C, (long long)H * W * C};
+  a.nsrc++;
+}
+
+// x = x + conv(gelu(conv(x))) on [B,H,W,C] (network.hpp:150-153); with
+// `out` != x the sum lands in out (x untouched).
+void conv_residual(lvsg_ctx* c, const float* x, float* out, float* tmp, int B, int H, int W,
+                   const ConvPairW& p) {
+  const int C = int(c->cfg.channels);
+  ConvArgs a = conv_args(B, H, W, C, C, p.w1, p.b1, tmp);
+  add_src(a, x, C, H, W);
+  a.gelu = 1;
+  conv3x3(a, c->stream);
+  ConvArgs b2 = conv_args(B, H, W, C, C, p.w2, p.b2, out);
+  add_src(b2, tmp, C, H, W);
+  b2.resid = x;
+  b2.res_pstride = C;
+  b2.res_bstride = (long long)H * W * C;
+  conv3x3(b2, c->stream);
+  g_launches += 2;
+}
+
+// run_update_cnn (network.hpp:155-160) on concatenated sources, all views.
+void update_cnn(lvsg_ctx* c, const StepW& sw, const ConvArgs& stem_in, int M, int Hf, int Wf) {
+  const int C = int(c->cfg.channels);
+  ConvArgs a = stem_in;
+  a.w = sw.stem_w;
+  a.bias = sw.stem_b;
+  a.Cin = int(sw.stem_cin);
+  a.Cout = C;
+  a.B = M;
+  a.H = Hf;
+  a.W = Wf;
+  a.out = c->uh.p;
+  a.out_pstride = C;
+  a.out_bstride = (long long)Hf * Wf * C;
+  conv3x3(a, c->stream);
+  g_launches += 1;
+  conv_residual(c, c->uh.p, c->uh.p, c->ut.p, M, Hf, Wf, sw.r1);
+  conv_residual(c, c->uh.p, c->uu.p, c->ut.p, M, Hf, Wf, sw.r2);
+}
+
+// fusion_block (attention.hpp:275-281): attention + conv MLPs, V in place.
+void fusion(lvsg_ctx* c, float* V, int64_t L, int64_t H, int64_t W, const FusionW& f) {
+  const int C = int(c->cfg.channels), M = int(c->cfg.views);
+  const int64_t P = L * H * W;
+  attend(V, c->deltas.p, P, C, M, f.heads, f.wq, nullptr, f.wo, f.gain, c->cfg.ablate_attention,
+         c->stream);
+  g_launches += 1;
+  for (const MlpW& m : f.mlps) {
+    // conv_mlp_residual (attention.hpp:262-267), batched over layers
+    rms_rinv(V, c->rinv.p, P, C, c->stream);
+    ConvArgs a = conv_args(int(L), int(H), int(W), C, C, m.w1, m.b1, c->t1.p);
+    add_src(a, V, C, int(H), int(W));
+    a.rinv = c->rinv.p;
+    a.gain = m.gain;
+    a.gelu = 1;
+    conv3x3(a, c->stream);
+    ConvArgs b = conv_args(int(L), int(H), int(W), C, C, m.w2, m.b2, V);
+    add_src(b, c->t1.p, C, int(H), int(W));
+    b.resid = V;
+    b.res_pstride = C;
+    b.res_bstride = (long long)H * W * C;
+    conv3x3(b, c->stream);
+    g_launches += 3;
+  }
+}
+
+struct CamTables {
+  DevCam* upd[LVSG_MAX_STEPS];
+  DevCam* rend[LVSG_MAX_STEPS];
+  DevCam* final_cams;
+  RayBaseCam* ray;
+};
+
+// Builds every per-frame camera table on the host and uploads them with one
+// async copy from pinned staging.
+CamTables upload_cams(lvsg_ctx* c, const lvsg_camera* enc_cams, const lvsg_frustum& target,
+                      const lvsg_camera* render_cams) {
+  const Plan& plan = c->plan;
+  const int64_t M = c->cfg.views;
+  const size_t S = plan.steps.size();
+  CUDA_OK(cudaEventSynchronize(c->staging_done));  // previous frame's upload has landed
+  char* host = static_cast<char*>(c->pinned);
+  char* dev = reinterpret_cast<char*>(c->cams_dev.p);
+  CamTables t;
+  size_t off = 0;
+  auto table = [&](auto fill) {
+    DevCam* h = reinterpret_cast<DevCam*>(host + off);
+    for (int64_t m = 0; m < M; ++m) h[m] = fill(m);
+    DevCam* d = reinterpret_cast<DevCam*>(dev + off);
+    off += size_t(M) * sizeof(DevCam);
+    return d;
+  };
+  for (size_t s = 0; s < S; ++s) {
+    const StepPlan& sp = plan.steps[s];
+    t.upd[s] = table([&](int64_t m) { return dev_cam(camera_scaled(enc_cams[m], sp.feat_w, sp.feat_h)); });
+    t.rend[s] = table([&](int64_t m) { return dev_cam(camera_scaled(enc_cams[m], sp.render_w, sp.render_h)); });
+  }
+  t.final_cams = render_cams ? table([&](int64_t m) { return dev_cam(render_cams[m]); }) : nullptr;
+  // ray_plane_delta cameras (geometry.hpp:343-353)
+  const int64_t hK = c->He >> c->cfg.pyramid_levels, wK = c->We >> c->cfg.pyramid_levels;
+  RayBaseCam* rh = reinterpret_cast<RayBaseCam*>(host + off);
+  const double* tm = target.camera.cam_from_world;
+  for (int64_t m = 0; m < M; ++m) {
+    lvsg_camera g = camera_scaled(enc_cams[m], wK, hK);
+    RayBaseCam& r = rh[m];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) r.Rwc_in[i * 3 + j] = g.cam_from_world[j * 4 + i];
+    double ow[3];
+    center_of(g, ow);
+    for (int i = 0; i < 3; ++i) {
+      double acc = tm[i * 4 + 0] * ow[0];
+      acc += tm[i * 4 + 1] * ow[1];
+      acc += tm[i * 4 + 2] * ow[2];
+      r.o[i] = acc + tm[i * 4 + 3];
+    }
+    r.fx = g.fx;
+    r.fy = g.fy;
+    r.cx = g.cx;
+    r.cy = g.cy;
+  }
+  t.ray = reinterpret_cast<RayBaseCam*>(dev + off);
+  off += size_t(M) * sizeof(RayBaseCam);
+  CUDA_OK(cudaMemcpyAsync(dev, host, off, cudaMemcpyHostToDevice, c->stream));
+  CUDA_OK(cudaEventRecord(c->staging_done, c->stream));
+  return t;
+}
+
+// forward() on device images [M, He, We, 3]; leaves pre_d / pre_s / logits
+// (volume resolution) and the final V resident.
+void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
+                    const lvsg_camera* enc_cams, const lvsg_frustum& target,
+                    const lvsg_camera* render_cams, CamTables* tables_out) {
+  const Config& cfg = c->cfg;
+  if (!c->have_weights) throw DimError("forward: no weights loaded (lvsg_load_weights / lvsg_init_weights)");
+  frustum_validate(target);
+  for (int64_t m = 0; m < cfg.views; ++m) camera_validate(enc_cams[m]);
+  ensure_plan(c, He, We);
+  const Plan& plan = c->plan;
+  const int M = int(cfg.views), C = int(cfg.channels), Ca = int(cfg.appear_channels());
+  const int K = int(cfg.pyramid_levels);
+  cudaStream_t st = c->stream;
+  const NetW& W = c->W;
+  const int64_t launches0 = g_launches;
+  CamTables cams = upload_cams(c, enc_cams, target, render_cams);
+  if (tables_out) *tables_out = cams;
+
+  // ---- encode_inputs --------------------------------------------------------
+  {
+    int h = int(He), w = int(We);
+    ConvArgs a = conv_args(M, h, w, 3, C, W.stem_w, W.stem_b, c->enc_x.p);
+    a.src[0] = ConvSrc{enc, 3, 3, (long long)h * w * 3};
+    a.nsrc = 1;
+    conv3x3(a, st);
+    g_launches += 1;
+    const float* x = c->enc_x.p;
+    for (int k = 0; k < K; ++k) {
+      float* xo = k == 0 ? c->enc_x.p : c->enc_x.p;  // level >= 1 reads feats[k-1], writes enc_x
+      conv_residual(c, x, xo, c->enc_t.p, M, h, w, W.lvl_r1[size_t(k)]);
+      conv_residual(c, xo, xo, c->enc_t.p, M, h, w, W.lvl_r2[size_t(k)]);
+      mean_pool2(xo, c->feats[size_t(k)].p, M, h, w, C, st);
+      g_launches += 1;
+      h /= 2;
+      w /= 2;
+      x = c->feats[size_t(k)].p;
+    }
+    const int hK = int(plan.pyramid.back().first), wK = int(plan.pyramid.back().second);
+    if (cfg.ablate_rays) {
+      for (int k = 0; k < K; ++k)
+        CUDA_OK(cudaMemsetAsync(c->rays[size_t(k)].p, 0,
+                                size_t(M) * plan.pyramid[size_t(k)].first * plan.pyramid[size_t(k)].second * C * sizeof(float), st));
+    } else {
+      RayBaseArgs ra;
+      const double* tm = target.camera.cam_from_world;
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) ra.Rcw_t[i * 3 + j] = tm[i * 4 + j];
+      ra.tfx = target.camera.fx;
+      ra.tfy = target.camera.fy;
+      ra.inv_span = 1.0 / target.far_depth - 1.0 / target.near_depth;
+      ra.half_w = double(target.camera.width) / 2.0;
+      ra.half_h = double(target.camera.height) / 2.0;
+      ra.h = hK;
+      ra.w = wK;
+      ra.M = M;
+      ray_base(cams.ray, ra, c->ray_base.p, st);
+      g_launches += 1;
+      for (int k = 0; k < K; ++k) {
+        ray_project(c->ray_base.p, M, hK, wK, int(plan.pyramid[size_t(k)].first),
+                    int(plan.pyramid[size_t(k)].second), W.ray_proj[size_t(k)], C,
+                    c->rays[size_t(k)].p, st);
+        g_launches += 1;
+      }
+    }
+  }
+
+  // ---- initialize -----------------------------------------------------------
+  float* V = c->V0.p;
+  float* Vs = c->V1.p;
+  int64_t L = plan.steps[0].layers, H = plan.steps[0].height, Wd = plan.steps[0].width;
+  {
+    const StepPlan& sp = plan.steps[0];
+    fill_rows(V, W.init_feature, L * H * Wd, C, st);
+    // flat band-centre depths (network.hpp:469-475)
+    fill_anchor_depths(c->depth_out.p, int(L), H * Wd, 1.0 / target.near_depth - 1.0 / target.far_depth,
+                       1.0 / target.far_depth, st);
+    g_launches += 2;
+    const int Hf = int(sp.feat_h), Wf = int(sp.feat_w);
+    ConvArgs in{};
+    in.nsrc = 0;
+    add_src(in, c->feats[size_t(sp.level)].p, C, Hf, Wf);
+    add_src(in, c->rays[size_t(sp.level)].p, C, Hf, Wf);
+    update_cnn(c, W.steps[0], in, M, Hf, Wf);
+    gather_stack(c->uu.p, M, Hf, Wf, C, cams.upd[0], ray_cam(target.camera, Wd, H),
+                 c->depth_out.p, int(L), int(H), int(Wd), c->deltas.p, st);
+    g_launches += 1;
+    for (const FusionW& f : W.steps[0].fusions) fusion(c, V, L, H, Wd, f);
+  }
+
+  // ---- update steps -----------------------------------------------------------
+  for (size_t s = 1; s < plan.steps.size(); ++s) {
+    const StepPlan& sp = plan.steps[s];
+    const StepW& sw = W.steps[s];
+    for (const ConvPairW& cw : sw.collapse) {
+      layer_collapse(V, int(L), H * Wd, C, cw.w1, cw.b1, cw.w2, cw.b2, Vs, st);
+      g_launches += 1;
+      std::swap(V, Vs);
+      L /= 2;
+    }
+    const int Hf = int(sp.feat_h), Wf = int(sp.feat_w), Hv = int(sp.render_h), Wv = int(sp.render_w);
+    const int Kp = Ca + 1;
+    const DepthAct act = depth_act(L, target);
+    // update_block: render the volume into every view (ldm.hpp:223-244)
+    decode_payload(V, int(L), int(H), int(Wd), C, W.w_appear, Ca, W.w_sigma, W.w_depth, act,
+                   ray_cam(target.camera, Wd, H), c->payload.p, c->depth_in.p, c->points.p, st);
+    g_launches += 1;
+    const float* feedback = c->fbr.p;
+    if (cfg.ablate_render) {
+      CUDA_OK(cudaMemsetAsync(c->fbr.p, 0, size_t(M) * Hf * Wf * Kp * sizeof(float), st));
+    } else {
+      CUDA_OK(cudaMemsetAsync(c->acc.p, 0, size_t(M) * L * Hv * Wv * (Kp + 1) * sizeof(float), st));
+      splat(c->payload.p, c->points.p, int(L), int(H * Wd), Kp, cams.rend[s], M, Hv, Wv, c->acc.p, st);
+      splat_composite(c->acc.p, M, int(L), Hv, Wv, Kp, c->fb.p, st);
+      g_launches += 2;
+      if (sp.doubled) {
+        resize_hwc(c->fb.p, c->fbr.p, M, Hv, Wv, Kp, Hf, Wf, st);
+        g_launches += 1;
+      } else {
+        feedback = c->fb.p;
+      }
+    }
+    ConvArgs in{};
+    in.nsrc = 0;
+    add_src(in, feedback, Kp, Hf, Wf);
+    add_src(in, c->feats[size_t(sp.level)].p, C, Hf, Wf);
+    add_src(in, c->rays[size_t(sp.level)].p, C, Hf, Wf);
+    update_cnn(c, sw, in, M, Hf, Wf);
+    // depth through the current volume, resized when the step doubles
+    const float* dgather = c->depth_in.p;
+    if (sp.doubled) {
+      resize_hwc(c->depth_in.p, c->depth_out.p, int(L), int(H), int(Wd), 1, int(sp.height),
+                 int(sp.width), st);
+      g_launches += 1;
+      dgather = c->depth_out.p;
+    }
+    gather_stack(c->uu.p, M, Hf, Wf, C, cams.upd[s], ray_cam(target.camera, sp.width, sp.height),
+                 dgather, int(L), int(sp.height), int(sp.width), c->deltas.p, st);
+    g_launches += 1;
+    if (sp.doubled) {
+      resize_hwc(V, Vs, int(L), int(H), int(Wd), C, int(sp.height), int(sp.width), st);
+      g_launches += 1;
+      std::swap(V, Vs);
+    }
+    H = sp.height;
+    Wd = sp.width;
+    for (const FusionW& f : sw.fusions) fusion(c, V, L, H, Wd, f);
+  }
+
+  // ---- decode_blend_logits + LDM pre-activation maps --------------------------
+  const int64_t P = L * H * Wd;
+  if (cfg.ablate_attention) {
+    CUDA_OK(cudaMemsetAsync(c->logits.p, 0, size_t(P) * M * sizeof(float), st));
+  } else {
+    blend_logits(V, c->deltas.p, P, C, M, W.blend_w, W.blend_gain, c->logits.p, st);
+    g_launches += 1;
+  }
+  decode_scalar(V, P, C, W.w_depth, c->pre_d.p, int(L), H * Wd, nullptr, st);
+  decode_scalar(V, P, C, W.w_sigma, c->pre_s.p, int(L), H * Wd, nullptr, st);
+  g_launches += 2;
+  c->have_ldm = true;
+  c->L = L;
+  c->H = H;
+  c->Wd = Wd;
+  c->M = M;
+  c->target = target;
+  c->V = V;
+  c->launches = g_launches - launches0;
+}
+
+RenderArgs render_args(lvsg_ctx* c, const float* images, int64_t Hr, int64_t Wr,
+                       const DevCam* cams_dev, float* rgb, int64_t row0, int64_t row1) {
+  RenderArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.pre_d = c->pre_d.p;
+  a.pre_s = c->pre_s.p;
+  a.logits = c->logits.p;
+  a.L = int(c->L);
+  a.H = int(c->H);
+  a.W = int(c->Wd);
+  a.M = int(c->M);
+  a.Ho = int(c->plan.out_height);
+  a.Wo = int(c->plan.out_width);
+  a.row0 = int(row0);
+  a.row1 = int(row1);
+  a.act = depth_act(c->L, c->target);
+  a.rc = ray_cam(c->target.camera, a.Wo, a.Ho);
+  a.cams = cams_dev;
+  a.images = images;
+  a.Hr = int(Hr);
+  a.Wr = int(Wr);
+  a.rgb = rgb;
+  a.bad_depth = c->bad_flag;
+  const double slack = 1e-3 * (c->target.far_depth - c->target.near_depth);
+  a.slack_lo = c->target.near_depth - slack;
+  a.slack_hi = c->target.far_depth + slack;
+  return a;
+}
+
+DevCam* upload_render_cams(lvsg_ctx* c, const lvsg_camera* cams) {
+  // render-only path (lvsg_render): a dedicated slot after the frame tables
+  const size_t M = size_t(c->M);
+  const size_t S = c->plan.steps.size();
+  const size_t off = (S * 2 + 1) * M * sizeof(DevCam) + M * sizeof(RayBaseCam);
+  CUDA_OK(cudaEventSynchronize(c->staging_done));
+  DevCam* h = reinterpret_cast<DevCam*>(static_cast<char*>(c->pinned) + off);
+  for (size_t m = 0; m < M; ++m) h[m] = dev_cam(cams[m]);
+  DevCam* d = reinterpret_cast<DevCam*>(reinterpret_cast<char*>(c->cams_dev.p) + off);
+  CUDA_OK(cudaMemcpyAsync(d, h, M * sizeof(DevCam), cudaMemcpyHostToDevice, c->stream));
+  CUDA_OK(cudaEventRecord(c->staging_done, c->stream));
+  return d;
+}
+
+void check_render_inputs(lvsg_ctx* c, int64_t views, const lvsg_camera* cams) {
+  if (!c->have_ldm) throw DimError("render_target: no LDM (call lvsg_forward first)");
+  if (views != c->M)
+    throw DimError("render_target: expected " + std::to_string(c->M) + " views, got " +
+                   std::to_string(views) + " images / " + std::to_string(views) + " cameras");
+  for (int64_t m = 0; m < views; ++m) camera_validate(cams[m]);
+}
+
+lvsg_status guard(lvsg_ctx* c, const auto& fn) {
+  try {
+    if (c) CUDA_OK(cudaSetDevice(c->device));
+    fn();
+    return LVSG_OK;
+  } catch (const DimError& e) {
+    if (c) c->err = e.what();
+    return LVSG_ERR_DIM;
+  } catch (const NumericError& e) {
+    if (c) c->err = e.what();
+    return LVSG_ERR_NUMERIC;
+  } catch (const CudaError& e) {
+    if (c) c->err = e.what();
+    return LVSG_ERR_CUDA;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    return LVSG_ERR_INTERNAL;
+  }
+}
+
+void sync_and_check(lvsg_ctx* c) {
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaStreamSynchronize(c->stream));
+  int bad = 0;
+  CUDA_OK(cudaMemcpy(&bad, c->bad_flag, sizeof(int), cudaMemcpyDeviceToHost));
+  if (bad) {
+    CUDA_OK(cudaMemset(c->bad_flag, 0, sizeof(int)));
+    throw DimError("world_points: depth outside [near, far]");
+  }
+}
+
+void upload_images(lvsg_ctx* c, Buf& dst, int64_t views, const float* const* images, int64_t H,
+                   int64_t W) {
+  if (!images) throw DimError("forward: null image list");
+  const size_t per = size_t(H * W * 3);
+  dst.ensure(per * size_t(views));
+  for (int64_t m = 0; m < views; ++m) {
+    if (!images[m]) throw DimError("forward: null image");
+    CUDA_OK(cudaMemcpyAsync(dst.p + per * size_t(m), images[m], per * sizeof(float),
+                            cudaMemcpyHostToDevice, c->stream));
+  }
+}
+
+void check_views(lvsg_ctx* c, int64_t views, int64_t H, int64_t W) {
+  if (views != c->cfg.views)
+    throw DimError("forward: expected " + std::to_string(c->cfg.views) + " views");
+  if (H < 1 || W < 1) throw DimError("forward: images must be [H,W,3]");
+}
+
+}  // namespace
+}  // namespace lvsg
+
+using namespace lvsg;
+
+extern "C" {
+
+lvsg_status lvsg_validate_config(const lvsg_model_config* cfg, char* err, size_t err_len) {
+  try {
+    Config::from_c(cfg).validate();
+    return LVSG_OK;
+  } catch (const std::exception& e) {
+    if (err && err_len) std::snprintf(err, err_len, "%s", e.what());
+    return LVSG_ERR_DIM;
+  }
+}
+
+lvsg_status lvsg_plan_forward(const lvsg_model_config* cfg, int64_t image_h, int64_t image_w,
+                              lvsg_plan* out, char* err, size_t err_len) {
+  try {
+    Plan p = plan_forward(Config::from_c(cfg), image_h, image_w);
+    std::memset(out, 0, sizeof(*out));
+    out->num_levels = int64_t(p.pyramid.size());
+    for (size_t k = 0; k < p.pyramid.size(); ++k) {
+      out->pyramid_h[k] = p.pyramid[k].first;
+      out->pyramid_w[k] = p.pyramid[k].second;
+    }
+    out->num_steps = int64_t(p.steps.size());
+    for (size_t s = 0; s < p.steps.size(); ++s) {
+      const StepPlan& sp = p.steps[s];
+      lvsg_step_plan& o = out->steps[s];
+      o.in_layers = sp.in_layers;
+      o.layers = sp.layers;
+      o.in_height = sp.in_height;
+      o.in_width = sp.in_width;
+      o.height = sp.height;
+      o.width = sp.width;
+      o.doubled = sp.doubled;
+      o.level = sp.level;
+      o.feat_h = sp.feat_h;
+      o.feat_w = sp.feat_w;
+      o.render_h = sp.render_h;
+      o.render_w = sp.render_w;
+      o.collapse_count = sp.collapse_count;
+      o.num_tokens = int64_t(sp.tokens.size());
+    }
+    out->out_height = p.out_height;
+    out->out_width = p.out_width;
+    return LVSG_OK;
+  } catch (const std::exception& e) {
+    if (err && err_len) std::snprintf(err, err_len, "%s", e.what());
+    return LVSG_ERR_DIM;
+  }
+}
+
+lvsg_status lvsg_param_count(const lvsg_model_config* cfg, int64_t* count, int64_t* total_numel) {
+  try {
+    auto l = param_layout(Config::from_c(cfg));
+    int64_t n = 0;
+    for (auto& p : l) n += p.numel();
+    if (count) *count = int64_t(l.size());
+    if (total_numel) *total_numel = n;
+    return LVSG_OK;
+  } catch (const std::exception&) {
+    return LVSG_ERR_DIM;
+  }
+}
+
+lvsg_status lvsg_param_shape(const lvsg_model_config* cfg, int64_t index, int32_t* rank,
+                             int64_t dims[4]) {
+  try {
+    auto l = param_layout(Config::from_c(cfg));
+    if (index < 0 || index >= int64_t(l.size())) return LVSG_ERR_DIM;
+    const auto& s = l[size_t(index)].shape;
+    *rank = int32_t(s.size());
+    for (int k = 0; k < 4; ++k) dims[k] = k < int(s.size()) ? s[size_t(k)] : 0;
+    return LVSG_OK;
+  } catch (const std::exception&) {
+    return LVSG_ERR_DIM;
+  }
+}
+
+lvsg_status lvsg_init_param_store(const lvsg_model_config* cfg, uint64_t seed, float* out) {
+  try {
+    init_param_store(Config::from_c(cfg), seed, out);
+    return LVSG_OK;
+  } catch (const std::exception&) {
+    return LVSG_ERR_DIM;
+  }
+}
+
+lvsg_status lvsg_create(const lvsg_model_config* cfg, int32_t device, lvsg_ctx** out) {
+  g_create_err.clear();
+  if (!out) return LVSG_ERR_DIM;
+  *out = nullptr;
+  std::unique_ptr<lvsg_ctx> c(new lvsg_ctx());
+  try {
+    c->cfg = Config::from_c(cfg);
+    c->cfg.validate();
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return LVSG_ERR_DIM;
+  }
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    g_create_err = "lvsg_create: no CUDA device";
+    return LVSG_ERR_NO_DEVICE;
+  }
+  if (device < 0 || device >= n) {
+    g_create_err = "lvsg_create: bad device ordinal";
+    return LVSG_ERR_NO_DEVICE;
+  }
+  c->device = device;
+  lvsg_status s = guard(c.get(), [&] {
+    cudaDeviceProp prop;
+    CUDA_OK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      throw CudaError("lvsg: built for sm_100a (B200); device is sm_" + std::to_string(prop.major) +
+                      std::to_string(prop.minor));
+    CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&c->staging_done, cudaEventDisableTiming));
+    CUDA_OK(cudaEventRecord(c->staging_done, c->stream));
+    CUDA_OK(cudaMalloc(&c->bad_flag, sizeof(int)));
+    CUDA_OK(cudaMemset(c->bad_flag, 0, sizeof(int)));
+    c->layout = param_layout(c->cfg);
+    c->total_params = 0;
+    for (auto& p : c->layout) c->total_params += p.numel();
+    c->weights.ensure(size_t(c->total_params));
+  });
+  if (s != LVSG_OK) {
+    g_create_err = c->err;
+    return s;
+  }
+  *out = c.release();
+  return LVSG_OK;
+}
+
+void lvsg_destroy(lvsg_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->bad_flag) cudaFree(c->bad_flag);
+  if (c->staging_done) cudaEventDestroy(c->staging_done);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* lvsg_last_error(const lvsg_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+lvsg_status lvsg_load_weights(lvsg_ctx* c, int64_t count, const float* const* tensors,
+                              const int32_t* ranks, const int64_t* dims) {
+  return guard(c, [&] {
+    if (count < int64_t(c->layout.size())) throw DimError("bind_params: store has too few tensors");
+    if (count > int64_t(c->layout.size())) throw DimError("bind_params: store has extra tensors");
+    std::vector<float> flat(size_t(c->total_params));
+    int64_t off = 0, doff = 0;
+    for (size_t i = 0; i < c->layout.size(); ++i) {
+      const auto& want = c->layout[i].shape;
+      std::vector<int64_t> got(dims + doff, dims + doff + ranks[i]);
+      doff += ranks[i];
+      if (got != want) {
+        auto str = [](const std::vector<int64_t>& s) {
+          std::string o = "[";
+          for (size_t k = 0; k < s.size(); ++k) o += (k ? "," : "") + std::to_string(s[k]);
+          return o + "]";
+        };
+        throw DimError("bind_params tensor: expected shape " + str(want) + ", got " + str(got));
+      }
+      const int64_t n = c->layout[i].numel();
+      std::memcpy(flat.data() + off, tensors[i], size_t(n) * sizeof(float));
+      off += n;
+    }
+    CUDA_OK(cudaMemcpy(c->weights.p, flat.data(), flat.size() * sizeof(float), cudaMemcpyHostToDevice));
+    bind_weights(c);
+    c->have_weights = true;
+  });
+}
+
+lvsg_status lvsg_init_weights(lvsg_ctx* c, uint64_t seed) {
+  return guard(c, [&] {
+    std::vector<float> flat(size_t(c->total_params));
+    init_param_store(c->cfg, seed, flat.data());
+    CUDA_OK(cudaMemcpy(c->weights.p, flat.data(), flat.size() * sizeof(float), cudaMemcpyHostToDevice));
+    bind_weights(c);
+    c->have_weights = true;
+  });
+}
+
+lvsg_status lvsg_forward(lvsg_ctx* c, int64_t views, const float* const* images, int64_t height,
+                         int64_t width, const lvsg_camera* cams, const lvsg_frustum* target,
+                         const lvsg_ldm_out* out) {
+  return guard(c, [&] {
+    check_views(c, views, height, width);
+    upload_images(c, c->enc_in, views, images, height, width);
+    forward_device(c, c->enc_in.p, height, width, cams, *target, nullptr, nullptr);
+    if (out) {
+      const int64_t P = c->L * c->H * c->Wd, M = c->M, C = c->cfg.channels;
+      const int64_t Po = c->L * c->plan.out_height * c->plan.out_width;
+      if (out->depth || out->density || out->blend) {
+        c->ldm_d.ensure(size_t(Po));
+        c->ldm_s.ensure(size_t(Po));
+        c->ldm_b.ensure(size_t(Po * M));
+        RenderArgs a = render_args(c, nullptr, 0, 0, nullptr, nullptr, 0, c->plan.out_height);
+        upsample_activate(a, c->ldm_d.p, c->ldm_s.p, c->ldm_b.p, c->stream);
+      }
+      sync_and_check(c);
+      auto d2h = [&](float* dst, const float* src, int64_t n) {
+        if (dst) CUDA_OK(cudaMemcpy(dst, src, size_t(n) * sizeof(float), cudaMemcpyDeviceToHost));
+      };
+      d2h(out->depth, c->ldm_d.p, Po);
+      d2h(out->density, c->ldm_s.p, Po);
+      d2h(out->blend, c->ldm_b.p, Po * M);
+      d2h(out->blend_logits, c->logits.p, P * M);
+      d2h(out->volume, c->V, P * C);
+    } else {
+      sync_and_check(c);
+    }
+  });
+}
+
+lvsg_status lvsg_render(lvsg_ctx* c, int64_t views, const float* const* images, int64_t height,
+                        int64_t width, const lvsg_camera* cams, float* rgb_out) {
+  return guard(c, [&] {
+    check_render_inputs(c, views, cams);
+    if (height < 1 || width < 1) throw DimError("render_target: images must be [H,W,3]");
+    upload_images(c, c->ren_in, views, images, height, width);
+    DevCam* dc = upload_render_cams(c, cams);
+    const int64_t Ho = c->plan.out_height, Wo = c->plan.out_width;
+    c->rgb.ensure(size_t(Ho * Wo * 3));
+    render_fused(render_args(c, c->ren_in.p, height, width, dc, c->rgb.p, 0, Ho), c->stream);
+    CUDA_OK(cudaMemcpyAsync(rgb_out, c->rgb.p, size_t(Ho * Wo * 3) * sizeof(float),
+                            cudaMemcpyDeviceToHost, c->stream));
+    sync_and_check(c);
+  });
+}
+
+lvsg_status lvsg_forward_render(lvsg_ctx* c, int64_t views, const float* const* enc_images,
+                                int64_t enc_h, int64_t enc_w, const lvsg_camera* enc_cams,
+                                const float* const* render_images, int64_t render_h,
+                                int64_t render_w, const lvsg_camera* render_cams,
+                                const lvsg_frustum* target, float* rgb_out) {
+  return guard(c, [&] {
+    check_views(c, views, enc_h, enc_w);
+    check_views(c, views, render_h, render_w);
+    for (int64_t m = 0; m < views; ++m) camera_validate(render_cams[m]);
+    upload_images(c, c->enc_in, views, enc_images, enc_h, enc_w);
+    upload_images(c, c->ren_in, views, render_images, render_h, render_w);
+    CamTables t;
+    forward_device(c, c->enc_in.p, enc_h, enc_w, enc_cams, *target, render_cams, &t);
+    const int64_t Ho = c->plan.out_height, Wo = c->plan.out_width;
+    c->rgb.ensure(size_t(Ho * Wo * 3));
+    render_fused(render_args(c, c->ren_in.p, render_h, render_w, t.final_cams, c->rgb.p, 0, Ho),
+                 c->stream);
+    c->launches += 1;
+    CUDA_OK(cudaMemcpyAsync(rgb_out, c->rgb.p, size_t(Ho * Wo * 3) * sizeof(float),
+                            cudaMemcpyDeviceToHost, c->stream));
+    sync_and_check(c);
+  });
+}
+
+lvsg_status lvsg_forward_render_device(lvsg_ctx* c, int64_t views, const float* enc_images,
+                                       int64_t enc_h, int64_t enc_w, const lvsg_camera* enc_cams,
+                                       const float* render_images, int64_t render_h,
+                                       int64_t render_w, const lvsg_camera* render_cams,
+                                       const lvsg_frustum* target, float* rgb_out, void* stream) {
+  return guard(c, [&] {
+    check_views(c, views, enc_h, enc_w);
+    check_views(c, views, render_h, render_w);
+    for (int64_t m = 0; m < views; ++m) camera_validate(render_cams[m]);
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    cudaStream_t own = c->stream;
+    if (user) c->stream = user;
+    try {
+      CamTables t;
+      forward_device(c, enc_images, enc_h, enc_w, enc_cams, *target, render_cams, &t);
+      const int64_t Ho = c->plan.out_height;
+      render_fused(render_args(c, render_images, render_h, render_w, t.final_cams, rgb_out, 0, Ho),
+                   c->stream);
+      c->launches += 1;
+      CUDA_OK(cudaGetLastError());
+    } catch (...) {
+      c->stream = own;
+      throw;
+    }
+    c->stream = own;
+  });
+}
+
+lvsg_status lvsg_render_rows_device(lvsg_ctx* c, int64_t views, const float* render_images,
+                                    int64_t render_h, int64_t render_w,
+                                    const lvsg_camera* render_cams, int64_t row0, int64_t row1,
+                                    float* rgb_out, void* stream) {
+  return guard(c, [&] {
+    check_render_inputs(c, views, render_cams);
+    if (row0 < 0 || row1 > c->plan.out_height || row0 > row1)
+      throw DimError("render_rows: bad row band");
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    cudaStream_t own = c->stream;
+    if (user) c->stream = user;
+    DevCam* dc = upload_render_cams(c, render_cams);
+    render_fused(render_args(c, render_images, render_h, render_w, dc, rgb_out, row0, row1),
+                 c->stream);
+    c->stream = own;
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+lvsg_status lvsg_synchronize(lvsg_ctx* c) {
+  return guard(c, [&] { sync_and_check(c); });
+}
+
+int64_t lvsg_last_launch_count(const lvsg_ctx* c) { return c ? c->launches : 0; }
+
+void* lvsg_stream(lvsg_ctx* c) { return c ? c->stream : nullptr; }
+
+lvsg_status lvsg_stage_world_points(lvsg_ctx* c, const lvsg_frustum* fr, const float* depth,
+                                    int64_t L, int64_t H, int64_t W, float* points) {
+  return guard(c, [&] {
+    frustum_validate(*fr);
+    if (L < 1 || H < 1 || W < 1) throw DimError("world_points: depth must be [L,H,W]");
+    const double slack = 1e-3 * (fr->far_depth - fr->near_depth);
+    stage_world_points(ray_cam(fr->camera, W, H), depth, int(L), int(H), int(W), points,
+                       fr->near_depth - slack, fr->far_depth + slack, c->bad_flag, c->stream);
+    sync_and_check(c);
+  });
+}
+
+lvsg_status lvsg_stage_footprints(lvsg_ctx* c, const lvsg_camera* cam, const float* points,
+                                  int64_t P, int32_t* taps, uint8_t* valid, double* fracs) {
+  return guard(c, [&] {
+    stage_footprints(dev_cam(*cam), points, P, taps, valid, fracs, c->stream);
+    sync_and_check(c);
+  });
+}
+
+lvsg_status lvsg_stage_gather(lvsg_ctx* c, const lvsg_camera* cam, const float* image,
+                              int64_t Hi, int64_t Wi, int64_t C, const float* points, int64_t P,
+                              float* values, float* mask) {
+  return guard(c, [&] {
+    stage_gather(dev_cam(*cam), image, int(Hi), int(Wi), int(C), points, P, values, mask, c->stream);
+    sync_and_check(c);
+  });
+}
+
+}  // extern "C"

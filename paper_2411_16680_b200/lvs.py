@@ -1,0 +1,324 @@
+"""Python mirror of the reference `lvs` C++ API for the per-frame path,
+backed by the native library (liblvsg.so) through the C ABI of
+include/lvsg.h.
+
+  reference (proj/include/lvs)                 here
+  ------------------------------------------  ----------------------------------
+  plan_forward (network.cpp:105-151)           plan_forward(cfg, h, w)
+  ModelConfig::validate (network.cpp:45-103)   validate_config(cfg)
+  init_param_store (network.hpp:354-362)       init_param_store(cfg, seed)
+  bind_params (network.hpp:330-339)            Model.load_weights(store)
+  forward (network.hpp:562-603)                Model.forward(images, cams, target)
+  render_target (ldm.hpp:193-199)              Model.render_target(images, cams)
+  forward-demo (main.cpp:533-541)              Model.forward_render(...)
+  RigSpec / make_scene / oracle_render         rig_cameras / scene_images
+
+Errors map to the reference's classes: DimError (shape / contract),
+NumericError, DeviceError. There is no CPU fallback: every compute call runs
+the CUDA kernels of liblvsg.so on the context's GPU.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import capi
+from .camera import Camera, Frustum, RigSpec
+from .config import ModelConfig
+
+vp = ctypes.c_void_p
+
+
+def _err_buf():
+    return ctypes.create_string_buffer(1024)
+
+
+def validate_config(cfg: ModelConfig) -> None:
+    cc = cfg.to_c()
+    e = _err_buf()
+    capi.raise_for(capi.lib().lvsg_validate_config(cc.ptr, e, 1024), e.value.decode())
+
+
+@dataclass
+class StepPlan:
+    in_layers: int
+    layers: int
+    in_height: int
+    in_width: int
+    height: int
+    width: int
+    doubled: bool
+    level: int
+    feat_h: int
+    feat_w: int
+    render_h: int
+    render_w: int
+    collapse_count: int
+    num_tokens: int
+
+
+@dataclass
+class ForwardPlan:
+    pyramid: List[tuple]
+    steps: List[StepPlan]
+    out_height: int
+    out_width: int
+
+
+def plan_forward(cfg: ModelConfig, image_h: int, image_w: int) -> ForwardPlan:
+    cc = cfg.to_c()
+    p = capi.PlanC()
+    e = _err_buf()
+    capi.raise_for(capi.lib().lvsg_plan_forward(cc.ptr, image_h, image_w, ctypes.byref(p), e, 1024),
+                   e.value.decode())
+    steps = []
+    for s in range(p.num_steps):
+        sp = p.steps[s]
+        steps.append(StepPlan(sp.in_layers, sp.layers, sp.in_height, sp.in_width, sp.height,
+                              sp.width, bool(sp.doubled), sp.level, sp.feat_h, sp.feat_w,
+                              sp.render_h, sp.render_w, sp.collapse_count, sp.num_tokens))
+    pyr = [(p.pyramid_h[k], p.pyramid_w[k]) for k in range(p.num_levels)]
+    return ForwardPlan(pyr, steps, p.out_height, p.out_width)
+
+
+def param_shapes(cfg: ModelConfig) -> List[tuple]:
+    cc = cfg.to_c()
+    n, tot = ctypes.c_int64(), ctypes.c_int64()
+    capi.raise_for(capi.lib().lvsg_param_count(cc.ptr, ctypes.byref(n), ctypes.byref(tot)),
+                   "bad config")
+    out = []
+    rank = ctypes.c_int32()
+    dims = (ctypes.c_int64 * 4)()
+    for i in range(n.value):
+        capi.lib().lvsg_param_shape(cc.ptr, i, ctypes.byref(rank), dims)
+        out.append(tuple(dims[k] for k in range(rank.value)))
+    return out
+
+
+def init_param_store(cfg: ModelConfig, seed: int, flat: bool = False):
+    """Bit-exact init_param_store<float>: a list of tensors in build_params
+    order (or one flat array with flat=True)."""
+    cc = cfg.to_c()
+    n, tot = ctypes.c_int64(), ctypes.c_int64()
+    capi.raise_for(capi.lib().lvsg_param_count(cc.ptr, ctypes.byref(n), ctypes.byref(tot)),
+                   "bad config")
+    buf = np.zeros(tot.value, np.float32)
+    capi.raise_for(capi.lib().lvsg_init_param_store(cc.ptr, seed, buf.ctypes.data_as(capi.c_f32p)),
+                   "bad config")
+    if flat:
+        return buf
+    out, off = [], 0
+    for shp in param_shapes(cfg):
+        k = int(np.prod(shp))
+        out.append(buf[off:off + k].reshape(shp))
+        off += k
+    return out
+
+
+def rig_cameras(rig: RigSpec):
+    """RigSpec::cameras() and ::target() (scenes.cpp:40-60)."""
+    n = rig.rows * rig.cols
+    cams = (capi.CameraC * n)()
+    tgt = capi.CameraC()
+    capi.raise_for(capi.lib().lvsg_rig_cameras(rig.rows, rig.cols, float(rig.baseline), rig.width,
+                                               rig.height, float(rig.focal), cams,
+                                               ctypes.byref(tgt)), "RigSpec")
+    return [Camera.from_c(c) for c in cams], Camera.from_c(tgt)
+
+
+def scene_images(seed: int, planes: int, scene_frustum: Frustum,
+                 cams: Sequence[Camera]) -> np.ndarray:
+    """make_scene + oracle_render (scenes.cpp:62-171) -> [M, H, W, 3] f32."""
+    H, W = cams[0].height, cams[0].width
+    assert all(c.height == H and c.width == W for c in cams)
+    out = np.zeros((len(cams), H, W, 3), np.float32)
+    arr = (capi.CameraC * len(cams))(*[c.to_c() for c in cams])
+    e = _err_buf()
+    L = capi.lib()
+    fr = scene_frustum.to_c()
+    capi.raise_for(L.lvsg_scene_images(seed, planes, ctypes.byref(fr), len(cams), arr,
+                                       out.ctypes.data_as(vp), e, 1024), e.value.decode())
+    return out
+
+
+def _cam_array(cams: Sequence[Camera]):
+    return (capi.CameraC * len(cams))(*[c.to_c() for c in cams])
+
+
+def _img_ptrs(images):
+    """images: [M,H,W,3] array or a list of [H,W,3] arrays (host, f32)."""
+    if isinstance(images, np.ndarray):
+        if images.ndim != 4 or images.shape[-1] != 3:
+            raise capi.DimError("images must be [M,H,W,3]")
+        ims = [np.ascontiguousarray(images[m], np.float32) for m in range(images.shape[0])]
+    else:
+        ims = [np.ascontiguousarray(im, np.float32) for im in images]
+    if not ims or any(im.ndim != 3 or im.shape[-1] != 3 for im in ims):
+        raise capi.DimError("images must be [H,W,3]")
+    H, W = ims[0].shape[:2]
+    if any(im.shape[:2] != (H, W) for im in ims):
+        raise capi.DimError("images must share one resolution")
+    arr = (capi.c_f32p * len(ims))(*[im.ctypes.data_as(capi.c_f32p) for im in ims])
+    return arr, ims, H, W
+
+
+@dataclass
+class Ldm:
+    """Ldm<T> (ldm.hpp:14-21) plus the pre-softmax blend logits and final
+    volume of ForwardResult (network.hpp:551-558)."""
+    depth: np.ndarray
+    density: np.ndarray
+    blend: np.ndarray
+    blend_logits: np.ndarray
+    volume: np.ndarray
+
+
+class Model:
+    """One lvsg context: device weights + stream + scratch arena for a
+    ModelConfig (forward is single-caller per instance, as SPEC.md:531)."""
+
+    def __init__(self, cfg: ModelConfig, device: int = 0):
+        self.cfg = cfg
+        self._cc = cfg.to_c()
+        self._lib = capi.lib()
+        h = ctypes.c_void_p()
+        code = self._lib.lvsg_create(self._cc.ptr, int(device), ctypes.byref(h))
+        capi.raise_for(code, (self._lib.lvsg_last_error(None) or b"").decode())
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.lvsg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, code):
+        if code != capi.OK:
+            capi.raise_for(code, (self._lib.lvsg_last_error(self._h) or b"").decode())
+
+    # --- weights (bind_params / init_params) ---
+    def load_weights(self, store: Sequence[np.ndarray]) -> None:
+        ts = [np.ascontiguousarray(t, np.float32) for t in store]
+        ptrs = (capi.c_f32p * len(ts))(*[t.ctypes.data_as(capi.c_f32p) for t in ts])
+        ranks = (ctypes.c_int32 * len(ts))(*[t.ndim for t in ts])
+        dims_l = [d for t in ts for d in t.shape]
+        dims = (ctypes.c_int64 * max(len(dims_l), 1))(*dims_l)
+        self._check(self._lib.lvsg_load_weights(self._h, len(ts), ptrs, ranks, dims))
+
+    def init_weights(self, seed: int) -> None:
+        self._check(self._lib.lvsg_init_weights(self._h, seed))
+
+    # --- forward / render ---
+    def forward(self, images, cams: Sequence[Camera], target: Frustum,
+                outputs: bool = True) -> Optional[Ldm]:
+        arr, keep, H, W = _img_ptrs(images)
+        fr = target.to_c()
+        out = None
+        res = None
+        if outputs:
+            plan = plan_forward(self.cfg, H, W)
+            last = plan.steps[-1]
+            L_, Hh, Ww, M, C = last.layers, last.height, last.width, self.cfg.views, self.cfg.channels
+            Ho, Wo = plan.out_height, plan.out_width
+            res = Ldm(np.zeros((L_, Ho, Wo), np.float32), np.zeros((L_, Ho, Wo), np.float32),
+                      np.zeros((L_, Ho, Wo, M), np.float32), np.zeros((L_, Hh, Ww, M), np.float32),
+                      np.zeros((L_, Hh, Ww, C), np.float32))
+            out = capi.LdmOutC(*[a.ctypes.data_as(capi.c_f32p) for a in
+                                 (res.depth, res.density, res.blend, res.blend_logits, res.volume)])
+        self._check(self._lib.lvsg_forward(self._h, len(keep), arr, H, W, _cam_array(cams),
+                                           ctypes.byref(fr), ctypes.byref(out) if out else None))
+        return res
+
+    def render_target(self, images, cams: Sequence[Camera]) -> np.ndarray:
+        arr, keep, H, W = _img_ptrs(images)
+        plan_h, plan_w = self._out_hw()
+        rgb = np.zeros((plan_h, plan_w, 3), np.float32)
+        self._check(self._lib.lvsg_render(self._h, len(keep), arr, H, W, _cam_array(cams),
+                                          rgb.ctypes.data_as(capi.c_f32p)))
+        return rgb
+
+    def forward_render(self, enc_images, enc_cams, render_images, render_cams,
+                       target: Frustum) -> np.ndarray:
+        ea, ek, He, We = _img_ptrs(enc_images)
+        ra, rk, Hr, Wr = _img_ptrs(render_images)
+        plan = plan_forward(self.cfg, He, We)
+        rgb = np.zeros((plan.out_height, plan.out_width, 3), np.float32)
+        fr = target.to_c()
+        self._last_enc_hw = (He, We)
+        self._check(self._lib.lvsg_forward_render(self._h, len(ek), ea, He, We,
+                                                  _cam_array(enc_cams), ra, Hr, Wr,
+                                                  _cam_array(render_cams), ctypes.byref(fr),
+                                                  rgb.ctypes.data_as(capi.c_f32p)))
+        return rgb
+
+    def forward_render_device(self, enc_images, enc_cams, render_images, render_cams,
+                              target: Frustum, rgb_out, stream=None) -> None:
+        """Device-resident path on torch CUDA tensors (enc [M,He,We,3],
+        render [M,Hr,Wr,3], rgb_out [Ho,Wo,3]); enqueued on `stream`
+        (torch.cuda.Stream or raw handle; default: torch's current stream)."""
+        import torch
+        for t in (enc_images, render_images, rgb_out):
+            if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+                raise capi.DimError("device tensors must be contiguous float32 CUDA tensors")
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        sh = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        M, He, We, _ = enc_images.shape
+        _, Hr, Wr, _ = render_images.shape
+        fr = target.to_c()
+        self._check(self._lib.lvsg_forward_render_device(
+            self._h, M, enc_images.data_ptr(), He, We, _cam_array(enc_cams),
+            render_images.data_ptr(), Hr, Wr, _cam_array(render_cams), ctypes.byref(fr),
+            rgb_out.data_ptr(), sh))
+
+    def render_rows_device(self, render_images, render_cams, row0, row1, rgb_out, stream=None):
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        sh = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        M, Hr, Wr, _ = render_images.shape
+        self._check(self._lib.lvsg_render_rows_device(self._h, M, render_images.data_ptr(), Hr, Wr,
+                                                      _cam_array(render_cams), row0, row1,
+                                                      rgb_out.data_ptr(), sh))
+
+    def synchronize(self):
+        self._check(self._lib.lvsg_synchronize(self._h))
+
+    def last_launch_count(self) -> int:
+        return int(self._lib.lvsg_last_launch_count(self._h))
+
+    def _out_hw(self):
+        last = self.cfg.steps[-1]
+        import math
+        return (int(math.floor(last.height * self.cfg.upsample + 0.5)),
+                int(math.floor(last.width * self.cfg.upsample + 0.5)))
+
+    # --- per-stage entry points (device pointers) ---
+    def stage_world_points(self, fr: Frustum, depth_t, points_t):
+        L_, H, W = depth_t.shape
+        f = fr.to_c()
+        self._check(self._lib.lvsg_stage_world_points(self._h, ctypes.byref(f), depth_t.data_ptr(),
+                                                      L_, H, W, points_t.data_ptr()))
+
+    def stage_footprints(self, cam: Camera, points_t, taps_t, valid_t, fracs_t):
+        c = cam.to_c()
+        P = points_t.numel() // 3
+        self._check(self._lib.lvsg_stage_footprints(self._h, ctypes.byref(c), points_t.data_ptr(), P,
+                                                    taps_t.data_ptr(), valid_t.data_ptr(),
+                                                    fracs_t.data_ptr()))
+
+    def stage_gather(self, cam: Camera, image_t, points_t, values_t, mask_t):
+        c = cam.to_c()
+        Hi, Wi, C = image_t.shape
+        P = points_t.numel() // 3
+        self._check(self._lib.lvsg_stage_gather(self._h, ctypes.byref(c), image_t.data_ptr(), Hi, Wi,
+                                                C, points_t.data_ptr(), P, values_t.data_ptr(),
+                                                mask_t.data_ptr()))
