@@ -1,0 +1,416 @@
+"""Benchmark: 1080p novel-view frames/s (reconstruct + render) on B200.
+
+Workload (BASELINE.json configs[1]): 8 synthetic
+input views (2x4 rig, 0.3 m span), full_scale_config (Table 6 schedule),
+encoder images 576x960, render images 1920x1080, 1080p target view,
+random-init weights (init_param_store seed 3), synthetic plane scene
+(make_scene seed 21). One step = one frame: lvs::forward + render_target.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lvsg|reference]
+
+N > 1 runs under torchrun, one rank per GPU; rank r renders its own target
+viewpoint (config 5 grid) of the same inputs, which rank 0 broadcasts over
+NCCL each step (weak scaling). Rank 0 prints one JSON line.
+
+`value` is device-timed (CUDA events on the launching stream) with inputs
+resident in HBM; `e2e` goes through the host C ABI (lvsg_forward_render)
+with pinned host buffers and both copies inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "1080p novel-view frames/sec (reconstruct+render), ms/frame, HBM GB/s vs peak"
+CPU_SAMPLE_DIV = 4  # the bounded CPU sample: config-2 schedule at 1/4 extents
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work per frame, from the plan
+# ---------------------------------------------------------------------------
+
+def frame_work(cfg, He, We, Hr, Wr):
+    from paper_2411_16680_b200 import plan_forward
+    from paper_2411_16680_b200.config import ModelConfig  # noqa: F401
+    plan = plan_forward(cfg, He, We)
+    M, C = cfg.views, cfg.channels
+    Ca = 3 if cfg.direct_rgb else C
+    conv = 2 * 27 * C * He * We * M
+    h, w = He, We
+    for _ in range(cfg.pyramid_levels):
+        conv += 4 * 2 * 9 * C * C * h * w * M
+        h //= 2
+        w //= 2
+    attn = 0
+    gather_texel_views = 0
+    from paper_2411_16680_b200.lvs import plan_forward as _pf  # noqa: F401
+    for s, sp in enumerate(plan.steps):
+        cin = 2 * C if s == 0 else 2 * C + Ca + 1
+        conv += 2 * 9 * cin * C * sp.feat_h * sp.feat_w * M
+        conv += 4 * 2 * 9 * C * C * sp.feat_h * sp.feat_w * M
+        P = sp.layers * sp.height * sp.width
+        gather_texel_views += P * M
+        toks = [t.strip() for t in cfg.steps[s].blocks.split(",")]
+        for t in toks:
+            if t.startswith("A"):
+                h_ = int(t[1:])
+                attn += P * (4 * h_ * C * C + 4 * M * h_ * C)
+            elif t == "C":
+                conv += 2 * 2 * 9 * C * C * sp.height * sp.width * sp.layers
+    last = plan.steps[-1]
+    Pf = last.layers * last.height * last.width
+    attn += Pf * (2 * C * C + 2 * M * C)  # blend head
+    Ho, Wo = plan.out_height, plan.out_width
+    # fused Stage 3 + 4: LDM pre-activation maps + M input images + output
+    render_bytes = Pf * (2 + M) * 4 + M * Hr * Wr * 3 * 4 + Ho * Wo * 3 * 4
+    gather_bytes = 0
+    for s, sp in enumerate(plan.steps):
+        gather_bytes += M * sp.feat_h * sp.feat_w * C * 4 + sp.layers * sp.height * sp.width * (4 + M * C * 4)
+    return {"conv_flops": conv, "attn_flops": attn, "render_bytes": render_bytes,
+            "gather_bytes": gather_bytes, "out_hw": (Ho, Wo),
+            "final_texel_views": last.layers * Ho * Wo * M}
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref): the bounded sample
+# ---------------------------------------------------------------------------
+
+_ref_state = {}
+
+
+def _ref_worker_init():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from bindings import Reference
+    from paper_2411_16680_b200.workloads import config2
+    c = config2(div=CPU_SAMPLE_DIV)
+    _ref_state.update(ref=Reference(), case=c, w=c.flat())
+
+
+def _ref_worker_frame(_):
+    r, c, w = _ref_state["ref"], _ref_state["case"], _ref_state["w"]
+    t = time.perf_counter()
+    r.forward_render(c.cfg, c.enc_images, c.enc_cams, c.ren_images, c.ren_cams, c.target, w)
+    return time.perf_counter() - t
+
+
+def cpu_sample_desc():
+    d = CPU_SAMPLE_DIV
+    return (f"config-2 schedule at 1/{d} extents (8 views, encoder {576 // d}x{960 // d}, render "
+            f"{1080 // d}x{1920 // d}, 1/{d * d} of every per-texel stage); one sample = "
+            f"1/{d * d} frame, fps scaled accordingly")
+
+
+def cpu_baseline_single():
+    """oracle/_ref (the reference built from its sources) on one host core."""
+    from bindings import REF_SO
+    if not os.path.exists(REF_SO):
+        return None
+    _ref_worker_init()
+    secs = _ref_worker_frame(0)
+    frames = 1.0 / (CPU_SAMPLE_DIV ** 2)
+    return {"value": frames / secs, "unit": "frames/s", "cores": 1, "kind": "reference",
+            "sample": cpu_sample_desc(), "sample_seconds": secs}
+
+
+def reference_arm(args):
+    """--impl reference: the reference CPU path on all usable host cores, as
+    P concurrent single-threaded processes (the reference is single-threaded,
+    SURVEY.md §8(d)); each step runs one bounded sample per process."""
+    import multiprocessing as mp
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from bindings import REF_SO
+    base = {"metric": METRIC, "unit": "frames/s", "impl": "reference", "n_gpus": args.gpus,
+            "higher_is_better": True}
+    if not os.path.exists(REF_SO):
+        print(json.dumps(dict(base, unavailable="oracle/_ref/libref.so not built")))
+        return
+    cores = os.cpu_count() or 1
+    try:
+        mem_gb = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 1e9
+    except Exception:
+        mem_gb = 64.0
+    procs = max(1, min(cores, int(mem_gb // 4.0), args.ref_procs or 10 ** 9))
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs, initializer=_ref_worker_init) as pool:
+        for _ in range(args.warmup):
+            pool.map(_ref_worker_frame, range(procs))
+        t0 = time.perf_counter()
+        per = []
+        for _ in range(args.steps):
+            per += pool.map(_ref_worker_frame, range(procs))
+        wall = time.perf_counter() - t0
+    frames = args.steps * procs / (CPU_SAMPLE_DIV ** 2)
+    fps = frames / wall
+    out = dict(base, value=fps, steps=args.steps, warmup=args.warmup,
+               ms_per_step=1000.0 * wall / args.steps, scaling="weak", vs_baseline=None,
+               dtype="f32", data="synthetic",
+               config={"workload": "config2 (8 views, full_scale_config, 576x960 -> 1080p)",
+                       "sample": cpu_sample_desc(), "processes": procs},
+               cpu_baseline={"value": fps, "unit": "frames/s", "cores": procs, "kind": "reference",
+                             "sample": cpu_sample_desc(),
+                             "mean_sample_seconds": statistics.mean(per)},
+               e2e={"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0})
+    print(json.dumps(out))
+
+
+# ---------------------------------------------------------------------------
+# the lvsg arm
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="lvsg", choices=["lvsg", "reference"])
+    ap.add_argument("--config", default="config2", choices=["config2", "config3"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--ref-procs", type=int, default=0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2411_16680_b200 as q
+    from paper_2411_16680_b200 import workloads as wl
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # each rank its own target viewpoint (config 5 grid) when sharded
+    center = (0.0, 0.0, 0.0) if world == 1 else wl.config5_targets()[rank % 8]
+    case = (wl.config2(target_center=center) if args.config == "config2"
+            else wl.config3())
+    cfg = case.cfg
+    M = cfg.views
+    model = q.Model(cfg, device=local)
+    model.init_weights(case.seed)
+    enc = torch.from_numpy(case.enc_images).to(dev)
+    ren = torch.from_numpy(case.ren_images).to(dev)
+    plan = q.plan_forward(cfg, enc.shape[1], enc.shape[2])
+    Ho, Wo = plan.out_height, plan.out_width
+    rgb = torch.empty((Ho, Wo, 3), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if world > 1:  # inputs arrive on rank 0; broadcast once per frame over NVLink
+            dist.broadcast(enc, 0)
+            dist.broadcast(ren, 0)
+        model.forward_render_device(enc, case.enc_cams, ren, case.ren_cams, case.target, rgb,
+                                    stream)
+
+    # warm-up (the first also sizes the arena); the last one is profiled per
+    # stage with CUDA events (never inside the timed region)
+    for i in range(args.warmup):
+        if i == args.warmup - 1:
+            model.profile(True)
+        step()
+        torch.cuda.synchronize()
+    stages = model.profile_read()
+    model.profile(False)
+    launches_per_step = model.last_launch_count()
+
+    # timed region: K frames, per-frame CUDA events, L2 flushed between frames
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            step()
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_per_step = ms_max / args.steps
+    fps = world * args.steps / (ms_max / 1000.0)
+
+    # e2e through the host C ABI: pinned host inputs, H2D + forward + render +
+    # D2H of the frame, every step
+    e2e = None
+    if not args.no_e2e:
+        enc_h = torch.from_numpy(case.enc_images).pin_memory()
+        ren_h = torch.from_numpy(case.ren_images).pin_memory()
+        out_h = torch.empty((Ho, Wo, 3), dtype=torch.float32).pin_memory()
+        e_np, r_np, o_np = enc_h.numpy(), ren_h.numpy(), out_h.numpy()
+        model.forward_render(e_np, case.enc_cams, r_np, case.ren_cams, case.target, out=o_np)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            model.forward_render(e_np, case.enc_cams, r_np, case.ren_cams, case.target, out=o_np)
+        sec = time.perf_counter() - t0
+        tt = torch.tensor([sec], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * args.e2e_steps / float(tt.item()), "unit": "frames/s",
+               "h2d_bytes_per_step": int(enc_h.numel() * 4 + ren_h.numel() * 4),
+               "d2h_bytes_per_step": int(out_h.numel() * 4), "steps": args.e2e_steps,
+               "path": "lvsg_forward_render (host C ABI, pinned buffers)"}
+
+    if rank == 0:
+        peaks = load_peaks()
+        work = frame_work(cfg, enc.shape[1], enc.shape[2], ren.shape[1], ren.shape[2])
+        stage_rows = {}
+        for k, (sms, n) in stages.items():
+            stage_rows[k] = {"ms": round(sms, 4), "launches": n}
+        if "conv" in stages:
+            ach = work["conv_flops"] / (stages["conv"][0] / 1e3) / 1e12
+            stage_rows["conv"].update(tflops=round(ach, 2), frac_bf16_peak=round(ach / peaks["bf16_tflops"], 4))
+        if "attention" in stages:
+            ach = work["attn_flops"] / (stages["attention"][0] / 1e3) / 1e12
+            stage_rows["attention"].update(tflops=round(ach, 2))
+        if "render" in stages:
+            gbs = work["render_bytes"] / (stages["render"][0] / 1e3) / 1e9
+            stage_rows["render"].update(gbs=round(gbs, 1), frac_hbm=round(gbs / peaks["hbm_gbs"], 4))
+        dom = max(stages.items(), key=lambda kv: kv[1][0])[0] if stages else None
+        if dom == "conv":
+            ach = work["conv_flops"] / (stages["conv"][0] / 1e3) / 1e12
+            roof = {"bound": "tensor", "kernel": "conv3x3_kernel (all conv3x3 launches of a frame)",
+                    "achieved": ach, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                    "frac": ach / peaks["bf16_tflops"], "traffic": None,
+                    "per_unit": f"{work['conv_flops'] / 1e9:.1f} GFLOP of conv3x3 per frame",
+                    "peak_source": peaks["source"] + ", dense bf16 burst",
+                    "note": "fp32 FFMA SIMT implicit GEMM (fp32-accurate solve); peak is the "
+                            "bf16 tensor figure"}
+        elif dom == "render":
+            gbs = work["render_bytes"] / (stages["render"][0] / 1e3) / 1e9
+            roof = {"bound": "hbm", "kernel": "render_fused_kernel", "achieved": gbs,
+                    "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"],
+                    "traffic": None, "peak_source": peaks["source"]}
+        else:
+            roof = {"bound": "hbm", "kernel": dom, "achieved": None, "peak": peaks["hbm_gbs"],
+                    "unit": "GB/s", "frac": None, "traffic": None}
+        roof["stages"] = stage_rows
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            try:
+                cpu = cpu_baseline_single()
+            except Exception as e:  # reported, never fatal
+                cpu = {"value": None, "error": str(e)}
+        out = {
+            "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (make_scene seed 21 plane scene, init_param_store seed 3 weights)",
+            "config": {"workload": f"{args.config}: {M} views, full_scale_config, encoder "
+                                   f"{enc.shape[1]}x{enc.shape[2]}, render {ren.shape[1]}x"
+                                   f"{ren.shape[2]}, output {Ho}x{Wo}",
+                       "per_gpu": "one target viewpoint per rank" if world > 1 else "1 target",
+                       "l2": "flushed (256 MB write) between timed frames",
+                       "parallelism": f"replicas x{world} (target-sharded), NCCL input broadcast"
+                       if world > 1 else "single GPU"},
+            "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "roofline": roof, "cpu_baseline": cpu, "clocks": clocks.summary(),
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -177,6 +177,12 @@ lvsg_status lvsg_synchronize(lvsg_ctx* ctx);
 /* Per-frame kernel-launch count of the last forward_render (for the bench's
  * gpu_launches claim) and the CUDA stream the context enqueues on. */
 int64_t lvsg_last_launch_count(const lvsg_ctx* ctx);
+/* Per-stage device timing: when enabled, an event closes every launch group
+ * (stages: conv, gather, attention, splat, collapse, render, misc);
+ * lvsg_profile_read writes "stage total_ms launches" lines accumulated since
+ * the last read. Adds event records, so never enabled in a timed run. */
+lvsg_status lvsg_profile_enable(lvsg_ctx* ctx, int32_t on);
+lvsg_status lvsg_profile_read(lvsg_ctx* ctx, char* buf, size_t len);
 void* lvsg_stream(lvsg_ctx* ctx);
 
 /* ---- stage entry points (per-stage parity, SURVEY.md §7 hard part 2) -----

@@ -99,6 +99,7 @@ SYMBOLS = [
     "lvsg_forward_render", "lvsg_forward_render_device", "lvsg_render_rows_device",
     "lvsg_synchronize", "lvsg_last_launch_count", "lvsg_stream", "lvsg_stage_world_points",
     "lvsg_stage_footprints", "lvsg_stage_gather", "lvsg_rig_cameras", "lvsg_scene_images",
+    "lvsg_profile_enable", "lvsg_profile_read",
 ]
 
 
@@ -148,5 +149,7 @@ def lib() -> ctypes.CDLL:
                                    P(CameraC)]
     L.lvsg_scene_images.argtypes = [ctypes.c_uint64, c_i64, P(FrustumC), c_i64, P(CameraC), vp,
                                     ctypes.c_char_p, ctypes.c_size_t]
+    L.lvsg_profile_enable.argtypes = [vp, c_i32]
+    L.lvsg_profile_read.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
     _lib = L
     return L

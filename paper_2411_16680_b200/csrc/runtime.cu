@@ -166,12 +166,51 @@ struct lvsg_ctx {
   lvsg_frustum target{};
   float* V = nullptr;
   int64_t launches = 0;
+
+  // optional per-stage device timing (lvsg_profile_*): one event after each
+  // group of launches; consecutive events bound that group's device time
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_pool;
+  std::vector<const char*> prof_labels;
+  std::vector<int> prof_counts;
+  std::map<std::string, std::pair<double, int64_t>> prof_acc;
 };
 
 namespace lvsg {
 namespace {
 
 thread_local std::string g_create_err;
+
+// Counts `n` kernel launches under `label`; when profiling, records an event
+// that closes the group on the context stream.
+void mark(lvsg_ctx* c, const char* label, int n) {
+  g_launches += n;
+  if (!c->prof) return;
+  const size_t i = c->prof_labels.size();
+  if (i >= c->prof_pool.size()) {
+    cudaEvent_t e;
+    CUDA_OK(cudaEventCreate(&e));
+    c->prof_pool.push_back(e);
+  }
+  CUDA_OK(cudaEventRecord(c->prof_pool[i], c->stream));
+  c->prof_labels.push_back(label);
+  c->prof_counts.push_back(n);
+}
+
+// Folds the recorded events of the last frame into the accumulators.
+void prof_collect(lvsg_ctx* c) {
+  if (!c->prof || c->prof_labels.size() < 2) return;
+  CUDA_OK(cudaEventSynchronize(c->prof_pool[c->prof_labels.size() - 1]));
+  for (size_t i = 1; i < c->prof_labels.size(); ++i) {
+    float ms = 0.f;
+    CUDA_OK(cudaEventElapsedTime(&ms, c->prof_pool[i - 1], c->prof_pool[i]));
+    auto& a = c->prof_acc[c->prof_labels[i]];
+    a.first += ms;
+    a.second += c->prof_counts[i];
+  }
+  c->prof_labels.clear();
+  c->prof_counts.clear();
+}
 
 void bind_weights(lvsg_ctx* c) {
   const Config& cfg = c->cfg;
@@ -351,7 +390,7 @@ void conv_residual(lvsg_ctx* c, const float* x, float* out, float* tmp, int B, i
   b2.res_pstride = C;
   b2.res_bstride = (long long)H * W * C;
   conv3x3(b2, c->stream);
-  g_launches += 2;
+  mark(c, "conv", 2);
 }
 
 // run_update_cnn (network.hpp:155-160) on concatenated sources, all views.
@@ -369,7 +408,7 @@ void update_cnn(lvsg_ctx* c, const StepW& sw, const ConvArgs& stem_in, int M, in
   a.out_pstride = C;
   a.out_bstride = (long long)Hf * Wf * C;
   conv3x3(a, c->stream);
-  g_launches += 1;
+  mark(c, "conv", 1);
   conv_residual(c, c->uh.p, c->uh.p, c->ut.p, M, Hf, Wf, sw.r1);
   conv_residual(c, c->uh.p, c->uu.p, c->ut.p, M, Hf, Wf, sw.r2);
 }
@@ -380,10 +419,11 @@ void fusion(lvsg_ctx* c, float* V, int64_t L, int64_t H, int64_t W, const Fusion
   const int64_t P = L * H * W;
   attend(V, c->deltas.p, P, C, M, f.heads, f.wq, nullptr, f.wo, f.gain, c->cfg.ablate_attention,
          c->stream);
-  g_launches += 1;
+  mark(c, "attention", 1);
   for (const MlpW& m : f.mlps) {
     // conv_mlp_residual (attention.hpp:262-267), batched over layers
     rms_rinv(V, c->rinv.p, P, C, c->stream);
+    mark(c, "misc", 1);
     ConvArgs a = conv_args(int(L), int(H), int(W), C, C, m.w1, m.b1, c->t1.p);
     add_src(a, V, C, int(H), int(W));
     a.rinv = c->rinv.p;
@@ -396,7 +436,7 @@ void fusion(lvsg_ctx* c, float* V, int64_t L, int64_t H, int64_t W, const Fusion
     b.res_pstride = C;
     b.res_bstride = (long long)H * W * C;
     conv3x3(b, c->stream);
-    g_launches += 3;
+    mark(c, "conv", 2);
   }
 }
 
@@ -477,6 +517,10 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
   cudaStream_t st = c->stream;
   const NetW& W = c->W;
   const int64_t launches0 = g_launches;
+  if (c->prof) {
+    prof_collect(c);
+    mark(c, "start", 0);
+  }
   CamTables cams = upload_cams(c, enc_cams, target, render_cams);
   if (tables_out) *tables_out = cams;
 
@@ -487,14 +531,14 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
     a.src[0] = ConvSrc{enc, 3, 3, (long long)h * w * 3};
     a.nsrc = 1;
     conv3x3(a, st);
-    g_launches += 1;
+    mark(c, "conv", 1);
     const float* x = c->enc_x.p;
     for (int k = 0; k < K; ++k) {
       float* xo = k == 0 ? c->enc_x.p : c->enc_x.p;  // level >= 1 reads feats[k-1], writes enc_x
       conv_residual(c, x, xo, c->enc_t.p, M, h, w, W.lvl_r1[size_t(k)]);
       conv_residual(c, xo, xo, c->enc_t.p, M, h, w, W.lvl_r2[size_t(k)]);
       mean_pool2(xo, c->feats[size_t(k)].p, M, h, w, C, st);
-      g_launches += 1;
+      mark(c, "misc", 1);
       h /= 2;
       w /= 2;
       x = c->feats[size_t(k)].p;
@@ -518,12 +562,12 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
       ra.w = wK;
       ra.M = M;
       ray_base(cams.ray, ra, c->ray_base.p, st);
-      g_launches += 1;
+      mark(c, "misc", 1);
       for (int k = 0; k < K; ++k) {
         ray_project(c->ray_base.p, M, hK, wK, int(plan.pyramid[size_t(k)].first),
                     int(plan.pyramid[size_t(k)].second), W.ray_proj[size_t(k)], C,
                     c->rays[size_t(k)].p, st);
-        g_launches += 1;
+        mark(c, "misc", 1);
       }
     }
   }
@@ -538,7 +582,7 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
     // flat band-centre depths (network.hpp:469-475)
     fill_anchor_depths(c->depth_out.p, int(L), H * Wd, 1.0 / target.near_depth - 1.0 / target.far_depth,
                        1.0 / target.far_depth, st);
-    g_launches += 2;
+    mark(c, "misc", 2);
     const int Hf = int(sp.feat_h), Wf = int(sp.feat_w);
     ConvArgs in{};
     in.nsrc = 0;
@@ -547,7 +591,7 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
     update_cnn(c, W.steps[0], in, M, Hf, Wf);
     gather_stack(c->uu.p, M, Hf, Wf, C, cams.upd[0], ray_cam(target.camera, Wd, H),
                  c->depth_out.p, int(L), int(H), int(Wd), c->deltas.p, st);
-    g_launches += 1;
+    mark(c, "gather", 1);
     for (const FusionW& f : W.steps[0].fusions) fusion(c, V, L, H, Wd, f);
   }
 
@@ -557,7 +601,7 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
     const StepW& sw = W.steps[s];
     for (const ConvPairW& cw : sw.collapse) {
       layer_collapse(V, int(L), H * Wd, C, cw.w1, cw.b1, cw.w2, cw.b2, Vs, st);
-      g_launches += 1;
+      mark(c, "collapse", 1);
       std::swap(V, Vs);
       L /= 2;
     }
@@ -567,7 +611,7 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
     // update_block: render the volume into every view (ldm.hpp:223-244)
     decode_payload(V, int(L), int(H), int(Wd), C, W.w_appear, Ca, W.w_sigma, W.w_depth, act,
                    ray_cam(target.camera, Wd, H), c->payload.p, c->depth_in.p, c->points.p, st);
-    g_launches += 1;
+    mark(c, "splat", 1);
     const float* feedback = c->fbr.p;
     if (cfg.ablate_render) {
       CUDA_OK(cudaMemsetAsync(c->fbr.p, 0, size_t(M) * Hf * Wf * Kp * sizeof(float), st));
@@ -575,10 +619,10 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
       CUDA_OK(cudaMemsetAsync(c->acc.p, 0, size_t(M) * L * Hv * Wv * (Kp + 1) * sizeof(float), st));
       splat(c->payload.p, c->points.p, int(L), int(H * Wd), Kp, cams.rend[s], M, Hv, Wv, c->acc.p, st);
       splat_composite(c->acc.p, M, int(L), Hv, Wv, Kp, c->fb.p, st);
-      g_launches += 2;
+      mark(c, "splat", 2);
       if (sp.doubled) {
         resize_hwc(c->fb.p, c->fbr.p, M, Hv, Wv, Kp, Hf, Wf, st);
-        g_launches += 1;
+        mark(c, "misc", 1);
       } else {
         feedback = c->fb.p;
       }
@@ -594,15 +638,15 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
     if (sp.doubled) {
       resize_hwc(c->depth_in.p, c->depth_out.p, int(L), int(H), int(Wd), 1, int(sp.height),
                  int(sp.width), st);
-      g_launches += 1;
+      mark(c, "misc", 1);
       dgather = c->depth_out.p;
     }
     gather_stack(c->uu.p, M, Hf, Wf, C, cams.upd[s], ray_cam(target.camera, sp.width, sp.height),
                  dgather, int(L), int(sp.height), int(sp.width), c->deltas.p, st);
-    g_launches += 1;
+    mark(c, "gather", 1);
     if (sp.doubled) {
       resize_hwc(V, Vs, int(L), int(H), int(Wd), C, int(sp.height), int(sp.width), st);
-      g_launches += 1;
+      mark(c, "misc", 1);
       std::swap(V, Vs);
     }
     H = sp.height;
@@ -616,11 +660,11 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
     CUDA_OK(cudaMemsetAsync(c->logits.p, 0, size_t(P) * M * sizeof(float), st));
   } else {
     blend_logits(V, c->deltas.p, P, C, M, W.blend_w, W.blend_gain, c->logits.p, st);
-    g_launches += 1;
+    mark(c, "attention", 1);
   }
   decode_scalar(V, P, C, W.w_depth, c->pre_d.p, int(L), H * Wd, nullptr, st);
   decode_scalar(V, P, C, W.w_sigma, c->pre_s.p, int(L), H * Wd, nullptr, st);
-  g_launches += 2;
+  mark(c, "misc", 2);
   c->have_ldm = true;
   c->L = L;
   c->H = H;
@@ -986,6 +1030,7 @@ lvsg_status lvsg_forward_render(lvsg_ctx* c, int64_t views, const float* const* 
     c->rgb.ensure(size_t(Ho * Wo * 3));
     render_fused(render_args(c, c->ren_in.p, render_h, render_w, t.final_cams, c->rgb.p, 0, Ho),
                  c->stream);
+    mark(c, "render", 1);
     c->launches += 1;
     CUDA_OK(cudaMemcpyAsync(rgb_out, c->rgb.p, size_t(Ho * Wo * 3) * sizeof(float),
                             cudaMemcpyDeviceToHost, c->stream));
@@ -1011,7 +1056,8 @@ lvsg_status lvsg_forward_render_device(lvsg_ctx* c, int64_t views, const float* 
       const int64_t Ho = c->plan.out_height;
       render_fused(render_args(c, render_images, render_h, render_w, t.final_cams, rgb_out, 0, Ho),
                    c->stream);
-      c->launches += 1;
+      mark(c, "render", 1);
+    c->launches += 1;
       CUDA_OK(cudaGetLastError());
     } catch (...) {
       c->stream = own;
@@ -1045,6 +1091,31 @@ lvsg_status lvsg_synchronize(lvsg_ctx* c) {
 }
 
 int64_t lvsg_last_launch_count(const lvsg_ctx* c) { return c ? c->launches : 0; }
+
+lvsg_status lvsg_profile_enable(lvsg_ctx* c, int32_t on) {
+  return guard(c, [&] {
+    prof_collect(c);
+    c->prof = on != 0;
+    c->prof_labels.clear();
+    c->prof_counts.clear();
+    c->prof_acc.clear();
+  });
+}
+
+lvsg_status lvsg_profile_read(lvsg_ctx* c, char* buf, size_t len) {
+  return guard(c, [&] {
+    prof_collect(c);
+    std::string out;
+    for (const auto& kv : c->prof_acc) {
+      char line[160];
+      std::snprintf(line, sizeof(line), "%s %.6f %lld\n", kv.first.c_str(), kv.second.first,
+                    (long long)kv.second.second);
+      out += line;
+    }
+    c->prof_acc.clear();
+    if (buf && len) std::snprintf(buf, len, "%s", out.c_str());
+  });
+}
 
 void* lvsg_stream(lvsg_ctx* c) { return c ? c->stream : nullptr; }
 

@@ -246,11 +246,17 @@ class Model:
         return rgb
 
     def forward_render(self, enc_images, enc_cams, render_images, render_cams,
-                       target: Frustum) -> np.ndarray:
+                       target: Frustum, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """Host buffers in, host RGB out (optionally into `out`, e.g. a view of
+        pinned memory)."""
         ea, ek, He, We = _img_ptrs(enc_images)
         ra, rk, Hr, Wr = _img_ptrs(render_images)
-        plan = plan_forward(self.cfg, He, We)
-        rgb = np.zeros((plan.out_height, plan.out_width, 3), np.float32)
+        if out is None:
+            plan = plan_forward(self.cfg, He, We)
+            rgb = np.zeros((plan.out_height, plan.out_width, 3), np.float32)
+        else:
+            rgb = out
+            assert rgb.dtype == np.float32 and rgb.flags.c_contiguous
         fr = target.to_c()
         self._last_enc_hw = (He, We)
         self._check(self._lib.lvsg_forward_render(self._h, len(ek), ea, He, We,
@@ -291,6 +297,19 @@ class Model:
 
     def synchronize(self):
         self._check(self._lib.lvsg_synchronize(self._h))
+
+    def profile(self, on: bool) -> None:
+        self._check(self._lib.lvsg_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self) -> dict:
+        """{stage: (device_ms, launches)} accumulated since the last read."""
+        buf = ctypes.create_string_buffer(8192)
+        self._check(self._lib.lvsg_profile_read(self._h, buf, 8192))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            k, ms, n = line.split()
+            out[k] = (float(ms), int(n))
+        return out
 
     def last_launch_count(self) -> int:
         return int(self._lib.lvsg_last_launch_count(self._h))
