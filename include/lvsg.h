@@ -214,6 +214,13 @@ lvsg_status lvsg_scene_images(uint64_t seed, int64_t planes, const lvsg_frustum*
                               int64_t views, const lvsg_camera* cams, float* images, char* err,
                               size_t err_len);
 
+/* conv3x3 (kernels_ref.hpp:72-96) on DEVICE channel-last tensors x
+ * [B,H,W,Cin] -> y [B,H,W,Cout], w [Cout,Cin,3,3], b [Cout] (nullable).
+ * impl: 0 auto, 1 fp32 SIMT, 2 tcgen05 3xTF32 (when Cin = Cout = 32). */
+lvsg_status lvsg_stage_conv3x3(lvsg_ctx* ctx, const float* x, const float* w, const float* b,
+                               float* y, int64_t B, int64_t Cin, int64_t Cout, int64_t H,
+                               int64_t W, int32_t impl);
+
 #ifdef __cplusplus
 }
 #endif

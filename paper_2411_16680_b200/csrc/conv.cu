@@ -11,6 +11,8 @@
 // memory 8 at a time as a (8+2)x(32+2) halo tile (row pitch 36 floats so every
 // lane's 8-wide window is 16-byte aligned and conflict-free); the 9x8x32
 // weight slab is read with warp-broadcast LDS.128.
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace lvsg {
@@ -129,7 +131,19 @@ __global__ void __launch_bounds__(NT) conv3x3_kernel(const ConvArgs a) {
 
 }  // namespace
 
-void conv3x3(const ConvArgs& a, cudaStream_t st) {
+void conv3x3(const ConvArgs& a, cudaStream_t st, int impl) {
+  static const int env = [] {
+    const char* e = getenv("LVSG_CONV");
+    return e && e[0] == 's' ? 1 : 0;  // LVSG_CONV=simt forces the SIMT kernel
+  }();
+  if (impl == 0) impl = env ? 1 : 2;
+  if (impl == 2 && conv3x3_tc_supported(a))
+    conv3x3_tc(a, st);
+  else
+    conv3x3_simt(a, st);
+}
+
+void conv3x3_simt(const ConvArgs& a, cudaStream_t st) {
   const int tiles = ((a.W + TW - 1) / TW) * ((a.H + TH - 1) / TH);
   dim3 grid(tiles, (a.Cout + COT - 1) / COT, a.B);
   conv3x3_kernel<<<grid, NT, 0, st>>>(a);

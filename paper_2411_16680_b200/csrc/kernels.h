@@ -37,7 +37,13 @@ struct ConvArgs {
   int res_pstride;
   long long res_bstride;
 };
-void conv3x3(const ConvArgs& a, cudaStream_t st);
+// Dispatches to the tcgen05 3xTF32 kernel when it applies (Cin = Cout = 32,
+// one 16-byte-aligned source), else to the fp32 SIMT kernel. impl: 0 auto,
+// 1 SIMT, 2 tcgen05 (unsupported shapes fall back to SIMT).
+void conv3x3(const ConvArgs& a, cudaStream_t st, int impl = 0);
+void conv3x3_simt(const ConvArgs& a, cudaStream_t st);
+bool conv3x3_tc_supported(const ConvArgs& a);
+void conv3x3_tc(const ConvArgs& a, cudaStream_t st);
 
 // ---- elementwise / layout ------------------------------------------------
 void fill_rows(float* out, const float* row, int64_t rows, int C, cudaStream_t st);

@@ -1139,6 +1139,18 @@ lvsg_status lvsg_stage_footprints(lvsg_ctx* c, const lvsg_camera* cam, const flo
   });
 }
 
+lvsg_status lvsg_stage_conv3x3(lvsg_ctx* c, const float* x, const float* w, const float* b,
+                               float* y, int64_t B, int64_t Cin, int64_t Cout, int64_t H,
+                               int64_t W, int32_t impl) {
+  return guard(c, [&] {
+    if (B < 1 || Cin < 1 || Cout < 1 || H < 1 || W < 1) throw DimError("conv3x3: bad shapes");
+    ConvArgs a = conv_args(int(B), int(H), int(W), int(Cin), int(Cout), w, b, y);
+    add_src(a, x, int(Cin), int(H), int(W));
+    conv3x3(a, c->stream, impl);
+    sync_and_check(c);
+  });
+}
+
 lvsg_status lvsg_stage_gather(lvsg_ctx* c, const lvsg_camera* cam, const float* image,
                               int64_t Hi, int64_t Wi, int64_t C, const float* points, int64_t P,
                               float* values, float* mask) {

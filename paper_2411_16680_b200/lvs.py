@@ -334,6 +334,15 @@ class Model:
                                                     taps_t.data_ptr(), valid_t.data_ptr(),
                                                     fracs_t.data_ptr()))
 
+    def stage_conv3x3(self, x_t, w_t, b_t, y_t, impl: int = 0):
+        """x [B,H,W,Cin] -> y [B,H,W,Cout] (device tensors); impl 0 auto,
+        1 fp32 SIMT, 2 tcgen05 3xTF32."""
+        B, H, W, Cin = x_t.shape
+        Cout = w_t.shape[0]
+        self._check(self._lib.lvsg_stage_conv3x3(self._h, x_t.data_ptr(), w_t.data_ptr(),
+                                                 b_t.data_ptr() if b_t is not None else None,
+                                                 y_t.data_ptr(), B, Cin, Cout, H, W, impl))
+
     def stage_gather(self, cam: Camera, image_t, points_t, values_t, mask_t):
         c = cam.to_c()
         Hi, Wi, C = image_t.shape
