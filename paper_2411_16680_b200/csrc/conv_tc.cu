@@ -56,22 +56,40 @@ __device__ __forceinline__ void stage_halo(const ConvArgs& a, const TileCoord& t
   const ConvSrc& S = a.src[0];
   const float* src = S.ptr + (long long)tc_.b * S.bstride;
   const long long HW = (long long)a.H * a.W;
-  for (int e = threadIdx.x; e < HALO_PX * NCH; e += NT) {
-    const int px = e >> 3, j = e & 7;
-    const int hy = px / HWD, hx = px - hy * HWD;
-    const int gy = tc_.y0 - 1 + hy, gx = tc_.x0 - 1 + hx;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W) {
-      const long long p = (long long)gy * a.W + gx;
-      v = __ldg(reinterpret_cast<const float4*>(src + p * S.pstride) + j);
-      if (a.rinv) {
-        const float r = __ldg(a.rinv + tc_.b * HW + p);
-        const float4 g = __ldg(reinterpret_cast<const float4*>(a.gain) + j);
-        v.x = fm(fm(v.x, r), g.x);
-        v.y = fm(fm(v.y, r), g.y);
-        v.z = fm(fm(v.z, r), g.z);
-        v.w = fm(fm(v.w, r), g.w);
+  // all global loads of this thread first (memory-level parallelism), then
+  // the tf32 split and the shared-memory stores
+  constexpr int PER = (HALO_PX * NCH + NT - 1) / NT;
+  float4 vals[PER];
+  float rs[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int e = threadIdx.x + k * NT;
+    vals[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    rs[k] = 1.f;
+    if (e < HALO_PX * NCH) {
+      const int px = e >> 3, j = e & 7;
+      const int hy = px / HWD, hx = px - hy * HWD;
+      const int gy = tc_.y0 - 1 + hy, gx = tc_.x0 - 1 + hx;
+      if (gy >= 0 && gy < a.H && gx >= 0 && gx < a.W) {
+        const long long p = (long long)gy * a.W + gx;
+        vals[k] = __ldg(reinterpret_cast<const float4*>(src + p * S.pstride) + j);
+        if (a.rinv) rs[k] = __ldg(a.rinv + tc_.b * HW + p);
       }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int e = threadIdx.x + k * NT;
+    if (e >= HALO_PX * NCH) break;
+    const int px = e >> 3, j = e & 7;
+    float4 v = vals[k];
+    if (a.rinv) {
+      const float r = rs[k];
+      const float4 g = __ldg(reinterpret_cast<const float4*>(a.gain) + j);
+      v.x = fm(fm(v.x, r), g.x);
+      v.y = fm(fm(v.y, r), g.y);
+      v.z = fm(fm(v.z, r), g.z);
+      v.w = fm(fm(v.w, r), g.w);
     }
     float4 h, l;
     tc::split_tf32(v.x, h.x, l.x);

@@ -1,0 +1,224 @@
+// C = 32 specialisations of the per-texel MLP kernels (the production
+// channel count): every per-texel vector lives in registers (float4 loads),
+// weights are shared-memory broadcasts. Same arithmetic order as the generic
+// kernels in kernels.cu.
+#include "kernels.h"
+
+namespace lvsg {
+namespace {
+
+constexpr int C = 32;
+
+__device__ __forceinline__ void load_row(const float* p, float* v) {
+  const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+  for (int k = 0; k < C / 4; ++k) {
+    const float4 t = __ldg(q + k);
+    v[4 * k] = t.x, v[4 * k + 1] = t.y, v[4 * k + 2] = t.z, v[4 * k + 3] = t.w;
+  }
+}
+
+// layer_collapse (network.hpp:440-455), one thread per output texel.
+__global__ void __launch_bounds__(128) layer_collapse32_kernel(
+    const float* __restrict__ V, int L2, int64_t PL, const float* __restrict__ w1,
+    const float* __restrict__ b1, const float* __restrict__ w2, const float* __restrict__ b2,
+    float* __restrict__ out) {
+  __shared__ __align__(16) float s_w1[2 * C * 2 * C];
+  __shared__ __align__(16) float s_w2[2 * C * C];
+  for (int e = threadIdx.x; e < 4 * C * C; e += blockDim.x) s_w1[e] = w1[e];
+  for (int e = threadIdx.x; e < 2 * C * C; e += blockDim.x) s_w2[e] = w2[e];
+  __syncthreads();
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)L2 * PL) return;
+  const int64_t l = t / PL, q = t % PL;
+  float a[C], b[C], r[C];
+  load_row(V + ((2 * l) * PL + q) * C, a);
+  load_row(V + ((2 * l + 1) * PL + q) * C, b);
+#pragma unroll
+  for (int c = 0; c < C; ++c) r[c] = 0.f;
+#pragma unroll 1
+  for (int j0 = 0; j0 < 2 * C; j0 += 8) {
+    float hc[8];
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) hc[jj] = 0.f;
+    // h[j] = sum_k cat[k] w1[k][j], k ascending over [a ; b]
+#pragma unroll
+    for (int k = 0; k < 2 * C; ++k) {
+      const float xk = k < C ? a[k] : b[k - C];
+      const float4 wa = *reinterpret_cast<const float4*>(s_w1 + k * 2 * C + j0);
+      const float4 wb = *reinterpret_cast<const float4*>(s_w1 + k * 2 * C + j0 + 4);
+      hc[0] = fmaf(xk, wa.x, hc[0]);
+      hc[1] = fmaf(xk, wa.y, hc[1]);
+      hc[2] = fmaf(xk, wa.z, hc[2]);
+      hc[3] = fmaf(xk, wa.w, hc[3]);
+      hc[4] = fmaf(xk, wb.x, hc[4]);
+      hc[5] = fmaf(xk, wb.y, hc[5]);
+      hc[6] = fmaf(xk, wb.z, hc[6]);
+      hc[7] = fmaf(xk, wb.w, hc[7]);
+    }
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const float hv = gelu_ref(fa(hc[jj], __ldg(b1 + j0 + jj)));
+      const float4* wr = reinterpret_cast<const float4*>(s_w2 + (j0 + jj) * C);
+#pragma unroll
+      for (int c4 = 0; c4 < C / 4; ++c4) {
+        const float4 w = wr[c4];
+        r[4 * c4] = fmaf(hv, w.x, r[4 * c4]);
+        r[4 * c4 + 1] = fmaf(hv, w.y, r[4 * c4 + 1]);
+        r[4 * c4 + 2] = fmaf(hv, w.z, r[4 * c4 + 2]);
+        r[4 * c4 + 3] = fmaf(hv, w.w, r[4 * c4 + 3]);
+      }
+    }
+  }
+  float4* o = reinterpret_cast<float4*>(out + t * C);
+#pragma unroll
+  for (int c4 = 0; c4 < C / 4; ++c4) {
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = 4 * c4 + k;
+      v[k] = fa(fm(fa(a[c], b[c]), 0.5f), fa(r[c], __ldg(b2 + c)));
+    }
+    o[c4] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
+// decode_blend_logits (network.hpp:539-549) for C = 32, M views.
+template <int M>
+__global__ void __launch_bounds__(128) blend_logits32_kernel(const float* __restrict__ V,
+                                                             const float* __restrict__ D, int64_t P,
+                                                             const float* __restrict__ bw,
+                                                             const float* __restrict__ gain,
+                                                             float* __restrict__ logits) {
+  __shared__ __align__(16) float s_bw[C * C];
+  for (int e = threadIdx.x; e < C * C; e += blockDim.x) s_bw[e] = bw[e];
+  __syncthreads();
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  float n[C], q[C];
+  load_row(V + p * C, n);
+  float ms = 0.f;
+#pragma unroll
+  for (int k = 0; k < C; ++k) ms = fmaf(n[k], n[k], ms);
+  const float r = __fdiv_rn(1.0f, __fsqrt_rn(fa(__fdiv_rn(ms, float(C)), 1e-6f)));
+#pragma unroll
+  for (int k = 0; k < C; ++k) n[k] = fm(fm(n[k], r), __ldg(gain + k));
+#pragma unroll
+  for (int c = 0; c < C; ++c) q[c] = 0.f;
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    const float nk = n[k];
+#pragma unroll
+    for (int c4 = 0; c4 < C / 4; ++c4) {
+      const float4 w = reinterpret_cast<const float4*>(s_bw + k * C)[c4];
+      q[4 * c4] = fmaf(nk, w.x, q[4 * c4]);
+      q[4 * c4 + 1] = fmaf(nk, w.y, q[4 * c4 + 1]);
+      q[4 * c4 + 2] = fmaf(nk, w.z, q[4 * c4 + 2]);
+      q[4 * c4 + 3] = fmaf(nk, w.w, q[4 * c4 + 3]);
+    }
+  }
+  const float inv_temp = __double2float_rn(1.0 / sqrt(double(C)));
+  const float* d = D + p * (int64_t)M * C;
+  float out[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const float4* dm4 = reinterpret_cast<const float4*>(d + m * C);
+    float acc = 0.f;
+#pragma unroll
+    for (int c4 = 0; c4 < C / 4; ++c4) {
+      const float4 t = __ldg(dm4 + c4);
+      acc = fmaf(q[4 * c4], t.x, acc);
+      acc = fmaf(q[4 * c4 + 1], t.y, acc);
+      acc = fmaf(q[4 * c4 + 2], t.z, acc);
+      acc = fmaf(q[4 * c4 + 3], t.w, acc);
+    }
+    out[m] = fm(acc, inv_temp);
+  }
+#pragma unroll
+  for (int m = 0; m < M; ++m) logits[p * M + m] = out[m];
+}
+
+// render_to_input_view decode for C = Ca = 32: payload [a(32), sigma],
+// activated depth and the world point, one thread per texel.
+__global__ void __launch_bounds__(128) decode_payload32_kernel(
+    const float* __restrict__ V, int L, int H, int W, const float* __restrict__ w_appear,
+    const float* __restrict__ w_sigma, const float* __restrict__ w_depth, DepthAct act,
+    DevRayCam rc, float* __restrict__ payload, float* __restrict__ depth,
+    float* __restrict__ points) {
+  constexpr int KW = C + 4;  // appear | sigma | depth | pad (16-byte rows)
+  __shared__ __align__(16) float s_w[C * KW];
+  for (int e = threadIdx.x; e < C * KW; e += blockDim.x) {
+    const int k = e / KW, c = e % KW;
+    s_w[e] = c < C ? w_appear[k * C + c] : (c == C ? w_sigma[k] : (c == C + 1 ? w_depth[k] : 0.f));
+  }
+  __syncthreads();
+  const int64_t P = (int64_t)L * H * W;
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  float v[C], acc[KW];
+  load_row(V + p * C, v);
+#pragma unroll
+  for (int c = 0; c < KW; ++c) acc[c] = 0.f;
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    const float vk = v[k];
+#pragma unroll
+    for (int c4 = 0; c4 < KW / 4; ++c4) {
+      const float4 w = reinterpret_cast<const float4*>(s_w + k * KW)[c4];
+      acc[4 * c4] = fmaf(vk, w.x, acc[4 * c4]);
+      acc[4 * c4 + 1] = fmaf(vk, w.y, acc[4 * c4 + 1]);
+      acc[4 * c4 + 2] = fmaf(vk, w.z, acc[4 * c4 + 2]);
+      acc[4 * c4 + 3] = fmaf(vk, w.w, acc[4 * c4 + 3]);
+    }
+  }
+  float* pay = payload + p * (C + 1);
+#pragma unroll
+  for (int c = 0; c < C + 1; ++c) pay[c] = sigmoid_ref(acc[c]);
+  const int l = int(p / ((int64_t)H * W));
+  const float d = activate_depth(acc[C + 1], l, act);
+  depth[p] = d;
+  const int j = int(p % W), i = int((p / W) % H);
+  float pt[3];
+  world_point(rc, i, j, d, pt);
+  points[p * 3 + 0] = pt[0];
+  points[p * 3 + 1] = pt[1];
+  points[p * 3 + 2] = pt[2];
+}
+
+inline int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
+
+}  // namespace
+
+bool layer_collapse32(const float* V, int L, int64_t PL, int C_, const float* w1, const float* b1,
+                      const float* w2, const float* b2, float* out, cudaStream_t st) {
+  if (C_ != C) return false;
+  const int L2 = L / 2;
+  layer_collapse32_kernel<<<blocks_for(L2 * PL, 128), 128, 0, st>>>(V, L2, PL, w1, b1, w2, b2, out);
+  return true;
+}
+
+bool blend_logits32(const float* V, const float* deltas, int64_t P, int C_, int M,
+                    const float* blend_w, const float* gain, float* logits, cudaStream_t st) {
+  if (C_ != C) return false;
+  const int g = blocks_for(P, 128);
+  switch (M) {
+    case 4: blend_logits32_kernel<4><<<g, 128, 0, st>>>(V, deltas, P, blend_w, gain, logits); return true;
+    case 8: blend_logits32_kernel<8><<<g, 128, 0, st>>>(V, deltas, P, blend_w, gain, logits); return true;
+    case 16: blend_logits32_kernel<16><<<g, 128, 0, st>>>(V, deltas, P, blend_w, gain, logits); return true;
+    default: return false;
+  }
+}
+
+bool decode_payload32(const float* V, int L, int H, int W, int C_, const float* w_appear, int Ca,
+                      const float* w_sigma, const float* w_depth, const DepthAct& act,
+                      const DevRayCam& rc, float* payload, float* depth, float* points,
+                      cudaStream_t st) {
+  if (C_ != C || Ca != C) return false;
+  const int64_t P = (int64_t)L * H * W;
+  decode_payload32_kernel<<<blocks_for(P, 128), 128, 0, st>>>(V, L, H, W, w_appear, w_sigma,
+                                                             w_depth, act, rc, payload, depth,
+                                                             points);
+  return true;
+}
+
+}  // namespace lvsg

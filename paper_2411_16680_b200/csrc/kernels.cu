@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(128) attend_kernel(float* V, const float* __re
 #pragma unroll
       for (int c = 0; c < C; ++c) s[c] = 0.f;
       const float* wh = s_wq + h * C * C;
-#pragma unroll 4
+#pragma unroll
       for (int k = 0; k < C; ++k) {
         const float nk = n[k];
 #pragma unroll
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(128) attend_kernel(float* V, const float* __re
       }
     }
     const float* wo_h = s_wo + h * C * C;
-#pragma unroll 4
+#pragma unroll
     for (int k = 0; k < C; ++k) {
       const float hk = hd[k];
 #pragma unroll
@@ -693,6 +693,9 @@ void decode_payload(const float* V, int L, int H, int W, int C, const float* w_a
                     const float* w_sigma, const float* w_depth, const DepthAct& act,
                     const DevRayCam& rc, float* payload, float* depth, float* points,
                     cudaStream_t st) {
+  if (decode_payload32(V, L, H, W, C, w_appear, Ca, w_sigma, w_depth, act, rc, payload, depth,
+                       points, st))
+    return;
   const int64_t P = (int64_t)L * H * W;
   decode_payload_kernel<<<blocks_for(P, 128), 128, C * (Ca + 2) * sizeof(float), st>>>(
       V, L, H, W, C, w_appear, Ca, w_sigma, w_depth, act, rc, payload, depth, points);
@@ -735,11 +738,13 @@ void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, c
 }
 void blend_logits(const float* V, const float* deltas, int64_t P, int C, int M,
                   const float* blend_w, const float* gain, float* logits, cudaStream_t st) {
+  if (blend_logits32(V, deltas, P, C, M, blend_w, gain, logits, st)) return;
   blend_logits_kernel<<<blocks_for(P, 128), 128, C * C * sizeof(float), st>>>(V, deltas, P, C, M,
                                                                               blend_w, gain, logits);
 }
 void layer_collapse(const float* V, int L, int64_t PL, int C, const float* w1, const float* b1,
                     const float* w2, const float* b2, float* out, cudaStream_t st) {
+  if (layer_collapse32(V, L, PL, C, w1, b1, w2, b2, out, st)) return;
   const int L2 = L / 2;
   layer_collapse_kernel<<<blocks_for(L2 * PL, 128), 128, 6 * C * C * sizeof(float), st>>>(
       V, L2, PL, C, w1, b1, w2, b2, out);

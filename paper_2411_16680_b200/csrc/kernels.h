@@ -108,6 +108,15 @@ void blend_logits(const float* V, const float* deltas, int64_t P, int C, int M,
 // layer_collapse (network.hpp:440-455): V [L,H,W,C] -> out [L/2,H,W,C].
 void layer_collapse(const float* V, int L, int64_t PL, int C, const float* w1, const float* b1,
                     const float* w2, const float* b2, float* out, cudaStream_t st);
+// C = 32 specialisations (fast32.cu); return false when the shape differs.
+bool layer_collapse32(const float* V, int L, int64_t PL, int C, const float* w1, const float* b1,
+                      const float* w2, const float* b2, float* out, cudaStream_t st);
+bool blend_logits32(const float* V, const float* deltas, int64_t P, int C, int M,
+                    const float* blend_w, const float* gain, float* logits, cudaStream_t st);
+bool decode_payload32(const float* V, int L, int H, int W, int C, const float* w_appear, int Ca,
+                      const float* w_sigma, const float* w_depth, const DepthAct& act,
+                      const DevRayCam& rc, float* payload, float* depth, float* points,
+                      cudaStream_t st);
 // out[p] = V[p,:] . w (decode_linear with K = 1), optionally activated depth.
 void decode_scalar(const float* V, int64_t P, int C, const float* w, float* out, int L,
                    int64_t PL, const DepthAct* act, cudaStream_t st);
