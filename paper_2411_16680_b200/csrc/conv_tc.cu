@@ -33,7 +33,8 @@ constexpr int HALO_BYTES = NCH * LBO_A;         // one plane (hi or lo)
 constexpr int W_ROWS = 64;                      // 32 hi + 32 lo
 constexpr int W_BYTES = 9 * NCH * W_ROWS * 16;  // 73728
 constexpr int SMEM_BYTES = W_BYTES + 4 * HALO_BYTES + 64;
-constexpr int NT = 128;
+constexpr int NWORK = 256;        // staging / epilogue threads (8 warps)
+constexpr int NT = NWORK + 32;     // + one MMA-issuer warp
 constexpr uint32_t TMEM_COLS = 128;  // two 64-column accumulators
 
 struct TileCoord {
@@ -58,12 +59,12 @@ __device__ __forceinline__ void stage_halo(const ConvArgs& a, const TileCoord& t
   const long long HW = (long long)a.H * a.W;
   // all global loads of this thread first (memory-level parallelism), then
   // the tf32 split and the shared-memory stores
-  constexpr int PER = (HALO_PX * NCH + NT - 1) / NT;
+  constexpr int PER = (HALO_PX * NCH + NWORK - 1) / NWORK;
   float4 vals[PER];
   float rs[PER];
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
-    const int e = threadIdx.x + k * NT;
+    const int e = threadIdx.x + k * NWORK;
     vals[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     rs[k] = 1.f;
     if (e < HALO_PX * NCH) {
@@ -79,7 +80,7 @@ __device__ __forceinline__ void stage_halo(const ConvArgs& a, const TileCoord& t
   }
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
-    const int e = threadIdx.x + k * NT;
+    const int e = threadIdx.x + k * NWORK;
     if (e >= HALO_PX * NCH) break;
     const int px = e >> 3, j = e & 7;
     float4 v = vals[k];
@@ -102,46 +103,49 @@ __device__ __forceinline__ void stage_halo(const ConvArgs& a, const TileCoord& t
   }
 }
 
-__device__ __forceinline__ void issue_tile(uint32_t hi_addr, uint32_t lo_addr, uint32_t w_addr,
-                                           uint32_t tmem_acc, uint64_t* bar) {
+// MMA issue for one tile: 9 taps x 4 K-steps x {N=64 hi, N=32 lo}. Every
+// descriptor is a base descriptor plus a compile-time start-address offset.
+__device__ __forceinline__ void issue_tile(uint64_t ah0, uint64_t al0, uint64_t b0,
+                                           uint32_t tmem_acc) {
   constexpr uint32_t id64 = tc::idesc_tf32(128, 64);
   constexpr uint32_t id32 = tc::idesc_tf32(128, 32);
-#pragma unroll 1
+#pragma unroll
   for (int tap = 0; tap < 9; ++tap) {
     const int dy = tap / 3, dx = tap % 3;
-    const uint32_t toff = uint32_t((dy * HWD + dx) * 16);
 #pragma unroll
     for (int s = 0; s < NCH / 2; ++s) {
-      const uint64_t ah = tc::smem_desc(hi_addr + 2 * s * LBO_A + toff, LBO_A, HWD * 16);
-      const uint64_t al = tc::smem_desc(lo_addr + 2 * s * LBO_A + toff, LBO_A, HWD * 16);
-      const uint64_t bd = tc::smem_desc(w_addr + (tap * NCH + 2 * s) * W_ROWS * 16, W_ROWS * 16, 128);
-      tc::mma_tf32(tmem_acc, ah, bd, id64, (tap | s) != 0);
-      tc::mma_tf32(tmem_acc + 32, al, bd, id32, 1u);
+      const uint64_t aoff = uint64_t((2 * s * LBO_A + (dy * HWD + dx) * 16) >> 4);
+      const uint64_t boff = uint64_t(((tap * NCH + 2 * s) * W_ROWS * 16) >> 4);
+      tc::mma_tf32(tmem_acc, ah0 + aoff, b0 + boff, id64, (tap | s) != 0);
+      tc::mma_tf32(tmem_acc + 32, al0 + aoff, b0 + boff, id32, 1u);
     }
   }
-  tc::commit(bar);
 }
 
-__device__ __forceinline__ void epilogue(const ConvArgs& a, const TileCoord& t, uint32_t tmem_acc) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row = warp * 32 + lane;
+// Worker warp w: TMEM lanes 32*(w%4).. (tile rows), accumulator columns
+// 16*(w/4).. of both halves.
+__device__ __forceinline__ void epilogue(const ConvArgs& a, const TileCoord& t, uint32_t tmem_acc,
+                                         int warp, int lane) {
+  const int q = warp & 3, h = warp >> 2;
+  const int row = q * 32 + lane;
   const int y = t.y0 + (row >> 3), x = t.x0 + (row & 7);
-  const uint32_t taddr = tmem_acc + (uint32_t(warp * 32) << 16);
-  float d0[32], d1[32];
-  tc::tmem_ld32(taddr, d0);
-  tc::tmem_ld32(taddr + 32, d1);
+  const uint32_t taddr = tmem_acc + (uint32_t(q * 32) << 16) + uint32_t(h * 16);
+  float d0[16], d1[16];
+  tc::tmem_ld16(taddr, d0);
+  tc::tmem_ld16(taddr + 32, d1);
   if (y >= a.H || x >= a.W) return;
   const long long pix = (long long)y * a.W + x;
-  float* o = a.out + (long long)t.b * a.out_bstride + pix * a.out_pstride;
-  const float* rs = a.resid ? a.resid + (long long)t.b * a.res_bstride + pix * a.res_pstride : nullptr;
+  float* o = a.out + (long long)t.b * a.out_bstride + pix * a.out_pstride + h * 16;
+  const float* rs =
+      a.resid ? a.resid + (long long)t.b * a.res_bstride + pix * a.res_pstride + h * 16 : nullptr;
 #pragma unroll
-  for (int c4 = 0; c4 < 8; ++c4) {
+  for (int c4 = 0; c4 < 4; ++c4) {
     float v[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int c = 4 * c4 + k;
       float y_ = fa(d0[c], d1[c]);
-      if (a.bias) y_ = fa(y_, __ldg(a.bias + c));
+      if (a.bias) y_ = fa(y_, __ldg(a.bias + h * 16 + c));
       if (a.gelu) y_ = gelu_ref(y_);
       v[k] = y_;
     }
@@ -156,6 +160,9 @@ __device__ __forceinline__ void epilogue(const ConvArgs& a, const TileCoord& t, 
   }
 }
 
+// Warp-specialised persistent CTA: warps 0..7 stage halos and run
+// epilogues, warp 8 issues the MMAs. mbarriers: halo_full[b] (256 worker
+// arrivals), mma_done[b] (tcgen05.commit), acc_empty[b] (256 arrivals).
 __global__ void __launch_bounds__(NT, 1) conv3x3_tc_kernel(const ConvArgs a, int num_tiles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   float* w_s = reinterpret_cast<float*>(smem);
@@ -164,11 +171,13 @@ __global__ void __launch_bounds__(NT, 1) conv3x3_tc_kernel(const ConvArgs a, int
   halo[0][1] = reinterpret_cast<float*>(smem + W_BYTES + HALO_BYTES);
   halo[1][0] = reinterpret_cast<float*>(smem + W_BYTES + 2 * HALO_BYTES);
   halo[1][1] = reinterpret_cast<float*>(smem + W_BYTES + 3 * HALO_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + W_BYTES + 4 * HALO_BYTES);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  uint64_t* halo_full = reinterpret_cast<uint64_t*>(smem + W_BYTES + 4 * HALO_BYTES);
+  uint64_t* mma_done = halo_full + 2;
+  uint64_t* acc_empty = halo_full + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(halo_full + 6);
 
   if (blockIdx.x >= num_tiles) return;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // weights: [tap][chunk j][row n][4], rows 0..31 = tf32 hi, 32..63 = lo
   for (int e = tid; e < 9 * NCH * W_ROWS * 4; e += NT) {
@@ -179,44 +188,68 @@ __global__ void __launch_bounds__(NT, 1) conv3x3_tc_kernel(const ConvArgs a, int
     tc::split_tf32(__ldg(a.w + (co * 32 + ci) * 9 + tap), h, l);
     w_s[e] = n < 32 ? h : l;
   }
+  tc::fence_proxy_async();
   if (tid == 0) {
-    tc::mbar_init(&bars[0], 1);
-    tc::mbar_init(&bars[1], 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&halo_full[b], NWORK);
+      tc::mbar_init(&mma_done[b], 1);
+      tc::mbar_init(&acc_empty[b], NWORK);
+    }
     tc::mbar_init_fence();
   }
-  if ((tid >> 5) == 0) tc::tmem_alloc(tmem_slot, TMEM_COLS);
-
-  int t = blockIdx.x;
-  stage_halo(a, tile_coord(t, a.H, a.W), halo[0][0], halo[0][1]);
-  tc::fence_proxy_async();
+  if (warp == 0) tc::tmem_alloc(tmem_slot, TMEM_COLS);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t w_addr = tc::smem_u32(w_s);
-  uint32_t phase[2] = {0u, 0u};
-  if (tid == 0)
-    issue_tile(tc::smem_u32(halo[0][0]), tc::smem_u32(halo[0][1]), w_addr, tmem, &bars[0]);
 
-  for (int it = 0; t < num_tiles; ++it, t += gridDim.x) {
-    const int b = it & 1;
-    const int tn = t + gridDim.x;
-    if (tn < num_tiles) {
-      stage_halo(a, tile_coord(tn, a.H, a.W), halo[b ^ 1][0], halo[b ^ 1][1]);
-      tc::fence_proxy_async();
+  if (warp == NWORK / 32) {
+    // ---- MMA issuer (one thread) ----
+    if (lane == 0) {
+      const uint64_t b0 = tc::smem_desc(tc::smem_u32(w_s), W_ROWS * 16, 128);
+      const uint64_t ah0 = tc::smem_desc(tc::smem_u32(halo[0][0]), LBO_A, HWD * 16);
+      const uint64_t al0 = tc::smem_desc(tc::smem_u32(halo[0][1]), LBO_A, HWD * 16);
+      const uint64_t ah1 = tc::smem_desc(tc::smem_u32(halo[1][0]), LBO_A, HWD * 16);
+      const uint64_t al1 = tc::smem_desc(tc::smem_u32(halo[1][1]), LBO_A, HWD * 16);
+      int i = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
+        const int b = i & 1;
+        tc::mbar_wait(&halo_full[b], uint32_t((i >> 1) & 1));
+        if (i >= 2) tc::mbar_wait(&acc_empty[b], uint32_t(((i - 2) >> 1) & 1));
+        tc::fence_after();
+        issue_tile(b ? ah1 : ah0, b ? al1 : al0, b0, tmem + uint32_t(b * 64));
+        tc::commit(&mma_done[b]);
+      }
     }
-    tc::mbar_wait(&bars[b], phase[b]);
-    phase[b] ^= 1u;
-    tc::fence_after();
-    __syncthreads();  // next halo staged by every thread; tile t's MMAs done
-    if (tn < num_tiles && tid == 0)
-      issue_tile(tc::smem_u32(halo[b ^ 1][0]), tc::smem_u32(halo[b ^ 1][1]), w_addr,
-                 tmem + uint32_t((b ^ 1) * 64), &bars[b ^ 1]);
-    epilogue(a, tile_coord(t, a.H, a.W), tmem + uint32_t(b * 64));
-    tc::fence_before();
-    __syncthreads();  // accumulator b drained before it is reused
+  } else {
+    // ---- workers: stage tile i, then drain tile i-1 ----
+    int i = 0;
+    int tprev = -1;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
+      const int b = i & 1;
+      stage_halo(a, tile_coord(t, a.H, a.W), halo[b][0], halo[b][1]);
+      tc::fence_proxy_async();
+      tc::mbar_arrive(&halo_full[b]);
+      if (tprev >= 0) {
+        const int pb = (i - 1) & 1;
+        tc::mbar_wait(&mma_done[pb], uint32_t(((i - 1) >> 1) & 1));
+        tc::fence_after();
+        epilogue(a, tile_coord(tprev, a.H, a.W), tmem + uint32_t(pb * 64), warp, lane);
+        tc::fence_before();
+        tc::mbar_arrive(&acc_empty[pb]);
+      }
+      tprev = t;
+    }
+    if (tprev >= 0) {
+      const int pb = (i - 1) & 1;
+      tc::mbar_wait(&mma_done[pb], uint32_t(((i - 1) >> 1) & 1));
+      tc::fence_after();
+      epilogue(a, tile_coord(tprev, a.H, a.W), tmem + uint32_t(pb * 64), warp, lane);
+    }
   }
-  if ((tid >> 5) == 0) tc::tmem_dealloc(tmem, TMEM_COLS);
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, TMEM_COLS);
 }
 
 }  // namespace
