@@ -118,15 +118,15 @@ __global__ void __launch_bounds__(128) blend_logits32_kernel(const float* __rest
     }
   }
   const float inv_temp = __double2float_rn(1.0 / sqrt(double(C)));
-  const float* d = D + p * (int64_t)M * C;
+  const float4* d4 = reinterpret_cast<const float4*>(D) + p;  // Δ[m][g][p][4]
   float out[M];
 #pragma unroll
   for (int m = 0; m < M; ++m) {
-    const float4* dm4 = reinterpret_cast<const float4*>(d + m * C);
+    const float4* dm4 = d4 + (int64_t)m * (C / 4) * P;
     float acc = 0.f;
 #pragma unroll
     for (int c4 = 0; c4 < C / 4; ++c4) {
-      const float4 t = __ldg(dm4 + c4);
+      const float4 t = __ldg(dm4 + c4 * P);
       acc = fmaf(q[4 * c4], t.x, acc);
       acc = fmaf(q[4 * c4 + 1], t.y, acc);
       acc = fmaf(q[4 * c4 + 2], t.z, acc);

@@ -170,34 +170,30 @@ __global__ void ray_project_kernel(const float* base, int M, int hK, int wK, int
 // Stage 1: reprojection + bilinear feature gather
 // ----------------------------------------------------------------------------
 
-// One thread per (texel, view, 4-channel group). The world point and the
-// footprint are recomputed per group (f64, bit-exact order); the four taps
-// are read as float4 (HWC, 16-byte aligned when C % 4 == 0).
+// One thread per (texel, view); consecutive threads = consecutive texels of
+// one view. The world point and footprint are computed once (f64, bit-exact
+// order); the 4 taps are read as whole channel rows and the result is written
+// in the view-major SoA layout Δ[m][g][p][4] (g = channel group of 4), so the
+// stores here and every Stage-2 read of Δ are fully coalesced.
 template <bool kVec4>
 __global__ void gather_stack_kernel(const float* __restrict__ feats, int M, int Hf, int Wf, int C,
                                     const DevCam* __restrict__ cams, DevRayCam rc,
                                     const float* __restrict__ depth, int L, int H, int W,
                                     float* __restrict__ deltas) {
-  const int G = kVec4 ? C / 4 : C;
-  const int64_t total = (int64_t)L * H * W * M * G;
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= total) return;
-  const int g = int(i % G);
-  int64_t t = i / G;
-  const int m = int(t % M);
-  const int64_t p = t / M;
+  const int64_t P = (int64_t)L * H * W;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= P * M) return;
+  const int m = int(i / P);
+  const int64_t p = i - m * P;
+  const int G = (C + 3) / 4;
   const int j = int(p % W);
   const int ii = int((p / W) % H);
   float pt[3];
   world_point(rc, ii, j, __ldg(depth + p), pt);
-  const DevCam cam = cams[m];
-  const Footprint f = project_footprint(cam, pt);
-  float* o = deltas + (p * M + m) * C;
+  const Footprint f = project_footprint(cams[m], pt);
+  float4* o = reinterpret_cast<float4*>(deltas) + (int64_t)m * G * P + p;
   if (!f.valid) {
-    if (kVec4)
-      reinterpret_cast<float4*>(o)[g] = make_float4(0.f, 0.f, 0.f, 0.f);
-    else
-      o[g] = 0.f;
+    for (int g = 0; g < G; ++g) o[g * P] = make_float4(0.f, 0.f, 0.f, 0.f);
     return;
   }
   double w[4];
@@ -208,15 +204,23 @@ __global__ void gather_stack_kernel(const float* __restrict__ feats, int M, int 
   const float* i01 = img + ((int64_t)f.y1 * Wf + f.x0) * C;
   const float* i11 = img + ((int64_t)f.y1 * Wf + f.x1) * C;
   if (kVec4) {
-    const float4 a = __ldg(reinterpret_cast<const float4*>(i00) + g);
-    const float4 b = __ldg(reinterpret_cast<const float4*>(i10) + g);
-    const float4 c = __ldg(reinterpret_cast<const float4*>(i01) + g);
-    const float4 d = __ldg(reinterpret_cast<const float4*>(i11) + g);
-    reinterpret_cast<float4*>(o)[g] =
-        make_float4(blend4(w, a.x, b.x, c.x, d.x), blend4(w, a.y, b.y, c.y, d.y),
-                    blend4(w, a.z, b.z, c.z, d.z), blend4(w, a.w, b.w, c.w, d.w));
+    for (int g = 0; g < G; ++g) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(i00) + g);
+      const float4 b = __ldg(reinterpret_cast<const float4*>(i10) + g);
+      const float4 c = __ldg(reinterpret_cast<const float4*>(i01) + g);
+      const float4 d = __ldg(reinterpret_cast<const float4*>(i11) + g);
+      o[g * P] = make_float4(blend4(w, a.x, b.x, c.x, d.x), blend4(w, a.y, b.y, c.y, d.y),
+                             blend4(w, a.z, b.z, c.z, d.z), blend4(w, a.w, b.w, c.w, d.w));
+    }
   } else {
-    o[g] = blend4(w, __ldg(i00 + g), __ldg(i10 + g), __ldg(i01 + g), __ldg(i11 + g));
+    for (int g = 0; g < G; ++g) {
+      float v[4];
+      for (int k = 0; k < 4; ++k) {
+        const int c = 4 * g + k;
+        v[k] = c < C ? blend4(w, __ldg(i00 + c), __ldg(i10 + c), __ldg(i01 + c), __ldg(i11 + c)) : 0.f;
+      }
+      o[g * P] = make_float4(v[0], v[1], v[2], v[3]);
+    }
   }
 }
 
@@ -356,7 +360,7 @@ __global__ void __launch_bounds__(128) attend_kernel(float* V, const float* __re
     for (int k = 0; k < C; ++k) n[k] = fm(fm(n[k], r), __ldg(gain + k));
   }
   const float inv_temp = __double2float_rn(1.0 / sqrt(double(C)));
-  const float* d = D + p * (int64_t)M * C;
+  const float4* d4 = reinterpret_cast<const float4*>(D) + p;  // Δ[m][g][p][4]
   float out[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) out[c] = 0.f;
@@ -386,11 +390,11 @@ __global__ void __launch_bounds__(128) attend_kernel(float* V, const float* __re
       float mx = -FLT_MAX;
 #pragma unroll
       for (int m = 0; m < M; ++m) {
-        const float4* dm4 = reinterpret_cast<const float4*>(d + m * C);
+        const float4* dm4 = d4 + (int64_t)m * (C / 4) * P;
         float acc = 0.f;
 #pragma unroll
         for (int c4 = 0; c4 < C / 4; ++c4) {
-          const float4 t = __ldg(dm4 + c4);
+          const float4 t = __ldg(dm4 + c4 * P);
           acc = fmaf(s[4 * c4], t.x, acc);
           acc = fmaf(s[4 * c4 + 1], t.y, acc);
           acc = fmaf(s[4 * c4 + 2], t.z, acc);
@@ -414,11 +418,11 @@ __global__ void __launch_bounds__(128) attend_kernel(float* V, const float* __re
     for (int c = 0; c < C; ++c) hd[c] = 0.f;
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      const float4* dm4 = reinterpret_cast<const float4*>(d + m * C);
+      const float4* dm4 = d4 + (int64_t)m * (C / 4) * P;
       const float wm = w[m];
 #pragma unroll
       for (int c4 = 0; c4 < C / 4; ++c4) {
-        const float4 t = __ldg(dm4 + c4);
+        const float4 t = __ldg(dm4 + c4 * P);
         hd[4 * c4] = fmaf(wm, t.x, hd[4 * c4]);
         hd[4 * c4 + 1] = fmaf(wm, t.y, hd[4 * c4 + 1]);
         hd[4 * c4 + 2] = fmaf(wm, t.z, hd[4 * c4 + 2]);
@@ -468,7 +472,6 @@ __global__ void attend_generic_kernel(float* V, const float* __restrict__ D, int
   const float r = __fdiv_rn(1.0f, __fsqrt_rn(fa(__fdiv_rn(ms, float(C)), 1e-6f)));
   for (int k = 0; k < C; ++k) n[k] = fm(fm(v[k], r), gain[k]), out[k] = 0.f;
   const float inv_temp = __double2float_rn(1.0 / sqrt(double(C)));
-  const float* d = D + p * (int64_t)M * C;
   float w[kMaxM];
   for (int h = 0; h < heads; ++h) {
     if (zero_scores) {
@@ -482,7 +485,7 @@ __global__ void attend_generic_kernel(float* V, const float* __restrict__ D, int
       float mx = 0.f;
       for (int m = 0; m < M; ++m) {
         float acc = 0.f;
-        for (int c = 0; c < C; ++c) acc = fmaf(s[c], d[m * C + c], acc);
+        for (int c = 0; c < C; ++c) acc = fmaf(s[c], D[((int64_t)(m * ((C + 3) / 4) + c / 4) * P + p) * 4 + (c & 3)], acc);
         w[m] = fm(acc, inv_temp);
         mx = m == 0 ? w[m] : fmaxf(mx, w[m]);
       }
@@ -493,7 +496,7 @@ __global__ void attend_generic_kernel(float* V, const float* __restrict__ D, int
     }
     for (int c = 0; c < C; ++c) {
       float acc = 0.f;
-      for (int m = 0; m < M; ++m) acc = fmaf(w[m], d[m * C + c], acc);
+      for (int m = 0; m < M; ++m) acc = fmaf(w[m], D[((int64_t)(m * ((C + 3) / 4) + c / 4) * P + p) * 4 + (c & 3)], acc);
       hd[c] = acc;
     }
     for (int c = 0; c < C; ++c) {
@@ -525,10 +528,9 @@ __global__ void blend_logits_kernel(const float* __restrict__ V, const float* __
     for (int k = 0; k < C; ++k) acc = fmaf(fm(fm(v[k], r), gain[k]), s_bw[k * C + c], acc);
     q[c] = acc;
   }
-  const float* d = D + p * (int64_t)M * C;
   for (int m = 0; m < M; ++m) {
     float acc = 0.f;
-    for (int c = 0; c < Cq; ++c) acc = fmaf(q[c], d[m * C + c], acc);
+    for (int c = 0; c < Cq; ++c) acc = fmaf(q[c], D[((int64_t)(m * ((C + 3) / 4) + c / 4) * P + p) * 4 + (c & 3)], acc);
     logits[p * M + m] = fm(acc, inv_temp);
   }
 }
@@ -681,7 +683,7 @@ void gather_stack(const float* feats, int M, int Hf, int Wf, int C, const DevCam
                   const DevRayCam& rc, const float* depth, int L, int H, int W, float* deltas,
                   cudaStream_t st) {
   const bool v4 = C % 4 == 0;
-  const int64_t n = (int64_t)L * H * W * M * (v4 ? C / 4 : C);
+  const int64_t n = (int64_t)L * H * W * M;
   if (v4)
     gather_stack_kernel<true><<<blocks_for(n, 256), 256, 0, st>>>(feats, M, Hf, Wf, C, cams_dev, rc,
                                                                   depth, L, H, W, deltas);

@@ -312,7 +312,8 @@ void ensure_plan(lvsg_ctx* c, int64_t He, int64_t We) {
     maxV = std::max({maxV, size_t(sp.in_layers * sp.in_height * sp.in_width),
                      size_t(sp.layers * sp.height * sp.width)});
     maxIn = std::max(maxIn, size_t(sp.layers * sp.in_height * sp.in_width));
-    maxD = std::max(maxD, size_t(sp.layers * sp.height * sp.width * M * C));
+    // Δ in the view-major SoA layout [M][ceil(C/4)][P][4]
+    maxD = std::max(maxD, size_t(sp.layers * sp.height * sp.width * M * ((C + 3) / 4) * 4));
     maxU = std::max(maxU, size_t(M * sp.feat_h * sp.feat_w));
     maxAcc = std::max(maxAcc, size_t(M * sp.layers * sp.render_h * sp.render_w * (Ca + 2)));
     maxFb = std::max(maxFb, size_t(M * sp.render_h * sp.render_w * (Ca + 1)));
