@@ -2,6 +2,7 @@
 // reprojection gather, the render-to-input-view splat, and the per-texel
 // One-to-many attention / blend-logit / layer-collapse MLPs.
 #include <cfloat>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -718,6 +719,11 @@ void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, c
             const float* const* wq_heads, const float* wo, const float* gain, int zero_scores,
             cudaStream_t st) {
   (void)wq_heads;
+  static const bool simt = [] {
+    const char* e = getenv("LVSG_ATTN");
+    return e && e[0] == 's';  // LVSG_ATTN=simt forces the SIMT kernel
+  }();
+  if (!simt && attend_tc(V, deltas, P, C, M, heads, wq, wo, gain, zero_scores, st)) return;
   const size_t smem = 2 * size_t(heads) * C * C * sizeof(float);
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

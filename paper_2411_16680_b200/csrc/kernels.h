@@ -102,6 +102,10 @@ void splat_composite(const float* acc, int M, int L, int Hv, int Wv, int K, floa
 void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
             const float* const* wq_heads, const float* wo, const float* gain, int zero_scores,
             cudaStream_t st);
+// tcgen05 3xTF32 fused attention (attn_tc.cu): C = 32, h in {1,2,4},
+// M in {4,8,16}; returns false otherwise.
+bool attend_tc(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
+               const float* wo, const float* gain, int zero_scores, cudaStream_t st);
 // logits [P, M] = <rms_norm(V,g) W_blend, Δ_m> / sqrt(C) (network.hpp:539-549).
 void blend_logits(const float* V, const float* deltas, int64_t P, int C, int M,
                   const float* blend_w, const float* gain, float* logits, cudaStream_t st);
