@@ -131,14 +131,18 @@ __global__ void __launch_bounds__(NT) conv3x3_kernel(const ConvArgs a) {
 
 }  // namespace
 
-void conv3x3(const ConvArgs& a, cudaStream_t st, int impl) {
+bool conv3x3_uses_tc(const ConvArgs& a, int impl) {
   static const int env = [] {
     const char* e = getenv("LVSG_CONV");
     return e && e[0] == 's' ? 1 : 0;  // LVSG_CONV=simt forces the SIMT kernel
   }();
   if (impl == 0) impl = env ? 1 : 2;
-  if (impl == 2 && conv3x3_tc_supported(a))
-    conv3x3_tc(a, st);
+  return impl == 2 && conv3x3_tc_supported(a);
+}
+
+void conv3x3(const ConvArgs& a, cudaStream_t st, int impl) {
+  if (conv3x3_uses_tc(a, impl))
+    conv3x3_tc(a, st);  // computes the rms-norm input scale itself
   else
     conv3x3_simt(a, st);
 }

@@ -42,6 +42,7 @@ struct ConvArgs {
 // 1 SIMT, 2 tcgen05 (unsupported shapes fall back to SIMT).
 void conv3x3(const ConvArgs& a, cudaStream_t st, int impl = 0);
 void conv3x3_simt(const ConvArgs& a, cudaStream_t st);
+bool conv3x3_uses_tc(const ConvArgs& a, int impl = 0);
 bool conv3x3_tc_supported(const ConvArgs& a);
 void conv3x3_tc(const ConvArgs& a, cudaStream_t st);
 

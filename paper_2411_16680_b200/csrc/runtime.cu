@@ -423,13 +423,15 @@ void fusion(lvsg_ctx* c, float* V, int64_t L, int64_t H, int64_t W, const Fusion
   mark(c, "attention", 1);
   for (const MlpW& m : f.mlps) {
     // conv_mlp_residual (attention.hpp:262-267), batched over layers
-    rms_rinv(V, c->rinv.p, P, C, c->stream);
-    mark(c, "misc", 1);
     ConvArgs a = conv_args(int(L), int(H), int(W), C, C, m.w1, m.b1, c->t1.p);
     add_src(a, V, C, int(H), int(W));
     a.rinv = c->rinv.p;
     a.gain = m.gain;
     a.gelu = 1;
+    if (!conv3x3_uses_tc(a)) {  // the tcgen05 conv normalises its own halo
+      rms_rinv(V, c->rinv.p, P, C, c->stream);
+      mark(c, "misc", 1);
+    }
     conv3x3(a, c->stream);
     ConvArgs b = conv_args(int(L), int(H), int(W), C, C, m.w2, m.b2, V);
     add_src(b, c->t1.p, C, int(H), int(W));
