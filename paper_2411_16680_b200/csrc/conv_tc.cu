@@ -5,22 +5,21 @@
 //
 // Tile = 16 rows x 8 columns of output pixels (M = 128 GEMM rows, row
 // m = 8g + i <-> pixel (y0+g, x0+i)), N = 32 output channels, K = 9 taps x 32
-// input channels. The 18 x 10 x 32 input halo arrives by TMA as eight
-// 4-channel planes ([18][10][4] floats each) -- exactly the K-major
-// "interleave" operand layout with core-matrix groups SBO = 160 B apart (one
-// halo row), so each tap (dy, dx) is the same descriptor with its start
-// address moved by (10*dy + dx) * 16 bytes: im2col costs nothing. Converter
-// warps round the planes to tf32 in place (hi) and write the residual planes
-// (lo); the optional conv-MLP rms-norm is applied there from the 32 channels
-// already in shared memory. Weights [Wh ; Wl] (N = 64) stay resident. Per K
+// input channels. The 18 x 10 x 32 input halo arrives as one TMA box; converter
+// warps rewrite it as eight 4-channel planes of tf32 hi and lo ([18][10][4]
+// floats each) -- the K-major "interleave" operand layout with core-matrix
+// groups SBO = 160 B apart (one halo row), so each tap (dy, dx) is the same
+// descriptor with its start address moved by (10*dy + dx) * 16 bytes: im2col
+// costs nothing. The optional conv-MLP rms-norm is applied in the converter
+// from the 32 channels already in shared memory. Weights [Wh ; Wl] (N = 64) stay resident. Per K
 // step (8 channels of one tap):
 //     MMA1  N=64: D[:, 0:64]  += Xh * [Wh ; Wl]^T
 //     MMA2  N=32: D[:, 32:64] += Xl * Wh^T
 // and the epilogue sums D[:, c] + D[:, 32+c].
 //
 // Warp roles of the persistent CTA (1 per SM): w0 TMA producer, w1 MMA issuer
-// (+ TMEM owner), w2-5 converters, w6-9 epilogue; a 3-stage halo ring and two
-// TMEM accumulators, all hand-offs through mbarriers.
+// (+ TMEM owner), w2-5 converters, w6-9 epilogue; two raw TMA stages, two
+// hi/lo plane buffers and two TMEM accumulators, hand-offs through mbarriers.
 // Semantics of kernels_ref.hpp:72-96 (zero padding) with the bias / GELU /
 // residual / rms-norm-input options of ConvArgs.
 #include <cuda.h>
@@ -38,17 +37,17 @@ constexpr int TW = 8, TH = 16;
 constexpr int HWD = TW + 2, HHT = TH + 2;       // 10 x 18 halo
 constexpr int HALO_PX = HWD * HHT;              // 180
 constexpr int NCH = 8;                          // 4-channel planes (Cin = 32)
-constexpr int LBO_A = 2944;                     // plane stride: >= 180*16, 128-B aligned (TMA)
-constexpr int PLANE_BYTES = HALO_PX * 16;       // 2880 written by one TMA box
-constexpr int HALF_BYTES = NCH * LBO_A;         // hi (or lo) half of a stage
-constexpr int STAGE_BYTES = 2 * HALF_BYTES;
-constexpr int NS = 3;                           // halo ring depth
+constexpr int RAW_BYTES = HALO_PX * 32 * 4;     // one TMA box [18][10][32] (23040)
+constexpr int LBO_A = HALO_PX * 16 + 16;        // plane stride (padded: conflict-free stores)
+constexpr int HALF_BYTES = NCH * LBO_A;         // hi (or lo) planes of one buffer
+constexpr int PLANES_BYTES = 2 * HALF_BYTES;
 constexpr int W_ROWS = 64;                      // 32 hi + 32 lo
 constexpr int W_BYTES = 9 * NCH * W_ROWS * 16;  // 73728
-constexpr int OFF_STAGE = W_BYTES;
-constexpr int OFF_RMS = OFF_STAGE + NS * STAGE_BYTES;
+constexpr int OFF_RAW = W_BYTES;                // 2 raw TMA stages
+constexpr int OFF_PLANES = OFF_RAW + 2 * RAW_BYTES;
+constexpr int OFF_RMS = OFF_PLANES + 2 * PLANES_BYTES;
 constexpr int OFF_BAR = OFF_RMS + 192 * 4;
-constexpr int NBAR = 3 * NS + 4;
+constexpr int NBAR = 12;
 constexpr int SMEM_BYTES = OFF_BAR + NBAR * 8 + 16;
 constexpr int NT = 320;  // 10 warps
 constexpr uint32_t TMEM_COLS = 128;
@@ -111,11 +110,12 @@ __global__ void __launch_bounds__(NT, 1)
   float* w_s = reinterpret_cast<float*>(smem);
   float* rms_s = reinterpret_cast<float*>(smem + OFF_RMS);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* tma_full = bars;                // [NS] tx bytes of the TMA boxes
-  uint64_t* conv_full = bars + NS;          // [NS] converters done (hi/lo ready)
-  uint64_t* halo_empty = bars + 2 * NS;     // [NS] MMAs done reading the stage
-  uint64_t* mma_done = bars + 3 * NS;       // [2]
-  uint64_t* acc_empty = bars + 3 * NS + 2;  // [2]
+  uint64_t* raw_full = bars;          // [2] TMA bytes landed
+  uint64_t* raw_empty = bars + 2;      // [2] converters done reading raw
+  uint64_t* conv_full = bars + 4;      // [2] hi/lo planes ready
+  uint64_t* planes_empty = bars + 6;   // [2] MMAs done reading the planes
+  uint64_t* mma_done = bars + 8;       // [2] accumulator ready
+  uint64_t* acc_empty = bars + 10;     // [2] accumulator drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
 
   if (blockIdx.x >= num_tiles) return;
@@ -132,12 +132,11 @@ __global__ void __launch_bounds__(NT, 1)
   }
   tc::fence_proxy_async();
   if (tid == 0) {
-    for (int s = 0; s < NS; ++s) {
-      tc::mbar_init(&tma_full[s], 1);
-      tc::mbar_init(&conv_full[s], NCONV);
-      tc::mbar_init(&halo_empty[s], 1);
-    }
     for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&raw_full[b], 1);
+      tc::mbar_init(&raw_empty[b], NCONV);
+      tc::mbar_init(&conv_full[b], NCONV);
+      tc::mbar_init(&planes_empty[b], 1);
       tc::mbar_init(&mma_done[b], 1);
       tc::mbar_init(&acc_empty[b], NEPI);
     }
@@ -151,18 +150,16 @@ __global__ void __launch_bounds__(NT, 1)
   const uint32_t sbase = tc::smem_u32(smem);
 
   if (warp == 0) {
-    // ---- TMA producer ----
+    // ---- TMA producer: one [18][10][32] box per tile into the raw ring ----
     if (lane == 0) {
       int i = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
-        const int s = i % NS;
-        if (i >= NS) tc::mbar_wait(&halo_empty[s], uint32_t((i / NS - 1) & 1));
+        const int r = i & 1;
+        if (i >= 2) tc::mbar_wait(&raw_empty[r], uint32_t(((i >> 1) - 1) & 1));
         const TileCoord tc_ = tile_coord(t, a.H, a.W);
-        mbar_expect_tx(&tma_full[s], NCH * PLANE_BYTES);
-        const uint32_t dst = sbase + OFF_STAGE + s * STAGE_BYTES;
-#pragma unroll
-        for (int j = 0; j < NCH; ++j)
-          tma_load_4d(dst + j * LBO_A, &xmap, 4 * j, tc_.x0 - 1, tc_.y0 - 1, tc_.b, &tma_full[s]);
+        mbar_expect_tx(&raw_full[r], RAW_BYTES);
+        tma_load_4d(sbase + OFF_RAW + r * RAW_BYTES, &xmap, 0, tc_.x0 - 1, tc_.y0 - 1, tc_.b,
+                    &raw_full[r]);
       }
     }
   } else if (warp == 1) {
@@ -171,26 +168,27 @@ __global__ void __launch_bounds__(NT, 1)
       const uint64_t b0 = tc::smem_desc(sbase, W_ROWS * 16, 128);
       int i = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
-        const int s = i % NS, b = i & 1;
-        tc::mbar_wait(&conv_full[s], uint32_t((i / NS) & 1));
+        const int b = i & 1;
+        tc::mbar_wait(&conv_full[b], uint32_t((i >> 1) & 1));
         if (i >= 2) tc::mbar_wait(&acc_empty[b], uint32_t(((i >> 1) - 1) & 1));
         tc::fence_after();
-        const uint32_t hi = sbase + OFF_STAGE + s * STAGE_BYTES;
+        const uint32_t hi = sbase + OFF_PLANES + b * PLANES_BYTES;
         issue_tile(tc::smem_desc(hi, LBO_A, HWD * 16),
                    tc::smem_desc(hi + HALF_BYTES, LBO_A, HWD * 16), b0, tmem + uint32_t(b * 64));
-        tc::commit(&halo_empty[s]);
+        tc::commit(&planes_empty[b]);
         tc::commit(&mma_done[b]);
       }
     }
   } else if (warp < 6) {
-    // ---- converters: raw fp32 planes -> tf32 hi (in place) + lo ----
+    // ---- converters: raw pixel-major box -> tf32 hi / lo K-major planes ----
     const int ct = tid - 64;
     int i = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
-      const int s = i % NS;
-      float* hi = reinterpret_cast<float*>(smem + OFF_STAGE + s * STAGE_BYTES);
-      float* lo = reinterpret_cast<float*>(smem + OFF_STAGE + s * STAGE_BYTES + HALF_BYTES);
-      tc::mbar_wait(&tma_full[s], uint32_t((i / NS) & 1));
+      const int b = i & 1;
+      const float* raw = reinterpret_cast<const float*>(smem + OFF_RAW + b * RAW_BYTES);
+      float* hi = reinterpret_cast<float*>(smem + OFF_PLANES + b * PLANES_BYTES);
+      float* lo = reinterpret_cast<float*>(smem + OFF_PLANES + b * PLANES_BYTES + HALF_BYTES);
+      tc::mbar_wait(&raw_full[b], uint32_t((i >> 1) & 1));
       if (a.rinv) {
         // conv_mlp_residual's rms_norm over the pixel's 32 channels
         named_sync(1, NCONV);  // previous tile's scale reads are done
@@ -198,7 +196,7 @@ __global__ void __launch_bounds__(NT, 1)
           float ms = 0.f;
 #pragma unroll
           for (int j = 0; j < NCH; ++j) {
-            const float4 v = *reinterpret_cast<const float4*>(hi + (j * LBO_A) / 4 + px * 4);
+            const float4 v = *reinterpret_cast<const float4*>(raw + px * 32 + 4 * j);
             ms = fmaf(v.x, v.x, ms);
             ms = fmaf(v.y, v.y, ms);
             ms = fmaf(v.z, v.z, ms);
@@ -208,10 +206,10 @@ __global__ void __launch_bounds__(NT, 1)
         }
         named_sync(1, NCONV);
       }
+      if (i >= 2) tc::mbar_wait(&planes_empty[b], uint32_t(((i >> 1) - 1) & 1));
       for (int e = ct; e < HALO_PX * NCH; e += NCONV) {
-        const int j = e / HALO_PX, px = e - j * HALO_PX;
-        const int off = (j * LBO_A) / 4 + px * 4;
-        float4 v = *reinterpret_cast<const float4*>(hi + off);
+        const int px = e >> 3, j = e & 7;
+        float4 v = *reinterpret_cast<const float4*>(raw + px * 32 + 4 * j);
         if (a.rinv) {
           const float r = rms_s[px];
           const float4 g = __ldg(reinterpret_cast<const float4*>(a.gain) + j);
@@ -225,11 +223,13 @@ __global__ void __launch_bounds__(NT, 1)
         tc::split_tf32(v.y, h.y, l.y);
         tc::split_tf32(v.z, h.z, l.z);
         tc::split_tf32(v.w, h.w, l.w);
+        const int off = (j * LBO_A) / 4 + px * 4;
         *reinterpret_cast<float4*>(hi + off) = h;
         *reinterpret_cast<float4*>(lo + off) = l;
       }
+      tc::mbar_arrive(&raw_empty[b]);
       tc::fence_proxy_async();
-      tc::mbar_arrive(&conv_full[s]);
+      tc::mbar_arrive(&conv_full[b]);
     }
   } else {
     // ---- epilogue: TMEM -> bias / GELU / residual -> global ----
@@ -316,7 +316,7 @@ void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
   cuuint64_t dims[4] = {32, cuuint64_t(a.W), cuuint64_t(a.H), cuuint64_t(a.B)};
   cuuint64_t strides[3] = {cuuint64_t(S.pstride) * 4, cuuint64_t(S.pstride) * 4 * a.W,
                            cuuint64_t(S.bstride) * 4};
-  cuuint32_t box[4] = {4, HWD, HHT, 1};
+  cuuint32_t box[4] = {32, HWD, HHT, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(S.ptr), dims, strides,
               box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
