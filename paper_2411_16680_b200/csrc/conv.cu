@@ -129,6 +129,66 @@ __global__ void __launch_bounds__(NT) conv3x3_kernel(const ConvArgs a) {
   }
 }
 
+// Encoder stem (Cin = 3 -> Cout = 32, encode_inputs network.hpp:390): one
+// thread per output pixel, the 27 taps in registers, weights [k = ci*9+tap][32]
+// broadcast from shared memory, k ascending from the bias like the reference.
+__global__ void __launch_bounds__(128) conv3x3_stem_kernel(const ConvArgs a) {
+  __shared__ __align__(16) float s_w[27 * 32];
+  __shared__ float s_b[32];
+  for (int e = threadIdx.x; e < 27 * 32; e += blockDim.x) {
+    const int co = e % 32, k = e / 32;
+    s_w[e] = __ldg(a.w + co * 27 + k);
+  }
+  if (threadIdx.x < 32) s_b[threadIdx.x] = a.bias ? __ldg(a.bias + threadIdx.x) : 0.f;
+  __syncthreads();
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t HW = (int64_t)a.H * a.W;
+  if (i >= HW * a.B) return;
+  const int b = int(i / HW);
+  const int64_t pix = i - b * HW;
+  const int y = int(pix / a.W), x = int(pix % a.W);
+  const ConvSrc& S = a.src[0];
+  const float* src = S.ptr + (long long)b * S.bstride;
+  float xin[27];
+#pragma unroll
+  for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+    for (int dx = 0; dx < 3; ++dx) {
+      const int yy = y + dy - 1, xx = x + dx - 1;
+      const bool ok = yy >= 0 && yy < a.H && xx >= 0 && xx < a.W;
+      const float* p = src + ((long long)yy * a.W + xx) * S.pstride;
+#pragma unroll
+      for (int ci = 0; ci < 3; ++ci) xin[ci * 9 + dy * 3 + dx] = ok ? __ldg(p + ci) : 0.f;
+    }
+  float acc[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) acc[c] = s_b[c];
+#pragma unroll
+  for (int k = 0; k < 27; ++k) {
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4) {
+      const float4 w = reinterpret_cast<const float4*>(s_w + k * 32)[c4];
+      acc[4 * c4] = fmaf(xin[k], w.x, acc[4 * c4]);
+      acc[4 * c4 + 1] = fmaf(xin[k], w.y, acc[4 * c4 + 1]);
+      acc[4 * c4 + 2] = fmaf(xin[k], w.z, acc[4 * c4 + 2]);
+      acc[4 * c4 + 3] = fmaf(xin[k], w.w, acc[4 * c4 + 3]);
+    }
+  }
+  float4* o = reinterpret_cast<float4*>(a.out + (long long)b * a.out_bstride + pix * a.out_pstride);
+#pragma unroll
+  for (int c4 = 0; c4 < 8; ++c4) {
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = a.gelu ? gelu_ref(acc[4 * c4 + k]) : acc[4 * c4 + k];
+    o[c4] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
+bool stem_supported(const ConvArgs& a) {
+  return a.Cin == 3 && a.Cout == 32 && a.nsrc == 1 && !a.rinv && !a.resid && a.out_pstride == 32 &&
+         (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 && a.out_bstride % 4 == 0;
+}
+
 }  // namespace
 
 bool conv3x3_uses_tc(const ConvArgs& a, int impl) {
@@ -141,10 +201,14 @@ bool conv3x3_uses_tc(const ConvArgs& a, int impl) {
 }
 
 void conv3x3(const ConvArgs& a, cudaStream_t st, int impl) {
-  if (conv3x3_uses_tc(a, impl))
+  if (conv3x3_uses_tc(a, impl)) {
     conv3x3_tc(a, st);  // computes the rms-norm input scale itself
-  else
+  } else if (impl != 1 && stem_supported(a)) {
+    const int64_t n = (int64_t)a.B * a.H * a.W;
+    conv3x3_stem_kernel<<<int((n + 127) / 128), 128, 0, st>>>(a);
+  } else {
     conv3x3_simt(a, st);
+  }
 }
 
 void conv3x3_simt(const ConvArgs& a, cudaStream_t st) {

@@ -171,9 +171,13 @@ __global__ void __launch_bounds__(128) decode_payload32_kernel(
       acc[4 * c4 + 3] = fmaf(vk, w.w, acc[4 * c4 + 3]);
     }
   }
-  float* pay = payload + p * (C + 1);
+  // payload row padded to 36 floats: [a(32), sigma, 0, 0, 0]
+  float4* pay = reinterpret_cast<float4*>(payload + p * (C + 4));
 #pragma unroll
-  for (int c = 0; c < C + 1; ++c) pay[c] = sigmoid_ref(acc[c]);
+  for (int c4 = 0; c4 < C / 4; ++c4)
+    pay[c4] = make_float4(sigmoid_ref(acc[4 * c4]), sigmoid_ref(acc[4 * c4 + 1]),
+                          sigmoid_ref(acc[4 * c4 + 2]), sigmoid_ref(acc[4 * c4 + 3]));
+  pay[C / 4] = make_float4(sigmoid_ref(acc[C]), 0.f, 0.f, 0.f);
   const int l = int(p / ((int64_t)H * W));
   const float d = activate_depth(acc[C + 1], l, act);
   depth[p] = d;

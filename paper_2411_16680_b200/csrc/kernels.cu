@@ -79,6 +79,33 @@ __global__ void resize_hwc_kernel(const float* in, float* out, int B, int H, int
                  s[((int64_t)y1 * W + x0) * C + c], s[((int64_t)y1 * W + x1) * C + c], fx, fy);
 }
 
+// resize_hwc for C % 4 == 0: one thread per output pixel, taps computed once,
+// channels moved as float4.
+__global__ void resize_hwc4_kernel(const float* __restrict__ in, float* __restrict__ out, int B,
+                                   int H, int W, int C, int Ho, int Wo) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * Ho * Wo) return;
+  const int x = int(i % Wo);
+  const int y = int((i / Wo) % Ho);
+  const int b = int(i / ((int64_t)Wo * Ho));
+  int y0, y1, x0, x1;
+  float fy, fx;
+  resize_tap(y, H, Ho, y0, y1, fy);
+  resize_tap(x, W, Wo, x0, x1, fx);
+  const float4* s = reinterpret_cast<const float4*>(in + (int64_t)b * H * W * C);
+  const int G = C / 4;
+  const float4* a = s + ((int64_t)y0 * W + x0) * G;
+  const float4* bb = s + ((int64_t)y0 * W + x1) * G;
+  const float4* c = s + ((int64_t)y1 * W + x0) * G;
+  const float4* d = s + ((int64_t)y1 * W + x1) * G;
+  float4* o = reinterpret_cast<float4*>(out) + i * G;
+  for (int g = 0; g < G; ++g) {
+    const float4 A = __ldg(a + g), Bv = __ldg(bb + g), Cv = __ldg(c + g), D = __ldg(d + g);
+    o[g] = make_float4(lerp2(A.x, Bv.x, Cv.x, D.x, fx, fy), lerp2(A.y, Bv.y, Cv.y, D.y, fx, fy),
+                       lerp2(A.z, Bv.z, Cv.z, D.z, fx, fy), lerp2(A.w, Bv.w, Cv.w, D.w, fx, fy));
+  }
+}
+
 // One warp per row: rinv = 1 / sqrt(sum(x^2)/C + 1e-6).
 __global__ void rms_rinv_kernel(const float* x, float* rinv, int64_t rows, int C) {
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -246,7 +273,7 @@ __global__ void decode_payload_kernel(const float* __restrict__ V, int L, int H,
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= P) return;
   const float* v = V + p * C;
-  float* pay = payload + p * (Ca + 1);
+  float* pay = payload + p * pay_stride(Ca + 1);
   // matmul order: k ascending from 0 (kernels_ref.hpp:40-48)
   for (int c = 0; c < Ca + 2; ++c) {
     float acc = 0.f;
@@ -267,57 +294,83 @@ __global__ void decode_payload_kernel(const float* __restrict__ V, int L, int H,
   }
 }
 
-// One warp per (texel, view): lanes stride the K payload channels + weight.
+__device__ __forceinline__ void red_add_v4(float* p, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+// One thread per (texel, view, 4-channel group): the texel's bilinear
+// footprint in the view (f64, shared rule with the gather) and four
+// vector reductions red.global.add.v4.f32 of (w_k * payload, w_k) into the
+// padded accumulator rows [.., acc_stride(K)] (geometry.hpp:245-263).
 __global__ void splat_kernel(const float* __restrict__ payload, const float* __restrict__ points,
                              int L, int PL, int K, const DevCam* __restrict__ cams, int M, int Hv,
                              int Wv, float* acc) {
-  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  const int PS = pay_stride(K), S = acc_stride(K), G = S / 4;
   const int64_t P = (int64_t)L * PL;
-  if (wid >= P * M) return;
-  const int m = int(wid % M);
-  const int64_t p = wid / M;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= P * M * G) return;
+  const int g = int(i % G);
+  const int64_t t = i / G;
+  const int m = int(t % M);
+  const int64_t p = t / M;
   const int l = int(p / PL);
   const float pt[3] = {points[p * 3], points[p * 3 + 1], points[p * 3 + 2]};
   const Footprint f = project_footprint(cams[m], pt);
   if (!f.valid) return;
   double w[4];
   bilinear_weights(f, w);
+  float val[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int c = 4 * g + k;
+    val[k] = c < K ? __ldg(payload + p * PS + c) : (c == K ? 1.0f : 0.0f);
+  }
   const int64_t base = (int64_t)m * L * Hv * Wv + (int64_t)l * Hv * Wv;
   const int64_t tap[4] = {base + (int64_t)f.y0 * Wv + f.x0, base + (int64_t)f.y0 * Wv + f.x1,
                           base + (int64_t)f.y1 * Wv + f.x0, base + (int64_t)f.y1 * Wv + f.x1};
-  for (int c = lane; c < K + 1; c += 32) {
-    const float val = c < K ? payload[p * K + c] : 1.0f;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float wk = __double2float_rn(w[k]);
-      atomicAdd(acc + tap[k] * (K + 1) + c, c < K ? fm(wk, val) : wk);
-    }
+  for (int k = 0; k < 4; ++k) {
+    const float wk = __double2float_rn(w[k]);
+    red_add_v4(acc + tap[k] * S + 4 * g,
+               make_float4(fm(wk, val[0]), fm(wk, val[1]), fm(wk, val[2]), fm(wk, val[3])));
   }
 }
 
-// One thread per (view pixel, output channel): normalise by max(wsum,1e-4)
+// One thread per (view pixel, 4-channel group): normalise by max(wsum,1e-4)
 // then composite back to front (geometry.hpp:317-326; ldm.hpp:98-115).
+// Output rows are padded to pay_stride(K) (channels K.. are zero).
 __global__ void splat_composite_kernel(const float* __restrict__ acc, int M, int L, int Hv, int Wv,
                                        int K, float* out) {
+  const int PS = pay_stride(K), S = acc_stride(K), G = PS / 4;
   const int64_t PV = (int64_t)Hv * Wv;
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= (int64_t)M * PV * K) return;
-  const int c = int(i % K);
-  const int64_t t = i / K;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)M * PV * G) return;
+  const int g = int(i % G);
+  const int64_t t = i / G;
   const int64_t pix = t % PV;
   const int m = int(t / PV);
   const int Ca = K - 1;
-  float o = 0.f;
+  float o[4] = {0.f, 0.f, 0.f, 0.f};
   for (int l = 0; l < L; ++l) {
-    const float* a = acc + (((int64_t)m * L + l) * PV + pix) * (K + 1);
-    const float ws = a[K];
+    const float* a = acc + (((int64_t)m * L + l) * PV + pix) * S;
+    const float ws = __ldg(a + K);
     const float n = __fdiv_rn(1.0f, ws > 1e-4f ? ws : 1e-4f);
-    const float s = fm(a[Ca], n);
-    const float v = c < Ca ? fm(a[c], n) : 1.0f;
-    o = fa(fm(v, s), fm(fsb(1.0f, s), o));
+    const float s = fm(__ldg(a + Ca), n);
+    const float4 v4 = __ldg(reinterpret_cast<const float4*>(a) + g);
+    const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = 4 * g + k;
+      const float v = c < Ca ? fm(vv[k], n) : 1.0f;
+      o[k] = fa(fm(v, s), fm(fsb(1.0f, s), o[k]));
+    }
   }
-  out[i] = o;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (4 * g + k >= K) o[k] = 0.f;
+  reinterpret_cast<float4*>(out)[t * G + g] = make_float4(o[0], o[1], o[2], o[3]);
 }
 
 // ----------------------------------------------------------------------------
@@ -665,6 +718,12 @@ void resize_hwc(const float* in, float* out, int B, int H, int W, int C, int Ho,
     cudaMemcpyAsync(out, in, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
     return;
   }
+  const bool al = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+  if (C % 4 == 0 && al) {
+    const int64_t px = (int64_t)B * Ho * Wo;
+    resize_hwc4_kernel<<<blocks_for(px, 128), 128, 0, st>>>(in, out, B, H, W, C, Ho, Wo);
+    return;
+  }
   resize_hwc_kernel<<<blocks_for(n, 256), 256, 0, st>>>(in, out, B, H, W, C, Ho, Wo);
 }
 void rms_rinv(const float* x, float* rinv, int64_t rows, int C, cudaStream_t st) {
@@ -705,13 +764,13 @@ void decode_payload(const float* V, int L, int H, int W, int C, const float* w_a
 }
 void splat(const float* payload, const float* points, int L, int PL, int K, const DevCam* cams_dev,
            int M, int Hv, int Wv, float* acc, cudaStream_t st) {
-  const int64_t warps = (int64_t)L * PL * M;
-  splat_kernel<<<blocks_for(warps * 32, 256), 256, 0, st>>>(payload, points, L, PL, K, cams_dev, M,
-                                                            Hv, Wv, acc);
+  const int64_t n = (int64_t)L * PL * M * (acc_stride(K) / 4);
+  splat_kernel<<<blocks_for(n, 256), 256, 0, st>>>(payload, points, L, PL, K, cams_dev, M, Hv, Wv,
+                                                   acc);
 }
 void splat_composite(const float* acc, int M, int L, int Hv, int Wv, int K, float* out,
                      cudaStream_t st) {
-  const int64_t n = (int64_t)M * Hv * Wv * K;
+  const int64_t n = (int64_t)M * Hv * Wv * (pay_stride(K) / 4);
   splat_composite_kernel<<<blocks_for(n, 256), 256, 0, st>>>(acc, M, L, Hv, Wv, K, out);
 }
 

@@ -82,6 +82,13 @@ void gather_stack(const float* feats, int M, int Hf, int Wf, int C, const DevCam
                   const DevRayCam& rc, const float* depth, int L, int H, int W, float* deltas,
                   cudaStream_t st);
 
+// Per-pixel strides of the render-to-input-view buffers, padded to 16 bytes
+// so every row moves as float4 / vector atomics and feeds TMA: the payload
+// and the composited feedback carry K = Ca+1 channels, the splat
+// accumulators K+1 (the bilinear weight sum).
+__host__ __device__ inline int pay_stride(int K) { return (K + 3) & ~3; }
+__host__ __device__ inline int acc_stride(int K) { return (K + 1 + 3) & ~3; }
+
 // render_to_input_view decode (ldm.hpp:229-235): payload [P, Ca+1] =
 // [sigmoid(V w_a), sigmoid(V w_sigma)], depth [P] = activate(V w_depth) and
 // world points [P,3].

@@ -26,14 +26,17 @@ __device__ __forceinline__ float sample(const float* map, int W, const Taps& t) 
 }
 
 // Activated LDM sample of layer l at output pixel: depth, sigma, beta[M].
+// MM > 0: compile-time view count (every per-view array stays in registers).
+template <int MM>
 __device__ __forceinline__ void ldm_sample(const RenderArgs& a, int l, const Taps& t, float& depth,
                                            float& sigma, float* beta) {
   const int64_t plane = (int64_t)a.H * a.W;
   depth = activate_depth(sample(a.pre_d + l * plane, a.W, t), l, a.act);
   sigma = sigmoid_ref(sample(a.pre_s + l * plane, a.W, t));
-  const float* lg = a.logits + l * plane * a.M;
-  const int M = a.M;
+  const int M = MM > 0 ? MM : a.M;
+  const float* lg = a.logits + l * plane * M;
   float mx = 0.f;
+#pragma unroll
   for (int m = 0; m < M; ++m) {
     const float v = lerp2(__ldg(lg + ((int64_t)t.y0 * a.W + t.x0) * M + m),
                           __ldg(lg + ((int64_t)t.y0 * a.W + t.x1) * M + m),
@@ -43,11 +46,13 @@ __device__ __forceinline__ void ldm_sample(const RenderArgs& a, int l, const Tap
     mx = m == 0 ? v : fmaxf(mx, v);
   }
   float sum = 0.f;
+#pragma unroll
   for (int m = 0; m < M; ++m) {
     beta[m] = expf(fsb(beta[m], mx));
     sum = fa(sum, beta[m]);
   }
   const float inv = __fdiv_rn(1.0f, sum);
+#pragma unroll
   for (int m = 0; m < M; ++m) beta[m] = fm(beta[m], inv);
 }
 
@@ -59,6 +64,7 @@ __device__ __forceinline__ Taps taps_for(const RenderArgs& a, int i, int j) {
 }
 
 // One thread per output pixel of the row band.
+template <int MM>
 __global__ void __launch_bounds__(128) render_fused_kernel(const RenderArgs a) {
   extern __shared__ DevCam s_cams[];
   for (int m = threadIdx.x; m < a.M; m += blockDim.x) s_cams[m] = a.cams[m];
@@ -68,21 +74,22 @@ __global__ void __launch_bounds__(128) render_fused_kernel(const RenderArgs a) {
   if (idx >= (int64_t)rows * a.Wo) return;
   const int i = a.row0 + int(idx / a.Wo), j = int(idx % a.Wo);
   const Taps t = taps_for(a, i, j);
-  const int M = a.M;
+  const int M = MM > 0 ? MM : a.M;
   float o[3] = {0.f, 0.f, 0.f};
-  float beta[kMaxViews];
+  float beta[MM > 0 ? MM : kMaxViews];
   int bad = 0;
   const int64_t img_stride = (int64_t)a.Hr * a.Wr * 3;
   for (int l = 0; l < a.L; ++l) {
     float depth, sigma;
-    ldm_sample(a, l, t, depth, sigma, beta);
+    ldm_sample<MM>(a, l, t, depth, sigma, beta);
     const double dv = double(depth);
     bad |= (dv < a.slack_lo || dv > a.slack_hi);
     float pt[3];
     world_point(a.rc, i, j, depth, pt);
     // blended_layer_colors: beta * mask, wsum (k ascending from 0), 1/(wsum+1e-8)
-    float col[kMaxViews][3];
+    float col[MM > 0 ? MM : kMaxViews][3];
     float wsum = 0.f;
+#pragma unroll
     for (int m = 0; m < M; ++m) {
       const Footprint f = project_footprint(s_cams[m], pt);
       if (f.valid) {
@@ -105,6 +112,7 @@ __global__ void __launch_bounds__(128) render_fused_kernel(const RenderArgs a) {
     }
     const float r = __fdiv_rn(1.0f, fa(wsum, 1e-8f));
     float rgb[3] = {0.f, 0.f, 0.f};
+#pragma unroll
     for (int m = 0; m < M; ++m) {
       const float b = fm(beta[m], r);
 #pragma unroll
@@ -132,7 +140,7 @@ __global__ void upsample_activate_kernel(const RenderArgs a, float* depth, float
   const Taps t = taps_for(a, i, j);
   float beta[kMaxViews];
   float d, s;
-  ldm_sample(a, l, t, d, s, beta);
+  ldm_sample<0>(a, l, t, d, s, beta);
   depth[idx] = d;
   density[idx] = s;
   for (int m = 0; m < a.M; ++m) blend[idx * a.M + m] = beta[m];
@@ -144,7 +152,14 @@ inline int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
 
 void render_fused(const RenderArgs& a, cudaStream_t st) {
   const int64_t n = (int64_t)(a.row1 - a.row0) * a.Wo;
-  render_fused_kernel<<<blocks_for(n, 128), 128, a.M * sizeof(DevCam), st>>>(a);
+  const int g = blocks_for(n, 128);
+  const size_t sm = a.M * sizeof(DevCam);
+  switch (a.M) {
+    case 4: render_fused_kernel<4><<<g, 128, sm, st>>>(a); break;
+    case 8: render_fused_kernel<8><<<g, 128, sm, st>>>(a); break;
+    case 16: render_fused_kernel<16><<<g, 128, sm, st>>>(a); break;
+    default: render_fused_kernel<0><<<g, 128, sm, st>>>(a); break;
+  }
 }
 
 void upsample_activate(const RenderArgs& a, float* depth, float* density, float* blend,

@@ -315,8 +315,8 @@ void ensure_plan(lvsg_ctx* c, int64_t He, int64_t We) {
     // Δ in the view-major SoA layout [M][ceil(C/4)][P][4]
     maxD = std::max(maxD, size_t(sp.layers * sp.height * sp.width * M * ((C + 3) / 4) * 4));
     maxU = std::max(maxU, size_t(M * sp.feat_h * sp.feat_w));
-    maxAcc = std::max(maxAcc, size_t(M * sp.layers * sp.render_h * sp.render_w * (Ca + 2)));
-    maxFb = std::max(maxFb, size_t(M * sp.render_h * sp.render_w * (Ca + 1)));
+    maxAcc = std::max(maxAcc, size_t(M * sp.layers * sp.render_h * sp.render_w * acc_stride(int(Ca) + 1)));
+    maxFb = std::max(maxFb, size_t(M * sp.render_h * sp.render_w * pay_stride(int(Ca) + 1)));
   }
   c->V0.ensure(maxV * C);
   c->V1.ensure(maxV * C);
@@ -326,13 +326,13 @@ void ensure_plan(lvsg_ctx* c, int64_t He, int64_t We) {
   c->uh.ensure(maxU * C);
   c->ut.ensure(maxU * C);
   c->uu.ensure(maxU * C);
-  c->payload.ensure(maxIn * (Ca + 1));
+  c->payload.ensure(maxIn * pay_stride(int(Ca) + 1));
   c->depth_in.ensure(maxIn);
   c->points.ensure(maxIn * 3);
   c->depth_out.ensure(maxV);
   c->acc.ensure(maxAcc);
   c->fb.ensure(maxFb);
-  c->fbr.ensure(maxU * (Ca + 1));
+  c->fbr.ensure(maxU * pay_stride(int(Ca) + 1));
   const StepPlan& last = plan.steps.back();
   const size_t Pf = size_t(last.layers * last.height * last.width);
   c->pre_d.ensure(Pf);
@@ -609,7 +609,7 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
       L /= 2;
     }
     const int Hf = int(sp.feat_h), Wf = int(sp.feat_w), Hv = int(sp.render_h), Wv = int(sp.render_w);
-    const int Kp = Ca + 1;
+    const int Kp = Ca + 1, PS = pay_stride(Kp);
     const DepthAct act = depth_act(L, target);
     // update_block: render the volume into every view (ldm.hpp:223-244)
     decode_payload(V, int(L), int(H), int(Wd), C, W.w_appear, Ca, W.w_sigma, W.w_depth, act,
@@ -617,14 +617,14 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
     mark(c, "splat", 1);
     const float* feedback = c->fbr.p;
     if (cfg.ablate_render) {
-      CUDA_OK(cudaMemsetAsync(c->fbr.p, 0, size_t(M) * Hf * Wf * Kp * sizeof(float), st));
+      CUDA_OK(cudaMemsetAsync(c->fbr.p, 0, size_t(M) * Hf * Wf * PS * sizeof(float), st));
     } else {
-      CUDA_OK(cudaMemsetAsync(c->acc.p, 0, size_t(M) * L * Hv * Wv * (Kp + 1) * sizeof(float), st));
+      CUDA_OK(cudaMemsetAsync(c->acc.p, 0, size_t(M) * L * Hv * Wv * acc_stride(Kp) * sizeof(float), st));
       splat(c->payload.p, c->points.p, int(L), int(H * Wd), Kp, cams.rend[s], M, Hv, Wv, c->acc.p, st);
       splat_composite(c->acc.p, M, int(L), Hv, Wv, Kp, c->fb.p, st);
       mark(c, "splat", 2);
       if (sp.doubled) {
-        resize_hwc(c->fb.p, c->fbr.p, M, Hv, Wv, Kp, Hf, Wf, st);
+        resize_hwc(c->fb.p, c->fbr.p, M, Hv, Wv, PS, Hf, Wf, st);
         mark(c, "misc", 1);
       } else {
         feedback = c->fb.p;
@@ -633,6 +633,8 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
     ConvArgs in{};
     in.nsrc = 0;
     add_src(in, feedback, Kp, Hf, Wf);
+    in.src[0].pstride = PS;  // padded feedback rows
+    in.src[0].bstride = (long long)Hf * Wf * PS;
     add_src(in, c->feats[size_t(sp.level)].p, C, Hf, Wf);
     add_src(in, c->rays[size_t(sp.level)].p, C, Hf, Wf);
     update_cnn(c, sw, in, M, Hf, Wf);
