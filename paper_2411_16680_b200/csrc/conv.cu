@@ -79,7 +79,8 @@ __global__ void __launch_bounds__(NT) conv3x3_kernel(const ConvArgs a) {
       const int ci = rest % CK, co = rest / CK;
       const int gci = c0 + ci, gco = co_base + co;
       float v = 0.f;
-      if (gci < a.Cin && gco < a.Cout) v = __ldg(a.w + ((long long)gco * a.Cin + gci) * 9 + tap);
+      if (gci < a.Cin && gco < a.Cout)
+        v = __ldg(a.w + ((long long)gco * w_cin_of(a) + a.w_ci0 + gci) * 9 + tap);
       s_w[(tap * CK + ci) * COT + co] = v;
     }
     __syncthreads();
@@ -185,7 +186,8 @@ __global__ void __launch_bounds__(128) conv3x3_stem_kernel(const ConvArgs a) {
 }
 
 bool stem_supported(const ConvArgs& a) {
-  return a.Cin == 3 && a.Cout == 32 && a.nsrc == 1 && !a.rinv && !a.resid && a.out_pstride == 32 &&
+  return a.Cin == 3 && w_cin_of(a) == 3 && a.Cout == 32 && a.nsrc == 1 && !a.rinv && !a.resid &&
+         a.out_pstride == 32 &&
          (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 && a.out_bstride % 4 == 0;
 }
 

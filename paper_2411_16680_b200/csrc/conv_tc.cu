@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int j = rest % NCH, tap = rest / NCH;
     const int co = n & 31, ci = 4 * j + c4;
     float h, l;
-    tc::split_tf32(__ldg(a.w + (co * 32 + ci) * 9 + tap), h, l);
+    tc::split_tf32(__ldg(a.w + (co * w_cin_of(a) + a.w_ci0 + ci) * 9 + tap), h, l);
     w_s[e] = n < 32 ? h : l;
   }
   tc::fence_proxy_async();

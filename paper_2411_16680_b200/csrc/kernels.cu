@@ -162,7 +162,7 @@ __global__ void ray_base_kernel(const RayBaseCam* cams, RayBaseArgs a, float* ba
 // rays_k[p, c] = sum_f resize(base)[p, f] * proj[f, c] (network.hpp:405-411).
 __global__ void ray_project_kernel(const float* base, int M, int hK, int wK, int Hk, int Wk,
                                    const float* proj, int C, float* out) {
-  extern __shared__ float s_proj[];
+  extern __shared__ __align__(16) float s_proj[];
   for (int e = threadIdx.x; e < 32 * C; e += blockDim.x) s_proj[e] = proj[e];
   __syncthreads();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -186,6 +186,27 @@ __global__ void ray_project_kernel(const float* base, int M, int hK, int wK, int
                    b[((int64_t)y1 * wK + x0) * 32 + k], b[((int64_t)y1 * wK + x1) * 32 + k], fx, fy);
   }
   float* o = out + i * C;
+  if (C == 32) {  // production width: accumulators in registers, float4 weight broadcasts
+    float acc[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) {
+        const float4 w = reinterpret_cast<const float4*>(s_proj + k * 32)[c4];
+        acc[4 * c4] = fmaf(f[k], w.x, acc[4 * c4]);
+        acc[4 * c4 + 1] = fmaf(f[k], w.y, acc[4 * c4 + 1]);
+        acc[4 * c4 + 2] = fmaf(f[k], w.z, acc[4 * c4 + 2]);
+        acc[4 * c4 + 3] = fmaf(f[k], w.w, acc[4 * c4 + 3]);
+      }
+    }
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4)
+      reinterpret_cast<float4*>(o)[c4] =
+          make_float4(acc[4 * c4], acc[4 * c4 + 1], acc[4 * c4 + 2], acc[4 * c4 + 3]);
+    return;
+  }
   for (int c = 0; c < C; ++c) {
     float acc = 0.f;
 #pragma unroll

@@ -36,7 +36,11 @@ struct ConvArgs {
   const float* resid;  // or null
   int res_pstride;
   long long res_bstride;
+  // input-channel slice of the weight tensor: w is [Cout, w_cin, 3, 3] and
+  // this conv uses channels [w_ci0, w_ci0 + Cin) (0 = w_cin = Cin when unset)
+  int w_cin, w_ci0;
 };
+__host__ __device__ inline int w_cin_of(const ConvArgs& a) { return a.w_cin ? a.w_cin : a.Cin; }
 // Dispatches to the tcgen05 3xTF32 kernel when it applies (Cin = Cout = 32,
 // one 16-byte-aligned source), else to the fp32 SIMT kernel. impl: 0 auto,
 // 1 SIMT, 2 tcgen05 (unsupported shapes fall back to SIMT).

@@ -408,8 +408,43 @@ void update_cnn(lvsg_ctx* c, const StepW& sw, const ConvArgs& stem_in, int M, in
   a.out = c->uh.p;
   a.out_pstride = C;
   a.out_bstride = (long long)Hf * Wf * C;
-  conv3x3(a, c->stream);
-  mark(c, "conv", 1);
+  a.w_cin = a.Cin;
+  a.w_ci0 = 0;
+  // By linearity the stem over concat(sources) is the sum of one conv per
+  // source over its weight slice: each 32-channel source runs on the tensor
+  // core, leftovers (the feedback's alpha channel) on the SIMT kernel, all
+  // accumulating into uh (the first one adds the bias).
+  bool split = C == 32;
+  std::vector<ConvArgs> parts;
+  if (split) {
+    int ci0 = 0;
+    for (int s = 0; s < a.nsrc && split; ++s) {
+      const ConvSrc& S = a.src[s];
+      for (int c0 = 0; c0 < S.C; c0 += 32) {
+        const int cn = std::min(32, S.C - c0);
+        ConvArgs p = conv_args(M, Hf, Wf, cn, C, sw.stem_w, parts.empty() ? sw.stem_b : nullptr, c->uh.p);
+        p.src[0] = ConvSrc{S.ptr + c0, cn, S.pstride, S.bstride};
+        p.nsrc = 1;
+        p.w_cin = a.Cin;
+        p.w_ci0 = ci0 + c0;
+        if (!parts.empty()) {
+          p.resid = c->uh.p;
+          p.res_pstride = C;
+          p.res_bstride = (long long)Hf * Wf * C;
+        }
+        if (cn == 32 && !conv3x3_uses_tc(p)) split = false;
+        parts.push_back(p);
+      }
+      ci0 += S.C;
+    }
+  }
+  if (split) {
+    for (const ConvArgs& p : parts) conv3x3(p, c->stream);
+    mark(c, "conv", int(parts.size()));
+  } else {
+    conv3x3(a, c->stream);
+    mark(c, "conv", 1);
+  }
   conv_residual(c, c->uh.p, c->uh.p, c->ut.p, M, Hf, Wf, sw.r1);
   conv_residual(c, c->uh.p, c->uu.p, c->ut.p, M, Hf, Wf, sw.r2);
 }
