@@ -130,15 +130,18 @@ __global__ void __launch_bounds__(NT) conv3x3_kernel(const ConvArgs a) {
   }
 }
 
-// Encoder stem (Cin = 3 -> Cout = 32, encode_inputs network.hpp:390): one
-// thread per output pixel, the 27 taps in registers, weights [k = ci*9+tap][32]
-// broadcast from shared memory, k ascending from the bias like the reference.
+// Few-input-channel conv (Cin = CI in {1, 3} -> Cout = 32): the encoder
+// stem (encode_inputs network.hpp:390) and the feedback-alpha slice of the
+// update stems. One thread per output pixel, the 9*CI taps in registers,
+// weights [k = ci*9+tap][32] broadcast from shared memory, k ascending from
+// the bias like the reference; optional residual (accumulating slices).
+template <int CI>
 __global__ void __launch_bounds__(128) conv3x3_stem_kernel(const ConvArgs a) {
-  __shared__ __align__(16) float s_w[27 * 32];
+  __shared__ __align__(16) float s_w[9 * CI * 32];
   __shared__ float s_b[32];
-  for (int e = threadIdx.x; e < 27 * 32; e += blockDim.x) {
+  for (int e = threadIdx.x; e < 9 * CI * 32; e += blockDim.x) {
     const int co = e % 32, k = e / 32;
-    s_w[e] = __ldg(a.w + co * 27 + k);
+    s_w[e] = __ldg(a.w + ((long long)co * w_cin_of(a) + a.w_ci0) * 9 + k);
   }
   if (threadIdx.x < 32) s_b[threadIdx.x] = a.bias ? __ldg(a.bias + threadIdx.x) : 0.f;
   __syncthreads();
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(128) conv3x3_stem_kernel(const ConvArgs a) {
   const int y = int(pix / a.W), x = int(pix % a.W);
   const ConvSrc& S = a.src[0];
   const float* src = S.ptr + (long long)b * S.bstride;
-  float xin[27];
+  float xin[9 * CI];
 #pragma unroll
   for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
@@ -159,13 +162,13 @@ __global__ void __launch_bounds__(128) conv3x3_stem_kernel(const ConvArgs a) {
       const bool ok = yy >= 0 && yy < a.H && xx >= 0 && xx < a.W;
       const float* p = src + ((long long)yy * a.W + xx) * S.pstride;
 #pragma unroll
-      for (int ci = 0; ci < 3; ++ci) xin[ci * 9 + dy * 3 + dx] = ok ? __ldg(p + ci) : 0.f;
+      for (int ci = 0; ci < CI; ++ci) xin[ci * 9 + dy * 3 + dx] = ok ? __ldg(p + ci) : 0.f;
     }
   float acc[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) acc[c] = s_b[c];
 #pragma unroll
-  for (int k = 0; k < 27; ++k) {
+  for (int k = 0; k < 9 * CI; ++k) {
 #pragma unroll
     for (int c4 = 0; c4 < 8; ++c4) {
       const float4 w = reinterpret_cast<const float4*>(s_w + k * 32)[c4];
@@ -176,19 +179,30 @@ __global__ void __launch_bounds__(128) conv3x3_stem_kernel(const ConvArgs a) {
     }
   }
   float4* o = reinterpret_cast<float4*>(a.out + (long long)b * a.out_bstride + pix * a.out_pstride);
+  const float4* rs = a.resid ? reinterpret_cast<const float4*>(a.resid + (long long)b * a.res_bstride +
+                                                               pix * a.res_pstride)
+                             : nullptr;
 #pragma unroll
   for (int c4 = 0; c4 < 8; ++c4) {
     float v[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = a.gelu ? gelu_ref(acc[4 * c4 + k]) : acc[4 * c4 + k];
+    if (rs) {
+      const float4 r = rs[c4];
+      v[0] = fa(r.x, v[0]);
+      v[1] = fa(r.y, v[1]);
+      v[2] = fa(r.z, v[2]);
+      v[3] = fa(r.w, v[3]);
+    }
     o[c4] = make_float4(v[0], v[1], v[2], v[3]);
   }
 }
 
 bool stem_supported(const ConvArgs& a) {
-  return a.Cin == 3 && w_cin_of(a) == 3 && a.Cout == 32 && a.nsrc == 1 && !a.rinv && !a.resid &&
-         a.out_pstride == 32 &&
-         (reinterpret_cast<uintptr_t>(a.out) & 15) == 0 && a.out_bstride % 4 == 0;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  return (a.Cin == 1 || a.Cin == 3) && a.Cout == 32 && a.nsrc == 1 && !a.rinv &&
+         a.out_pstride == 32 && al(a.out) && a.out_bstride % 4 == 0 &&
+         (!a.resid || (al(a.resid) && a.res_pstride % 4 == 0 && a.res_bstride % 4 == 0));
 }
 
 }  // namespace
@@ -207,7 +221,10 @@ void conv3x3(const ConvArgs& a, cudaStream_t st, int impl) {
     conv3x3_tc(a, st);  // computes the rms-norm input scale itself
   } else if (impl != 1 && stem_supported(a)) {
     const int64_t n = (int64_t)a.B * a.H * a.W;
-    conv3x3_stem_kernel<<<int((n + 127) / 128), 128, 0, st>>>(a);
+    if (a.Cin == 3)
+      conv3x3_stem_kernel<3><<<int((n + 127) / 128), 128, 0, st>>>(a);
+    else
+      conv3x3_stem_kernel<1><<<int((n + 127) / 128), 128, 0, st>>>(a);
   } else {
     conv3x3_simt(a, st);
   }

@@ -1,21 +1,26 @@
 """Summarise an ncu --metrics gpu__time_duration.sum --csv launch list:
-per-kernel total device time, launch count and share."""
+per-kernel total device time, launch count and share. With --last-frame,
+only launches after the last L2-flush fill kernel (bench.py flushes before
+every timed frame) are counted, i.e. exactly one timed frame."""
 import collections
 import csv
 import sys
 
 
-def main(path):
+def main(path, last_frame=False):
     rows = list(csv.reader(open(path)))
     hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hdr]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    body = [r for r in rows[hdr + 1:] if len(r) > vi]
+    if last_frame:
+        flush = [i for i, r in enumerate(body) if "FillFunctor" in r[ki]]
+        if flush:
+            body = body[flush[-1] + 1:]
     agg = collections.defaultdict(lambda: [0.0, 0])
     tot = 0.0
     scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1.0, "msecond": 1.0}
-    for r in rows[hdr + 1:]:
-        if len(r) <= vi:
-            continue
+    for r in body:
         v = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
         name = r[ki].split("(")[0].replace("void ", "").replace("lvsg::", "")
         name = name.replace("<unnamed>::", "")
@@ -29,4 +34,4 @@ def main(path):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], "--last-frame" in sys.argv)
