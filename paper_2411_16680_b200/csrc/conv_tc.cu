@@ -1,21 +1,25 @@
 // conv3x3 (Cin = Cout = 32, channel-last) as an implicit GEMM on the sm_100a
-// tensor core: tcgen05.mma kind::tf32 with a 3xTF32 split so the solve stays
-// fp32-accurate (SURVEY.md §7 hard part 2):
-//     y = b + sum_tap,ci x*w  ~=  xh*wh + (xh*wl + xl*wh)
+// tensor core: tcgen05.mma kind::f16 with a 3-term fp16 split so the solve
+// stays fp32-accurate (SURVEY.md §7 hard part 2):
+//     x = xh + 2^-11 xl',  w = wh + 2^-11 wl'   (tc::split_f16)
+//     y = b + sum_tap,ci x*w  ~=  xh*wh + 2^-11 (xh*wl' + xl'*wh)
+// -- the same ~2^-22 relative error per product as 3xTF32, at half the
+// shared-memory operand bytes per MAC (K = 16 per instruction), which is what
+// bounds this N = 32-output-channel GEMM.
 //
 // Tile = 16 rows x 8 columns of output pixels (M = 128 GEMM rows, row
 // m = 8g + i <-> pixel (y0+g, x0+i)), N = 32 output channels, K = 9 taps x 32
-// input channels. The 18 x 10 x 32 input halo arrives as one TMA box; converter
-// warps rewrite it as eight 4-channel planes of tf32 hi and lo ([18][10][4]
-// floats each) -- the K-major "interleave" operand layout with core-matrix
-// groups SBO = 160 B apart (one halo row), so each tap (dy, dx) is the same
-// descriptor with its start address moved by (10*dy + dx) * 16 bytes: im2col
-// costs nothing. The optional conv-MLP rms-norm is applied in the converter
-// from the 32 channels already in shared memory. Weights [Wh ; Wl] (N = 64) stay resident. Per K
-// step (8 channels of one tap):
-//     MMA1  N=64: D[:, 0:64]  += Xh * [Wh ; Wl]^T
-//     MMA2  N=32: D[:, 32:64] += Xl * Wh^T
-// and the epilogue sums D[:, c] + D[:, 32+c].
+// input channels. The 18 x 10 x 32 input halo arrives as one TMA box;
+// converter warps rewrite it as four 8-channel fp16 planes of hi and lo'
+// ([18][10][8] halves each) -- the K-major "interleave" operand layout with
+// core-matrix groups SBO = 160 B apart (one halo row), so each tap (dy, dx) is
+// the same descriptor with its start address moved by (10*dy + dx) * 16
+// bytes: im2col costs nothing. The optional conv-MLP rms-norm is applied in
+// the converter from the 32 channels already in shared memory. Weights
+// [Wh ; Wl'] (N = 64) stay resident. Per K step (16 channels of one tap):
+//     MMA1  N=64: D[:, 0:64]  += Xh  * [Wh ; Wl']^T
+//     MMA2  N=32: D[:, 32:64] += Xl' * Wh^T
+// and the epilogue forms D[:, c] + 2^-11 D[:, 32+c].
 //
 // Warp roles of the persistent CTA (1 per SM): w0 TMA producer, w1 MMA issuer
 // (+ TMEM owner), w2-5 converters, w6-9 epilogue; two raw TMA stages, two
@@ -36,13 +40,13 @@ namespace {
 constexpr int TW = 8, TH = 16;
 constexpr int HWD = TW + 2, HHT = TH + 2;       // 10 x 18 halo
 constexpr int HALO_PX = HWD * HHT;              // 180
-constexpr int NCH = 8;                          // 4-channel planes (Cin = 32)
+constexpr int NCH = 4;                          // 8-channel fp16 planes (Cin = 32)
 constexpr int RAW_BYTES = HALO_PX * 32 * 4;     // one TMA box [18][10][32] (23040)
 constexpr int LBO_A = HALO_PX * 16 + 16;        // plane stride (padded: conflict-free stores)
 constexpr int HALF_BYTES = NCH * LBO_A;         // hi (or lo) planes of one buffer
 constexpr int PLANES_BYTES = 2 * HALF_BYTES;
 constexpr int W_ROWS = 64;                      // 32 hi + 32 lo
-constexpr int W_BYTES = 9 * NCH * W_ROWS * 16;  // 73728
+constexpr int W_BYTES = 9 * NCH * W_ROWS * 16;  // 36864
 constexpr int OFF_RAW = W_BYTES;                // 2 raw TMA stages
 constexpr int OFF_PLANES = OFF_RAW + 2 * RAW_BYTES;
 constexpr int OFF_RMS = OFF_PLANES + 2 * PLANES_BYTES;
@@ -89,8 +93,8 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 
 __device__ __forceinline__ void issue_tile(uint64_t ah0, uint64_t al0, uint64_t b0,
                                            uint32_t tmem_acc) {
-  constexpr uint32_t id64 = tc::idesc_tf32(128, 64);
-  constexpr uint32_t id32 = tc::idesc_tf32(128, 32);
+  constexpr uint32_t id64 = tc::idesc_f16(128, 64);
+  constexpr uint32_t id32 = tc::idesc_f16(128, 32);
 #pragma unroll
   for (int tap = 0; tap < 9; ++tap) {
     const int dy = tap / 3, dx = tap % 3;
@@ -98,8 +102,8 @@ __device__ __forceinline__ void issue_tile(uint64_t ah0, uint64_t al0, uint64_t 
     for (int s = 0; s < NCH / 2; ++s) {
       const uint64_t aoff = uint64_t((2 * s * LBO_A + (dy * HWD + dx) * 16) >> 4);
       const uint64_t boff = uint64_t(((tap * NCH + 2 * s) * W_ROWS * 16) >> 4);
-      tc::mma_tf32(tmem_acc, ah0 + aoff, b0 + boff, id64, (tap | s) != 0);
-      tc::mma_tf32(tmem_acc + 32, al0 + aoff, b0 + boff, id32, 1u);
+      tc::mma_f16(tmem_acc, ah0 + aoff, b0 + boff, id64, (tap | s) != 0);
+      tc::mma_f16(tmem_acc + 32, al0 + aoff, b0 + boff, id32, 1u);
     }
   }
 }
@@ -107,7 +111,7 @@ __device__ __forceinline__ void issue_tile(uint64_t ah0, uint64_t al0, uint64_t 
 __global__ void __launch_bounds__(NT, 1)
     conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const ConvArgs a, int num_tiles) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  float* w_s = reinterpret_cast<float*>(smem);
+  __half* w_s = reinterpret_cast<__half*>(smem);
   float* rms_s = reinterpret_cast<float*>(smem + OFF_RMS);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* raw_full = bars;          // [2] TMA bytes landed
@@ -121,13 +125,13 @@ __global__ void __launch_bounds__(NT, 1)
   if (blockIdx.x >= num_tiles) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  // weights: [tap][plane j][row n][4], rows 0..31 = tf32 hi, 32..63 = lo
-  for (int e = tid; e < 9 * NCH * W_ROWS * 4; e += NT) {
-    const int c4 = e & 3, n = (e >> 2) & 63, rest = e >> 8;
+  // weights: [tap][plane j][row n][8 halves], rows 0..31 = fp16 hi, 32..63 = lo'
+  for (int e = tid; e < 9 * NCH * W_ROWS * 8; e += NT) {
+    const int k8 = e & 7, n = (e >> 3) & 63, rest = e >> 9;
     const int j = rest % NCH, tap = rest / NCH;
-    const int co = n & 31, ci = 4 * j + c4;
-    float h, l;
-    tc::split_tf32(__ldg(a.w + (co * w_cin_of(a) + a.w_ci0 + ci) * 9 + tap), h, l);
+    const int co = n & 31, ci = 8 * j + k8;
+    __half h, l;
+    tc::split_f16(__ldg(a.w + (co * w_cin_of(a) + a.w_ci0 + ci) * 9 + tap), h, l);
     w_s[e] = n < 32 ? h : l;
   }
   tc::fence_proxy_async();
@@ -180,7 +184,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
   } else if (warp < 6) {
-    // ---- converters: raw pixel-major box -> tf32 hi / lo K-major planes ----
+    // ---- converters: raw pixel-major box -> fp16 hi / lo' K-major planes ----
     const int ct = tid - 64;
     int i = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
@@ -208,24 +212,25 @@ __global__ void __launch_bounds__(NT, 1)
       }
       if (i >= 2) tc::mbar_wait(&planes_empty[b], uint32_t(((i >> 1) - 1) & 1));
       for (int e = ct; e < HALO_PX * NCH; e += NCONV) {
-        const int px = e >> 3, j = e & 7;
-        float4 v = *reinterpret_cast<const float4*>(raw + px * 32 + 4 * j);
+        const int px = e >> 2, j = e & 3;
+        float v[8];
+        {
+          const float4 v0 = *reinterpret_cast<const float4*>(raw + px * 32 + 8 * j);
+          const float4 v1 = *reinterpret_cast<const float4*>(raw + px * 32 + 8 * j + 4);
+          v[0] = v0.x, v[1] = v0.y, v[2] = v0.z, v[3] = v0.w;
+          v[4] = v1.x, v[5] = v1.y, v[6] = v1.z, v[7] = v1.w;
+        }
         if (a.rinv) {
           const float r = rms_s[px];
-          const float4 g = __ldg(reinterpret_cast<const float4*>(a.gain) + j);
-          v.x = fm(fm(v.x, r), g.x);
-          v.y = fm(fm(v.y, r), g.y);
-          v.z = fm(fm(v.z, r), g.z);
-          v.w = fm(fm(v.w, r), g.w);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] = fm(fm(v[k], r), __ldg(a.gain + 8 * j + k));
         }
-        float4 h, l;
-        tc::split_tf32(v.x, h.x, l.x);
-        tc::split_tf32(v.y, h.y, l.y);
-        tc::split_tf32(v.z, h.z, l.z);
-        tc::split_tf32(v.w, h.w, l.w);
-        const int off = (j * LBO_A) / 4 + px * 4;
-        *reinterpret_cast<float4*>(hi + off) = h;
-        *reinterpret_cast<float4*>(lo + off) = l;
+        __align__(16) __half h[8], l[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) tc::split_f16(v[k], h[k], l[k]);
+        const int off = j * LBO_A + px * 16;  // bytes
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(hi) + off) = *reinterpret_cast<uint4*>(h);
+        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(lo) + off) = *reinterpret_cast<uint4*>(l);
       }
       tc::mbar_arrive(&raw_empty[b]);
       tc::fence_proxy_async();
@@ -259,7 +264,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int c = 4 * c4 + k;
-          float y_ = fa(d0[c], d1[c]);
+          float y_ = fmaf(d1[c], 1.0f / tc::kF16LoScale, d0[c]);
           if (a.bias) y_ = fa(y_, __ldg(a.bias + c));
           if (a.gelu) y_ = gelu_ref(y_);
           v[k] = y_;

@@ -3,6 +3,7 @@
 // (SmemDescriptor / InstrDescriptor bit layouts of the sm_100 ISA).
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -33,6 +34,24 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
          | (2u << 10)                    // B format TF32
          | (uint32_t(N >> 3) << 17)      // N / 8
          | (uint32_t(M >> 4) << 24);     // M / 16
+}
+
+// Instruction descriptor: kind::f16 with fp16 A/B, fp32 accumulate, K-major.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4)                       // D format F32
+         | (0u << 7)                     // A format F16
+         | (0u << 10)                    // B format F16
+         | (uint32_t(N >> 3) << 17)      // N / 8
+         | (uint32_t(M >> 4) << 24);     // M / 16
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
 // D[tmem] (+)= A[smem] * B[smem]^T, one elected thread issues.
@@ -142,6 +161,17 @@ __device__ __forceinline__ float to_tf32(float x) {
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
   hi = to_tf32(x);
   lo = to_tf32(__fsub_rn(x, hi));
+}
+
+// fp32 -> (hi, lo') fp16 pair with hi = rn_f16(x), lo' = rn_f16((x - hi) * 2^11)
+// (x - hi is exact; the 2^11 scale keeps lo' in the normal fp16 range).
+// 3-term product with the scale folded out of a second accumulator:
+//   a*b ~= ah*bh + 2^-11 * (ah*bl' + al'*bh), the same ~2^-22 relative error
+// as 3xTF32 at half the operand bytes (SURVEY.md §7 hard part 2).
+constexpr float kF16LoScale = 2048.0f;
+__device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
+  hi = __float2half_rn(x);
+  lo = __float2half_rn(__fmul_rn(__fsub_rn(x, __half2float(hi)), kF16LoScale));
 }
 
 }  // namespace tc
