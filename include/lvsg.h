@@ -220,6 +220,15 @@ lvsg_status lvsg_scene_images(uint64_t seed, int64_t planes, const lvsg_frustum*
 lvsg_status lvsg_stage_conv3x3(lvsg_ctx* ctx, const float* x, const float* w, const float* b,
                                float* y, int64_t B, int64_t Cin, int64_t Cout, int64_t H,
                                int64_t W, int32_t impl);
+/* The fused forms used inside the solve: x with pixel stride x_pstride;
+ * weights sliced to input channels [w_ci0, w_ci0+Cin) of a [Cout,w_cin,3,3]
+ * tensor; optional rms_norm(x)*norm_gain on the input (conv_mlp_residual,
+ * attention.hpp:262-266), GELU, and y = resid + conv (resid may alias y). */
+lvsg_status lvsg_stage_conv3x3_fused(lvsg_ctx* ctx, const float* x, int64_t x_pstride,
+                                     const float* w, int64_t w_cin, int64_t w_ci0, const float* b,
+                                     const float* norm_gain, int32_t gelu, const float* resid,
+                                     float* y, int64_t B, int64_t Cin, int64_t Cout, int64_t H,
+                                     int64_t W, int32_t impl);
 
 #ifdef __cplusplus
 }

@@ -99,7 +99,7 @@ SYMBOLS = [
     "lvsg_forward_render", "lvsg_forward_render_device", "lvsg_render_rows_device",
     "lvsg_synchronize", "lvsg_last_launch_count", "lvsg_stream", "lvsg_stage_world_points",
     "lvsg_stage_footprints", "lvsg_stage_gather", "lvsg_rig_cameras", "lvsg_scene_images",
-    "lvsg_profile_enable", "lvsg_profile_read", "lvsg_stage_conv3x3",
+    "lvsg_profile_enable", "lvsg_profile_read", "lvsg_stage_conv3x3", "lvsg_stage_conv3x3_fused",
 ]
 
 
@@ -152,5 +152,7 @@ def lib() -> ctypes.CDLL:
     L.lvsg_profile_enable.argtypes = [vp, c_i32]
     L.lvsg_profile_read.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
     L.lvsg_stage_conv3x3.argtypes = [vp, vp, vp, vp, vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32]
+    L.lvsg_stage_conv3x3_fused.argtypes = [vp, vp, c_i64, vp, c_i64, c_i64, vp, vp, c_i32, vp, vp,
+                                           c_i64, c_i64, c_i64, c_i64, c_i64, c_i32]
     _lib = L
     return L

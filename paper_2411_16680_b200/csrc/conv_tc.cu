@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(NT, 1)
         for (int px = ct; px < HALO_PX; px += NCONV) {
           float ms = 0.f;
 #pragma unroll
-          for (int j = 0; j < NCH; ++j) {
+          for (int j = 0; j < 8; ++j) {  // all 32 channels
             const float4 v = *reinterpret_cast<const float4*>(raw + px * 32 + 4 * j);
             ms = fmaf(v.x, v.x, ms);
             ms = fmaf(v.y, v.y, ms);

@@ -1191,6 +1191,38 @@ lvsg_status lvsg_stage_conv3x3(lvsg_ctx* c, const float* x, const float* w, cons
   });
 }
 
+lvsg_status lvsg_stage_conv3x3_fused(lvsg_ctx* c, const float* x, int64_t x_pstride,
+                                     const float* w, int64_t w_cin, int64_t w_ci0, const float* b,
+                                     const float* norm_gain, int32_t gelu, const float* resid,
+                                     float* y, int64_t B, int64_t Cin, int64_t Cout, int64_t H,
+                                     int64_t W, int32_t impl) {
+  return guard(c, [&] {
+    if (B < 1 || Cin < 1 || Cout < 1 || H < 1 || W < 1 || x_pstride < Cin || w_ci0 < 0 ||
+        w_ci0 + Cin > w_cin)
+      throw DimError("conv3x3: bad shapes");
+    ConvArgs a = conv_args(int(B), int(H), int(W), int(Cin), int(Cout), w, b, y);
+    a.src[0] = ConvSrc{x, int(Cin), int(x_pstride), (long long)H * W * x_pstride};
+    a.nsrc = 1;
+    a.w_cin = int(w_cin);
+    a.w_ci0 = int(w_ci0);
+    a.gelu = gelu;
+    if (resid) {
+      a.resid = resid;
+      a.res_pstride = int(Cout);
+      a.res_bstride = (long long)H * W * Cout;
+    }
+    if (norm_gain) {  // conv_mlp_residual's rms_norm on the input
+      if (x_pstride != Cin) throw DimError("conv3x3: rms-norm input must be dense");
+      c->rinv.ensure(size_t(B * H * W));
+      a.rinv = c->rinv.p;
+      a.gain = norm_gain;
+      if (!conv3x3_uses_tc(a, impl)) rms_rinv(x, c->rinv.p, B * H * W, int(Cin), c->stream);
+    }
+    conv3x3(a, c->stream, impl);
+    sync_and_check(c);
+  });
+}
+
 lvsg_status lvsg_stage_gather(lvsg_ctx* c, const lvsg_camera* cam, const float* image,
                               int64_t Hi, int64_t Wi, int64_t C, const float* points, int64_t P,
                               float* values, float* mask) {

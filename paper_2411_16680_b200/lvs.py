@@ -343,6 +343,18 @@ class Model:
                                                  b_t.data_ptr() if b_t is not None else None,
                                                  y_t.data_ptr(), B, Cin, Cout, H, W, impl))
 
+    def stage_conv3x3_fused(self, x_t, w_t, b_t, y_t, cin, ci0=0, norm_gain_t=None, gelu=False,
+                            resid_t=None, impl: int = 0):
+        """The solve's fused conv: x [B,H,W,pstride] (first `cin` channels),
+        weight slice [:, ci0:ci0+cin] of w [Cout, w_cin, 3, 3], optional
+        rms-norm input scale, GELU and residual (y = resid + conv)."""
+        B, H, W, ps = x_t.shape
+        Cout, w_cin = w_t.shape[0], w_t.shape[1]
+        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        self._check(self._lib.lvsg_stage_conv3x3_fused(
+            self._h, x_t.data_ptr(), ps, w_t.data_ptr(), w_cin, ci0, ptr(b_t), ptr(norm_gain_t),
+            1 if gelu else 0, ptr(resid_t), y_t.data_ptr(), B, cin, Cout, H, W, impl))
+
     def stage_gather(self, cam: Camera, image_t, points_t, values_t, mask_t):
         c = cam.to_c()
         Hi, Wi, C = image_t.shape
