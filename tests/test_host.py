@@ -20,7 +20,7 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 def test_library_exports_every_header_symbol():
     hdr = open(os.path.join(ROOT, "include", "lvsg.h")).read()
-    declared = set(re.findall(r"\b(lvsg_[a-z_]+)\s*\(", hdr))
+    declared = set(re.findall(r"\b(lvsg_[a-z_0-9]+)\s*\(", hdr))
     lib = capi.lib()
     for name in sorted(declared):
         assert hasattr(lib, name), name
