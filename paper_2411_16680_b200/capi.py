@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblvsg.so")
+# LVSG_LIB overrides the library path (development probes of alternative builds).
+LIB_PATH = os.environ.get("LVSG_LIB") or os.path.join(_HERE, "liblvsg.so")
 
 c_i64 = ctypes.c_int64
 c_i32 = ctypes.c_int32

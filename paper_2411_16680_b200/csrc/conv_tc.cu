@@ -22,8 +22,12 @@
 // and the epilogue forms D[:, c] + 2^-11 D[:, 32+c].
 //
 // Warp roles of the persistent CTA (1 per SM): w0 TMA producer, w1 MMA issuer
-// (+ TMEM owner), w2-5 converters, w6-9 epilogue; two raw TMA stages, two
-// hi/lo plane buffers and two TMEM accumulators, hand-offs through mbarriers.
+// (+ TMEM owner), w2-5 converters, w6-13 epilogue (two warpgroups taking
+// alternate tiles); NR raw TMA stages, NP hi/lo plane buffers and NA TMEM
+// accumulators, hand-offs through mbarriers. Each epilogue warp owns one
+// 4-row x 8-column sub-box of the tile: its residual arrives by TMA one tile
+// ahead, and its output is staged in 128B-swizzled shared memory and leaves as
+// one TMA tile store (full-line writes; image edges clipped by the TMA unit).
 // Semantics of kernels_ref.hpp:72-96 (zero padding) with the bias / GELU /
 // residual / rms-norm-input options of ConvArgs.
 #include <cuda.h>
@@ -31,8 +35,16 @@
 
 #include <cstring>
 
+#include "host.h"
 #include "kernels.h"
 #include "tc.cuh"
+
+// Development probe bitmask (0 in every shipped build): skip the MMAs (1), the
+// epilogue's TMEM reads / math / stores (2), the converters' work (4), the
+// TMA loads (8); timing-only: 128B-aligned A plane starts (16), SBO = 128 (32).
+#ifndef LVSG_CONV_PROBE
+#define LVSG_CONV_PROBE 0
+#endif
 
 namespace lvsg {
 namespace {
@@ -47,15 +59,27 @@ constexpr int HALF_BYTES = NCH * LBO_A;         // hi (or lo) planes of one buff
 constexpr int PLANES_BYTES = 2 * HALF_BYTES;
 constexpr int W_ROWS = 64;                      // 32 hi + 32 lo
 constexpr int W_BYTES = 9 * NCH * W_ROWS * 16;  // 36864
-constexpr int OFF_RAW = W_BYTES;                // 2 raw TMA stages
-constexpr int OFF_PLANES = OFF_RAW + 2 * RAW_BYTES;
-constexpr int OFF_RMS = OFF_PLANES + 2 * PLANES_BYTES;
-constexpr int OFF_BAR = OFF_RMS + 192 * 4;
-constexpr int NBAR = 12;
+constexpr int NR = 3;   // raw TMA stages
+constexpr int NP = 2;   // converted hi/lo plane buffers
+constexpr int NA = 4;   // TMEM accumulators (64 columns each)
+constexpr int EPW = 2;  // epilogue warpgroups
+constexpr int NEW = 4 * EPW;                    // epilogue warps
+constexpr int SUB_ROWS = 4;                     // image rows per epilogue sub-box
+constexpr int SUB_BYTES = SUB_ROWS * TW * 128;  // [4][8][32] fp32 = 4096
+constexpr int OFF_OUT = 0;                      // 1024-aligned (128B swizzle)
+constexpr int OFF_RES = OFF_OUT + NEW * SUB_BYTES;
+constexpr int OFF_W = OFF_RES + NEW * SUB_BYTES;
+constexpr int OFF_RAW = OFF_W + W_BYTES;
+constexpr int OFF_PLANES = OFF_RAW + NR * RAW_BYTES;
+constexpr int OFF_SMALL = OFF_PLANES + NP * PLANES_BYTES;  // rms[192], bias[32], gain[32]
+constexpr int OFF_BAR = OFF_SMALL + 256 * 4;
+constexpr int NBAR = 2 * NR + 2 * NP + 2 * NA + NEW;
 constexpr int SMEM_BYTES = OFF_BAR + NBAR * 8 + 16;
-constexpr int NT = 320;  // 10 warps
-constexpr uint32_t TMEM_COLS = 128;
+constexpr int NT = 64 + 128 + 128 * EPW;
+constexpr uint32_t TMEM_COLS = 64 * NA;
 constexpr int NCONV = 128, NEPI = 128;
+static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
+static_assert((OFF_RES | OFF_W) % 1024 == 0, "swizzled staging alignment");
 
 struct TileCoord {
   int b, y0, x0;
@@ -76,21 +100,6 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c, int x,
-                                            int y, int b, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(x), "r"(y), "r"(b), "r"(tc::smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
 __device__ __forceinline__ void issue_tile(uint64_t ah0, uint64_t al0, uint64_t b0,
                                            uint32_t tmem_acc) {
   constexpr uint32_t id64 = tc::idesc_f16(128, 64);
@@ -100,7 +109,8 @@ __device__ __forceinline__ void issue_tile(uint64_t ah0, uint64_t al0, uint64_t 
     const int dy = tap / 3, dx = tap % 3;
 #pragma unroll
     for (int s = 0; s < NCH / 2; ++s) {
-      const uint64_t aoff = uint64_t((2 * s * LBO_A + (dy * HWD + dx) * 16) >> 4);
+      const uint64_t aoff = (LVSG_CONV_PROBE & 16) ? uint64_t(s * 2048 >> 4)
+                                                   : uint64_t((2 * s * LBO_A + (dy * HWD + dx) * 16) >> 4);
       const uint64_t boff = uint64_t(((tap * NCH + 2 * s) * W_ROWS * 16) >> 4);
       tc::mma_f16(tmem_acc, ah0 + aoff, b0 + boff, id64, (tap | s) != 0);
       tc::mma_f16(tmem_acc + 32, al0 + aoff, b0 + boff, id32, 1u);
@@ -108,22 +118,34 @@ __device__ __forceinline__ void issue_tile(uint64_t ah0, uint64_t al0, uint64_t 
   }
 }
 
+// 16-byte chunk c4 of row r in a 128B-swizzled [rows][128 B] staging buffer.
+__device__ __forceinline__ uint32_t swz(int r, int c4) {
+  return uint32_t(r * 128 + ((c4 ^ (r & 7)) << 4));
+}
+
 __global__ void __launch_bounds__(NT, 1)
-    conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap, const ConvArgs a, int num_tiles) {
+    conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap,
+                      const __grid_constant__ CUtensorMap omap,
+                      const __grid_constant__ CUtensorMap rmap, const ConvArgs a, int num_tiles) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __half* w_s = reinterpret_cast<__half*>(smem);
-  float* rms_s = reinterpret_cast<float*>(smem + OFF_RMS);
+  __half* w_s = reinterpret_cast<__half*>(smem + OFF_W);
+  float* rms_s = reinterpret_cast<float*>(smem + OFF_SMALL);
+  float* bias_s = rms_s + 192;
+  float* gain_s = bias_s + 32;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* raw_full = bars;          // [2] TMA bytes landed
-  uint64_t* raw_empty = bars + 2;      // [2] converters done reading raw
-  uint64_t* conv_full = bars + 4;      // [2] hi/lo planes ready
-  uint64_t* planes_empty = bars + 6;   // [2] MMAs done reading the planes
-  uint64_t* mma_done = bars + 8;       // [2] accumulator ready
-  uint64_t* acc_empty = bars + 10;     // [2] accumulator drained
+  uint64_t* raw_full = bars;                 // [NR] TMA bytes landed
+  uint64_t* raw_empty = raw_full + NR;       // [NR] converters done reading raw
+  uint64_t* conv_full = raw_empty + NR;      // [NP] hi/lo planes ready
+  uint64_t* planes_empty = conv_full + NP;   // [NP] MMAs done reading the planes
+  uint64_t* mma_done = planes_empty + NP;    // [NA] accumulator ready
+  uint64_t* acc_empty = mma_done + NA;       // [NA] accumulator drained
+  uint64_t* res_full = acc_empty + NA;       // [NEW] residual sub-box landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
 
   if (blockIdx.x >= num_tiles) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t sbase = tc::smem_u32(smem);
+  if (tid == 0 && (sbase & 1023u)) __trap();  // swizzle atoms need 1 KB alignment
 
   // weights: [tap][plane j][row n][8 halves], rows 0..31 = fp16 hi, 32..63 = lo'
   for (int e = tid; e < 9 * NCH * W_ROWS * 8; e += NT) {
@@ -134,16 +156,23 @@ __global__ void __launch_bounds__(NT, 1)
     tc::split_f16(__ldg(a.w + (co * w_cin_of(a) + a.w_ci0 + ci) * 9 + tap), h, l);
     w_s[e] = n < 32 ? h : l;
   }
+  if (tid < 32) bias_s[tid] = a.bias ? __ldg(a.bias + tid) : 0.f;
+  else if (tid < 64) gain_s[tid - 32] = a.gain ? __ldg(a.gain + tid - 32) : 1.f;
   tc::fence_proxy_async();
   if (tid == 0) {
-    for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&raw_full[b], 1);
-      tc::mbar_init(&raw_empty[b], NCONV);
-      tc::mbar_init(&conv_full[b], NCONV);
-      tc::mbar_init(&planes_empty[b], 1);
-      tc::mbar_init(&mma_done[b], 1);
-      tc::mbar_init(&acc_empty[b], NEPI);
+    for (int k = 0; k < NR; ++k) {
+      tc::mbar_init(&raw_full[k], 1);
+      tc::mbar_init(&raw_empty[k], NCONV);
     }
+    for (int k = 0; k < NP; ++k) {
+      tc::mbar_init(&conv_full[k], NCONV);
+      tc::mbar_init(&planes_empty[k], 1);
+    }
+    for (int k = 0; k < NA; ++k) {
+      tc::mbar_init(&mma_done[k], 1);
+      tc::mbar_init(&acc_empty[k], NEPI);
+    }
+    for (int k = 0; k < NEW; ++k) tc::mbar_init(&res_full[k], 1);
     tc::mbar_init_fence();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, TMEM_COLS);
@@ -151,56 +180,68 @@ __global__ void __launch_bounds__(NT, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t sbase = tc::smem_u32(smem);
 
   if (warp == 0) {
     // ---- TMA producer: one [18][10][32] box per tile into the raw ring ----
     if (lane == 0) {
       int i = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
-        const int r = i & 1;
-        if (i >= 2) tc::mbar_wait(&raw_empty[r], uint32_t(((i >> 1) - 1) & 1));
+        const int r = i % NR;
+        if (i >= NR) tc::mbar_wait(&raw_empty[r], uint32_t((i / NR - 1) & 1));
+        if ((LVSG_CONV_PROBE & 8)) {
+          tc::mbar_arrive(&raw_full[r]);
+          continue;
+        }
         const TileCoord tc_ = tile_coord(t, a.H, a.W);
-        mbar_expect_tx(&raw_full[r], RAW_BYTES);
-        tma_load_4d(sbase + OFF_RAW + r * RAW_BYTES, &xmap, 0, tc_.x0 - 1, tc_.y0 - 1, tc_.b,
-                    &raw_full[r]);
+        tc::mbar_expect_tx(&raw_full[r], RAW_BYTES);
+        tc::tma_load_4d(sbase + OFF_RAW + r * RAW_BYTES, &xmap, 0, tc_.x0 - 1, tc_.y0 - 1, tc_.b,
+                        &raw_full[r]);
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer ----
-    if (lane == 0) {
-      const uint64_t b0 = tc::smem_desc(sbase, W_ROWS * 16, 128);
-      int i = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
-        const int b = i & 1;
-        tc::mbar_wait(&conv_full[b], uint32_t((i >> 1) & 1));
-        if (i >= 2) tc::mbar_wait(&acc_empty[b], uint32_t(((i >> 1) - 1) & 1));
-        tc::fence_after();
-        const uint32_t hi = sbase + OFF_PLANES + b * PLANES_BYTES;
-        issue_tile(tc::smem_desc(hi, LBO_A, HWD * 16),
-                   tc::smem_desc(hi + HALF_BYTES, LBO_A, HWD * 16), b0, tmem + uint32_t(b * 64));
+    // ---- MMA issuer: the whole warp walks the ring, one elected lane issues ----
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);  // provably warp-uniform
+    const uint64_t b0 = tc::smem_desc(sbase + OFF_W, W_ROWS * 16, 128);
+    int i = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
+      const int b = i % NP, ac = i % NA;
+      tc::mbar_wait(&conv_full[b], uint32_t((i / NP) & 1));
+      if (i >= NA) tc::mbar_wait(&acc_empty[ac], uint32_t((i / NA - 1) & 1));
+      tc::fence_after();
+      const uint32_t hi = sbase + OFF_PLANES + b * PLANES_BYTES;
+      constexpr uint32_t sbo = (LVSG_CONV_PROBE & 32) ? 128 : HWD * 16;
+      constexpr uint32_t lbo = (LVSG_CONV_PROBE & 16) ? 2944 : LBO_A;
+      if (tc::elect_one()) {
+        if (!(LVSG_CONV_PROBE & 1))
+          issue_tile(tc::smem_desc(hi, lbo, sbo), tc::smem_desc(hi + HALF_BYTES, lbo, sbo), b0,
+                     tm + uint32_t(ac * 64));
         tc::commit(&planes_empty[b]);
-        tc::commit(&mma_done[b]);
+        tc::commit(&mma_done[ac]);
       }
+      __syncwarp();
     }
   } else if (warp < 6) {
     // ---- converters: raw pixel-major box -> fp16 hi / lo' K-major planes ----
     const int ct = tid - 64;
+    const int j = ct & 3;  // this thread's 8-channel plane (NCONV % 4 == 0)
+    float g8[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) g8[k] = gain_s[8 * j + k];
     int i = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
-      const int b = i & 1;
-      const float* raw = reinterpret_cast<const float*>(smem + OFF_RAW + b * RAW_BYTES);
-      float* hi = reinterpret_cast<float*>(smem + OFF_PLANES + b * PLANES_BYTES);
-      float* lo = reinterpret_cast<float*>(smem + OFF_PLANES + b * PLANES_BYTES + HALF_BYTES);
-      tc::mbar_wait(&raw_full[b], uint32_t((i >> 1) & 1));
+      const int r = i % NR, b = i % NP;
+      const float* raw = reinterpret_cast<const float*>(smem + OFF_RAW + r * RAW_BYTES);
+      uint8_t* hi = smem + OFF_PLANES + b * PLANES_BYTES;
+      uint8_t* lo = hi + HALF_BYTES;
+      tc::mbar_wait(&raw_full[r], uint32_t((i / NR) & 1));
       if (a.rinv) {
         // conv_mlp_residual's rms_norm over the pixel's 32 channels
         named_sync(1, NCONV);  // previous tile's scale reads are done
         for (int px = ct; px < HALO_PX; px += NCONV) {
           float ms = 0.f;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {  // all 32 channels
-            const float4 v = *reinterpret_cast<const float4*>(raw + px * 32 + 4 * j);
+          for (int q = 0; q < 8; ++q) {  // all 32 channels
+            const float4 v = *reinterpret_cast<const float4*>(raw + px * 32 + 4 * q);
             ms = fmaf(v.x, v.x, ms);
             ms = fmaf(v.y, v.y, ms);
             ms = fmaf(v.z, v.z, ms);
@@ -210,9 +251,9 @@ __global__ void __launch_bounds__(NT, 1)
         }
         named_sync(1, NCONV);
       }
-      if (i >= 2) tc::mbar_wait(&planes_empty[b], uint32_t(((i >> 1) - 1) & 1));
-      for (int e = ct; e < HALO_PX * NCH; e += NCONV) {
-        const int px = e >> 2, j = e & 3;
+      if (i >= NP) tc::mbar_wait(&planes_empty[b], uint32_t((i / NP - 1) & 1));
+      for (int e = ct; e < ((LVSG_CONV_PROBE & 4) ? 0 : HALO_PX * NCH); e += NCONV) {
+        const int px = e >> 2;
         float v[8];
         {
           const float4 v0 = *reinterpret_cast<const float4*>(raw + px * 32 + 8 * j);
@@ -221,64 +262,96 @@ __global__ void __launch_bounds__(NT, 1)
           v[4] = v1.x, v[5] = v1.y, v[6] = v1.z, v[7] = v1.w;
         }
         if (a.rinv) {
-          const float r = rms_s[px];
+          const float rr = rms_s[px];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) v[k] = fm(fm(v[k], r), __ldg(a.gain + 8 * j + k));
+          for (int k = 0; k < 8; ++k) v[k] = fm(fm(v[k], rr), g8[k]);
         }
         __align__(16) __half h[8], l[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) tc::split_f16(v[k], h[k], l[k]);
         const int off = j * LBO_A + px * 16;  // bytes
-        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(hi) + off) = *reinterpret_cast<uint4*>(h);
-        *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(lo) + off) = *reinterpret_cast<uint4*>(l);
+        *reinterpret_cast<uint4*>(hi + off) = *reinterpret_cast<uint4*>(h);
+        *reinterpret_cast<uint4*>(lo + off) = *reinterpret_cast<uint4*>(l);
       }
-      tc::mbar_arrive(&raw_empty[b]);
+      tc::mbar_arrive(&raw_empty[r]);
       tc::fence_proxy_async();
       tc::mbar_arrive(&conv_full[b]);
     }
   } else {
-    // ---- epilogue: TMEM -> bias / GELU / residual -> global ----
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
-    const int row = q * 32 + lane;
-    int i = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
-      const int b = i & 1;
-      tc::mbar_wait(&mma_done[b], uint32_t((i >> 1) & 1));
+    // ---- epilogue: TMEM -> bias / GELU / residual -> swizzled smem -> TMA store ----
+    const int ew = warp - 6;   // 0..NEW-1
+    const int g = ew >> 2;     // warpgroup: tiles i with i % EPW == g
+    const int q = warp & 3;    // TMEM lane quadrant this warp may access
+    const int sy = q * SUB_ROWS;  // sub-box row offset inside the tile
+    const uint32_t out_s = sbase + OFF_OUT + ew * SUB_BYTES;
+    const uint32_t res_s = sbase + OFF_RES + ew * SUB_BYTES;
+    uint8_t* out_p = smem + OFF_OUT + ew * SUB_BYTES;
+    const uint8_t* res_p = smem + OFF_RES + ew * SUB_BYTES;
+    const bool has_res = a.resid != nullptr;
+    const int step = EPW * gridDim.x;
+    uint32_t rph = 0;
+    auto sub_valid = [&](const TileCoord& c) { return c.y0 + sy < a.H; };
+    auto res_issue = [&](int t) {
+      const TileCoord c = tile_coord(t, a.H, a.W);
+      if (lane == 0 && sub_valid(c)) {
+        tc::mbar_expect_tx(&res_full[ew], SUB_BYTES);
+        tc::tma_load_4d(res_s, &rmap, 0, c.x0, c.y0 + sy, c.b, &res_full[ew]);
+      }
+    };
+    int t = blockIdx.x + g * gridDim.x;
+    if (has_res && t < num_tiles) res_issue(t);
+    for (int i = g; t < num_tiles; t += step, i += EPW) {
+      const int ac = i % NA;
+      tc::mbar_wait(&mma_done[ac], uint32_t((i / NA) & 1));
       tc::fence_after();
-      const uint32_t taddr = tmem + uint32_t(b * 64) + (uint32_t(q * 32) << 16);
+      if ((LVSG_CONV_PROBE & 2)) {
+        tc::mbar_arrive(&acc_empty[ac]);
+        continue;
+      }
+      const uint32_t taddr = tmem + uint32_t(ac * 64) + (uint32_t(q * 32) << 16);
       float d0[32], d1[32];
       tc::tmem_ld32(taddr, d0);
       tc::tmem_ld32(taddr + 32, d1);
       tc::fence_before();
-      tc::mbar_arrive(&acc_empty[b]);
+      tc::mbar_arrive(&acc_empty[ac]);
       const TileCoord tt = tile_coord(t, a.H, a.W);
-      const int y = tt.y0 + (row >> 3), x = tt.x0 + (row & 7);
-      if (y >= a.H || x >= a.W) continue;
-      const long long pix = (long long)y * a.W + x;
-      float* o = a.out + (long long)tt.b * a.out_bstride + pix * a.out_pstride;
-      const float* rs =
-          a.resid ? a.resid + (long long)tt.b * a.res_bstride + pix * a.res_pstride : nullptr;
+      const bool valid = sub_valid(tt);
 #pragma unroll
-      for (int c4 = 0; c4 < 8; ++c4) {
-        float v[4];
+      for (int c = 0; c < 32; ++c) {
+        float y_ = fmaf(d1[c], 1.0f / tc::kF16LoScale, d0[c]);
+        if (a.bias) y_ = fa(y_, bias_s[c]);
+        if (a.gelu) y_ = gelu_ref(y_);
+        d0[c] = y_;
+      }
+      if (has_res && valid) {
+        tc::mbar_wait(&res_full[ew], rph);
+        rph ^= 1u;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int c = 4 * c4 + k;
-          float y_ = fmaf(d1[c], 1.0f / tc::kF16LoScale, d0[c]);
-          if (a.bias) y_ = fa(y_, __ldg(a.bias + c));
-          if (a.gelu) y_ = gelu_ref(y_);
-          v[k] = y_;
+        for (int c4 = 0; c4 < 8; ++c4) {
+          const float4 r = *reinterpret_cast<const float4*>(res_p + swz(lane, c4));
+          d0[4 * c4 + 0] = fa(r.x, d0[4 * c4 + 0]);
+          d0[4 * c4 + 1] = fa(r.y, d0[4 * c4 + 1]);
+          d0[4 * c4 + 2] = fa(r.z, d0[4 * c4 + 2]);
+          d0[4 * c4 + 3] = fa(r.w, d0[4 * c4 + 3]);
         }
-        if (rs) {
-          const float4 r = *reinterpret_cast<const float4*>(rs + 4 * c4);
-          v[0] = fa(r.x, v[0]);
-          v[1] = fa(r.y, v[1]);
-          v[2] = fa(r.z, v[2]);
-          v[3] = fa(r.w, v[3]);
-        }
-        *reinterpret_cast<float4*>(o + 4 * c4) = make_float4(v[0], v[1], v[2], v[3]);
+        __syncwarp();
+      }
+      if (has_res && t + step < num_tiles) res_issue(t + step);
+      if (!valid) continue;
+      if (lane == 0) tc::bulk_wait_read<0>();  // previous store left the staging buffer
+      __syncwarp();
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4)
+        *reinterpret_cast<float4*>(out_p + swz(lane, c4)) =
+            make_float4(d0[4 * c4], d0[4 * c4 + 1], d0[4 * c4 + 2], d0[4 * c4 + 3]);
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        tc::tma_store_4d(&omap, out_s, 0, tt.x0, tt.y0 + sy, tt.b);
+        tc::bulk_commit();
       }
     }
+    if (lane == 0) tc::bulk_wait<0>();
   }
   tc::fence_before();
   __syncthreads();
@@ -302,11 +375,33 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 bool conv3x3_tc_supported(const ConvArgs& a) {
   if (a.Cin != 32 || a.Cout != 32 || a.nsrc != 1 || a.src[0].C != 32) return false;
   if (a.src[0].pstride % 4 || a.out_pstride % 4 || (a.resid && a.res_pstride % 4)) return false;
-  if (a.src[0].bstride % 4) return false;
+  if (a.src[0].bstride % 4 || a.out_bstride % 4 || (a.resid && a.res_bstride % 4)) return false;
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   return encode_fn() && al(a.src[0].ptr) && al(a.out) && (!a.resid || al(a.resid)) &&
          (!a.gain || al(a.gain));
 }
+
+namespace {
+
+// [B][H][W][pstride] fp32 (first 32 channels) as a 4-D tensor map.
+CUtensorMap make_map(const float* p, long long pstride, long long bstride, int W, int H, int B,
+                     cuuint32_t bw, cuuint32_t bh, CUtensorMapSwizzle swz) {
+  CUtensorMap map;
+  std::memset(&map, 0, sizeof(map));
+  cuuint64_t dims[4] = {32, cuuint64_t(W), cuuint64_t(H), cuuint64_t(B)};
+  cuuint64_t strides[3] = {cuuint64_t(pstride) * 4, cuuint64_t(pstride) * 4 * W,
+                           cuuint64_t(bstride) * 4};
+  cuuint32_t box[4] = {32, bw, bh, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(p),
+                                 dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed");
+  return map;
+}
+
+}  // namespace
 
 void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
   static bool attr = false;
@@ -314,18 +409,14 @@ void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(conv3x3_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr = true;
   }
-  // input [B, H, W, 32] (pixel stride pstride, batch stride bstride floats)
-  CUtensorMap map;
-  std::memset(&map, 0, sizeof(map));
   const ConvSrc& S = a.src[0];
-  cuuint64_t dims[4] = {32, cuuint64_t(a.W), cuuint64_t(a.H), cuuint64_t(a.B)};
-  cuuint64_t strides[3] = {cuuint64_t(S.pstride) * 4, cuuint64_t(S.pstride) * 4 * a.W,
-                           cuuint64_t(S.bstride) * 4};
-  cuuint32_t box[4] = {32, HWD, HHT, 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(S.ptr), dims, strides,
-              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUtensorMap xmap =
+      make_map(S.ptr, S.pstride, S.bstride, a.W, a.H, a.B, HWD, HHT, CU_TENSOR_MAP_SWIZZLE_NONE);
+  const CUtensorMap omap = make_map(a.out, a.out_pstride, a.out_bstride, a.W, a.H, a.B, TW,
+                                    SUB_ROWS, CU_TENSOR_MAP_SWIZZLE_128B);
+  const CUtensorMap rmap = a.resid ? make_map(a.resid, a.res_pstride, a.res_bstride, a.W, a.H, a.B,
+                                              TW, SUB_ROWS, CU_TENSOR_MAP_SWIZZLE_128B)
+                                   : omap;
   const int tiles = a.B * ((a.H + TH - 1) / TH) * ((a.W + TW - 1) / TW);
   static int sms = 0;
   if (!sms) {
@@ -334,7 +425,7 @@ void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int grid = tiles < sms ? tiles : sms;
-  conv3x3_tc_kernel<<<grid, NT, SMEM_BYTES, st>>>(map, a, tiles);
+  conv3x3_tc_kernel<<<grid, NT, SMEM_BYTES, st>>>(xmap, omap, rmap, a, tiles);
 }
 
 }  // namespace lvsg
