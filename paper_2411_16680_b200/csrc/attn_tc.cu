@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(NT, 2) attend_tc_kernel(float* V, const float*
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
   const uint32_t lane_base = uint32_t(warp * 32) << 16;
   const uint32_t tmem_s = tmem, tmem_o = tmem + 128;
 
@@ -164,9 +164,12 @@ __global__ void __launch_bounds__(NT, 2) attend_tc_kernel(float* V, const float*
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    if (tid == 0) {
-      mma3(tmem_s, ahi, alo, bqh, bql, S::BQ_LBO, id_s, false);
-      tc::commit(bar_s);
+    if (warp == 0) {  // whole warp, one elected lane issues (uniform descriptors)
+      if (tc::elect_one()) {
+        mma3(tmem_s, ahi, alo, bqh, bql, S::BQ_LBO, id_s, false);
+        tc::commit(bar_s);
+      }
+      __syncwarp();
     }
 
     // ---- scores: one pass over Δ, S_i re-read from TMEM per view ----
@@ -252,11 +255,15 @@ __global__ void __launch_bounds__(NT, 2) attend_tc_kernel(float* V, const float*
       tc::fence_before();
       __syncthreads();
       tc::fence_after();
-      if (tid == 0) {
-        const uint64_t boh = tc::smem_desc(sb + S::OFF_BO + (2 * i) * S::BO_BYTES, S::BO_LBO, 128);
-        const uint64_t bol = tc::smem_desc(sb + S::OFF_BO + (2 * i + 1) * S::BO_BYTES, S::BO_LBO, 128);
-        mma3(tmem_o, ahi, alo, boh, bol, S::BO_LBO, id_o, i > 0);
-        tc::commit(bar_o);
+      if (warp == 0) {
+        if (tc::elect_one()) {
+          const uint64_t boh = tc::smem_desc(sb + S::OFF_BO + (2 * i) * S::BO_BYTES, S::BO_LBO, 128);
+          const uint64_t bol =
+              tc::smem_desc(sb + S::OFF_BO + (2 * i + 1) * S::BO_BYTES, S::BO_LBO, 128);
+          mma3(tmem_o, ahi, alo, boh, bol, S::BO_LBO, id_o, i > 0);
+          tc::commit(bar_o);
+        }
+        __syncwarp();
       }
     }
     tc::mbar_wait(bar_o, ph_o);

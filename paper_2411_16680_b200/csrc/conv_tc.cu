@@ -73,7 +73,7 @@ constexpr int OFF_RAW = OFF_W + W_BYTES;
 constexpr int OFF_PLANES = OFF_RAW + NR * RAW_BYTES;
 constexpr int OFF_SMALL = OFF_PLANES + NP * PLANES_BYTES;  // rms[192], bias[32], gain[32]
 constexpr int OFF_BAR = OFF_SMALL + 256 * 4;
-constexpr int NBAR = 2 * NR + 2 * NP + 2 * NA + NEW;
+constexpr int NBAR = 2 * NR + 2 * NP + 2 * NA + NEW + 1;
 constexpr int SMEM_BYTES = OFF_BAR + NBAR * 8 + 16;
 constexpr int NT = 64 + 128 + 128 * EPW;
 constexpr uint32_t TMEM_COLS = 64 * NA;
@@ -94,10 +94,6 @@ __device__ __forceinline__ TileCoord tile_coord(int t, int H, int W) {
   c.y0 = (r / tx_n) * TH;
   c.x0 = (r % tx_n) * TW;
   return c;
-}
-
-__device__ __forceinline__ void named_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 __device__ __forceinline__ void issue_tile(uint64_t ah0, uint64_t al0, uint64_t b0,
@@ -128,7 +124,6 @@ __global__ void __launch_bounds__(NT, 1)
                       const __grid_constant__ CUtensorMap omap,
                       const __grid_constant__ CUtensorMap rmap, const ConvArgs a, int num_tiles) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __half* w_s = reinterpret_cast<__half*>(smem + OFF_W);
   float* rms_s = reinterpret_cast<float*>(smem + OFF_SMALL);
   float* bias_s = rms_s + 192;
   float* gain_s = bias_s + 32;
@@ -140,6 +135,7 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* mma_done = planes_empty + NP;    // [NA] accumulator ready
   uint64_t* acc_empty = mma_done + NA;       // [NA] accumulator drained
   uint64_t* res_full = acc_empty + NA;       // [NEW] residual sub-box landed
+  uint64_t* w_full = res_full + NEW;         // weight image landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
 
   if (blockIdx.x >= num_tiles) return;
@@ -147,15 +143,6 @@ __global__ void __launch_bounds__(NT, 1)
   const uint32_t sbase = tc::smem_u32(smem);
   if (tid == 0 && (sbase & 1023u)) __trap();  // swizzle atoms need 1 KB alignment
 
-  // weights: [tap][plane j][row n][8 halves], rows 0..31 = fp16 hi, 32..63 = lo'
-  for (int e = tid; e < 9 * NCH * W_ROWS * 8; e += NT) {
-    const int k8 = e & 7, n = (e >> 3) & 63, rest = e >> 9;
-    const int j = rest % NCH, tap = rest / NCH;
-    const int co = n & 31, ci = 8 * j + k8;
-    __half h, l;
-    tc::split_f16(__ldg(a.w + (co * w_cin_of(a) + a.w_ci0 + ci) * 9 + tap), h, l);
-    w_s[e] = n < 32 ? h : l;
-  }
   if (tid < 32) bias_s[tid] = a.bias ? __ldg(a.bias + tid) : 0.f;
   else if (tid < 64) gain_s[tid - 32] = a.gain ? __ldg(a.gain + tid - 32) : 1.f;
   tc::fence_proxy_async();
@@ -173,7 +160,10 @@ __global__ void __launch_bounds__(NT, 1)
       tc::mbar_init(&acc_empty[k], NEPI);
     }
     for (int k = 0; k < NEW; ++k) tc::mbar_init(&res_full[k], 1);
+    tc::mbar_init(w_full, 1);
     tc::mbar_init_fence();
+    tc::mbar_expect_tx(w_full, W_BYTES);
+    tc::bulk_load(sbase + OFF_W, a.wsplit, W_BYTES, w_full);
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, TMEM_COLS);
   tc::fence_before();
@@ -202,6 +192,7 @@ __global__ void __launch_bounds__(NT, 1)
     // ---- MMA issuer: the whole warp walks the ring, one elected lane issues ----
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);  // provably warp-uniform
     const uint64_t b0 = tc::smem_desc(sbase + OFF_W, W_ROWS * 16, 128);
+    tc::mbar_wait(w_full, 0);
     int i = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
       const int b = i % NP, ac = i % NA;
@@ -234,23 +225,6 @@ __global__ void __launch_bounds__(NT, 1)
       uint8_t* hi = smem + OFF_PLANES + b * PLANES_BYTES;
       uint8_t* lo = hi + HALF_BYTES;
       tc::mbar_wait(&raw_full[r], uint32_t((i / NR) & 1));
-      if (a.rinv) {
-        // conv_mlp_residual's rms_norm over the pixel's 32 channels
-        named_sync(1, NCONV);  // previous tile's scale reads are done
-        for (int px = ct; px < HALO_PX; px += NCONV) {
-          float ms = 0.f;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {  // all 32 channels
-            const float4 v = *reinterpret_cast<const float4*>(raw + px * 32 + 4 * q);
-            ms = fmaf(v.x, v.x, ms);
-            ms = fmaf(v.y, v.y, ms);
-            ms = fmaf(v.z, v.z, ms);
-            ms = fmaf(v.w, v.w, ms);
-          }
-          rms_s[px] = __fdiv_rn(1.0f, __fsqrt_rn(fa(__fdiv_rn(ms, 32.0f), 1e-6f)));
-        }
-        named_sync(1, NCONV);
-      }
       if (i >= NP) tc::mbar_wait(&planes_empty[b], uint32_t((i / NP - 1) & 1));
       for (int e = ct; e < ((LVSG_CONV_PROBE & 4) ? 0 : HALO_PX * NCH); e += NCONV) {
         const int px = e >> 2;
@@ -262,7 +236,15 @@ __global__ void __launch_bounds__(NT, 1)
           v[4] = v1.x, v[5] = v1.y, v[6] = v1.z, v[7] = v1.w;
         }
         if (a.rinv) {
-          const float rr = rms_s[px];
+          // conv_mlp_residual's rms_norm over the pixel's 32 channels: the
+          // pixel's 4 plane threads are adjacent lanes (quad reduction)
+          float ms = 0.f;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) ms = fmaf(v[k], v[k], ms);
+          const unsigned qm = __activemask();  // the loop tail cuts at a quad boundary
+          ms += __shfl_xor_sync(qm, ms, 1);
+          ms += __shfl_xor_sync(qm, ms, 2);
+          const float rr = __fdiv_rn(1.0f, __fsqrt_rn(fa(__fdiv_rn(ms, 32.0f), 1e-6f)));
 #pragma unroll
           for (int k = 0; k < 8; ++k) v[k] = fm(fm(v[k], rr), g8[k]);
         }
@@ -358,6 +340,19 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, TMEM_COLS);
 }
 
+// Weight image: [tap][plane j][row n][8 halves], rows 0..31 = fp16 hi of
+// w[co = n][w_ci0 + 8j + k8][tap], rows 32..63 = lo' (tc::split_f16).
+__global__ void conv3x3_tc_weights_kernel(const ConvArgs a, __half* out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 9 * NCH * W_ROWS * 8) return;
+  const int k8 = e & 7, n = (e >> 3) & 63, rest = e >> 9;
+  const int j = rest % NCH, tap = rest / NCH;
+  const int co = n & 31, ci = 8 * j + k8;
+  __half h, l;
+  tc::split_f16(__ldg(a.w + (co * w_cin_of(a) + a.w_ci0 + ci) * 9 + tap), h, l);
+  out[e] = n < 32 ? h : l;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* p = nullptr;
@@ -403,7 +398,14 @@ CUtensorMap make_map(const float* p, long long pstride, long long bstride, int W
 
 }  // namespace
 
+void conv3x3_tc_prepare(const ConvArgs& a, void* dst, cudaStream_t st) {
+  static_assert(kConvTcWeightBytes == W_BYTES, "weight image size");
+  conv3x3_tc_weights_kernel<<<(W_BYTES / 2 + 255) / 256, 256, 0, st>>>(a, static_cast<__half*>(dst));
+}
+
 void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
+  if (!a.wsplit || (reinterpret_cast<uintptr_t>(a.wsplit) & 15))
+    throw CudaError("conv3x3_tc: missing or misaligned weight image (conv3x3_tc_prepare)");
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(conv3x3_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);

@@ -39,6 +39,8 @@ struct ConvArgs {
   // input-channel slice of the weight tensor: w is [Cout, w_cin, 3, 3] and
   // this conv uses channels [w_ci0, w_ci0 + Cin) (0 = w_cin = Cin when unset)
   int w_cin, w_ci0;
+  // tensor-core weight image (conv3x3_tc_prepare) for conv3x3_tc; required there
+  const void* wsplit;
 };
 __host__ __device__ inline int w_cin_of(const ConvArgs& a) { return a.w_cin ? a.w_cin : a.Cin; }
 // Dispatches to the tcgen05 3xTF32 kernel when it applies (Cin = Cout = 32,
@@ -49,6 +51,11 @@ void conv3x3_simt(const ConvArgs& a, cudaStream_t st);
 bool conv3x3_uses_tc(const ConvArgs& a, int impl = 0);
 bool conv3x3_tc_supported(const ConvArgs& a);
 void conv3x3_tc(const ConvArgs& a, cudaStream_t st);
+// Bytes of one tensor-core weight image: the [tap][8-channel plane][64 rows]
+// fp16 hi / lo' split of w[:, w_ci0 : w_ci0 + 32] in the kernel's shared
+// memory layout, loaded by one bulk copy per CTA.
+constexpr size_t kConvTcWeightBytes = 9 * 4 * 64 * 16;
+void conv3x3_tc_prepare(const ConvArgs& a, void* dst, cudaStream_t st);
 
 // ---- elementwise / layout ------------------------------------------------
 void fill_rows(float* out, const float* row, int64_t rows, int C, cudaStream_t st);

@@ -18,6 +18,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "host.h"
@@ -174,6 +175,11 @@ struct lvsg_ctx {
   std::vector<const char*> prof_labels;
   std::vector<int> prof_counts;
   std::map<std::string, std::pair<double, int64_t>> prof_acc;
+
+  // tensor-core conv weight images (conv3x3_tc_prepare), keyed by weight
+  // tensor and input-channel slice; rebuilt whenever weights are (re)bound
+  std::map<std::tuple<const float*, int, int>, std::unique_ptr<lvsg::Buf>> wimg;
+  lvsg::Buf wimg_tmp;  // uncached image for the stage entry points
 };
 
 namespace lvsg {
@@ -213,6 +219,7 @@ void prof_collect(lvsg_ctx* c) {
 }
 
 void bind_weights(lvsg_ctx* c) {
+  c->wimg.clear();
   const Config& cfg = c->cfg;
   const int64_t C = cfg.channels, Ca = cfg.appear_channels();
   const float* cur = c->weights.p;
@@ -371,6 +378,31 @@ ConvArgs conv_args(int B, int H, int W, int Cin, int Cout, const float* w, const
   return a;
 }
 
+// conv3x3 through the dispatcher; a tensor-core launch gets its weight image
+// from the context cache (cached = true: weights bound to the context) or a
+// fresh one in scratch (stage entry points: arbitrary caller weights).
+void run_conv(lvsg_ctx* c, ConvArgs a, cudaStream_t st, int impl = 0, bool cached = true) {
+  if (conv3x3_uses_tc(a, impl)) {
+    const size_t nf = kConvTcWeightBytes / sizeof(float);
+    if (cached) {
+      auto key = std::make_tuple(a.w, w_cin_of(a), a.w_ci0);
+      auto it = c->wimg.find(key);
+      if (it == c->wimg.end()) {
+        auto buf = std::make_unique<Buf>();
+        buf->ensure(nf);
+        conv3x3_tc_prepare(a, buf->p, st);
+        it = c->wimg.emplace(key, std::move(buf)).first;
+      }
+      a.wsplit = it->second->p;
+    } else {
+      c->wimg_tmp.ensure(nf);
+      conv3x3_tc_prepare(a, c->wimg_tmp.p, st);
+      a.wsplit = c->wimg_tmp.p;
+    }
+  }
+  conv3x3(a, st, impl);
+}
+
 void add_src(ConvArgs& a, const float* p, int C, int H, int W) {
   a.src[a.nsrc] = ConvSrc{p, C, C, (long long)H * W * C};
   a.nsrc++;
@@ -384,13 +416,13 @@ void conv_residual(lvsg_ctx* c, const float* x, float* out, float* tmp, int B, i
   ConvArgs a = conv_args(B, H, W, C, C, p.w1, p.b1, tmp);
   add_src(a, x, C, H, W);
   a.gelu = 1;
-  conv3x3(a, c->stream);
+  run_conv(c, a, c->stream);
   ConvArgs b2 = conv_args(B, H, W, C, C, p.w2, p.b2, out);
   add_src(b2, tmp, C, H, W);
   b2.resid = x;
   b2.res_pstride = C;
   b2.res_bstride = (long long)H * W * C;
-  conv3x3(b2, c->stream);
+  run_conv(c, b2, c->stream);
   mark(c, "conv", 2);
 }
 
@@ -439,10 +471,10 @@ void update_cnn(lvsg_ctx* c, const StepW& sw, const ConvArgs& stem_in, int M, in
     }
   }
   if (split) {
-    for (const ConvArgs& p : parts) conv3x3(p, c->stream);
+    for (const ConvArgs& p : parts) run_conv(c, p, c->stream);
     mark(c, "conv", int(parts.size()));
   } else {
-    conv3x3(a, c->stream);
+    run_conv(c, a, c->stream);
     mark(c, "conv", 1);
   }
   conv_residual(c, c->uh.p, c->uh.p, c->ut.p, M, Hf, Wf, sw.r1);
@@ -467,13 +499,13 @@ void fusion(lvsg_ctx* c, float* V, int64_t L, int64_t H, int64_t W, const Fusion
       rms_rinv(V, c->rinv.p, P, C, c->stream);
       mark(c, "misc", 1);
     }
-    conv3x3(a, c->stream);
+    run_conv(c, a, c->stream);
     ConvArgs b = conv_args(int(L), int(H), int(W), C, C, m.w2, m.b2, V);
     add_src(b, c->t1.p, C, int(H), int(W));
     b.resid = V;
     b.res_pstride = C;
     b.res_bstride = (long long)H * W * C;
-    conv3x3(b, c->stream);
+    run_conv(c, b, c->stream);
     mark(c, "conv", 2);
   }
 }
@@ -568,7 +600,7 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
     ConvArgs a = conv_args(M, h, w, 3, C, W.stem_w, W.stem_b, c->enc_x.p);
     a.src[0] = ConvSrc{enc, 3, 3, (long long)h * w * 3};
     a.nsrc = 1;
-    conv3x3(a, st);
+    run_conv(c, a, st);
     mark(c, "conv", 1);
     const float* x = c->enc_x.p;
     for (int k = 0; k < K; ++k) {
@@ -1186,7 +1218,7 @@ lvsg_status lvsg_stage_conv3x3(lvsg_ctx* c, const float* x, const float* w, cons
     if (B < 1 || Cin < 1 || Cout < 1 || H < 1 || W < 1) throw DimError("conv3x3: bad shapes");
     ConvArgs a = conv_args(int(B), int(H), int(W), int(Cin), int(Cout), w, b, y);
     add_src(a, x, int(Cin), int(H), int(W));
-    conv3x3(a, c->stream, impl);
+    run_conv(c, a, c->stream, impl, false);
     sync_and_check(c);
   });
 }
@@ -1218,7 +1250,7 @@ lvsg_status lvsg_stage_conv3x3_fused(lvsg_ctx* c, const float* x, int64_t x_pstr
       a.gain = norm_gain;
       if (!conv3x3_uses_tc(a, impl)) rms_rinv(x, c->rinv.p, B * H * W, int(Cin), c->stream);
     }
-    conv3x3(a, c->stream, impl);
+    run_conv(c, a, c->stream, impl, false);
     sync_and_check(c);
   });
 }
