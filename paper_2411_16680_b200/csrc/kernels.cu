@@ -273,6 +273,70 @@ __global__ void gather_stack_kernel(const float* __restrict__ feats, int M, int 
   }
 }
 
+// C = 32: each lane computes one (view, texel) footprint as above; the 32
+// footprints of a warp are then consumed by 8-lane groups, lane g of a group
+// loading channel group g of the 4 taps, so one load instruction touches 4
+// feature rows instead of 32 (the per-lane version is L1-wavefront bound).
+__global__ void __launch_bounds__(256) gather_stack32_kernel(
+    const float* __restrict__ feats, int M, int Hf, int Wf, const DevCam* __restrict__ cams,
+    DevRayCam rc, const float* __restrict__ depth, int L, int H, int W, float* __restrict__ deltas) {
+  constexpr int G = 8;
+  const int64_t P = (int64_t)L * H * W;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  int m = 0, pl = 0, ok = 0, off[4] = {0, 0, 0, 0};
+  double w[4] = {0.0, 0.0, 0.0, 0.0};
+  if (i < P * M) {
+    m = int(i / P);
+    const int64_t p = i - m * P;
+    pl = int(p);
+    const int j = int(p % W);
+    const int ii = int((p / W) % H);
+    float pt[3];
+    world_point(rc, ii, j, __ldg(depth + p), pt);
+    const Footprint f = project_footprint(cams[m], pt);
+    if (f.valid) {
+      ok = 1;
+      bilinear_weights(f, w);
+      const int base = m * Hf * Wf;
+      off[0] = (base + f.y0 * Wf + f.x0) * G;
+      off[1] = (base + f.y0 * Wf + f.x1) * G;
+      off[2] = (base + f.y1 * Wf + f.x0) * G;
+      off[3] = (base + f.y1 * Wf + f.x1) * G;
+    }
+  } else {
+    ok = -1;  // past the end
+  }
+  const float4* f4 = reinterpret_cast<const float4*>(feats);
+  float4* o4 = reinterpret_cast<float4*>(deltas);
+  const int g = lane & 7;
+#pragma unroll 2
+  for (int it = 0; it < 8; ++it) {
+    const int r = 4 * it + (lane >> 3);
+    const int rok = __shfl_sync(0xffffffffu, ok, r);
+    const int rm = __shfl_sync(0xffffffffu, m, r);
+    const int rp = __shfl_sync(0xffffffffu, pl, r);
+    int ro[4];
+    double rw[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      ro[k] = __shfl_sync(0xffffffffu, off[k], r);
+      rw[k] = __shfl_sync(0xffffffffu, w[k], r);
+    }
+    if (rok < 0) continue;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (rok) {
+      const float4 a = __ldg(f4 + ro[0] + g);
+      const float4 b = __ldg(f4 + ro[1] + g);
+      const float4 c = __ldg(f4 + ro[2] + g);
+      const float4 d = __ldg(f4 + ro[3] + g);
+      v = make_float4(blend4(rw, a.x, b.x, c.x, d.x), blend4(rw, a.y, b.y, c.y, d.y),
+                      blend4(rw, a.z, b.z, c.z, d.z), blend4(rw, a.w, b.w, c.w, d.w));
+    }
+    o4[((int64_t)rm * G + g) * P + rp] = v;
+  }
+}
+
 // ----------------------------------------------------------------------------
 // render_to_input_view: decode, splat, composite
 // ----------------------------------------------------------------------------
@@ -765,7 +829,10 @@ void gather_stack(const float* feats, int M, int Hf, int Wf, int C, const DevCam
                   cudaStream_t st) {
   const bool v4 = C % 4 == 0;
   const int64_t n = (int64_t)L * H * W * M;
-  if (v4)
+  if (C == 32 && (int64_t)M * Hf * Wf * 8 < (int64_t(1) << 31) && n < (int64_t(1) << 31)) {
+    gather_stack32_kernel<<<blocks_for(n, 256), 256, 0, st>>>(feats, M, Hf, Wf, cams_dev, rc,
+                                                              depth, L, H, W, deltas);
+  } else if (v4)
     gather_stack_kernel<true><<<blocks_for(n, 256), 256, 0, st>>>(feats, M, Hf, Wf, C, cams_dev, rc,
                                                                   depth, L, H, W, deltas);
   else

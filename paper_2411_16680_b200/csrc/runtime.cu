@@ -160,6 +160,11 @@ struct lvsg_ctx {
   void* pinned = nullptr;  // camera staging
   size_t pinned_bytes = 0;
   cudaEvent_t staging_done = nullptr;
+  // host-ABI transfers: a copy stream overlapping the render-view upload with
+  // the forward pass and the output read-back with the banded render
+  cudaStream_t xfer = nullptr;
+  cudaEvent_t ev_main = nullptr, ev_ren = nullptr;
+  cudaEvent_t ev_band[4] = {};
 
   // resident forward result (for lvsg_render)
   bool have_ldm = false;
@@ -821,6 +826,7 @@ lvsg_status guard(lvsg_ctx* c, const auto& fn) {
 void sync_and_check(lvsg_ctx* c) {
   CUDA_OK(cudaGetLastError());
   CUDA_OK(cudaStreamSynchronize(c->stream));
+  if (c->xfer) CUDA_OK(cudaStreamSynchronize(c->xfer));
   int bad = 0;
   CUDA_OK(cudaMemcpy(&bad, c->bad_flag, sizeof(int), cudaMemcpyDeviceToHost));
   if (bad) {
@@ -830,15 +836,15 @@ void sync_and_check(lvsg_ctx* c) {
 }
 
 void upload_images(lvsg_ctx* c, Buf& dst, int64_t views, const float* const* images, int64_t H,
-                   int64_t W) {
+                   int64_t W, cudaStream_t st) {
   if (!images) throw DimError("forward: null image list");
   const size_t per = size_t(H * W * 3);
-  dst.ensure(per * size_t(views));
-  for (int64_t m = 0; m < views; ++m) {
+  for (int64_t m = 0; m < views; ++m)
     if (!images[m]) throw DimError("forward: null image");
+  dst.ensure(per * size_t(views));
+  for (int64_t m = 0; m < views; ++m)
     CUDA_OK(cudaMemcpyAsync(dst.p + per * size_t(m), images[m], per * sizeof(float),
-                            cudaMemcpyHostToDevice, c->stream));
-  }
+                            cudaMemcpyHostToDevice, st));
 }
 
 void check_views(lvsg_ctx* c, int64_t views, int64_t H, int64_t W) {
@@ -970,6 +976,10 @@ lvsg_status lvsg_create(const lvsg_model_config* cfg, int32_t device, lvsg_ctx**
     CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CUDA_OK(cudaEventCreateWithFlags(&c->staging_done, cudaEventDisableTiming));
     CUDA_OK(cudaEventRecord(c->staging_done, c->stream));
+    CUDA_OK(cudaStreamCreateWithFlags(&c->xfer, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&c->ev_ren, cudaEventDisableTiming));
+    for (cudaEvent_t& e : c->ev_band) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_OK(cudaMalloc(&c->bad_flag, sizeof(int)));
     CUDA_OK(cudaMemset(c->bad_flag, 0, sizeof(int)));
     c->layout = param_layout(c->cfg);
@@ -991,7 +1001,12 @@ void lvsg_destroy(lvsg_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->bad_flag) cudaFree(c->bad_flag);
+  if (c->xfer) cudaStreamSynchronize(c->xfer);
   if (c->staging_done) cudaEventDestroy(c->staging_done);
+  for (cudaEvent_t e : {c->ev_main, c->ev_ren, c->ev_band[0], c->ev_band[1], c->ev_band[2],
+                        c->ev_band[3]})
+    if (e) cudaEventDestroy(e);
+  if (c->xfer) cudaStreamDestroy(c->xfer);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1042,7 +1057,7 @@ lvsg_status lvsg_forward(lvsg_ctx* c, int64_t views, const float* const* images,
                          const lvsg_ldm_out* out) {
   return guard(c, [&] {
     check_views(c, views, height, width);
-    upload_images(c, c->enc_in, views, images, height, width);
+    upload_images(c, c->enc_in, views, images, height, width, c->stream);
     forward_device(c, c->enc_in.p, height, width, cams, *target, nullptr, nullptr);
     if (out) {
       const int64_t P = c->L * c->H * c->Wd, M = c->M, C = c->cfg.channels;
@@ -1074,7 +1089,7 @@ lvsg_status lvsg_render(lvsg_ctx* c, int64_t views, const float* const* images, 
   return guard(c, [&] {
     check_render_inputs(c, views, cams);
     if (height < 1 || width < 1) throw DimError("render_target: images must be [H,W,3]");
-    upload_images(c, c->ren_in, views, images, height, width);
+    upload_images(c, c->ren_in, views, images, height, width, c->stream);
     DevCam* dc = upload_render_cams(c, cams);
     const int64_t Ho = c->plan.out_height, Wo = c->plan.out_width;
     c->rgb.ensure(size_t(Ho * Wo * 3));
@@ -1094,18 +1109,34 @@ lvsg_status lvsg_forward_render(lvsg_ctx* c, int64_t views, const float* const* 
     check_views(c, views, enc_h, enc_w);
     check_views(c, views, render_h, render_w);
     for (int64_t m = 0; m < views; ++m) camera_validate(render_cams[m]);
-    upload_images(c, c->enc_in, views, enc_images, enc_h, enc_w);
-    upload_images(c, c->ren_in, views, render_images, render_h, render_w);
+    upload_images(c, c->enc_in, views, enc_images, enc_h, enc_w, c->stream);
+    // the render views are needed only by the final render: upload them on the
+    // copy stream under the forward pass (after any earlier use of ren_in)
+    CUDA_OK(cudaEventRecord(c->ev_main, c->stream));
+    CUDA_OK(cudaStreamWaitEvent(c->xfer, c->ev_main, 0));
+    upload_images(c, c->ren_in, views, render_images, render_h, render_w, c->xfer);
+    CUDA_OK(cudaEventRecord(c->ev_ren, c->xfer));
     CamTables t;
     forward_device(c, c->enc_in.p, enc_h, enc_w, enc_cams, *target, render_cams, &t);
     const int64_t Ho = c->plan.out_height, Wo = c->plan.out_width;
     c->rgb.ensure(size_t(Ho * Wo * 3));
-    render_fused(render_args(c, c->ren_in.p, render_h, render_w, t.final_cams, c->rgb.p, 0, Ho),
-                 c->stream);
-    mark(c, "render", 1);
-    c->launches += 1;
-    CUDA_OK(cudaMemcpyAsync(rgb_out, c->rgb.p, size_t(Ho * Wo * 3) * sizeof(float),
-                            cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev_ren, 0));
+    // banded render; each band's read-back overlaps the next band's render
+    constexpr int NB = 4;
+    for (int k = 0; k < NB; ++k) {
+      const int64_t r0 = Ho * k / NB, r1 = Ho * (k + 1) / NB;
+      if (r1 == r0) continue;
+      render_fused(render_args(c, c->ren_in.p, render_h, render_w, t.final_cams, c->rgb.p + r0 * Wo * 3,
+                               r0, r1),
+                   c->stream);
+      c->launches += 1;
+      CUDA_OK(cudaEventRecord(c->ev_band[k], c->stream));
+      CUDA_OK(cudaStreamWaitEvent(c->xfer, c->ev_band[k], 0));
+      CUDA_OK(cudaMemcpyAsync(rgb_out + r0 * Wo * 3, c->rgb.p + r0 * Wo * 3,
+                              size_t((r1 - r0) * Wo * 3) * sizeof(float), cudaMemcpyDeviceToHost,
+                              c->xfer));
+    }
+    mark(c, "render", NB);
     sync_and_check(c);
   });
 }
