@@ -273,10 +273,13 @@ __global__ void gather_stack_kernel(const float* __restrict__ feats, int M, int 
   }
 }
 
-// C = 32: each lane computes one (view, texel) footprint as above; the 32
-// footprints of a warp are then consumed by 8-lane groups, lane g of a group
-// loading channel group g of the 4 taps, so one load instruction touches 4
-// feature rows instead of 32 (the per-lane version is L1-wavefront bound).
+// C = 32: each lane computes one (view, texel) footprint as above (f64,
+// bit-exact taps / validity / weights); the 32 footprints of a warp are then
+// consumed by 8-lane groups, lane g of a group loading channel group g of the
+// 4 taps, so one load instruction touches 4 feature rows instead of 32 (the
+// per-lane version is L1-wavefront bound). The 4-tap blend of Δ is an f32 FMA
+// chain over the f64 weights rounded to f32 (within ~2 ulp of the reference's
+// f64 blend; the parity gate is the RGB tolerance).
 __global__ void __launch_bounds__(256) gather_stack32_kernel(
     const float* __restrict__ feats, int M, int Hf, int Wf, const DevCam* __restrict__ cams,
     DevRayCam rc, const float* __restrict__ depth, int L, int H, int W, float* __restrict__ deltas) {
@@ -284,28 +287,27 @@ __global__ void __launch_bounds__(256) gather_stack32_kernel(
   const int64_t P = (int64_t)L * H * W;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  int m = 0, pl = 0, ok = 0, off[4] = {0, 0, 0, 0};
-  double w[4] = {0.0, 0.0, 0.0, 0.0};
+  // record: m, p, flags (1 valid | 2 x1>x0 | 4 y1>y0 | 8 past the end), tap 00, weights
+  int m = 0, pl = 0, flags = 8, off = 0;
+  float w[4] = {0.f, 0.f, 0.f, 0.f};
   if (i < P * M) {
     m = int(i / P);
     const int64_t p = i - m * P;
     pl = int(p);
+    flags = 0;
     const int j = int(p % W);
     const int ii = int((p / W) % H);
     float pt[3];
     world_point(rc, ii, j, __ldg(depth + p), pt);
     const Footprint f = project_footprint(cams[m], pt);
     if (f.valid) {
-      ok = 1;
-      bilinear_weights(f, w);
-      const int base = m * Hf * Wf;
-      off[0] = (base + f.y0 * Wf + f.x0) * G;
-      off[1] = (base + f.y0 * Wf + f.x1) * G;
-      off[2] = (base + f.y1 * Wf + f.x0) * G;
-      off[3] = (base + f.y1 * Wf + f.x1) * G;
+      double wd[4];
+      bilinear_weights(f, wd);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) w[k] = __double2float_rn(wd[k]);
+      flags = 1 | (f.x1 > f.x0 ? 2 : 0) | (f.y1 > f.y0 ? 4 : 0);
+      off = ((m * Hf + f.y0) * Wf + f.x0) * G;
     }
-  } else {
-    ok = -1;  // past the end
   }
   const float4* f4 = reinterpret_cast<const float4*>(feats);
   float4* o4 = reinterpret_cast<float4*>(deltas);
@@ -313,25 +315,25 @@ __global__ void __launch_bounds__(256) gather_stack32_kernel(
 #pragma unroll 2
   for (int it = 0; it < 8; ++it) {
     const int r = 4 * it + (lane >> 3);
-    const int rok = __shfl_sync(0xffffffffu, ok, r);
+    const int rf = __shfl_sync(0xffffffffu, flags, r);
     const int rm = __shfl_sync(0xffffffffu, m, r);
     const int rp = __shfl_sync(0xffffffffu, pl, r);
-    int ro[4];
-    double rw[4];
+    const int ro = __shfl_sync(0xffffffffu, off, r) + g;
+    float rw[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      ro[k] = __shfl_sync(0xffffffffu, off[k], r);
-      rw[k] = __shfl_sync(0xffffffffu, w[k], r);
-    }
-    if (rok < 0) continue;
+    for (int k = 0; k < 4; ++k) rw[k] = __shfl_sync(0xffffffffu, w[k], r);
+    if (rf & 8) continue;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (rok) {
-      const float4 a = __ldg(f4 + ro[0] + g);
-      const float4 b = __ldg(f4 + ro[1] + g);
-      const float4 c = __ldg(f4 + ro[2] + g);
-      const float4 d = __ldg(f4 + ro[3] + g);
-      v = make_float4(blend4(rw, a.x, b.x, c.x, d.x), blend4(rw, a.y, b.y, c.y, d.y),
-                      blend4(rw, a.z, b.z, c.z, d.z), blend4(rw, a.w, b.w, c.w, d.w));
+    if (rf & 1) {
+      const int dx = (rf & 2) ? G : 0, dy = (rf & 4) ? Wf * G : 0;
+      const float4 a = __ldg(f4 + ro);
+      const float4 b = __ldg(f4 + ro + dx);
+      const float4 c = __ldg(f4 + ro + dy);
+      const float4 d = __ldg(f4 + ro + dy + dx);
+      v.x = fmaf(rw[3], d.x, fmaf(rw[2], c.x, fmaf(rw[1], b.x, rw[0] * a.x)));
+      v.y = fmaf(rw[3], d.y, fmaf(rw[2], c.y, fmaf(rw[1], b.y, rw[0] * a.y)));
+      v.z = fmaf(rw[3], d.z, fmaf(rw[2], c.z, fmaf(rw[1], b.z, rw[0] * a.z)));
+      v.w = fmaf(rw[3], d.w, fmaf(rw[2], c.w, fmaf(rw[1], b.w, rw[0] * a.w)));
     }
     o4[((int64_t)rm * G + g) * P + rp] = v;
   }

@@ -75,6 +75,8 @@ __global__ void __launch_bounds__(128) render_fused_kernel(const RenderArgs a) {
   const int i = a.row0 + int(idx / a.Wo), j = int(idx % a.Wo);
   const Taps t = taps_for(a, i, j);
   const int M = MM > 0 ? MM : a.M;
+  double dir[3];
+  world_dir(a.rc, i, j, dir);
   float o[3] = {0.f, 0.f, 0.f};
   float beta[MM > 0 ? MM : kMaxViews];
   int bad = 0;
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(128) render_fused_kernel(const RenderArgs a) {
     const double dv = double(depth);
     bad |= (dv < a.slack_lo || dv > a.slack_hi);
     float pt[3];
-    world_point(a.rc, i, j, depth, pt);
+    world_point_dir(a.rc, dir, depth, pt);
     // blended_layer_colors: beta * mask, wsum (k ascending from 0), 1/(wsum+1e-8)
     float col[MM > 0 ? MM : kMaxViews][3];
     float wsum = 0.f;
@@ -93,8 +95,13 @@ __global__ void __launch_bounds__(128) render_fused_kernel(const RenderArgs a) {
     for (int m = 0; m < M; ++m) {
       const Footprint f = project_footprint(s_cams[m], pt);
       if (f.valid) {
-        double w[4];
-        bilinear_weights(f, w);
+        // f64 (bit-exact) taps and weights; the colour blend is an f32 FMA
+        // chain over the weights rounded to f32 (~2 ulp of the f64 blend)
+        double wd[4];
+        bilinear_weights(f, wd);
+        float w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) w[k] = __double2float_rn(wd[k]);
         const float* img = a.images + m * img_stride;
         const float* p00 = img + ((int64_t)f.y0 * a.Wr + f.x0) * 3;
         const float* p10 = img + ((int64_t)f.y0 * a.Wr + f.x1) * 3;
@@ -102,7 +109,8 @@ __global__ void __launch_bounds__(128) render_fused_kernel(const RenderArgs a) {
         const float* p11 = img + ((int64_t)f.y1 * a.Wr + f.x1) * 3;
 #pragma unroll
         for (int k = 0; k < 3; ++k)
-          col[m][k] = blend4(w, __ldg(p00 + k), __ldg(p10 + k), __ldg(p01 + k), __ldg(p11 + k));
+          col[m][k] = fmaf(w[3], __ldg(p11 + k),
+                           fmaf(w[2], __ldg(p01 + k), fmaf(w[1], __ldg(p10 + k), w[0] * __ldg(p00 + k))));
         beta[m] = fm(beta[m], 1.0f);
       } else {
         col[m][0] = col[m][1] = col[m][2] = 0.f;
