@@ -29,7 +29,17 @@ constexpr int NT = 128;
 constexpr int NCH = C / 4;                 // 16-byte K chunks
 constexpr int A_LBO = TILE * 16;           // 2048
 constexpr int A_BYTES = NCH * A_LBO;       // 16 KB per plane
-constexpr uint32_t TMEM_COLS = 256;        // S: 32h <= 128 cols, O: 32 cols at 128
+// TMEM per CTA: S (32h columns) then O (32 columns), rounded up to a power of
+// two -- 64 / 128 / 256 columns for h = 1 / 2 / 4, which bounds how many
+// CTAs share an SM's 512 columns; registers set the rest (4 / 3 / 2 CTAs).
+template <int H>
+constexpr uint32_t tmem_cols() {
+  return H == 1 ? 64u : H == 2 ? 128u : 256u;
+}
+template <int H>
+constexpr int ctas_per_sm() {
+  return H == 1 ? 4 : H == 2 ? 3 : 2;
+}
 
 template <int H>
 struct Smem {
@@ -78,7 +88,7 @@ __device__ __forceinline__ void mma3(uint32_t tmem_d, uint64_t ahi, uint64_t alo
 }
 
 template <int H, int M>
-__global__ void __launch_bounds__(NT, 2) attend_tc_kernel(float* V, const float* __restrict__ D,
+__global__ void __launch_bounds__(NT, ctas_per_sm<H>()) attend_tc_kernel(float* V, const float* __restrict__ D,
                                                          int64_t P, const float* __restrict__ wq,
                                                          const float* __restrict__ wo,
                                                          const float* __restrict__ gain,
@@ -88,7 +98,7 @@ __global__ void __launch_bounds__(NT, 2) attend_tc_kernel(float* V, const float*
   uint64_t* bar_s = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
   uint64_t* bar_o = bar_s + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_s + 2);
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (blockIdx.x >= num_tiles) return;
 
   // resident weights, tf32 hi/lo, K-major:
@@ -118,14 +128,14 @@ __global__ void __launch_bounds__(NT, 2) attend_tc_kernel(float* V, const float*
     tc::mbar_init(bar_o, 1);
     tc::mbar_init_fence();
   }
-  if (warp == 0) tc::tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 0) tc::tmem_alloc(tmem_slot, tmem_cols<H>());
   tc::fence_proxy_async();
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
   const uint32_t lane_base = uint32_t(warp * 32) << 16;
-  const uint32_t tmem_s = tmem, tmem_o = tmem + 128;
+  const uint32_t tmem_s = tmem, tmem_o = tmem + 32 * H;
 
   const uint32_t sb = tc::smem_u32(smem);
   const uint64_t ahi = tc::smem_desc(sb + 0, A_LBO, 128);
@@ -184,14 +194,25 @@ __global__ void __launch_bounds__(NT, 2) attend_tc_kernel(float* V, const float*
 #pragma unroll
         for (int m = 0; m < M; ++m) w[i][m] = __fdiv_rn(1.0f, float(M));
     } else {
+      // software pipeline: view m+1's Δ row is in flight while view m's
+      // dot products run
+      float4 nx[C / 4];
+#pragma unroll
+      for (int g = 0; g < C / 4; ++g)
+        nx[g] = valid ? __ldg(d4 + int64_t(g) * P) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
       for (int m = 0; m < M; ++m) {
         float dm[C];
 #pragma unroll
         for (int g = 0; g < C / 4; ++g) {
-          const float4 t = valid ? __ldg(d4 + (int64_t(m) * (C / 4) + g) * P)
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+          const float4 t = nx[g];
           dm[4 * g] = t.x, dm[4 * g + 1] = t.y, dm[4 * g + 2] = t.z, dm[4 * g + 3] = t.w;
+        }
+        if (m + 1 < M) {
+#pragma unroll
+          for (int g = 0; g < C / 4; ++g)
+            nx[g] = valid ? __ldg(d4 + (int64_t(m + 1) * (C / 4) + g) * P)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int i = 0; i < H; ++i) {
@@ -286,7 +307,7 @@ __global__ void __launch_bounds__(NT, 2) attend_tc_kernel(float* V, const float*
     tc::fence_before();
     __syncthreads();  // A, S and O are reused by the next tile
   }
-  if (warp == 0) tc::tmem_dealloc(tmem, TMEM_COLS);
+  if (warp == 0) tc::tmem_dealloc(tmem, tmem_cols<H>());
 }
 
 template <int H, int M>
@@ -305,7 +326,8 @@ void launch(float* V, const float* D, int64_t P, const float* wq, const float* w
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int tiles = int((P + TILE - 1) / TILE);
-  const int grid = tiles < 2 * sms ? tiles : 2 * sms;
+  const int cap = ctas_per_sm<H>() * sms;
+  const int grid = tiles < cap ? tiles : cap;
   attend_tc_kernel<H, M><<<grid, NT, Smem<H>::BYTES, st>>>(V, D, P, wq, wo, gain, zero, tiles);
 }
 
