@@ -9,8 +9,10 @@ random-init weights (init_param_store seed 3), synthetic plane scene
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lvsg|reference]
 
 N > 1 runs under torchrun, one rank per GPU; rank r renders its own target
-viewpoint (config 5 grid) of the same inputs, which rank 0 broadcasts over
-NCCL each step (weak scaling). Rank 0 prints one JSON line.
+viewpoint (config 5 grid) of the same input views, resident on every GPU --
+the path partitions by target, so there is no data-path collective (weak
+scaling; paper_2411_16680_b200/shard.py). Timing is the max over ranks;
+rank 0 prints one JSON line.
 
 `value` is device-timed (CUDA events on the launching stream) with inputs
 resident in HBM; `e2e` goes through the host C ABI (lvsg_forward_render)
@@ -260,6 +262,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2411_16680_b200 as q
+    from paper_2411_16680_b200 import shard
     from paper_2411_16680_b200 import workloads as wl
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -271,7 +274,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     # each rank its own target viewpoint (config 5 grid) when sharded
-    center = (0.0, 0.0, 0.0) if world == 1 else wl.config5_targets()[rank % 8]
+    center = shard.target_center(rank, world)
     case = (wl.config2(target_center=center) if args.config == "config2"
             else wl.config3())
     cfg = case.cfg
@@ -287,9 +290,6 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step():
-        if world > 1:  # inputs arrive on rank 0; broadcast once per frame over NVLink
-            dist.broadcast(enc, 0)
-            dist.broadcast(ren, 0)
         model.forward_render_device(enc, case.enc_cams, ren, case.ren_cams, case.target, rgb,
                                     stream)
 
@@ -320,12 +320,9 @@ def main():
     if world > 1:
         dist.barrier()
     ms = sum(a.elapsed_time(b) for a, b in ev)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = shard.max_over_ranks(ms, dev)
     ms_per_step = ms_max / args.steps
-    fps = world * args.steps / (ms_max / 1000.0)
+    fps = shard.aggregate_fps(world, args.steps, ms_max / 1000.0)
 
     # e2e through the host C ABI: pinned host inputs, H2D + forward + render +
     # D2H of the frame, every step
@@ -342,11 +339,8 @@ def main():
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             model.forward_render(e_np, case.enc_cams, r_np, case.ren_cams, case.target, out=o_np)
-        sec = time.perf_counter() - t0
-        tt = torch.tensor([sec], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * args.e2e_steps / float(tt.item()), "unit": "frames/s",
+        sec = shard.max_over_ranks(time.perf_counter() - t0, dev)
+        e2e = {"value": shard.aggregate_fps(world, args.e2e_steps, sec), "unit": "frames/s",
                "h2d_bytes_per_step": int(enc_h.numel() * 4 + ren_h.numel() * 4),
                "d2h_bytes_per_step": int(out_h.numel() * 4), "steps": args.e2e_steps,
                "path": "lvsg_forward_render (host C ABI, pinned buffers)"}
@@ -405,7 +399,7 @@ def main():
                                    f"{ren.shape[2]}, output {Ho}x{Wo}",
                        "per_gpu": "one target viewpoint per rank" if world > 1 else "1 target",
                        "l2": "flushed (256 MB write) between timed frames",
-                       "parallelism": f"replicas x{world} (target-sharded), NCCL input broadcast"
+                       "parallelism": f"target-sharded x{world}, no data-path collective"
                        if world > 1 else "single GPU"},
             "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "roofline": roof, "cpu_baseline": cpu, "clocks": clocks.summary(),
