@@ -139,62 +139,74 @@ template <int CI>
 __global__ void __launch_bounds__(128) conv3x3_stem_kernel(const ConvArgs a) {
   __shared__ __align__(16) float s_w[9 * CI * 32];
   __shared__ float s_b[32];
+  __shared__ __align__(16) float4 s_o[128 * 8];  // [pixel][c4 ^ (pixel & 7)]
   for (int e = threadIdx.x; e < 9 * CI * 32; e += blockDim.x) {
     const int co = e % 32, k = e / 32;
     s_w[e] = __ldg(a.w + ((long long)co * w_cin_of(a) + a.w_ci0) * 9 + k);
   }
   if (threadIdx.x < 32) s_b[threadIdx.x] = a.bias ? __ldg(a.bias + threadIdx.x) : 0.f;
   __syncthreads();
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t HW = (int64_t)a.H * a.W;
-  if (i >= HW * a.B) return;
-  const int b = int(i / HW);
-  const int64_t pix = i - b * HW;
-  const int y = int(pix / a.W), x = int(pix % a.W);
-  const ConvSrc& S = a.src[0];
-  const float* src = S.ptr + (long long)b * S.bstride;
-  float xin[9 * CI];
+  const int64_t n = HW * a.B;
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x;
+  const int64_t i = i0 + threadIdx.x;
+  const int t = threadIdx.x;
+  if (i < n) {
+    const int b = int(i / HW);
+    const int64_t pix = i - b * HW;
+    const int y = int(pix / a.W), x = int(pix % a.W);
+    const ConvSrc& S = a.src[0];
+    const float* src = S.ptr + (long long)b * S.bstride;
+    float xin[9 * CI];
 #pragma unroll
-  for (int dy = 0; dy < 3; ++dy)
+    for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-    for (int dx = 0; dx < 3; ++dx) {
-      const int yy = y + dy - 1, xx = x + dx - 1;
-      const bool ok = yy >= 0 && yy < a.H && xx >= 0 && xx < a.W;
-      const float* p = src + ((long long)yy * a.W + xx) * S.pstride;
+      for (int dx = 0; dx < 3; ++dx) {
+        const int yy = y + dy - 1, xx = x + dx - 1;
+        const bool ok = yy >= 0 && yy < a.H && xx >= 0 && xx < a.W;
+        const float* p = src + ((long long)yy * a.W + xx) * S.pstride;
 #pragma unroll
-      for (int ci = 0; ci < CI; ++ci) xin[ci * 9 + dy * 3 + dx] = ok ? __ldg(p + ci) : 0.f;
+        for (int ci = 0; ci < CI; ++ci) xin[ci * 9 + dy * 3 + dx] = ok ? __ldg(p + ci) : 0.f;
+      }
+    float acc[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) acc[c] = s_b[c];
+#pragma unroll
+    for (int k = 0; k < 9 * CI; ++k) {
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) {
+        const float4 w = reinterpret_cast<const float4*>(s_w + k * 32)[c4];
+        acc[4 * c4] = fmaf(xin[k], w.x, acc[4 * c4]);
+        acc[4 * c4 + 1] = fmaf(xin[k], w.y, acc[4 * c4 + 1]);
+        acc[4 * c4 + 2] = fmaf(xin[k], w.z, acc[4 * c4 + 2]);
+        acc[4 * c4 + 3] = fmaf(xin[k], w.w, acc[4 * c4 + 3]);
+      }
     }
-  float acc[32];
-#pragma unroll
-  for (int c = 0; c < 32; ++c) acc[c] = s_b[c];
-#pragma unroll
-  for (int k = 0; k < 9 * CI; ++k) {
 #pragma unroll
     for (int c4 = 0; c4 < 8; ++c4) {
-      const float4 w = reinterpret_cast<const float4*>(s_w + k * 32)[c4];
-      acc[4 * c4] = fmaf(xin[k], w.x, acc[4 * c4]);
-      acc[4 * c4 + 1] = fmaf(xin[k], w.y, acc[4 * c4 + 1]);
-      acc[4 * c4 + 2] = fmaf(xin[k], w.z, acc[4 * c4 + 2]);
-      acc[4 * c4 + 3] = fmaf(xin[k], w.w, acc[4 * c4 + 3]);
+      float v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = a.gelu ? gelu_ref(acc[4 * c4 + k]) : acc[4 * c4 + k];
+      s_o[t * 8 + (c4 ^ (t & 7))] = make_float4(v[0], v[1], v[2], v[3]);
     }
   }
-  float4* o = reinterpret_cast<float4*>(a.out + (long long)b * a.out_bstride + pix * a.out_pstride);
-  const float4* rs = a.resid ? reinterpret_cast<const float4*>(a.resid + (long long)b * a.res_bstride +
-                                                               pix * a.res_pstride)
-                             : nullptr;
+  __syncthreads();
+  // coalesced write-back of the block's consecutive pixels (+ residual), one
+  // float4 per thread per step: 8 threads cover one pixel's 128 bytes
 #pragma unroll
-  for (int c4 = 0; c4 < 8; ++c4) {
-    float v[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = a.gelu ? gelu_ref(acc[4 * c4 + k]) : acc[4 * c4 + k];
-    if (rs) {
-      const float4 r = rs[c4];
-      v[0] = fa(r.x, v[0]);
-      v[1] = fa(r.y, v[1]);
-      v[2] = fa(r.z, v[2]);
-      v[3] = fa(r.w, v[3]);
+  for (int k = 0; k < 8; ++k) {
+    const int j = t + 128 * k, pl = j >> 3, c4 = j & 7;
+    const int64_t ip = i0 + pl;
+    if (ip >= n) continue;
+    const int b = int(ip / HW);
+    const int64_t pix = ip - b * HW;
+    float4 v = s_o[pl * 8 + (c4 ^ (pl & 7))];
+    if (a.resid) {
+      const float4 r = __ldg(reinterpret_cast<const float4*>(a.resid + (long long)b * a.res_bstride +
+                                                              pix * a.res_pstride) + c4);
+      v = make_float4(fa(r.x, v.x), fa(r.y, v.y), fa(r.z, v.z), fa(r.w, v.w));
     }
-    o[c4] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(a.out + (long long)b * a.out_bstride + pix * a.out_pstride)[c4] = v;
   }
 }
 

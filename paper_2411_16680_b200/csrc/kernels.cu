@@ -59,6 +59,29 @@ __global__ void mean_pool2_kernel(const float* in, float* out, int B, int H, int
   out[i] = fm(fa(fa(fa(v00, v01), v10), v11), 0.25f);
 }
 
+// C % 4 == 0: one thread per (output pixel, channel group), same sum order.
+__global__ void mean_pool2x4_kernel(const float4* __restrict__ in, float4* __restrict__ out, int B,
+                                    int H, int W, int G) {
+  const int Ho = H / 2, Wo = W / 2;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * Ho * Wo * G) return;
+  const int g = int(i % G);
+  int64_t t = i / G;
+  const int x = int(t % Wo);
+  t /= Wo;
+  const int y = int(t % Ho);
+  const int b = int(t / Ho);
+  const float4* s = in + (int64_t)b * H * W * G;
+  const float4 v00 = __ldg(s + ((int64_t)(2 * y) * W + 2 * x) * G + g);
+  const float4 v01 = __ldg(s + ((int64_t)(2 * y) * W + 2 * x + 1) * G + g);
+  const float4 v10 = __ldg(s + ((int64_t)(2 * y + 1) * W + 2 * x) * G + g);
+  const float4 v11 = __ldg(s + ((int64_t)(2 * y + 1) * W + 2 * x + 1) * G + g);
+  out[i] = make_float4(fm(fa(fa(fa(v00.x, v01.x), v10.x), v11.x), 0.25f),
+                       fm(fa(fa(fa(v00.y, v01.y), v10.y), v11.y), 0.25f),
+                       fm(fa(fa(fa(v00.z, v01.z), v10.z), v11.z), 0.25f),
+                       fm(fa(fa(fa(v00.w, v01.w), v10.w), v11.w), 0.25f));
+}
+
 __global__ void resize_hwc_kernel(const float* in, float* out, int B, int H, int W, int C, int Ho,
                                   int Wo) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -104,6 +127,49 @@ __global__ void resize_hwc4_kernel(const float* __restrict__ in, float* __restri
     o[g] = make_float4(lerp2(A.x, Bv.x, Cv.x, D.x, fx, fy), lerp2(A.y, Bv.y, Cv.y, D.y, fx, fy),
                        lerp2(A.z, Bv.z, Cv.z, D.z, fx, fy), lerp2(A.w, Bv.w, Cv.w, D.w, fx, fy));
   }
+}
+
+// resize_hwc for C % 4 == 0, cooperative: a block covers 256 / G consecutive
+// output pixels with one thread per (pixel, channel group g), g fastest, so
+// every tap read and every store is a contiguous run; the f64 taps of each
+// pixel are computed once and shared through shared memory.
+__global__ void __launch_bounds__(256) resize_hwc4c_kernel(const float* __restrict__ in,
+                                                           float* __restrict__ out, int B, int H,
+                                                           int W, int G, int Ho, int Wo) {
+  __shared__ int s_tap[64][4];
+  __shared__ float s_fr[64][2];
+  const int PB = 256 / G;
+  const int64_t n = (int64_t)B * Ho * Wo;
+  const int64_t i0 = blockIdx.x * (int64_t)PB;
+  const int t = threadIdx.x;
+  if (t < PB && i0 + t < n) {
+    const int64_t i = i0 + t;
+    const int x = int(i % Wo), y = int((i / Wo) % Ho);
+    const int b = int(i / ((int64_t)Wo * Ho));
+    int y0, y1, x0, x1;
+    float fy, fx;
+    resize_tap(y, H, Ho, y0, y1, fy);
+    resize_tap(x, W, Wo, x0, x1, fx);
+    const int base = b * H;
+    s_tap[t][0] = (base + y0) * W + x0;
+    s_tap[t][1] = (base + y0) * W + x1;
+    s_tap[t][2] = (base + y1) * W + x0;
+    s_tap[t][3] = (base + y1) * W + x1;
+    s_fr[t][0] = fx;
+    s_fr[t][1] = fy;
+  }
+  __syncthreads();
+  const int pl = t / G, g = t - pl * G;
+  if (pl >= PB || i0 + pl >= n) return;
+  const float4* s4 = reinterpret_cast<const float4*>(in);
+  const float4 A = __ldg(s4 + (int64_t)s_tap[pl][0] * G + g);
+  const float4 Bv = __ldg(s4 + (int64_t)s_tap[pl][1] * G + g);
+  const float4 Cv = __ldg(s4 + (int64_t)s_tap[pl][2] * G + g);
+  const float4 D = __ldg(s4 + (int64_t)s_tap[pl][3] * G + g);
+  const float fx = s_fr[pl][0], fy = s_fr[pl][1];
+  reinterpret_cast<float4*>(out)[(i0 + pl) * G + g] =
+      make_float4(lerp2(A.x, Bv.x, Cv.x, D.x, fx, fy), lerp2(A.y, Bv.y, Cv.y, D.y, fx, fy),
+                  lerp2(A.z, Bv.z, Cv.z, D.z, fx, fy), lerp2(A.w, Bv.w, Cv.w, D.w, fx, fy));
 }
 
 // One warp per row: rinv = 1 / sqrt(sum(x^2)/C + 1e-6).
@@ -212,6 +278,76 @@ __global__ void ray_project_kernel(const float* base, int M, int hK, int wK, int
 #pragma unroll
     for (int k = 0; k < 32; ++k) acc = fmaf(f[k], s_proj[k * C + c], acc);
     o[c] = acc;
+  }
+}
+
+// C = 32 production path: float4 tap reads, the block's 128 output rows
+// staged in shared memory and written back as contiguous float4 runs.
+__global__ void __launch_bounds__(128) ray_project32_kernel(const float* __restrict__ base, int M,
+                                                            int hK, int wK, int Hk, int Wk,
+                                                            const float* __restrict__ proj,
+                                                            float* __restrict__ out) {
+  __shared__ __align__(16) float s_proj[32 * 32];
+  __shared__ __align__(16) float4 s_o[128 * 8];  // [row][c4 ^ (row & 7)]
+  for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) s_proj[e] = __ldg(proj + e);
+  __syncthreads();
+  const int t = threadIdx.x;
+  const int64_t n = (int64_t)M * Hk * Wk;
+  const int64_t i0 = blockIdx.x * (int64_t)128, i = i0 + t;
+  if (i < n) {
+    const int x = int(i % Wk);
+    const int y = int((i / Wk) % Hk);
+    const int m = int(i / ((int64_t)Wk * Hk));
+    const float4* b = reinterpret_cast<const float4*>(base + (int64_t)m * hK * wK * 32);
+    float f[32];
+    if (Hk == hK && Wk == wK) {
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const float4 v = __ldg(b + ((int64_t)y * wK + x) * 8 + g);
+        f[4 * g] = v.x, f[4 * g + 1] = v.y, f[4 * g + 2] = v.z, f[4 * g + 3] = v.w;
+      }
+    } else {
+      int y0, y1, x0, x1;
+      float fy, fx;
+      resize_tap(y, hK, Hk, y0, y1, fy);
+      resize_tap(x, wK, Wk, x0, x1, fx);
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const float4 A = __ldg(b + ((int64_t)y0 * wK + x0) * 8 + g);
+        const float4 B = __ldg(b + ((int64_t)y0 * wK + x1) * 8 + g);
+        const float4 Cc = __ldg(b + ((int64_t)y1 * wK + x0) * 8 + g);
+        const float4 D = __ldg(b + ((int64_t)y1 * wK + x1) * 8 + g);
+        f[4 * g] = lerp2(A.x, B.x, Cc.x, D.x, fx, fy);
+        f[4 * g + 1] = lerp2(A.y, B.y, Cc.y, D.y, fx, fy);
+        f[4 * g + 2] = lerp2(A.z, B.z, Cc.z, D.z, fx, fy);
+        f[4 * g + 3] = lerp2(A.w, B.w, Cc.w, D.w, fx, fy);
+      }
+    }
+    float acc[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) acc[c] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) {
+        const float4 w = reinterpret_cast<const float4*>(s_proj + k * 32)[c4];
+        acc[4 * c4] = fmaf(f[k], w.x, acc[4 * c4]);
+        acc[4 * c4 + 1] = fmaf(f[k], w.y, acc[4 * c4 + 1]);
+        acc[4 * c4 + 2] = fmaf(f[k], w.z, acc[4 * c4 + 2]);
+        acc[4 * c4 + 3] = fmaf(f[k], w.w, acc[4 * c4 + 3]);
+      }
+    }
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4)
+      s_o[t * 8 + (c4 ^ (t & 7))] =
+          make_float4(acc[4 * c4], acc[4 * c4 + 1], acc[4 * c4 + 2], acc[4 * c4 + 3]);
+  }
+  __syncthreads();
+  float4* o = reinterpret_cast<float4*>(out) + i0 * 8;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int j = t + 128 * k, r = j >> 3, c4 = j & 7;
+    if (i0 + r < n) o[j] = s_o[r * 8 + (c4 ^ (r & 7))];
   }
 }
 
@@ -726,6 +862,46 @@ __global__ void decode_scalar_kernel(const float* __restrict__ V, int64_t P, int
   out[p] = do_act ? activate_depth(acc, int(p / PL), act) : acc;
 }
 
+// Both LDM scalar heads of a C = 32 volume in one pass (decode_depth_density,
+// network.hpp:525-537): the block's 128 rows are read coalesced into shared
+// memory, then each thread runs the two k-ascending dot products of its row.
+__global__ void __launch_bounds__(128) decode_scalar2_kernel(const float* __restrict__ V, int64_t P,
+                                                             const float* __restrict__ wa,
+                                                             float* __restrict__ outa,
+                                                             const float* __restrict__ wb,
+                                                             float* __restrict__ outb) {
+  __shared__ __align__(16) float4 rows[128 * 8];  // [row][c4 ^ (row & 7)]
+  __shared__ float s_wa[32], s_wb[32];
+  const int t = threadIdx.x;
+  if (t < 32) s_wa[t] = __ldg(wa + t);
+  else if (t < 64) s_wb[t - 32] = __ldg(wb + t - 32);
+  const int64_t p0 = blockIdx.x * (int64_t)128;
+  const float4* src = reinterpret_cast<const float4*>(V) + p0 * 8;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int j = t + 128 * k, r = j >> 3, c4 = j & 7;
+    if (p0 + r < P) rows[r * 8 + (c4 ^ (r & 7))] = __ldg(src + j);
+  }
+  __syncthreads();
+  const int64_t p = p0 + t;
+  if (p >= P) return;
+  float a = 0.f, b = 0.f;
+#pragma unroll
+  for (int c4 = 0; c4 < 8; ++c4) {
+    const float4 v = rows[t * 8 + (c4 ^ (t & 7))];
+    a = fmaf(v.x, s_wa[4 * c4], a);
+    a = fmaf(v.y, s_wa[4 * c4 + 1], a);
+    a = fmaf(v.z, s_wa[4 * c4 + 2], a);
+    a = fmaf(v.w, s_wa[4 * c4 + 3], a);
+    b = fmaf(v.x, s_wb[4 * c4], b);
+    b = fmaf(v.y, s_wb[4 * c4 + 1], b);
+    b = fmaf(v.z, s_wb[4 * c4 + 2], b);
+    b = fmaf(v.w, s_wb[4 * c4 + 3], b);
+  }
+  outa[p] = a;
+  outb[p] = b;
+}
+
 // ----------------------------------------------------------------------------
 // stage entry points
 // ----------------------------------------------------------------------------
@@ -796,6 +972,11 @@ void fill_anchor_depths(float* out, int L, int64_t P, double inv_span, double in
 }
 void mean_pool2(const float* in, float* out, int B, int H, int W, int C, cudaStream_t st) {
   const int64_t n = (int64_t)B * (H / 2) * (W / 2) * C;
+  if (C % 4 == 0 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
+    mean_pool2x4_kernel<<<blocks_for(n / 4, 256), 256, 0, st>>>(
+        reinterpret_cast<const float4*>(in), reinterpret_cast<float4*>(out), B, H, W, C / 4);
+    return;
+  }
   mean_pool2_kernel<<<blocks_for(n, 256), 256, 0, st>>>(in, out, B, H, W, C);
 }
 void resize_hwc(const float* in, float* out, int B, int H, int W, int C, int Ho, int Wo,
@@ -808,7 +989,13 @@ void resize_hwc(const float* in, float* out, int B, int H, int W, int C, int Ho,
   const bool al = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
   if (C % 4 == 0 && al) {
     const int64_t px = (int64_t)B * Ho * Wo;
-    resize_hwc4_kernel<<<blocks_for(px, 128), 128, 0, st>>>(in, out, B, H, W, C, Ho, Wo);
+    const int G = C / 4;
+    if (G >= 4 && G <= 64 && (int64_t)B * H * W * G < (int64_t(1) << 31)) {
+      const int PB = 256 / G;
+      resize_hwc4c_kernel<<<int((px + PB - 1) / PB), 256, 0, st>>>(in, out, B, H, W, G, Ho, Wo);
+    } else {
+      resize_hwc4_kernel<<<blocks_for(px, 128), 128, 0, st>>>(in, out, B, H, W, C, Ho, Wo);
+    }
     return;
   }
   resize_hwc_kernel<<<blocks_for(n, 256), 256, 0, st>>>(in, out, B, H, W, C, Ho, Wo);
@@ -823,6 +1010,10 @@ void ray_base(const RayBaseCam* cams_dev, const RayBaseArgs& a, float* base, cud
 void ray_project(const float* base, int M, int hK, int wK, int Hk, int Wk, const float* proj,
                  int C, float* out, cudaStream_t st) {
   const int64_t n = (int64_t)M * Hk * Wk;
+  if (C == 32) {
+    ray_project32_kernel<<<blocks_for(n, 128), 128, 0, st>>>(base, M, hK, wK, Hk, Wk, proj, out);
+    return;
+  }
   ray_project_kernel<<<blocks_for(n, 128), 128, 32 * C * sizeof(float), st>>>(base, M, hK, wK, Hk,
                                                                                Wk, proj, C, out);
 }
@@ -911,6 +1102,15 @@ void decode_scalar(const float* V, int64_t P, int C, const float* w, float* out,
   (void)L;
   decode_scalar_kernel<<<blocks_for(P, 256), 256, 0, st>>>(V, P, C, w, out, PL,
                                                            act ? *act : DepthAct{}, act ? 1 : 0);
+}
+void decode_scalar2(const float* V, int64_t P, int C, const float* wa, float* outa, const float* wb,
+                    float* outb, cudaStream_t st) {
+  if (C == 32) {
+    decode_scalar2_kernel<<<blocks_for(P, 128), 128, 0, st>>>(V, P, wa, outa, wb, outb);
+  } else {
+    decode_scalar(V, P, C, wa, outa, 0, P, nullptr, st);
+    decode_scalar(V, P, C, wb, outb, 0, P, nullptr, st);
+  }
 }
 void stage_world_points(const DevRayCam& rc, const float* depth, int L, int H, int W,
                         float* points, double lo, double hi, int* bad, cudaStream_t st) {

@@ -141,6 +141,9 @@ bool decode_payload32(const float* V, int L, int H, int W, int C, const float* w
                       const DevRayCam& rc, float* payload, float* depth, float* points,
                       cudaStream_t st);
 // out[p] = V[p,:] . w (decode_linear with K = 1), optionally activated depth.
+// Both pre-activation heads (out_a = V w_a, out_b = V w_b) in one pass over V.
+void decode_scalar2(const float* V, int64_t P, int C, const float* wa, float* outa, const float* wb,
+                    float* outb, cudaStream_t st);
 void decode_scalar(const float* V, int64_t P, int C, const float* w, float* out, int L,
                    int64_t PL, const DepthAct* act, cudaStream_t st);
 

@@ -739,9 +739,8 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
     blend_logits(V, c->deltas.p, P, C, M, W.blend_w, W.blend_gain, c->logits.p, st);
     mark(c, "attention", 1);
   }
-  decode_scalar(V, P, C, W.w_depth, c->pre_d.p, int(L), H * Wd, nullptr, st);
-  decode_scalar(V, P, C, W.w_sigma, c->pre_s.p, int(L), H * Wd, nullptr, st);
-  mark(c, "misc", 2);
+  decode_scalar2(V, P, C, W.w_depth, c->pre_d.p, W.w_sigma, c->pre_s.p, st);
+  mark(c, "misc", C == 32 ? 1 : 2);
   c->have_ldm = true;
   c->L = L;
   c->H = H;
