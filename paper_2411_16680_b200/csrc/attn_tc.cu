@@ -2,24 +2,29 @@
 // sm_100a tensor core, C = 32, h <= 4 heads, M views:
 //
 //   n      = rms_norm(V) * g                     (SIMT, thread = texel)
-//   S      = n [Wq_0 | ... | Wq_{h-1}]           tcgen05.mma kind::tf32, 3xTF32,
-//                                                M=128 texels, N=32h, TMEM
+//   S      = n [Wq_0 | ... | Wq_{h-1}]           tcgen05.mma kind::f16, 3-term
+//                                                fp16 split, M=128, TMEM
 //   l_im   = <S_i, Δ_m> / sqrt(C); w = softmax_m; head_i = sum_m w_im Δ_m
-//   O      = sum_i head_i Wo_i                   tcgen05.mma, 3xTF32, TMEM
+//   O      = sum_i head_i Wo_i                   tcgen05.mma kind::f16, split
 //   V     += O
 //
+// The projections use the conv's fp16 split (tc::split_f16, same ~2^-22
+// relative error per product as 3xTF32): per 16-channel K step
+//   MMA1 N=64h: D[:, 0:64h] (+)= Xh * [Wh ; Wl']^T,   MMA2 N=32h: D[:, 32h:64h] += Xl' * Wh^T
+// and S = D[:, c] + 2^-11 D[:, 32h + c] (likewise O with h = 1).
+//
 // Persistent warp-specialised CTA, one per SM, 128-texel tiles:
-//   w0     TMA producer: the V tile (128B-swizzled, 2 buffers) and, per view,
-//          the tile's Δ slice [8 channel groups][128 texels][16 B] (8 bulk
-//          copies of 2 KB from the view-major SoA Δ[m][g][p][4]) into an NS-deep ring --
-//          twice per tile (scores, then mix; the second read hits L2)
+//   w0     TMA producer: V tiles (128B-swizzled, 4 buffers, one tile ahead of
+//          the Δ slices) and, per view, the tile's Δ slice [8 channel groups]
+//          [128 texels][16 B] (8 bulk copies of 2 KB from the view-major SoA
+//          Δ[m][g][p][4]) into an NS-deep ring -- twice per tile (scores, then
+//          mix; the second read hits L2)
 //   w1     MMA issuer (one elected lane; warp-uniform descriptors)
-//   w2-5   consumers, thread <-> texel row <-> TMEM lane: rms-norm, stage n,
-//          S for every head held in registers through the score pass, softmax,
-//          one mix pass for all heads, stage each head for O (two A buffers),
-//          V + O back through the swizzled tile and one TMA store
-// Weights are split into tf32 hi/lo once per CTA and stay resident in the
-// K-major interleave layout.
+//   w2-5   consumers, thread <-> texel row <-> TMEM lane, software-pipelined
+//          across tiles so neither MMA round trip is on the critical path:
+//            scores(i) [S(i) requested an iteration earlier] -> finish(i-1)
+//            [O(i-1) + V, TMA store] -> stage n(i+1) -> mix(i) -> stage heads(i)
+// Weights are split once per CTA and stay resident (K-major interleave).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -37,69 +42,76 @@ constexpr int C = 32;
 constexpr int TILE = 128;
 constexpr int NT = 192;                    // 6 warps
 constexpr int NCONS = 128;                 // consumer threads
-constexpr int NCH = C / 4;                 // 16-byte K chunks
-constexpr int A_LBO = TILE * 16;           // 2048
-constexpr int A_PLANE = NCH * A_LBO;       // 16 KB per tf32 plane
-constexpr int A_BYTES = 2 * A_PLANE;       // hi + lo
+constexpr int NJ = C / 8;                  // 8-channel fp16 K chunks
+constexpr int NG = C / 4;                  // 4-channel Δ groups
+constexpr int A_LBO = TILE * 16;           // 2 KB: one 8-channel plane of 128 rows
+constexpr int A_HALF = NJ * A_LBO;         // 8 KB: hi (or lo') planes
+constexpr int A_BYTES = 2 * A_HALF;        // 16 KB per staging buffer
 constexpr int V_BYTES = TILE * C * 4;      // 16 KB
-constexpr int D_BYTES = NCH * TILE * 16;   // one view slice, 16 KB
+constexpr int D_BYTES = NG * TILE * 16;    // one view slice, 16 KB
+constexpr int NV = 4;                      // V tile buffers
 
 template <int H>
-constexpr uint32_t tmem_cols() {  // S (32h columns) + O (32 columns), power of two
-  return H == 1 ? 64u : H == 2 ? 128u : 256u;
+constexpr uint32_t tmem_cols() {  // S (64h columns) + O (64 columns), power of two
+  return H == 1 ? 128u : H == 2 ? 256u : 512u;
 }
 
 template <int H>
 struct Smem {
-  static constexpr int BQ_LBO = 32 * H * 16;
-  static constexpr int BQ_BYTES = NCH * BQ_LBO;  // one plane
-  static constexpr int BO_LBO = 32 * 16;
-  static constexpr int BO_BYTES = NCH * BO_LBO;  // one head, one plane
-  static constexpr int OFF_V = 0;                // 2 buffers, 1 KB aligned (swizzle)
-  static constexpr int OFF_A = OFF_V + 2 * V_BYTES;
-  static constexpr int OFF_BQH = OFF_A + 2 * A_BYTES;
-  static constexpr int OFF_BQL = OFF_BQH + BQ_BYTES;
-  static constexpr int OFF_BO = OFF_BQL + BQ_BYTES;  // [head][hi|lo]
-  static constexpr int OFF_D = OFF_BO + 2 * H * BO_BYTES;
+  static constexpr int BQ_ROWS = 64 * H;            // [Wq hi ; Wq lo'] rows
+  static constexpr int BQ_LBO = BQ_ROWS * 16;
+  static constexpr int BQ_BYTES = NJ * BQ_LBO;
+  static constexpr int BO_LBO = 64 * 16;            // per head [Wo hi ; Wo lo']
+  static constexpr int BO_BYTES = NJ * BO_LBO;
+  static constexpr int OFF_V = 0;                   // NV buffers, 1 KB aligned (swizzle)
+  static constexpr int OFF_A = OFF_V + NV * V_BYTES;
+  static constexpr int OFF_BQ = OFF_A + 2 * A_BYTES;
+  static constexpr int OFF_BO = OFF_BQ + BQ_BYTES;
+  static constexpr int OFF_D = OFF_BO + H * BO_BYTES;
   static constexpr int BUDGET = 227 * 1024 - 512;
   static constexpr int NS = (BUDGET - OFF_D) / D_BYTES > 8 ? 8 : (BUDGET - OFF_D) / D_BYTES;
   static constexpr int OFF_BAR = OFF_D + NS * D_BYTES;
-  // bars: v_full[2] v_empty[2] d_full[NS] d_empty[NS] a_full[2] a_free[2] s_done o_done
-  static constexpr int NBAR = 4 + 2 * NS + 4 + 2;
+  // bars: v_full[NV] v_empty[NV] d_full[NS] d_empty[NS] a_full[2] a_free[2] s_done o_done
+  static constexpr int NBAR = 2 * NV + 2 * NS + 4 + 2;
   static constexpr int BYTES = OFF_BAR + NBAR * 8 + 16;
-  static_assert(NS >= 2, "shared memory budget");
+  static_assert(NS >= 3, "shared memory budget");
 };
 
-__device__ __forceinline__ void put_split(float* hi, float* lo, int off, float4 v) {
-  float4 h, l;
-  tc::split_tf32(v.x, h.x, l.x);
-  tc::split_tf32(v.y, h.y, l.y);
-  tc::split_tf32(v.z, h.z, l.z);
-  tc::split_tf32(v.w, h.w, l.w);
-  *reinterpret_cast<float4*>(hi + off) = h;
-  *reinterpret_cast<float4*>(lo + off) = l;
-}
-
-// A[j][row][4] <- x[32] of this thread's row, split into tf32 hi/lo planes.
+// A[j][row][8 halves] (hi) and A[4 + j][row] (lo') <- x[32] of this row.
 __device__ __forceinline__ void stage_row(uint8_t* a, int row, const float* x) {
-  float* hi = reinterpret_cast<float*>(a);
-  float* lo = reinterpret_cast<float*>(a + A_PLANE);
 #pragma unroll
-  for (int j = 0; j < NCH; ++j)
-    put_split(hi, lo, (j * A_LBO) / 4 + row * 4,
-              make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]));
+  for (int j = 0; j < NJ; ++j) {
+    __align__(16) __half h[8], l[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tc::split_f16(x[8 * j + k], h[k], l[k]);
+    *reinterpret_cast<uint4*>(a + j * A_LBO + row * 16) = *reinterpret_cast<uint4*>(h);
+    *reinterpret_cast<uint4*>(a + A_HALF + j * A_LBO + row * 16) = *reinterpret_cast<uint4*>(l);
+  }
 }
 
-// D (N columns) (+)= Ahi*Bhi + Ahi*Blo + Alo*Bhi over K = 32.
-__device__ __forceinline__ void mma3(uint32_t tmem_d, uint64_t ahi, uint64_t alo, uint64_t bhi,
-                                     uint64_t blo, uint32_t bstep, uint32_t idesc, bool acc0) {
+// B rows (K-major interleave): w(n, k) for n < N, hi in rows [0, N), lo' in [N, 2N).
+template <typename F>
+__device__ __forceinline__ void stage_weights(uint8_t* b, int N, int tid, F w) {
+  __half* bh = reinterpret_cast<__half*>(b);
+  for (int e = tid; e < NJ * N * 8; e += NT) {
+    const int k8 = e & 7, n = (e >> 3) % N, j = (e >> 3) / N;
+    __half hi, lo;
+    tc::split_f16(w(n, 8 * j + k8), hi, lo);
+    bh[(j * 2 * N + n) * 8 + k8] = hi;
+    bh[(j * 2 * N + N + n) * 8 + k8] = lo;
+  }
+}
+
+// D (+)= A * B over K = 32: MMA1 N = 2n into d, MMA2 N = n (lo' x hi) into d + n.
+__device__ __forceinline__ void mma_split(uint32_t d, uint32_t a, uint32_t b, int n, bool acc0) {
+  const uint32_t id1 = tc::idesc_f16(128, 2 * n), id2 = tc::idesc_f16(128, n);
+  const uint64_t ah = tc::smem_desc(a, A_LBO, 128), al = tc::smem_desc(a + A_HALF, A_LBO, 128);
+  const uint64_t bd = tc::smem_desc(b, 2 * n * 16, 128);
 #pragma unroll
-  for (int s = 0; s < NCH / 2; ++s) {
-    const uint64_t ao = uint64_t((2 * s * A_LBO) >> 4);
-    const uint64_t bo = uint64_t((2 * s * bstep) >> 4);
-    tc::mma_tf32(tmem_d, ahi + ao, bhi + bo, idesc, (acc0 || s > 0) ? 1u : 0u);
-    tc::mma_tf32(tmem_d, ahi + ao, blo + bo, idesc, 1u);
-    tc::mma_tf32(tmem_d, alo + ao, bhi + bo, idesc, 1u);
+  for (int s = 0; s < NJ / 2; ++s) {
+    const uint64_t ao = uint64_t((2 * s * A_LBO) >> 4), bo = uint64_t((2 * s * 2 * n * 16) >> 4);
+    tc::mma_f16(d, ah + ao, bd + bo, id1, (acc0 || s > 0) ? 1u : 0u);
+    tc::mma_f16(d + uint32_t(n), al + ao, bd + bo, id2, 1u);
   }
 }
 
@@ -135,9 +147,9 @@ __global__ void __launch_bounds__(NT, 1)
   constexpr int NS = S::NS;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
-  uint64_t* v_full = bars;            // [2] V tile landed
-  uint64_t* v_empty = bars + 2;       // [2] V tile stored back (buffer free)
-  uint64_t* d_full = bars + 4;        // [NS] Δ slice landed
+  uint64_t* v_full = bars;            // [NV] V tile landed
+  uint64_t* v_empty = bars + NV;      // [NV] V tile stored back (buffer free)
+  uint64_t* d_full = bars + 2 * NV;   // [NS] Δ slice landed
   uint64_t* d_empty = d_full + NS;    // [NS] consumers done with the slice
   uint64_t* a_full = d_empty + NS;    // [2] A operand staged
   uint64_t* a_free = a_full + 2;      // [2] MMAs done reading A
@@ -149,33 +161,21 @@ __global__ void __launch_bounds__(NT, 1)
   const uint32_t sb = tc::smem_u32(smem);
   if (tid == 0 && (sb & 1023u)) __trap();  // swizzle atoms need 1 KB alignment
   const int passes = zero_scores ? 1 : 2;
+  const int ntl = (num_tiles - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x);  // my tiles
+  auto tile_of = [&](int i) { return int(blockIdx.x) + i * int(gridDim.x); };
 
-  // resident weights, tf32 hi/lo, K-major:
-  //   Bq[j][n][4]  n = 32*i + c : Wq_i[4j..4j+3][c]
-  //   Bo[i][j][n][4]            : Wo[32i + 4j..][n]
-  {
-    float* bqh = reinterpret_cast<float*>(smem + S::OFF_BQH);
-    float* bql = reinterpret_cast<float*>(smem + S::OFF_BQL);
-    for (int e = tid; e < NCH * 32 * H; e += NT) {
-      const int n = e % (32 * H), j = e / (32 * H);
-      const int i = n / 32, c = n % 32;
-      const float* src = wq + (i * C + 4 * j) * C + c;
-      put_split(bqh, bql, (j * S::BQ_LBO) / 4 + n * 4,
-                make_float4(__ldg(src), __ldg(src + C), __ldg(src + 2 * C), __ldg(src + 3 * C)));
-    }
-    for (int e = tid; e < H * NCH * 32; e += NT) {
-      const int n = e % 32, j = (e / 32) % NCH, i = e / (32 * NCH);
-      float* bh = reinterpret_cast<float*>(smem + S::OFF_BO + (2 * i) * S::BO_BYTES);
-      float* bl = reinterpret_cast<float*>(smem + S::OFF_BO + (2 * i + 1) * S::BO_BYTES);
-      const float* src = wo + (i * C + 4 * j) * C + n;
-      put_split(bh, bl, (j * S::BO_LBO) / 4 + n * 4,
-                make_float4(__ldg(src), __ldg(src + C), __ldg(src + 2 * C), __ldg(src + 3 * C)));
-    }
-  }
+  // resident weights: Bq rows n = 32*i + c -> Wq_i[k][c]; Bo_i rows n -> Wo[32i + k][n]
+  stage_weights(smem + S::OFF_BQ, 32 * H, tid,
+                [&](int n, int k) { return __ldg(wq + ((n >> 5) * C + k) * C + (n & 31)); });
+  for (int h = 0; h < H; ++h)
+    stage_weights(smem + S::OFF_BO + h * S::BO_BYTES, 32, tid,
+                  [&](int n, int k) { return __ldg(wo + (h * C + k) * C + n); });
   if (tid == 0) {
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < NV; ++k) {
       tc::mbar_init(&v_full[k], 1);
       tc::mbar_init(&v_empty[k], 1);
+    }
+    for (int k = 0; k < 2; ++k) {
       tc::mbar_init(&a_full[k], NCONS);
       tc::mbar_init(&a_free[k], 1);
     }
@@ -193,62 +193,67 @@ __global__ void __launch_bounds__(NT, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
-  const uint32_t tmem_s = tmem, tmem_o = tmem + 32 * H;
+  const uint32_t tmem_s = tmem, tmem_o = tmem + 64 * H;
 
   if (warp == 0) {
-    // ---- producer ----
+    // ---- producer: V(i+1) is issued before tile i's slices ----
     if (lane == 0) {
-      int k = 0, i = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++i) {
-        const int vb = i & 1;
-        if (i >= 2) tc::mbar_wait(&v_empty[vb], uint32_t(((i >> 1) - 1) & 1));
+      int k = 0;
+      auto load_v = [&](int j) {
+        const int vb = j % NV;
+        if (j >= NV) tc::mbar_wait(&v_empty[vb], uint32_t((j / NV - 1) & 1));
         tc::mbar_expect_tx(&v_full[vb], V_BYTES);
-        tma_load_2d(sb + S::OFF_V + vb * V_BYTES, &vmap, 0, tile * TILE, &v_full[vb]);
+        tma_load_2d(sb + S::OFF_V + vb * V_BYTES, &vmap, 0, tile_of(j) * TILE, &v_full[vb]);
+      };
+      load_v(0);
+      for (int i = 0; i < ntl; ++i) {
+        if (i + 1 < ntl) load_v(i + 1);
         // Δ[m][g][p0 .. p0+n) is 8 contiguous runs of n*16 bytes: plain bulk copies
-        const int64_t p0 = int64_t(tile) * TILE;
+        const int64_t p0 = int64_t(tile_of(i)) * TILE;
         const uint32_t run = uint32_t((P - p0 < TILE ? P - p0 : TILE) * 16);
         for (int pass = 0; pass < passes; ++pass)
           for (int m = 0; m < M; ++m, ++k) {
             const int sl = k % NS;
             if (k >= NS) tc::mbar_wait(&d_empty[sl], uint32_t((k / NS - 1) & 1));
-            tc::mbar_expect_tx(&d_full[sl], run * NCH);
-            for (int g = 0; g < NCH; ++g)
+            tc::mbar_expect_tx(&d_full[sl], run * NG);
+            for (int g = 0; g < NG; ++g)
               tc::bulk_load(sb + S::OFF_D + sl * D_BYTES + g * TILE * 16,
-                            D + ((int64_t(m) * NCH + g) * P + p0) * 4, run, &d_full[sl]);
+                            D + ((int64_t(m) * NG + g) * P + p0) * 4, run, &d_full[sl]);
           }
       }
     }
   } else if (warp == 1) {
-    // ---- MMA issuer: per tile S (from A staging u), then O over the heads ----
-    const uint64_t bqh = tc::smem_desc(sb + S::OFF_BQH, S::BQ_LBO, 128);
-    const uint64_t bql = tc::smem_desc(sb + S::OFF_BQL, S::BQ_LBO, 128);
-    constexpr uint32_t id_s = tc::idesc_tf32(128, 32 * H);
-    constexpr uint32_t id_o = tc::idesc_tf32(128, 32);
+    // ---- MMA issuer: S(first); per tile i: S(i+1), then O over the heads ----
     int u = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      for (int st = 0; st <= H; ++st, ++u) {
-        const int b = u & 1;
-        tc::mbar_wait(&a_full[b], uint32_t((u >> 1) & 1));
-        tc::fence_after();
-        const uint32_t ab = sb + S::OFF_A + b * A_BYTES;
-        const uint64_t ahi = tc::smem_desc(ab, A_LBO, 128);
-        const uint64_t alo = tc::smem_desc(ab + A_PLANE, A_LBO, 128);
+    auto next_a = [&]() {
+      const int b = u & 1;
+      tc::mbar_wait(&a_full[b], uint32_t((u >> 1) & 1));
+      tc::fence_after();
+      return b;
+    };
+    auto issue_s = [&]() {
+      const int b = next_a();
+      if (tc::elect_one()) {
+        mma_split(tmem_s, sb + S::OFF_A + b * A_BYTES, sb + S::OFF_BQ, 32 * H, false);
+        tc::commit(s_done);
+        tc::commit(&a_free[b]);
+      }
+      __syncwarp();
+      ++u;
+    };
+    issue_s();
+    for (int i = 0; i < ntl; ++i) {
+      if (i + 1 < ntl) issue_s();
+      for (int h = 0; h < H; ++h) {
+        const int b = next_a();
         if (tc::elect_one()) {
-          if (st == 0) {
-            mma3(tmem_s, ahi, alo, bqh, bql, S::BQ_LBO, id_s, false);
-            tc::commit(s_done);
-          } else {
-            const int hh = st - 1;
-            const uint64_t boh =
-                tc::smem_desc(sb + S::OFF_BO + (2 * hh) * S::BO_BYTES, S::BO_LBO, 128);
-            const uint64_t bol =
-                tc::smem_desc(sb + S::OFF_BO + (2 * hh + 1) * S::BO_BYTES, S::BO_LBO, 128);
-            mma3(tmem_o, ahi, alo, boh, bol, S::BO_LBO, id_o, hh > 0);
-            if (hh == H - 1) tc::commit(o_done);
-          }
+          mma_split(tmem_o, sb + S::OFF_A + b * A_BYTES, sb + S::OFF_BO + h * S::BO_BYTES, 32,
+                    h > 0);
+          if (h == H - 1) tc::commit(o_done);
           tc::commit(&a_free[b]);
         }
         __syncwarp();
+        ++u;
       }
     }
   } else {
@@ -257,10 +262,8 @@ __global__ void __launch_bounds__(NT, 1)
     const int row = q * 32 + lane;  // texel row of the tile == TMEM lane
     const uint32_t lane_base = uint32_t(q * 32) << 16;
     const float inv_temp = __double2float_rn(1.0 / sqrt(double(C)));
-    float g32[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) g32[c] = __ldg(gain + c);
-    int k = 0, u = 0, i = 0;
+    const bool storer = warp == 2 && lane == 0;
+    int k = 0, u = 0;
     auto stage = [&](const float* x) {  // A staging u (buffer u & 1)
       const int b = u & 1;
       if (u >= 2) tc::mbar_wait(&a_free[b], uint32_t(((u >> 1) - 1) & 1));
@@ -274,34 +277,71 @@ __global__ void __launch_bounds__(NT, 1)
       tc::mbar_wait(&d_full[sl], uint32_t((k / NS) & 1));
       const uint8_t* d = smem + S::OFF_D + sl * D_BYTES + row * 16;
 #pragma unroll
-      for (int g = 0; g < NCH; ++g) {
+      for (int g = 0; g < NG; ++g) {
         const float4 t = *reinterpret_cast<const float4*>(d + g * TILE * 16);
         dm[4 * g] = t.x, dm[4 * g + 1] = t.y, dm[4 * g + 2] = t.z, dm[4 * g + 3] = t.w;
       }
       tc::mbar_arrive(&d_empty[sl]);
       ++k;
     };
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++i) {
-      const int vb = i & 1;
-      uint8_t* vt = smem + S::OFF_V + vb * V_BYTES;
-      // ---- n = rms_norm(V) * g -> A ----
-      tc::mbar_wait(&v_full[vb], uint32_t((i >> 1) & 1));
-      {
-        float x[C];
+    auto tmem_split = [&](uint32_t col, int n, float* out) {  // D[:, col] + 2^-11 D[:, col + n]
+      float lo[32];
+      tc::tmem_ld32(lane_base + col, out);
+      tc::tmem_ld32(lane_base + col + uint32_t(n), lo);
 #pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4) {
-          const float4 t = *reinterpret_cast<const float4*>(vt + swz(row, c4));
-          x[4 * c4] = t.x, x[4 * c4 + 1] = t.y, x[4 * c4 + 2] = t.z, x[4 * c4 + 3] = t.w;
-        }
-        float ms = 0.f;
+      for (int c = 0; c < 32; ++c) out[c] = fmaf(lo[c], 1.0f / tc::kF16LoScale, out[c]);
+    };
+    auto start_tile = [&](int j) {  // n = rms_norm(V) * g -> A (requests S(j))
+      const int vb = j % NV;
+      const uint8_t* vt = smem + S::OFF_V + vb * V_BYTES;
+      tc::mbar_wait(&v_full[vb], uint32_t((j / NV) & 1));
+      float x[C];
 #pragma unroll
-        for (int c = 0; c < C; ++c) ms = fmaf(x[c], x[c], ms);
-        const float r = __fdiv_rn(1.0f, __fsqrt_rn(fa(__fdiv_rn(ms, float(C)), 1e-6f)));
-#pragma unroll
-        for (int c = 0; c < C; ++c) x[c] = fm(fm(x[c], r), g32[c]);
-        stage(x);
+      for (int c4 = 0; c4 < 8; ++c4) {
+        const float4 t = *reinterpret_cast<const float4*>(vt + swz(row, c4));
+        x[4 * c4] = t.x, x[4 * c4 + 1] = t.y, x[4 * c4 + 2] = t.z, x[4 * c4 + 3] = t.w;
       }
-      // ---- scores: S held in registers, one pass over Δ ----
+      float ms = 0.f;
+#pragma unroll
+      for (int c = 0; c < C; ++c) ms = fmaf(x[c], x[c], ms);
+      const float r = __fdiv_rn(1.0f, __fsqrt_rn(fa(__fdiv_rn(ms, float(C)), 1e-6f)));
+#pragma unroll
+      for (int c = 0; c < C; ++c) x[c] = fm(fm(x[c], r), __ldg(gain + c));
+      stage(x);
+    };
+    auto finish_tile = [&](int j) {  // V(j) += O(j), TMA store
+      const int vb = j % NV;
+      uint8_t* vt = smem + S::OFF_V + vb * V_BYTES;
+      tc::mbar_wait(o_done, uint32_t(j & 1));
+      tc::fence_after();
+      float o[C];
+      tmem_split(tmem_o, 32, o);
+      tc::fence_before();
+#pragma unroll
+      for (int c4 = 0; c4 < 8; ++c4) {
+        float4* pv = reinterpret_cast<float4*>(vt + swz(row, c4));
+        float4 t = *pv;
+        t.x = fa(t.x, o[4 * c4]);
+        t.y = fa(t.y, o[4 * c4 + 1]);
+        t.z = fa(t.z, o[4 * c4 + 2]);
+        t.w = fa(t.w, o[4 * c4 + 3]);
+        *pv = t;
+      }
+      tc::fence_proxy_async();
+      named_sync(1, NCONS);
+      if (storer) {
+        if (j > 0) {  // the previous store has left its buffer: hand it back
+          tc::bulk_wait_read<0>();
+          tc::mbar_arrive(&v_empty[(j - 1) % NV]);
+        }
+        tma_store_2d(&vmap, sb + S::OFF_V + vb * V_BYTES, 0, tile_of(j) * TILE);
+        tc::bulk_commit();
+      }
+    };
+
+    start_tile(0);
+    for (int i = 0; i < ntl; ++i) {
+      // ---- scores(i): S held in registers, one pass over Δ ----
       float w[H][M];
       if (zero_scores) {
 #pragma unroll
@@ -313,7 +353,7 @@ __global__ void __launch_bounds__(NT, 1)
         tc::mbar_wait(s_done, uint32_t(i & 1));
         tc::fence_after();
 #pragma unroll
-        for (int h = 0; h < H; ++h) tc::tmem_ld32(tmem_s + lane_base + uint32_t(32 * h), sv[h]);
+        for (int h = 0; h < H; ++h) tmem_split(tmem_s + uint32_t(32 * h), 32 * H, sv[h]);
         tc::fence_before();
 #pragma unroll
         for (int m = 0; m < M; ++m) {
@@ -344,7 +384,9 @@ __global__ void __launch_bounds__(NT, 1)
           for (int m = 0; m < M; ++m) w[h][m] = fm(w[h][m], inv);
         }
       }
-      // ---- mix: every head in one pass over Δ ----
+      if (i > 0) finish_tile(i - 1);
+      if (i + 1 < ntl) start_tile(i + 1);
+      // ---- mix(i): every head in one pass over Δ ----
       float hd[H][C];
 #pragma unroll
       for (int h = 0; h < H; ++h)
@@ -359,35 +401,11 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int c = 0; c < C; ++c) hd[h][c] = fmaf(w[h][m], dm[c], hd[h][c]);
       }
-      // ---- O = sum_i head_i Wo_i ----
 #pragma unroll
       for (int h = 0; h < H; ++h) stage(hd[h]);
-      tc::mbar_wait(o_done, uint32_t(i & 1));
-      tc::fence_after();
-      float o[C];
-      tc::tmem_ld32(tmem_o + lane_base, o);
-      tc::fence_before();
-      // ---- V += O, back through the swizzled tile and one TMA store ----
-#pragma unroll
-      for (int c4 = 0; c4 < 8; ++c4) {
-        float4* pv = reinterpret_cast<float4*>(vt + swz(row, c4));
-        float4 t = *pv;
-        t.x = fa(t.x, o[4 * c4]);
-        t.y = fa(t.y, o[4 * c4 + 1]);
-        t.z = fa(t.z, o[4 * c4 + 2]);
-        t.w = fa(t.w, o[4 * c4 + 3]);
-        *pv = t;
-      }
-      tc::fence_proxy_async();
-      named_sync(1, NCONS);
-      if (warp == 2 && lane == 0) {
-        tma_store_2d(&vmap, sb + S::OFF_V + vb * V_BYTES, 0, tile * TILE);
-        tc::bulk_commit();
-        tc::bulk_wait_read<0>();
-        tc::mbar_arrive(&v_empty[vb]);
-      }
     }
-    if (warp == 2 && lane == 0) tc::bulk_wait<0>();
+    finish_tile(ntl - 1);
+    if (storer) tc::bulk_wait<0>();
   }
   tc::fence_before();
   __syncthreads();
