@@ -16,9 +16,9 @@
 // Persistent warp-specialised CTA, one per SM, 128-texel tiles:
 //   w0     TMA producer: V tiles (128B-swizzled, 4 buffers, one tile ahead of
 //          the Δ slices) and, per view, the tile's Δ slice [8 channel groups]
-//          [128 texels][16 B] (8 bulk copies of 2 KB from the view-major SoA
-//          Δ[m][g][p][4]) into an NS-deep ring -- twice per tile (scores, then
-//          mix; the second read hits L2)
+//          [128 texels][16 B] (one 3-D TMA box over the view-major SoA
+//          Δ[m][g][p][4], 512-byte rows) into an NS-deep ring -- twice per tile
+//          (scores, then mix; the second read hits L2)
 //   w1     MMA issuer (one elected lane; warp-uniform descriptors)
 //   w2-5   consumers, thread <-> texel row <-> TMEM lane, software-pipelined
 //          across tiles so neither MMA round trip is on the critical path:
@@ -127,6 +127,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* map, int c
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(tc::smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(tc::smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tma_store_2d(const void* map, uint32_t src, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -140,7 +148,8 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 
 template <int H, int M>
 __global__ void __launch_bounds__(NT, 1)
-    attend_tc_kernel(const __grid_constant__ CUtensorMap vmap, const float* __restrict__ D, int64_t P,
+    attend_tc_kernel(const __grid_constant__ CUtensorMap vmap,
+                     const __grid_constant__ CUtensorMap dmap, int64_t P,
                      const float* __restrict__ wq, const float* __restrict__ wo,
                      const float* __restrict__ gain, int zero_scores, int num_tiles) {
   using S = Smem<H>;
@@ -208,17 +217,14 @@ __global__ void __launch_bounds__(NT, 1)
       load_v(0);
       for (int i = 0; i < ntl; ++i) {
         if (i + 1 < ntl) load_v(i + 1);
-        // Δ[m][g][p0 .. p0+n) is 8 contiguous runs of n*16 bytes: plain bulk copies
-        const int64_t p0 = int64_t(tile_of(i)) * TILE;
-        const uint32_t run = uint32_t((P - p0 < TILE ? P - p0 : TILE) * 16);
+        // one 3-D box per view slice: [8 planes][4 rows of 32 texels][128 floats]
         for (int pass = 0; pass < passes; ++pass)
           for (int m = 0; m < M; ++m, ++k) {
             const int sl = k % NS;
             if (k >= NS) tc::mbar_wait(&d_empty[sl], uint32_t((k / NS - 1) & 1));
-            tc::mbar_expect_tx(&d_full[sl], run * NG);
-            for (int g = 0; g < NG; ++g)
-              tc::bulk_load(sb + S::OFF_D + sl * D_BYTES + g * TILE * 16,
-                            D + ((int64_t(m) * NG + g) * P + p0) * 4, run, &d_full[sl]);
+            tc::mbar_expect_tx(&d_full[sl], D_BYTES);
+            tma_load_3d(sb + S::OFF_D + sl * D_BYTES, &dmap, 0, tile_of(i) * (TILE / 32), m * NG,
+                        &d_full[sl]);
           }
       }
     }
@@ -355,16 +361,26 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int h = 0; h < H; ++h) tmem_split(tmem_s + uint32_t(32 * h), 32 * H, sv[h]);
         tc::fence_before();
+        // views in pairs, each dot as 4 interleaved partial sums: 8 independent
+        // 8-deep FMA chains instead of one 32-deep chain per (view, head)
 #pragma unroll
-        for (int m = 0; m < M; ++m) {
-          float dm[C];
-          slice_row(dm);
+        for (int m = 0; m < M; m += 2) {
+          float d0[C], d1[C];
+          slice_row(d0);
+          slice_row(d1);
 #pragma unroll
           for (int h = 0; h < H; ++h) {
-            float acc = 0.f;
+            float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int c = 0; c < C; ++c) acc = fmaf(sv[h][c], dm[c], acc);
-            w[h][m] = fm(acc, inv_temp);
+            for (int c = 0; c < C; c += 4) {
+#pragma unroll
+              for (int r = 0; r < 4; ++r) {
+                a0[r] = fmaf(sv[h][c + r], d0[c + r], a0[r]);
+                a1[r] = fmaf(sv[h][c + r], d1[c + r], a1[r]);
+              }
+            }
+            w[h][m] = fm(fa(fa(a0[0], a0[1]), fa(a0[2], a0[3])), inv_temp);
+            w[h][m + 1] = fm(fa(fa(a1[0], a1[1]), fa(a1[2], a1[3])), inv_temp);
           }
         }
         // softmax over views (tape.hpp:390-404: max, exp(x - max), sum, * 1/sum)
@@ -393,13 +409,15 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int c = 0; c < C; ++c) hd[h][c] = 0.f;
 #pragma unroll
-      for (int m = 0; m < M; ++m) {
-        float dm[C];
-        slice_row(dm);
+      for (int m = 0; m < M; m += 2) {
+        float d0[C], d1[C];
+        slice_row(d0);
+        slice_row(d1);
 #pragma unroll
         for (int h = 0; h < H; ++h)
 #pragma unroll
-          for (int c = 0; c < C; ++c) hd[h][c] = fmaf(w[h][m], dm[c], hd[h][c]);
+          for (int c = 0; c < C; ++c)
+            hd[h][c] = fmaf(w[h][m + 1], d1[c], fmaf(w[h][m], d0[c], hd[h][c]));
       }
 #pragma unroll
       for (int h = 0; h < H; ++h) stage(hd[h]);
@@ -440,8 +458,9 @@ void launch(float* V, const float* D, int64_t P, const float* wq, const float* w
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   // V [P][32] fp32 as a 2-D map, 128-texel boxes (128B swizzle)
-  CUtensorMap vmap;
+  CUtensorMap vmap, dmap;
   std::memset(&vmap, 0, sizeof(vmap));
+  std::memset(&dmap, 0, sizeof(dmap));
   {
     cuuint64_t dims[2] = {cuuint64_t(C), cuuint64_t(P)};
     cuuint64_t strides[1] = {cuuint64_t(C) * 4};
@@ -452,9 +471,21 @@ void launch(float* V, const float* D, int64_t P, const float* wq, const float* w
                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       throw CudaError("attention: V tensor map");
   }
+  {
+    // each Δ plane (m, g) as [ceil(P/32) rows][128 floats]; a partial last row
+    // reads past the plane (texels >= P are never used; the buffer has slack)
+    cuuint64_t dims[3] = {128, cuuint64_t((P + 31) / 32), cuuint64_t(M) * NG};
+    cuuint64_t strides[2] = {512, cuuint64_t(P) * 16};
+    cuuint32_t box[3] = {128, TILE / 32, NG};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (encode_fn()(&dmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(D), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      throw CudaError("attention: delta tensor map");
+  }
   const int tiles = int((P + TILE - 1) / TILE);
   const int grid = tiles < sms ? tiles : sms;
-  attend_tc_kernel<H, M><<<grid, NT, Smem<H>::BYTES, st>>>(vmap, D, P, wq, wo, gain, zero, tiles);
+  attend_tc_kernel<H, M><<<grid, NT, Smem<H>::BYTES, st>>>(vmap, dmap, P, wq, wo, gain, zero, tiles);
 }
 
 }  // namespace

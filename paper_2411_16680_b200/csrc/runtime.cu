@@ -332,7 +332,7 @@ void ensure_plan(lvsg_ctx* c, int64_t He, int64_t We) {
   }
   c->V0.ensure(maxV * C);
   c->V1.ensure(maxV * C);
-  c->deltas.ensure(maxD);
+  c->deltas.ensure(maxD + 128);  // slack: attention's Δ boxes may read a partial row past the end
   c->t1.ensure(maxV * C);
   c->rinv.ensure(maxV);
   c->uh.ensure(maxU * C);
