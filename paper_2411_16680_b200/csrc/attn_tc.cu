@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* o_done = s_done + 1;      // O ready
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + S::NBAR);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  tc::pdl_launch_dependents();
   if (blockIdx.x >= num_tiles) return;
   const uint32_t sb = tc::smem_u32(smem);
   if (tid == 0 && (sb & 1023u)) __trap();  // swizzle atoms need 1 KB alignment
@@ -203,6 +204,7 @@ __global__ void __launch_bounds__(NT, 1)
   tc::fence_after();
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
   const uint32_t tmem_s = tmem, tmem_o = tmem + 64 * H;
+  tc::pdl_wait();  // the prologue above overlaps the previous kernel (weights are static)
 
   if (warp == 0) {
     // ---- producer: V(i+1) is issued before tile i's slices ----
@@ -485,7 +487,8 @@ void launch(float* V, const float* D, int64_t P, const float* wq, const float* w
   }
   const int tiles = int((P + TILE - 1) / TILE);
   const int grid = tiles < sms ? tiles : sms;
-  attend_tc_kernel<H, M><<<grid, NT, Smem<H>::BYTES, st>>>(vmap, dmap, P, wq, wo, gain, zero, tiles);
+  launch_pdl(true, attend_tc_kernel<H, M>, grid, NT, Smem<H>::BYTES, st, vmap, dmap, P, wq, wo,
+             gain, zero, tiles);
 }
 
 }  // namespace

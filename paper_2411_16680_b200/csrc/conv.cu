@@ -36,6 +36,7 @@ __device__ __forceinline__ float load_src(const ConvArgs& a, int b, int pix, int
 }
 
 __global__ void __launch_bounds__(NT) conv3x3_kernel(const ConvArgs a) {
+  pdl_grid_sync();
   __shared__ __align__(16) float s_in[CK * HP * WP];
   __shared__ __align__(16) float s_w[9 * CK * COT];
 
@@ -137,6 +138,7 @@ __global__ void __launch_bounds__(NT) conv3x3_kernel(const ConvArgs a) {
 // the bias like the reference; optional residual (accumulating slices).
 template <int CI>
 __global__ void __launch_bounds__(128) conv3x3_stem_kernel(const ConvArgs a) {
+  pdl_grid_sync();
   __shared__ __align__(16) float s_w[9 * CI * 32];
   __shared__ float s_b[32];
   __shared__ __align__(16) float4 s_o[128 * 8];  // [pixel][c4 ^ (pixel & 7)]
@@ -234,9 +236,9 @@ void conv3x3(const ConvArgs& a, cudaStream_t st, int impl) {
   } else if (impl != 1 && stem_supported(a)) {
     const int64_t n = (int64_t)a.B * a.H * a.W;
     if (a.Cin == 3)
-      conv3x3_stem_kernel<3><<<int((n + 127) / 128), 128, 0, st>>>(a);
+      launch_k(conv3x3_stem_kernel<3>, int((n + 127) / 128), 128, 0, st, a);
     else
-      conv3x3_stem_kernel<1><<<int((n + 127) / 128), 128, 0, st>>>(a);
+      launch_k(conv3x3_stem_kernel<1>, int((n + 127) / 128), 128, 0, st, a);
   } else {
     conv3x3_simt(a, st);
   }
@@ -245,7 +247,7 @@ void conv3x3(const ConvArgs& a, cudaStream_t st, int impl) {
 void conv3x3_simt(const ConvArgs& a, cudaStream_t st) {
   const int tiles = ((a.W + TW - 1) / TW) * ((a.H + TH - 1) / TH);
   dim3 grid(tiles, (a.Cout + COT - 1) / COT, a.B);
-  conv3x3_kernel<<<grid, NT, 0, st>>>(a);
+  launch_k(conv3x3_kernel, grid, NT, 0, st, a);
 }
 
 }  // namespace lvsg

@@ -33,6 +33,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "host.h"
@@ -138,6 +139,7 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* w_full = res_full + NEW;         // weight image landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
 
+  tc::pdl_launch_dependents();
   if (blockIdx.x >= num_tiles) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t sbase = tc::smem_u32(smem);
@@ -162,14 +164,19 @@ __global__ void __launch_bounds__(NT, 1)
     for (int k = 0; k < NEW; ++k) tc::mbar_init(&res_full[k], 1);
     tc::mbar_init(w_full, 1);
     tc::mbar_init_fence();
-    tc::mbar_expect_tx(w_full, W_BYTES);
-    tc::bulk_load(sbase + OFF_W, a.wsplit, W_BYTES, w_full);
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, TMEM_COLS);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
+  // everything above overlaps the previous kernel under PDL; global data
+  // (inputs, residual, outputs, a freshly prepared weight image) only below
+  tc::pdl_wait();
+  if (tid == 0) {
+    tc::mbar_expect_tx(w_full, W_BYTES);
+    tc::bulk_load(sbase + OFF_W, a.wsplit, W_BYTES, w_full);
+  }
 
   if (warp == 0) {
     // ---- TMA producer: one [18][10][32] box per tile into the raw ring ----
@@ -343,6 +350,7 @@ __global__ void __launch_bounds__(NT, 1)
 // Weight image: [tap][plane j][row n][8 halves], rows 0..31 = fp16 hi of
 // w[co = n][w_ci0 + 8j + k8][tap], rows 32..63 = lo' (tc::split_f16).
 __global__ void conv3x3_tc_weights_kernel(const ConvArgs a, __half* out) {
+  pdl_grid_sync();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= 9 * NCH * W_ROWS * 8) return;
   const int k8 = e & 7, n = (e >> 3) & 63, rest = e >> 9;
@@ -400,7 +408,8 @@ CUtensorMap make_map(const float* p, long long pstride, long long bstride, int W
 
 void conv3x3_tc_prepare(const ConvArgs& a, void* dst, cudaStream_t st) {
   static_assert(kConvTcWeightBytes == W_BYTES, "weight image size");
-  conv3x3_tc_weights_kernel<<<(W_BYTES / 2 + 255) / 256, 256, 0, st>>>(a, static_cast<__half*>(dst));
+  launch_k(conv3x3_tc_weights_kernel, (W_BYTES / 2 + 255) / 256, 256, 0, st, a,
+           static_cast<__half*>(dst));
 }
 
 void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
@@ -427,7 +436,18 @@ void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int grid = tiles < sms ? tiles : sms;
-  conv3x3_tc_kernel<<<grid, NT, SMEM_BYTES, st>>>(xmap, omap, rmap, a, tiles);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute lattr[1];
+  lattr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  lattr[0].val.programmaticStreamSerializationAllowed = (a.pdl && pdl_enabled()) ? 1 : 0;
+  cfg.attrs = lattr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel, xmap, omap, rmap, a, tiles) != cudaSuccess)
+    throw CudaError("conv3x3_tc: launch failed");
 }
 
 }  // namespace lvsg

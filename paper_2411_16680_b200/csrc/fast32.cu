@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(128) layer_collapse32_kernel(
     const float* __restrict__ V, int L2, int64_t PL, const float* __restrict__ w1,
     const float* __restrict__ b1, const float* __restrict__ w2, const float* __restrict__ b2,
     float* __restrict__ out) {
+  pdl_grid_sync();
   __shared__ __align__(16) float s_w1[2 * C * 2 * C];
   __shared__ __align__(16) float s_w2[2 * C * C];
   for (int e = threadIdx.x; e < 4 * C * C; e += blockDim.x) s_w1[e] = w1[e];
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(128) blend_logits32_kernel(const float* __rest
                                                              const float* __restrict__ bw,
                                                              const float* __restrict__ gain,
                                                              float* __restrict__ logits) {
+  pdl_grid_sync();
   __shared__ __align__(16) float s_bw[C * C];
   for (int e = threadIdx.x; e < C * C; e += blockDim.x) s_bw[e] = bw[e];
   __syncthreads();
@@ -145,6 +147,7 @@ __global__ void __launch_bounds__(128) decode_payload32_kernel(
     const float* __restrict__ w_sigma, const float* __restrict__ w_depth, DepthAct act,
     DevRayCam rc, float* __restrict__ payload, float* __restrict__ depth,
     float* __restrict__ points) {
+  pdl_grid_sync();
   constexpr int KW = C + 4;  // appear | sigma | depth | pad (16-byte rows)
   __shared__ __align__(16) float s_w[C * KW];
   for (int e = threadIdx.x; e < C * KW; e += blockDim.x) {
@@ -197,7 +200,7 @@ bool layer_collapse32(const float* V, int L, int64_t PL, int C_, const float* w1
                       const float* w2, const float* b2, float* out, cudaStream_t st) {
   if (C_ != C) return false;
   const int L2 = L / 2;
-  layer_collapse32_kernel<<<blocks_for(L2 * PL, 128), 128, 0, st>>>(V, L2, PL, w1, b1, w2, b2, out);
+  launch_k(layer_collapse32_kernel, blocks_for(L2 * PL, 128), 128, 0, st, V, L2, PL, w1, b1, w2, b2, out);
   return true;
 }
 
@@ -206,9 +209,9 @@ bool blend_logits32(const float* V, const float* deltas, int64_t P, int C_, int 
   if (C_ != C) return false;
   const int g = blocks_for(P, 128);
   switch (M) {
-    case 4: blend_logits32_kernel<4><<<g, 128, 0, st>>>(V, deltas, P, blend_w, gain, logits); return true;
-    case 8: blend_logits32_kernel<8><<<g, 128, 0, st>>>(V, deltas, P, blend_w, gain, logits); return true;
-    case 16: blend_logits32_kernel<16><<<g, 128, 0, st>>>(V, deltas, P, blend_w, gain, logits); return true;
+    case 4: launch_k(blend_logits32_kernel<4>, g, 128, 0, st, V, deltas, P, blend_w, gain, logits); return true;
+    case 8: launch_k(blend_logits32_kernel<8>, g, 128, 0, st, V, deltas, P, blend_w, gain, logits); return true;
+    case 16: launch_k(blend_logits32_kernel<16>, g, 128, 0, st, V, deltas, P, blend_w, gain, logits); return true;
     default: return false;
   }
 }
@@ -219,7 +222,7 @@ bool decode_payload32(const float* V, int L, int H, int W, int C_, const float* 
                       cudaStream_t st) {
   if (C_ != C || Ca != C) return false;
   const int64_t P = (int64_t)L * H * W;
-  decode_payload32_kernel<<<blocks_for(P, 128), 128, 0, st>>>(V, L, H, W, w_appear, w_sigma,
+  launch_k(decode_payload32_kernel, blocks_for(P, 128), 128, 0, st, V, L, H, W, w_appear, w_sigma,
                                                              w_depth, act, rc, payload, depth,
                                                              points);
   return true;

@@ -7,6 +7,15 @@
 #include "kernels.h"
 
 namespace lvsg {
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("LVSG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 namespace {
 
 constexpr int kMaxM = 32;  // views handled per texel in registers
@@ -18,6 +27,7 @@ inline int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
 // ----------------------------------------------------------------------------
 
 __global__ void fill_rows_kernel(float* out, const float* row, int64_t rows, int C) {
+  pdl_grid_sync();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= rows * C) return;
   // matmul(ones[P,1], f[1,C]) == 0 + 1*f (network.hpp:466-467)
@@ -25,6 +35,7 @@ __global__ void fill_rows_kernel(float* out, const float* row, int64_t rows, int
 }
 
 __global__ void fill_layers_kernel(float* out, const float* per_layer, int L, int64_t P) {
+  pdl_grid_sync();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= L * P) return;
   out[i] = per_layer[i / P];
@@ -32,6 +43,7 @@ __global__ void fill_layers_kernel(float* out, const float* per_layer, int L, in
 
 __global__ void fill_anchor_depths_kernel(float* out, int L, int64_t P, double inv_span,
                                           double inv_far) {
+  pdl_grid_sync();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= L * P) return;
   const int l = int(i / P);
@@ -41,6 +53,7 @@ __global__ void fill_anchor_depths_kernel(float* out, int L, int64_t P, double i
 
 // mean_pool2 (tape.hpp:816-836): ((a+b)+c+d)*0.25, channel-last.
 __global__ void mean_pool2_kernel(const float* in, float* out, int B, int H, int W, int C) {
+  pdl_grid_sync();
   const int Ho = H / 2, Wo = W / 2;
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t n = (int64_t)B * Ho * Wo * C;
@@ -62,6 +75,7 @@ __global__ void mean_pool2_kernel(const float* in, float* out, int B, int H, int
 // C % 4 == 0: one thread per (output pixel, channel group), same sum order.
 __global__ void mean_pool2x4_kernel(const float4* __restrict__ in, float4* __restrict__ out, int B,
                                     int H, int W, int G) {
+  pdl_grid_sync();
   const int Ho = H / 2, Wo = W / 2;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)B * Ho * Wo * G) return;
@@ -84,6 +98,7 @@ __global__ void mean_pool2x4_kernel(const float4* __restrict__ in, float4* __res
 
 __global__ void resize_hwc_kernel(const float* in, float* out, int B, int H, int W, int C, int Ho,
                                   int Wo) {
+  pdl_grid_sync();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t n = (int64_t)B * Ho * Wo * C;
   if (i >= n) return;
@@ -106,6 +121,7 @@ __global__ void resize_hwc_kernel(const float* in, float* out, int B, int H, int
 // channels moved as float4.
 __global__ void resize_hwc4_kernel(const float* __restrict__ in, float* __restrict__ out, int B,
                                    int H, int W, int C, int Ho, int Wo) {
+  pdl_grid_sync();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)B * Ho * Wo) return;
   const int x = int(i % Wo);
@@ -136,6 +152,7 @@ __global__ void resize_hwc4_kernel(const float* __restrict__ in, float* __restri
 __global__ void __launch_bounds__(256) resize_hwc4c_kernel(const float* __restrict__ in,
                                                            float* __restrict__ out, int B, int H,
                                                            int W, int G, int Ho, int Wo) {
+  pdl_grid_sync();
   __shared__ int s_tap[64][4];
   __shared__ float s_fr[64][2];
   const int PB = 256 / G;
@@ -174,6 +191,7 @@ __global__ void __launch_bounds__(256) resize_hwc4c_kernel(const float* __restri
 
 // One warp per row: rinv = 1 / sqrt(sum(x^2)/C + 1e-6).
 __global__ void rms_rinv_kernel(const float* x, float* rinv, int64_t rows, int C) {
+  pdl_grid_sync();
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -192,6 +210,7 @@ __global__ void rms_rinv_kernel(const float* x, float* rinv, int64_t rows, int C
 
 // ray_plane_delta + ray_encoding_base (geometry.hpp:343-391): [M, h, w, 32].
 __global__ void ray_base_kernel(const RayBaseCam* cams, RayBaseArgs a, float* base) {
+  pdl_grid_sync();
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)a.M * a.h * a.w) return;
   const int j = int(i % a.w);
@@ -228,6 +247,7 @@ __global__ void ray_base_kernel(const RayBaseCam* cams, RayBaseArgs a, float* ba
 // rays_k[p, c] = sum_f resize(base)[p, f] * proj[f, c] (network.hpp:405-411).
 __global__ void ray_project_kernel(const float* base, int M, int hK, int wK, int Hk, int Wk,
                                    const float* proj, int C, float* out) {
+  pdl_grid_sync();
   extern __shared__ __align__(16) float s_proj[];
   for (int e = threadIdx.x; e < 32 * C; e += blockDim.x) s_proj[e] = proj[e];
   __syncthreads();
@@ -287,6 +307,7 @@ __global__ void __launch_bounds__(128) ray_project32_kernel(const float* __restr
                                                             int hK, int wK, int Hk, int Wk,
                                                             const float* __restrict__ proj,
                                                             float* __restrict__ out) {
+  pdl_grid_sync();
   __shared__ __align__(16) float s_proj[32 * 32];
   __shared__ __align__(16) float4 s_o[128 * 8];  // [row][c4 ^ (row & 7)]
   for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) s_proj[e] = __ldg(proj + e);
@@ -365,6 +386,7 @@ __global__ void gather_stack_kernel(const float* __restrict__ feats, int M, int 
                                     const DevCam* __restrict__ cams, DevRayCam rc,
                                     const float* __restrict__ depth, int L, int H, int W,
                                     float* __restrict__ deltas) {
+  pdl_grid_sync();
   const int64_t P = (int64_t)L * H * W;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= P * M) return;
@@ -419,6 +441,7 @@ __global__ void gather_stack_kernel(const float* __restrict__ feats, int M, int 
 __global__ void __launch_bounds__(256) gather_stack32_kernel(
     const float* __restrict__ feats, int M, int Hf, int Wf, const DevCam* __restrict__ cams,
     DevRayCam rc, const float* __restrict__ depth, int L, int H, int W, float* __restrict__ deltas) {
+  pdl_grid_sync();
   constexpr int G = 8;
   const int64_t P = (int64_t)L * H * W;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -485,6 +508,7 @@ __global__ void decode_payload_kernel(const float* __restrict__ V, int L, int H,
                                       const float* __restrict__ w_sigma,
                                       const float* __restrict__ w_depth, DepthAct act, DevRayCam rc,
                                       float* payload, float* depth, float* points) {
+  pdl_grid_sync();
   extern __shared__ float s_w[];  // [C, Ca+2]: appear | sigma | depth
   const int K2 = Ca + 2;
   for (int e = threadIdx.x; e < C * K2; e += blockDim.x) {
@@ -530,6 +554,7 @@ __device__ __forceinline__ void red_add_v4(float* p, float4 v) {
 __global__ void splat_kernel(const float* __restrict__ payload, const float* __restrict__ points,
                              int L, int PL, int K, const DevCam* __restrict__ cams, int M, int Hv,
                              int Wv, float* acc) {
+  pdl_grid_sync();
   const int PS = pay_stride(K), S = acc_stride(K), G = S / 4;
   const int64_t P = (int64_t)L * PL;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -561,11 +586,75 @@ __global__ void splat_kernel(const float* __restrict__ payload, const float* __r
   }
 }
 
+// Cooperative splat: lane r of a warp projects (texel, view) pair r of the
+// warp's 32 (the f64 footprint once per pair, not once per channel group);
+// the warp then deals the 32 x G (pair, group) items round-robin, so lanes
+// with consecutive groups of one pair reduce into one contiguous accumulator
+// row. Same values and reduction targets as splat_kernel.
+__global__ void __launch_bounds__(256) splat_coop_kernel(const float* __restrict__ payload,
+                                                         const float* __restrict__ points, int L,
+                                                         int PL, int K,
+                                                         const DevCam* __restrict__ cams, int M,
+                                                         int Hv, int Wv, float* acc) {
+  pdl_grid_sync();
+  const int PS = pay_stride(K), S = acc_stride(K), G = S / 4;
+  const int64_t P = (int64_t)L * PL;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // pair (p, m), m fastest
+  const int lane = threadIdx.x & 31;
+  int ok = 0, pp = 0, tb = 0, dx = 0, dy = 0;
+  float w[4] = {0.f, 0.f, 0.f, 0.f};
+  if (i < P * M) {
+    const int m = int(i % M);
+    const int64_t p = i / M;
+    const int l = int(p / PL);
+    const float pt[3] = {points[p * 3], points[p * 3 + 1], points[p * 3 + 2]};
+    const Footprint f = project_footprint(cams[m], pt);
+    if (f.valid) {
+      double wd[4];
+      bilinear_weights(f, wd);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) w[k] = __double2float_rn(wd[k]);
+      ok = 1;
+      pp = int(p);
+      tb = int(((int64_t)m * L + l) * Hv * Wv + (int64_t)f.y0 * Wv + f.x0);
+      dx = f.x1 - f.x0;
+      dy = (f.y1 - f.y0) * Wv;
+    }
+  }
+  const int items = 32 * G;
+  for (int j = lane; j - lane < items; j += 32) {
+    const int r = j / G, g = j - r * G;  // r < 32 for j < items
+    const int src = r < 32 ? r : 31;
+    const int rok = __shfl_sync(0xffffffffu, ok, src);
+    const int rp = __shfl_sync(0xffffffffu, pp, src);
+    const int rtb = __shfl_sync(0xffffffffu, tb, src);
+    const int rdx = __shfl_sync(0xffffffffu, dx, src);
+    const int rdy = __shfl_sync(0xffffffffu, dy, src);
+    float rw[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) rw[k] = __shfl_sync(0xffffffffu, w[k], src);
+    if (j >= items || !rok) continue;
+    float val[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = 4 * g + k;
+      val[k] = c < K ? __ldg(payload + (int64_t)rp * PS + c) : (c == K ? 1.0f : 0.0f);
+    }
+    const int tap[4] = {rtb, rtb + rdx, rtb + rdy, rtb + rdy + rdx};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      red_add_v4(acc + (int64_t)tap[k] * S + 4 * g,
+                 make_float4(fm(rw[k], val[0]), fm(rw[k], val[1]), fm(rw[k], val[2]),
+                             fm(rw[k], val[3])));
+  }
+}
+
 // One thread per (view pixel, 4-channel group): normalise by max(wsum,1e-4)
 // then composite back to front (geometry.hpp:317-326; ldm.hpp:98-115).
 // Output rows are padded to pay_stride(K) (channels K.. are zero).
 __global__ void splat_composite_kernel(const float* __restrict__ acc, int M, int L, int Hv, int Wv,
                                        int K, float* out) {
+  pdl_grid_sync();
   const int PS = pay_stride(K), S = acc_stride(K), G = PS / 4;
   const int64_t PV = (int64_t)Hv * Wv;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -611,6 +700,7 @@ __global__ void __launch_bounds__(128) attend_kernel(float* V, const float* __re
                                                      const float* __restrict__ wo,
                                                      const float* __restrict__ gain,
                                                      int zero_scores) {
+  pdl_grid_sync();
   extern __shared__ __align__(16) float smem[];
   float* s_wq = smem;                    // [heads][C][C]
   float* s_wo = smem + heads * C * C;    // [heads*C][C]
@@ -737,6 +827,7 @@ __global__ void attend_generic_kernel(float* V, const float* __restrict__ D, int
                                       int M, int heads, const float* __restrict__ wq,
                                       const float* __restrict__ wo, const float* __restrict__ gain,
                                       int zero_scores, float* scratch) {
+  pdl_grid_sync();
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= P) return;
   float* n = scratch + p * 4 * C;
@@ -788,6 +879,7 @@ __global__ void attend_generic_kernel(float* V, const float* __restrict__ D, int
 __global__ void blend_logits_kernel(const float* __restrict__ V, const float* __restrict__ D,
                                     int64_t P, int C, int M, const float* __restrict__ bw,
                                     const float* __restrict__ gain, float* logits) {
+  pdl_grid_sync();
   extern __shared__ float s_bw[];
   for (int e = threadIdx.x; e < C * C; e += blockDim.x) s_bw[e] = bw[e];
   __syncthreads();
@@ -819,6 +911,7 @@ __global__ void layer_collapse_kernel(const float* __restrict__ V, int L2, int64
                                       const float* __restrict__ w1, const float* __restrict__ b1,
                                       const float* __restrict__ w2, const float* __restrict__ b2,
                                       float* out) {
+  pdl_grid_sync();
   extern __shared__ float smem[];
   float* s_w1 = smem;                 // [2C][2C]
   float* s_w2 = smem + 4 * C * C;     // [2C][C]
@@ -854,6 +947,7 @@ __global__ void layer_collapse_kernel(const float* __restrict__ V, int L2, int64
 __global__ void decode_scalar_kernel(const float* __restrict__ V, int64_t P, int C,
                                      const float* __restrict__ w, float* out, int64_t PL,
                                      DepthAct act, int do_act) {
+  pdl_grid_sync();
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= P) return;
   const float* v = V + p * C;
@@ -870,6 +964,7 @@ __global__ void __launch_bounds__(128) decode_scalar2_kernel(const float* __rest
                                                              float* __restrict__ outa,
                                                              const float* __restrict__ wb,
                                                              float* __restrict__ outb) {
+  pdl_grid_sync();
   __shared__ __align__(16) float4 rows[128 * 8];  // [row][c4 ^ (row & 7)]
   __shared__ float s_wa[32], s_wb[32];
   const int t = threadIdx.x;
@@ -908,6 +1003,7 @@ __global__ void __launch_bounds__(128) decode_scalar2_kernel(const float* __rest
 
 __global__ void stage_world_points_kernel(DevRayCam rc, const float* depth, int L, int H, int W,
                                           float* points, double lo, double hi, int* bad) {
+  pdl_grid_sync();
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= (int64_t)L * H * W) return;
   const float d = depth[p];
@@ -922,6 +1018,7 @@ __global__ void stage_world_points_kernel(DevRayCam rc, const float* depth, int 
 
 __global__ void stage_footprints_kernel(DevCam cam, const float* points, int64_t P, int32_t* taps,
                                         uint8_t* valid, double* fracs) {
+  pdl_grid_sync();
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= P) return;
   const float pt[3] = {points[p * 3], points[p * 3 + 1], points[p * 3 + 2]};
@@ -937,6 +1034,7 @@ __global__ void stage_footprints_kernel(DevCam cam, const float* points, int64_t
 
 __global__ void stage_gather_kernel(DevCam cam, const float* image, int Hi, int Wi, int C,
                                     const float* points, int64_t P, float* values, float* mask) {
+  pdl_grid_sync();
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= P) return;
   const float pt[3] = {points[p * 3], points[p * 3 + 1], points[p * 3 + 2]};
@@ -961,23 +1059,23 @@ __global__ void stage_gather_kernel(DevCam cam, const float* image, int Hi, int 
 // ---------------------------------------------------------------------------
 
 void fill_rows(float* out, const float* row, int64_t rows, int C, cudaStream_t st) {
-  fill_rows_kernel<<<blocks_for(rows * C, 256), 256, 0, st>>>(out, row, rows, C);
+  launch_k(fill_rows_kernel, blocks_for(rows * C, 256), 256, 0, st, out, row, rows, C);
 }
 void fill_layers(float* out, const float* per_layer, int L, int64_t P, cudaStream_t st) {
-  fill_layers_kernel<<<blocks_for(L * P, 256), 256, 0, st>>>(out, per_layer, L, P);
+  launch_k(fill_layers_kernel, blocks_for(L * P, 256), 256, 0, st, out, per_layer, L, P);
 }
 void fill_anchor_depths(float* out, int L, int64_t P, double inv_span, double inv_far,
                         cudaStream_t st) {
-  fill_anchor_depths_kernel<<<blocks_for(L * P, 256), 256, 0, st>>>(out, L, P, inv_span, inv_far);
+  launch_k(fill_anchor_depths_kernel, blocks_for(L * P, 256), 256, 0, st, out, L, P, inv_span, inv_far);
 }
 void mean_pool2(const float* in, float* out, int B, int H, int W, int C, cudaStream_t st) {
   const int64_t n = (int64_t)B * (H / 2) * (W / 2) * C;
   if (C % 4 == 0 && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
-    mean_pool2x4_kernel<<<blocks_for(n / 4, 256), 256, 0, st>>>(
+    launch_k(mean_pool2x4_kernel, blocks_for(n / 4, 256), 256, 0, st, 
         reinterpret_cast<const float4*>(in), reinterpret_cast<float4*>(out), B, H, W, C / 4);
     return;
   }
-  mean_pool2_kernel<<<blocks_for(n, 256), 256, 0, st>>>(in, out, B, H, W, C);
+  launch_k(mean_pool2_kernel, blocks_for(n, 256), 256, 0, st, in, out, B, H, W, C);
 }
 void resize_hwc(const float* in, float* out, int B, int H, int W, int C, int Ho, int Wo,
                 cudaStream_t st) {
@@ -992,29 +1090,29 @@ void resize_hwc(const float* in, float* out, int B, int H, int W, int C, int Ho,
     const int G = C / 4;
     if (G >= 4 && G <= 64 && (int64_t)B * H * W * G < (int64_t(1) << 31)) {
       const int PB = 256 / G;
-      resize_hwc4c_kernel<<<int((px + PB - 1) / PB), 256, 0, st>>>(in, out, B, H, W, G, Ho, Wo);
+      launch_k(resize_hwc4c_kernel, int((px + PB - 1) / PB), 256, 0, st, in, out, B, H, W, G, Ho, Wo);
     } else {
-      resize_hwc4_kernel<<<blocks_for(px, 128), 128, 0, st>>>(in, out, B, H, W, C, Ho, Wo);
+      launch_k(resize_hwc4_kernel, blocks_for(px, 128), 128, 0, st, in, out, B, H, W, C, Ho, Wo);
     }
     return;
   }
-  resize_hwc_kernel<<<blocks_for(n, 256), 256, 0, st>>>(in, out, B, H, W, C, Ho, Wo);
+  launch_k(resize_hwc_kernel, blocks_for(n, 256), 256, 0, st, in, out, B, H, W, C, Ho, Wo);
 }
 void rms_rinv(const float* x, float* rinv, int64_t rows, int C, cudaStream_t st) {
-  rms_rinv_kernel<<<blocks_for(rows * 32, 256), 256, 0, st>>>(x, rinv, rows, C);
+  launch_k(rms_rinv_kernel, blocks_for(rows * 32, 256), 256, 0, st, x, rinv, rows, C);
 }
 void ray_base(const RayBaseCam* cams_dev, const RayBaseArgs& a, float* base, cudaStream_t st) {
   const int64_t n = (int64_t)a.M * a.h * a.w;
-  ray_base_kernel<<<blocks_for(n, 128), 128, 0, st>>>(cams_dev, a, base);
+  launch_k(ray_base_kernel, blocks_for(n, 128), 128, 0, st, cams_dev, a, base);
 }
 void ray_project(const float* base, int M, int hK, int wK, int Hk, int Wk, const float* proj,
                  int C, float* out, cudaStream_t st) {
   const int64_t n = (int64_t)M * Hk * Wk;
   if (C == 32) {
-    ray_project32_kernel<<<blocks_for(n, 128), 128, 0, st>>>(base, M, hK, wK, Hk, Wk, proj, out);
+    launch_k(ray_project32_kernel, blocks_for(n, 128), 128, 0, st, base, M, hK, wK, Hk, Wk, proj, out);
     return;
   }
-  ray_project_kernel<<<blocks_for(n, 128), 128, 32 * C * sizeof(float), st>>>(base, M, hK, wK, Hk,
+  launch_k(ray_project_kernel, blocks_for(n, 128), 128, 32 * C * sizeof(float), st, base, M, hK, wK, Hk,
                                                                                Wk, proj, C, out);
 }
 void gather_stack(const float* feats, int M, int Hf, int Wf, int C, const DevCam* cams_dev,
@@ -1023,13 +1121,13 @@ void gather_stack(const float* feats, int M, int Hf, int Wf, int C, const DevCam
   const bool v4 = C % 4 == 0;
   const int64_t n = (int64_t)L * H * W * M;
   if (C == 32 && (int64_t)M * Hf * Wf * 8 < (int64_t(1) << 31) && n < (int64_t(1) << 31)) {
-    gather_stack32_kernel<<<blocks_for(n, 256), 256, 0, st>>>(feats, M, Hf, Wf, cams_dev, rc,
+    launch_k(gather_stack32_kernel, blocks_for(n, 256), 256, 0, st, feats, M, Hf, Wf, cams_dev, rc,
                                                               depth, L, H, W, deltas);
   } else if (v4)
-    gather_stack_kernel<true><<<blocks_for(n, 256), 256, 0, st>>>(feats, M, Hf, Wf, C, cams_dev, rc,
+    launch_k(gather_stack_kernel<true>, blocks_for(n, 256), 256, 0, st, feats, M, Hf, Wf, C, cams_dev, rc,
                                                                   depth, L, H, W, deltas);
   else
-    gather_stack_kernel<false><<<blocks_for(n, 256), 256, 0, st>>>(feats, M, Hf, Wf, C, cams_dev,
+    launch_k(gather_stack_kernel<false>, blocks_for(n, 256), 256, 0, st, feats, M, Hf, Wf, C, cams_dev,
                                                                    rc, depth, L, H, W, deltas);
 }
 void decode_payload(const float* V, int L, int H, int W, int C, const float* w_appear, int Ca,
@@ -1040,19 +1138,26 @@ void decode_payload(const float* V, int L, int H, int W, int C, const float* w_a
                        points, st))
     return;
   const int64_t P = (int64_t)L * H * W;
-  decode_payload_kernel<<<blocks_for(P, 128), 128, C * (Ca + 2) * sizeof(float), st>>>(
+  launch_k(decode_payload_kernel, blocks_for(P, 128), 128, C * (Ca + 2) * sizeof(float), st, 
       V, L, H, W, C, w_appear, Ca, w_sigma, w_depth, act, rc, payload, depth, points);
 }
 void splat(const float* payload, const float* points, int L, int PL, int K, const DevCam* cams_dev,
            int M, int Hv, int Wv, float* acc, cudaStream_t st) {
-  const int64_t n = (int64_t)L * PL * M * (acc_stride(K) / 4);
-  splat_kernel<<<blocks_for(n, 256), 256, 0, st>>>(payload, points, L, PL, K, cams_dev, M, Hv, Wv,
+  const int64_t pairs = (int64_t)L * PL * M;
+  if (acc_stride(K) / 4 <= 32 && pairs < (int64_t(1) << 31) &&
+      (int64_t)M * L * Hv * Wv < (int64_t(1) << 31)) {
+    launch_k(splat_coop_kernel, blocks_for(pairs, 256), 256, 0, st, payload, points, L, PL, K, cams_dev, M,
+                                                              Hv, Wv, acc);
+    return;
+  }
+  const int64_t n = pairs * (acc_stride(K) / 4);
+  launch_k(splat_kernel, blocks_for(n, 256), 256, 0, st, payload, points, L, PL, K, cams_dev, M, Hv, Wv,
                                                    acc);
 }
 void splat_composite(const float* acc, int M, int L, int Hv, int Wv, int K, float* out,
                      cudaStream_t st) {
   const int64_t n = (int64_t)M * Hv * Wv * (pay_stride(K) / 4);
-  splat_composite_kernel<<<blocks_for(n, 256), 256, 0, st>>>(acc, M, L, Hv, Wv, K, out);
+  launch_k(splat_composite_kernel, blocks_for(n, 256), 256, 0, st, acc, M, L, Hv, Wv, K, out);
 }
 
 void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
@@ -1067,7 +1172,7 @@ void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, c
   const size_t smem = 2 * size_t(heads) * C * C * sizeof(float);
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    kern<<<blocks_for(P, 128), 128, smem, st>>>(V, deltas, P, heads, wq, wo, gain, zero_scores);
+    launch_k(kern, blocks_for(P, 128), 128, smem, st, V, deltas, P, heads, wq, wo, gain, zero_scores);
   };
   if (C == 32 && M == 8 && smem <= 200 * 1024) {
     launch(attend_kernel<32, 8>);
@@ -1079,7 +1184,7 @@ void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, c
     // scratch: 4C floats per texel, carved from the caller-visible heap
     float* scratch = nullptr;
     cudaMallocAsync(&scratch, size_t(P) * 4 * C * sizeof(float), st);
-    attend_generic_kernel<<<blocks_for(P, 128), 128, 0, st>>>(V, deltas, P, C, M, heads, wq, wo,
+    launch_k(attend_generic_kernel, blocks_for(P, 128), 128, 0, st, V, deltas, P, C, M, heads, wq, wo,
                                                               gain, zero_scores, scratch);
     cudaFreeAsync(scratch, st);
   }
@@ -1087,26 +1192,26 @@ void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, c
 void blend_logits(const float* V, const float* deltas, int64_t P, int C, int M,
                   const float* blend_w, const float* gain, float* logits, cudaStream_t st) {
   if (blend_logits32(V, deltas, P, C, M, blend_w, gain, logits, st)) return;
-  blend_logits_kernel<<<blocks_for(P, 128), 128, C * C * sizeof(float), st>>>(V, deltas, P, C, M,
+  launch_k(blend_logits_kernel, blocks_for(P, 128), 128, C * C * sizeof(float), st, V, deltas, P, C, M,
                                                                               blend_w, gain, logits);
 }
 void layer_collapse(const float* V, int L, int64_t PL, int C, const float* w1, const float* b1,
                     const float* w2, const float* b2, float* out, cudaStream_t st) {
   if (layer_collapse32(V, L, PL, C, w1, b1, w2, b2, out, st)) return;
   const int L2 = L / 2;
-  layer_collapse_kernel<<<blocks_for(L2 * PL, 128), 128, 6 * C * C * sizeof(float), st>>>(
+  launch_k(layer_collapse_kernel, blocks_for(L2 * PL, 128), 128, 6 * C * C * sizeof(float), st, 
       V, L2, PL, C, w1, b1, w2, b2, out);
 }
 void decode_scalar(const float* V, int64_t P, int C, const float* w, float* out, int L,
                    int64_t PL, const DepthAct* act, cudaStream_t st) {
   (void)L;
-  decode_scalar_kernel<<<blocks_for(P, 256), 256, 0, st>>>(V, P, C, w, out, PL,
+  launch_k(decode_scalar_kernel, blocks_for(P, 256), 256, 0, st, V, P, C, w, out, PL,
                                                            act ? *act : DepthAct{}, act ? 1 : 0);
 }
 void decode_scalar2(const float* V, int64_t P, int C, const float* wa, float* outa, const float* wb,
                     float* outb, cudaStream_t st) {
   if (C == 32) {
-    decode_scalar2_kernel<<<blocks_for(P, 128), 128, 0, st>>>(V, P, wa, outa, wb, outb);
+    launch_k(decode_scalar2_kernel, blocks_for(P, 128), 128, 0, st, V, P, wa, outa, wb, outb);
   } else {
     decode_scalar(V, P, C, wa, outa, 0, P, nullptr, st);
     decode_scalar(V, P, C, wb, outb, 0, P, nullptr, st);
@@ -1115,16 +1220,16 @@ void decode_scalar2(const float* V, int64_t P, int C, const float* wa, float* ou
 void stage_world_points(const DevRayCam& rc, const float* depth, int L, int H, int W,
                         float* points, double lo, double hi, int* bad, cudaStream_t st) {
   const int64_t n = (int64_t)L * H * W;
-  stage_world_points_kernel<<<blocks_for(n, 256), 256, 0, st>>>(rc, depth, L, H, W, points, lo, hi,
+  launch_k(stage_world_points_kernel, blocks_for(n, 256), 256, 0, st, rc, depth, L, H, W, points, lo, hi,
                                                                 bad);
 }
 void stage_footprints(const DevCam& cam, const float* points, int64_t P, int32_t* taps,
                       uint8_t* valid, double* fracs, cudaStream_t st) {
-  stage_footprints_kernel<<<blocks_for(P, 256), 256, 0, st>>>(cam, points, P, taps, valid, fracs);
+  launch_k(stage_footprints_kernel, blocks_for(P, 256), 256, 0, st, cam, points, P, taps, valid, fracs);
 }
 void stage_gather(const DevCam& cam, const float* image, int Hi, int Wi, int C,
                   const float* points, int64_t P, float* values, float* mask, cudaStream_t st) {
-  stage_gather_kernel<<<blocks_for(P, 256), 256, 0, st>>>(cam, image, Hi, Wi, C, points, P, values,
+  launch_k(stage_gather_kernel, blocks_for(P, 256), 256, 0, st, cam, image, Hi, Wi, C, points, P, values,
                                                           mask);
 }
 

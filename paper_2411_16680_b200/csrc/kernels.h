@@ -9,6 +9,45 @@
 
 namespace lvsg {
 
+// Programmatic dependent launch. Every kernel of the path opens with
+// pdl_grid_sync() (allow the next kernel to launch, then wait until the
+// previous one has completed and its memory is visible), so it is correct to
+// launch any of them with the attribute. It is set only for the persistent
+// tensor-core kernels (conv3x3_tc, attention: one CTA per SM, > 200 KB smem):
+// their CTAs cannot co-reside with each other, so an early launch only
+// overlaps the predecessor's tail with their prologue, whereas small
+// dependents launched early would sit in griddepcontrol.wait beside a
+// running persistent kernel and slow it down (measured: 111.6 vs 107.4
+// frames/s). LVSG_PDL=0 turns the attribute off everywhere.
+bool pdl_enabled();
+
+__device__ __forceinline__ void pdl_grid_sync() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (pdl && pdl_enabled()) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t st, Args... args) {
+  launch_pdl(false, kernel, grid, block, smem, st, args...);
+}
+
 // ---- conv3x3 (kernels_ref.hpp:72-96 semantics, zero padding) -------------
 // Input = channel concatenation of up to 3 sources, each [B, H, W, C_i] with
 // pixel stride `pstride` floats and batch stride `bstride` floats. Optional
@@ -41,6 +80,10 @@ struct ConvArgs {
   int w_cin, w_ci0;
   // tensor-core weight image (conv3x3_tc_prepare) for conv3x3_tc; required there
   const void* wsplit;
+  // launch conv3x3_tc with programmatic dependent launch (its prologue overlaps
+  // the previous kernel's tail); only when nothing it reads before its grid
+  // dependency wait was produced by that kernel
+  int pdl;
 };
 __host__ __device__ inline int w_cin_of(const ConvArgs& a) { return a.w_cin ? a.w_cin : a.Cin; }
 // Dispatches to the tcgen05 3xTF32 kernel when it applies (Cin = Cout = 32,

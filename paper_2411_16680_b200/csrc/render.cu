@@ -66,6 +66,7 @@ __device__ __forceinline__ Taps taps_for(const RenderArgs& a, int i, int j) {
 // One thread per output pixel of the row band.
 template <int MM>
 __global__ void __launch_bounds__(128) render_fused_kernel(const RenderArgs a) {
+  pdl_grid_sync();
   extern __shared__ DevCam s_cams[];
   for (int m = threadIdx.x; m < a.M; m += blockDim.x) s_cams[m] = a.cams[m];
   __syncthreads();
@@ -139,6 +140,7 @@ __global__ void __launch_bounds__(128) render_fused_kernel(const RenderArgs a) {
 
 __global__ void upsample_activate_kernel(const RenderArgs a, float* depth, float* density,
                                          float* blend) {
+  pdl_grid_sync();
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t plane = (int64_t)a.Ho * a.Wo;
   if (idx >= plane * a.L) return;
@@ -163,17 +165,17 @@ void render_fused(const RenderArgs& a, cudaStream_t st) {
   const int g = blocks_for(n, 128);
   const size_t sm = a.M * sizeof(DevCam);
   switch (a.M) {
-    case 4: render_fused_kernel<4><<<g, 128, sm, st>>>(a); break;
-    case 8: render_fused_kernel<8><<<g, 128, sm, st>>>(a); break;
-    case 16: render_fused_kernel<16><<<g, 128, sm, st>>>(a); break;
-    default: render_fused_kernel<0><<<g, 128, sm, st>>>(a); break;
+    case 4: launch_k(render_fused_kernel<4>, g, 128, sm, st, a); break;
+    case 8: launch_k(render_fused_kernel<8>, g, 128, sm, st, a); break;
+    case 16: launch_k(render_fused_kernel<16>, g, 128, sm, st, a); break;
+    default: launch_k(render_fused_kernel<0>, g, 128, sm, st, a); break;
   }
 }
 
 void upsample_activate(const RenderArgs& a, float* depth, float* density, float* blend,
                        cudaStream_t st) {
   const int64_t n = (int64_t)a.L * a.Ho * a.Wo;
-  upsample_activate_kernel<<<blocks_for(n, 128), 128, 0, st>>>(a, depth, density, blend);
+  launch_k(upsample_activate_kernel, blocks_for(n, 128), 128, 0, st, a, depth, density, blend);
 }
 
 }  // namespace lvsg

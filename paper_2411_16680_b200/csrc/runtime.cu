@@ -392,6 +392,7 @@ void run_conv(lvsg_ctx* c, ConvArgs a, cudaStream_t st, int impl = 0, bool cache
     if (cached) {
       auto key = std::make_tuple(a.w, w_cin_of(a), a.w_ci0);
       auto it = c->wimg.find(key);
+      a.pdl = 1;
       if (it == c->wimg.end()) {
         auto buf = std::make_unique<Buf>();
         buf->ensure(nf);

@@ -83,6 +83,14 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Programmatic dependent launch: let the next kernel in the stream start its
+// prologue now / wait here until the previous kernel has completed and its
+// memory is visible (no-ops without the launch attribute).
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // One lane of a converged warp (lowest active lane) -- the issue predicate for
 // tcgen05.mma / commit: the issuing loop runs on the whole warp so descriptor
 // arithmetic stays warp-uniform (uniform registers, no per-MMA waterfall).
