@@ -361,12 +361,21 @@ def main():
             gbs = work["render_bytes"] / (stages["render"][0] / 1e3) / 1e9
             stage_rows["render"].update(gbs=round(gbs, 1), frac_hbm=round(gbs / peaks["hbm_gbs"], 4))
         dom = max(stages.items(), key=lambda kv: kv[1][0])[0] if stages else None
+        traffic = {}
+        tj = os.path.join(ROOT, "profiles", "r1", "traffic.json")
+        if os.path.exists(tj):
+            traffic = json.load(open(tj))
         if dom == "conv":
             ach = work["conv_flops"] / (stages["conv"][0] / 1e3) / 1e12
+            tc = traffic.get("conv3x3_tc_kernel", {})
             roof = {"bound": "tensor",
                     "kernel": "conv3x3_tc_kernel (all conv3x3 launches of a frame)",
                     "achieved": ach, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                    "frac": ach / peaks["bf16_tflops"], "traffic": None,
+                    "frac": ach / peaks["bf16_tflops"],
+                    "traffic": tc.get("dram_bytes_per_launch"),
+                    "traffic_note": (f"DRAM bytes of one {tc['launch']} launch vs "
+                                     f"{tc['algorithmic_bytes']} algorithmic ({tc['source']})"
+                                     if tc else None),
                     "per_unit": f"{work['conv_flops'] / 1e9:.1f} GFLOP of conv3x3 per frame",
                     "peak_source": peaks["source"] + ", dense bf16 burst",
                     "note": "achieved counts fp32 conv FLOPs; they run as a 3-term fp16 split "
