@@ -20,7 +20,8 @@
 //          Δ[m][g][p][4], 512-byte rows) into an NS-deep ring -- twice per tile
 //          (scores, then mix; the second read hits L2)
 //   w1     MMA issuer (one elected lane; warp-uniform descriptors)
-//   w2-5   consumers, thread <-> texel row <-> TMEM lane, software-pipelined
+//   w2-5   consumers (and w6-9 for h >= 2: the heads split over two groups),
+//          thread <-> texel row <-> TMEM lane, software-pipelined
 //          across tiles so neither MMA round trip is on the critical path:
 //            scores(i) [S(i) requested an iteration earlier] -> finish(i-1)
 //            [O(i-1) + V, TMA store] -> stage n(i+1) -> mix(i) -> stage heads(i)
@@ -40,8 +41,7 @@ namespace {
 
 constexpr int C = 32;
 constexpr int TILE = 128;
-constexpr int NT = 192;                    // 6 warps
-constexpr int NCONS = 128;                 // consumer threads
+constexpr int NCONS = 128;                 // threads of one consumer group
 constexpr int NJ = C / 8;                  // 8-channel fp16 K chunks
 constexpr int NG = C / 4;                  // 4-channel Δ groups
 constexpr int A_LBO = TILE * 16;           // 2 KB: one 8-channel plane of 128 rows
@@ -50,6 +50,17 @@ constexpr int A_BYTES = 2 * A_HALF;        // 16 KB per staging buffer
 constexpr int V_BYTES = TILE * C * 4;      // 16 KB
 constexpr int D_BYTES = NG * TILE * 16;    // one view slice, 16 KB
 constexpr int NV = 4;                      // V tile buffers
+
+// h >= 2: two consumer groups (warps 2-5, 6-9) split the heads over the same
+// texels, so two consumer warps share each SM sub-partition
+template <int H>
+constexpr int groups() {
+  return H >= 2 ? 2 : 1;
+}
+template <int H>
+constexpr int nthreads() {
+  return 64 + NCONS * groups<H>();
+}
 
 template <int H>
 constexpr uint32_t tmem_cols() {  // S (64h columns) + O (64 columns), power of two
@@ -91,9 +102,9 @@ __device__ __forceinline__ void stage_row(uint8_t* a, int row, const float* x) {
 
 // B rows (K-major interleave): w(n, k) for n < N, hi in rows [0, N), lo' in [N, 2N).
 template <typename F>
-__device__ __forceinline__ void stage_weights(uint8_t* b, int N, int tid, F w) {
+__device__ __forceinline__ void stage_weights(uint8_t* b, int N, int tid, int nt, F w) {
   __half* bh = reinterpret_cast<__half*>(b);
-  for (int e = tid; e < NJ * N * 8; e += NT) {
+  for (int e = tid; e < NJ * N * 8; e += nt) {
     const int k8 = e & 7, n = (e >> 3) % N, j = (e >> 3) / N;
     __half hi, lo;
     tc::split_f16(w(n, 8 * j + k8), hi, lo);
@@ -147,13 +158,14 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 }
 
 template <int H, int M>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(nthreads<H>(), 1)
     attend_tc_kernel(const __grid_constant__ CUtensorMap vmap,
                      const __grid_constant__ CUtensorMap dmap, int64_t P,
                      const float* __restrict__ wq, const float* __restrict__ wo,
                      const float* __restrict__ gain, int zero_scores, int num_tiles) {
   using S = Smem<H>;
   constexpr int NS = S::NS;
+  constexpr int NTH = nthreads<H>(), NGRP = groups<H>(), HG = H / NGRP;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::OFF_BAR);
   uint64_t* v_full = bars;            // [NV] V tile landed
@@ -175,10 +187,10 @@ __global__ void __launch_bounds__(NT, 1)
   auto tile_of = [&](int i) { return int(blockIdx.x) + i * int(gridDim.x); };
 
   // resident weights: Bq rows n = 32*i + c -> Wq_i[k][c]; Bo_i rows n -> Wo[32i + k][n]
-  stage_weights(smem + S::OFF_BQ, 32 * H, tid,
+  stage_weights(smem + S::OFF_BQ, 32 * H, tid, NTH,
                 [&](int n, int k) { return __ldg(wq + ((n >> 5) * C + k) * C + (n & 31)); });
   for (int h = 0; h < H; ++h)
-    stage_weights(smem + S::OFF_BO + h * S::BO_BYTES, 32, tid,
+    stage_weights(smem + S::OFF_BO + h * S::BO_BYTES, 32, tid, NTH,
                   [&](int n, int k) { return __ldg(wo + (h * C + k) * C + n); });
   if (tid == 0) {
     for (int k = 0; k < NV; ++k) {
@@ -191,7 +203,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
     for (int k = 0; k < NS; ++k) {
       tc::mbar_init(&d_full[k], 1);
-      tc::mbar_init(&d_empty[k], NCONS);
+      tc::mbar_init(&d_empty[k], NCONS * NGRP);
     }
     tc::mbar_init(s_done, 1);
     tc::mbar_init(o_done, 1);
@@ -265,20 +277,25 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
   } else {
-    // ---- consumers ----
+    // ---- consumers: group grp owns heads [grp*HG, (grp+1)*HG); group 0 also
+    //      stages n and writes V back ----
+    const int grp = (warp - 2) >> 2;
     const int q = warp & 3;
     const int row = q * 32 + lane;  // texel row of the tile == TMEM lane
     const uint32_t lane_base = uint32_t(q * 32) << 16;
     const float inv_temp = __double2float_rn(1.0 / sqrt(double(C)));
     const bool storer = warp == 2 && lane == 0;
-    int k = 0, u = 0;
-    auto stage = [&](const float* x) {  // A staging u (buffer u & 1)
+    int k = 0;
+    // A staging sequence (shared with the MMA issuer): n(0) at 0; in iteration
+    // i, n(i+1) then the H heads of tile i
+    auto u_n = [&](int j) { return j == 0 ? 0 : 1 + (j - 1) * (H + 1); };
+    auto u_h = [&](int i, int h) { return 1 + i * (H + 1) + (i + 1 < ntl ? 1 : 0) + h; };
+    auto stage = [&](int u, const float* x) {  // staging u into buffer u & 1
       const int b = u & 1;
       if (u >= 2) tc::mbar_wait(&a_free[b], uint32_t(((u >> 1) - 1) & 1));
       stage_row(smem + S::OFF_A + b * A_BYTES, row, x);
       tc::fence_proxy_async();
       tc::mbar_arrive(&a_full[b]);
-      ++u;
     };
     auto slice_row = [&](float* dm) {  // this texel's row of the next Δ slice
       const int sl = k % NS;
@@ -299,7 +316,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
       for (int c = 0; c < 32; ++c) out[c] = fmaf(lo[c], 1.0f / tc::kF16LoScale, out[c]);
     };
-    auto start_tile = [&](int j) {  // n = rms_norm(V) * g -> A (requests S(j))
+    auto start_tile = [&](int j) {  // n = rms_norm(V) * g -> A (requests S(j)); group 0
       const int vb = j % NV;
       const uint8_t* vt = smem + S::OFF_V + vb * V_BYTES;
       tc::mbar_wait(&v_full[vb], uint32_t((j / NV) & 1));
@@ -315,9 +332,9 @@ __global__ void __launch_bounds__(NT, 1)
       const float r = __fdiv_rn(1.0f, __fsqrt_rn(fa(__fdiv_rn(ms, float(C)), 1e-6f)));
 #pragma unroll
       for (int c = 0; c < C; ++c) x[c] = fm(fm(x[c], r), __ldg(gain + c));
-      stage(x);
+      stage(u_n(j), x);
     };
-    auto finish_tile = [&](int j) {  // V(j) += O(j), TMA store
+    auto finish_tile = [&](int j) {  // V(j) += O(j), TMA store; group 0
       const int vb = j % NV;
       uint8_t* vt = smem + S::OFF_V + vb * V_BYTES;
       tc::mbar_wait(o_done, uint32_t(j & 1));
@@ -347,21 +364,22 @@ __global__ void __launch_bounds__(NT, 1)
       }
     };
 
-    start_tile(0);
+    if (grp == 0) start_tile(0);
     for (int i = 0; i < ntl; ++i) {
-      // ---- scores(i): S held in registers, one pass over Δ ----
-      float w[H][M];
+      // ---- scores(i) for this group's heads: S in registers, one pass over Δ ----
+      float w[HG][M];
       if (zero_scores) {
 #pragma unroll
-        for (int h = 0; h < H; ++h)
+        for (int h = 0; h < HG; ++h)
 #pragma unroll
           for (int m = 0; m < M; ++m) w[h][m] = __fdiv_rn(1.0f, float(M));
       } else {
-        float sv[H][C];
+        float sv[HG][C];
         tc::mbar_wait(s_done, uint32_t(i & 1));
         tc::fence_after();
 #pragma unroll
-        for (int h = 0; h < H; ++h) tmem_split(tmem_s + uint32_t(32 * h), 32 * H, sv[h]);
+        for (int h = 0; h < HG; ++h)
+          tmem_split(tmem_s + uint32_t(32 * (grp * HG + h)), 32 * H, sv[h]);
         tc::fence_before();
         // views in pairs, each dot as 4 interleaved partial sums: 8 independent
         // 8-deep FMA chains instead of one 32-deep chain per (view, head)
@@ -371,7 +389,7 @@ __global__ void __launch_bounds__(NT, 1)
           slice_row(d0);
           slice_row(d1);
 #pragma unroll
-          for (int h = 0; h < H; ++h) {
+          for (int h = 0; h < HG; ++h) {
             float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int c = 0; c < C; c += 4) {
@@ -387,7 +405,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
         // softmax over views (tape.hpp:390-404: max, exp(x - max), sum, * 1/sum)
 #pragma unroll
-        for (int h = 0; h < H; ++h) {
+        for (int h = 0; h < HG; ++h) {
           float mx = w[h][0];
 #pragma unroll
           for (int m = 1; m < M; ++m) mx = fmaxf(mx, w[h][m]);
@@ -402,12 +420,14 @@ __global__ void __launch_bounds__(NT, 1)
           for (int m = 0; m < M; ++m) w[h][m] = fm(w[h][m], inv);
         }
       }
-      if (i > 0) finish_tile(i - 1);
-      if (i + 1 < ntl) start_tile(i + 1);
-      // ---- mix(i): every head in one pass over Δ ----
-      float hd[H][C];
+      if (grp == 0) {
+        if (i > 0) finish_tile(i - 1);
+        if (i + 1 < ntl) start_tile(i + 1);
+      }
+      // ---- mix(i): this group's heads in one pass over Δ ----
+      float hd[HG][C];
 #pragma unroll
-      for (int h = 0; h < H; ++h)
+      for (int h = 0; h < HG; ++h)
 #pragma unroll
         for (int c = 0; c < C; ++c) hd[h][c] = 0.f;
 #pragma unroll
@@ -416,16 +436,18 @@ __global__ void __launch_bounds__(NT, 1)
         slice_row(d0);
         slice_row(d1);
 #pragma unroll
-        for (int h = 0; h < H; ++h)
+        for (int h = 0; h < HG; ++h)
 #pragma unroll
           for (int c = 0; c < C; ++c)
             hd[h][c] = fmaf(w[h][m + 1], d1[c], fmaf(w[h][m], d0[c], hd[h][c]));
       }
 #pragma unroll
-      for (int h = 0; h < H; ++h) stage(hd[h]);
+      for (int h = 0; h < HG; ++h) stage(u_h(i, grp * HG + h), hd[h]);
     }
-    finish_tile(ntl - 1);
-    if (storer) tc::bulk_wait<0>();
+    if (grp == 0) {
+      finish_tile(ntl - 1);
+      if (storer) tc::bulk_wait<0>();
+    }
   }
   tc::fence_before();
   __syncthreads();
@@ -487,8 +509,8 @@ void launch(float* V, const float* D, int64_t P, const float* wq, const float* w
   }
   const int tiles = int((P + TILE - 1) / TILE);
   const int grid = tiles < sms ? tiles : sms;
-  launch_pdl(true, attend_tc_kernel<H, M>, grid, NT, Smem<H>::BYTES, st, vmap, dmap, P, wq, wo,
-             gain, zero, tiles);
+  launch_pdl(true, attend_tc_kernel<H, M>, grid, nthreads<H>(), Smem<H>::BYTES, st, vmap, dmap, P,
+             wq, wo, gain, zero, tiles);
 }
 
 }  // namespace
