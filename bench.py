@@ -287,7 +287,9 @@ def main():
     Ho, Wo = plan.out_height, plan.out_width
     rgb = torch.empty((Ho, Wo, 3), dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
-    stream = torch.cuda.current_stream()
+    # one dedicated stream carries the frames, the L2 flushes and the timing
+    # events (the library enqueues every kernel of the frame on it)
+    stream = torch.cuda.Stream(device=dev)
 
     def step():
         model.forward_render_device(enc, case.enc_cams, ren, case.ren_cams, case.target, rgb,
@@ -310,7 +312,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local) as clocks, torch.cuda.stream(stream):
         for k in range(args.steps):
             flush.zero_()
             ev[k][0].record(stream)

@@ -15,6 +15,13 @@ bool pdl_enabled() {
   }();
   return on;
 }
+bool pdl_all() {
+  static const bool on = [] {
+    const char* e = getenv("LVSG_PDL");
+    return e && e[0] == '2';
+  }();
+  return on;
+}
 
 namespace {
 

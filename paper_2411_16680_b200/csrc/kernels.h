@@ -20,6 +20,7 @@ namespace lvsg {
 // running persistent kernel and slow it down (measured: 111.6 vs 107.4
 // frames/s). LVSG_PDL=0 turns the attribute off everywhere.
 bool pdl_enabled();
+bool pdl_all();  // LVSG_PDL=2: the attribute on every launch (measurement switch)
 
 __device__ __forceinline__ void pdl_grid_sync() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -36,7 +37,7 @@ inline void launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = (pdl && pdl_enabled()) ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = ((pdl || pdl_all()) && pdl_enabled()) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);

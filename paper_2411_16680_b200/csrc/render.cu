@@ -36,14 +36,32 @@ __device__ __forceinline__ void ldm_sample(const RenderArgs& a, int l, const Tap
   const int M = MM > 0 ? MM : a.M;
   const float* lg = a.logits + l * plane * M;
   float mx = 0.f;
+  if (MM > 0 && MM % 4 == 0) {  // each tap's M logits as float4 runs
+    const float4* q00 = reinterpret_cast<const float4*>(lg + ((int64_t)t.y0 * a.W + t.x0) * M);
+    const float4* q10 = reinterpret_cast<const float4*>(lg + ((int64_t)t.y0 * a.W + t.x1) * M);
+    const float4* q01 = reinterpret_cast<const float4*>(lg + ((int64_t)t.y1 * a.W + t.x0) * M);
+    const float4* q11 = reinterpret_cast<const float4*>(lg + ((int64_t)t.y1 * a.W + t.x1) * M);
 #pragma unroll
-  for (int m = 0; m < M; ++m) {
-    const float v = lerp2(__ldg(lg + ((int64_t)t.y0 * a.W + t.x0) * M + m),
-                          __ldg(lg + ((int64_t)t.y0 * a.W + t.x1) * M + m),
-                          __ldg(lg + ((int64_t)t.y1 * a.W + t.x0) * M + m),
-                          __ldg(lg + ((int64_t)t.y1 * a.W + t.x1) * M + m), t.fx, t.fy);
-    beta[m] = v;
-    mx = m == 0 ? v : fmaxf(mx, v);
+    for (int g = 0; g < (MM > 0 ? MM : 4) / 4; ++g) {
+      const float4 A = __ldg(q00 + g), B = __ldg(q10 + g), Cc = __ldg(q01 + g), D = __ldg(q11 + g);
+      const float v[4] = {lerp2(A.x, B.x, Cc.x, D.x, t.fx, t.fy), lerp2(A.y, B.y, Cc.y, D.y, t.fx, t.fy),
+                          lerp2(A.z, B.z, Cc.z, D.z, t.fx, t.fy), lerp2(A.w, B.w, Cc.w, D.w, t.fx, t.fy)};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        beta[4 * g + k] = v[k];
+        mx = (g == 0 && k == 0) ? v[k] : fmaxf(mx, v[k]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const float v = lerp2(__ldg(lg + ((int64_t)t.y0 * a.W + t.x0) * M + m),
+                            __ldg(lg + ((int64_t)t.y0 * a.W + t.x1) * M + m),
+                            __ldg(lg + ((int64_t)t.y1 * a.W + t.x0) * M + m),
+                            __ldg(lg + ((int64_t)t.y1 * a.W + t.x1) * M + m), t.fx, t.fy);
+      beta[m] = v;
+      mx = m == 0 ? v : fmaxf(mx, v);
+    }
   }
   float sum = 0.f;
 #pragma unroll

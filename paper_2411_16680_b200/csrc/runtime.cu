@@ -51,6 +51,10 @@ DevCam dev_cam(const lvsg_camera& c) {
   d.cy = c.cy;
   d.W = int(c.width);
   d.H = int(c.height);
+  d.wm = double(d.W) - 0.5;  // IEEE binary64 like the device's __dsub_rn / __dadd_rn
+  d.hm = double(d.H) - 0.5;
+  d.hu = d.wm + 1e-4;
+  d.hv = d.hm + 1e-4;
   return d;
 }
 
@@ -842,9 +846,17 @@ void upload_images(lvsg_ctx* c, Buf& dst, int64_t views, const float* const* ima
   for (int64_t m = 0; m < views; ++m)
     if (!images[m]) throw DimError("forward: null image");
   dst.ensure(per * size_t(views));
-  for (int64_t m = 0; m < views; ++m)
-    CUDA_OK(cudaMemcpyAsync(dst.p + per * size_t(m), images[m], per * sizeof(float),
+  // host->device copies carry a large fixed cost per call on this link
+  // (profiles/h2d_bw.py: 14 GB/s at 6 MB, 50 GB/s at 199 MB): views that are
+  // adjacent in one host buffer go up as a single copy
+  int64_t m = 0;
+  while (m < views) {
+    int64_t run = 1;
+    while (m + run < views && images[m + run] == images[m] + per * size_t(run)) ++run;
+    CUDA_OK(cudaMemcpyAsync(dst.p + per * size_t(m), images[m], per * size_t(run) * sizeof(float),
                             cudaMemcpyHostToDevice, st));
+    m += run;
+  }
 }
 
 void check_views(lvsg_ctx* c, int64_t views, int64_t H, int64_t W) {
@@ -1111,7 +1123,9 @@ lvsg_status lvsg_forward_render(lvsg_ctx* c, int64_t views, const float* const* 
     for (int64_t m = 0; m < views; ++m) camera_validate(render_cams[m]);
     upload_images(c, c->enc_in, views, enc_images, enc_h, enc_w, c->stream);
     // the render views are needed only by the final render: upload them on the
-    // copy stream under the forward pass (after any earlier use of ren_in)
+    // copy stream under the forward pass, after the encoder views (which gate
+    // the forward and so get the host link to themselves) and after any earlier
+    // use of ren_in
     CUDA_OK(cudaEventRecord(c->ev_main, c->stream));
     CUDA_OK(cudaStreamWaitEvent(c->xfer, c->ev_main, 0));
     upload_images(c, c->ren_in, views, render_images, render_h, render_w, c->xfer);

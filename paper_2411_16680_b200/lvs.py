@@ -144,6 +144,20 @@ def scene_images(seed: int, planes: int, scene_frustum: Frustum,
     return out
 
 
+# cudaStreamLegacy: torch's default stream reports handle 0, which the C ABI
+# reads as "the context's own stream"; pass the legacy default stream instead
+# so the work really is ordered with the caller's stream (events, copies).
+_CUDA_STREAM_LEGACY = 1
+
+
+def _stream_handle(stream) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    h = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    return h if h else _CUDA_STREAM_LEGACY
+
+
 def _cam_array(cams: Sequence[Camera]):
     return (capi.CameraC * len(cams))(*[c.to_c() for c in cams])
 
@@ -274,9 +288,7 @@ class Model:
         for t in (enc_images, render_images, rgb_out):
             if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
                 raise capi.DimError("device tensors must be contiguous float32 CUDA tensors")
-        if stream is None:
-            stream = torch.cuda.current_stream()
-        sh = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        sh = _stream_handle(stream)
         M, He, We, _ = enc_images.shape
         _, Hr, Wr, _ = render_images.shape
         fr = target.to_c()
@@ -286,10 +298,7 @@ class Model:
             rgb_out.data_ptr(), sh))
 
     def render_rows_device(self, render_images, render_cams, row0, row1, rgb_out, stream=None):
-        import torch
-        if stream is None:
-            stream = torch.cuda.current_stream()
-        sh = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        sh = _stream_handle(stream)
         M, Hr, Wr, _ = render_images.shape
         self._check(self._lib.lvsg_render_rows_device(self._h, M, render_images.data_ptr(), Hr, Wr,
                                                       _cam_array(render_cams), row0, row1,
