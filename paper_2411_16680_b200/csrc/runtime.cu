@@ -169,6 +169,7 @@ struct lvsg_ctx {
   cudaStream_t xfer = nullptr;
   cudaEvent_t ev_main = nullptr, ev_ren = nullptr;
   cudaEvent_t ev_band[4] = {};
+  std::vector<cudaEvent_t> ev_enc;  // per-view encoder upload landed
 
   // resident forward result (for lvsg_render)
   bool have_ldm = false;
@@ -583,9 +584,14 @@ CamTables upload_cams(lvsg_ctx* c, const lvsg_camera* enc_cams, const lvsg_frust
 
 // forward() on device images [M, He, We, 3]; leaves pre_d / pre_s / logits
 // (volume resolution) and the final V resident.
+// enc_ready (optional, one event per view): view m's encoder image is only
+// valid on the device once enc_ready[m] has fired (host-ABI uploads); level 0
+// of the encoder then runs view by view so each view's upload overlaps the
+// previous view's convolutions.
 void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
                     const lvsg_camera* enc_cams, const lvsg_frustum& target,
-                    const lvsg_camera* render_cams, CamTables* tables_out) {
+                    const lvsg_camera* render_cams, CamTables* tables_out,
+                    const cudaEvent_t* enc_ready = nullptr) {
   const Config& cfg = c->cfg;
   if (!c->have_weights) throw DimError("forward: no weights loaded (lvsg_load_weights / lvsg_init_weights)");
   frustum_validate(target);
@@ -607,13 +613,37 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
   // ---- encode_inputs --------------------------------------------------------
   {
     int h = int(He), w = int(We);
-    ConvArgs a = conv_args(M, h, w, 3, C, W.stem_w, W.stem_b, c->enc_x.p);
-    a.src[0] = ConvSrc{enc, 3, 3, (long long)h * w * 3};
-    a.nsrc = 1;
-    run_conv(c, a, st);
-    mark(c, "conv", 1);
     const float* x = c->enc_x.p;
-    for (int k = 0; k < K; ++k) {
+    int k0 = 0;
+    if (enc_ready) {
+      // level 0 per view, each behind its upload
+      const size_t per_in = size_t(h) * w * 3, per_x = size_t(h) * w * C;
+      const size_t per_f = size_t(h / 2) * (w / 2) * C;
+      for (int m = 0; m < M; ++m) {
+        CUDA_OK(cudaStreamWaitEvent(st, enc_ready[m], 0));
+        float* xm = c->enc_x.p + per_x * m;
+        ConvArgs a = conv_args(1, h, w, 3, C, W.stem_w, W.stem_b, xm);
+        a.src[0] = ConvSrc{enc + per_in * m, 3, 3, (long long)per_in};
+        a.nsrc = 1;
+        run_conv(c, a, st);
+        mark(c, "conv", 1);
+        conv_residual(c, xm, xm, c->enc_t.p, 1, h, w, W.lvl_r1[0]);
+        conv_residual(c, xm, xm, c->enc_t.p, 1, h, w, W.lvl_r2[0]);
+        mean_pool2(xm, c->feats[0].p + per_f * m, 1, h, w, C, st);
+        mark(c, "misc", 1);
+      }
+      h /= 2;
+      w /= 2;
+      x = c->feats[0].p;
+      k0 = 1;
+    } else {
+      ConvArgs a = conv_args(M, h, w, 3, C, W.stem_w, W.stem_b, c->enc_x.p);
+      a.src[0] = ConvSrc{enc, 3, 3, (long long)h * w * 3};
+      a.nsrc = 1;
+      run_conv(c, a, st);
+      mark(c, "conv", 1);
+    }
+    for (int k = k0; k < K; ++k) {
       float* xo = k == 0 ? c->enc_x.p : c->enc_x.p;  // level >= 1 reads feats[k-1], writes enc_x
       conv_residual(c, x, xo, c->enc_t.p, M, h, w, W.lvl_r1[size_t(k)]);
       conv_residual(c, xo, xo, c->enc_t.p, M, h, w, W.lvl_r2[size_t(k)]);
@@ -1018,6 +1048,7 @@ void lvsg_destroy(lvsg_ctx* c) {
   for (cudaEvent_t e : {c->ev_main, c->ev_ren, c->ev_band[0], c->ev_band[1], c->ev_band[2],
                         c->ev_band[3]})
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ev_enc) cudaEventDestroy(e);
   if (c->xfer) cudaStreamDestroy(c->xfer);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -1121,17 +1152,32 @@ lvsg_status lvsg_forward_render(lvsg_ctx* c, int64_t views, const float* const* 
     check_views(c, views, enc_h, enc_w);
     check_views(c, views, render_h, render_w);
     for (int64_t m = 0; m < views; ++m) camera_validate(render_cams[m]);
-    upload_images(c, c->enc_in, views, enc_images, enc_h, enc_w, c->stream);
-    // the render views are needed only by the final render: upload them on the
-    // copy stream under the forward pass, after the encoder views (which gate
-    // the forward and so get the host link to themselves) and after any earlier
-    // use of ren_in
+    // All uploads go on the copy stream (after any earlier use of the input
+    // buffers): the encoder views one by one, each with an event the encoder's
+    // per-view level 0 waits on, then the render views, needed only by the
+    // final render, under the rest of the forward pass.
     CUDA_OK(cudaEventRecord(c->ev_main, c->stream));
     CUDA_OK(cudaStreamWaitEvent(c->xfer, c->ev_main, 0));
+    const size_t per = size_t(enc_h * enc_w * 3);
+    if (!enc_images) throw DimError("forward: null image list");
+    for (int64_t m = 0; m < views; ++m)
+      if (!enc_images[m]) throw DimError("forward: null image");
+    c->enc_in.ensure(per * size_t(views));
+    while (c->ev_enc.size() < size_t(views)) {
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->ev_enc.push_back(e);
+    }
+    for (int64_t m = 0; m < views; ++m) {
+      CUDA_OK(cudaMemcpyAsync(c->enc_in.p + per * size_t(m), enc_images[m], per * sizeof(float),
+                              cudaMemcpyHostToDevice, c->xfer));
+      CUDA_OK(cudaEventRecord(c->ev_enc[size_t(m)], c->xfer));
+    }
     upload_images(c, c->ren_in, views, render_images, render_h, render_w, c->xfer);
     CUDA_OK(cudaEventRecord(c->ev_ren, c->xfer));
     CamTables t;
-    forward_device(c, c->enc_in.p, enc_h, enc_w, enc_cams, *target, render_cams, &t);
+    forward_device(c, c->enc_in.p, enc_h, enc_w, enc_cams, *target, render_cams, &t,
+                   c->ev_enc.data());
     const int64_t Ho = c->plan.out_height, Wo = c->plan.out_width;
     c->rgb.ensure(size_t(Ho * Wo * 3));
     CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev_ren, 0));
