@@ -214,3 +214,31 @@ def test_config2_full_scale_matches_oracle(oracle):
     np.save("gpurun_out/config2_full_gpu_rgb.npy", rgb) if __import__("os").path.isdir(
         "gpurun_out") else None
     assert d.max() <= RGB_MAX_ABS and psnr(rgb, want) >= RGB_PSNR_DB
+
+
+def _variants():
+    from paper_2411_16680_b200 import workloads as wl
+    return {
+        # 16 views (4x4 rig): the M = 16 attention / blend / render kernels
+        "config3_div4": lambda: wl.config3(div=4),
+        # a moving scene (config 4's frame sequence), frame 3
+        "config4_frame3_div4": lambda: wl.config4_frame(3, div=4),
+        # an off-centre target (one of config 5's eight viewpoints)
+        "config5_target5_div4": lambda: wl.config2(div=4, target_center=wl.config5_targets()[5]),
+        # 4 views (2x2 rig): the M = 4 kernels
+        "config2_m4_div4": lambda: wl.config2(div=4, views_rig=(2, 2)),
+    }
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", list(_variants()))
+def test_config_variants_match_oracle(oracle, name):
+    """The config-2 schedule at 1/4 extents across the view counts and target
+    poses of BASELINE.json's configs 3-5."""
+    case = _variants()[name]()
+    _, rgb = run_gpu(case)
+    want = run_oracle(oracle, case)["rgb"]
+    err = float(np.abs(rgb - want).max())
+    print(f"{name}: max-abs {err:.3e} psnr {psnr(rgb, want):.1f} dB")
+    assert np.isfinite(rgb).all()
+    assert err <= RGB_MAX_ABS and psnr(rgb, want) >= RGB_PSNR_DB
