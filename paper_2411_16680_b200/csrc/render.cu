@@ -83,7 +83,7 @@ __device__ __forceinline__ Taps taps_for(const RenderArgs& a, int i, int j) {
 
 // One thread per output pixel of the row band.
 template <int MM>
-__global__ void __launch_bounds__(128) render_fused_kernel(const RenderArgs a) {
+__global__ void __launch_bounds__(128, MM == 16 ? 4 : 6) render_fused_kernel(const RenderArgs a) {
   pdl_grid_sync();
   extern __shared__ DevCam s_cams[];
   for (int m = threadIdx.x; m < a.M; m += blockDim.x) s_cams[m] = a.cams[m];
