@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(NT, 1)
           const unsigned qm = __activemask();  // the loop tail cuts at a quad boundary
           ms += __shfl_xor_sync(qm, ms, 1);
           ms += __shfl_xor_sync(qm, ms, 2);
-          const float rr = __fdiv_rn(1.0f, __fsqrt_rn(fa(__fdiv_rn(ms, 32.0f), 1e-6f)));
+          const float rr = __fdiv_rn(1.0f, __fsqrt_rn(fa(fm(ms, 0.03125f), 1e-6f)));  // ms / 32, exactly
 #pragma unroll
           for (int k = 0; k < 8; ++k) v[k] = fm(fm(v[k], rr), g8[k]);
         }
