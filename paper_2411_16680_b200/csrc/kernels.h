@@ -100,6 +100,15 @@ void conv3x3_tc(const ConvArgs& a, cudaStream_t st);
 // memory layout, loaded by one bulk copy per CTA.
 constexpr size_t kConvTcWeightBytes = 9 * 4 * 64 * 16;
 void conv3x3_tc_prepare(const ConvArgs& a, void* dst, cudaStream_t st);
+// 1-D Winograd F(2,3) tensor-core conv (conv_wino.cu): same shapes as
+// conv3x3_tc; its weight image holds G g per (xi, dy) (48 KB).
+bool conv3x3_wino_supported(const ConvArgs& a);
+void conv3x3_wino(const ConvArgs& a, cudaStream_t st);
+constexpr size_t kConvWinoWeightBytes = 4 * 3 * 4 * 64 * 16;
+void conv3x3_wino_prepare(const ConvArgs& a, void* dst, cudaStream_t st);
+// Which conv runs: 1 SIMT / stem, 2 direct tensor core, 3 Winograd tensor core
+// (impl: 0 auto = direct tensor core where supported; LVSG_CONV=simt|wino).
+int conv3x3_path(const ConvArgs& a, int impl = 0);
 
 // ---- elementwise / layout ------------------------------------------------
 void fill_rows(float* out, const float* row, int64_t rows, int C, cudaStream_t st);

@@ -392,22 +392,30 @@ ConvArgs conv_args(int B, int H, int W, int Cin, int Cout, const float* w, const
 // from the context cache (cached = true: weights bound to the context) or a
 // fresh one in scratch (stage entry points: arbitrary caller weights).
 void run_conv(lvsg_ctx* c, ConvArgs a, cudaStream_t st, int impl = 0, bool cached = true) {
-  if (conv3x3_uses_tc(a, impl)) {
-    const size_t nf = kConvTcWeightBytes / sizeof(float);
+  const int path = conv3x3_path(a, impl);
+  if (path >= 2) {
+    const bool wino = path == 3;
+    const size_t nf = (wino ? kConvWinoWeightBytes : kConvTcWeightBytes) / sizeof(float);
+    auto prepare = [&](void* dst) {
+      if (wino)
+        conv3x3_wino_prepare(a, dst, st);
+      else
+        conv3x3_tc_prepare(a, dst, st);
+    };
     if (cached) {
-      auto key = std::make_tuple(a.w, w_cin_of(a), a.w_ci0);
+      auto key = std::make_tuple(a.w, w_cin_of(a), a.w_ci0 + (wino ? (1 << 20) : 0));
       auto it = c->wimg.find(key);
       a.pdl = 1;
       if (it == c->wimg.end()) {
         auto buf = std::make_unique<Buf>();
         buf->ensure(nf);
-        conv3x3_tc_prepare(a, buf->p, st);
+        prepare(buf->p);
         it = c->wimg.emplace(key, std::move(buf)).first;
       }
       a.wsplit = it->second->p;
     } else {
       c->wimg_tmp.ensure(nf);
-      conv3x3_tc_prepare(a, c->wimg_tmp.p, st);
+      prepare(c->wimg_tmp.p);
       a.wsplit = c->wimg_tmp.p;
     }
   }

@@ -33,14 +33,15 @@ def main():
         "rms_gelu": dict(norm_gain_t=gain, gelu=True),
         "resid": dict(resid_t=res),
     }
-    out = {"lib": os.environ.get("LVSG_LIB", "default"), "shape": [B, H, W, C]}
+    impl = int(os.environ.get("CONV_IMPL", "2"))
+    out = {"lib": os.environ.get("LVSG_LIB", "default"), "impl": impl, "shape": [B, H, W, C]}
     for name, kw in variants.items():
         ts = []
         for it in range(8):
             flush.fill_(it)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            m.stage_conv3x3_fused(x, w, b, y, C, impl=2, **kw)
+            m.stage_conv3x3_fused(x, w, b, y, C, impl=impl, **kw)
             e1.record(st)
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) * 1000)
