@@ -72,8 +72,8 @@ constexpr int OFF_RES = OFF_OUT + NEW * SUB_BYTES;
 constexpr int OFF_W = OFF_RES + NEW * SUB_BYTES;
 constexpr int OFF_RAW = OFF_W + W_BYTES;
 constexpr int OFF_PLANES = OFF_RAW + NR * RAW_BYTES;
-constexpr int OFF_SMALL = OFF_PLANES + NP * PLANES_BYTES;  // rms[192], bias[32], gain[32]
-constexpr int OFF_BAR = OFF_SMALL + 256 * 4;
+constexpr int OFF_SMALL = OFF_PLANES + NP * PLANES_BYTES;  // rms[192], bias[32], gain[32], walpha[288]
+constexpr int OFF_BAR = OFF_SMALL + (256 + 288) * 4;
 constexpr int NBAR = 2 * NR + 2 * NP + 2 * NA + NEW + 1;
 constexpr int SMEM_BYTES = OFF_BAR + NBAR * 8 + 16;
 constexpr int NT = 64 + 128 + 128 * EPW;
@@ -120,6 +120,7 @@ __device__ __forceinline__ uint32_t swz(int r, int c4) {
   return uint32_t(r * 128 + ((c4 ^ (r & 7)) << 4));
 }
 
+template <bool kAlpha>
 __global__ void __launch_bounds__(NT, 1)
     conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap,
                       const __grid_constant__ CUtensorMap omap,
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(NT, 1)
   float* rms_s = reinterpret_cast<float*>(smem + OFF_SMALL);
   float* bias_s = rms_s + 192;
   float* gain_s = bias_s + 32;
+  float* walpha_s = gain_s + 32;  // [tap][co] weights of the folded alpha channel
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* raw_full = bars;                 // [NR] TMA bytes landed
   uint64_t* raw_empty = raw_full + NR;       // [NR] converters done reading raw
@@ -147,6 +149,11 @@ __global__ void __launch_bounds__(NT, 1)
 
   if (tid < 32) bias_s[tid] = a.bias ? __ldg(a.bias + tid) : 0.f;
   else if (tid < 64) gain_s[tid - 32] = a.gain ? __ldg(a.gain + tid - 32) : 1.f;
+  if constexpr (kAlpha)
+    for (int e = tid; e < 288; e += NT) {
+      const int co = e & 31, tap = e >> 5;
+      walpha_s[e] = __ldg(a.w + ((long long)co * w_cin_of(a) + a.alpha_ci) * 9 + tap);
+    }
   tc::fence_proxy_async();
   if (tid == 0) {
     for (int k = 0; k < NR; ++k) {
@@ -305,9 +312,28 @@ __global__ void __launch_bounds__(NT, 1)
       tc::mbar_arrive(&acc_empty[ac]);
       const TileCoord tt = tile_coord(t, a.H, a.W);
       const bool valid = sub_valid(tt);
+      float al[9];
+      if constexpr (kAlpha) {  // the folded single-channel input: its 9 taps here
+        const int row = q * 32 + lane;  // tile row m <-> pixel (y0 + m/8, x0 + m%8)
+        const int py = tt.y0 + (row >> 3), px = tt.x0 + (row & 7);
+        const float* ab = a.alpha + (long long)tt.b * a.alpha_bstride;
+#pragma unroll
+        for (int tap = 0; tap < 9; ++tap) {
+          const int yy = py + tap / 3 - 1, xx = px + tap % 3 - 1;
+          al[tap] = (yy >= 0 && yy < a.H && xx >= 0 && xx < a.W)
+                        ? __ldg(ab + ((long long)yy * a.W + xx) * a.alpha_pstride)
+                        : 0.f;
+        }
+      }
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
         float y_ = fmaf(d1[c], 1.0f / tc::kF16LoScale, d0[c]);
+        if constexpr (kAlpha) {
+          float s = 0.f;
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) s = fmaf(al[tap], walpha_s[tap * 32 + c], s);
+          y_ = fa(y_, s);
+        }
         if (a.bias) y_ = fa(y_, bias_s[c]);
         if (a.gelu) y_ = gelu_ref(y_);
         d0[c] = y_;
@@ -417,7 +443,10 @@ void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
     throw CudaError("conv3x3_tc: missing or misaligned weight image (conv3x3_tc_prepare)");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(conv3x3_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(conv3x3_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SMEM_BYTES);
+    cudaFuncSetAttribute(conv3x3_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SMEM_BYTES);
     attr = true;
   }
   const ConvSrc& S = a.src[0];
@@ -446,7 +475,8 @@ void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
   lattr[0].val.programmaticStreamSerializationAllowed = (a.pdl && pdl_enabled()) ? 1 : 0;
   cfg.attrs = lattr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, conv3x3_tc_kernel, xmap, omap, rmap, a, tiles) != cudaSuccess)
+  if (cudaLaunchKernelEx(&cfg, a.alpha ? conv3x3_tc_kernel<true> : conv3x3_tc_kernel<false>, xmap,
+                         omap, rmap, a, tiles) != cudaSuccess)
     throw CudaError("conv3x3_tc: launch failed");
 }
 

@@ -85,6 +85,13 @@ struct ConvArgs {
   // the previous kernel's tail); only when nothing it reads before its grid
   // dependency wait was produced by that kernel
   int pdl;
+  // conv3x3_tc only: one extra single-channel input folded into the epilogue
+  // (the feedback's alpha channel of the update-CNN stem): out += sum_tap
+  // alpha(y+dy-1, x+dx-1) * w[co][alpha_ci][tap], alpha at alpha[b*alpha_bstride
+  // + pix*alpha_pstride] (a separate kernel instantiation)
+  const float* alpha;
+  int alpha_pstride, alpha_ci;
+  long long alpha_bstride;
 };
 __host__ __device__ inline int w_cin_of(const ConvArgs& a) { return a.w_cin ? a.w_cin : a.Cin; }
 // Dispatches to the tcgen05 3xTF32 kernel when it applies (Cin = Cout = 32,

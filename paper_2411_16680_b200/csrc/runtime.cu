@@ -473,6 +473,17 @@ void update_cnn(lvsg_ctx* c, const StepW& sw, const ConvArgs& stem_in, int M, in
       const ConvSrc& S = a.src[s];
       for (int c0 = 0; c0 < S.C; c0 += 32) {
         const int cn = std::min(32, S.C - c0);
+        if (cn == 1 && !parts.empty() && parts.back().src[0].ptr == S.ptr + c0 - 32 &&
+            conv3x3_path(parts.back()) == 2) {
+          // a trailing single channel (the feedback's alpha) folds into the
+          // previous tensor-core part's epilogue instead of its own launch
+          ConvArgs& q = parts.back();
+          q.alpha = S.ptr + c0;
+          q.alpha_pstride = int(S.pstride);
+          q.alpha_bstride = S.bstride;
+          q.alpha_ci = ci0 + c0;
+          continue;
+        }
         ConvArgs p = conv_args(M, Hf, Wf, cn, C, sw.stem_w, parts.empty() ? sw.stem_b : nullptr, c->uh.p);
         p.src[0] = ConvSrc{S.ptr + c0, cn, S.pstride, S.bstride};
         p.nsrc = 1;
