@@ -120,7 +120,7 @@ __device__ __forceinline__ uint32_t swz(int r, int c4) {
   return uint32_t(r * 128 + ((c4 ^ (r & 7)) << 4));
 }
 
-template <bool kAlpha>
+template <bool kAlpha, bool kPool>
 __global__ void __launch_bounds__(NT, 1)
     conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap,
                       const __grid_constant__ CUtensorMap omap,
@@ -352,6 +352,30 @@ __global__ void __launch_bounds__(NT, 1)
         __syncwarp();
       }
       if (has_res && t + step < num_tiles) res_issue(t + step);
+      if constexpr (kPool) {
+        // the encoder's mean_pool2 of this warp's 4 x 8 sub-box: 2 x 2 groups
+        // are lanes (l, l+1, l+8, l+9); same summation order as mean_pool2
+        if (valid) {
+          const int py = tt.y0 + sy + (lane >> 3), px = tt.x0 + (lane & 7);
+          const bool writer = !(lane & 1) && !((lane >> 3) & 1) && (py >> 1) < (a.H >> 1) &&
+                              (px >> 1) < (a.W >> 1);
+          float* po = a.pool_out + (long long)tt.b * a.pool_bstride +
+                      ((long long)(py >> 1) * (a.W >> 1) + (px >> 1)) * 32;
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4) {
+            float r[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float v00 = d0[4 * c4 + k];
+              const float v01 = __shfl_down_sync(0xffffffffu, v00, 1);
+              const float v10 = __shfl_down_sync(0xffffffffu, v00, 8);
+              const float v11 = __shfl_down_sync(0xffffffffu, v00, 9);
+              r[k] = fm(fa(fa(fa(v00, v01), v10), v11), 0.25f);
+            }
+            if (writer) *reinterpret_cast<float4*>(po + 4 * c4) = make_float4(r[0], r[1], r[2], r[3]);
+          }
+        }
+      }
       if (!valid) continue;
       if (lane == 0) tc::bulk_wait_read<0>();  // previous store left the staging buffer
       __syncwarp();
@@ -443,10 +467,12 @@ void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
     throw CudaError("conv3x3_tc: missing or misaligned weight image (conv3x3_tc_prepare)");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(conv3x3_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SMEM_BYTES);
-    cudaFuncSetAttribute(conv3x3_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SMEM_BYTES);
+    cudaFuncSetAttribute(conv3x3_tc_kernel<false, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(conv3x3_tc_kernel<true, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(conv3x3_tc_kernel<false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr = true;
   }
   const ConvSrc& S = a.src[0];
@@ -475,8 +501,11 @@ void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
   lattr[0].val.programmaticStreamSerializationAllowed = (a.pdl && pdl_enabled()) ? 1 : 0;
   cfg.attrs = lattr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, a.alpha ? conv3x3_tc_kernel<true> : conv3x3_tc_kernel<false>, xmap,
-                         omap, rmap, a, tiles) != cudaSuccess)
+  auto kern = a.alpha      ? conv3x3_tc_kernel<true, false>
+              : a.pool_out ? conv3x3_tc_kernel<false, true>
+                           : conv3x3_tc_kernel<false, false>;
+  if (a.alpha && a.pool_out) throw CudaError("conv3x3_tc: alpha and pool together are not built");
+  if (cudaLaunchKernelEx(&cfg, kern, xmap, omap, rmap, a, tiles) != cudaSuccess)
     throw CudaError("conv3x3_tc: launch failed");
 }
 

@@ -92,6 +92,10 @@ struct ConvArgs {
   const float* alpha;
   int alpha_pstride, alpha_ci;
   long long alpha_bstride;
+  // conv3x3_tc only: also write the 2x2 mean pool of the output (the encoder's
+  // mean_pool2, same summation order) to pool_out [B, H/2, W/2, 32]
+  float* pool_out;
+  long long pool_bstride;
 };
 __host__ __device__ inline int w_cin_of(const ConvArgs& a) { return a.w_cin ? a.w_cin : a.Cin; }
 // Dispatches to the tcgen05 3xTF32 kernel when it applies (Cin = Cout = 32,

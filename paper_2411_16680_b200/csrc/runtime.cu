@@ -429,8 +429,10 @@ void add_src(ConvArgs& a, const float* p, int C, int H, int W) {
 
 // x = x + conv(gelu(conv(x))) on [B,H,W,C] (network.hpp:150-153); with
 // `out` != x the sum lands in out (x untouched).
+// pool_out (optional): also the 2x2 mean pool of the result ([B,H/2,W/2,C]),
+// fused into the second conv's epilogue on the tensor-core path.
 void conv_residual(lvsg_ctx* c, const float* x, float* out, float* tmp, int B, int H, int W,
-                   const ConvPairW& p) {
+                   const ConvPairW& p, float* pool_out = nullptr) {
   const int C = int(c->cfg.channels);
   ConvArgs a = conv_args(B, H, W, C, C, p.w1, p.b1, tmp);
   add_src(a, x, C, H, W);
@@ -441,8 +443,17 @@ void conv_residual(lvsg_ctx* c, const float* x, float* out, float* tmp, int B, i
   b2.resid = x;
   b2.res_pstride = C;
   b2.res_bstride = (long long)H * W * C;
+  const bool fuse_pool = pool_out && conv3x3_path(b2) == 2;
+  if (fuse_pool) {
+    b2.pool_out = pool_out;
+    b2.pool_bstride = (long long)(H / 2) * (W / 2) * C;
+  }
   run_conv(c, b2, c->stream);
   mark(c, "conv", 2);
+  if (pool_out && !fuse_pool) {
+    mean_pool2(out, pool_out, B, H, W, C, c->stream);
+    mark(c, "misc", 1);
+  }
 }
 
 // run_update_cnn (network.hpp:155-160) on concatenated sources, all views.
@@ -647,9 +658,7 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
         run_conv(c, a, st);
         mark(c, "conv", 1);
         conv_residual(c, xm, xm, c->enc_t.p, 1, h, w, W.lvl_r1[0]);
-        conv_residual(c, xm, xm, c->enc_t.p, 1, h, w, W.lvl_r2[0]);
-        mean_pool2(xm, c->feats[0].p + per_f * m, 1, h, w, C, st);
-        mark(c, "misc", 1);
+        conv_residual(c, xm, xm, c->enc_t.p, 1, h, w, W.lvl_r2[0], c->feats[0].p + per_f * m);
       }
       h /= 2;
       w /= 2;
@@ -665,9 +674,7 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
     for (int k = k0; k < K; ++k) {
       float* xo = k == 0 ? c->enc_x.p : c->enc_x.p;  // level >= 1 reads feats[k-1], writes enc_x
       conv_residual(c, x, xo, c->enc_t.p, M, h, w, W.lvl_r1[size_t(k)]);
-      conv_residual(c, xo, xo, c->enc_t.p, M, h, w, W.lvl_r2[size_t(k)]);
-      mean_pool2(xo, c->feats[size_t(k)].p, M, h, w, C, st);
-      mark(c, "misc", 1);
+      conv_residual(c, xo, xo, c->enc_t.p, M, h, w, W.lvl_r2[size_t(k)], c->feats[size_t(k)].p);
       h /= 2;
       w /= 2;
       x = c->feats[size_t(k)].p;
