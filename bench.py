@@ -254,6 +254,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--ref-procs", type=int, default=0)
+    ap.add_argument("--shard-encoder", action="store_true",
+                    help="view-sharded encode + pyramid all-gather even at N=1 (default at N>1)")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)
@@ -291,20 +293,54 @@ def main():
     # events (the library enqueues every kernel of the frame on it)
     stream = torch.cuda.Stream(device=dev)
 
+    He, We = enc.shape[1], enc.shape[2]
+    K = cfg.pyramid_levels
+    # N > 1: the encoder is view-sharded -- rank r encodes views
+    # view_range(r) of the frame and the pyramid levels are all-gathered over
+    # NVLink (NCCL, on the frame stream) -- then every rank reconstructs and
+    # renders its own target from the full pyramid
+    sharded = world > 1 or args.shard_encoder
+    v0, v1 = shard.view_range(rank, world, M)
+    levels = []
+
     def step():
-        model.forward_render_device(enc, case.enc_cams, ren, case.ren_cams, case.target, rgb,
-                                    stream)
+        if not sharded:
+            model.forward_render_device(enc, case.enc_cams, ren, case.ren_cams, case.target, rgb,
+                                        stream)
+            return
+        model.encode_device(enc, v0, v1, stream)
+        for lv in levels:
+            shard.allgather_views(lv, M)
+        model.forward_render_device(None, case.enc_cams, ren, case.ren_cams, case.target, rgb,
+                                    stream, enc_hw=(He, We))
 
     # warm-up (the first also sizes the arena); the last one is profiled per
-    # stage with CUDA events (never inside the timed region)
-    for i in range(args.warmup):
-        if i == args.warmup - 1:
-            model.profile(True)
-        step()
+    # stage with CUDA events (never inside the timed region). N > 1 profiles
+    # the full single-GPU frame so the stage table means the same at every N.
+    with torch.cuda.stream(stream):
+        if sharded:
+            model.encode_device(enc, 0, M, stream)
+            levels = [model.pyramid_level(k) for k in range(K)]
+        for i in range(args.warmup):
+            if i == args.warmup - 1:
+                model.profile(True)
+                model.forward_render_device(enc, case.enc_cams, ren, case.ren_cams, case.target,
+                                            rgb, stream)
+                torch.cuda.synchronize()
+                stages = model.profile_read()
+                model.profile(False)
+            step()
+            torch.cuda.synchronize()
+        if sharded:
+            model.encode_device(enc, v0, v1, stream)
+            n_enc = model.last_launch_count()
+            model.forward_render_device(None, case.enc_cams, ren, case.ren_cams, case.target, rgb,
+                                        stream, enc_hw=(He, We))
+            launches_per_step = n_enc + model.last_launch_count()
+        else:
+            step()
+            launches_per_step = model.last_launch_count()
         torch.cuda.synchronize()
-    stages = model.profile_read()
-    model.profile(False)
-    launches_per_step = model.last_launch_count()
 
     # timed region: K frames, per-frame CUDA events, L2 flushed between frames
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -334,18 +370,40 @@ def main():
         ren_h = torch.from_numpy(case.ren_images).pin_memory()
         out_h = torch.empty((Ho, Wo, 3), dtype=torch.float32).pin_memory()
         e_np, r_np, o_np = enc_h.numpy(), ren_h.numpy(), out_h.numpy()
-        model.forward_render(e_np, case.enc_cams, r_np, case.ren_cams, case.target, out=o_np)
+        cstream = torch.cuda.ExternalStream(model.stream_handle(), device=dev)
+        def e2e_step():
+            if not sharded:
+                model.forward_render(e_np, case.enc_cams, r_np, case.ren_cams, case.target,
+                                     out=o_np)
+                return
+            # this rank's encoder views up and encoded, the shares
+            # all-gathered (all on the context's stream), then the host C ABI
+            # with a NULL encoder list: render views uploaded under the
+            # forward pass, the frame read back in bands
+            with torch.cuda.stream(cstream):
+                enc[v0:v1].copy_(enc_h[v0:v1], non_blocking=True)
+                model.encode_device(enc, v0, v1, cstream)
+                for lv in levels:
+                    shard.allgather_views(lv, M)
+            model.forward_render(None, case.enc_cams, r_np, case.ren_cams, case.target, out=o_np,
+                                 enc_hw=(He, We))
+
+        e2e_step()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            model.forward_render(e_np, case.enc_cams, r_np, case.ren_cams, case.target, out=o_np)
+            e2e_step()
         sec = shard.max_over_ranks(time.perf_counter() - t0, dev)
+        h2d = (enc_h[v0:v1].numel() if sharded else enc_h.numel()) * 4 + ren_h.numel() * 4
         e2e = {"value": shard.aggregate_fps(world, args.e2e_steps, sec), "unit": "frames/s",
-               "h2d_bytes_per_step": int(enc_h.numel() * 4 + ren_h.numel() * 4),
+               "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(out_h.numel() * 4), "steps": args.e2e_steps,
-               "path": "lvsg_forward_render (host C ABI, pinned buffers)"}
+               "path": ("lvsg_forward_render (host C ABI, pinned buffers)" if not sharded else
+                        "pinned host encoder views (own share) -> lvsg_encode_device -> NCCL "
+                        "all-gather -> lvsg_forward_render (NULL encoder list; pinned render "
+                        "views in, pinned frame out)")}
 
     if rank == 0:
         peaks = load_peaks()
@@ -408,14 +466,19 @@ def main():
             "config": {"workload": f"{args.config}: {M} views, full_scale_config, encoder "
                                    f"{enc.shape[1]}x{enc.shape[2]}, render {ren.shape[1]}x"
                                    f"{ren.shape[2]}, output {Ho}x{Wo}",
-                       "per_gpu": "one target viewpoint per rank" if world > 1 else "1 target",
+                       "per_gpu": ("one target viewpoint per rank (config-5 grid), "
+                                   f"{v1 - v0} of {M} encoder views per rank")
+                       if world > 1 else "1 target",
                        "l2": "flushed (256 MB write) between timed frames",
-                       "parallelism": f"target-sharded x{world}, no data-path collective"
+                       "parallelism": (f"target-sharded x{world}; encoder view-sharded with an "
+                                       "NCCL all-gather of the feature pyramid per frame")
                        if world > 1 else "single GPU"},
             "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "roofline": roof, "cpu_baseline": cpu, "clocks": clocks.summary(),
         }
         print(json.dumps(out))
+    torch.cuda.synchronize()
+    model.close()  # release the context before torch tears CUDA down
     if world > 1:
         dist.destroy_process_group()
 

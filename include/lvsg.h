@@ -95,6 +95,9 @@ typedef struct {
   float* blend;        /* [L,Ho,Wo,M] */
   float* blend_logits; /* [L,H,W,M] pre-softmax, volume resolution */
   float* volume;       /* [L,H,W,C] final feature volume V         */
+  float* deltas;       /* [L,H,W,M,C] the final step's update features */
+  float* rgb;          /* [Ho,Wo,3] decoded-colour composite; direct_rgb
+                          configs only (ForwardResult.rgb, network.hpp:596-601) */
 } lvsg_ldm_out;
 
 typedef struct lvsg_ctx lvsg_ctx;
@@ -146,7 +149,9 @@ lvsg_status lvsg_forward(lvsg_ctx* ctx, int64_t views, const float* const* image
 lvsg_status lvsg_render(lvsg_ctx* ctx, int64_t views, const float* const* images, int64_t height,
                         int64_t width, const lvsg_camera* cams, float* rgb_out);
 /* forward() + render_target() in one call (the CLI forward-demo path,
- * main.cpp:533-541). */
+ * main.cpp:533-541). enc_images == NULL: the resident feature pyramid of
+ * lvsg_encode_device (enc_h x enc_w, complete on the context's stream,
+ * lvsg_stream) is used instead of uploading and encoding. */
 lvsg_status lvsg_forward_render(lvsg_ctx* ctx, int64_t views, const float* const* enc_images,
                                 int64_t enc_h, int64_t enc_w, const lvsg_camera* enc_cams,
                                 const float* const* render_images, int64_t render_h,
@@ -156,12 +161,29 @@ lvsg_status lvsg_forward_render(lvsg_ctx* ctx, int64_t views, const float* const
 /* Device-resident variant: enc_images [M,He,We,3] and render_images
  * [M,Hr,Wr,3] are contiguous DEVICE buffers, rgb_out a DEVICE buffer
  * [Ho,Wo,3]; work is enqueued on `stream` (cudaStream_t, NULL = the
- * context's stream) and the call returns without synchronising. */
+ * context's stream) and the call returns without synchronising.
+ * enc_images == NULL: encode_inputs' convolutions are skipped and the
+ * resident feature pyramid (lvsg_encode_device, He x We) is used, so one
+ * encode serves several targets of the same frame. */
 lvsg_status lvsg_forward_render_device(lvsg_ctx* ctx, int64_t views, const float* enc_images,
                                        int64_t enc_h, int64_t enc_w, const lvsg_camera* enc_cams,
                                        const float* render_images, int64_t render_h,
                                        int64_t render_w, const lvsg_camera* render_cams,
                                        const lvsg_frustum* target, float* rgb_out, void* stream);
+
+/* encode_inputs' convolutional part (network.hpp:388-395: stem, residual
+ * pairs, mean pools) of views [view0, view1) of the DEVICE images
+ * [views,He,We,3] into the context's resident feature pyramid. The pyramid
+ * is target-independent: one encode per frame serves every target, and a
+ * view-sharded encode (each GPU its own view range) is completed by an
+ * all-gather of the level buffers (lvsg_pyramid_level). Enqueued on
+ * `stream` (NULL = the context's stream), no synchronisation. */
+lvsg_status lvsg_encode_device(lvsg_ctx* ctx, int64_t views, const float* enc_images,
+                               int64_t enc_h, int64_t enc_w, int64_t view0, int64_t view1,
+                               void* stream);
+/* Device pointer and extent [M, H_k, W_k, C] (fp32, view-major) of pyramid
+ * level k of the resident feature pyramid. */
+lvsg_status lvsg_pyramid_level(lvsg_ctx* ctx, int64_t level, float** data, int64_t dims[4]);
 
 /* Row-band render for output sharding across GPUs: renders
  * output rows [row0,row1) of the resident LDM into rgb_out (device,

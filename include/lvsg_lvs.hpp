@@ -42,8 +42,11 @@ inline lvsg_frustum to_c(const Frustum& f) {
   return o;
 }
 
+// ForwardResult (network.hpp:551-558) without the tape: the LDM, the
+// pre-softmax blend logits, the final volume and deltas, and (direct_rgb
+// configs only, else empty) the decoded-colour composite rgb.
 struct Ldm {
-  Tensor<float> depth, density, blend, blend_logits, volume;
+  Tensor<float> depth, density, blend, blend_logits, volume, deltas, rgb;
 };
 
 class Model {
@@ -97,9 +100,12 @@ class Model {
     const int64_t L = last.layers, Ho = plan.out_height, Wo = plan.out_width, M = cfg_.views;
     Ldm out{Tensor<float>({L, Ho, Wo}), Tensor<float>({L, Ho, Wo}), Tensor<float>({L, Ho, Wo, M}),
             Tensor<float>({L, last.height, last.width, M}),
-            Tensor<float>({L, last.height, last.width, cfg_.channels})};
+            Tensor<float>({L, last.height, last.width, cfg_.channels}),
+            Tensor<float>({L, last.height, last.width, M, cfg_.channels}),
+            cfg_.direct_rgb ? Tensor<float>({Ho, Wo, 3}) : Tensor<float>()};
     lvsg_ldm_out o{out.depth.data(), out.density.data(), out.blend.data(), out.blend_logits.data(),
-                   out.volume.data()};
+                   out.volume.data(), out.deltas.data(),
+                   cfg_.direct_rgb ? out.rgb.data() : nullptr};
     lvsg_frustum t = to_c(target);
     check(lvsg_forward(ctx_, int64_t(images.size()), ptrs.data(), H, W, cc.data(), &t, &o));
     out_hw_ = {Ho, Wo};

@@ -74,9 +74,10 @@ class Oracle:
         self.lib = ctypes.CDLL(ORACLE_SO)
         L = self.lib
         L.lvso_set_threads.argtypes = [ctypes.c_int]
-        L.lvso_forward_render.argtypes = [P(capi.ModelConfigC), i64, vp, i64, i64, P(capi.CameraC),
-                                          vp, i64, i64, P(capi.CameraC), P(capi.FrustumC), vp, vp,
-                                          vp, vp, vp, vp, vp, ctypes.c_char_p, ctypes.c_size_t]
+        L.lvso_forward_render_ex.argtypes = [P(capi.ModelConfigC), i64, vp, i64, i64,
+                                             P(capi.CameraC), vp, i64, i64, P(capi.CameraC),
+                                             P(capi.FrustumC), vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                             ctypes.c_char_p, ctypes.c_size_t]
         L.lvso_world_points.argtypes = [P(capi.FrustumC), vp, i64, i64, i64, vp]
         L.lvso_footprints.argtypes = [P(capi.CameraC), vp, i64, vp, vp, vp]
         L.lvso_gather.argtypes = [P(capi.CameraC), vp, i64, i64, i64, vp, i64, vp, vp]
@@ -94,8 +95,8 @@ class Oracle:
     def forward_render(self, cfg, enc_images, enc_cams, render_images, render_cams, target,
                        weights, plan_out=None, outputs=("rgb",)):
         """Returns a dict with the requested outputs among rgb, depth,
-        density, blend, blend_logits, volume."""
-        return _forward_render(self.lib.lvso_forward_render, cfg, enc_images, enc_cams,
+        density, blend, blend_logits, volume, deltas, rgb_direct."""
+        return _forward_render(self.lib.lvso_forward_render_ex, cfg, enc_images, enc_cams,
                                render_images, render_cams, target, weights, outputs,
                                errfirst=False)
 
@@ -161,7 +162,8 @@ def _out_shapes(cfg, M, He, We):
     Wo = int(math.floor(W * cfg.upsample + 0.5))
     C = cfg.channels
     return {"rgb": (Ho, Wo, 3), "depth": (L_, Ho, Wo), "density": (L_, Ho, Wo),
-            "blend": (L_, Ho, Wo, M), "blend_logits": (L_, H, W, M), "volume": (L_, H, W, C)}
+            "blend": (L_, Ho, Wo, M), "blend_logits": (L_, H, W, M), "volume": (L_, H, W, C),
+            "deltas": (L_, H, W, M, C), "rgb_direct": (Ho, Wo, 3)}
 
 
 def _forward_render(fn, cfg, enc_images, enc_cams, render_images, render_cams, target, weights,
@@ -180,7 +182,7 @@ def _forward_render(fn, cfg, enc_images, enc_cams, render_images, render_cams, t
     args = [ctypes.byref(cc.c), M, _f32(enc_images), He, We, _cams(enc_cams), _f32(render_images),
             Hr, Wr, rc, ctypes.byref(_fr(target)), _f32(weights)]
     args += [_f32(outs.get(k)) for k in ("rgb", "depth", "density", "blend", "blend_logits",
-                                          "volume")]
+                                          "volume", "deltas", "rgb_direct")]
     secs = (ctypes.c_double * 2)()
     if errfirst:
         args += [secs]
@@ -208,9 +210,10 @@ class Reference:
                               P(capi.CameraC), cp, sz]
         L.ref_scene_images.argtypes = [ctypes.c_uint64, i64, P(capi.FrustumC), i64, P(capi.CameraC),
                                        vp, cp, sz]
-        L.ref_forward_render.argtypes = [P(capi.ModelConfigC), i64, vp, i64, i64, P(capi.CameraC),
-                                         vp, i64, i64, P(capi.CameraC), P(capi.FrustumC), vp, vp,
-                                         vp, vp, vp, vp, vp, vp, cp, sz]
+        L.ref_forward_render_ex.argtypes = [P(capi.ModelConfigC), i64, vp, i64, i64,
+                                            P(capi.CameraC), vp, i64, i64, P(capi.CameraC),
+                                            P(capi.FrustumC), vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                            vp, cp, sz]
         L.ref_world_points.argtypes = [P(capi.FrustumC), vp, i64, i64, i64, vp, cp, sz]
         L.ref_gather.argtypes = [P(capi.CameraC), vp, i64, i64, i64, vp, i64, vp, vp, cp, sz]
         L.ref_footprints.argtypes = [P(capi.CameraC), vp, i64, vp, vp, vp, cp, sz]
@@ -259,7 +262,7 @@ class Reference:
     def forward_render(self, cfg, enc_images, enc_cams, render_images, render_cams, target,
                        weights, outputs=("rgb",)):
         def fn(*a):
-            return self.lib.ref_forward_render(*a)
+            return self.lib.ref_forward_render_ex(*a)
         return _forward_render(fn, cfg, enc_images, enc_cams, render_images, render_cams, target,
                                weights, outputs, errfirst=True)
 

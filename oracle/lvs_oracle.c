@@ -1102,6 +1102,19 @@ int lvso_forward_render(const lvsg_model_config* cfg, int64_t M, const float* en
                         const float* weights, float* rgb_out, float* depth_out,
                         float* density_out, float* blend_out, float* logits_out,
                         float* volume_out, char* err, size_t errlen) {
+  return lvso_forward_render_ex(cfg, M, enc_images, He, We, enc_cams, render_images, Hr, Wr,
+                                render_cams, target, weights, rgb_out, depth_out, density_out,
+                                blend_out, logits_out, volume_out, NULL, NULL, err, errlen);
+}
+
+int lvso_forward_render_ex(const lvsg_model_config* cfg, int64_t M, const float* enc_images,
+                           int64_t He, int64_t We, const lvsg_camera* enc_cams,
+                           const float* render_images, int64_t Hr, int64_t Wr,
+                           const lvsg_camera* render_cams, const lvsg_frustum* target,
+                           const float* weights, float* rgb_out, float* depth_out,
+                           float* density_out, float* blend_out, float* logits_out,
+                           float* volume_out, float* deltas_out, float* rgb_direct_out, char* err,
+                           size_t errlen) {
   if (M != cfg->views) {
     seterr(err, errlen, "forward: expected %lld views", (long long)cfg->views);
     return 1;
@@ -1315,6 +1328,20 @@ int lvso_forward_render(const lvsg_model_config* cfg, int64_t M, const float* en
   if (blend_out) memcpy(blend_out, blend, sizeof(float) * (size_t)(PO * M));
   if (logits_out) memcpy(logits_out, logits, sizeof(float) * (size_t)(PT * M));
   if (volume_out) memcpy(volume_out, V, sizeof(float) * (size_t)(PT * C));
+  if (deltas_out) memcpy(deltas_out, deltas, sizeof(float) * (size_t)(PT * M * C));
+  /* ForwardResult.rgb under direct_rgb (network.hpp:596-601): decode_linear
+   * of the appearance head, bilinear resize to the output grid, sigmoid,
+   * over-composite with the activated density */
+  if (rgb_direct_out && cfg->direct_rgb) {
+    float* pa = falloc(PT * 3);
+    float* ua = falloc(PO * 3);
+    decode_linear(V, PT, C, P.w_appear, 3, pa);
+    resize_hwc(pa, ua, L, H, W, 3, Ho, Wo);
+    for (int64_t q = 0; q < PO * 3; ++q) ua[q] = sigmoidf_(ua[q]);
+    over_composite(ua, density, rgb_direct_out, L, Ho * Wo, 3);
+    free(pa);
+    free(ua);
+  }
 
   /* --- render_target (ldm.hpp:193-199) --- */
   if (render_images && rgb_out) {

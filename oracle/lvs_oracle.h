@@ -41,6 +41,16 @@ int lvso_forward_render(const lvsg_model_config* cfg, int64_t M, const float* en
                         const float* weights, float* rgb, float* depth, float* density,
                         float* blend, float* blend_logits, float* volume, char* err,
                         size_t errlen);
+/* The same with ForwardResult's two remaining fields: deltas [L,H,W,M,C]
+ * (the final step's update features) and, under direct_rgb, rgb [Ho,Wo,3]
+ * (ForwardResult.rgb, network.hpp:596-601). Either may be NULL. */
+int lvso_forward_render_ex(const lvsg_model_config* cfg, int64_t M, const float* enc_images,
+                           int64_t He, int64_t We, const lvsg_camera* enc_cams,
+                           const float* render_images, int64_t Hr, int64_t Wr,
+                           const lvsg_camera* render_cams, const lvsg_frustum* target,
+                           const float* weights, float* rgb, float* depth, float* density,
+                           float* blend, float* blend_logits, float* volume, float* deltas,
+                           float* rgb_direct, char* err, size_t errlen);
 
 /* Stage restatements for per-stage parity. */
 int lvso_world_points(const lvsg_frustum* fr, const float* depth, int64_t L, int64_t H, int64_t W,

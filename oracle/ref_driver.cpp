@@ -196,6 +196,14 @@ int ref_scene_images(uint64_t seed, int64_t planes, const lvsg_frustum* scene_fr
 // forward<float> + render_target<float> with weights bound from a flat store
 // in build_params order. Any output pointer may be NULL. Images are
 // contiguous [M,H,W,3].
+int ref_forward_render_ex(const lvsg_model_config* c, int64_t M, const float* enc_images,
+                          int64_t He, int64_t We, const lvsg_camera* enc_cams,
+                          const float* render_images, int64_t Hr, int64_t Wr,
+                          const lvsg_camera* render_cams, const lvsg_frustum* target,
+                          const float* weights, float* rgb, float* depth, float* density,
+                          float* blend, float* blend_logits, float* volume, float* deltas,
+                          float* rgb_direct, double* seconds, char* err, size_t len);
+
 int ref_forward_render(const lvsg_model_config* c, int64_t M, const float* enc_images,
                        int64_t He, int64_t We, const lvsg_camera* enc_cams,
                        const float* render_images, int64_t Hr, int64_t Wr,
@@ -203,6 +211,20 @@ int ref_forward_render(const lvsg_model_config* c, int64_t M, const float* enc_i
                        const float* weights, float* rgb, float* depth, float* density,
                        float* blend, float* blend_logits, float* volume, double* seconds,
                        char* err, size_t len) {
+  return ref_forward_render_ex(c, M, enc_images, He, We, enc_cams, render_images, Hr, Wr,
+                               render_cams, target, weights, rgb, depth, density, blend,
+                               blend_logits, volume, nullptr, nullptr, seconds, err, len);
+}
+
+// ... plus ForwardResult.deltas ([L,H,W,M,C]) and ForwardResult.rgb (set
+// only under direct_rgb, [Ho,Wo,3]).
+int ref_forward_render_ex(const lvsg_model_config* c, int64_t M, const float* enc_images,
+                          int64_t He, int64_t We, const lvsg_camera* enc_cams,
+                          const float* render_images, int64_t Hr, int64_t Wr,
+                          const lvsg_camera* render_cams, const lvsg_frustum* target,
+                          const float* weights, float* rgb, float* depth, float* density,
+                          float* blend, float* blend_logits, float* volume, float* deltas,
+                          float* rgb_direct, double* seconds, char* err, size_t len) {
   return guarded(err, len, [&] {
     ModelConfig cfg = to_cfg(c);
     std::vector<Tensor<float>> shapes = init_param_store<float>(cfg, 0);
@@ -243,6 +265,8 @@ int ref_forward_render(const lvsg_model_config* c, int64_t M, const float* enc_i
     copy_out(tape.value(r.ldm.blend), blend);
     copy_out(tape.value(r.blend_logits), blend_logits);
     copy_out(tape.value(r.volume.V), volume);
+    copy_out(tape.value(r.deltas), deltas);
+    if (cfg.direct_rgb) copy_out(tape.value(r.rgb), rgb_direct);
     if (seconds) {
       seconds[0] = std::chrono::duration<double>(t1 - t0).count();
       seconds[1] = std::chrono::duration<double>(t2 - t1).count();

@@ -60,7 +60,8 @@ class PlanC(ctypes.Structure):
 
 class LdmOutC(ctypes.Structure):
     _fields_ = [("depth", c_f32p), ("density", c_f32p), ("blend", c_f32p),
-                ("blend_logits", c_f32p), ("volume", c_f32p)]
+                ("blend_logits", c_f32p), ("volume", c_f32p), ("deltas", c_f32p),
+                ("rgb", c_f32p)]
 
 
 # Error classes (include/lvsg.h; reference tensor.hpp:15-25).
@@ -98,6 +99,7 @@ SYMBOLS = [
     "lvsg_init_param_store", "lvsg_create", "lvsg_destroy", "lvsg_last_error",
     "lvsg_load_weights", "lvsg_init_weights", "lvsg_forward", "lvsg_render",
     "lvsg_forward_render", "lvsg_forward_render_device", "lvsg_render_rows_device",
+    "lvsg_encode_device", "lvsg_pyramid_level",
     "lvsg_synchronize", "lvsg_last_launch_count", "lvsg_stream", "lvsg_stage_world_points",
     "lvsg_stage_footprints", "lvsg_stage_gather", "lvsg_rig_cameras", "lvsg_scene_images",
     "lvsg_profile_enable", "lvsg_profile_read", "lvsg_stage_conv3x3", "lvsg_stage_conv3x3_fused",
@@ -138,6 +140,8 @@ def lib() -> ctypes.CDLL:
                                              c_i64, P(CameraC), P(FrustumC), vp, vp]
     L.lvsg_render_rows_device.argtypes = [vp, c_i64, vp, c_i64, c_i64, P(CameraC), c_i64, c_i64,
                                           vp, vp]
+    L.lvsg_encode_device.argtypes = [vp, c_i64, vp, c_i64, c_i64, c_i64, c_i64, vp]
+    L.lvsg_pyramid_level.argtypes = [vp, c_i64, P(vp), P(c_i64)]
     L.lvsg_synchronize.argtypes = [vp]
     L.lvsg_last_launch_count.argtypes = [vp]
     L.lvsg_last_launch_count.restype = c_i64

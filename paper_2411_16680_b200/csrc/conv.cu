@@ -131,34 +131,58 @@ __global__ void __launch_bounds__(NT) conv3x3_kernel(const ConvArgs a) {
   }
 }
 
+// Stem weights by value: [k = ci*9+tap][32] and the bias (zero when the
+// conv has none), in the kernel's parameter space.
+struct StemParam {
+  float w[27 * 32];
+  float b[32];
+};
+
 // Few-input-channel conv (Cin = CI in {1, 3} -> Cout = 32): the encoder
 // stem (encode_inputs network.hpp:390) and the feedback-alpha slice of the
 // update stems. One thread per output pixel, the 9*CI taps in registers,
-// weights [k = ci*9+tap][32] broadcast from shared memory, k ascending from
-// the bias like the reference; optional residual (accumulating slices).
-template <int CI>
-__global__ void __launch_bounds__(128) conv3x3_stem_kernel(const ConvArgs a) {
+// weights [k = ci*9+tap][32], k ascending from the bias like the reference;
+// optional residual (accumulating slices). PW: the weights come from the
+// parameter block `pw` (constant-bank FMA operands: the shared-memory
+// version is bound by its 27*8 weight loads per pixel); else they are
+// staged in shared memory and read as broadcast float4s.
+template <int CI, bool PW>
+__global__ void __launch_bounds__(128) conv3x3_stem_kernel(const ConvArgs a,
+                                                           const __grid_constant__ StemParam pw) {
   pdl_grid_sync();
-  __shared__ __align__(16) float s_w[9 * CI * 32];
+  __shared__ __align__(16) float s_w[PW ? 4 : 9 * CI * 32];
   __shared__ float s_b[32];
   __shared__ __align__(16) float4 s_o[128 * 8];  // [pixel][c4 ^ (pixel & 7)]
-  for (int e = threadIdx.x; e < 9 * CI * 32; e += blockDim.x) {
-    const int co = e % 32, k = e / 32;
-    s_w[e] = __ldg(a.w + ((long long)co * w_cin_of(a) + a.w_ci0) * 9 + k);
+  if (!PW) {
+    for (int e = threadIdx.x; e < 9 * CI * 32; e += blockDim.x) {
+      const int co = e % 32, k = e / 32;
+      s_w[e] = __ldg(a.w + ((long long)co * w_cin_of(a) + a.w_ci0) * 9 + k);
+    }
+    if (threadIdx.x < 32) s_b[threadIdx.x] = a.bias ? __ldg(a.bias + threadIdx.x) : 0.f;
+    __syncthreads();
   }
-  if (threadIdx.x < 32) s_b[threadIdx.x] = a.bias ? __ldg(a.bias + threadIdx.x) : 0.f;
-  __syncthreads();
   const int64_t HW = (int64_t)a.H * a.W;
   const int64_t n = HW * a.B;
   const int64_t i0 = blockIdx.x * (int64_t)blockDim.x;
   const int64_t i = i0 + threadIdx.x;
   const int t = threadIdx.x;
+  // the block's 128 consecutive pixels: one 64-bit division per block, then
+  // 32-bit arithmetic per thread (the carry loop also covers images smaller
+  // than a block)
+  const int b_blk = int(i0 / HW);
+  const int pix_blk = int(i0 - b_blk * HW);
+  auto locate = [&](int k, int& b, int& pix) {  // pixel i0 + k -> (image, pixel)
+    b = b_blk;
+    pix = pix_blk + k;
+    while (pix >= HW) pix -= int(HW), ++b;
+  };
   if (i < n) {
-    const int b = int(i / HW);
-    const int64_t pix = i - b * HW;
-    const int y = int(pix / a.W), x = int(pix % a.W);
+    int b, pix;
+    locate(t, b, pix);
+    const int y = pix / a.W, x = pix - (pix / a.W) * a.W;
     const ConvSrc& S = a.src[0];
-    const float* src = S.ptr + (long long)b * S.bstride;
+    const float* src = S.ptr + (long long)b * S.bstride + (long long)pix * S.pstride;
+    const int row = a.W * S.pstride;
     float xin[9 * CI];
 #pragma unroll
     for (int dy = 0; dy < 3; ++dy)
@@ -166,18 +190,20 @@ __global__ void __launch_bounds__(128) conv3x3_stem_kernel(const ConvArgs a) {
       for (int dx = 0; dx < 3; ++dx) {
         const int yy = y + dy - 1, xx = x + dx - 1;
         const bool ok = yy >= 0 && yy < a.H && xx >= 0 && xx < a.W;
-        const float* p = src + ((long long)yy * a.W + xx) * S.pstride;
+        const float* p = src + ((dy - 1) * row + (dx - 1) * S.pstride);
 #pragma unroll
         for (int ci = 0; ci < CI; ++ci) xin[ci * 9 + dy * 3 + dx] = ok ? __ldg(p + ci) : 0.f;
       }
     float acc[32];
 #pragma unroll
-    for (int c = 0; c < 32; ++c) acc[c] = s_b[c];
+    for (int c = 0; c < 32; ++c) acc[c] = PW ? pw.b[c] : s_b[c];
 #pragma unroll
     for (int k = 0; k < 9 * CI; ++k) {
 #pragma unroll
       for (int c4 = 0; c4 < 8; ++c4) {
-        const float4 w = reinterpret_cast<const float4*>(s_w + k * 32)[c4];
+        const float4 w = PW ? make_float4(pw.w[k * 32 + 4 * c4], pw.w[k * 32 + 4 * c4 + 1],
+                                          pw.w[k * 32 + 4 * c4 + 2], pw.w[k * 32 + 4 * c4 + 3])
+                            : reinterpret_cast<const float4*>(s_w + k * 32)[c4];
         acc[4 * c4] = fmaf(xin[k], w.x, acc[4 * c4]);
         acc[4 * c4 + 1] = fmaf(xin[k], w.y, acc[4 * c4 + 1]);
         acc[4 * c4 + 2] = fmaf(xin[k], w.z, acc[4 * c4 + 2]);
@@ -200,15 +226,97 @@ __global__ void __launch_bounds__(128) conv3x3_stem_kernel(const ConvArgs a) {
     const int j = t + 128 * k, pl = j >> 3, c4 = j & 7;
     const int64_t ip = i0 + pl;
     if (ip >= n) continue;
-    const int b = int(ip / HW);
-    const int64_t pix = ip - b * HW;
+    int b, pix;
+    locate(pl, b, pix);
     float4 v = s_o[pl * 8 + (c4 ^ (pl & 7))];
     if (a.resid) {
       const float4 r = __ldg(reinterpret_cast<const float4*>(a.resid + (long long)b * a.res_bstride +
-                                                              pix * a.res_pstride) + c4);
+                                                              (long long)pix * a.res_pstride) + c4);
       v = make_float4(fa(r.x, v.x), fa(r.y, v.y), fa(r.z, v.z), fa(r.w, v.w));
     }
-    reinterpret_cast<float4*>(a.out + (long long)b * a.out_bstride + pix * a.out_pstride)[c4] = v;
+    reinterpret_cast<float4*>(a.out + (long long)b * a.out_bstride + (long long)pix * a.out_pstride)[c4] = v;
+  }
+}
+
+// The encoder stem (Cin = 3, weights by value as in conv3x3_stem_kernel<3,
+// true>) with two horizontally adjacent output pixels per thread: each
+// constant-bank weight feeds two FMAs and the two pixels share 8 of their
+// 12 tap columns. Requires an even W (pairs never straddle a row or an
+// image); same per-pixel arithmetic and order as the one-pixel kernel.
+__global__ void __launch_bounds__(128) conv3x3_stem3x2_kernel(const ConvArgs a,
+                                                              const __grid_constant__ StemParam pw) {
+  pdl_grid_sync();
+  __shared__ __align__(16) float4 s_o[256 * 8];  // [pixel][c4 ^ (pixel & 7)]
+  const int64_t HW = (int64_t)a.H * a.W;
+  const int64_t n = HW * a.B;
+  const int64_t i0 = blockIdx.x * (int64_t)256;
+  const int t = threadIdx.x;
+  const int b_blk = int(i0 / HW);
+  const int pix_blk = int(i0 - b_blk * HW);
+  auto locate = [&](int k, int& b, int& pix) {  // pixel i0 + k -> (image, pixel)
+    b = b_blk;
+    pix = pix_blk + k;
+    while (pix >= HW) pix -= int(HW), ++b;
+  };
+  if (i0 + 2 * t < n) {
+    int b, pix;
+    locate(2 * t, b, pix);
+    const int y = pix / a.W, x = pix - y * a.W;  // x even
+    const ConvSrc& S = a.src[0];
+    const float* src = S.ptr + (long long)b * S.bstride + (long long)pix * S.pstride;
+    const int row = a.W * S.pstride;
+    float xin[3][4][3];  // [dy][column x-1 .. x+2][ci]
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+      for (int cx = 0; cx < 4; ++cx) {
+        const int yy = y + dy - 1, xx = x + cx - 1;
+        const bool ok = yy >= 0 && yy < a.H && xx >= 0 && xx < a.W;
+        const float* p = src + ((dy - 1) * row + (cx - 1) * S.pstride);
+#pragma unroll
+        for (int ci = 0; ci < 3; ++ci) xin[dy][cx][ci] = ok ? __ldg(p + ci) : 0.f;
+      }
+    float acc0[32], acc1[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) acc0[c] = acc1[c] = pw.b[c];
+#pragma unroll
+    for (int ci = 0; ci < 3; ++ci)
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+          const int k = ci * 9 + dy * 3 + dx;
+          const float x0 = xin[dy][dx][ci], x1 = xin[dy][dx + 1][ci];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            acc0[c] = fmaf(x0, pw.w[k * 32 + c], acc0[c]);
+            acc1[c] = fmaf(x1, pw.w[k * 32 + c], acc1[c]);
+          }
+        }
+#pragma unroll
+    for (int c4 = 0; c4 < 8; ++c4) {
+      const int p0 = 2 * t, p1 = 2 * t + 1;
+      s_o[p0 * 8 + (c4 ^ (p0 & 7))] = make_float4(acc0[4 * c4], acc0[4 * c4 + 1], acc0[4 * c4 + 2],
+                                                  acc0[4 * c4 + 3]);
+      s_o[p1 * 8 + (c4 ^ (p1 & 7))] = make_float4(acc1[4 * c4], acc1[4 * c4 + 1], acc1[4 * c4 + 2],
+                                                  acc1[4 * c4 + 3]);
+    }
+  }
+  __syncthreads();
+  // coalesced write-back (+ residual): 8 threads per pixel's 128 bytes
+#pragma unroll 4
+  for (int k = 0; k < 16; ++k) {
+    const int j = t + 128 * k, pl = j >> 3, c4 = j & 7;
+    if (i0 + pl >= n) continue;
+    int b, pix;
+    locate(pl, b, pix);
+    float4 v = s_o[pl * 8 + (c4 ^ (pl & 7))];
+    if (a.resid) {
+      const float4 r = __ldg(reinterpret_cast<const float4*>(a.resid + (long long)b * a.res_bstride +
+                                                              (long long)pix * a.res_pstride) + c4);
+      v = make_float4(fa(r.x, v.x), fa(r.y, v.y), fa(r.z, v.z), fa(r.w, v.w));
+    }
+    reinterpret_cast<float4*>(a.out + (long long)b * a.out_bstride + (long long)pix * a.out_pstride)[c4] = v;
   }
 }
 
@@ -244,10 +352,22 @@ void conv3x3(const ConvArgs& a, cudaStream_t st, int impl) {
     conv3x3_tc(a, st);
   } else if (impl != 1 && stem_supported(a)) {
     const int64_t n = (int64_t)a.B * a.H * a.W;
-    if (a.Cin == 3)
-      launch_k(conv3x3_stem_kernel<3>, int((n + 127) / 128), 128, 0, st, a);
-    else
-      launch_k(conv3x3_stem_kernel<1>, int((n + 127) / 128), 128, 0, st, a);
+    const int g = int((n + 127) / 128);
+    StemParam pw;
+    if (a.Cin == 3 && a.stem_host && a.w_ci0 == 0 && w_cin_of(a) == 3) {
+      for (int co = 0; co < 32; ++co) {
+        for (int k = 0; k < 27; ++k) pw.w[k * 32 + co] = a.stem_host[co * 27 + k];
+        pw.b[co] = a.bias ? a.stem_host[27 * 32 + co] : 0.f;
+      }
+      if (a.W % 2 == 0 && !a.gelu)
+        launch_k(conv3x3_stem3x2_kernel, int((n + 255) / 256), 128, 0, st, a, pw);
+      else
+        launch_k(conv3x3_stem_kernel<3, true>, g, 128, 0, st, a, pw);
+    } else if (a.Cin == 3) {
+      launch_k(conv3x3_stem_kernel<3, false>, g, 128, 0, st, a, pw);
+    } else {
+      launch_k(conv3x3_stem_kernel<1, false>, g, 128, 0, st, a, pw);
+    }
   } else {
     conv3x3_simt(a, st);
   }

@@ -951,6 +951,19 @@ __global__ void layer_collapse_kernel(const float* __restrict__ V, int L2, int64
   for (int c = 0; c < C; ++c) o[c] = fa(fm(fa(a[c], b[c]), 0.5f), fa(r[c], b2[c]));
 }
 
+__global__ void decode_linear_kernel(const float* __restrict__ V, int64_t P, int C,
+                                     const float* __restrict__ w, int K, float* out) {
+  pdl_grid_sync();
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= P * K) return;
+  const int64_t p = i / K;
+  const int j = int(i % K);
+  const float* v = V + p * C;
+  float acc = 0.f;
+  for (int k = 0; k < C; ++k) acc = fmaf(v[k], __ldg(w + k * K + j), acc);
+  out[i] = acc;
+}
+
 __global__ void decode_scalar_kernel(const float* __restrict__ V, int64_t P, int C,
                                      const float* __restrict__ w, float* out, int64_t PL,
                                      DepthAct act, int do_act) {
@@ -1127,6 +1140,12 @@ void gather_stack(const float* feats, int M, int Hf, int Wf, int C, const DevCam
                   cudaStream_t st) {
   const bool v4 = C % 4 == 0;
   const int64_t n = (int64_t)L * H * W * M;
+  static const bool tiled = [] {  // LVSG_GATHER=tile: shared-memory windows (gather_tile.cu)
+    const char* e = getenv("LVSG_GATHER");
+    return e && e[0] == 't';
+  }();
+  if (tiled && gather_tile32(feats, M, Hf, Wf, C, cams_dev, rc, depth, L, H, W, deltas, st))
+    return;
   if (C == 32 && (int64_t)M * Hf * Wf * 8 < (int64_t(1) << 31) && n < (int64_t(1) << 31)) {
     launch_k(gather_stack32_kernel, blocks_for(n, 256), 256, 0, st, feats, M, Hf, Wf, cams_dev, rc,
                                                               depth, L, H, W, deltas);
@@ -1214,6 +1233,10 @@ void decode_scalar(const float* V, int64_t P, int C, const float* w, float* out,
   (void)L;
   launch_k(decode_scalar_kernel, blocks_for(P, 256), 256, 0, st, V, P, C, w, out, PL,
                                                            act ? *act : DepthAct{}, act ? 1 : 0);
+}
+void decode_linear(const float* V, int64_t P, int C, const float* w, int K, float* out,
+                   cudaStream_t st) {
+  launch_k(decode_linear_kernel, blocks_for(P * K, 256), 256, 0, st, V, P, C, w, K, out);
 }
 void decode_scalar2(const float* V, int64_t P, int C, const float* wa, float* outa, const float* wb,
                     float* outb, cudaStream_t st) {

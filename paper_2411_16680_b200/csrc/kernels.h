@@ -96,6 +96,11 @@ struct ConvArgs {
   // mean_pool2, same summation order) to pool_out [B, H/2, W/2, 32]
   float* pool_out;
   long long pool_bstride;
+  // Cin = 3 stem only: host copy of the weights [32][3][3][3] and bias [32]
+  // (the encoder stem, bound at weight load). The stem kernel then takes
+  // them by value in its parameter space, so every FMA reads its weight as
+  // a constant-bank operand (no shared-memory weight loads).
+  const float* stem_host;
 };
 __host__ __device__ inline int w_cin_of(const ConvArgs& a) { return a.w_cin ? a.w_cin : a.Cin; }
 // Dispatches to the tcgen05 3xTF32 kernel when it applies (Cin = Cout = 32,
@@ -156,6 +161,11 @@ void ray_project(const float* base, int M, int hK, int wK, int Hk, int Wk, const
 void gather_stack(const float* feats, int M, int Hf, int Wf, int C, const DevCam* cams_dev,
                   const DevRayCam& rc, const float* depth, int L, int H, int W, float* deltas,
                   cudaStream_t st);
+// The same for C = 32 with the feature windows staged in shared memory by
+// bulk async copies (gather_tile.cu); false when the shape does not apply.
+bool gather_tile32(const float* feats, int M, int Hf, int Wf, int C, const DevCam* cams_dev,
+                   const DevRayCam& rc, const float* depth, int L, int H, int W, float* deltas,
+                   cudaStream_t st);
 
 // Per-pixel strides of the render-to-input-view buffers, padded to 16 bytes
 // so every row moves as float4 / vector atomics and feeds TMA: the payload
@@ -175,6 +185,14 @@ void decode_payload(const float* V, int L, int H, int W, int C, const float* w_a
 // view: acc [M, L, Hv, Wv, K+1] (atomics; zeroed by the caller).
 void splat(const float* payload, const float* points, int L, int PL, int K, const DevCam* cams_dev,
            int M, int Hv, int Wv, float* acc, cudaStream_t st);
+// Deterministic splat + normalise + composite (splat_det.cu): the same
+// result as splat + splat_composite, summed per view pixel in the
+// reference's order (bit-identical from run to run). scratch holds
+// splat_det_scratch_ints(L*PL*M, M*L*Hv*Wv) ints.
+size_t splat_det_scratch_ints(int64_t pairs, int64_t bins);
+void splat_det(const float* payload, const float* points, int L, int PL, int K,
+               const DevCam* cams_dev, int M, int Hv, int Wv, int* scratch, float* out,
+               cudaStream_t st);
 // normalise (splat_project) + over_composite colour and alpha
 // (ldm.hpp:236-243): acc -> out [M, Hv, Wv, K] (K-1 colour + alpha).
 void splat_composite(const float* acc, int M, int L, int Hv, int Wv, int K, float* out,
@@ -212,6 +230,7 @@ void decode_scalar(const float* V, int64_t P, int C, const float* w, float* out,
                    int64_t PL, const DepthAct* act, cudaStream_t st);
 
 // ---- Stage 3 + 4 ------------------------------------------------------------
+constexpr int kRenderParamViews = 16;
 struct RenderArgs {
   const float* pre_d;   // [L,H,W]
   const float* pre_s;   // [L,H,W]
@@ -221,6 +240,8 @@ struct RenderArgs {
   DepthAct act;
   DevRayCam rc;           // target camera re-digitised to (Wo, Ho)
   const DevCam* cams;     // [M] render cameras (device)
+  DevCam pc[kRenderParamViews];  // the same by value (M <= 16; the M-specialised kernels)
+  int pc_valid;                  // pc holds the M cameras
   const float* images;    // [M, Hr, Wr, 3]
   int Hr, Wr;
   float* rgb;             // [row1-row0, Wo, 3]
@@ -230,6 +251,12 @@ struct RenderArgs {
 };
 // upsample_activate + render_target fused (ldm.hpp:193-199, :249-271).
 void render_fused(const RenderArgs& a, cudaStream_t st);
+// ForwardResult.rgb of a direct_rgb config (network.hpp:596-601): pre_a =
+// decode_linear(V, w_appear) [L,H,W,3] -> out [Ho,Wo,3].
+void direct_rgb(const RenderArgs& a, const float* pre_a, float* out, cudaStream_t st);
+// decode_linear (ldm.hpp:58-67): out[p, j] = sum_k V[p, k] w[k, j], k ascending.
+void decode_linear(const float* V, int64_t P, int C, const float* w, int K, float* out,
+                   cudaStream_t st);
 // upsample_activate only (materialised LDM for lvsg_forward outputs).
 void upsample_activate(const RenderArgs& a, float* depth, float* density, float* blend,
                        cudaStream_t st);

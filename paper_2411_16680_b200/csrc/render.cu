@@ -81,13 +81,20 @@ __device__ __forceinline__ Taps taps_for(const RenderArgs& a, int i, int j) {
   return t;
 }
 
-// One thread per output pixel of the row band.
+// One thread per output pixel of the row band. MM > 0: the view count is a
+// compile-time constant, the cameras are read from the kernel's parameter
+// space (a.pc: constant-bank operands of the f64 instructions) and each
+// view's footprint is branch-free (taps always in range; an invalid view's
+// colour and weight are zeroed by select). MM == 0: cameras staged in shared
+// memory, branchy footprint.
 template <int MM>
 __global__ void __launch_bounds__(128, MM == 16 ? 4 : 6) render_fused_kernel(const RenderArgs a) {
   pdl_grid_sync();
   extern __shared__ DevCam s_cams[];
-  for (int m = threadIdx.x; m < a.M; m += blockDim.x) s_cams[m] = a.cams[m];
-  __syncthreads();
+  if (MM == 0) {
+    for (int m = threadIdx.x; m < a.M; m += blockDim.x) s_cams[m] = a.cams[m];
+    __syncthreads();
+  }
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int rows = a.row1 - a.row0;
   if (idx >= (int64_t)rows * a.Wo) return;
@@ -112,28 +119,49 @@ __global__ void __launch_bounds__(128, MM == 16 ? 4 : 6) render_fused_kernel(con
     float wsum = 0.f;
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      const Footprint f = project_footprint(s_cams[m], pt);
-      if (f.valid) {
+      const float* img = a.images + m * img_stride;
+      if (MM > 0) {
         // f64 (bit-exact) taps and weights; the colour blend is an f32 FMA
         // chain over the weights rounded to f32 (~2 ulp of the f64 blend)
+        const Footprint f = project_footprint_nb(a.pc[m], pt);
         double wd[4];
         bilinear_weights(f, wd);
         float w[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) w[k] = __double2float_rn(wd[k]);
-        const float* img = a.images + m * img_stride;
-        const float* p00 = img + ((int64_t)f.y0 * a.Wr + f.x0) * 3;
-        const float* p10 = img + ((int64_t)f.y0 * a.Wr + f.x1) * 3;
-        const float* p01 = img + ((int64_t)f.y1 * a.Wr + f.x0) * 3;
-        const float* p11 = img + ((int64_t)f.y1 * a.Wr + f.x1) * 3;
+        const int r0 = f.y0 * a.Wr, r1 = f.y1 * a.Wr;  // one view < 2^31 floats
+        const float* p00 = img + (r0 + f.x0) * 3;
+        const float* p10 = img + (r0 + f.x1) * 3;
+        const float* p01 = img + (r1 + f.x0) * 3;
+        const float* p11 = img + (r1 + f.x1) * 3;
 #pragma unroll
-        for (int k = 0; k < 3; ++k)
-          col[m][k] = fmaf(w[3], __ldg(p11 + k),
-                           fmaf(w[2], __ldg(p01 + k), fmaf(w[1], __ldg(p10 + k), w[0] * __ldg(p00 + k))));
-        beta[m] = fm(beta[m], 1.0f);
+        for (int k = 0; k < 3; ++k) {
+          const float v = fmaf(w[3], __ldg(p11 + k),
+                               fmaf(w[2], __ldg(p01 + k), fmaf(w[1], __ldg(p10 + k), w[0] * __ldg(p00 + k))));
+          col[m][k] = f.valid ? v : 0.f;
+        }
+        beta[m] = fm(beta[m], f.valid ? 1.0f : 0.0f);
       } else {
-        col[m][0] = col[m][1] = col[m][2] = 0.f;
-        beta[m] = fm(beta[m], 0.0f);
+        const Footprint f = project_footprint(s_cams[m], pt);
+        if (f.valid) {
+          double wd[4];
+          bilinear_weights(f, wd);
+          float w[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) w[k] = __double2float_rn(wd[k]);
+          const float* p00 = img + ((int64_t)f.y0 * a.Wr + f.x0) * 3;
+          const float* p10 = img + ((int64_t)f.y0 * a.Wr + f.x1) * 3;
+          const float* p01 = img + ((int64_t)f.y1 * a.Wr + f.x0) * 3;
+          const float* p11 = img + ((int64_t)f.y1 * a.Wr + f.x1) * 3;
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            col[m][k] = fmaf(w[3], __ldg(p11 + k),
+                             fmaf(w[2], __ldg(p01 + k), fmaf(w[1], __ldg(p10 + k), w[0] * __ldg(p00 + k))));
+          beta[m] = fm(beta[m], 1.0f);
+        } else {
+          col[m][0] = col[m][1] = col[m][2] = 0.f;
+          beta[m] = fm(beta[m], 0.0f);
+        }
       }
       wsum = fa(wsum, fm(beta[m], 1.0f));
     }
@@ -174,6 +202,38 @@ __global__ void upsample_activate_kernel(const RenderArgs a, float* depth, float
   for (int m = 0; m < a.M; ++m) blend[idx * a.M + m] = beta[m];
 }
 
+// ForwardResult.rgb under direct_rgb (network.hpp:596-601): the appearance
+// head pre_a = V w_appear [L,H,W,3] resized bilinearly to the output grid
+// (the same taps and f32 lerps as the LDM maps), sigmoid, over-composited
+// back to front with the activated density sigmoid(resize(pre_s)). One
+// thread per output pixel.
+__global__ void direct_rgb_kernel(const RenderArgs a, const float* __restrict__ pre_a,
+                                  float* __restrict__ out) {
+  pdl_grid_sync();
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)a.Ho * a.Wo) return;
+  const int i = int(idx / a.Wo), j = int(idx % a.Wo);
+  const Taps t = taps_for(a, i, j);
+  const int64_t plane = (int64_t)a.H * a.W;
+  const int64_t q00 = (int64_t)t.y0 * a.W + t.x0, q10 = (int64_t)t.y0 * a.W + t.x1;
+  const int64_t q01 = (int64_t)t.y1 * a.W + t.x0, q11 = (int64_t)t.y1 * a.W + t.x1;
+  float o[3] = {0.f, 0.f, 0.f};
+  for (int l = 0; l < a.L; ++l) {
+    const float s = sigmoid_ref(sample(a.pre_s + l * plane, a.W, t));
+    const float* pa = pre_a + l * plane * 3;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float x = lerp2(__ldg(pa + q00 * 3 + k), __ldg(pa + q10 * 3 + k), __ldg(pa + q01 * 3 + k),
+                            __ldg(pa + q11 * 3 + k), t.fx, t.fy);
+      const float v = sigmoid_ref(x);
+      o[k] = fa(fm(v, s), fm(fsb(1.0f, s), o[k]));
+    }
+  }
+  out[idx * 3 + 0] = o[0];
+  out[idx * 3 + 1] = o[1];
+  out[idx * 3 + 2] = o[2];
+}
+
 inline int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
 
 }  // namespace
@@ -181,8 +241,9 @@ inline int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
 void render_fused(const RenderArgs& a, cudaStream_t st) {
   const int64_t n = (int64_t)(a.row1 - a.row0) * a.Wo;
   const int g = blocks_for(n, 128);
-  const size_t sm = a.M * sizeof(DevCam);
-  switch (a.M) {
+  const int mm = a.pc_valid && (a.M == 4 || a.M == 8 || a.M == 16) ? a.M : 0;
+  const size_t sm = mm ? 0 : a.M * sizeof(DevCam);  // <0> stages the cameras in smem
+  switch (mm) {
     case 4: launch_k(render_fused_kernel<4>, g, 128, sm, st, a); break;
     case 8: launch_k(render_fused_kernel<8>, g, 128, sm, st, a); break;
     case 16: launch_k(render_fused_kernel<16>, g, 128, sm, st, a); break;
@@ -194,6 +255,11 @@ void upsample_activate(const RenderArgs& a, float* depth, float* density, float*
                        cudaStream_t st) {
   const int64_t n = (int64_t)a.L * a.Ho * a.Wo;
   launch_k(upsample_activate_kernel, blocks_for(n, 128), 128, 0, st, a, depth, density, blend);
+}
+
+void direct_rgb(const RenderArgs& a, const float* pre_a, float* out, cudaStream_t st) {
+  const int64_t n = (int64_t)a.Ho * a.Wo;
+  launch_k(direct_rgb_kernel, blocks_for(n, 128), 128, 0, st, a, pre_a, out);
 }
 
 }  // namespace lvsg

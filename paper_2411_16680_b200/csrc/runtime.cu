@@ -157,6 +157,7 @@ struct lvsg_ctx {
   // arena
   lvsg::Buf enc_in, ren_in, rgb, enc_x, enc_t, ray_base;
   std::vector<lvsg::Buf> feats, rays;
+  lvsg::Buf splat_scratch;  // deterministic splat: counts, runs, keys, footprints (ints)
   lvsg::Buf V0, V1, deltas, t1, rinv, uh, ut, uu, payload, depth_in, points, depth_out, acc, fb,
       fbr, pre_d, pre_s, logits, anchors, ldm_d, ldm_s, ldm_b;
   lvsg::Buf cams_dev;  // DevCam / RayBaseCam tables
@@ -190,6 +191,8 @@ struct lvsg_ctx {
   // tensor and input-channel slice; rebuilt whenever weights are (re)bound
   std::map<std::tuple<const float*, int, int>, std::unique_ptr<lvsg::Buf>> wimg;
   lvsg::Buf wimg_tmp;  // uncached image for the stage entry points
+  std::vector<float> stem_host;  // encoder stem weights [32*27] + bias [32] (host copy)
+  int64_t pyr_He = -1, pyr_We = -1;  // encoder resolution of the resident feature pyramid
 };
 
 namespace lvsg {
@@ -251,6 +254,10 @@ void bind_weights(lvsg_ctx* c) {
   W.init_feature = take(C);
   W.stem_w = take(C * 27);
   W.stem_b = take(C);
+  c->stem_host.assign(size_t(C * 27 + C), 0.f);
+  CUDA_OK(cudaMemcpy(c->stem_host.data(), W.stem_w, size_t(C * 27) * sizeof(float), cudaMemcpyDeviceToHost));
+  CUDA_OK(cudaMemcpy(c->stem_host.data() + C * 27, W.stem_b, size_t(C) * sizeof(float),
+                     cudaMemcpyDeviceToHost));
   for (int64_t k = 0; k < cfg.pyramid_levels; ++k) {
     W.lvl_r1.push_back(pair());
     W.lvl_r2.push_back(pair());
@@ -311,6 +318,7 @@ void bind_weights(lvsg_ctx* c) {
 // Sizes every arena buffer for encoder input (He, We); no allocation after.
 void ensure_plan(lvsg_ctx* c, int64_t He, int64_t We) {
   if (c->He == He && c->We == We) return;
+  c->pyr_He = c->pyr_We = -1;  // buffers re-sized: no resident pyramid
   const Config& cfg = c->cfg;
   Plan plan = plan_forward(cfg, He, We);
   const int64_t M = cfg.views, C = cfg.channels, Ca = cfg.appear_channels(), K = cfg.pyramid_levels;
@@ -324,7 +332,7 @@ void ensure_plan(lvsg_ctx* c, int64_t He, int64_t We) {
     c->rays[size_t(k)].ensure(n);
   }
   c->ray_base.ensure(size_t(M * plan.pyramid.back().first * plan.pyramid.back().second * 32));
-  size_t maxV = 0, maxD = 0, maxU = 0, maxAcc = 0, maxFb = 0, maxIn = 0;
+  size_t maxV = 0, maxD = 0, maxU = 0, maxAcc = 0, maxFb = 0, maxIn = 0, maxSplat = 0;
   for (const StepPlan& sp : plan.steps) {
     maxV = std::max({maxV, size_t(sp.in_layers * sp.in_height * sp.in_width),
                      size_t(sp.layers * sp.height * sp.width)});
@@ -333,6 +341,12 @@ void ensure_plan(lvsg_ctx* c, int64_t He, int64_t We) {
     maxD = std::max(maxD, size_t(sp.layers * sp.height * sp.width * M * ((C + 3) / 4) * 4));
     maxU = std::max(maxU, size_t(M * sp.feat_h * sp.feat_w));
     maxAcc = std::max(maxAcc, size_t(M * sp.layers * sp.render_h * sp.render_w * acc_stride(int(Ca) + 1)));
+    // deterministic splat over the volume entering the step (at most
+    // max(in_layers, layers) x in_height x in_width texels, all views):
+    // bins = views x layers x render pixels
+    const int64_t Ls = std::max(sp.in_layers, sp.layers);
+    maxSplat = std::max(maxSplat, splat_det_scratch_ints(M * Ls * sp.in_height * sp.in_width,
+                                                         M * Ls * sp.render_h * sp.render_w));
     maxFb = std::max(maxFb, size_t(M * sp.render_h * sp.render_w * pay_stride(int(Ca) + 1)));
   }
   c->V0.ensure(maxV * C);
@@ -348,6 +362,7 @@ void ensure_plan(lvsg_ctx* c, int64_t He, int64_t We) {
   c->points.ensure(maxIn * 3);
   c->depth_out.ensure(maxV);
   c->acc.ensure(maxAcc);
+  c->splat_scratch.ensure(maxSplat);
   c->fb.ensure(maxFb);
   c->fbr.ensure(maxU * pay_stride(int(Ca) + 1));
   const StepPlan& last = plan.steps.back();
@@ -612,12 +627,74 @@ CamTables upload_cams(lvsg_ctx* c, const lvsg_camera* enc_cams, const lvsg_frust
   return t;
 }
 
-// forward() on device images [M, He, We, 3]; leaves pre_d / pre_s / logits
-// (volume resolution) and the final V resident.
+// encode_inputs' convolutional part (network.hpp:388-395) for views
+// [m0, m1) of the device images [M, He, We, 3]: stem, per-level residual
+// pairs and mean pools, written into those views' slices of the resident
+// feature pyramid feats[k] ([M, H_k, W_k, C]). Target-independent: one
+// encode serves every target of the frame (and, view-sharded, every GPU).
 // enc_ready (optional, one event per view): view m's encoder image is only
 // valid on the device once enc_ready[m] has fired (host-ABI uploads); level 0
-// of the encoder then runs view by view so each view's upload overlaps the
-// previous view's convolutions.
+// then runs view by view so each view's upload overlaps the previous view's
+// convolutions.
+void encode_views(lvsg_ctx* c, const float* enc, int64_t He, int64_t We, int m0, int m1,
+                  const cudaEvent_t* enc_ready = nullptr) {
+  const Config& cfg = c->cfg;
+  const int C = int(cfg.channels), K = int(cfg.pyramid_levels), B = m1 - m0;
+  cudaStream_t st = c->stream;
+  const NetW& W = c->W;
+  int h = int(He), w = int(We);
+  const size_t per_in = size_t(h) * w * 3;
+  auto fslice = [&](int k) {  // views [m0, m1) of pyramid level k
+    const auto& e = c->plan.pyramid[size_t(k)];
+    return c->feats[size_t(k)].p + size_t(m0) * e.first * e.second * C;
+  };
+  const float* x = c->enc_x.p;
+  int k0 = 0;
+  if (enc_ready) {
+    const size_t per_x = size_t(h) * w * C;
+    const size_t per_f = size_t(h / 2) * (w / 2) * C;
+    for (int m = m0; m < m1; ++m) {
+      CUDA_OK(cudaStreamWaitEvent(st, enc_ready[m], 0));
+      float* xm = c->enc_x.p + per_x * (m - m0);
+      ConvArgs a = conv_args(1, h, w, 3, C, W.stem_w, W.stem_b, xm);
+      a.stem_host = c->stem_host.data();
+      a.src[0] = ConvSrc{enc + per_in * m, 3, 3, (long long)per_in};
+      a.nsrc = 1;
+      run_conv(c, a, st);
+      mark(c, "conv", 1);
+      conv_residual(c, xm, xm, c->enc_t.p, 1, h, w, W.lvl_r1[0]);
+      conv_residual(c, xm, xm, c->enc_t.p, 1, h, w, W.lvl_r2[0], fslice(0) + per_f * (m - m0));
+    }
+    h /= 2;
+    w /= 2;
+    x = fslice(0);
+    k0 = 1;
+  } else {
+    ConvArgs a = conv_args(B, h, w, 3, C, W.stem_w, W.stem_b, c->enc_x.p);
+    a.stem_host = c->stem_host.data();
+    a.src[0] = ConvSrc{enc + per_in * m0, 3, 3, (long long)per_in};
+    a.nsrc = 1;
+    run_conv(c, a, st);
+    mark(c, "conv", 1);
+  }
+  for (int k = k0; k < K; ++k) {
+    // level 0 reads the stem output in enc_x, level >= 1 feats[k-1]; both
+    // write the level's residual pairs to enc_x and the pool to feats[k]
+    float* xo = c->enc_x.p;
+    conv_residual(c, x, xo, c->enc_t.p, B, h, w, W.lvl_r1[size_t(k)]);
+    conv_residual(c, xo, xo, c->enc_t.p, B, h, w, W.lvl_r2[size_t(k)], fslice(k));
+    h /= 2;
+    w /= 2;
+    x = fslice(k);
+  }
+  c->pyr_He = He;
+  c->pyr_We = We;
+}
+
+// forward() on device images [M, He, We, 3]; leaves pre_d / pre_s / logits
+// (volume resolution) and the final V resident. enc == nullptr: the encoder
+// is skipped and the resident pyramid (lvsg_encode_device, all M views, at
+// this He x We) is used. enc_ready: see encode_views.
 void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
                     const lvsg_camera* enc_cams, const lvsg_frustum& target,
                     const lvsg_camera* render_cams, CamTables* tables_out,
@@ -627,6 +704,9 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
   frustum_validate(target);
   for (int64_t m = 0; m < cfg.views; ++m) camera_validate(enc_cams[m]);
   ensure_plan(c, He, We);
+  if (!enc && (c->pyr_He != He || c->pyr_We != We))
+    throw DimError("forward: no resident feature pyramid for " + std::to_string(He) + "x" +
+                   std::to_string(We) + " inputs (lvsg_encode_device first)");
   const Plan& plan = c->plan;
   const int M = int(cfg.views), C = int(cfg.channels), Ca = int(cfg.appear_channels());
   const int K = int(cfg.pyramid_levels);
@@ -642,43 +722,7 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
 
   // ---- encode_inputs --------------------------------------------------------
   {
-    int h = int(He), w = int(We);
-    const float* x = c->enc_x.p;
-    int k0 = 0;
-    if (enc_ready) {
-      // level 0 per view, each behind its upload
-      const size_t per_in = size_t(h) * w * 3, per_x = size_t(h) * w * C;
-      const size_t per_f = size_t(h / 2) * (w / 2) * C;
-      for (int m = 0; m < M; ++m) {
-        CUDA_OK(cudaStreamWaitEvent(st, enc_ready[m], 0));
-        float* xm = c->enc_x.p + per_x * m;
-        ConvArgs a = conv_args(1, h, w, 3, C, W.stem_w, W.stem_b, xm);
-        a.src[0] = ConvSrc{enc + per_in * m, 3, 3, (long long)per_in};
-        a.nsrc = 1;
-        run_conv(c, a, st);
-        mark(c, "conv", 1);
-        conv_residual(c, xm, xm, c->enc_t.p, 1, h, w, W.lvl_r1[0]);
-        conv_residual(c, xm, xm, c->enc_t.p, 1, h, w, W.lvl_r2[0], c->feats[0].p + per_f * m);
-      }
-      h /= 2;
-      w /= 2;
-      x = c->feats[0].p;
-      k0 = 1;
-    } else {
-      ConvArgs a = conv_args(M, h, w, 3, C, W.stem_w, W.stem_b, c->enc_x.p);
-      a.src[0] = ConvSrc{enc, 3, 3, (long long)h * w * 3};
-      a.nsrc = 1;
-      run_conv(c, a, st);
-      mark(c, "conv", 1);
-    }
-    for (int k = k0; k < K; ++k) {
-      float* xo = k == 0 ? c->enc_x.p : c->enc_x.p;  // level >= 1 reads feats[k-1], writes enc_x
-      conv_residual(c, x, xo, c->enc_t.p, M, h, w, W.lvl_r1[size_t(k)]);
-      conv_residual(c, xo, xo, c->enc_t.p, M, h, w, W.lvl_r2[size_t(k)], c->feats[size_t(k)].p);
-      h /= 2;
-      w /= 2;
-      x = c->feats[size_t(k)].p;
-    }
+    if (enc) encode_views(c, enc, He, We, 0, M, enc_ready);
     const int hK = int(plan.pyramid.back().first), wK = int(plan.pyramid.back().second);
     if (cfg.ablate_rays) {
       for (int k = 0; k < K; ++k)
@@ -752,10 +796,20 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
     if (cfg.ablate_render) {
       CUDA_OK(cudaMemsetAsync(c->fbr.p, 0, size_t(M) * Hf * Wf * PS * sizeof(float), st));
     } else {
-      CUDA_OK(cudaMemsetAsync(c->acc.p, 0, size_t(M) * L * Hv * Wv * acc_stride(Kp) * sizeof(float), st));
-      splat(c->payload.p, c->points.p, int(L), int(H * Wd), Kp, cams.rend[s], M, Hv, Wv, c->acc.p, st);
-      splat_composite(c->acc.p, M, int(L), Hv, Wv, Kp, c->fb.p, st);
-      mark(c, "splat", 2);
+      static const bool atomic_splat = [] {
+        const char* e = getenv("LVSG_SPLAT");
+        return e && e[0] == 'a';  // LVSG_SPLAT=atomic: the fp32-atomics splat (A/B runs)
+      }();
+      if (atomic_splat) {
+        CUDA_OK(cudaMemsetAsync(c->acc.p, 0, size_t(M) * L * Hv * Wv * acc_stride(Kp) * sizeof(float), st));
+        splat(c->payload.p, c->points.p, int(L), int(H * Wd), Kp, cams.rend[s], M, Hv, Wv, c->acc.p, st);
+        splat_composite(c->acc.p, M, int(L), Hv, Wv, Kp, c->fb.p, st);
+        mark(c, "splat", 2);
+      } else {
+        splat_det(c->payload.p, c->points.p, int(L), int(H * Wd), Kp, cams.rend[s], M, Hv, Wv,
+                  reinterpret_cast<int*>(c->splat_scratch.p), c->fb.p, st);
+        mark(c, "splat", 6);
+      }
       if (sp.doubled) {
         resize_hwc(c->fb.p, c->fbr.p, M, Hv, Wv, PS, Hf, Wf, st);
         mark(c, "misc", 1);
@@ -813,7 +867,8 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
 }
 
 RenderArgs render_args(lvsg_ctx* c, const float* images, int64_t Hr, int64_t Wr,
-                       const DevCam* cams_dev, float* rgb, int64_t row0, int64_t row1) {
+                       const DevCam* cams_dev, float* rgb, int64_t row0, int64_t row1,
+                       const lvsg_camera* host_cams = nullptr) {
   RenderArgs a;
   std::memset(&a, 0, sizeof(a));
   a.pre_d = c->pre_d.p;
@@ -830,6 +885,12 @@ RenderArgs render_args(lvsg_ctx* c, const float* images, int64_t Hr, int64_t Wr,
   a.act = depth_act(c->L, c->target);
   a.rc = ray_cam(c->target.camera, a.Wo, a.Ho);
   a.cams = cams_dev;
+  // the same cameras by value in the kernel's parameter space (constant-bank
+  // operands, no per-view shared-memory loads)
+  if (host_cams && a.M <= kRenderParamViews) {
+    for (int m = 0; m < a.M; ++m) a.pc[m] = dev_cam(host_cams[m]);
+    a.pc_valid = 1;
+  }
   a.images = images;
   a.Hr = int(Hr);
   a.Wr = int(Wr);
@@ -1147,6 +1208,30 @@ lvsg_status lvsg_forward(lvsg_ctx* c, int64_t views, const float* const* images,
       d2h(out->blend, c->ldm_b.p, Po * M);
       d2h(out->blend_logits, c->logits.p, P * M);
       d2h(out->volume, c->V, P * C);
+      if (out->deltas) {
+        // device layout: view-major SoA [M][G = ceil(C/4)][P][4] (channels
+        // padded to 4G) -> [L,H,W,M,C]
+        const int64_t G = (C + 3) / 4;
+        std::vector<float> soa(size_t(P * M * G * 4));
+        d2h(soa.data(), c->deltas.p, P * M * G * 4);
+        for (int64_t m = 0; m < M; ++m)
+          for (int64_t g = 0; g < G; ++g) {
+            const int64_t n = std::min<int64_t>(4, C - 4 * g);
+            for (int64_t p = 0; p < P; ++p)
+              std::memcpy(out->deltas + (p * M + m) * C + 4 * g,
+                          soa.data() + ((m * G + g) * P + p) * 4, size_t(n) * sizeof(float));
+          }
+      }
+      if (out->rgb && c->cfg.direct_rgb) {
+        const int64_t Ho = c->plan.out_height, Wo = c->plan.out_width;
+        c->ldm_d.ensure(size_t(P * 3));  // pre_a, then the composite
+        c->rgb.ensure(size_t(Ho * Wo * 3));
+        decode_linear(c->V, P, int(C), c->W.w_appear, 3, c->ldm_d.p, c->stream);
+        RenderArgs a = render_args(c, nullptr, 0, 0, nullptr, nullptr, 0, Ho);
+        direct_rgb(a, c->ldm_d.p, c->rgb.p, c->stream);
+        sync_and_check(c);
+        d2h(out->rgb, c->rgb.p, Ho * Wo * 3);
+      }
     } else {
       sync_and_check(c);
     }
@@ -1162,7 +1247,7 @@ lvsg_status lvsg_render(lvsg_ctx* c, int64_t views, const float* const* images, 
     DevCam* dc = upload_render_cams(c, cams);
     const int64_t Ho = c->plan.out_height, Wo = c->plan.out_width;
     c->rgb.ensure(size_t(Ho * Wo * 3));
-    render_fused(render_args(c, c->ren_in.p, height, width, dc, c->rgb.p, 0, Ho), c->stream);
+    render_fused(render_args(c, c->ren_in.p, height, width, dc, c->rgb.p, 0, Ho, cams), c->stream);
     CUDA_OK(cudaMemcpyAsync(rgb_out, c->rgb.p, size_t(Ho * Wo * 3) * sizeof(float),
                             cudaMemcpyDeviceToHost, c->stream));
     sync_and_check(c);
@@ -1182,28 +1267,34 @@ lvsg_status lvsg_forward_render(lvsg_ctx* c, int64_t views, const float* const* 
     // buffers): the encoder views one by one, each with an event the encoder's
     // per-view level 0 waits on, then the render views, needed only by the
     // final render, under the rest of the forward pass.
-    CUDA_OK(cudaEventRecord(c->ev_main, c->stream));
-    CUDA_OK(cudaStreamWaitEvent(c->xfer, c->ev_main, 0));
+    // enc_images == NULL: no encoder upload, the resident pyramid
+    // (lvsg_encode_device, completed on this context's stream) is used, and
+    // the render views go up at once, under the encode still in flight on
+    // the stream (ren_in is only read by calls that synchronise before they
+    // return, so no earlier work can still be reading it).
     const size_t per = size_t(enc_h * enc_w * 3);
-    if (!enc_images) throw DimError("forward: null image list");
-    for (int64_t m = 0; m < views; ++m)
-      if (!enc_images[m]) throw DimError("forward: null image");
-    c->enc_in.ensure(per * size_t(views));
-    while (c->ev_enc.size() < size_t(views)) {
-      cudaEvent_t e;
-      CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      c->ev_enc.push_back(e);
-    }
-    for (int64_t m = 0; m < views; ++m) {
-      CUDA_OK(cudaMemcpyAsync(c->enc_in.p + per * size_t(m), enc_images[m], per * sizeof(float),
-                              cudaMemcpyHostToDevice, c->xfer));
-      CUDA_OK(cudaEventRecord(c->ev_enc[size_t(m)], c->xfer));
+    if (enc_images) {
+      CUDA_OK(cudaEventRecord(c->ev_main, c->stream));
+      CUDA_OK(cudaStreamWaitEvent(c->xfer, c->ev_main, 0));
+      for (int64_t m = 0; m < views; ++m)
+        if (!enc_images[m]) throw DimError("forward: null image");
+      c->enc_in.ensure(per * size_t(views));
+      while (c->ev_enc.size() < size_t(views)) {
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ev_enc.push_back(e);
+      }
+      for (int64_t m = 0; m < views; ++m) {
+        CUDA_OK(cudaMemcpyAsync(c->enc_in.p + per * size_t(m), enc_images[m], per * sizeof(float),
+                                cudaMemcpyHostToDevice, c->xfer));
+        CUDA_OK(cudaEventRecord(c->ev_enc[size_t(m)], c->xfer));
+      }
     }
     upload_images(c, c->ren_in, views, render_images, render_h, render_w, c->xfer);
     CUDA_OK(cudaEventRecord(c->ev_ren, c->xfer));
     CamTables t;
-    forward_device(c, c->enc_in.p, enc_h, enc_w, enc_cams, *target, render_cams, &t,
-                   c->ev_enc.data());
+    forward_device(c, enc_images ? c->enc_in.p : nullptr, enc_h, enc_w, enc_cams, *target,
+                   render_cams, &t, enc_images ? c->ev_enc.data() : nullptr);
     const int64_t Ho = c->plan.out_height, Wo = c->plan.out_width;
     c->rgb.ensure(size_t(Ho * Wo * 3));
     CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev_ren, 0));
@@ -1213,7 +1304,7 @@ lvsg_status lvsg_forward_render(lvsg_ctx* c, int64_t views, const float* const* 
       const int64_t r0 = Ho * k / NB, r1 = Ho * (k + 1) / NB;
       if (r1 == r0) continue;
       render_fused(render_args(c, c->ren_in.p, render_h, render_w, t.final_cams, c->rgb.p + r0 * Wo * 3,
-                               r0, r1),
+                               r0, r1, render_cams),
                    c->stream);
       c->launches += 1;
       CUDA_OK(cudaEventRecord(c->ev_band[k], c->stream));
@@ -1232,6 +1323,8 @@ lvsg_status lvsg_forward_render_device(lvsg_ctx* c, int64_t views, const float* 
                                        const float* render_images, int64_t render_h,
                                        int64_t render_w, const lvsg_camera* render_cams,
                                        const lvsg_frustum* target, float* rgb_out, void* stream) {
+  // enc_images == NULL: the encoder is skipped and the resident pyramid of
+  // lvsg_encode_device is used (one encode, many targets / GPUs)
   return guard(c, [&] {
     check_views(c, views, enc_h, enc_w);
     check_views(c, views, render_h, render_w);
@@ -1243,7 +1336,8 @@ lvsg_status lvsg_forward_render_device(lvsg_ctx* c, int64_t views, const float* 
       CamTables t;
       forward_device(c, enc_images, enc_h, enc_w, enc_cams, *target, render_cams, &t);
       const int64_t Ho = c->plan.out_height;
-      render_fused(render_args(c, render_images, render_h, render_w, t.final_cams, rgb_out, 0, Ho),
+      render_fused(render_args(c, render_images, render_h, render_w, t.final_cams, rgb_out, 0, Ho,
+                               render_cams),
                    c->stream);
       mark(c, "render", 1);
     c->launches += 1;
@@ -1253,6 +1347,46 @@ lvsg_status lvsg_forward_render_device(lvsg_ctx* c, int64_t views, const float* 
       throw;
     }
     c->stream = own;
+  });
+}
+
+lvsg_status lvsg_encode_device(lvsg_ctx* c, int64_t views, const float* enc_images, int64_t enc_h,
+                               int64_t enc_w, int64_t view0, int64_t view1, void* stream) {
+  return guard(c, [&] {
+    check_views(c, views, enc_h, enc_w);
+    if (view0 < 0 || view1 > views || view0 > view1) throw DimError("encode_inputs: bad view range");
+    if (!c->have_weights)
+      throw DimError("forward: no weights loaded (lvsg_load_weights / lvsg_init_weights)");
+    plan_forward(c->cfg, enc_h, enc_w);  // DimError on a bad extent, before any launch
+    ensure_plan(c, enc_h, enc_w);
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    cudaStream_t own = c->stream;
+    if (user) c->stream = user;
+    const int64_t launches0 = g_launches;
+    try {
+      if (view1 > view0) encode_views(c, enc_images, enc_h, enc_w, int(view0), int(view1));
+      c->pyr_He = enc_h;
+      c->pyr_We = enc_w;
+      CUDA_OK(cudaGetLastError());
+    } catch (...) {
+      c->stream = own;
+      throw;
+    }
+    c->stream = own;
+    c->launches = g_launches - launches0;
+  });
+}
+
+lvsg_status lvsg_pyramid_level(lvsg_ctx* c, int64_t level, float** data, int64_t dims[4]) {
+  return guard(c, [&] {
+    if (c->pyr_He < 0) throw DimError("pyramid: no resident feature pyramid (lvsg_encode_device)");
+    if (level < 0 || level >= c->cfg.pyramid_levels) throw DimError("pyramid: bad level");
+    const auto& e = c->plan.pyramid[size_t(level)];
+    *data = c->feats[size_t(level)].p;
+    dims[0] = c->cfg.views;
+    dims[1] = e.first;
+    dims[2] = e.second;
+    dims[3] = c->cfg.channels;
   });
 }
 
@@ -1268,7 +1402,8 @@ lvsg_status lvsg_render_rows_device(lvsg_ctx* c, int64_t views, const float* ren
     cudaStream_t own = c->stream;
     if (user) c->stream = user;
     DevCam* dc = upload_render_cams(c, render_cams);
-    render_fused(render_args(c, render_images, render_h, render_w, dc, rgb_out, row0, row1),
+    render_fused(render_args(c, render_images, render_h, render_w, dc, rgb_out, row0, row1,
+                               render_cams),
                  c->stream);
     c->stream = own;
     CUDA_OK(cudaGetLastError());

@@ -181,13 +181,17 @@ def _img_ptrs(images):
 
 @dataclass
 class Ldm:
-    """Ldm<T> (ldm.hpp:14-21) plus the pre-softmax blend logits and final
-    volume of ForwardResult (network.hpp:551-558)."""
+    """Ldm<T> (ldm.hpp:14-21) plus the rest of ForwardResult
+    (network.hpp:551-558): pre-softmax blend logits, final volume, the final
+    step's deltas and, for direct_rgb configs, the decoded-colour composite
+    `rgb` (None otherwise)."""
     depth: np.ndarray
     density: np.ndarray
     blend: np.ndarray
     blend_logits: np.ndarray
     volume: np.ndarray
+    deltas: Optional[np.ndarray] = None
+    rgb: Optional[np.ndarray] = None
 
 
 class Model:
@@ -196,6 +200,7 @@ class Model:
 
     def __init__(self, cfg: ModelConfig, device: int = 0):
         self.cfg = cfg
+        self.device = int(device)
         self._cc = cfg.to_c()
         self._lib = capi.lib()
         h = ctypes.c_void_p()
@@ -232,7 +237,7 @@ class Model:
 
     # --- forward / render ---
     def forward(self, images, cams: Sequence[Camera], target: Frustum,
-                outputs: bool = True) -> Optional[Ldm]:
+                outputs: bool = True, deltas: bool = False) -> Optional[Ldm]:
         arr, keep, H, W = _img_ptrs(images)
         fr = target.to_c()
         out = None
@@ -244,9 +249,12 @@ class Model:
             Ho, Wo = plan.out_height, plan.out_width
             res = Ldm(np.zeros((L_, Ho, Wo), np.float32), np.zeros((L_, Ho, Wo), np.float32),
                       np.zeros((L_, Ho, Wo, M), np.float32), np.zeros((L_, Hh, Ww, M), np.float32),
-                      np.zeros((L_, Hh, Ww, C), np.float32))
-            out = capi.LdmOutC(*[a.ctypes.data_as(capi.c_f32p) for a in
-                                 (res.depth, res.density, res.blend, res.blend_logits, res.volume)])
+                      np.zeros((L_, Hh, Ww, C), np.float32),
+                      np.zeros((L_, Hh, Ww, M, C), np.float32) if deltas else None,
+                      np.zeros((Ho, Wo, 3), np.float32) if self.cfg.direct_rgb else None)
+            out = capi.LdmOutC(*[a.ctypes.data_as(capi.c_f32p) if a is not None else None for a in
+                                 (res.depth, res.density, res.blend, res.blend_logits, res.volume,
+                                  res.deltas, res.rgb)])
         self._check(self._lib.lvsg_forward(self._h, len(keep), arr, H, W, _cam_array(cams),
                                            ctypes.byref(fr), ctypes.byref(out) if out else None))
         return res
@@ -260,10 +268,16 @@ class Model:
         return rgb
 
     def forward_render(self, enc_images, enc_cams, render_images, render_cams,
-                       target: Frustum, out: Optional[np.ndarray] = None) -> np.ndarray:
+                       target: Frustum, out: Optional[np.ndarray] = None,
+                       enc_hw=None) -> np.ndarray:
         """Host buffers in, host RGB out (optionally into `out`, e.g. a view of
-        pinned memory)."""
-        ea, ek, He, We = _img_ptrs(enc_images)
+        pinned memory). enc_images=None: the resident pyramid of encode_device
+        (complete on stream_handle()) at encoder resolution enc_hw."""
+        if enc_images is None:
+            ea, ek = None, [None] * self.cfg.views
+            He, We = enc_hw
+        else:
+            ea, ek, He, We = _img_ptrs(enc_images)
         ra, rk, Hr, Wr = _img_ptrs(render_images)
         if out is None:
             plan = plan_forward(self.cfg, He, We)
@@ -280,22 +294,53 @@ class Model:
         return rgb
 
     def forward_render_device(self, enc_images, enc_cams, render_images, render_cams,
-                              target: Frustum, rgb_out, stream=None) -> None:
+                              target: Frustum, rgb_out, stream=None, enc_hw=None) -> None:
         """Device-resident path on torch CUDA tensors (enc [M,He,We,3],
         render [M,Hr,Wr,3], rgb_out [Ho,Wo,3]); enqueued on `stream`
-        (torch.cuda.Stream or raw handle; default: torch's current stream)."""
+        (torch.cuda.Stream or raw handle; default: torch's current stream).
+        enc_images=None: the resident pyramid of encode_device (encoder
+        resolution enc_hw) is used instead of encoding."""
         import torch
-        for t in (enc_images, render_images, rgb_out):
+        for t in (render_images, rgb_out) + ((enc_images,) if enc_images is not None else ()):
             if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
                 raise capi.DimError("device tensors must be contiguous float32 CUDA tensors")
         sh = _stream_handle(stream)
-        M, He, We, _ = enc_images.shape
-        _, Hr, Wr, _ = render_images.shape
+        M, Hr, Wr, _ = render_images.shape
+        if enc_images is not None:
+            _, He, We, _ = enc_images.shape
+            ep = enc_images.data_ptr()
+        else:
+            He, We = enc_hw
+            ep = None
         fr = target.to_c()
         self._check(self._lib.lvsg_forward_render_device(
-            self._h, M, enc_images.data_ptr(), He, We, _cam_array(enc_cams),
+            self._h, M, ep, He, We, _cam_array(enc_cams),
             render_images.data_ptr(), Hr, Wr, _cam_array(render_cams), ctypes.byref(fr),
             rgb_out.data_ptr(), sh))
+
+    def encode_device(self, enc_images, view0: int = 0, view1: Optional[int] = None,
+                      stream=None) -> None:
+        """encode_inputs' convolutions for views [view0, view1) of the device
+        images [M,He,We,3] into the resident feature pyramid (lvsg_encode_device)."""
+        M, He, We, _ = enc_images.shape
+        self._check(self._lib.lvsg_encode_device(self._h, M, enc_images.data_ptr(), He, We, view0,
+                                                 M if view1 is None else view1,
+                                                 _stream_handle(stream)))
+
+    def pyramid_level(self, level: int):
+        """Level `level` of the resident feature pyramid as a torch CUDA tensor
+        [M, H_k, W_k, C] aliasing the context's buffer (e.g. for an NCCL
+        all-gather of a view-sharded encode)."""
+        import torch
+        ptr = ctypes.c_void_p()
+        dims = (ctypes.c_int64 * 4)()
+        self._check(self._lib.lvsg_pyramid_level(self._h, level, ctypes.byref(ptr), dims))
+        shape = tuple(int(d) for d in dims)
+
+        class _Cai:  # __cuda_array_interface__ v3 view of the device buffer
+            __cuda_array_interface__ = {"shape": shape, "typestr": "<f4", "data": (ptr.value, False),
+                                        "version": 3, "strides": None, "stream": None}
+        return torch.as_tensor(_Cai(), device=torch.device("cuda", self.device))
 
     def render_rows_device(self, render_images, render_cams, row0, row1, rgb_out, stream=None):
         sh = _stream_handle(stream)
@@ -303,6 +348,11 @@ class Model:
         self._check(self._lib.lvsg_render_rows_device(self._h, M, render_images.data_ptr(), Hr, Wr,
                                                       _cam_array(render_cams), row0, row1,
                                                       rgb_out.data_ptr(), sh))
+
+    def stream_handle(self) -> int:
+        """The context's own CUDA stream (cudaStream_t as int), e.g. for
+        torch.cuda.ExternalStream."""
+        return int(self._lib.lvsg_stream(self._h) or 0)
 
     def synchronize(self):
         self._check(self._lib.lvsg_synchronize(self._h))

@@ -78,3 +78,39 @@ def split_counts(n: int, world: int) -> Sequence[int]:
     """Units per rank when n independent units (targets, frames) are dealt
     round-robin."""
     return [n // world + (1 if r < n % world else 0) for r in range(world)]
+
+
+def view_range(rank: int, world: int, views: int) -> Tuple[int, int]:
+    """[v0, v1) input views encoded by `rank` in a view-sharded encode: the
+    feature pyramid is target-independent (encode_inputs, network.hpp:368-417),
+    so each GPU encodes a contiguous share of the M views once per frame and
+    the shares are all-gathered."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("view_range: bad rank / world")
+    return views * rank // world, views * (rank + 1) // world
+
+
+def allgather_views(level, views: int) -> None:
+    """In-place all-gather of one pyramid level [M, H_k, W_k, C] whose view
+    slices [v0, v1) (view_range) were each produced on their own rank: after
+    the call every rank holds all M views. NCCL with an even split: one
+    in-place all_gather_into_tensor over NVLink on the current stream; other
+    backends / uneven splits: a padded all_gather."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return
+    world, rank = dist.get_world_size(), dist.get_rank()
+    v0, v1 = view_range(rank, world, views)
+    if views % world == 0 and dist.get_backend() == "nccl":
+        dist.all_gather_into_tensor(level, level[v0:v1])
+        return
+    per = max(view_range(r, world, views)[1] - view_range(r, world, views)[0] for r in range(world))
+    pad = torch.zeros((per,) + tuple(level.shape[1:]), dtype=level.dtype, device=level.device)
+    pad[: v1 - v0] = level[v0:v1]
+    parts: List = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad)
+    for r, p in enumerate(parts):
+        a, b = view_range(r, world, views)
+        if r != rank:
+            level[a:b] = p[: b - a]

@@ -68,10 +68,11 @@ def test_forward_outputs_match_oracle(oracle):
     case = config1()
     m = q.Model(case.cfg, device=0)
     m.load_weights(case.store())
-    ldm = m.forward(case.enc_images, case.enc_cams, case.target)
-    want = run_oracle(oracle, case, outputs=("depth", "density", "blend", "blend_logits", "volume"))
+    ldm = m.forward(case.enc_images, case.enc_cams, case.target, deltas=True)
+    want = run_oracle(oracle, case, outputs=("depth", "density", "blend", "blend_logits", "volume",
+                                             "deltas"))
     for k, tol in (("depth", 1e-4), ("density", 1e-4), ("blend", 1e-4), ("blend_logits", 1e-3),
-                   ("volume", 1e-3)):
+                   ("volume", 1e-3), ("deltas", 1e-3)):
         got = getattr(ldm, k)
         rel = float(np.abs(got - want[k]).max() / max(1.0, np.abs(want[k]).max()))
         print(k, rel)
@@ -81,14 +82,42 @@ def test_forward_outputs_match_oracle(oracle):
     assert float(np.abs(rgb - run_oracle(oracle, case)["rgb"]).max()) <= RGB_MAX_ABS
 
 
-def test_repeat_calls_are_stable():
-    """Repeated forwards: the splat uses fp32 atomics, so bits may move by
-    accumulation order, but results stay within 1e-5."""
-    case = nano()
+def test_direct_rgb_forward_result_matches_oracle(oracle):
+    """ForwardResult.rgb of a direct_rgb config (network.hpp:596-601): the
+    decoded-colour composite, fp32 RGB gate, next to the deltas."""
+    case = nano(direct_rgb=True)
+    m = q.Model(case.cfg, device=0)
+    m.load_weights(case.store())
+    ldm = m.forward(case.enc_images, case.enc_cams, case.target, deltas=True)
+    want = run_oracle(oracle, case, outputs=("rgb_direct", "deltas"))
+    assert ldm.rgb is not None and ldm.rgb.shape == want["rgb_direct"].shape
+    err = float(np.abs(ldm.rgb - want["rgb_direct"]).max())
+    print(f"direct rgb max-abs {err:.3e} psnr {psnr(ldm.rgb, want['rgb_direct']):.1f} dB")
+    assert err <= RGB_MAX_ABS and psnr(ldm.rgb, want["rgb_direct"]) >= RGB_PSNR_DB
+    assert float(np.abs(ldm.deltas - want["deltas"]).max()) <= 1e-3
+    # a non-direct_rgb config has no ForwardResult.rgb
+    c2 = nano()
+    m2 = q.Model(c2.cfg, device=0)
+    m2.load_weights(c2.store())
+    assert m2.forward(c2.enc_images, c2.enc_cams, c2.target).rgb is None
+
+
+@pytest.mark.parametrize("make", [nano, config1], ids=["nano", "config1"])
+def test_repeat_calls_are_bit_identical(make):
+    """test_network.cpp:614-619: repeated forwards are bit-identical. Every
+    reduction is owner-computes in a fixed order (the splat included), so the
+    frame, the LDM and the volume repeat bit for bit, also across contexts."""
+    case = make()
     m, a = run_gpu(case)
     b = m.forward_render(case.enc_images, case.enc_cams, case.ren_images, case.ren_cams,
                          case.target)
-    assert float(np.abs(a - b).max()) <= 1e-5
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    l1 = m.forward(case.enc_images, case.enc_cams, case.target)
+    _, c = run_gpu(case)
+    assert np.array_equal(a.view(np.uint32), c.view(np.uint32))
+    l2 = m.forward(case.enc_images, case.enc_cams, case.target)
+    for k in ("depth", "density", "blend", "blend_logits", "volume"):
+        assert np.array_equal(getattr(l1, k).view(np.uint32), getattr(l2, k).view(np.uint32)), k
 
 
 def test_view_order_invariance():
@@ -141,6 +170,54 @@ def test_device_path_matches_host_path():
         m.render_rows_device(r, case.ren_cams, a, b, band[a:b])
     torch.cuda.synchronize()
     assert torch.equal(band, out)
+
+
+def test_resident_pyramid_serves_targets_and_view_shards():
+    """One encode per frame (lvsg_encode_device) serves several targets, and a
+    view-sharded encode (views [0, 4) and [4, 8) separately, as two GPUs
+    would before the all-gather) gives a bit-identical pyramid. Frames from
+    the resident pyramid match the full forward to 1e-5 (the splat's fp32
+    atomics make repeated frames differ in accumulation order only)."""
+    import torch
+    from paper_2411_16680_b200 import workloads as wl
+    dev = torch.device("cuda:0")
+    grid = wl.config5_targets()
+    cases = [wl.config2(div=4, target_center=grid[i]) for i in (0, 5)]
+    c0 = cases[0]
+    m = q.Model(c0.cfg, device=0)
+    m.init_weights(c0.seed)
+    e = torch.from_numpy(c0.enc_images).to(dev)
+    r = torch.from_numpy(c0.ren_images).to(dev)
+    He, We = e.shape[1], e.shape[2]
+    plan = q.plan_forward(c0.cfg, He, We)
+    shape = (plan.out_height, plan.out_width, 3)
+    with pytest.raises(q.DimError):  # no resident pyramid yet
+        m.forward_render_device(None, c0.enc_cams, r, c0.ren_cams, c0.target,
+                                torch.empty(shape, device=dev), enc_hw=(He, We))
+    full = []
+    for c in cases:
+        out = torch.empty(shape, dtype=torch.float32, device=dev)
+        m.forward_render_device(e, c.enc_cams, r, c.ren_cams, c.target, out)
+        full.append(out)
+    m.encode_device(e)
+    lv0 = m.pyramid_level(0).clone()
+    for c, want in zip(cases, full):
+        out = torch.empty(shape, dtype=torch.float32, device=dev)
+        m.forward_render_device(None, c.enc_cams, r, c.ren_cams, c.target, out, enc_hw=(He, We))
+        torch.cuda.synchronize()
+        assert torch.equal(out, want)
+    m.pyramid_level(0).zero_()
+    M = c0.cfg.views
+    m.encode_device(e, 0, M // 2)
+    m.encode_device(e, M // 2, M)
+    torch.cuda.synchronize()
+    assert torch.equal(m.pyramid_level(0), lv0)
+    assert tuple(lv0.shape) == (M, He // 2, We // 2, c0.cfg.channels)
+    out = torch.empty(shape, dtype=torch.float32, device=dev)
+    m.forward_render_device(None, cases[1].enc_cams, r, cases[1].ren_cams, cases[1].target, out,
+                            enc_hw=(He, We))
+    torch.cuda.synchronize()
+    assert torch.equal(out, full[1])
 
 
 def test_stage_indices_bit_exact(oracle):

@@ -49,6 +49,17 @@ def _worker(rank, world, port, out_dir):
         np.save(os.path.join(out_dir, f"full{rank}.npy"), full)
         with open(os.path.join(out_dir, f"t{rank}.txt"), "w") as f:
             f.write(f"{slowest} {fps}")
+
+        # (4) view-sharded encode: rank r produces pyramid views view_range(r)
+        # (here a deterministic stand-in per view), the all-gather completes
+        # every rank's copy; even (M=4) and uneven (M=5) splits
+        for M in (4, 5):
+            full_lv = torch.arange(M * 3 * 5 * 8, dtype=torch.float32).reshape(M, 3, 5, 8)
+            mine = torch.full_like(full_lv, float("nan"))
+            v0, v1 = shard.view_range(rank, world, M)
+            mine[v0:v1] = full_lv[v0:v1]
+            shard.allgather_views(mine, M)
+            np.save(os.path.join(out_dir, f"pyr{M}_{rank}.npy"), mine.numpy())
     finally:
         dist.destroy_process_group()
 
@@ -92,3 +103,14 @@ def test_two_rank_gloo(oracle, tmp_path):
         assert slowest == 2.0 and abs(fps - world * 3 / 2.0) < 1e-12
         g = np.load(tmp_path / f"gathered{r}.npy")
         assert np.array_equal(g, np.load(tmp_path / f"full{r}.npy"))
+        for M in (4, 5):
+            want = np.arange(M * 3 * 5 * 8, dtype=np.float32).reshape(M, 3, 5, 8)
+            assert np.array_equal(np.load(tmp_path / f"pyr{M}_{r}.npy"), want)
+
+
+def test_view_ranges_partition_views():
+    for world in (1, 2, 4, 8):
+        for views in (8, 16, 5):
+            rs = [shard.view_range(r, world, views) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == views
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))

@@ -86,11 +86,16 @@ def test_oracle_stages_vs_golden(oracle):
                               "ablate_rays", "direct_rgb"])
 def test_oracle_bit_exact_vs_live_reference(oracle, reference, make):
     c = make()
+    # every ForwardResult field: the LDM, blend logits, volume, the final
+    # step's deltas and, under direct_rgb, the decoded colour composite
+    outs = OUTS + ("deltas",) + (("rgb_direct",) if c.cfg.direct_rgb else ())
     r = reference.forward_render(c.cfg, c.enc_images, c.enc_cams, c.ren_images, c.ren_cams,
-                                 c.target, c.flat(), outputs=OUTS)
+                                 c.target, c.flat(), outputs=outs)
     o = oracle.forward_render(c.cfg, c.enc_images, c.enc_cams, c.ren_images, c.ren_cams, c.target,
-                              c.flat(), outputs=OUTS)
-    for k in OUTS:
+                              c.flat(), outputs=outs)
+    for k in outs:
+        assert np.isfinite(r[k]).all(), k
+        assert k not in ("deltas", "rgb_direct") or r[k].any(), k
         assert np.array_equal(bits(r[k]), bits(o[k])), k
 
 
