@@ -214,6 +214,8 @@ class Reference:
                                             P(capi.CameraC), vp, i64, i64, P(capi.CameraC),
                                             P(capi.FrustumC), vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                             vp, cp, sz]
+        L.ref_model_config_to_json.argtypes = [P(capi.ModelConfigC), cp, sz, cp, sz]
+        L.ref_model_config_roundtrip.argtypes = [cp, cp, sz, cp, sz]
         L.ref_world_points.argtypes = [P(capi.FrustumC), vp, i64, i64, i64, vp, cp, sz]
         L.ref_gather.argtypes = [P(capi.CameraC), vp, i64, i64, i64, vp, i64, vp, vp, cp, sz]
         L.ref_footprints.argtypes = [P(capi.CameraC), vp, i64, vp, vp, vp, cp, sz]
@@ -237,6 +239,19 @@ class Reference:
         self._call(self.lib.ref_init_param_store, ctypes.byref(cc.c), seed, _f32(out),
                    ranks.ctypes.data_as(vp), dims.ctypes.data_as(vp))
         return out, ranks, dims
+
+    def model_config_to_json(self, cfg) -> str:
+        cc = cfg.to_c()
+        buf = ctypes.create_string_buffer(1 << 16)
+        self._call(self.lib.ref_model_config_to_json, ctypes.byref(cc.c), buf, 1 << 16)
+        return buf.value.decode()
+
+    def model_config_roundtrip(self, text: str) -> str:
+        """model_config_to_json(model_config_from_json(text)); raises with the
+        reference's SchemaError / DimError message on a rejected document."""
+        buf = ctypes.create_string_buffer(1 << 16)
+        self._call(self.lib.ref_model_config_roundtrip, text.encode(), buf, 1 << 16)
+        return buf.value.decode()
 
     def plan_forward(self, cfg, h, w):
         cc = cfg.to_c()

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../include/lvsg.h"
+#include "lvs/io.hpp"
 #include "lvs/network.hpp"
 #include "lvs/scenes.hpp"
 
@@ -375,6 +376,28 @@ int ref_render_target(const lvsg_frustum* fr, const float* depth, const float* d
       cs.push_back(to_cam(cams[m]));
     }
     copy_out(tape.value(render_target(tape, ldm, ims, cs)), rgb);
+  });
+}
+
+// model_config_to_json (io.cpp:571-596) into out (NUL-terminated).
+int ref_model_config_to_json(const lvsg_model_config* c, char* out, size_t out_len, char* err,
+                             size_t len) {
+  return guarded(err, len, [&] {
+    const std::string j = model_config_to_json(to_cfg(c));
+    if (j.size() + 1 > out_len) throw std::runtime_error("ref_model_config_to_json: buffer too small");
+    std::memcpy(out, j.c_str(), j.size() + 1);
+  });
+}
+
+// model_config_from_json (io.cpp:598-633), re-serialised by
+// model_config_to_json into out (the parsed config, as text); SchemaError
+// and DimError keep their messages in err.
+int ref_model_config_roundtrip(const char* text, char* out, size_t out_len, char* err,
+                               size_t len) {
+  return guarded(err, len, [&] {
+    const std::string j = model_config_to_json(model_config_from_json(text));
+    if (j.size() + 1 > out_len) throw std::runtime_error("ref_model_config_roundtrip: buffer too small");
+    std::memcpy(out, j.c_str(), j.size() + 1);
   });
 }
 

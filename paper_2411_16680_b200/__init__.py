@@ -7,7 +7,8 @@ is its Python mirror. See DESIGN.md.
 """
 from .camera import Camera, Frustum, RigSpec, pose_cam_from_world  # noqa: F401
 from .capi import DeviceError, DimError, NumericError  # noqa: F401
-from .config import (ModelConfig, StepConfig, config1, full_scale_config,  # noqa: F401
-                     micro_config, nano_config, scaled_full_config)
+from .config import (ModelConfig, SchemaError, StepConfig, config1,  # noqa: F401
+                     full_scale_config, micro_config, model_config_from_json,
+                     model_config_to_json, nano_config, scaled_full_config)
 from .lvs import (Ldm, Model, init_param_store, param_shapes, plan_forward,  # noqa: F401
                   rig_cameras, scene_images, validate_config)

@@ -117,3 +117,113 @@ def scaled_full_config(div: int = 4) -> ModelConfig:
     steps = [StepConfig(s.in_layers, s.layers, s.height // div, s.width // div, s.pyramid_level,
                         s.blocks) for s in base.steps]
     return replace(base, steps=steps)
+
+
+# --- ModelConfig JSON (io.cpp:571-633) ----------------------------------------
+
+class SchemaError(ValueError):
+    """A config document that does not fit the schema (reference SchemaError,
+    io.hpp:28-31): bad JSON, a missing / mistyped / unknown field, or a
+    config that fails ModelConfig::validate ("$: ..." prefix)."""
+
+
+class _ObjView:
+    """io.cpp:345-402: typed field access that records what it consumed, so
+    close() can reject stray fields by name."""
+
+    def __init__(self, j, path):
+        if not isinstance(j, dict):
+            raise SchemaError(f"{path}: expected an object")
+        self.j, self.path, self.seen = j, path, set()
+
+    def _get(self, key):
+        self.seen.add(key)
+        if key not in self.j:
+            raise SchemaError(f"{self.path}.{key}: missing field")
+        return self.j[key]
+
+    def num(self, key):
+        v = self._get(key)
+        if isinstance(v, bool) or not isinstance(v, (int, float)):
+            raise SchemaError(f"{self.path}.{key}: expected a number")
+        return float(v)
+
+    def integer(self, key):
+        v = self._get(key)
+        if isinstance(v, bool) or not isinstance(v, int):
+            raise SchemaError(f"{self.path}.{key}: expected an integer")
+        return int(v)
+
+    def boolean(self, key, fallback):
+        self.seen.add(key)
+        if key not in self.j:
+            return fallback
+        v = self.j[key]
+        if not isinstance(v, bool):
+            raise SchemaError(f"{self.path}.{key}: expected a boolean")
+        return v
+
+    def str(self, key):
+        v = self._get(key)
+        if not isinstance(v, str):
+            raise SchemaError(f"{self.path}.{key}: expected a string")
+        return v
+
+    def array(self, key, min_len=0):
+        v = self._get(key)
+        if not isinstance(v, list):
+            raise SchemaError(f"{self.path}.{key}: expected an array")
+        if len(v) < min_len:
+            raise SchemaError(f"{self.path}.{key}: expected at least {min_len} entries")
+        return v
+
+    def close(self):
+        for k in self.j:
+            if k not in self.seen:
+                raise SchemaError(f'{self.path}: unknown field "{k}"')
+
+
+def model_config_to_json(cfg: ModelConfig) -> str:
+    """model_config_to_json (io.cpp:571-596): the same fields, 2-space indent,
+    keys in nlohmann's (sorted) order, trailing newline."""
+    import json
+    d = {"channels": cfg.channels, "views": cfg.views, "pyramid_levels": cfg.pyramid_levels,
+         "upsample": float(cfg.upsample), "near": float(cfg.near), "far": float(cfg.far),
+         "ablate_render": cfg.ablate_render, "ablate_attention": cfg.ablate_attention,
+         "ablate_rays": cfg.ablate_rays, "direct_rgb": cfg.direct_rgb,
+         "steps": [{"in_layers": s.in_layers, "layers": s.layers, "height": s.height,
+                    "width": s.width, "pyramid_level": s.pyramid_level, "blocks": s.blocks}
+                   for s in cfg.steps]}
+    return json.dumps(d, indent=2, sort_keys=True) + "\n"
+
+
+def model_config_from_json(text: str) -> ModelConfig:
+    """model_config_from_json (io.cpp:598-633): schema-checked parse, then
+    ModelConfig::validate through the native library (DimError -> SchemaError)."""
+    import json
+    try:
+        j = json.loads(text)
+    except ValueError as e:
+        raise SchemaError(f"invalid json: {e}") from None
+    ov = _ObjView(j, "$")
+    cfg = ModelConfig(channels=ov.integer("channels"), views=ov.integer("views"),
+                      pyramid_levels=ov.integer("pyramid_levels"), upsample=ov.num("upsample"),
+                      near=ov.num("near"), far=ov.num("far"),
+                      ablate_render=ov.boolean("ablate_render", False),
+                      ablate_attention=ov.boolean("ablate_attention", False),
+                      ablate_rays=ov.boolean("ablate_rays", False),
+                      direct_rgb=ov.boolean("direct_rgb", False))
+    steps = ov.array("steps", 1)
+    for i, sj in enumerate(steps):
+        sv = _ObjView(sj, f"$.steps[{i}]")
+        cfg.steps.append(StepConfig(sv.integer("in_layers"), sv.integer("layers"),
+                                    sv.integer("height"), sv.integer("width"),
+                                    sv.integer("pyramid_level"), sv.str("blocks")))
+        sv.close()
+    ov.close()
+    from .lvs import validate_config
+    try:
+        validate_config(cfg)
+    except capi.DimError as e:
+        raise SchemaError(f"$: {e}") from None
+    return cfg

@@ -319,3 +319,45 @@ def test_config_variants_match_oracle(oracle, name):
     print(f"{name}: max-abs {err:.3e} psnr {psnr(rgb, want):.1f} dB")
     assert np.isfinite(rgb).all()
     assert err <= RGB_MAX_ABS and psnr(rgb, want) >= RGB_PSNR_DB
+
+
+_VARIANT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + '/tests')
+import paper_2411_16680_b200 as q
+from cases import config2
+c = config2(div=4)
+m = q.Model(c.cfg, device=0)
+m.load_weights(c.store())
+np.save(sys.argv[2], m.forward_render(c.enc_images, c.enc_cams, c.ren_images, c.ren_cams, c.target))
+m.close()
+"""
+
+
+@pytest.mark.parametrize("env", [{"LVSG_GATHER": "tile"}, {"LVSG_GATHER": "tile1"},
+                                 {"LVSG_SPLAT_RED": "3"}, {"LVSG_SPLAT": "atomic"}],
+                         ids=["gather_pipelined", "gather_window", "splat_reduce_3lane",
+                              "splat_atomic"])
+def test_kernel_variants_match_default(tmp_path, env):
+    """The opt-in kernel variants (env-selected, one per process) against the
+    default path on 1/4-scale config 2: the gather windows and the splat
+    reduction layouts are bit-identical by construction; the atomic splat
+    differs only in accumulation order (RGB gate)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for name, extra in (("default", {}), ("variant", env)):
+        path = str(tmp_path / f"{name}.npy")
+        e = dict(os.environ)
+        for k in ("LVSG_GATHER", "LVSG_SPLAT", "LVSG_SPLAT_RED"):
+            e.pop(k, None)
+        e.update(extra)
+        subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root, path], env=e, check=True,
+                       timeout=600)
+        outs[name] = np.load(path)
+    if env.get("LVSG_SPLAT") == "atomic":
+        assert float(np.abs(outs["default"] - outs["variant"]).max()) <= RGB_MAX_ABS
+    else:
+        assert np.array_equal(outs["default"].view(np.uint32), outs["variant"].view(np.uint32))
