@@ -252,7 +252,7 @@ def main():
     ap.add_argument("--config", default="config2", choices=["config2", "config3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--ref-procs", type=int, default=0)
     ap.add_argument("--shard-encoder", action="store_true",
                     help="view-sharded encode + pyramid all-gather even at N=1 (default at N>1)")
@@ -370,21 +370,30 @@ def main():
         ren_h = torch.from_numpy(case.ren_images).pin_memory()
         out_h = torch.empty((Ho, Wo, 3), dtype=torch.float32).pin_memory()
         e_np, r_np, o_np = enc_h.numpy(), ren_h.numpy(), out_h.numpy()
-        cstream = torch.cuda.ExternalStream(model.stream_handle(), device=dev)
+        outs = [o_np, torch.empty_like(out_h).pin_memory().numpy()]
+        pending = []
+        nsub = [0]
+
         def e2e_step():
             if not sharded:
-                model.forward_render(e_np, case.enc_cams, r_np, case.ren_cams, case.target,
-                                     out=o_np)
+                # pipelined host frames (lvsg_submit_frame / lvsg_wait_frame): at
+                # most two in flight, so frame k+1's uploads run under frame k
+                if len(pending) == 2:
+                    model.wait_frame(pending.pop(0))
+                pending.append(model.submit_frame(e_np, case.enc_cams, r_np, case.ren_cams,
+                                                  case.target, outs[nsub[0] % 2]))
+                nsub[0] += 1
                 return
             # this rank's encoder views up and encoded, the shares
-            # all-gathered (all on the context's stream), then the host C ABI
-            # with a NULL encoder list: render views uploaded under the
-            # forward pass, the frame read back in bands
-            with torch.cuda.stream(cstream):
+            # all-gathered (on the frame stream), then the host C ABI with a
+            # NULL encoder list: render views uploaded under the forward pass,
+            # the frame read back in bands
+            with torch.cuda.stream(stream):
                 enc[v0:v1].copy_(enc_h[v0:v1], non_blocking=True)
-                model.encode_device(enc, v0, v1, cstream)
+                model.encode_device(enc, v0, v1, stream)
                 for lv in levels:
                     shard.allgather_views(lv, M)
+            stream.synchronize()
             model.forward_render(None, case.enc_cams, r_np, case.ren_cams, case.target, out=o_np,
                                  enc_hw=(He, We))
 
@@ -392,15 +401,20 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        while pending:
+            model.wait_frame(pending.pop(0))
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             e2e_step()
+        while pending:
+            model.wait_frame(pending.pop(0))
         sec = shard.max_over_ranks(time.perf_counter() - t0, dev)
         h2d = (enc_h[v0:v1].numel() if sharded else enc_h.numel()) * 4 + ren_h.numel() * 4
         e2e = {"value": shard.aggregate_fps(world, args.e2e_steps, sec), "unit": "frames/s",
                "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(out_h.numel() * 4), "steps": args.e2e_steps,
-               "path": ("lvsg_forward_render (host C ABI, pinned buffers)" if not sharded else
+               "path": ("lvsg_submit_frame / lvsg_wait_frame (host C ABI, pinned buffers, "
+                        "two frames in flight)" if not sharded else
                         "pinned host encoder views (own share) -> lvsg_encode_device -> NCCL "
                         "all-gather -> lvsg_forward_render (NULL encoder list; pinned render "
                         "views in, pinned frame out)")}

@@ -158,6 +158,22 @@ lvsg_status lvsg_forward_render(lvsg_ctx* ctx, int64_t views, const float* const
                                 int64_t render_w, const lvsg_camera* render_cams,
                                 const lvsg_frustum* target, float* rgb_out);
 
+/* Pipelined host-buffer frames (video, config 4): lvsg_submit_frame enqueues
+ * the work of lvsg_forward_render and returns at once with a ticket;
+ * lvsg_wait_frame(ticket) blocks until that frame's rgb_out is filled and
+ * reports its errors. Two frames may be in flight (submitting a third waits
+ * for the oldest, and reports its errors; waiting a retired ticket returns
+ * LVSG_OK at once): frame k+1's uploads run under frame k's compute and
+ * frame k's read-back on its own stream. Host buffers must stay valid (and,
+ * for overlap, be pinned) until the frame's wait returns.
+ * lvsg_forward_render == submit + wait. */
+lvsg_status lvsg_submit_frame(lvsg_ctx* ctx, int64_t views, const float* const* enc_images,
+                              int64_t enc_h, int64_t enc_w, const lvsg_camera* enc_cams,
+                              const float* const* render_images, int64_t render_h,
+                              int64_t render_w, const lvsg_camera* render_cams,
+                              const lvsg_frustum* target, float* rgb_out, int64_t* ticket);
+lvsg_status lvsg_wait_frame(lvsg_ctx* ctx, int64_t ticket);
+
 /* Device-resident variant: enc_images [M,He,We,3] and render_images
  * [M,Hr,Wr,3] are contiguous DEVICE buffers, rgb_out a DEVICE buffer
  * [Ho,Wo,3]; work is enqueued on `stream` (cudaStream_t, NULL = the

@@ -139,6 +139,19 @@ struct NetW {
 }  // namespace
 }  // namespace lvsg
 
+namespace lvsg {
+// One in-flight pipelined host frame: its device copies of the inputs and
+// the output, the events that order them, its own depth-range flag.
+struct FrameSlot {
+  Buf enc_in, ren_in, rgb;
+  std::vector<cudaEvent_t> ev_enc;
+  cudaEvent_t ev_ren = nullptr, ev_free = nullptr, ev_done = nullptr;
+  cudaEvent_t ev_band[4] = {};
+  int* bad = nullptr;
+  int64_t ticket = -1;  // frame owning the slot, -1 = free
+};
+}  // namespace lvsg
+
 struct lvsg_ctx {
   lvsg::Config cfg;
   int device = 0;
@@ -171,6 +184,10 @@ struct lvsg_ctx {
   cudaEvent_t ev_main = nullptr, ev_ren = nullptr;
   cudaEvent_t ev_band[4] = {};
   std::vector<cudaEvent_t> ev_enc;  // per-view encoder upload landed
+  // pipelined host frames (lvsg_submit_frame): two slots, a download stream
+  lvsg::FrameSlot slots[2];
+  cudaStream_t down = nullptr;
+  int64_t next_ticket = 0;
 
   // resident forward result (for lvsg_render)
   bool have_ldm = false;
@@ -956,6 +973,20 @@ void sync_and_check(lvsg_ctx* c) {
   }
 }
 
+// Host wait for a pipelined frame: its read-back landed; its depth-range
+// check (the reference's world_points DimError) is reported here.
+void wait_slot(lvsg_ctx* c, FrameSlot& S) {
+  S.ticket = -1;
+  CUDA_OK(cudaEventSynchronize(S.ev_done));
+  int bad = 0;
+  CUDA_OK(cudaMemcpy(&bad, S.bad, sizeof(int), cudaMemcpyDeviceToHost));
+  if (bad) {
+    CUDA_OK(cudaMemset(S.bad, 0, sizeof(int)));
+    throw DimError("world_points: depth outside [near, far]");
+  }
+  (void)c;
+}
+
 void upload_images(lvsg_ctx* c, Buf& dst, int64_t views, const float* const* images, int64_t H,
                    int64_t W, cudaStream_t st) {
   if (!images) throw DimError("forward: null image list");
@@ -1136,6 +1167,15 @@ void lvsg_destroy(lvsg_ctx* c) {
                         c->ev_band[3]})
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_enc) cudaEventDestroy(e);
+  if (c->down) cudaStreamSynchronize(c->down);
+  for (FrameSlot& S : c->slots) {
+    for (cudaEvent_t e : {S.ev_ren, S.ev_free, S.ev_done, S.ev_band[0], S.ev_band[1],
+                          S.ev_band[2], S.ev_band[3]})
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : S.ev_enc) cudaEventDestroy(e);
+    if (S.bad) cudaFree(S.bad);
+  }
+  if (c->down) cudaStreamDestroy(c->down);
   if (c->xfer) cudaStreamDestroy(c->xfer);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -1254,68 +1294,120 @@ lvsg_status lvsg_render(lvsg_ctx* c, int64_t views, const float* const* images, 
   });
 }
 
+// ---- pipelined host-buffer frames (lvsg_submit_frame / lvsg_wait_frame) ----
+//
+// The same work as the synchronous host call, split at the host wait: two
+// frame slots (their own upload / output buffers and events) so frame k+1's
+// uploads run on the copy stream under frame k's compute, and frame k's
+// banded read-back runs on a separate download stream. lvsg_forward_render
+// is submit + wait.
+lvsg_status lvsg_submit_frame(lvsg_ctx* c, int64_t views, const float* const* enc_images,
+                              int64_t enc_h, int64_t enc_w, const lvsg_camera* enc_cams,
+                              const float* const* render_images, int64_t render_h,
+                              int64_t render_w, const lvsg_camera* render_cams,
+                              const lvsg_frustum* target, float* rgb_out, int64_t* ticket) {
+  return guard(c, [&] {
+    check_views(c, views, enc_h, enc_w);
+    check_views(c, views, render_h, render_w);
+    for (int64_t m = 0; m < views; ++m) camera_validate(render_cams[m]);
+    if (!rgb_out) throw DimError("forward: null output");
+    if (enc_images)
+      for (int64_t m = 0; m < views; ++m)
+        if (!enc_images[m]) throw DimError("forward: null image");
+    const int64_t k = c->next_ticket;
+    FrameSlot& S = c->slots[k & 1];
+    if (S.ticket >= 0) wait_slot(c, S);  // frame k-2 still owns the slot's buffers
+    if (!S.ev_ren) {
+      CUDA_OK(cudaEventCreateWithFlags(&S.ev_ren, cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&S.ev_free, cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&S.ev_done, cudaEventDisableTiming));
+      for (cudaEvent_t& e : S.ev_band) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CUDA_OK(cudaMalloc(&S.bad, sizeof(int)));
+      CUDA_OK(cudaMemset(S.bad, 0, sizeof(int)));
+      CUDA_OK(cudaEventRecord(S.ev_free, c->stream));
+    }
+    if (!c->down) CUDA_OK(cudaStreamCreateWithFlags(&c->down, cudaStreamNonBlocking));
+    // uploads (copy stream), once the slot's previous frame stopped reading
+    // its buffers: the encoder views one by one, each with an event the
+    // encoder's per-view level 0 waits on, then the render views, needed
+    // only by the final render, under the rest of the forward pass
+    CUDA_OK(cudaStreamWaitEvent(c->xfer, S.ev_free, 0));
+    const size_t per = size_t(enc_h * enc_w * 3);
+    if (enc_images) {
+      S.enc_in.ensure(per * size_t(views));
+      while (S.ev_enc.size() < size_t(views)) {
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        S.ev_enc.push_back(e);
+      }
+      for (int64_t m = 0; m < views; ++m) {
+        CUDA_OK(cudaMemcpyAsync(S.enc_in.p + per * size_t(m), enc_images[m], per * sizeof(float),
+                                cudaMemcpyHostToDevice, c->xfer));
+        CUDA_OK(cudaEventRecord(S.ev_enc[size_t(m)], c->xfer));
+      }
+    }
+    upload_images(c, S.ren_in, views, render_images, render_h, render_w, c->xfer);
+    CUDA_OK(cudaEventRecord(S.ev_ren, c->xfer));
+    // enc_images == NULL: the resident pyramid (lvsg_encode_device, complete
+    // on the context's stream) is used. With the previous frame still in
+    // flight the uploads finish under its compute, so the encoder runs
+    // batched over the views behind the last upload; otherwise its level 0
+    // runs view by view behind each view's upload.
+    const bool behind = c->slots[(k + 1) & 1].ticket >= 0;
+    if (enc_images && behind)
+      CUDA_OK(cudaStreamWaitEvent(c->stream, S.ev_enc[size_t(views - 1)], 0));
+    CamTables t;
+    forward_device(c, enc_images ? S.enc_in.p : nullptr, enc_h, enc_w, enc_cams, *target,
+                   render_cams, &t, enc_images && !behind ? S.ev_enc.data() : nullptr);
+    const int64_t Ho = c->plan.out_height, Wo = c->plan.out_width;
+    S.rgb.ensure(size_t(Ho * Wo * 3));
+    CUDA_OK(cudaStreamWaitEvent(c->stream, S.ev_ren, 0));
+    // banded render; each band's read-back (download stream) overlaps the
+    // next band's render
+    constexpr int NB = 4;
+    for (int b = 0; b < NB; ++b) {
+      const int64_t r0 = Ho * b / NB, r1 = Ho * (b + 1) / NB;
+      if (r1 == r0) continue;
+      RenderArgs a = render_args(c, S.ren_in.p, render_h, render_w, t.final_cams,
+                                 S.rgb.p + r0 * Wo * 3, r0, r1, render_cams);
+      a.bad_depth = S.bad;
+      render_fused(a, c->stream);
+      c->launches += 1;
+      CUDA_OK(cudaEventRecord(S.ev_band[b], c->stream));
+      CUDA_OK(cudaStreamWaitEvent(c->down, S.ev_band[b], 0));
+      CUDA_OK(cudaMemcpyAsync(rgb_out + r0 * Wo * 3, S.rgb.p + r0 * Wo * 3,
+                              size_t((r1 - r0) * Wo * 3) * sizeof(float), cudaMemcpyDeviceToHost,
+                              c->down));
+    }
+    mark(c, "render", NB);
+    CUDA_OK(cudaEventRecord(S.ev_free, c->stream));
+    CUDA_OK(cudaEventRecord(S.ev_done, c->down));
+    CUDA_OK(cudaGetLastError());
+    S.ticket = k;
+    c->next_ticket = k + 1;
+    if (ticket) *ticket = k;
+  });
+}
+
+lvsg_status lvsg_wait_frame(lvsg_ctx* c, int64_t ticket) {
+  return guard(c, [&] {
+    if (ticket < 0 || ticket >= c->next_ticket) throw DimError("wait_frame: no such frame");
+    FrameSlot& S = c->slots[ticket & 1];
+    if (S.ticket == ticket) wait_slot(c, S);  // else already retired (waited, or by a later submit)
+  });
+}
+
 lvsg_status lvsg_forward_render(lvsg_ctx* c, int64_t views, const float* const* enc_images,
                                 int64_t enc_h, int64_t enc_w, const lvsg_camera* enc_cams,
                                 const float* const* render_images, int64_t render_h,
                                 int64_t render_w, const lvsg_camera* render_cams,
                                 const lvsg_frustum* target, float* rgb_out) {
-  return guard(c, [&] {
-    check_views(c, views, enc_h, enc_w);
-    check_views(c, views, render_h, render_w);
-    for (int64_t m = 0; m < views; ++m) camera_validate(render_cams[m]);
-    // All uploads go on the copy stream (after any earlier use of the input
-    // buffers): the encoder views one by one, each with an event the encoder's
-    // per-view level 0 waits on, then the render views, needed only by the
-    // final render, under the rest of the forward pass.
-    // enc_images == NULL: no encoder upload, the resident pyramid
-    // (lvsg_encode_device, completed on this context's stream) is used, and
-    // the render views go up at once, under the encode still in flight on
-    // the stream (ren_in is only read by calls that synchronise before they
-    // return, so no earlier work can still be reading it).
-    const size_t per = size_t(enc_h * enc_w * 3);
-    if (enc_images) {
-      CUDA_OK(cudaEventRecord(c->ev_main, c->stream));
-      CUDA_OK(cudaStreamWaitEvent(c->xfer, c->ev_main, 0));
-      for (int64_t m = 0; m < views; ++m)
-        if (!enc_images[m]) throw DimError("forward: null image");
-      c->enc_in.ensure(per * size_t(views));
-      while (c->ev_enc.size() < size_t(views)) {
-        cudaEvent_t e;
-        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        c->ev_enc.push_back(e);
-      }
-      for (int64_t m = 0; m < views; ++m) {
-        CUDA_OK(cudaMemcpyAsync(c->enc_in.p + per * size_t(m), enc_images[m], per * sizeof(float),
-                                cudaMemcpyHostToDevice, c->xfer));
-        CUDA_OK(cudaEventRecord(c->ev_enc[size_t(m)], c->xfer));
-      }
-    }
-    upload_images(c, c->ren_in, views, render_images, render_h, render_w, c->xfer);
-    CUDA_OK(cudaEventRecord(c->ev_ren, c->xfer));
-    CamTables t;
-    forward_device(c, enc_images ? c->enc_in.p : nullptr, enc_h, enc_w, enc_cams, *target,
-                   render_cams, &t, enc_images ? c->ev_enc.data() : nullptr);
-    const int64_t Ho = c->plan.out_height, Wo = c->plan.out_width;
-    c->rgb.ensure(size_t(Ho * Wo * 3));
-    CUDA_OK(cudaStreamWaitEvent(c->stream, c->ev_ren, 0));
-    // banded render; each band's read-back overlaps the next band's render
-    constexpr int NB = 4;
-    for (int k = 0; k < NB; ++k) {
-      const int64_t r0 = Ho * k / NB, r1 = Ho * (k + 1) / NB;
-      if (r1 == r0) continue;
-      render_fused(render_args(c, c->ren_in.p, render_h, render_w, t.final_cams, c->rgb.p + r0 * Wo * 3,
-                               r0, r1, render_cams),
-                   c->stream);
-      c->launches += 1;
-      CUDA_OK(cudaEventRecord(c->ev_band[k], c->stream));
-      CUDA_OK(cudaStreamWaitEvent(c->xfer, c->ev_band[k], 0));
-      CUDA_OK(cudaMemcpyAsync(rgb_out + r0 * Wo * 3, c->rgb.p + r0 * Wo * 3,
-                              size_t((r1 - r0) * Wo * 3) * sizeof(float), cudaMemcpyDeviceToHost,
-                              c->xfer));
-    }
-    mark(c, "render", NB);
-    sync_and_check(c);
-  });
+  int64_t ticket = -1;
+  const lvsg_status s = lvsg_submit_frame(c, views, enc_images, enc_h, enc_w, enc_cams,
+                                          render_images, render_h, render_w, render_cams, target,
+                                          rgb_out, &ticket);
+  if (s != LVSG_OK) return s;
+  return lvsg_wait_frame(c, ticket);
 }
 
 lvsg_status lvsg_forward_render_device(lvsg_ctx* c, int64_t views, const float* enc_images,

@@ -293,6 +293,30 @@ class Model:
                                                   rgb.ctypes.data_as(capi.c_f32p)))
         return rgb
 
+    def submit_frame(self, enc_images, enc_cams, render_images, render_cams, target: Frustum,
+                     out: np.ndarray) -> int:
+        """lvsg_submit_frame: enqueue one host-buffer frame (pinned arrays
+        for overlap) and return its ticket; `out` [Ho,Wo,3] is filled by
+        wait_frame(ticket). The arrays must stay alive until then."""
+        ea, ek, He, We = _img_ptrs(enc_images)
+        ra, rk, Hr, Wr = _img_ptrs(render_images)
+        assert out.dtype == np.float32 and out.flags.c_contiguous
+        fr = target.to_c()
+        t = ctypes.c_int64(-1)
+        self._check(self._lib.lvsg_submit_frame(self._h, len(ek), ea, He, We, _cam_array(enc_cams),
+                                                ra, Hr, Wr, _cam_array(render_cams),
+                                                ctypes.byref(fr), out.ctypes.data_as(capi.c_f32p),
+                                                ctypes.byref(t)))
+        self._inflight = getattr(self, "_inflight", {})
+        self._inflight[t.value] = (ea, ek, ra, rk, out)  # keep the host views alive
+        return t.value
+
+    def wait_frame(self, ticket: int) -> None:
+        try:
+            self._check(self._lib.lvsg_wait_frame(self._h, int(ticket)))
+        finally:
+            getattr(self, "_inflight", {}).pop(int(ticket), None)
+
     def forward_render_device(self, enc_images, enc_cams, render_images, render_cams,
                               target: Frustum, rgb_out, stream=None, enc_hw=None) -> None:
         """Device-resident path on torch CUDA tensors (enc [M,He,We,3],

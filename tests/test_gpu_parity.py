@@ -361,3 +361,29 @@ def test_kernel_variants_match_default(tmp_path, env):
         assert float(np.abs(outs["default"] - outs["variant"]).max()) <= RGB_MAX_ABS
     else:
         assert np.array_equal(outs["default"].view(np.uint32), outs["variant"].view(np.uint32))
+
+
+def test_pipelined_frames_match_synchronous():
+    """lvsg_submit_frame / lvsg_wait_frame: two frames in flight (different
+    targets, then a repeat) give exactly the synchronous frames."""
+    import torch
+    from paper_2411_16680_b200 import workloads as wl
+    grid = wl.config5_targets()
+    cases = [wl.config2(div=4, target_center=grid[i]) for i in (1, 6, 1)]
+    m = q.Model(cases[0].cfg, device=0)
+    m.init_weights(cases[0].seed)
+    want = [m.forward_render(c.enc_images, c.enc_cams, c.ren_images, c.ren_cams, c.target)
+            for c in cases]
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    enc, ren = pin(cases[0].enc_images), pin(cases[0].ren_images)
+    outs = [pin(np.zeros_like(w)) for w in want]
+    tickets = []
+    for c, o in zip(cases, outs):
+        tickets.append(m.submit_frame(enc, c.enc_cams, ren, c.ren_cams, c.target, o))
+    for t in tickets:
+        m.wait_frame(t)
+    for o, w in zip(outs, want):
+        assert np.array_equal(o.view(np.uint32), w.view(np.uint32))
+    m.wait_frame(tickets[0])  # retired: returns at once
+    with pytest.raises(q.DimError):
+        m.wait_frame(tickets[-1] + 1)  # never submitted
