@@ -397,15 +397,18 @@ def main():
             model.forward_render(None, case.enc_cams, r_np, case.ren_cams, case.target, out=o_np,
                                  enc_hw=(He, We))
 
-        e2e_step()
+        for _ in range(3):  # warm-up: both frame slots allocate their buffers
+            e2e_step()
+        while pending:
+            model.wait_frame(pending.pop(0))
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        while pending:
-            model.wait_frame(pending.pop(0))
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             e2e_step()
+            if os.environ.get("LVSG_BENCH_DEBUG"):
+                print(f"e2e step {time.perf_counter() - t0:.4f}", file=sys.stderr)
         while pending:
             model.wait_frame(pending.pop(0))
         sec = shard.max_over_ranks(time.perf_counter() - t0, dev)

@@ -303,6 +303,18 @@ __global__ void __launch_bounds__(128) conv3x3_stem3x2_kernel(const ConvArgs a,
     }
   }
   __syncthreads();
+  if (a.out_bstride == HW * 32 && !a.resid) {
+    // contiguous [B*H*W, 32] output (the encoder stem): the block's 256
+    // pixels are one linear 32 KB run
+    float4* dst = reinterpret_cast<float4*>(a.out) + i0 * 8;
+    const int np = n - i0 < 256 ? int(n - i0) : 256;
+#pragma unroll 4
+    for (int k = 0; k < 16; ++k) {
+      const int j = t + 128 * k, pl = j >> 3, c4 = j & 7;
+      if (pl < np) dst[j] = s_o[pl * 8 + (c4 ^ (pl & 7))];
+    }
+    return;
+  }
   // coalesced write-back (+ residual): 8 threads per pixel's 128 bytes
 #pragma unroll 4
   for (int k = 0; k < 16; ++k) {
