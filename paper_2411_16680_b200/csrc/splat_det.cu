@@ -445,6 +445,102 @@ __global__ void __launch_bounds__(320, 2) splat_reduce_px3_kernel(
   }
 }
 
+// One thread per (view m, pixel, layer): the run of a layer's bin is summed
+// in parallel across layers (the early steps have 24 layers over small view
+// images, where a thread per pixel walking the layers in sequence left the
+// SMs nearly empty); the normalised values go through shared memory and
+// the back-to-front composite then runs per (pixel, channel group) in the
+// reference's layer order. Same additions, same order, as
+// splat_reduce_px_kernel.
+template <int NG>
+__global__ void __launch_bounds__(192) splat_reduce_pl_kernel(
+    const float* __restrict__ payload, int K, int M, int L, int Hv, int Wv,
+    const int* __restrict__ off, const int* __restrict__ cnt, const int2* __restrict__ ent,
+    float* __restrict__ out, int ppb) {
+  pdl_grid_sync();
+  extern __shared__ float s_val[];  // [ppb][L][NG*4]: normalised channels, [Ca] = alpha
+  const int64_t PV = (int64_t)Hv * Wv;
+  const int Ca = K - 1;
+  const float4* pay4 = reinterpret_cast<const float4*>(payload);
+  const int64_t t0 = (int64_t)blockIdx.x * ppb;  // first (m, pixel) of the block
+  const int lp = threadIdx.x / L, l = threadIdx.x - lp * L;
+  const int64_t t = t0 + lp;
+  if (lp < ppb && t < (int64_t)M * PV) {
+    const int64_t pix = t % PV;
+    const int m = int(t / PV);
+    float acc[NG * 4];
+#pragma unroll
+    for (int c = 0; c < NG * 4; ++c) acc[c] = 0.f;
+    float ws = 0.f;
+    auto add = [&](const int2 en) {
+      const float w = __int_as_float(en.y);
+      const float4* row = pay4 + (int64_t)(en.x >> 2) * NG;
+      float4 v[NG];
+#pragma unroll
+      for (int q = 0; q < NG; ++q) v[q] = __ldg(row + q);
+#pragma unroll
+      for (int q = 0; q < NG; ++q) {
+        acc[4 * q] = fa(acc[4 * q], fm(w, v[q].x));
+        acc[4 * q + 1] = fa(acc[4 * q + 1], fm(w, v[q].y));
+        acc[4 * q + 2] = fa(acc[4 * q + 2], fm(w, v[q].z));
+        acc[4 * q + 3] = fa(acc[4 * q + 3], fm(w, v[q].w));
+      }
+      ws = fa(ws, w);
+    };
+    const int64_t bin = ((int64_t)m * L + l) * PV + pix;
+    const int n = __ldg(cnt + bin), b0 = __ldg(off + bin);
+    if (n <= 4) {
+      int2 e[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) e[k] = k < n ? __ldg(ent + b0 + k) : make_int2(0x7fffffff, 0);
+      sort4(e);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k < n) add(e[k]);
+    } else {
+      int last = -1;  // ascending keys by repeated minimum search
+      for (int r = 0; r < n; ++r) {
+        int2 best = make_int2(0x7fffffff, 0);
+        for (int j = 0; j < n; ++j) {
+          const int2 ej = __ldg(ent + b0 + j);
+          if (ej.x > last && ej.x < best.x) best = ej;
+        }
+        last = best.x;
+        add(best);
+      }
+    }
+    // splat_project: * 1/max(wsum, eps)
+    const float nrm = __fdiv_rn(1.0f, ws > 1e-4f ? ws : 1e-4f);
+    float4* dst = reinterpret_cast<float4*>(s_val + ((int64_t)lp * L + l) * NG * 4);
+#pragma unroll
+    for (int q = 0; q < NG; ++q)
+      dst[q] = make_float4(fm(acc[4 * q], nrm), fm(acc[4 * q + 1], nrm), fm(acc[4 * q + 2], nrm),
+                           fm(acc[4 * q + 3], nrm));
+  }
+  __syncthreads();
+  // over_composite colour / alpha, layer 0 (far) first
+  for (int u = threadIdx.x; u < ppb * NG; u += blockDim.x) {
+    const int p = u / NG, g = u - p * NG;
+    const int64_t tt = t0 + p;
+    if (tt >= (int64_t)M * PV) break;
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int ll = 0; ll < L; ++ll) {
+      const float* vv = s_val + ((int64_t)p * L + ll) * NG * 4;
+      const float s = vv[Ca];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = 4 * g + k;
+        const float v = c < Ca ? vv[c] : 1.0f;
+        o[k] = fa(fm(v, s), fm(fsb(1.0f, s), o[k]));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (4 * g + k >= K) o[k] = 0.f;
+    reinterpret_cast<float4*>(out)[tt * NG + g] = make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 inline int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
 
 }  // namespace
@@ -482,11 +578,25 @@ void splat_det(const float* payload, const float* points, int L, int PL, int K,
            (const float4*)fp_w, cursor, ent);
   const int G = pay_stride(K) / 4;
   if (G == 9) {
-    static const int variant = [] {  // LVSG_SPLAT_RED=3: three lanes per pixel (A/B runs;
-      const char* e = getenv("LVSG_SPLAT_RED");  // measured slower, 1.00 vs 0.85 ms a frame)
-      return e ? atoi(e) : 1;
+    // LVSG_SPLAT_RED (A/B runs): 1 = one thread per pixel walking the layers,
+    // 3 = three lanes per pixel; default: one thread per (pixel, layer)
+    static const int variant = [] {
+      const char* e = getenv("LVSG_SPLAT_RED");
+      return e ? atoi(e) : 0;
     }();
-    if (variant != 3)
+    if (variant == 0 && L <= 192) {
+      const int ppb = std::max(1, 192 / L);
+      const size_t smem = size_t(ppb) * L * 36 * sizeof(float);
+      static bool attr = [] {
+        cudaFuncSetAttribute(splat_reduce_pl_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             192 * 36 * 4);
+        return true;
+      }();
+      (void)attr;
+      launch_k(splat_reduce_pl_kernel<9>, blocks_for((int64_t)M * Hv * Wv, ppb), ppb * L, smem, st,
+               payload, K, M, L, Hv, Wv, (const int*)off, (const int*)cnt, (const int2*)ent, out,
+               ppb);
+    } else if (variant != 3)
       launch_k(splat_reduce_px_kernel<9>, blocks_for((int64_t)M * Hv * Wv, 128), 128, 0, st, payload,
                K, M, L, Hv, Wv, (const int*)off, (const int*)cnt, (const int2*)ent, out);
     else

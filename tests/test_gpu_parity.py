@@ -335,9 +335,10 @@ m.close()
 
 
 @pytest.mark.parametrize("env", [{"LVSG_GATHER": "tile"}, {"LVSG_GATHER": "tile1"},
-                                 {"LVSG_SPLAT_RED": "3"}, {"LVSG_SPLAT": "atomic"}],
-                         ids=["gather_pipelined", "gather_window", "splat_reduce_3lane",
-                              "splat_atomic"])
+                                 {"LVSG_SPLAT_RED": "1"}, {"LVSG_SPLAT_RED": "3"},
+                                 {"LVSG_SPLAT": "atomic"}],
+                         ids=["gather_pipelined", "gather_window", "splat_reduce_pixel",
+                              "splat_reduce_3lane", "splat_atomic"])
 def test_kernel_variants_match_default(tmp_path, env):
     """The opt-in kernel variants (env-selected, one per process) against the
     default path on 1/4-scale config 2: the gather windows and the splat
