@@ -152,48 +152,37 @@ __global__ void resize_hwc4_kernel(const float* __restrict__ in, float* __restri
   }
 }
 
-// resize_hwc for C % 4 == 0, cooperative: a block covers 256 / G consecutive
-// output pixels with one thread per (pixel, channel group g), g fastest, so
-// every tap read and every store is a contiguous run; the f64 taps of each
-// pixel are computed once and shared through shared memory.
+// resize_hwc for C % 4 == 0, cooperative: one thread per (output pixel,
+// channel group g), g fastest, so every tap read and every store is a
+// contiguous run; a grid-stride loop keeps each block busy across many
+// pixels (the one-pass version's blocks wrote 4 KB each and left the
+// kernel at ~40% of HBM bandwidth).
 __global__ void __launch_bounds__(256) resize_hwc4c_kernel(const float* __restrict__ in,
                                                            float* __restrict__ out, int B, int H,
                                                            int W, int G, int Ho, int Wo) {
   pdl_grid_sync();
-  __shared__ int s_tap[64][4];
-  __shared__ float s_fr[64][2];
-  const int PB = 256 / G;
-  const int64_t n = (int64_t)B * Ho * Wo;
-  const int64_t i0 = blockIdx.x * (int64_t)PB;
-  const int t = threadIdx.x;
-  if (t < PB && i0 + t < n) {
-    const int64_t i = i0 + t;
-    const int x = int(i % Wo), y = int((i / Wo) % Ho);
-    const int b = int(i / ((int64_t)Wo * Ho));
+  // grid-stride over (output pixel, channel group), g fastest; each thread
+  // derives its pixel's taps itself (32-bit index math: the caller checks
+  // the element counts)
+  const int total = B * Ho * Wo * G;
+  const float4* s4 = reinterpret_cast<const float4*>(in);
+  float4* o4 = reinterpret_cast<float4*>(out);
+  for (int e = blockIdx.x * 256 + threadIdx.x; e < total; e += gridDim.x * 256) {
+    const int i = e / G, g = e - i * G;
+    const int q = i / Wo, x = i - q * Wo;
+    const int b = q / Ho, y = q - b * Ho;
     int y0, y1, x0, x1;
     float fy, fx;
     resize_tap(y, H, Ho, y0, y1, fy);
     resize_tap(x, W, Wo, x0, x1, fx);
-    const int base = b * H;
-    s_tap[t][0] = (base + y0) * W + x0;
-    s_tap[t][1] = (base + y0) * W + x1;
-    s_tap[t][2] = (base + y1) * W + x0;
-    s_tap[t][3] = (base + y1) * W + x1;
-    s_fr[t][0] = fx;
-    s_fr[t][1] = fy;
+    const int r0 = (b * H + y0) * W, r1 = (b * H + y1) * W;
+    const float4 A = __ldg(s4 + (r0 + x0) * G + g);
+    const float4 Bv = __ldg(s4 + (r0 + x1) * G + g);
+    const float4 Cv = __ldg(s4 + (r1 + x0) * G + g);
+    const float4 D = __ldg(s4 + (r1 + x1) * G + g);
+    o4[e] = make_float4(lerp2(A.x, Bv.x, Cv.x, D.x, fx, fy), lerp2(A.y, Bv.y, Cv.y, D.y, fx, fy),
+                        lerp2(A.z, Bv.z, Cv.z, D.z, fx, fy), lerp2(A.w, Bv.w, Cv.w, D.w, fx, fy));
   }
-  __syncthreads();
-  const int pl = t / G, g = t - pl * G;
-  if (pl >= PB || i0 + pl >= n) return;
-  const float4* s4 = reinterpret_cast<const float4*>(in);
-  const float4 A = __ldg(s4 + (int64_t)s_tap[pl][0] * G + g);
-  const float4 Bv = __ldg(s4 + (int64_t)s_tap[pl][1] * G + g);
-  const float4 Cv = __ldg(s4 + (int64_t)s_tap[pl][2] * G + g);
-  const float4 D = __ldg(s4 + (int64_t)s_tap[pl][3] * G + g);
-  const float fx = s_fr[pl][0], fy = s_fr[pl][1];
-  reinterpret_cast<float4*>(out)[(i0 + pl) * G + g] =
-      make_float4(lerp2(A.x, Bv.x, Cv.x, D.x, fx, fy), lerp2(A.y, Bv.y, Cv.y, D.y, fx, fy),
-                  lerp2(A.z, Bv.z, Cv.z, D.z, fx, fy), lerp2(A.w, Bv.w, Cv.w, D.w, fx, fy));
 }
 
 // One warp per row: rinv = 1 / sqrt(sum(x^2)/C + 1e-6).
@@ -310,28 +299,40 @@ __global__ void ray_project_kernel(const float* base, int M, int hK, int wK, int
 
 // C = 32 production path: float4 tap reads, the block's 128 output rows
 // staged in shared memory and written back as contiguous float4 runs.
+// ray_proj weights [32][32] by value (parameter space): every FMA takes its
+// weight as a constant-bank / uniform-register operand (the shared-memory
+// version spent a broadcast float4 load per four FMAs).
+struct RayProjParam {
+  float w[32 * 32];
+};
+
+// rays_k = resize(base) @ ray_proj for C = 32: thread per output pixel,
+// 32-bit index math; PW: weights from `pw`, else staged in shared memory.
+template <bool PW>
 __global__ void __launch_bounds__(128) ray_project32_kernel(const float* __restrict__ base, int M,
                                                             int hK, int wK, int Hk, int Wk,
                                                             const float* __restrict__ proj,
-                                                            float* __restrict__ out) {
+                                                            float* __restrict__ out,
+                                                            const __grid_constant__ RayProjParam pw) {
   pdl_grid_sync();
-  __shared__ __align__(16) float s_proj[32 * 32];
+  __shared__ __align__(16) float s_proj[PW ? 4 : 32 * 32];
   __shared__ __align__(16) float4 s_o[128 * 8];  // [row][c4 ^ (row & 7)]
-  for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) s_proj[e] = __ldg(proj + e);
-  __syncthreads();
+  if (!PW) {
+    for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) s_proj[e] = __ldg(proj + e);
+    __syncthreads();
+  }
   const int t = threadIdx.x;
-  const int64_t n = (int64_t)M * Hk * Wk;
-  const int64_t i0 = blockIdx.x * (int64_t)128, i = i0 + t;
+  const int n = M * Hk * Wk;  // < 2^31 (checked by the caller)
+  const int i0 = blockIdx.x * 128, i = i0 + t;
   if (i < n) {
-    const int x = int(i % Wk);
-    const int y = int((i / Wk) % Hk);
-    const int m = int(i / ((int64_t)Wk * Hk));
+    const int q = i / Wk, x = i - q * Wk;
+    const int m = q / Hk, y = q - m * Hk;
     const float4* b = reinterpret_cast<const float4*>(base + (int64_t)m * hK * wK * 32);
     float f[32];
     if (Hk == hK && Wk == wK) {
 #pragma unroll
       for (int g = 0; g < 8; ++g) {
-        const float4 v = __ldg(b + ((int64_t)y * wK + x) * 8 + g);
+        const float4 v = __ldg(b + (y * wK + x) * 8 + g);
         f[4 * g] = v.x, f[4 * g + 1] = v.y, f[4 * g + 2] = v.z, f[4 * g + 3] = v.w;
       }
     } else {
@@ -341,10 +342,10 @@ __global__ void __launch_bounds__(128) ray_project32_kernel(const float* __restr
       resize_tap(x, wK, Wk, x0, x1, fx);
 #pragma unroll
       for (int g = 0; g < 8; ++g) {
-        const float4 A = __ldg(b + ((int64_t)y0 * wK + x0) * 8 + g);
-        const float4 B = __ldg(b + ((int64_t)y0 * wK + x1) * 8 + g);
-        const float4 Cc = __ldg(b + ((int64_t)y1 * wK + x0) * 8 + g);
-        const float4 D = __ldg(b + ((int64_t)y1 * wK + x1) * 8 + g);
+        const float4 A = __ldg(b + (y0 * wK + x0) * 8 + g);
+        const float4 B = __ldg(b + (y0 * wK + x1) * 8 + g);
+        const float4 Cc = __ldg(b + (y1 * wK + x0) * 8 + g);
+        const float4 D = __ldg(b + (y1 * wK + x1) * 8 + g);
         f[4 * g] = lerp2(A.x, B.x, Cc.x, D.x, fx, fy);
         f[4 * g + 1] = lerp2(A.y, B.y, Cc.y, D.y, fx, fy);
         f[4 * g + 2] = lerp2(A.z, B.z, Cc.z, D.z, fx, fy);
@@ -358,7 +359,9 @@ __global__ void __launch_bounds__(128) ray_project32_kernel(const float* __restr
     for (int k = 0; k < 32; ++k) {
 #pragma unroll
       for (int c4 = 0; c4 < 8; ++c4) {
-        const float4 w = reinterpret_cast<const float4*>(s_proj + k * 32)[c4];
+        const float4 w = PW ? make_float4(pw.w[k * 32 + 4 * c4], pw.w[k * 32 + 4 * c4 + 1],
+                                          pw.w[k * 32 + 4 * c4 + 2], pw.w[k * 32 + 4 * c4 + 3])
+                            : reinterpret_cast<const float4*>(s_proj + k * 32)[c4];
         acc[4 * c4] = fmaf(f[k], w.x, acc[4 * c4]);
         acc[4 * c4 + 1] = fmaf(f[k], w.y, acc[4 * c4 + 1]);
         acc[4 * c4 + 2] = fmaf(f[k], w.z, acc[4 * c4 + 2]);
@@ -371,7 +374,7 @@ __global__ void __launch_bounds__(128) ray_project32_kernel(const float* __restr
           make_float4(acc[4 * c4], acc[4 * c4 + 1], acc[4 * c4 + 2], acc[4 * c4 + 3]);
   }
   __syncthreads();
-  float4* o = reinterpret_cast<float4*>(out) + i0 * 8;
+  float4* o = reinterpret_cast<float4*>(out) + (int64_t)i0 * 8;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const int j = t + 128 * k, r = j >> 3, c4 = j & 7;
@@ -1108,9 +1111,11 @@ void resize_hwc(const float* in, float* out, int B, int H, int W, int C, int Ho,
   if (C % 4 == 0 && al) {
     const int64_t px = (int64_t)B * Ho * Wo;
     const int G = C / 4;
-    if (G >= 4 && G <= 64 && (int64_t)B * H * W * G < (int64_t(1) << 31)) {
-      const int PB = 256 / G;
-      launch_k(resize_hwc4c_kernel, int((px + PB - 1) / PB), 256, 0, st, in, out, B, H, W, G, Ho, Wo);
+    if (G >= 4 && G <= 64 && (int64_t)B * H * W * G < (int64_t(1) << 31) &&
+        px * G < (int64_t(1) << 31)) {
+      const int64_t blocks = (px * G + 255) / 256;
+      launch_k(resize_hwc4c_kernel, int(std::min<int64_t>(blocks, 148 * 16)), 256, 0, st, in, out, B,
+               H, W, G, Ho, Wo);
     } else {
       launch_k(resize_hwc4_kernel, blocks_for(px, 128), 128, 0, st, in, out, B, H, W, C, Ho, Wo);
     }
@@ -1126,10 +1131,18 @@ void ray_base(const RayBaseCam* cams_dev, const RayBaseArgs& a, float* base, cud
   launch_k(ray_base_kernel, blocks_for(n, 128), 128, 0, st, cams_dev, a, base);
 }
 void ray_project(const float* base, int M, int hK, int wK, int Hk, int Wk, const float* proj,
-                 int C, float* out, cudaStream_t st) {
+                 int C, float* out, cudaStream_t st, const float* proj_host) {
   const int64_t n = (int64_t)M * Hk * Wk;
-  if (C == 32) {
-    launch_k(ray_project32_kernel, blocks_for(n, 128), 128, 0, st, base, M, hK, wK, Hk, Wk, proj, out);
+  if (C == 32 && n < (int64_t(1) << 31) && (int64_t)M * hK * wK * 32 < (int64_t(1) << 31)) {
+    RayProjParam pw;
+    if (proj_host) {
+      for (int e = 0; e < 32 * 32; ++e) pw.w[e] = proj_host[e];
+      launch_k(ray_project32_kernel<true>, blocks_for(n, 128), 128, 0, st, base, M, hK, wK, Hk, Wk,
+               proj, out, pw);
+    } else {
+      launch_k(ray_project32_kernel<false>, blocks_for(n, 128), 128, 0, st, base, M, hK, wK, Hk, Wk,
+               proj, out, pw);
+    }
     return;
   }
   launch_k(ray_project_kernel, blocks_for(n, 128), 128, 32 * C * sizeof(float), st, base, M, hK, wK, Hk,

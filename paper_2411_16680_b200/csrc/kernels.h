@@ -152,8 +152,10 @@ struct RayBaseArgs {
 };
 void ray_base(const RayBaseCam* cams_dev, const RayBaseArgs& a, float* base, cudaStream_t st);
 // rays_k = resize(base -> Hk,Wk) @ ray_proj [32,C]
+// proj_host (optional): host copy of proj ([32, C], C = 32) for the
+// parameter-space kernel.
 void ray_project(const float* base, int M, int hK, int wK, int Hk, int Wk, const float* proj,
-                 int C, float* out, cudaStream_t st);
+                 int C, float* out, cudaStream_t st, const float* proj_host = nullptr);
 
 // ---- geometry --------------------------------------------------------------
 // Δ[p, m, :] = gather of feats[m] ([M, Hf, Wf, C]) at world_point(p) through

@@ -209,6 +209,7 @@ struct lvsg_ctx {
   std::map<std::tuple<const float*, int, int>, std::unique_ptr<lvsg::Buf>> wimg;
   lvsg::Buf wimg_tmp;  // uncached image for the stage entry points
   std::vector<float> stem_host;  // encoder stem weights [32*27] + bias [32] (host copy)
+  std::vector<std::vector<float>> rayproj_host;  // per-level ray_proj [32, C] (host copies)
   int64_t pyr_He = -1, pyr_We = -1;  // encoder resolution of the resident feature pyramid
 };
 
@@ -250,6 +251,7 @@ void prof_collect(lvsg_ctx* c) {
 
 void bind_weights(lvsg_ctx* c) {
   c->wimg.clear();
+  c->rayproj_host.clear();
   const Config& cfg = c->cfg;
   const int64_t C = cfg.channels, Ca = cfg.appear_channels();
   const float* cur = c->weights.p;
@@ -279,6 +281,9 @@ void bind_weights(lvsg_ctx* c) {
     W.lvl_r1.push_back(pair());
     W.lvl_r2.push_back(pair());
     W.ray_proj.push_back(take(32 * C));
+    c->rayproj_host.emplace_back(size_t(32 * C));
+    CUDA_OK(cudaMemcpy(c->rayproj_host.back().data(), W.ray_proj.back(), size_t(32 * C) * sizeof(float),
+                       cudaMemcpyDeviceToHost));
   }
   W.w_sigma = take(C);
   W.w_depth = take(C);
@@ -763,7 +768,8 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
       for (int k = 0; k < K; ++k) {
         ray_project(c->ray_base.p, M, hK, wK, int(plan.pyramid[size_t(k)].first),
                     int(plan.pyramid[size_t(k)].second), W.ray_proj[size_t(k)], C,
-                    c->rays[size_t(k)].p, st);
+                    c->rays[size_t(k)].p, st,
+                    k < int(c->rayproj_host.size()) ? c->rayproj_host[size_t(k)].data() : nullptr);
         mark(c, "misc", 1);
       }
     }
