@@ -256,6 +256,10 @@ def main():
     ap.add_argument("--ref-procs", type=int, default=0)
     ap.add_argument("--shard-encoder", action="store_true",
                     help="view-sharded encode + pyramid all-gather even at N=1 (default at N>1)")
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
+                    help="N>1 pyramid exchange: stores fused into the encoder epilogue over "
+                         "CUDA IPC (falls back to nccl if any rank cannot map its peers) or "
+                         "an NCCL all-gather per level")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)
@@ -303,14 +307,45 @@ def main():
     v0, v1 = shard.view_range(rank, world, M)
     levels = []
 
+    # N > 1 exchange: fused into the encoder (each rank's pooled levels stored
+    # straight into every peer's pyramid over NVLink, then a one-element NCCL
+    # all-reduce as the stream-ordered barrier) or an NCCL all-gather
+    exchange = "nccl"
+    barrier_t = None
+    if world > 1 and args.exchange == "fused":
+        ok = 1
+        try:
+            mine = model.pyramid_export((He, We))
+            handles = [None] * world
+            dist.all_gather_object(handles, mine)
+            model.pyramid_import([h for r, h in enumerate(handles) if r != rank])
+        except Exception as e:  # reported; every rank then uses the all-gather
+            print(f"rank {rank}: fused pyramid exchange unavailable ({e})", file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 1:
+            exchange = "fused"
+            barrier_t = torch.zeros(1, dtype=torch.int32, device=dev)
+        else:
+            model.pyramid_import([])
+
+    def exchange_levels():
+        if exchange == "fused":
+            dist.all_reduce(barrier_t)  # every rank's encoder (and its peer stores) done
+        else:
+            for lv in levels:
+                shard.allgather_views(lv, M)
+
     def step():
         if not sharded:
             model.forward_render_device(enc, case.enc_cams, ren, case.ren_cams, case.target, rgb,
                                         stream)
             return
+        if exchange == "fused":
+            dist.all_reduce(barrier_t)  # no rank still reads the pyramid the encode overwrites
         model.encode_device(enc, v0, v1, stream)
-        for lv in levels:
-            shard.allgather_views(lv, M)
+        exchange_levels()
         model.forward_render_device(None, case.enc_cams, ren, case.ren_cams, case.target, rgb,
                                     stream, enc_hw=(He, We))
 
@@ -390,9 +425,10 @@ def main():
             # the frame read back in bands
             with torch.cuda.stream(stream):
                 enc[v0:v1].copy_(enc_h[v0:v1], non_blocking=True)
+                if exchange == "fused":
+                    dist.all_reduce(barrier_t)
                 model.encode_device(enc, v0, v1, stream)
-                for lv in levels:
-                    shard.allgather_views(lv, M)
+                exchange_levels()
             stream.synchronize()
             model.forward_render(None, case.enc_cams, r_np, case.ren_cams, case.target, out=o_np,
                                  enc_hw=(He, We))
@@ -418,8 +454,8 @@ def main():
                "d2h_bytes_per_step": int(out_h.numel() * 4), "steps": args.e2e_steps,
                "path": ("lvsg_submit_frame / lvsg_wait_frame (host C ABI, pinned buffers, "
                         "two frames in flight)" if not sharded else
-                        "pinned host encoder views (own share) -> lvsg_encode_device -> NCCL "
-                        "all-gather -> lvsg_forward_render (NULL encoder list; pinned render "
+                        "pinned host encoder views (own share) -> lvsg_encode_device -> pyramid "
+                        "exchange -> lvsg_forward_render (NULL encoder list; pinned render "
                         "views in, pinned frame out)")}
 
     if rank == 0:
@@ -487,8 +523,11 @@ def main():
                                    f"{v1 - v0} of {M} encoder views per rank")
                        if world > 1 else "1 target",
                        "l2": "flushed (256 MB write) between timed frames",
-                       "parallelism": (f"target-sharded x{world}; encoder view-sharded with an "
-                                       "NCCL all-gather of the feature pyramid per frame")
+                       "parallelism": (f"target-sharded x{world}; encoder view-sharded, pyramid "
+                                       + ("exchange fused into the encoder epilogue (CUDA IPC "
+                                          "stores over NVLink + NCCL one-element barrier)"
+                                          if exchange == "fused" else
+                                          "all-gathered per level with NCCL") + " per frame")
                        if world > 1 else "single GPU"},
             "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "roofline": roof, "cpu_baseline": cpu, "clocks": clocks.summary(),

@@ -198,8 +198,22 @@ lvsg_status lvsg_encode_device(lvsg_ctx* ctx, int64_t views, const float* enc_im
                                int64_t enc_h, int64_t enc_w, int64_t view0, int64_t view1,
                                void* stream);
 /* Device pointer and extent [M, H_k, W_k, C] (fp32, view-major) of pyramid
- * level k of the resident feature pyramid. */
+ * level k of the context's feature pyramid buffers (allocated by the first
+ * encode / export at an encoder resolution). */
 lvsg_status lvsg_pyramid_level(lvsg_ctx* ctx, int64_t level, float** data, int64_t dims[4]);
+
+/* Fused pyramid exchange across GPUs (one process per GPU): export the
+ * context's pyramid level buffers for encoder input enc_h x enc_w as CUDA IPC
+ * handles (handles: pyramid_levels x 64 bytes), hand every other rank's
+ * handles to lvsg_pyramid_import (npeers x pyramid_levels x 64 bytes, any
+ * order). From then on lvsg_encode_device's last conv of every level stores
+ * each pooled value into its own and every peer's level buffer over NVLink, so
+ * after a stream-ordered barrier across the ranks (e.g. a one-element NCCL
+ * all-reduce) every rank holds the whole pyramid with no separate
+ * all-gather. The buffers stay fixed until the context is destroyed (a new
+ * encoder resolution is then a DimError). */
+lvsg_status lvsg_pyramid_export(lvsg_ctx* ctx, int64_t enc_h, int64_t enc_w, uint8_t* handles);
+lvsg_status lvsg_pyramid_import(lvsg_ctx* ctx, int64_t npeers, const uint8_t* handles);
 
 /* Row-band render for output sharding across GPUs: renders
  * output rows [row0,row1) of the resident LDM into rgb_out (device,

@@ -100,6 +100,7 @@ SYMBOLS = [
     "lvsg_load_weights", "lvsg_init_weights", "lvsg_forward", "lvsg_render",
     "lvsg_forward_render", "lvsg_forward_render_device", "lvsg_render_rows_device",
     "lvsg_encode_device", "lvsg_pyramid_level", "lvsg_submit_frame", "lvsg_wait_frame",
+    "lvsg_pyramid_export", "lvsg_pyramid_import",
     "lvsg_synchronize", "lvsg_last_launch_count", "lvsg_stream", "lvsg_stage_world_points",
     "lvsg_stage_footprints", "lvsg_stage_gather", "lvsg_rig_cameras", "lvsg_scene_images",
     "lvsg_profile_enable", "lvsg_profile_read", "lvsg_stage_conv3x3", "lvsg_stage_conv3x3_fused",
@@ -145,6 +146,8 @@ def lib() -> ctypes.CDLL:
     L.lvsg_wait_frame.argtypes = [vp, c_i64]
     L.lvsg_encode_device.argtypes = [vp, c_i64, vp, c_i64, c_i64, c_i64, c_i64, vp]
     L.lvsg_pyramid_level.argtypes = [vp, c_i64, P(vp), P(c_i64)]
+    L.lvsg_pyramid_export.argtypes = [vp, c_i64, c_i64, ctypes.c_char_p]
+    L.lvsg_pyramid_import.argtypes = [vp, c_i64, ctypes.c_char_p]
     L.lvsg_synchronize.argtypes = [vp]
     L.lvsg_last_launch_count.argtypes = [vp]
     L.lvsg_last_launch_count.restype = c_i64

@@ -372,8 +372,15 @@ __global__ void __launch_bounds__(NT, 1)
               const float v11 = __shfl_down_sync(0xffffffffu, v00, 9);
               r[k] = fm(fa(fa(fa(v00, v01), v10), v11), 0.25f);
             }
-            if (writer) *reinterpret_cast<float4*>(po + 4 * c4) = make_float4(r[0], r[1], r[2], r[3]);
+            if (writer) {
+              const float4 pv = make_float4(r[0], r[1], r[2], r[3]);
+              *reinterpret_cast<float4*>(po + 4 * c4) = pv;
+              // fused pyramid exchange: the same float4 into every peer's copy
+              for (int q = 0; q < a.npool_peer; ++q)
+                *reinterpret_cast<float4*>(a.pool_peer[q] + (po - a.pool_out) + 4 * c4) = pv;
+            }
           }
+          if (a.npool_peer) __threadfence_system();  // peer stores before the exchange barrier
         }
       }
       if (!valid) continue;

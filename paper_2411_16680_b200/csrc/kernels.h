@@ -96,6 +96,11 @@ struct ConvArgs {
   // mean_pool2, same summation order) to pool_out [B, H/2, W/2, 32]
   float* pool_out;
   long long pool_bstride;
+  // ... and the same pooled values stored into up to 7 peer GPUs' copies of
+  // the pyramid level (same offsets, mapped over NVLink by CUDA IPC): the
+  // view-sharded encode's exchange fused into the producing epilogue
+  float* pool_peer[7];
+  int npool_peer;
   // Cin = 3 stem only: host copy of the weights [32][3][3][3] and bias [32]
   // (the encoder stem, bound at weight load). The stem kernel then takes
   // them by value in its parameter space, so every FMA reads its weight as

@@ -211,6 +211,9 @@ struct lvsg_ctx {
   std::vector<float> stem_host;  // encoder stem weights [32*27] + bias [32] (host copy)
   std::vector<std::vector<float>> rayproj_host;  // per-level ray_proj [32, C] (host copies)
   int64_t pyr_He = -1, pyr_We = -1;  // encoder resolution of the resident feature pyramid
+  // fused pyramid exchange: every peer's level buffers (CUDA IPC mappings)
+  std::vector<std::vector<float*>> peer_feats;
+  std::vector<void*> peer_maps;
 };
 
 namespace lvsg {
@@ -341,6 +344,8 @@ void bind_weights(lvsg_ctx* c) {
 void ensure_plan(lvsg_ctx* c, int64_t He, int64_t We) {
   if (c->He == He && c->We == We) return;
   c->pyr_He = c->pyr_We = -1;  // buffers re-sized: no resident pyramid
+  if (!c->peer_feats.empty())
+    throw DimError("pyramid exchange: encoder resolution changed after lvsg_pyramid_import");
   const Config& cfg = c->cfg;
   Plan plan = plan_forward(cfg, He, We);
   const int64_t M = cfg.views, C = cfg.channels, Ca = cfg.appear_channels(), K = cfg.pyramid_levels;
@@ -469,7 +474,8 @@ void add_src(ConvArgs& a, const float* p, int C, int H, int W) {
 // pool_out (optional): also the 2x2 mean pool of the result ([B,H/2,W/2,C]),
 // fused into the second conv's epilogue on the tensor-core path.
 void conv_residual(lvsg_ctx* c, const float* x, float* out, float* tmp, int B, int H, int W,
-                   const ConvPairW& p, float* pool_out = nullptr) {
+                   const ConvPairW& p, float* pool_out = nullptr,
+                   const std::vector<float*>* pool_peers = nullptr) {
   const int C = int(c->cfg.channels);
   ConvArgs a = conv_args(B, H, W, C, C, p.w1, p.b1, tmp);
   add_src(a, x, C, H, W);
@@ -481,9 +487,15 @@ void conv_residual(lvsg_ctx* c, const float* x, float* out, float* tmp, int B, i
   b2.res_pstride = C;
   b2.res_bstride = (long long)H * W * C;
   const bool fuse_pool = pool_out && conv3x3_path(b2) == 2;
+  if (pool_peers && !pool_peers->empty() && !fuse_pool)
+    throw CudaError("pyramid exchange: needs the fused-pool tensor-core conv");
   if (fuse_pool) {
     b2.pool_out = pool_out;
     b2.pool_bstride = (long long)(H / 2) * (W / 2) * C;
+    if (pool_peers) {
+      b2.npool_peer = int(pool_peers->size());
+      for (size_t q = 0; q < pool_peers->size(); ++q) b2.pool_peer[q] = (*pool_peers)[q];
+    }
   }
   run_conv(c, b2, c->stream);
   mark(c, "conv", 2);
@@ -670,6 +682,17 @@ void encode_views(lvsg_ctx* c, const float* enc, int64_t He, int64_t We, int m0,
     const auto& e = c->plan.pyramid[size_t(k)];
     return c->feats[size_t(k)].p + size_t(m0) * e.first * e.second * C;
   };
+  // fused exchange (lvsg_pyramid_import): the same slices of every peer
+  const bool exch = !c->peer_feats.empty();
+  std::vector<float*> peer_sl;
+  auto peers = [&](int k, size_t extra) -> const std::vector<float*>* {
+    if (!exch) return nullptr;
+    const auto& e = c->plan.pyramid[size_t(k)];
+    peer_sl.clear();
+    for (auto& pf : c->peer_feats)
+      peer_sl.push_back(pf[size_t(k)] + size_t(m0) * e.first * e.second * C + extra);
+    return &peer_sl;
+  };
   const float* x = c->enc_x.p;
   int k0 = 0;
   if (enc_ready) {
@@ -685,7 +708,8 @@ void encode_views(lvsg_ctx* c, const float* enc, int64_t He, int64_t We, int m0,
       run_conv(c, a, st);
       mark(c, "conv", 1);
       conv_residual(c, xm, xm, c->enc_t.p, 1, h, w, W.lvl_r1[0]);
-      conv_residual(c, xm, xm, c->enc_t.p, 1, h, w, W.lvl_r2[0], fslice(0) + per_f * (m - m0));
+      conv_residual(c, xm, xm, c->enc_t.p, 1, h, w, W.lvl_r2[0], fslice(0) + per_f * (m - m0),
+                    peers(0, per_f * (m - m0)));
     }
     h /= 2;
     w /= 2;
@@ -704,7 +728,7 @@ void encode_views(lvsg_ctx* c, const float* enc, int64_t He, int64_t We, int m0,
     // write the level's residual pairs to enc_x and the pool to feats[k]
     float* xo = c->enc_x.p;
     conv_residual(c, x, xo, c->enc_t.p, B, h, w, W.lvl_r1[size_t(k)]);
-    conv_residual(c, xo, xo, c->enc_t.p, B, h, w, W.lvl_r2[size_t(k)], fslice(k));
+    conv_residual(c, xo, xo, c->enc_t.p, B, h, w, W.lvl_r2[size_t(k)], fslice(k), peers(k, 0));
     h /= 2;
     w /= 2;
     x = fslice(k);
@@ -1174,6 +1198,7 @@ void lvsg_destroy(lvsg_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_enc) cudaEventDestroy(e);
   if (c->down) cudaStreamSynchronize(c->down);
+  for (void* p : c->peer_maps) cudaIpcCloseMemHandle(p);
   for (FrameSlot& S : c->slots) {
     for (cudaEvent_t e : {S.ev_ren, S.ev_free, S.ev_done, S.ev_band[0], S.ev_band[1],
                           S.ev_band[2], S.ev_band[3]})
@@ -1477,7 +1502,8 @@ lvsg_status lvsg_encode_device(lvsg_ctx* c, int64_t views, const float* enc_imag
 
 lvsg_status lvsg_pyramid_level(lvsg_ctx* c, int64_t level, float** data, int64_t dims[4]) {
   return guard(c, [&] {
-    if (c->pyr_He < 0) throw DimError("pyramid: no resident feature pyramid (lvsg_encode_device)");
+    if (c->He <= 0)
+      throw DimError("pyramid: no pyramid buffers yet (lvsg_encode_device / lvsg_pyramid_export)");
     if (level < 0 || level >= c->cfg.pyramid_levels) throw DimError("pyramid: bad level");
     const auto& e = c->plan.pyramid[size_t(level)];
     *data = c->feats[size_t(level)].p;
@@ -1485,6 +1511,44 @@ lvsg_status lvsg_pyramid_level(lvsg_ctx* c, int64_t level, float** data, int64_t
     dims[1] = e.first;
     dims[2] = e.second;
     dims[3] = c->cfg.channels;
+  });
+}
+
+lvsg_status lvsg_pyramid_export(lvsg_ctx* c, int64_t enc_h, int64_t enc_w, uint8_t* handles) {
+  return guard(c, [&] {
+    plan_forward(c->cfg, enc_h, enc_w);
+    ensure_plan(c, enc_h, enc_w);
+    for (int64_t k = 0; k < c->cfg.pyramid_levels; ++k) {
+      cudaIpcMemHandle_t h;
+      CUDA_OK(cudaIpcGetMemHandle(&h, c->feats[size_t(k)].p));
+      std::memcpy(handles + k * 64, &h, 64);
+    }
+  });
+}
+
+lvsg_status lvsg_pyramid_import(lvsg_ctx* c, int64_t npeers, const uint8_t* handles) {
+  return guard(c, [&] {
+    if (npeers < 0 || npeers > 7) throw DimError("pyramid exchange: 0..7 peers");
+    if (npeers == 0) {  // back to a private pyramid (mappings stay open until destroy)
+      c->peer_feats.clear();
+      return;
+    }
+    if (c->He <= 0) throw DimError("pyramid exchange: lvsg_pyramid_export first");
+    const int64_t K = c->cfg.pyramid_levels;
+    std::vector<std::vector<float*>> feats;
+    for (int64_t q = 0; q < npeers; ++q) {
+      std::vector<float*> lv;
+      for (int64_t k = 0; k < K; ++k) {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handles + (q * K + k) * 64, 64);
+        void* p = nullptr;
+        CUDA_OK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        c->peer_maps.push_back(p);
+        lv.push_back(static_cast<float*>(p));
+      }
+      feats.push_back(std::move(lv));
+    }
+    c->peer_feats = std::move(feats);
   });
 }
 

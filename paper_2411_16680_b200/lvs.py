@@ -351,6 +351,21 @@ class Model:
                                                  M if view1 is None else view1,
                                                  _stream_handle(stream)))
 
+    def pyramid_export(self, enc_hw) -> bytes:
+        """CUDA IPC handles of the pyramid level buffers (lvsg_pyramid_export):
+        pyramid_levels x 64 bytes, to be handed to the other ranks."""
+        n = self.cfg.pyramid_levels * 64
+        buf = ctypes.create_string_buffer(n)
+        self._check(self._lib.lvsg_pyramid_export(self._h, int(enc_hw[0]), int(enc_hw[1]), buf))
+        return buf.raw[:n]
+
+    def pyramid_import(self, peer_handles) -> None:
+        """lvsg_pyramid_import: the other ranks' exported handles (a list of
+        bytes); from then on encode_device writes its pooled levels into every
+        peer's pyramid as well (the fused exchange)."""
+        blob = b"".join(peer_handles) or None
+        self._check(self._lib.lvsg_pyramid_import(self._h, len(peer_handles), blob))
+
     def pyramid_level(self, level: int):
         """Level `level` of the resident feature pyramid as a torch CUDA tensor
         [M, H_k, W_k, C] aliasing the context's buffer (e.g. for an NCCL
