@@ -84,17 +84,26 @@ __global__ void __launch_bounds__(128) layer_collapse32_kernel(
   }
 }
 
+// blend_w [32][32] by value (parameter space): the q = n W_blend products
+// take their weights as constant-bank / uniform-register operands.
+struct BlendParam {
+  float w[C * C];
+};
+
 // decode_blend_logits (network.hpp:539-549) for C = 32, M views.
-template <int M>
+template <int M, bool PW>
 __global__ void __launch_bounds__(128) blend_logits32_kernel(const float* __restrict__ V,
                                                              const float* __restrict__ D, int64_t P,
                                                              const float* __restrict__ bw,
                                                              const float* __restrict__ gain,
-                                                             float* __restrict__ logits) {
+                                                             float* __restrict__ logits,
+                                                             const __grid_constant__ BlendParam pw) {
   pdl_grid_sync();
-  __shared__ __align__(16) float s_bw[C * C];
-  for (int e = threadIdx.x; e < C * C; e += blockDim.x) s_bw[e] = bw[e];
-  __syncthreads();
+  __shared__ __align__(16) float s_bw[PW ? 4 : C * C];
+  if (!PW) {
+    for (int e = threadIdx.x; e < C * C; e += blockDim.x) s_bw[e] = bw[e];
+    __syncthreads();
+  }
   const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= P) return;
   float n[C], q[C];
@@ -112,7 +121,9 @@ __global__ void __launch_bounds__(128) blend_logits32_kernel(const float* __rest
     const float nk = n[k];
 #pragma unroll
     for (int c4 = 0; c4 < C / 4; ++c4) {
-      const float4 w = reinterpret_cast<const float4*>(s_bw + k * C)[c4];
+      const float4 w = PW ? make_float4(pw.w[k * C + 4 * c4], pw.w[k * C + 4 * c4 + 1],
+                                        pw.w[k * C + 4 * c4 + 2], pw.w[k * C + 4 * c4 + 3])
+                          : reinterpret_cast<const float4*>(s_bw + k * C)[c4];
       q[4 * c4] = fmaf(nk, w.x, q[4 * c4]);
       q[4 * c4 + 1] = fmaf(nk, w.y, q[4 * c4 + 1]);
       q[4 * c4 + 2] = fmaf(nk, w.z, q[4 * c4 + 2]);
@@ -142,21 +153,31 @@ __global__ void __launch_bounds__(128) blend_logits32_kernel(const float* __rest
 
 // render_to_input_view decode for C = Ca = 32: payload [a(32), sigma],
 // activated depth and the world point, one thread per texel.
+// The three heads by value: [k][36] = appear(32) | sigma | depth | 0 0.
+struct DecodeParam {
+  float w[C * (C + 4)];
+};
+
+// PW: weights from `pw` (constant-bank FMA operands), else staged in shared
+// memory; 32-bit texel indexing (the caller checks P < 2^31).
+template <bool PW>
 __global__ void __launch_bounds__(128) decode_payload32_kernel(
     const float* __restrict__ V, int L, int H, int W, const float* __restrict__ w_appear,
     const float* __restrict__ w_sigma, const float* __restrict__ w_depth, DepthAct act,
     DevRayCam rc, float* __restrict__ payload, float* __restrict__ depth,
-    float* __restrict__ points) {
+    float* __restrict__ points, const __grid_constant__ DecodeParam pw) {
   pdl_grid_sync();
   constexpr int KW = C + 4;  // appear | sigma | depth | pad (16-byte rows)
-  __shared__ __align__(16) float s_w[C * KW];
-  for (int e = threadIdx.x; e < C * KW; e += blockDim.x) {
-    const int k = e / KW, c = e % KW;
-    s_w[e] = c < C ? w_appear[k * C + c] : (c == C ? w_sigma[k] : (c == C + 1 ? w_depth[k] : 0.f));
+  __shared__ __align__(16) float s_w[PW ? 4 : C * KW];
+  if (!PW) {
+    for (int e = threadIdx.x; e < C * KW; e += blockDim.x) {
+      const int k = e / KW, c = e % KW;
+      s_w[e] = c < C ? w_appear[k * C + c] : (c == C ? w_sigma[k] : (c == C + 1 ? w_depth[k] : 0.f));
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  const int64_t P = (int64_t)L * H * W;
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int P = L * H * W;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P) return;
   float v[C], acc[KW];
   load_row(V + p * C, v);
@@ -167,7 +188,9 @@ __global__ void __launch_bounds__(128) decode_payload32_kernel(
     const float vk = v[k];
 #pragma unroll
     for (int c4 = 0; c4 < KW / 4; ++c4) {
-      const float4 w = reinterpret_cast<const float4*>(s_w + k * KW)[c4];
+      const float4 w = PW ? make_float4(pw.w[k * KW + 4 * c4], pw.w[k * KW + 4 * c4 + 1],
+                                        pw.w[k * KW + 4 * c4 + 2], pw.w[k * KW + 4 * c4 + 3])
+                          : reinterpret_cast<const float4*>(s_w + k * KW)[c4];
       acc[4 * c4] = fmaf(vk, w.x, acc[4 * c4]);
       acc[4 * c4 + 1] = fmaf(vk, w.y, acc[4 * c4 + 1]);
       acc[4 * c4 + 2] = fmaf(vk, w.z, acc[4 * c4 + 2]);
@@ -175,21 +198,21 @@ __global__ void __launch_bounds__(128) decode_payload32_kernel(
     }
   }
   // payload row padded to 36 floats: [a(32), sigma, 0, 0, 0]
-  float4* pay = reinterpret_cast<float4*>(payload + p * (C + 4));
+  float4* pay = reinterpret_cast<float4*>(payload + (int64_t)p * (C + 4));
 #pragma unroll
   for (int c4 = 0; c4 < C / 4; ++c4)
     pay[c4] = make_float4(sigmoid_ref(acc[4 * c4]), sigmoid_ref(acc[4 * c4 + 1]),
                           sigmoid_ref(acc[4 * c4 + 2]), sigmoid_ref(acc[4 * c4 + 3]));
   pay[C / 4] = make_float4(sigmoid_ref(acc[C]), 0.f, 0.f, 0.f);
-  const int l = int(p / ((int64_t)H * W));
+  const int q = p / W, j = p - q * W;
+  const int l = q / H, i = q - l * H;
   const float d = activate_depth(acc[C + 1], l, act);
   depth[p] = d;
-  const int j = int(p % W), i = int((p / W) % H);
   float pt[3];
   world_point(rc, i, j, d, pt);
-  points[p * 3 + 0] = pt[0];
-  points[p * 3 + 1] = pt[1];
-  points[p * 3 + 2] = pt[2];
+  points[(int64_t)p * 3 + 0] = pt[0];
+  points[(int64_t)p * 3 + 1] = pt[1];
+  points[(int64_t)p * 3 + 2] = pt[2];
 }
 
 inline int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
@@ -205,26 +228,43 @@ bool layer_collapse32(const float* V, int L, int64_t PL, int C_, const float* w1
 }
 
 bool blend_logits32(const float* V, const float* deltas, int64_t P, int C_, int M,
-                    const float* blend_w, const float* gain, float* logits, cudaStream_t st) {
+                    const float* blend_w, const float* gain, float* logits, cudaStream_t st,
+                    const float* blend_w_host) {
   if (C_ != C) return false;
   const int g = blocks_for(P, 128);
+  BlendParam pw;
+  if (blend_w_host)
+    for (int e = 0; e < C * C; ++e) pw.w[e] = blend_w_host[e];
+  const bool h = blend_w_host != nullptr;
+#define LVSG_BL(MM)                                                                             \
+  if (h)                                                                                         \
+    launch_k(blend_logits32_kernel<MM, true>, g, 128, 0, st, V, deltas, P, blend_w, gain, logits, pw); \
+  else                                                                                           \
+    launch_k(blend_logits32_kernel<MM, false>, g, 128, 0, st, V, deltas, P, blend_w, gain, logits, pw);
   switch (M) {
-    case 4: launch_k(blend_logits32_kernel<4>, g, 128, 0, st, V, deltas, P, blend_w, gain, logits); return true;
-    case 8: launch_k(blend_logits32_kernel<8>, g, 128, 0, st, V, deltas, P, blend_w, gain, logits); return true;
-    case 16: launch_k(blend_logits32_kernel<16>, g, 128, 0, st, V, deltas, P, blend_w, gain, logits); return true;
+    case 4: LVSG_BL(4) return true;
+    case 8: LVSG_BL(8) return true;
+    case 16: LVSG_BL(16) return true;
     default: return false;
   }
+#undef LVSG_BL
 }
 
 bool decode_payload32(const float* V, int L, int H, int W, int C_, const float* w_appear, int Ca,
                       const float* w_sigma, const float* w_depth, const DepthAct& act,
                       const DevRayCam& rc, float* payload, float* depth, float* points,
-                      cudaStream_t st) {
-  if (C_ != C || Ca != C) return false;
+                      cudaStream_t st, const float* w_host) {
   const int64_t P = (int64_t)L * H * W;
-  launch_k(decode_payload32_kernel, blocks_for(P, 128), 128, 0, st, V, L, H, W, w_appear, w_sigma,
-                                                             w_depth, act, rc, payload, depth,
-                                                             points);
+  if (C_ != C || Ca != C || P * (C + 4) >= (int64_t(1) << 31)) return false;
+  DecodeParam pw;
+  if (w_host) {
+    for (int e = 0; e < C * (C + 4); ++e) pw.w[e] = w_host[e];
+    launch_k(decode_payload32_kernel<true>, blocks_for(P, 128), 128, 0, st, V, L, H, W, w_appear,
+             w_sigma, w_depth, act, rc, payload, depth, points, pw);
+  } else {
+    launch_k(decode_payload32_kernel<false>, blocks_for(P, 128), 128, 0, st, V, L, H, W, w_appear,
+             w_sigma, w_depth, act, rc, payload, depth, points, pw);
+  }
   return true;
 }
 

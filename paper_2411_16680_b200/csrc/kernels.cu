@@ -1172,9 +1172,9 @@ void gather_stack(const float* feats, int M, int Hf, int Wf, int C, const DevCam
 void decode_payload(const float* V, int L, int H, int W, int C, const float* w_appear, int Ca,
                     const float* w_sigma, const float* w_depth, const DepthAct& act,
                     const DevRayCam& rc, float* payload, float* depth, float* points,
-                    cudaStream_t st) {
+                    cudaStream_t st, const float* w_host) {
   if (decode_payload32(V, L, H, W, C, w_appear, Ca, w_sigma, w_depth, act, rc, payload, depth,
-                       points, st))
+                       points, st, w_host))
     return;
   const int64_t P = (int64_t)L * H * W;
   launch_k(decode_payload_kernel, blocks_for(P, 128), 128, C * (Ca + 2) * sizeof(float), st, 
@@ -1229,8 +1229,9 @@ void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, c
   }
 }
 void blend_logits(const float* V, const float* deltas, int64_t P, int C, int M,
-                  const float* blend_w, const float* gain, float* logits, cudaStream_t st) {
-  if (blend_logits32(V, deltas, P, C, M, blend_w, gain, logits, st)) return;
+                  const float* blend_w, const float* gain, float* logits, cudaStream_t st,
+                  const float* blend_w_host) {
+  if (blend_logits32(V, deltas, P, C, M, blend_w, gain, logits, st, blend_w_host)) return;
   launch_k(blend_logits_kernel, blocks_for(P, 128), 128, C * C * sizeof(float), st, V, deltas, P, C, M,
                                                                               blend_w, gain, logits);
 }

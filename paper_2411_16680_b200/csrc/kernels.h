@@ -184,10 +184,12 @@ __host__ __device__ inline int acc_stride(int K) { return (K + 1 + 3) & ~3; }
 // render_to_input_view decode (ldm.hpp:229-235): payload [P, Ca+1] =
 // [sigmoid(V w_a), sigmoid(V w_sigma)], depth [P] = activate(V w_depth) and
 // world points [P,3].
+// w_host (optional, C = Ca = 32): host copy of the three heads as [k][36]
+// (appear | sigma | depth | 0 0) for the parameter-space kernel.
 void decode_payload(const float* V, int L, int H, int W, int C, const float* w_appear, int Ca,
                     const float* w_sigma, const float* w_depth, const DepthAct& da,
                     const DevRayCam& rc, float* payload, float* depth, float* points,
-                    cudaStream_t st);
+                    cudaStream_t st, const float* w_host = nullptr);
 // splat_accumulate (geometry.hpp:230-264) of payload [L*H*W, K] into every
 // view: acc [M, L, Hv, Wv, K+1] (atomics; zeroed by the caller).
 void splat(const float* payload, const float* points, int L, int PL, int K, const DevCam* cams_dev,
@@ -216,7 +218,8 @@ bool attend_tc(float* V, const float* deltas, int64_t P, int C, int M, int heads
                const float* wo, const float* gain, int zero_scores, cudaStream_t st);
 // logits [P, M] = <rms_norm(V,g) W_blend, Δ_m> / sqrt(C) (network.hpp:539-549).
 void blend_logits(const float* V, const float* deltas, int64_t P, int C, int M,
-                  const float* blend_w, const float* gain, float* logits, cudaStream_t st);
+                  const float* blend_w, const float* gain, float* logits, cudaStream_t st,
+                  const float* blend_w_host = nullptr);
 // layer_collapse (network.hpp:440-455): V [L,H,W,C] -> out [L/2,H,W,C].
 void layer_collapse(const float* V, int L, int64_t PL, int C, const float* w1, const float* b1,
                     const float* w2, const float* b2, float* out, cudaStream_t st);
@@ -224,11 +227,12 @@ void layer_collapse(const float* V, int L, int64_t PL, int C, const float* w1, c
 bool layer_collapse32(const float* V, int L, int64_t PL, int C, const float* w1, const float* b1,
                       const float* w2, const float* b2, float* out, cudaStream_t st);
 bool blend_logits32(const float* V, const float* deltas, int64_t P, int C, int M,
-                    const float* blend_w, const float* gain, float* logits, cudaStream_t st);
+                    const float* blend_w, const float* gain, float* logits, cudaStream_t st,
+                    const float* blend_w_host = nullptr);
 bool decode_payload32(const float* V, int L, int H, int W, int C, const float* w_appear, int Ca,
                       const float* w_sigma, const float* w_depth, const DepthAct& act,
                       const DevRayCam& rc, float* payload, float* depth, float* points,
-                      cudaStream_t st);
+                      cudaStream_t st, const float* w_host = nullptr);
 // out[p] = V[p,:] . w (decode_linear with K = 1), optionally activated depth.
 // Both pre-activation heads (out_a = V w_a, out_b = V w_b) in one pass over V.
 void decode_scalar2(const float* V, int64_t P, int C, const float* wa, float* outa, const float* wb,

@@ -210,6 +210,8 @@ struct lvsg_ctx {
   lvsg::Buf wimg_tmp;  // uncached image for the stage entry points
   std::vector<float> stem_host;  // encoder stem weights [32*27] + bias [32] (host copy)
   std::vector<std::vector<float>> rayproj_host;  // per-level ray_proj [32, C] (host copies)
+  std::vector<float> blendw_host;                // blend_w [C, C] (host copy)
+  std::vector<float> decw_host;                  // decode heads [C][C+4] (host copy)
   int64_t pyr_He = -1, pyr_We = -1;  // encoder resolution of the resident feature pyramid
   // fused pyramid exchange: every peer's level buffers (CUDA IPC mappings)
   std::vector<std::vector<float*>> peer_feats;
@@ -291,7 +293,25 @@ void bind_weights(lvsg_ctx* c) {
   W.w_sigma = take(C);
   W.w_depth = take(C);
   W.w_appear = take(C * Ca);
+  if (Ca == C) {  // the decode heads as [k][C+4] for the parameter-space kernel
+    std::vector<float> wa(static_cast<size_t>(C * Ca)), ws(static_cast<size_t>(C)),
+        wd(static_cast<size_t>(C));
+    CUDA_OK(cudaMemcpy(wa.data(), W.w_appear, wa.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(ws.data(), W.w_sigma, ws.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(wd.data(), W.w_depth, wd.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    c->decw_host.assign(size_t(C * (C + 4)), 0.f);
+    for (int64_t k = 0; k < C; ++k) {
+      for (int64_t j = 0; j < C; ++j) c->decw_host[size_t(k * (C + 4) + j)] = wa[size_t(k * C + j)];
+      c->decw_host[size_t(k * (C + 4) + C)] = ws[size_t(k)];
+      c->decw_host[size_t(k * (C + 4) + C + 1)] = wd[size_t(k)];
+    }
+  } else {
+    c->decw_host.clear();
+  }
   W.blend_w = take(C * C);
+  c->blendw_host.assign(size_t(C * C), 0.f);
+  CUDA_OK(cudaMemcpy(c->blendw_host.data(), W.blend_w, size_t(C * C) * sizeof(float),
+                     cudaMemcpyDeviceToHost));
   W.blend_gain = take(C);
   for (const Step& st : cfg.steps) {
     StepW sw;
@@ -837,7 +857,8 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
     const DepthAct act = depth_act(L, target);
     // update_block: render the volume into every view (ldm.hpp:223-244)
     decode_payload(V, int(L), int(H), int(Wd), C, W.w_appear, Ca, W.w_sigma, W.w_depth, act,
-                   ray_cam(target.camera, Wd, H), c->payload.p, c->depth_in.p, c->points.p, st);
+                   ray_cam(target.camera, Wd, H), c->payload.p, c->depth_in.p, c->points.p, st,
+                   c->decw_host.empty() ? nullptr : c->decw_host.data());
     mark(c, "splat", 1);
     const float* feedback = c->fbr.p;
     if (cfg.ablate_render) {
@@ -898,7 +919,8 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
   if (cfg.ablate_attention) {
     CUDA_OK(cudaMemsetAsync(c->logits.p, 0, size_t(P) * M * sizeof(float), st));
   } else {
-    blend_logits(V, c->deltas.p, P, C, M, W.blend_w, W.blend_gain, c->logits.p, st);
+    blend_logits(V, c->deltas.p, P, C, M, W.blend_w, W.blend_gain, c->logits.p, st,
+                 c->blendw_host.data());
     mark(c, "attention", 1);
   }
   decode_scalar2(V, P, C, W.w_depth, c->pre_d.p, W.w_sigma, c->pre_s.p, st);
