@@ -120,7 +120,10 @@ __device__ __forceinline__ uint32_t swz(int r, int c4) {
   return uint32_t(r * 128 + ((c4 ^ (r & 7)) << 4));
 }
 
-template <bool kAlpha, bool kPool>
+// kPool: 0 none, 1 the fused mean pool, 2 the pool also stored into peer
+// GPUs' pyramids (the fused exchange; its own instantiation so the common
+// pool path carries no peer code)
+template <bool kAlpha, int kPool>
 __global__ void __launch_bounds__(NT, 1)
     conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap,
                       const __grid_constant__ CUtensorMap omap,
@@ -376,11 +379,12 @@ __global__ void __launch_bounds__(NT, 1)
               const float4 pv = make_float4(r[0], r[1], r[2], r[3]);
               *reinterpret_cast<float4*>(po + 4 * c4) = pv;
               // fused pyramid exchange: the same float4 into every peer's copy
-              for (int q = 0; q < a.npool_peer; ++q)
-                *reinterpret_cast<float4*>(a.pool_peer[q] + (po - a.pool_out) + 4 * c4) = pv;
+              if constexpr (kPool == 2)
+                for (int q = 0; q < a.npool_peer; ++q)
+                  *reinterpret_cast<float4*>(a.pool_peer[q] + (po - a.pool_out) + 4 * c4) = pv;
             }
           }
-          if (a.npool_peer) __threadfence_system();  // peer stores before the exchange barrier
+          if constexpr (kPool == 2) __threadfence_system();  // peer stores before the barrier
         }
       }
       if (!valid) continue;
@@ -474,11 +478,13 @@ void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
     throw CudaError("conv3x3_tc: missing or misaligned weight image (conv3x3_tc_prepare)");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(conv3x3_tc_kernel<false, false>,
+    cudaFuncSetAttribute(conv3x3_tc_kernel<false, 0>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(conv3x3_tc_kernel<true, false>,
+    cudaFuncSetAttribute(conv3x3_tc_kernel<true, 0>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(conv3x3_tc_kernel<false, true>,
+    cudaFuncSetAttribute(conv3x3_tc_kernel<false, 1>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(conv3x3_tc_kernel<false, 2>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr = true;
   }
@@ -508,9 +514,10 @@ void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
   lattr[0].val.programmaticStreamSerializationAllowed = (a.pdl && pdl_enabled()) ? 1 : 0;
   cfg.attrs = lattr;
   cfg.numAttrs = 1;
-  auto kern = a.alpha      ? conv3x3_tc_kernel<true, false>
-              : a.pool_out ? conv3x3_tc_kernel<false, true>
-                           : conv3x3_tc_kernel<false, false>;
+  auto kern = a.alpha                         ? conv3x3_tc_kernel<true, 0>
+              : a.pool_out && a.npool_peer > 0 ? conv3x3_tc_kernel<false, 2>
+              : a.pool_out                    ? conv3x3_tc_kernel<false, 1>
+                                              : conv3x3_tc_kernel<false, 0>;
   if (a.alpha && a.pool_out) throw CudaError("conv3x3_tc: alpha and pool together are not built");
   if (cudaLaunchKernelEx(&cfg, kern, xmap, omap, rmap, a, tiles) != cudaSuccess)
     throw CudaError("conv3x3_tc: launch failed");
