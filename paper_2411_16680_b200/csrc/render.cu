@@ -88,7 +88,7 @@ __device__ __forceinline__ Taps taps_for(const RenderArgs& a, int i, int j) {
 // colour and weight are zeroed by select). MM == 0: cameras staged in shared
 // memory, branchy footprint.
 template <int MM>
-__global__ void __launch_bounds__(128, MM == 16 ? 4 : 6) render_fused_kernel(const RenderArgs a) {
+__global__ void __launch_bounds__(128, MM == 16 ? 4 : 8) render_fused_kernel(const RenderArgs a) {
   pdl_grid_sync();
   extern __shared__ DevCam s_cams[];
   if (MM == 0) {
