@@ -293,6 +293,19 @@ def test_config2_full_scale_matches_oracle(oracle):
     assert d.max() <= RGB_MAX_ABS and psnr(rgb, want) >= RGB_PSNR_DB
 
 
+@pytest.mark.slow
+def test_config3_full_scale_matches_oracle(oracle):
+    """BASELINE config 3 at full scale: 16 views of 1080p (576x960 encoder),
+    the across-view attention stress case, against the oracle."""
+    from paper_2411_16680_b200 import workloads as wl
+    case = wl.config3(div=1)
+    _, rgb = run_gpu(case)
+    want = run_oracle(oracle, case)["rgb"]
+    d = np.abs(rgb - want)
+    print(f"{case.name}: max-abs {d.max():.3e} psnr {psnr(rgb, want):.1f} dB")
+    assert d.max() <= RGB_MAX_ABS and psnr(rgb, want) >= RGB_PSNR_DB
+
+
 def _variants():
     from paper_2411_16680_b200 import workloads as wl
     return {
