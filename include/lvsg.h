@@ -134,6 +134,19 @@ const char* lvsg_last_error(const lvsg_ctx* ctx);
  * mismatches and wrong counts -> LVSG_ERR_DIM. */
 lvsg_status lvsg_load_weights(lvsg_ctx* ctx, int64_t count, const float* const* tensors,
                               const int32_t* ranks, const int64_t* dims);
+/* The same store as a QNTC named-tensor container (pack_tensors,
+ * io.cpp:100-124): `count` f32 entries bound by position as above (names are
+ * carried, not used for binding). A malformed container -> LVSG_ERR_IO with
+ * unpack_tensors' message (io.cpp:126-171); an f64 entry -> LVSG_ERR_DIM
+ * (NamedTensor::as_f32's SchemaError, io.cpp:86-90). */
+lvsg_status lvsg_load_weights_qntc(lvsg_ctx* ctx, const void* bytes, size_t len);
+/* NetParams member path of build_params tensor `index`
+ * ("encoder.levels.0.res1.w1", network.hpp:95-132). */
+lvsg_status lvsg_param_name(const lvsg_model_config* cfg, int64_t index, char* out, size_t len);
+/* init_param_store(cfg, seed) packed as a QNTC container with those names:
+ * *len receives the byte size; out == NULL only sizes it. */
+lvsg_status lvsg_pack_param_store_qntc(const lvsg_model_config* cfg, uint64_t seed, void* out,
+                                       size_t cap, size_t* len);
 /* init_params(cfg, seed) on the host, uploaded (network.hpp:321-328). */
 lvsg_status lvsg_init_weights(lvsg_ctx* ctx, uint64_t seed);
 

@@ -30,6 +30,7 @@ REF_SRC = "/root/reference/proj"
 P = ctypes.POINTER
 vp = ctypes.c_void_p
 i64 = ctypes.c_int64
+sz = ctypes.c_size_t
 
 
 def _f32(a):
@@ -216,6 +217,9 @@ class Reference:
                                             vp, cp, sz]
         L.ref_model_config_to_json.argtypes = [P(capi.ModelConfigC), cp, sz, cp, sz]
         L.ref_model_config_roundtrip.argtypes = [cp, cp, sz, cp, sz]
+        L.ref_pack_param_store.argtypes = [P(capi.ModelConfigC), ctypes.c_uint64, cp, vp, sz,
+                                           P(sz), cp, sz]
+        L.ref_qntc_roundtrip.argtypes = [cp, sz, vp, sz, P(sz), cp, sz]
         L.ref_world_points.argtypes = [P(capi.FrustumC), vp, i64, i64, i64, vp, cp, sz]
         L.ref_gather.argtypes = [P(capi.CameraC), vp, i64, i64, i64, vp, i64, vp, vp, cp, sz]
         L.ref_footprints.argtypes = [P(capi.CameraC), vp, i64, vp, vp, vp, cp, sz]
@@ -245,6 +249,27 @@ class Reference:
         buf = ctypes.create_string_buffer(1 << 16)
         self._call(self.lib.ref_model_config_to_json, ctypes.byref(cc.c), buf, 1 << 16)
         return buf.value.decode()
+
+    def pack_param_store(self, cfg, seed, names) -> bytes:
+        """The reference's pack_tensors over its own init_param_store."""
+        cc = cfg.to_c()
+        n = sz()
+        nm = "\n".join(names).encode()
+        self._call(self.lib.ref_pack_param_store, ctypes.byref(cc.c), seed, nm, None, 0,
+                   ctypes.byref(n))
+        buf = ctypes.create_string_buffer(n.value)
+        self._call(self.lib.ref_pack_param_store, ctypes.byref(cc.c), seed, nm, buf, n.value,
+                   ctypes.byref(n))
+        return buf.raw[:n.value]
+
+    def qntc_roundtrip(self, data: bytes) -> bytes:
+        """pack_tensors(unpack_tensors(data)); raises the reference's
+        IoError / SchemaError message (codes 3 / 1)."""
+        n = sz()
+        self._call(self.lib.ref_qntc_roundtrip, data, len(data), None, 0, ctypes.byref(n))
+        buf = ctypes.create_string_buffer(max(n.value, 1))
+        self._call(self.lib.ref_qntc_roundtrip, data, len(data), buf, n.value, ctypes.byref(n))
+        return buf.raw[:n.value]
 
     def model_config_roundtrip(self, text: str) -> str:
         """model_config_to_json(model_config_from_json(text)); raises with the

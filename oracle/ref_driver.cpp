@@ -93,6 +93,12 @@ int guarded(char* err, size_t len, Fn&& fn) {
   } catch (const NumericError& e) {
     set_err(err, len, e.what());
     return 2;
+  } catch (const SchemaError& e) {
+    set_err(err, len, e.what());
+    return 1;
+  } catch (const IoError& e) {
+    set_err(err, len, e.what());
+    return 3;
   } catch (const std::exception& e) {
     set_err(err, len, e.what());
     return 13;
@@ -398,6 +404,37 @@ int ref_model_config_roundtrip(const char* text, char* out, size_t out_len, char
     const std::string j = model_config_to_json(model_config_from_json(text));
     if (j.size() + 1 > out_len) throw std::runtime_error("ref_model_config_roundtrip: buffer too small");
     std::memcpy(out, j.c_str(), j.size() + 1);
+  });
+}
+
+// pack_tensors (io.cpp:100-124) of init_param_store(cfg, seed), entry i
+// named by line i of `names` ('\n'-separated). *outlen = bytes needed.
+int ref_pack_param_store(const lvsg_model_config* c, uint64_t seed, const char* names, char* out,
+                         size_t cap, size_t* outlen, char* err, size_t len) {
+  return guarded(err, len, [&] {
+    std::vector<Tensor<float>> s = init_param_store<float>(to_cfg(c), seed);
+    std::vector<NamedTensor> entries;
+    std::string all(names), cur;
+    size_t at = 0;
+    for (size_t i = 0; i < s.size(); ++i) {
+      const size_t nl = all.find('\n', at);
+      entries.push_back(NamedTensor::wrap(all.substr(at, nl - at), s[i]));
+      at = nl == std::string::npos ? all.size() : nl + 1;
+    }
+    const std::string b = pack_tensors(entries);
+    *outlen = b.size();
+    if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
+  });
+}
+
+// pack_tensors(unpack_tensors(in)) (io.cpp:100-171): the reference's
+// IoError / SchemaError messages for malformed input.
+int ref_qntc_roundtrip(const char* in, size_t n, char* out, size_t cap, size_t* outlen, char* err,
+                       size_t len) {
+  return guarded(err, len, [&] {
+    const std::string b = pack_tensors(unpack_tensors(std::string_view(in, n)));
+    *outlen = b.size();
+    if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
   });
 }
 

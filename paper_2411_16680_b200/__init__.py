@@ -6,7 +6,7 @@ CUDA for sm_100a + C++ host runtime, C ABI in include/lvsg.h); this package
 is its Python mirror. See DESIGN.md.
 """
 from .camera import Camera, Frustum, RigSpec, pose_cam_from_world  # noqa: F401
-from .capi import DeviceError, DimError, NumericError  # noqa: F401
+from .capi import DeviceError, DimError, IoError, NumericError  # noqa: F401
 from .config import (ModelConfig, SchemaError, StepConfig, config1,  # noqa: F401
                      full_scale_config, micro_config, model_config_from_json,
                      model_config_to_json, nano_config, scaled_full_config)

@@ -77,6 +77,10 @@ class NumericError(ArithmeticError):
     """NaN / Inf (reference NumericError, tensor.hpp:21-25)."""
 
 
+class IoError(OSError):
+    """Corrupt / truncated container (reference IoError, io.hpp:20-24)."""
+
+
 class DeviceError(RuntimeError):
     """CUDA / NCCL / runtime failure in the native library."""
 
@@ -88,6 +92,8 @@ def raise_for(code: int, msg: str):
         raise DimError(msg)
     if code == ERR_NUMERIC:
         raise NumericError(msg)
+    if code == ERR_IO:
+        raise IoError(msg)
     raise DeviceError(f"lvsg error {code}: {msg}")
 
 
@@ -104,6 +110,7 @@ SYMBOLS = [
     "lvsg_synchronize", "lvsg_last_launch_count", "lvsg_stream", "lvsg_stage_world_points",
     "lvsg_stage_footprints", "lvsg_stage_gather", "lvsg_rig_cameras", "lvsg_scene_images",
     "lvsg_profile_enable", "lvsg_profile_read", "lvsg_stage_conv3x3", "lvsg_stage_conv3x3_fused",
+    "lvsg_load_weights_qntc", "lvsg_param_name", "lvsg_pack_param_store_qntc",
 ]
 
 
@@ -132,6 +139,10 @@ def lib() -> ctypes.CDLL:
     L.lvsg_last_error.restype = ctypes.c_char_p
     L.lvsg_load_weights.argtypes = [vp, c_i64, P(c_f32p), P(c_i32), P(c_i64)]
     L.lvsg_init_weights.argtypes = [vp, ctypes.c_uint64]
+    L.lvsg_load_weights_qntc.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
+    L.lvsg_param_name.argtypes = [P(ModelConfigC), c_i64, ctypes.c_char_p, ctypes.c_size_t]
+    L.lvsg_pack_param_store_qntc.argtypes = [P(ModelConfigC), ctypes.c_uint64, vp, ctypes.c_size_t,
+                                             P(ctypes.c_size_t)]
     L.lvsg_forward.argtypes = [vp, c_i64, P(c_f32p), c_i64, c_i64, P(CameraC), P(FrustumC),
                                P(LdmOutC)]
     L.lvsg_render.argtypes = [vp, c_i64, P(c_f32p), c_i64, c_i64, P(CameraC), c_f32p]

@@ -18,6 +18,15 @@ struct DimError : std::runtime_error {
 struct NumericError : std::runtime_error {
   explicit NumericError(const std::string& m) : std::runtime_error(m) {}
 };
+// io.hpp:20-31: corrupt / truncated containers (exit 3) and content that
+// does not fit the expected schema (exit 1, like DimError).
+struct IoError : std::runtime_error {
+  explicit IoError(const std::string& m) : std::runtime_error(m) {}
+};
+struct SchemaError : std::runtime_error {
+  explicit SchemaError(const std::string& m) : std::runtime_error(m) {}
+};
+
 struct CudaError : std::runtime_error {
   explicit CudaError(const std::string& m) : std::runtime_error(m) {}
 };
@@ -68,6 +77,8 @@ struct ParamSpec {
   std::vector<int64_t> shape;
   Init init;
   double scale;
+  // NetParams member path, e.g. "encoder.levels.0.res1.w1" (network.hpp:95-132)
+  std::string name;
   int64_t numel() const {
     int64_t n = 1;
     for (int64_t d : shape) n *= d;
@@ -75,6 +86,27 @@ struct ParamSpec {
   }
 };
 std::vector<ParamSpec> param_layout(const Config& cfg);
+
+// QNTC named-tensor container (io.hpp:33-60, io.cpp:100-171): "QNTC", u32
+// version 1, u32 count, then per entry u32 name length, name, u8 dtype
+// (0 f32, 1 f64), u32 rank, u64 dims, little-endian payload.
+struct QntcEntry {
+  std::string name;
+  uint8_t dtype = 0;  // 0 f32, 1 f64
+  std::vector<int64_t> dims;
+  const uint8_t* payload = nullptr;  // points into the parsed buffer
+  int64_t numel() const {
+    int64_t n = 1;
+    for (int64_t d : dims) n *= d;
+    return n;
+  }
+};
+// Throws IoError with the reference's messages on a malformed container.
+std::vector<QntcEntry> qntc_unpack(const uint8_t* bytes, size_t len);
+// Appends one f32 entry.
+void qntc_put_f32(std::string& out, const std::string& name, const std::vector<int64_t>& dims,
+                  const float* data);
+std::string qntc_header(uint32_t count);
 
 // init_param_store<float> (network.hpp:354-362), bit-exact.
 void init_param_store(const Config& cfg, uint64_t seed, float* out);

@@ -1001,6 +1001,12 @@ lvsg_status guard(lvsg_ctx* c, const auto& fn) {
   } catch (const DimError& e) {
     if (c) c->err = e.what();
     return LVSG_ERR_DIM;
+  } catch (const SchemaError& e) {
+    if (c) c->err = e.what();
+    return LVSG_ERR_DIM;
+  } catch (const IoError& e) {
+    if (c) c->err = e.what();
+    return LVSG_ERR_IO;
   } catch (const NumericError& e) {
     if (c) c->err = e.what();
     return LVSG_ERR_NUMERIC;
@@ -1263,6 +1269,29 @@ lvsg_status lvsg_load_weights(lvsg_ctx* c, int64_t count, const float* const* te
     bind_weights(c);
     c->have_weights = true;
   });
+}
+
+lvsg_status lvsg_load_weights_qntc(lvsg_ctx* c, const void* bytes, size_t len) {
+  std::vector<std::vector<float>> store;
+  std::vector<const float*> ptrs;
+  std::vector<int32_t> ranks;
+  std::vector<int64_t> dims;
+  const lvsg_status s = guard(c, [&] {
+    if (!bytes && len) throw IoError("tensor container: null buffer");
+    const auto entries = qntc_unpack(static_cast<const uint8_t*>(bytes), len);
+    for (const QntcEntry& e : entries) {
+      // NamedTensor::as_f32 (io.cpp:86-90): a float model binds f32 entries
+      if (e.dtype != 0)
+        throw SchemaError("tensor container: entry \"" + e.name + "\" holds f64, expected f32");
+      store.emplace_back(size_t(e.numel()));
+      std::memcpy(store.back().data(), e.payload, store.back().size() * sizeof(float));
+      ranks.push_back(int32_t(e.dims.size()));
+      dims.insert(dims.end(), e.dims.begin(), e.dims.end());
+    }
+    for (const auto& t : store) ptrs.push_back(t.data());
+  });
+  if (s != LVSG_OK) return s;
+  return lvsg_load_weights(c, int64_t(ptrs.size()), ptrs.data(), ranks.data(), dims.data());
 }
 
 lvsg_status lvsg_init_weights(lvsg_ctx* c, uint64_t seed) {

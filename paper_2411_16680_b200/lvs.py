@@ -235,6 +235,12 @@ class Model:
     def init_weights(self, seed: int) -> None:
         self._check(self._lib.lvsg_init_weights(self._h, seed))
 
+    def load_weights_qntc(self, data: bytes) -> None:
+        """A parameter store as a QNTC container (qntc.pack_tensors /
+        the reference's pack_tensors), bound by position."""
+        data = bytes(data)
+        self._check(self._lib.lvsg_load_weights_qntc(self._h, data, len(data)))
+
     # --- forward / render ---
     def forward(self, images, cams: Sequence[Camera], target: Frustum,
                 outputs: bool = True, deltas: bool = False) -> Optional[Ldm]:

@@ -401,3 +401,39 @@ def test_pipelined_frames_match_synchronous():
     m.wait_frame(tickets[0])  # retired: returns at once
     with pytest.raises(q.DimError):
         m.wait_frame(tickets[-1] + 1)  # never submitted
+
+
+def test_load_weights_qntc_binds_like_load_weights():
+    """The QNTC weight hand-off (lvsg_load_weights_qntc): a store packed by
+    the reference's pack_tensors layout binds exactly like lvsg_load_weights
+    (bit-identical frame); malformed containers -> IoError, f64 entries and
+    shape / count mismatches -> DimError (SchemaError / bind_params)."""
+    from paper_2411_16680_b200 import qntc
+    case = nano()
+    names = qntc.param_names(case.cfg)
+    store = list(case.store())
+    m = q.Model(case.cfg, device=0)
+    m.load_weights(store)
+    a = m.forward_render(case.enc_images, case.enc_cams, case.ren_images, case.ren_cams,
+                         case.target)
+    m2 = q.Model(case.cfg, device=0)
+    m2.load_weights_qntc(qntc.pack_tensors(list(zip(names, store))))
+    b = m2.forward_render(case.enc_images, case.enc_cams, case.ren_images, case.ren_cams,
+                          case.target)
+    assert np.array_equal(a, b)
+    with pytest.raises(q.IoError, match="bad magic"):
+        m2.load_weights_qntc(b"QNTX" + bytes(8))
+    with pytest.raises(q.IoError, match="trailing bytes"):
+        m2.load_weights_qntc(qntc.pack_tensors(list(zip(names, store))) + b"\0")
+    with pytest.raises(q.DimError, match="holds f64"):
+        m2.load_weights_qntc(qntc.pack_tensors(
+            [(n, t.astype(np.float64) if i == 5 else t) for i, (n, t) in enumerate(zip(names, store))]))
+    with pytest.raises(q.DimError, match="too few"):
+        m2.load_weights_qntc(qntc.pack_tensors(list(zip(names, store))[:-1]))
+    with pytest.raises(q.DimError, match="expected shape"):
+        m2.load_weights_qntc(qntc.pack_tensors(
+            [(n, t[:4] if i == 1 else t) for i, (n, t) in enumerate(zip(names, store))]))
+    # the failed loads left the bound weights in place
+    c = m2.forward_render(case.enc_images, case.enc_cams, case.ren_images, case.ren_cams,
+                          case.target)
+    assert np.array_equal(a, c)
