@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 
 def test_forward_demo_outputs(tmp_path, oracle):
-    res = demo.run("nano", str(tmp_path), seed=3, sweep=(2, 4), frames=3)
+    res = demo.run("nano", str(tmp_path), seed=3, sweep=(2, 4), frames=3)  # nano has 4 views
     case = wl.nano()
     rgb = np.load(tmp_path / "target.npy")
     ref = oracle.forward_render(case.cfg, case.enc_images, case.enc_cams, case.ren_images,
