@@ -187,6 +187,31 @@ lvsg_status lvsg_submit_frame(lvsg_ctx* ctx, int64_t views, const float* const* 
                               const lvsg_frustum* target, float* rgb_out, int64_t* ticket);
 lvsg_status lvsg_wait_frame(lvsg_ctx* ctx, int64_t ticket);
 
+/* Input-side decimation: the caller passes only the
+ * full-resolution views (e.g. 1080p); they are uploaded once, and the
+ * encoder input is their resize_bilinear to (enc_h, enc_w) on the device
+ * (tape.hpp:858-917, per channel of the HWC image, as the reference's
+ * chw_to_hwc(resize_bilinear(hwc_to_chw(x)))) seen by cameras
+ * Camera::scaled(enc_w, enc_h) (camera.cpp:67-77) of the render cameras.
+ * Otherwise identical to lvsg_forward_render / lvsg_submit_frame (same
+ * tickets, same two frames in flight). */
+lvsg_status lvsg_forward_render_decimated(lvsg_ctx* ctx, int64_t views,
+                                          const float* const* render_images, int64_t render_h,
+                                          int64_t render_w, const lvsg_camera* render_cams,
+                                          int64_t enc_h, int64_t enc_w,
+                                          const lvsg_frustum* target, float* rgb_out);
+lvsg_status lvsg_submit_frame_decimated(lvsg_ctx* ctx, int64_t views,
+                                        const float* const* render_images, int64_t render_h,
+                                        int64_t render_w, const lvsg_camera* render_cams,
+                                        int64_t enc_h, int64_t enc_w, const lvsg_frustum* target,
+                                        float* rgb_out, int64_t* ticket);
+/* The decimation alone on DEVICE buffers: src [M,h,w,3] -> dst
+ * [M,out_h,out_w,3] (resize_bilinear per channel), on `stream` (NULL: the
+ * context's stream). */
+lvsg_status lvsg_decimate_views_device(lvsg_ctx* ctx, int64_t views, const float* src, int64_t h,
+                                       int64_t w, float* dst, int64_t out_h, int64_t out_w,
+                                       void* stream);
+
 /* Device-resident variant: enc_images [M,He,We,3] and render_images
  * [M,Hr,Wr,3] are contiguous DEVICE buffers, rgb_out a DEVICE buffer
  * [Ho,Wo,3]; work is enqueued on `stream` (cudaStream_t, NULL = the

@@ -220,6 +220,7 @@ class Reference:
         L.ref_pack_param_store.argtypes = [P(capi.ModelConfigC), ctypes.c_uint64, cp, vp, sz,
                                            P(sz), cp, sz]
         L.ref_qntc_roundtrip.argtypes = [cp, sz, vp, sz, P(sz), cp, sz]
+        L.ref_resize_hwc.argtypes = [vp, i64, i64, i64, i64, i64, i64, vp, cp, sz]
         L.ref_world_points.argtypes = [P(capi.FrustumC), vp, i64, i64, i64, vp, cp, sz]
         L.ref_gather.argtypes = [P(capi.CameraC), vp, i64, i64, i64, vp, i64, vp, vp, cp, sz]
         L.ref_footprints.argtypes = [P(capi.CameraC), vp, i64, vp, vp, vp, cp, sz]
@@ -261,6 +262,14 @@ class Reference:
         self._call(self.lib.ref_pack_param_store, ctypes.byref(cc.c), seed, nm, buf, n.value,
                    ctypes.byref(n))
         return buf.raw[:n.value]
+
+    def resize_hwc(self, x, Ho, Wo):
+        """The reference's resize_bilinear of [B,H,W,C] per channel."""
+        x = np.ascontiguousarray(x, np.float32)
+        B, H, W, C = x.shape
+        out = np.zeros((B, Ho, Wo, C), np.float32)
+        self._call(self.lib.ref_resize_hwc, _f32(x), B, H, W, C, Ho, Wo, _f32(out))
+        return out
 
     def qntc_roundtrip(self, data: bytes) -> bytes:
         """pack_tensors(unpack_tensors(data)); raises the reference's

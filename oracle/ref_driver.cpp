@@ -407,6 +407,18 @@ int ref_model_config_roundtrip(const char* text, char* out, size_t out_len, char
   });
 }
 
+// chw_to_hwc(resize_bilinear(hwc_to_chw(x))) (tape.hpp:629-917) of a
+// [B,H,W,C] batch: the input-side decimation of 1080p views.
+int ref_resize_hwc(const float* in, int64_t B, int64_t H, int64_t W, int64_t C, int64_t Ho,
+                   int64_t Wo, float* out, char* err, size_t len) {
+  return guarded(err, len, [&] {
+    Tape<float> tape;
+    std::vector<float> v(in, in + B * H * W * C);
+    Var x = tape.constant(Tensor<float>({B, H, W, C}, std::move(v)));
+    copy_out(tape.value(tape.chw_to_hwc(tape.resize_bilinear(tape.hwc_to_chw(x), Ho, Wo))), out);
+  });
+}
+
 // pack_tensors (io.cpp:100-124) of init_param_store(cfg, seed), entry i
 // named by line i of `names` ('\n'-separated). *outlen = bytes needed.
 int ref_pack_param_store(const lvsg_model_config* c, uint64_t seed, const char* names, char* out,

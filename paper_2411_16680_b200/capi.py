@@ -111,6 +111,7 @@ SYMBOLS = [
     "lvsg_stage_footprints", "lvsg_stage_gather", "lvsg_rig_cameras", "lvsg_scene_images",
     "lvsg_profile_enable", "lvsg_profile_read", "lvsg_stage_conv3x3", "lvsg_stage_conv3x3_fused",
     "lvsg_load_weights_qntc", "lvsg_param_name", "lvsg_pack_param_store_qntc",
+    "lvsg_forward_render_decimated", "lvsg_submit_frame_decimated", "lvsg_decimate_views_device",
 ]
 
 
@@ -155,6 +156,11 @@ def lib() -> ctypes.CDLL:
     L.lvsg_submit_frame.argtypes = [vp, c_i64, P(c_f32p), c_i64, c_i64, P(CameraC), P(c_f32p),
                                     c_i64, c_i64, P(CameraC), P(FrustumC), c_f32p, P(c_i64)]
     L.lvsg_wait_frame.argtypes = [vp, c_i64]
+    L.lvsg_forward_render_decimated.argtypes = [vp, c_i64, P(c_f32p), c_i64, c_i64, P(CameraC),
+                                                c_i64, c_i64, P(FrustumC), c_f32p]
+    L.lvsg_submit_frame_decimated.argtypes = [vp, c_i64, P(c_f32p), c_i64, c_i64, P(CameraC),
+                                              c_i64, c_i64, P(FrustumC), c_f32p, P(c_i64)]
+    L.lvsg_decimate_views_device.argtypes = [vp, c_i64, vp, c_i64, c_i64, vp, c_i64, c_i64, vp]
     L.lvsg_encode_device.argtypes = [vp, c_i64, vp, c_i64, c_i64, c_i64, c_i64, vp]
     L.lvsg_pyramid_level.argtypes = [vp, c_i64, P(vp), P(c_i64)]
     L.lvsg_pyramid_export.argtypes = [vp, c_i64, c_i64, ctypes.c_char_p]

@@ -1383,12 +1383,25 @@ lvsg_status lvsg_render(lvsg_ctx* c, int64_t views, const float* const* images, 
 // uploads run on the copy stream under frame k's compute, and frame k's
 // banded read-back runs on a separate download stream. lvsg_forward_render
 // is submit + wait.
-lvsg_status lvsg_submit_frame(lvsg_ctx* c, int64_t views, const float* const* enc_images,
-                              int64_t enc_h, int64_t enc_w, const lvsg_camera* enc_cams,
-                              const float* const* render_images, int64_t render_h,
-                              int64_t render_w, const lvsg_camera* render_cams,
-                              const lvsg_frustum* target, float* rgb_out, int64_t* ticket) {
+namespace lvsg {
+namespace {
+// decimate: no encoder images; the encoder input is resize_bilinear of the
+// uploaded render views to (enc_h, enc_w) on the device (tape.hpp:858-917
+// per channel), with the render cameras .scaled(enc_w, enc_h)
+// (camera.cpp:67-77) as encoder cameras.
+lvsg_status submit_impl(lvsg_ctx* c, int64_t views, const float* const* enc_images,
+                        int64_t enc_h, int64_t enc_w, const lvsg_camera* enc_cams,
+                        const float* const* render_images, int64_t render_h, int64_t render_w,
+                        const lvsg_camera* render_cams, const lvsg_frustum* target,
+                        float* rgb_out, int64_t* ticket, bool decimate) {
+  std::unique_ptr<lvsg_camera[]> dec_cams;
+  if (decimate && render_cams && views > 0 && views <= 4096 && enc_h > 0 && enc_w > 0) {
+    dec_cams.reset(new lvsg_camera[size_t(views)]);
+    for (int64_t m = 0; m < views; ++m) dec_cams[m] = camera_scaled(render_cams[m], enc_w, enc_h);
+  }
+  const lvsg_camera* enc_cams_used = decimate ? dec_cams.get() : enc_cams;
   return guard(c, [&] {
+    if (decimate && !dec_cams) throw DimError("forward: bad decimation extents or cameras");
     check_views(c, views, enc_h, enc_w);
     check_views(c, views, render_h, render_w);
     for (int64_t m = 0; m < views; ++m) camera_validate(render_cams[m]);
@@ -1430,6 +1443,19 @@ lvsg_status lvsg_submit_frame(lvsg_ctx* c, int64_t views, const float* const* en
     }
     upload_images(c, S.ren_in, views, render_images, render_h, render_w, c->xfer);
     CUDA_OK(cudaEventRecord(S.ev_ren, c->xfer));
+    if (decimate) {
+      S.enc_in.ensure(per * size_t(views));
+      if (S.ev_enc.empty()) {
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        S.ev_enc.push_back(e);
+      }
+      resize_hwc(S.ren_in.p, S.enc_in.p, int(views), int(render_h), int(render_w), 3, int(enc_h),
+                 int(enc_w), c->xfer);
+      c->launches += 1;
+      CUDA_OK(cudaEventRecord(S.ev_enc[0], c->xfer));
+      CUDA_OK(cudaStreamWaitEvent(c->stream, S.ev_enc[0], 0));
+    }
     // enc_images == NULL: the resident pyramid (lvsg_encode_device, complete
     // on the context's stream) is used. With the previous frame still in
     // flight the uploads finish under its compute, so the encoder runs
@@ -1439,8 +1465,8 @@ lvsg_status lvsg_submit_frame(lvsg_ctx* c, int64_t views, const float* const* en
     if (enc_images && behind)
       CUDA_OK(cudaStreamWaitEvent(c->stream, S.ev_enc[size_t(views - 1)], 0));
     CamTables t;
-    forward_device(c, enc_images ? S.enc_in.p : nullptr, enc_h, enc_w, enc_cams, *target,
-                   render_cams, &t, enc_images && !behind ? S.ev_enc.data() : nullptr);
+    forward_device(c, enc_images || decimate ? S.enc_in.p : nullptr, enc_h, enc_w, enc_cams_used,
+                   *target, render_cams, &t, enc_images && !behind ? S.ev_enc.data() : nullptr);
     const int64_t Ho = c->plan.out_height, Wo = c->plan.out_width;
     S.rgb.ensure(size_t(Ho * Wo * 3));
     CUDA_OK(cudaStreamWaitEvent(c->stream, S.ev_ren, 0));
@@ -1468,6 +1494,52 @@ lvsg_status lvsg_submit_frame(lvsg_ctx* c, int64_t views, const float* const* en
     S.ticket = k;
     c->next_ticket = k + 1;
     if (ticket) *ticket = k;
+  });
+}
+}  // namespace
+}  // namespace lvsg
+
+lvsg_status lvsg_submit_frame(lvsg_ctx* c, int64_t views, const float* const* enc_images,
+                              int64_t enc_h, int64_t enc_w, const lvsg_camera* enc_cams,
+                              const float* const* render_images, int64_t render_h,
+                              int64_t render_w, const lvsg_camera* render_cams,
+                              const lvsg_frustum* target, float* rgb_out, int64_t* ticket) {
+  return submit_impl(c, views, enc_images, enc_h, enc_w, enc_cams, render_images, render_h,
+                     render_w, render_cams, target, rgb_out, ticket, false);
+}
+
+lvsg_status lvsg_submit_frame_decimated(lvsg_ctx* c, int64_t views,
+                                        const float* const* render_images, int64_t render_h,
+                                        int64_t render_w, const lvsg_camera* render_cams,
+                                        int64_t enc_h, int64_t enc_w, const lvsg_frustum* target,
+                                        float* rgb_out, int64_t* ticket) {
+  return submit_impl(c, views, nullptr, enc_h, enc_w, nullptr, render_images, render_h, render_w,
+                     render_cams, target, rgb_out, ticket, true);
+}
+
+lvsg_status lvsg_forward_render_decimated(lvsg_ctx* c, int64_t views,
+                                          const float* const* render_images, int64_t render_h,
+                                          int64_t render_w, const lvsg_camera* render_cams,
+                                          int64_t enc_h, int64_t enc_w,
+                                          const lvsg_frustum* target, float* rgb_out) {
+  int64_t ticket = -1;
+  const lvsg_status s = lvsg_submit_frame_decimated(c, views, render_images, render_h, render_w,
+                                                    render_cams, enc_h, enc_w, target, rgb_out,
+                                                    &ticket);
+  if (s != LVSG_OK) return s;
+  return lvsg_wait_frame(c, ticket);
+}
+
+lvsg_status lvsg_decimate_views_device(lvsg_ctx* c, int64_t views, const float* src, int64_t h,
+                                       int64_t w, float* dst, int64_t out_h, int64_t out_w,
+                                       void* stream) {
+  return guard(c, [&] {
+    if (views < 1 || h < 1 || w < 1 || out_h < 1 || out_w < 1 || !src || !dst)
+      throw DimError("decimate: bad extents or null buffer");
+    resize_hwc(src, dst, int(views), int(h), int(w), 3, int(out_h), int(out_w),
+               stream ? static_cast<cudaStream_t>(stream) : c->stream);
+    c->launches += 1;
+    CUDA_OK(cudaGetLastError());
   });
 }
 

@@ -299,6 +299,33 @@ class Model:
                                                   rgb.ctypes.data_as(capi.c_f32p)))
         return rgb
 
+    def forward_render_decimated(self, render_images, render_cams, target: Frustum,
+                                 enc_hw, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """lvsg_forward_render_decimated: only the full-resolution views are
+        passed; the encoder sees their resize_bilinear to enc_hw through
+        Camera.scaled cameras."""
+        ra, rk, Hr, Wr = _img_ptrs(render_images)
+        He, We = enc_hw
+        if out is None:
+            plan = plan_forward(self.cfg, He, We)
+            out = np.zeros((plan.out_height, plan.out_width, 3), np.float32)
+        assert out.dtype == np.float32 and out.flags.c_contiguous
+        fr = target.to_c()
+        self._last_enc_hw = (He, We)
+        self._check(self._lib.lvsg_forward_render_decimated(
+            self._h, len(rk), ra, Hr, Wr, _cam_array(render_cams), He, We, ctypes.byref(fr),
+            out.ctypes.data_as(capi.c_f32p)))
+        return out
+
+    def decimate_views_device(self, src, dst, stream=None) -> None:
+        """lvsg_decimate_views_device on torch CUDA tensors [M,h,w,3] ->
+        [M,out_h,out_w,3]."""
+        for t in (src, dst):
+            assert t.is_cuda and t.is_contiguous() and t.dtype.itemsize == 4 and t.shape[-1] == 3
+        self._check(self._lib.lvsg_decimate_views_device(
+            self._h, src.shape[0], src.data_ptr(), src.shape[1], src.shape[2], dst.data_ptr(),
+            dst.shape[1], dst.shape[2], _stream_handle(stream)))
+
     def submit_frame(self, enc_images, enc_cams, render_images, render_cams, target: Frustum,
                      out: np.ndarray) -> int:
         """lvsg_submit_frame: enqueue one host-buffer frame (pinned arrays

@@ -437,3 +437,42 @@ def test_load_weights_qntc_binds_like_load_weights():
     c = m2.forward_render(case.enc_images, case.enc_cams, case.ren_images, case.ren_cams,
                           case.target)
     assert np.array_equal(a, c)
+
+
+def test_decimation_matches_reference_resize(reference):
+    """lvsg_decimate_views_device == the reference's resize_bilinear of the
+    HWC views (tape.hpp:858-917 through hwc_to_chw / chw_to_hwc), bit-exact,
+    1080p -> 576 x 960 (config 2's encoder input)."""
+    import torch
+    from paper_2411_16680_b200 import workloads as wl
+    case = wl.config2(div=1)
+    src = case.ren_images[:2]
+    want = reference.resize_hwc(src, 576, 960)
+    m = q.Model(case.cfg, device=0)
+    d_src = torch.from_numpy(np.ascontiguousarray(src)).cuda()
+    d_dst = torch.empty((2, 576, 960, 3), device="cuda")
+    m.decimate_views_device(d_src, d_dst)
+    torch.cuda.synchronize()
+    assert np.array_equal(d_dst.cpu().numpy(), want)
+
+
+def test_forward_render_decimated(oracle, reference):
+    """Only the full-resolution views in: the frame equals forward_render with
+    the reference-decimated encoder images and Camera.scaled cameras
+    (bit-identical), and the oracle on the same inputs within the gate."""
+    from paper_2411_16680_b200 import workloads as wl
+    case = wl.config2(div=4)
+    He, We = case.enc_images.shape[1:3]
+    enc = reference.resize_hwc(case.ren_images, He, We)
+    ecams = [c.scaled(We, He) for c in case.ren_cams]
+    m = q.Model(case.cfg, device=0)
+    m.load_weights(case.store())
+    a = m.forward_render_decimated(case.ren_images, case.ren_cams, case.target, (He, We))
+    b = m.forward_render(enc, ecams, case.ren_images, case.ren_cams, case.target)
+    assert np.array_equal(a, b)
+    for _ in range(3):  # pipelined slots reuse: still identical
+        assert np.array_equal(m.forward_render_decimated(case.ren_images, case.ren_cams,
+                                                         case.target, (He, We)), a)
+    ref = oracle.forward_render(case.cfg, enc, ecams, case.ren_images, case.ren_cams,
+                                case.target, case.flat(), outputs=("rgb",))["rgb"]
+    assert float(np.max(np.abs(a - ref))) <= RGB_MAX_ABS and psnr(a, ref) >= RGB_PSNR_DB
