@@ -317,6 +317,21 @@ class Model:
             out.ctypes.data_as(capi.c_f32p)))
         return out
 
+    def submit_frame_decimated(self, render_images, render_cams, target: Frustum, enc_hw,
+                               out: np.ndarray) -> int:
+        """lvsg_submit_frame_decimated: the pipelined form of
+        forward_render_decimated; wait_frame(ticket) fills `out`."""
+        ra, rk, Hr, Wr = _img_ptrs(render_images)
+        assert out.dtype == np.float32 and out.flags.c_contiguous
+        fr = target.to_c()
+        t = ctypes.c_int64(-1)
+        self._check(self._lib.lvsg_submit_frame_decimated(
+            self._h, len(rk), ra, Hr, Wr, _cam_array(render_cams), enc_hw[0], enc_hw[1],
+            ctypes.byref(fr), out.ctypes.data_as(capi.c_f32p), ctypes.byref(t)))
+        self._inflight = getattr(self, "_inflight", {})
+        self._inflight[t.value] = (ra, rk, out)
+        return t.value
+
     def decimate_views_device(self, src, dst, stream=None) -> None:
         """lvsg_decimate_views_device on torch CUDA tensors [M,h,w,3] ->
         [M,out_h,out_w,3]."""
