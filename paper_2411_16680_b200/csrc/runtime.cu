@@ -1450,11 +1450,12 @@ lvsg_status submit_impl(lvsg_ctx* c, int64_t views, const float* const* enc_imag
         CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         S.ev_enc.push_back(e);
       }
+      // on the compute stream behind the upload: a kernel on the copy
+      // stream would interleave with the previous frame's persistent kernels
+      CUDA_OK(cudaStreamWaitEvent(c->stream, S.ev_ren, 0));
       resize_hwc(S.ren_in.p, S.enc_in.p, int(views), int(render_h), int(render_w), 3, int(enc_h),
-                 int(enc_w), c->xfer);
+                 int(enc_w), c->stream);
       c->launches += 1;
-      CUDA_OK(cudaEventRecord(S.ev_enc[0], c->xfer));
-      CUDA_OK(cudaStreamWaitEvent(c->stream, S.ev_enc[0], 0));
     }
     // enc_images == NULL: the resident pyramid (lvsg_encode_device, complete
     // on the context's stream) is used. With the previous frame still in
