@@ -525,6 +525,7 @@ bool attend_tc(float* V, const float* deltas, int64_t P, int C_, int M, int head
     launch<HH, MM>(V, deltas, P, wq, wo, gain, zero_scores, st);             \
     return true;                                                             \
   }
+  LVSG_ATT(1, 2) LVSG_ATT(2, 2) LVSG_ATT(4, 2)
   LVSG_ATT(1, 4) LVSG_ATT(2, 4) LVSG_ATT(4, 4)
   LVSG_ATT(1, 8) LVSG_ATT(2, 8) LVSG_ATT(4, 8)
   LVSG_ATT(1, 16) LVSG_ATT(2, 16) LVSG_ATT(4, 16)

@@ -242,6 +242,7 @@ bool blend_logits32(const float* V, const float* deltas, int64_t P, int C_, int 
   else                                                                                           \
     launch_k(blend_logits32_kernel<MM, false>, g, 128, 0, st, V, deltas, P, blend_w, gain, logits, pw);
   switch (M) {
+    case 2: LVSG_BL(2) return true;
     case 4: LVSG_BL(4) return true;
     case 8: LVSG_BL(8) return true;
     case 16: LVSG_BL(16) return true;

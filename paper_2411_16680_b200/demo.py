@@ -73,7 +73,7 @@ def _device_ms(cfg, case, views: int, frames: int, weights: bytes) -> tuple:
 
 
 def run(workload: str, out_dir: str, seed: int = 3, weights_path: str | None = None,
-        config_path: str | None = None, sweep=(4, 8, 16), frames: int = 10) -> dict:
+        config_path: str | None = None, sweep=(2, 4, 8, 16), frames: int = 10) -> dict:
     case = WORKLOADS[workload]()
     cfg = case.cfg
     if config_path:
@@ -136,7 +136,7 @@ def main(argv=None):
     ap.add_argument("--weights", default=None, help="QNTC parameter store")
     ap.add_argument("--out", required=True)
     ap.add_argument("--frames", type=int, default=10)
-    ap.add_argument("--sweep", default="4,8,16")
+    ap.add_argument("--sweep", default="2,4,8,16")
     a = ap.parse_args(argv)
     res = run(a.workload, a.out, a.seed, a.weights, a.config,
               tuple(int(x) for x in a.sweep.split(",") if x), a.frames)

@@ -476,3 +476,14 @@ def test_forward_render_decimated(oracle, reference):
     ref = oracle.forward_render(case.cfg, enc, ecams, case.ren_images, case.ren_cams,
                                 case.target, case.flat(), outputs=("rgb",))["rgb"]
     assert float(np.max(np.abs(a - ref))) <= RGB_MAX_ABS and psnr(a, ref) >= RGB_PSNR_DB
+
+
+def test_two_views_match_oracle(oracle):
+    """M = 2 (the reference forward-demo's smallest sweep point,
+    main.cpp:582) runs the view-specialised tensor-core attention and blend
+    kernels like M = 4 / 8 / 16."""
+    from paper_2411_16680_b200 import workloads as wl
+    case = wl.config2(div=4, views_rig=(1, 2))
+    m, rgb = run_gpu(case)
+    ref = run_oracle(oracle, case)["rgb"]
+    assert float(np.max(np.abs(rgb - ref))) <= RGB_MAX_ABS and psnr(rgb, ref) >= RGB_PSNR_DB
