@@ -1075,6 +1075,31 @@ __global__ void stage_gather_kernel(DevCam cam, const float* image, int Hi, int 
                   image[((int64_t)f.y1 * Wi + f.x0) * C + c], image[((int64_t)f.y1 * Wi + f.x1) * C + c]);
 }
 
+// resize_hwc for RGB (the input-side decimation of the views): one thread
+// per output pixel, taps computed once for its three channels.
+__global__ void resize_rgb_kernel(const float* __restrict__ in, float* __restrict__ out, int B,
+                                  int H, int W, int Ho, int Wo) {
+  pdl_grid_sync();
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * Ho * Wo) return;
+  const int x = int(i % Wo);
+  const int64_t t = i / Wo;
+  const int y = int(t % Ho);
+  const int b = int(t / Ho);
+  int y0, y1, x0, x1;
+  float fy, fx;
+  resize_tap(y, H, Ho, y0, y1, fy);
+  resize_tap(x, W, Wo, x0, x1, fx);
+  const float* s = in + (int64_t)b * H * W * 3;
+  const float* p00 = s + ((int64_t)y0 * W + x0) * 3;
+  const float* p10 = s + ((int64_t)y0 * W + x1) * 3;
+  const float* p01 = s + ((int64_t)y1 * W + x0) * 3;
+  const float* p11 = s + ((int64_t)y1 * W + x1) * 3;
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    out[i * 3 + c] = lerp2(__ldg(p00 + c), __ldg(p10 + c), __ldg(p01 + c), __ldg(p11 + c), fx, fy);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -1119,6 +1144,11 @@ void resize_hwc(const float* in, float* out, int B, int H, int W, int C, int Ho,
     } else {
       launch_k(resize_hwc4_kernel, blocks_for(px, 128), 128, 0, st, in, out, B, H, W, C, Ho, Wo);
     }
+    return;
+  }
+  if (C == 3) {
+    launch_k(resize_rgb_kernel, blocks_for((int64_t)B * Ho * Wo, 256), 256, 0, st, in, out, B, H, W,
+             Ho, Wo);
     return;
   }
   launch_k(resize_hwc_kernel, blocks_for(n, 256), 256, 0, st, in, out, B, H, W, C, Ho, Wo);
