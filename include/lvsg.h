@@ -291,6 +291,29 @@ lvsg_status lvsg_stage_footprints(lvsg_ctx* ctx, const lvsg_camera* cam, const f
 lvsg_status lvsg_stage_gather(lvsg_ctx* ctx, const lvsg_camera* cam, const float* image,
                               int64_t Hi, int64_t Wi, int64_t C, const float* points, int64_t P,
                               float* values, float* mask);
+/* attend_residual (attention.hpp:248-252) in place on V [P, C] (device),
+ * Δ in the reference layout [P, M, C] (backproject_stack, network.hpp:421-436),
+ * wq heads x [C, C] contiguous, wo [heads*C, C], gain [C] (all device). */
+lvsg_status lvsg_stage_attend(lvsg_ctx* ctx, float* V, const float* deltas, int64_t P, int64_t M,
+                              int64_t heads, const float* wq, const float* wo, const float* gain,
+                              int32_t zero_scores);
+/* upsample_activate + render_target (ldm.hpp:249-271, :193-199) of a given
+ * final volume: V [L,H,W,C], blend logits [L,H,W,M], heads w_depth / w_sigma
+ * [C], images [M,Hr,Wr,3] (all device) seen through cams -> rgb [Ho,Wo,3]
+ * (device). A depth outside the frustum -> LVSG_ERR_DIM (world_points). */
+lvsg_status lvsg_stage_upsample_render(lvsg_ctx* ctx, const lvsg_frustum* target, const float* V,
+                                       const float* logits, int64_t L, int64_t H, int64_t W,
+                                       int64_t M, const float* w_depth, const float* w_sigma,
+                                       const float* images, int64_t Hr, int64_t Wr,
+                                       const lvsg_camera* cams, int64_t Ho, int64_t Wo,
+                                       float* rgb);
+/* render_to_input_view (ldm.hpp:223-244; splat geometry.hpp:230-326) of
+ * V [L,H,W,C] (device) in the frustum `target` into one camera:
+ * out [cam.height, cam.width, Ca+1] (device; composited appearance + alpha). */
+lvsg_status lvsg_stage_render_to_view(lvsg_ctx* ctx, const lvsg_frustum* target, const float* V,
+                                      int64_t L, int64_t H, int64_t W, const float* w_appear,
+                                      int64_t Ca, const float* w_sigma, const float* w_depth,
+                                      const lvsg_camera* cam, float* out);
 
 /* ---- synthetic inputs (host; the benchmarks' generator) -----------------
  * RigSpec::cameras / ::target (scenes.cpp:40-60): rows*cols cameras, row
@@ -303,6 +326,11 @@ lvsg_status lvsg_rig_cameras(int64_t rows, int64_t cols, double baseline, int64_
 lvsg_status lvsg_scene_images(uint64_t seed, int64_t planes, const lvsg_frustum* scene_fr,
                               int64_t views, const lvsg_camera* cams, float* images, char* err,
                               size_t err_len);
+/* The same with every plane except the last (the backdrop wall) shifted by
+ * shift_x metres along x: config 4's moving content. */
+lvsg_status lvsg_scene_images_shifted(uint64_t seed, int64_t planes, const lvsg_frustum* scene_fr,
+                                      double shift_x, int64_t views, const lvsg_camera* cams,
+                                      float* images, char* err, size_t err_len);
 
 /* conv3x3 (kernels_ref.hpp:72-96) on DEVICE channel-last tensors x
  * [B,H,W,Cin] -> y [B,H,W,Cout], w [Cout,Cin,3,3], b [Cout] (nullable).

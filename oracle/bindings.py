@@ -87,6 +87,9 @@ class Oracle:
         L.lvso_render_target.argtypes = [P(capi.FrustumC), vp, vp, vp, i64, i64, i64, i64, vp,
                                          i64, i64, P(capi.CameraC), vp]
         L.lvso_conv3x3.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64]
+        L.lvso_attend_residual.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp, vp, ctypes.c_int]
+        L.lvso_render_to_view.argtypes = [P(capi.FrustumC), vp, i64, i64, i64, i64, i64, vp, vp,
+                                          vp, P(capi.CameraC), vp]
         self.set_threads(threads or os.cpu_count() or 1)
 
     def set_threads(self, n: int):
@@ -153,6 +156,27 @@ class Oracle:
                                           _cams(cams), _f32(rgb))
         return rgb, bool(bad)
 
+    def attend_residual(self, V, deltas, wq, wo, gain, zero_scores=False):
+        """V [P,C] (not modified) -> V + OTM(rms_norm(V)); deltas [P,M,C];
+        wq [h,C,C]; wo [h*C,C]."""
+        V = np.array(V, np.float32, copy=True, order="C")
+        P_, C = V.shape
+        M = deltas.shape[1]
+        wq = np.ascontiguousarray(wq, np.float32)
+        self.lib.lvso_attend_residual(_f32(V), _f32(np.ascontiguousarray(deltas)), P_, C, M,
+                                      wq.shape[0], _f32(wq), _f32(np.ascontiguousarray(wo)),
+                                      _f32(np.ascontiguousarray(gain)), int(zero_scores))
+        return V
+
+    def render_to_view(self, fr, V, w_appear, w_sigma, w_depth, cam):
+        L_, H, W, C = V.shape
+        Ca = w_appear.shape[1]
+        out = np.zeros((cam.height, cam.width, Ca + 1), np.float32)
+        bad = self.lib.lvso_render_to_view(ctypes.byref(_fr(fr)), _f32(V), L_, H, W, C, Ca,
+                                           _f32(w_appear), _f32(w_sigma), _f32(w_depth),
+                                           _cams([cam]), _f32(out))
+        return out, bool(bad)
+
 
 def _out_shapes(cfg, M, He, We):
     """Output extents of forward/render (network.cpp:118-150 restated)."""
@@ -211,6 +235,12 @@ class Reference:
                               P(capi.CameraC), cp, sz]
         L.ref_scene_images.argtypes = [ctypes.c_uint64, i64, P(capi.FrustumC), i64, P(capi.CameraC),
                                        vp, cp, sz]
+        L.ref_scene_images_shifted.argtypes = [ctypes.c_uint64, i64, P(capi.FrustumC),
+                                               ctypes.c_double, i64, P(capi.CameraC), vp, cp, sz]
+        L.ref_attend_residual.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp, vp, ctypes.c_int,
+                                          cp, sz]
+        L.ref_render_to_input_view.argtypes = [P(capi.FrustumC), vp, i64, i64, i64, i64, i64,
+                                               vp, vp, vp, P(capi.CameraC), vp, cp, sz]
         L.ref_forward_render_ex.argtypes = [P(capi.ModelConfigC), i64, vp, i64, i64,
                                             P(capi.CameraC), vp, i64, i64, P(capi.CameraC),
                                             P(capi.FrustumC), vp, vp, vp, vp, vp, vp, vp, vp, vp,
@@ -300,12 +330,12 @@ class Reference:
                    ctypes.byref(tgt))
         return list(cams), tgt
 
-    def scene_images(self, seed, planes, scene_fr, cams):
+    def scene_images(self, seed, planes, scene_fr, cams, shift_x=0.0):
         M = len(cams)
         H, W = cams[0].height, cams[0].width
         out = np.zeros((M, H, W, 3), np.float32)
-        self._call(self.lib.ref_scene_images, seed, planes, ctypes.byref(_fr(scene_fr)), M,
-                   _cams(cams), _f32(out))
+        self._call(self.lib.ref_scene_images_shifted, seed, planes, ctypes.byref(_fr(scene_fr)),
+                   float(shift_x), M, _cams(cams), _f32(out))
         return out
 
     def forward_render(self, cfg, enc_images, enc_cams, render_images, render_cams, target,
@@ -358,6 +388,24 @@ class Reference:
         self._call(self.lib.ref_render_target, ctypes.byref(_fr(fr)), _f32(depth), _f32(density),
                    _f32(blend), L_, Ho, Wo, M, _f32(images), Hr, Wr, _cams(cams), _f32(rgb))
         return rgb
+
+    def attend_residual(self, V, deltas, wq, wo, gain, zero_scores=False):
+        V = np.array(V, np.float32, copy=True, order="C")
+        P_, C = V.shape
+        M = deltas.shape[1]
+        wq = np.ascontiguousarray(wq, np.float32)
+        self._call(self.lib.ref_attend_residual, _f32(V), _f32(np.ascontiguousarray(deltas)), P_,
+                   C, M, wq.shape[0], _f32(wq), _f32(np.ascontiguousarray(wo)),
+                   _f32(np.ascontiguousarray(gain)), int(zero_scores))
+        return V
+
+    def render_to_view(self, fr, V, w_appear, w_sigma, w_depth, cam):
+        L_, H, W, C = V.shape
+        Ca = w_appear.shape[1]
+        out = np.zeros((cam.height, cam.width, Ca + 1), np.float32)
+        self._call(self.lib.ref_render_to_input_view, ctypes.byref(_fr(fr)), _f32(V), L_, H, W,
+                   C, Ca, _f32(w_appear), _f32(w_sigma), _f32(w_depth), _cams([cam]), _f32(out))
+        return out
 
 
 def fnv1a64(arr: np.ndarray) -> str:

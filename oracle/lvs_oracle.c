@@ -941,6 +941,32 @@ static int render_to_view(const float* V, int64_t L, int64_t H, int64_t W, int64
   return bad;
 }
 
+/* Stage exports for per-stage parity on oracle-supplied inputs. */
+void lvso_attend_residual(float* V, const float* D, int64_t P, int64_t C, int64_t M,
+                          int64_t heads, const float* wq, const float* wo, const float* gain,
+                          int zero) {
+  fusion_p f;
+  memset(&f, 0, sizeof(f));
+  f.heads = (int)heads;
+  f.wq = (const float**)malloc(sizeof(float*) * (size_t)heads);
+  for (int64_t h = 0; h < heads; ++h) f.wq[h] = wq + h * C * C;
+  f.wo = wo;
+  f.gain = gain;
+  attend_residual(V, D, &f, P, C, M, zero);
+  free((void*)f.wq);
+}
+
+int lvso_render_to_view(const lvsg_frustum* fr, const float* V, int64_t L, int64_t H, int64_t W,
+                        int64_t C, int64_t Ca, const float* w_appear, const float* w_sigma,
+                        const float* w_depth, const lvsg_camera* cam, float* out) {
+  params_t P;
+  memset(&P, 0, sizeof(P));
+  P.w_appear = w_appear;
+  P.w_sigma = w_sigma;
+  P.w_depth = w_depth;
+  return render_to_view(V, L, H, W, C, Ca, &P, fr, cam, out);
+}
+
 /* ------------------------------------------------------------------------ */
 /* plan (network.cpp:105-151), validated config assumed                      */
 /* ------------------------------------------------------------------------ */

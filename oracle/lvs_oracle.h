@@ -67,6 +67,16 @@ int lvso_render_target(const lvsg_frustum* fr, const float* depth, const float* 
                        const float* blend, int64_t L, int64_t Ho, int64_t Wo, int64_t M,
                        const float* images, int64_t Hr, int64_t Wr, const lvsg_camera* cams,
                        float* rgb);
+/* attend_residual (attention.hpp:248-252): V [P,C] in place, deltas [P,M,C],
+ * wq heads x [C,C] contiguous, wo [heads*C,C], gain [C]. */
+void lvso_attend_residual(float* V, const float* D, int64_t P, int64_t C, int64_t M,
+                          int64_t heads, const float* wq, const float* wo, const float* gain,
+                          int zero);
+/* render_to_input_view (ldm.hpp:223-244) -> out [cam.height, cam.width, Ca+1];
+ * returns nonzero when world_points saw an out-of-frustum depth. */
+int lvso_render_to_view(const lvsg_frustum* fr, const float* V, int64_t L, int64_t H, int64_t W,
+                        int64_t C, int64_t Ca, const float* w_appear, const float* w_sigma,
+                        const float* w_depth, const lvsg_camera* cam, float* out);
 /* conv3x3 (kernels_ref.hpp:72-96), CHW / OIHW, zero pad by tap skipping. */
 void lvso_conv3x3(const float* x, const float* w, const float* b, float* y, int64_t Cin,
                   int64_t Cout, int64_t H, int64_t W);

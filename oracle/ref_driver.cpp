@@ -186,10 +186,29 @@ int ref_rig(int64_t rows, int64_t cols, double baseline, int64_t width, int64_t 
 
 // make_scene(seed, planes, scene_frustum) then oracle_render per camera,
 // f64 -> f32 (scenes.cpp:62-171). images: [M,H,W,3] contiguous.
+int ref_scene_images_shifted(uint64_t seed, int64_t planes, const lvsg_frustum* scene_fr,
+                             double shift_x, int64_t M, const lvsg_camera* cams, float* images,
+                             char* err, size_t len);
+
 int ref_scene_images(uint64_t seed, int64_t planes, const lvsg_frustum* scene_fr, int64_t M,
                      const lvsg_camera* cams, float* images, char* err, size_t len) {
+  return ref_scene_images_shifted(seed, planes, scene_fr, 0.0, M, cams, images, err, len);
+}
+
+// The same with every plane but the last moved by shift_x along x, then
+// PlaneScene::validate (config 4's moving content).
+int ref_scene_images_shifted(uint64_t seed, int64_t planes, const lvsg_frustum* scene_fr,
+                             double shift_x, int64_t M, const lvsg_camera* cams, float* images,
+                             char* err, size_t len) {
   return guarded(err, len, [&] {
     PlaneScene sc = make_scene(seed, planes, to_fr(*scene_fr));
+    if (shift_x != 0.0) {
+      for (size_t i = 0; i + 1 < sc.planes.size(); ++i) {
+        sc.planes[i].x0 += shift_x;
+        sc.planes[i].x1 += shift_x;
+      }
+      sc.validate();
+    }
     int64_t off = 0;
     for (int64_t m = 0; m < M; ++m) {
       Camera cam = to_cam(cams[m]);
@@ -354,6 +373,47 @@ int ref_upsample_activate(const lvsg_frustum* fr, const float* V, int64_t L, int
     copy_out(tape.value(ldm.depth), depth);
     copy_out(tape.value(ldm.density), density);
     copy_out(tape.value(ldm.blend), blend);
+  });
+}
+
+// attend_residual (attention.hpp:248-252) on V [P,C] in place; deltas
+// [P,M,C]; wq: heads x [C,C] contiguous; wo [heads*C, C]; gain [C].
+int ref_attend_residual(float* V, const float* deltas, int64_t P, int64_t C, int64_t M,
+                        int64_t heads, const float* wq, const float* wo, const float* gain,
+                        int zero_scores, char* err, size_t len) {
+  return guarded(err, len, [&] {
+    Tape<float> tape;
+    auto mk = [&](const float* src, Shape s) {
+      Tensor<float> t(s);
+      std::memcpy(t.data(), src, size_t(t.numel()) * sizeof(float));
+      return tape.constant(std::move(t));
+    };
+    AttendParams ap;
+    for (int64_t h = 0; h < heads; ++h) ap.attn.w_q.push_back(mk(wq + h * C * C, {C, C}));
+    ap.attn.w_o = mk(wo, {heads * C, C});
+    ap.norm_gain = mk(gain, {C});
+    ap.zero_scores = zero_scores != 0;
+    Var out = attend_residual(tape, mk(V, {P, C}), mk(deltas, {P, M, C}), ap);
+    copy_out(tape.value(out), V);
+  });
+}
+
+// render_to_input_view (ldm.hpp:223-244) of V [L,H,W,C] in the frustum fr
+// into camera cam: out [cam.height, cam.width, Ca+1].
+int ref_render_to_input_view(const lvsg_frustum* fr, const float* V, int64_t L, int64_t H,
+                             int64_t W, int64_t C, int64_t Ca, const float* w_appear,
+                             const float* w_sigma, const float* w_depth, const lvsg_camera* cam,
+                             float* out, char* err, size_t len) {
+  return guarded(err, len, [&] {
+    Tape<float> tape;
+    auto mk = [&](const float* src, Shape s) {
+      Tensor<float> t(s);
+      std::memcpy(t.data(), src, size_t(t.numel()) * sizeof(float));
+      return tape.constant(std::move(t));
+    };
+    FeatureVolume<float> fv{mk(V, {L, H, W, C}), 0, to_fr(*fr)};
+    DecodeHeads heads{mk(w_sigma, {C, 1}), mk(w_depth, {C, 1}), mk(w_appear, {C, Ca})};
+    copy_out(tape.value(render_to_input_view(tape, fv, heads, to_cam(*cam))), out);
   });
 }
 

@@ -109,6 +109,8 @@ SYMBOLS = [
     "lvsg_pyramid_export", "lvsg_pyramid_import",
     "lvsg_synchronize", "lvsg_last_launch_count", "lvsg_stream", "lvsg_stage_world_points",
     "lvsg_stage_footprints", "lvsg_stage_gather", "lvsg_rig_cameras", "lvsg_scene_images",
+    "lvsg_scene_images_shifted", "lvsg_stage_attend", "lvsg_stage_upsample_render",
+    "lvsg_stage_render_to_view",
     "lvsg_profile_enable", "lvsg_profile_read", "lvsg_stage_conv3x3", "lvsg_stage_conv3x3_fused",
     "lvsg_load_weights_qntc", "lvsg_param_name", "lvsg_pack_param_store_qntc",
     "lvsg_forward_render_decimated", "lvsg_submit_frame_decimated", "lvsg_decimate_views_device",
@@ -177,6 +179,14 @@ def lib() -> ctypes.CDLL:
                                    P(CameraC)]
     L.lvsg_scene_images.argtypes = [ctypes.c_uint64, c_i64, P(FrustumC), c_i64, P(CameraC), vp,
                                     ctypes.c_char_p, ctypes.c_size_t]
+    L.lvsg_scene_images_shifted.argtypes = [ctypes.c_uint64, c_i64, P(FrustumC), c_f64, c_i64,
+                                            P(CameraC), vp, ctypes.c_char_p, ctypes.c_size_t]
+    L.lvsg_stage_attend.argtypes = [vp, vp, vp, c_i64, c_i64, c_i64, vp, vp, vp, c_i32]
+    L.lvsg_stage_upsample_render.argtypes = [vp, P(FrustumC), vp, vp, c_i64, c_i64, c_i64, c_i64,
+                                             vp, vp, vp, c_i64, c_i64, P(CameraC), c_i64, c_i64,
+                                             vp]
+    L.lvsg_stage_render_to_view.argtypes = [vp, P(FrustumC), vp, c_i64, c_i64, c_i64, vp, c_i64,
+                                            vp, vp, P(CameraC), vp]
     L.lvsg_profile_enable.argtypes = [vp, c_i32]
     L.lvsg_profile_read.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t]
     L.lvsg_stage_conv3x3.argtypes = [vp, vp, vp, vp, vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_i32]

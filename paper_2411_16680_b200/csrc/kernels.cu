@@ -1229,6 +1229,28 @@ void splat_composite(const float* acc, int M, int L, int Hv, int Wv, int K, floa
   launch_k(splat_composite_kernel, blocks_for(n, 256), 256, 0, st, acc, M, L, Hv, Wv, K, out);
 }
 
+__global__ void deltas_to_soa_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                     int64_t P, int M, int C) {
+  pdl_grid_sync();
+  const int G = (C + 3) / 4;
+  const int64_t n = P * M * G * 4;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    // e enumerates dst: ((m * G + g) * P + p) * 4 + k
+    const int k = int(e & 3);
+    const int64_t r = e >> 2;
+    const int64_t p = r % P;
+    const int mg = int(r / P);
+    const int g = mg % G, m = mg / G;
+    const int ch = g * 4 + k;
+    dst[e] = ch < C ? src[(p * M + m) * C + ch] : 0.f;
+  }
+}
+void deltas_to_soa(const float* src, float* dst, int64_t P, int M, int C, cudaStream_t st) {
+  const int64_t n = P * M * ((C + 3) / 4) * 4;
+  launch_k(deltas_to_soa_kernel, int(std::min<int64_t>((n + 255) / 256, 148 * 16)), 256, 0, st, src,
+           dst, P, M, C);
+}
 void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
             const float* const* wq_heads, const float* wo, const float* gain, int zero_scores,
             cudaStream_t st) {

@@ -208,6 +208,9 @@ void splat_composite(const float* acc, int M, int L, int Hv, int Wv, int K, floa
                      cudaStream_t st);
 
 // ---- attention / fusion ----------------------------------------------------
+// Δ from the reference layout [P, M, C] (network.hpp:421-436) into the
+// kernels' view-major SoA [M][ceil(C/4)][P][4] (stage entry points).
+void deltas_to_soa(const float* src, float* dst, int64_t P, int M, int C, cudaStream_t st);
 // V += OTM(rms_norm(V), Δ) (attention.hpp:207-252), in place.
 void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
             const float* const* wq_heads, const float* wo, const float* gain, int zero_scores,

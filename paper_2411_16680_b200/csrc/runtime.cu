@@ -208,6 +208,7 @@ struct lvsg_ctx {
   // tensor and input-channel slice; rebuilt whenever weights are (re)bound
   std::map<std::tuple<const float*, int, int>, std::unique_ptr<lvsg::Buf>> wimg;
   lvsg::Buf wimg_tmp;  // uncached image for the stage entry points
+  lvsg::Buf stage_a, stage_b, stage_c, stage_cams;  // scratch of the per-stage entry points
   std::vector<float> stem_host;  // encoder stem weights [32*27] + bias [32] (host copy)
   std::vector<std::vector<float>> rayproj_host;  // per-level ray_proj [32, C] (host copies)
   std::vector<float> blendw_host;                // blend_w [C, C] (host copy)
@@ -1798,6 +1799,113 @@ lvsg_status lvsg_stage_gather(lvsg_ctx* c, const lvsg_camera* cam, const float* 
                               float* values, float* mask) {
   return guard(c, [&] {
     stage_gather(dev_cam(*cam), image, int(Hi), int(Wi), int(C), points, P, values, mask, c->stream);
+    sync_and_check(c);
+  });
+}
+
+// ---- per-stage entry points on caller-supplied (oracle) inputs --------------
+
+lvsg_status lvsg_stage_attend(lvsg_ctx* c, float* V, const float* deltas, int64_t P, int64_t M,
+                              int64_t heads, const float* wq, const float* wo, const float* gain,
+                              int32_t zero_scores) {
+  return guard(c, [&] {
+    const int C = int(c->cfg.channels);
+    if (P < 1 || M < 1 || heads < 1 || heads > 8) throw DimError("attend_residual: bad shapes");
+    // Δ from the reference layout [P, M, C] into the kernels' view-major SoA
+    // [M][ceil(C/4)][P][4] (+ slack for the attention's partial Δ rows)
+    const size_t n = size_t(P) * M * ((C + 3) / 4) * 4;
+    c->stage_a.ensure(n + 128);
+    deltas_to_soa(deltas, c->stage_a.p, P, int(M), C, c->stream);
+    attend(V, c->stage_a.p, P, C, int(M), int(heads), wq, nullptr, wo, gain, zero_scores,
+           c->stream);
+    sync_and_check(c);
+  });
+}
+
+lvsg_status lvsg_stage_upsample_render(lvsg_ctx* c, const lvsg_frustum* target, const float* V,
+                                       const float* logits, int64_t L, int64_t H, int64_t W,
+                                       int64_t M, const float* w_depth, const float* w_sigma,
+                                       const float* images, int64_t Hr, int64_t Wr,
+                                       const lvsg_camera* cams, int64_t Ho, int64_t Wo,
+                                       float* rgb) {
+  return guard(c, [&] {
+    frustum_validate(*target);
+    const int C = int(c->cfg.channels);
+    if (L < 1 || H < 1 || W < 1 || M < 1 || M > 32 || Ho < 1 || Wo < 1 || Hr < 1 || Wr < 1)
+      throw DimError("render_target: bad shapes");
+    for (int64_t m = 0; m < M; ++m) camera_validate(cams[m]);
+    const int64_t P = L * H * W;
+    c->stage_b.ensure(size_t(2 * P));
+    decode_scalar2(V, P, C, w_depth, c->stage_b.p, w_sigma, c->stage_b.p + P, c->stream);
+    std::vector<DevCam> hc(static_cast<size_t>(M));
+    for (int64_t m = 0; m < M; ++m) hc[size_t(m)] = dev_cam(cams[m]);
+    c->stage_cams.ensure((hc.size() * sizeof(DevCam) + 3) / 4);
+    CUDA_OK(cudaMemcpyAsync(c->stage_cams.p, hc.data(), hc.size() * sizeof(DevCam),
+                            cudaMemcpyHostToDevice, c->stream));
+    RenderArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.pre_d = c->stage_b.p;
+    a.pre_s = c->stage_b.p + P;
+    a.logits = logits;
+    a.L = int(L);
+    a.H = int(H);
+    a.W = int(W);
+    a.M = int(M);
+    a.Ho = int(Ho);
+    a.Wo = int(Wo);
+    a.row0 = 0;
+    a.row1 = int(Ho);
+    a.act = depth_act(L, *target);
+    a.rc = ray_cam(target->camera, Wo, Ho);
+    a.cams = reinterpret_cast<const DevCam*>(c->stage_cams.p);
+    if (M <= kRenderParamViews) {
+      for (int64_t m = 0; m < M; ++m) a.pc[m] = hc[size_t(m)];
+      a.pc_valid = 1;
+    }
+    a.images = images;
+    a.Hr = int(Hr);
+    a.Wr = int(Wr);
+    a.rgb = rgb;
+    a.bad_depth = c->bad_flag;
+    const double slack = 1e-3 * (target->far_depth - target->near_depth);
+    a.slack_lo = target->near_depth - slack;
+    a.slack_hi = target->far_depth + slack;
+    render_fused(a, c->stream);
+    sync_and_check(c);
+  });
+}
+
+lvsg_status lvsg_stage_render_to_view(lvsg_ctx* c, const lvsg_frustum* target, const float* V,
+                                      int64_t L, int64_t H, int64_t W, const float* w_appear,
+                                      int64_t Ca, const float* w_sigma, const float* w_depth,
+                                      const lvsg_camera* cam, float* out) {
+  return guard(c, [&] {
+    frustum_validate(*target);
+    camera_validate(*cam);
+    const int C = int(c->cfg.channels);
+    if (L < 1 || H < 1 || W < 1 || Ca < 1) throw DimError("render_to_input_view: bad shapes");
+    const int64_t P = L * H * W, Hv = cam->height, Wv = cam->width;
+    const int K = int(Ca) + 1, PS = pay_stride(K);
+    c->stage_a.ensure(size_t(P) * PS);      // payload
+    c->stage_b.ensure(size_t(P) * 4);       // depth + points
+    c->stage_c.ensure(size_t(Hv * Wv) * PS + splat_det_scratch_ints(P, L * Hv * Wv));
+    float* depth = c->stage_b.p;
+    float* points = c->stage_b.p + P;
+    decode_payload(V, int(L), int(H), int(W), C, w_appear, int(Ca), w_sigma, w_depth,
+                   depth_act(L, *target), ray_cam(target->camera, W, H), c->stage_a.p, depth,
+                   points, c->stream);
+    const DevCam hc = dev_cam(*cam);
+    c->stage_cams.ensure((sizeof(DevCam) + 3) / 4);
+    CUDA_OK(cudaMemcpyAsync(c->stage_cams.p, &hc, sizeof(DevCam), cudaMemcpyHostToDevice,
+                            c->stream));
+    float* fb = c->stage_c.p;
+    splat_det(c->stage_a.p, points, int(L), int(H * W), K,
+              reinterpret_cast<const DevCam*>(c->stage_cams.p), 1, int(Hv), int(Wv),
+              reinterpret_cast<int*>(fb + size_t(Hv * Wv) * PS), fb, c->stream);
+    // padded feedback rows [Hv*Wv][PS] -> [Hv*Wv][K]
+    CUDA_OK(cudaMemcpy2DAsync(out, size_t(K) * sizeof(float), fb, size_t(PS) * sizeof(float),
+                              size_t(K) * sizeof(float), size_t(Hv * Wv),
+                              cudaMemcpyDeviceToDevice, c->stream));
     sync_and_check(c);
   });
 }

@@ -231,8 +231,26 @@ lvsg_status lvsg_rig_cameras(int64_t rows, int64_t cols, double baseline, int64_
 lvsg_status lvsg_scene_images(uint64_t seed, int64_t planes, const lvsg_frustum* scene_fr,
                               int64_t views, const lvsg_camera* cams, float* images, char* err,
                               size_t err_len) {
+  return lvsg_scene_images_shifted(seed, planes, scene_fr, 0.0, views, cams, images, err,
+                                   err_len);
+}
+
+lvsg_status lvsg_scene_images_shifted(uint64_t seed, int64_t planes, const lvsg_frustum* scene_fr,
+                                      double shift_x, int64_t views, const lvsg_camera* cams,
+                                      float* images, char* err, size_t err_len) {
   return lvsg::guard(err, err_len, [&] {
     lvsg::Scene sc = lvsg::make_scene(seed, planes, *scene_fr);
+    // Config 4's dynamic content: every plane but the last
+    // (the opaque full-coverage wall, scenes.cpp:91-93) moves by shift_x
+    // along x; the shifted scene is re-validated (PlaneScene::validate,
+    // scenes.cpp:19-32: only depths / extents, which a shift keeps).
+    if (shift_x != 0.0)
+      for (size_t i = 0; i + 1 < sc.planes.size(); ++i) {
+        sc.planes[i].x0 += shift_x;
+        sc.planes[i].x1 += shift_x;
+        if (!(sc.planes[i].x1 > sc.planes[i].x0))
+          throw lvsg::DimError("PlaneScene: empty plane extent");
+      }
     int64_t off = 0;
     for (int64_t m = 0; m < views; ++m) {
       lvsg::render(sc, cams[m], images + off);

@@ -130,8 +130,10 @@ def rig_cameras(rig: RigSpec):
 
 
 def scene_images(seed: int, planes: int, scene_frustum: Frustum,
-                 cams: Sequence[Camera]) -> np.ndarray:
-    """make_scene + oracle_render (scenes.cpp:62-171) -> [M, H, W, 3] f32."""
+                 cams: Sequence[Camera], shift_x: float = 0.0) -> np.ndarray:
+    """make_scene + oracle_render (scenes.cpp:62-171) -> [M, H, W, 3] f32.
+    shift_x != 0 moves every plane but the backdrop wall along x (config 4's
+    dynamic content)."""
     H, W = cams[0].height, cams[0].width
     assert all(c.height == H and c.width == W for c in cams)
     out = np.zeros((len(cams), H, W, 3), np.float32)
@@ -139,8 +141,9 @@ def scene_images(seed: int, planes: int, scene_frustum: Frustum,
     e = _err_buf()
     L = capi.lib()
     fr = scene_frustum.to_c()
-    capi.raise_for(L.lvsg_scene_images(seed, planes, ctypes.byref(fr), len(cams), arr,
-                                       out.ctypes.data_as(vp), e, 1024), e.value.decode())
+    capi.raise_for(L.lvsg_scene_images_shifted(seed, planes, ctypes.byref(fr), float(shift_x),
+                                               len(cams), arr, out.ctypes.data_as(vp), e, 1024),
+                   e.value.decode())
     return out
 
 
@@ -500,6 +503,40 @@ class Model:
         self._check(self._lib.lvsg_stage_conv3x3_fused(
             self._h, x_t.data_ptr(), ps, w_t.data_ptr(), w_cin, ci0, ptr(b_t), ptr(norm_gain_t),
             1 if gelu else 0, ptr(resid_t), y_t.data_ptr(), B, cin, Cout, H, W, impl))
+
+    def stage_attend(self, V_t, deltas_t, wq_t, wo_t, gain_t, zero_scores=False):
+        """attend_residual (attention.hpp:248-252) in place on V [P, C];
+        deltas [P, M, C] in the reference layout; wq [h, C, C]; wo [h*C, C]."""
+        P_, M = deltas_t.shape[0], deltas_t.shape[1]
+        self._check(self._lib.lvsg_stage_attend(self._h, V_t.data_ptr(), deltas_t.data_ptr(), P_,
+                                                M, wq_t.shape[0], wq_t.data_ptr(),
+                                                wo_t.data_ptr(), gain_t.data_ptr(),
+                                                1 if zero_scores else 0))
+
+    def stage_upsample_render(self, target: Frustum, V_t, logits_t, w_depth_t, w_sigma_t,
+                              images_t, cams: Sequence[Camera], rgb_t):
+        """upsample_activate + render_target (ldm.hpp:193-199, :249-271) of
+        the final volume V [L,H,W,C] and logits [L,H,W,M] into rgb [Ho,Wo,3]."""
+        L_, H, W, _ = V_t.shape
+        M = logits_t.shape[-1]
+        _, Hr, Wr, _ = images_t.shape
+        Ho, Wo, _ = rgb_t.shape
+        f = target.to_c()
+        self._check(self._lib.lvsg_stage_upsample_render(
+            self._h, ctypes.byref(f), V_t.data_ptr(), logits_t.data_ptr(), L_, H, W, M,
+            w_depth_t.data_ptr(), w_sigma_t.data_ptr(), images_t.data_ptr(), Hr, Wr,
+            _cam_array(cams), Ho, Wo, rgb_t.data_ptr()))
+
+    def stage_render_to_view(self, target: Frustum, V_t, w_appear_t, w_sigma_t, w_depth_t,
+                             cam: Camera, out_t):
+        """render_to_input_view (ldm.hpp:223-244) of V [L,H,W,C] into one
+        camera: out [cam.height, cam.width, Ca+1]."""
+        L_, H, W, _ = V_t.shape
+        f, c = target.to_c(), cam.to_c()
+        self._check(self._lib.lvsg_stage_render_to_view(
+            self._h, ctypes.byref(f), V_t.data_ptr(), L_, H, W, w_appear_t.data_ptr(),
+            w_appear_t.shape[1], w_sigma_t.data_ptr(), w_depth_t.data_ptr(), ctypes.byref(c),
+            out_t.data_ptr()))
 
     def stage_gather(self, cam: Camera, image_t, points_t, values_t, mask_t):
         c = cam.to_c()

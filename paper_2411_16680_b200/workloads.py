@@ -119,15 +119,9 @@ def config3(div: int = 1) -> Case:
 
 
 def _shifted_scene_images(scene_fr, cams, shift):
-    # Dynamic content for config 4 is approximated by translating the cameras
-    # by -shift in x (equivalent to shifting every plane by +shift, including
-    # the backdrop; SURVEY.md §8(d) config 4 keeps the backdrop fixed).
-    moved = []
-    for c in cams:
-        m = c.cam_from_world.copy()
-        m[0, 3] = m[0, 3] + shift
-        moved.append(Camera(c.fx, c.fy, c.cx, c.cy, c.width, c.height, m))
-    return scene_images(21, 3, scene_fr, moved)
+    # Config 4's dynamic content: make_scene(21, 3) with
+    # every plane except the backdrop wall shifted by `shift` metres along x.
+    return scene_images(21, 3, scene_fr, cams, shift_x=shift)
 
 
 def config4_frame(t: int, div: int = 1) -> Case:

@@ -134,6 +134,11 @@ def test_scene_generator_bit_exact(reference):
     b = reference.scene_images(21, 3, fr, cams)
     assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
     assert a.min() > 0.0 and a.max() < 1.0
+    # config 4's moving content: planes but the backdrop shifted along x
+    a = q.scene_images(21, 3, fr, cams, shift_x=0.07)
+    b = reference.scene_images(21, 3, fr, cams, shift_x=0.07)
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert not np.array_equal(a, q.scene_images(21, 3, fr, cams))
 
 
 def test_camera_helpers():

@@ -137,3 +137,60 @@ def test_reference_unit_suite_passes(reference):
     r = subprocess.run([REF_UNIT], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+def test_flip_attribution_metrics(oracle):
+    """tests/parity_util.py on the oracle's own nano frame: identical depth
+    gives no flips and zero error; a depth perturbation large enough to move
+    footprints across a view edge is reported as flip pixels."""
+    import numpy as np
+    from cases import nano
+    from parity_util import flip_mask, frame_metrics, gate
+    case = nano()
+    want = oracle.forward_render(case.cfg, case.enc_images, case.enc_cams, case.ren_images,
+                                 case.ren_cams, case.target, case.flat(), outputs=("rgb", "depth"))
+    m = frame_metrics(oracle, case, want["rgb"], want["depth"], want)
+    assert m["rgb_max_abs"] == 0.0 and m["flip_px"] == 0 and gate(m)
+    d2 = want["depth"] * np.float32(1.3)
+    fl = flip_mask(oracle, case.target, case.ren_cams, want["depth"], d2)
+    assert fl.shape == want["depth"].shape[1:] and fl.any()
+
+
+@pytest.mark.parametrize("heads,M,zero", [(1, 4, False), (2, 8, False), (4, 16, False),
+                                          (2, 8, True)])
+def test_attend_residual_stage_matches_reference(oracle, reference, heads, M, zero):
+    """The oracle's attend_residual export (per-stage parity input, SURVEY.md
+    §7.2 step 1) is bit-identical to the reference's (attention.hpp:248-252)."""
+    import numpy as np
+    rng = np.random.default_rng(7 + heads + M)
+    P_, C = 777, 32
+    V = rng.standard_normal((P_, C)).astype(np.float32)
+    D = rng.standard_normal((P_, M, C)).astype(np.float32)
+    wq = (rng.standard_normal((heads, C, C)) / np.sqrt(C)).astype(np.float32)
+    wo = (0.1 * rng.standard_normal((heads * C, C)) / np.sqrt(heads * C)).astype(np.float32)
+    g = (1 + 0.1 * rng.standard_normal(C)).astype(np.float32)
+    a = oracle.attend_residual(V, D, wq, wo, g, zero)
+    b = reference.attend_residual(V, D, wq, wo, g, zero)
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert not np.array_equal(a, V)
+
+
+def test_render_to_view_stage_matches_reference(oracle, reference):
+    """The oracle's render_to_input_view export (ldm.hpp:223-244, the splat
+    into one input view) is bit-identical to the reference's, on the
+    oracle's own config-1 final volume."""
+    import numpy as np
+    from cases import config1
+    from paper_2411_16680_b200.qntc import param_names
+    case = config1()
+    V = oracle.forward_render(case.cfg, case.enc_images, case.enc_cams, None, None, case.target,
+                              case.flat(), outputs=("volume",))["volume"]
+    w = dict(zip(param_names(case.cfg), case.store()))
+    cam = case.enc_cams[1].scaled(48, 40)
+    a, bad = oracle.render_to_view(case.target, V, w["heads.w_appear"], w["heads.w_sigma"],
+                                   w["heads.w_depth"], cam)
+    b = reference.render_to_view(case.target, V, w["heads.w_appear"], w["heads.w_sigma"],
+                                 w["heads.w_depth"], cam)
+    assert not bad and a.shape == (40, 48, 33)
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert a[..., -1].max() > 0.5
