@@ -469,18 +469,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 template <int H, int M>
 void launch(float* V, const float* D, int64_t P, const float* wq, const float* wo,
             const float* gain, int zero, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attend_tc_kernel<H, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Smem<H>::BYTES);
-    attr = true;
-  }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  smem_optin(reinterpret_cast<const void*>(attend_tc_kernel<H, M>), Smem<H>::BYTES);
+  const int sms = sm_count();
   // V [P][32] fp32 as a 2-D map, 128-texel boxes (128B swizzle)
   CUtensorMap vmap, dmap;
   std::memset(&vmap, 0, sizeof(vmap));
@@ -514,6 +504,11 @@ void launch(float* V, const float* D, int64_t P, const float* wq, const float* w
 }
 
 }  // namespace
+
+bool attend_tc_supported(int C_, int M, int heads) {
+  return C_ == C && (heads == 1 || heads == 2 || heads == 4) &&
+         (M == 2 || M == 4 || M == 8 || M == 16);
+}
 
 bool attend_tc(float* V, const float* deltas, int64_t P, int C_, int M, int heads, const float* wq,
                const float* wo, const float* gain, int zero_scores, cudaStream_t st) {

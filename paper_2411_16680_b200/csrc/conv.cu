@@ -344,13 +344,10 @@ bool stem_supported(const ConvArgs& a) {
 int conv3x3_path(const ConvArgs& a, int impl) {
   static const int env = [] {
     const char* e = getenv("LVSG_CONV");
-    return !e ? 0 : e[0] == 's' ? 1 : e[0] == 'w' ? 3 : 0;  // simt | wino
+    return e && e[0] == 's' ? 1 : 0;  // LVSG_CONV=simt
   }();
-  // default: the direct tensor-core conv (the Winograd variant is measured
-  // slower end to end; LVSG_CONV=wino or impl 3 selects it)
   if (impl == 0) impl = env ? env : 2;
   if (impl == 1 || !conv3x3_tc_supported(a)) return 1;
-  if (impl == 3 && conv3x3_wino_supported(a)) return 3;
   return 2;
 }
 
@@ -358,9 +355,7 @@ bool conv3x3_uses_tc(const ConvArgs& a, int impl) { return conv3x3_path(a, impl)
 
 void conv3x3(const ConvArgs& a, cudaStream_t st, int impl) {
   const int path = conv3x3_path(a, impl);
-  if (path == 3) {
-    conv3x3_wino(a, st);  // computes the rms-norm input scale itself
-  } else if (path == 2) {
+  if (path == 2) {
     conv3x3_tc(a, st);
   } else if (impl != 1 && stem_supported(a)) {
     const int64_t n = (int64_t)a.B * a.H * a.W;

@@ -476,18 +476,6 @@ void conv3x3_tc_prepare(const ConvArgs& a, void* dst, cudaStream_t st) {
 void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
   if (!a.wsplit || (reinterpret_cast<uintptr_t>(a.wsplit) & 15))
     throw CudaError("conv3x3_tc: missing or misaligned weight image (conv3x3_tc_prepare)");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(conv3x3_tc_kernel<false, 0>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(conv3x3_tc_kernel<true, 0>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(conv3x3_tc_kernel<false, 1>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(conv3x3_tc_kernel<false, 2>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    attr = true;
-  }
   const ConvSrc& S = a.src[0];
   const CUtensorMap xmap =
       make_map(S.ptr, S.pstride, S.bstride, a.W, a.H, a.B, HWD, HHT, CU_TENSOR_MAP_SWIZZLE_NONE);
@@ -497,12 +485,7 @@ void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
                                               TW, SUB_ROWS, CU_TENSOR_MAP_SWIZZLE_128B)
                                    : omap;
   const int tiles = a.B * ((a.H + TH - 1) / TH) * ((a.W + TW - 1) / TW);
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = sm_count();
   const int grid = tiles < sms ? tiles : sms;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -518,6 +501,7 @@ void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
               : a.pool_out && a.npool_peer > 0 ? conv3x3_tc_kernel<false, 2>
               : a.pool_out                    ? conv3x3_tc_kernel<false, 1>
                                               : conv3x3_tc_kernel<false, 0>;
+  smem_optin(reinterpret_cast<const void*>(kern), SMEM_BYTES);
   if (a.alpha && a.pool_out) throw CudaError("conv3x3_tc: alpha and pool together are not built");
   if (cudaLaunchKernelEx(&cfg, kern, xmap, omap, rmap, a, tiles) != cudaSuccess)
     throw CudaError("conv3x3_tc: launch failed");

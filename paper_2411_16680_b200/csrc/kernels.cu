@@ -3,7 +3,12 @@
 // One-to-many attention / blend-logit / layer-collapse MLPs.
 #include <cfloat>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <set>
+#include <string>
 
+#include "host.h"
 #include "kernels.h"
 
 namespace lvsg {
@@ -21,6 +26,42 @@ bool pdl_all() {
     return e && e[0] == '2';
   }();
   return on;
+}
+
+namespace {
+std::mutex g_dev_mu;
+std::set<std::pair<int, const void*>> g_optin;  // (device, kernel) opted in
+std::map<int, int> g_sms;
+int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) throw CudaError("cudaGetDevice failed");
+  return d;
+}
+}  // namespace
+
+void smem_optin(const void* kernel, int bytes) {
+  const int d = current_device();
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (!g_optin.insert({d, kernel}).second) return;
+  const cudaError_t e =
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) {
+    g_optin.erase({d, kernel});
+    throw CudaError(std::string("cudaFuncSetAttribute(MaxDynamicSharedMemorySize): ") +
+                    cudaGetErrorString(e));
+  }
+}
+
+int sm_count() {
+  const int d = current_device();
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto it = g_sms.find(d);
+  if (it != g_sms.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || n < 1)
+    throw CudaError("cudaDeviceGetAttribute(MultiProcessorCount) failed");
+  g_sms[d] = n;
+  return n;
 }
 
 namespace {
@@ -551,286 +592,10 @@ __global__ void decode_payload_kernel(const float* __restrict__ V, int L, int H,
   }
 }
 
-__device__ __forceinline__ void red_add_v4(float* p, float4 v) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y),
-               "f"(v.z), "f"(v.w)
-               : "memory");
-}
-
-// One thread per (texel, view, 4-channel group): the texel's bilinear
-// footprint in the view (f64, shared rule with the gather) and four
-// vector reductions red.global.add.v4.f32 of (w_k * payload, w_k) into the
-// padded accumulator rows [.., acc_stride(K)] (geometry.hpp:245-263).
-__global__ void splat_kernel(const float* __restrict__ payload, const float* __restrict__ points,
-                             int L, int PL, int K, const DevCam* __restrict__ cams, int M, int Hv,
-                             int Wv, float* acc) {
-  pdl_grid_sync();
-  const int PS = pay_stride(K), S = acc_stride(K), G = S / 4;
-  const int64_t P = (int64_t)L * PL;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= P * M * G) return;
-  const int g = int(i % G);
-  const int64_t t = i / G;
-  const int m = int(t % M);
-  const int64_t p = t / M;
-  const int l = int(p / PL);
-  const float pt[3] = {points[p * 3], points[p * 3 + 1], points[p * 3 + 2]};
-  const Footprint f = project_footprint(cams[m], pt);
-  if (!f.valid) return;
-  double w[4];
-  bilinear_weights(f, w);
-  float val[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int c = 4 * g + k;
-    val[k] = c < K ? __ldg(payload + p * PS + c) : (c == K ? 1.0f : 0.0f);
-  }
-  const int64_t base = (int64_t)m * L * Hv * Wv + (int64_t)l * Hv * Wv;
-  const int64_t tap[4] = {base + (int64_t)f.y0 * Wv + f.x0, base + (int64_t)f.y0 * Wv + f.x1,
-                          base + (int64_t)f.y1 * Wv + f.x0, base + (int64_t)f.y1 * Wv + f.x1};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float wk = __double2float_rn(w[k]);
-    red_add_v4(acc + tap[k] * S + 4 * g,
-               make_float4(fm(wk, val[0]), fm(wk, val[1]), fm(wk, val[2]), fm(wk, val[3])));
-  }
-}
-
-// Cooperative splat: lane r of a warp projects (texel, view) pair r of the
-// warp's 32 (the f64 footprint once per pair, not once per channel group);
-// the warp then deals the 32 x G (pair, group) items round-robin, so lanes
-// with consecutive groups of one pair reduce into one contiguous accumulator
-// row. Same values and reduction targets as splat_kernel.
-__global__ void __launch_bounds__(256) splat_coop_kernel(const float* __restrict__ payload,
-                                                         const float* __restrict__ points, int L,
-                                                         int PL, int K,
-                                                         const DevCam* __restrict__ cams, int M,
-                                                         int Hv, int Wv, float* acc) {
-  pdl_grid_sync();
-  const int PS = pay_stride(K), S = acc_stride(K), G = S / 4;
-  const int64_t P = (int64_t)L * PL;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // pair (p, m), m fastest
-  const int lane = threadIdx.x & 31;
-  int ok = 0, pp = 0, tb = 0, dx = 0, dy = 0;
-  float w[4] = {0.f, 0.f, 0.f, 0.f};
-  if (i < P * M) {
-    const int m = int(i % M);
-    const int64_t p = i / M;
-    const int l = int(p / PL);
-    const float pt[3] = {points[p * 3], points[p * 3 + 1], points[p * 3 + 2]};
-    const Footprint f = project_footprint(cams[m], pt);
-    if (f.valid) {
-      double wd[4];
-      bilinear_weights(f, wd);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) w[k] = __double2float_rn(wd[k]);
-      ok = 1;
-      pp = int(p);
-      tb = int(((int64_t)m * L + l) * Hv * Wv + (int64_t)f.y0 * Wv + f.x0);
-      dx = f.x1 - f.x0;
-      dy = (f.y1 - f.y0) * Wv;
-    }
-  }
-  const int items = 32 * G;
-  for (int j = lane; j - lane < items; j += 32) {
-    const int r = j / G, g = j - r * G;  // r < 32 for j < items
-    const int src = r < 32 ? r : 31;
-    const int rok = __shfl_sync(0xffffffffu, ok, src);
-    const int rp = __shfl_sync(0xffffffffu, pp, src);
-    const int rtb = __shfl_sync(0xffffffffu, tb, src);
-    const int rdx = __shfl_sync(0xffffffffu, dx, src);
-    const int rdy = __shfl_sync(0xffffffffu, dy, src);
-    float rw[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) rw[k] = __shfl_sync(0xffffffffu, w[k], src);
-    if (j >= items || !rok) continue;
-    float val[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int c = 4 * g + k;
-      val[k] = c < K ? __ldg(payload + (int64_t)rp * PS + c) : (c == K ? 1.0f : 0.0f);
-    }
-    const int tap[4] = {rtb, rtb + rdx, rtb + rdy, rtb + rdy + rdx};
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      red_add_v4(acc + (int64_t)tap[k] * S + 4 * g,
-                 make_float4(fm(rw[k], val[0]), fm(rw[k], val[1]), fm(rw[k], val[2]),
-                             fm(rw[k], val[3])));
-  }
-}
-
-// One thread per (view pixel, 4-channel group): normalise by max(wsum,1e-4)
-// then composite back to front (geometry.hpp:317-326; ldm.hpp:98-115).
-// Output rows are padded to pay_stride(K) (channels K.. are zero).
-__global__ void splat_composite_kernel(const float* __restrict__ acc, int M, int L, int Hv, int Wv,
-                                       int K, float* out) {
-  pdl_grid_sync();
-  const int PS = pay_stride(K), S = acc_stride(K), G = PS / 4;
-  const int64_t PV = (int64_t)Hv * Wv;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= (int64_t)M * PV * G) return;
-  const int g = int(i % G);
-  const int64_t t = i / G;
-  const int64_t pix = t % PV;
-  const int m = int(t / PV);
-  const int Ca = K - 1;
-  float o[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int l = 0; l < L; ++l) {
-    const float* a = acc + (((int64_t)m * L + l) * PV + pix) * S;
-    const float ws = __ldg(a + K);
-    const float n = __fdiv_rn(1.0f, ws > 1e-4f ? ws : 1e-4f);
-    const float s = fm(__ldg(a + Ca), n);
-    const float4 v4 = __ldg(reinterpret_cast<const float4*>(a) + g);
-    const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int c = 4 * g + k;
-      const float v = c < Ca ? fm(vv[k], n) : 1.0f;
-      o[k] = fa(fm(v, s), fm(fsb(1.0f, s), o[k]));
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-    if (4 * g + k >= K) o[k] = 0.f;
-  reinterpret_cast<float4*>(out)[t * G + g] = make_float4(o[0], o[1], o[2], o[3]);
-}
 
 // ----------------------------------------------------------------------------
 // Stage 2: One-to-many attention, blend logits, layer collapse
 // ----------------------------------------------------------------------------
-
-// One thread per texel. Weights in shared memory (broadcast reads). Per head
-// i: s = n W_q[i]; logits_m = <s, Δ_m>/sqrt(C); softmax over views (max,
-// exp, sum, *1/sum as tape.hpp:390-404); head = sum_m w_m Δ_m; the output
-// projection accumulates head by head (== cat W_O with k ascending).
-template <int C, int M>
-__global__ void __launch_bounds__(128) attend_kernel(float* V, const float* __restrict__ D,
-                                                     int64_t P, int heads,
-                                                     const float* __restrict__ wq,
-                                                     const float* __restrict__ wo,
-                                                     const float* __restrict__ gain,
-                                                     int zero_scores) {
-  pdl_grid_sync();
-  extern __shared__ __align__(16) float smem[];
-  float* s_wq = smem;                    // [heads][C][C]
-  float* s_wo = smem + heads * C * C;    // [heads*C][C]
-  for (int e = threadIdx.x; e < heads * C * C; e += blockDim.x) {
-    s_wq[e] = wq[e];
-    s_wo[e] = wo[e];
-  }
-  __syncthreads();
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (p >= P) return;
-  float n[C];
-  {
-    const float4* vr = reinterpret_cast<const float4*>(V + p * C);
-    float ms = 0.f;
-#pragma unroll
-    for (int k = 0; k < C / 4; ++k) {
-      const float4 t = vr[k];
-      n[4 * k] = t.x, n[4 * k + 1] = t.y, n[4 * k + 2] = t.z, n[4 * k + 3] = t.w;
-    }
-#pragma unroll
-    for (int k = 0; k < C; ++k) ms = fmaf(n[k], n[k], ms);
-    const float r = __fdiv_rn(1.0f, __fsqrt_rn(fa(__fdiv_rn(ms, float(C)), 1e-6f)));
-#pragma unroll
-    for (int k = 0; k < C; ++k) n[k] = fm(fm(n[k], r), __ldg(gain + k));
-  }
-  const float inv_temp = __double2float_rn(1.0 / sqrt(double(C)));
-  const float4* d4 = reinterpret_cast<const float4*>(D) + p;  // Δ[m][g][p][4]
-  float out[C];
-#pragma unroll
-  for (int c = 0; c < C; ++c) out[c] = 0.f;
-  float w[M];
-  for (int h = 0; h < heads; ++h) {
-    if (zero_scores) {
-      const float u = __fdiv_rn(1.0f, float(M));
-#pragma unroll
-      for (int m = 0; m < M; ++m) w[m] = u;
-    } else {
-      float s[C];
-#pragma unroll
-      for (int c = 0; c < C; ++c) s[c] = 0.f;
-      const float* wh = s_wq + h * C * C;
-#pragma unroll
-      for (int k = 0; k < C; ++k) {
-        const float nk = n[k];
-#pragma unroll
-        for (int c4 = 0; c4 < C / 4; ++c4) {
-          const float4 wv = reinterpret_cast<const float4*>(wh + k * C)[c4];
-          s[4 * c4] = fmaf(nk, wv.x, s[4 * c4]);
-          s[4 * c4 + 1] = fmaf(nk, wv.y, s[4 * c4 + 1]);
-          s[4 * c4 + 2] = fmaf(nk, wv.z, s[4 * c4 + 2]);
-          s[4 * c4 + 3] = fmaf(nk, wv.w, s[4 * c4 + 3]);
-        }
-      }
-      float mx = -FLT_MAX;
-#pragma unroll
-      for (int m = 0; m < M; ++m) {
-        const float4* dm4 = d4 + (int64_t)m * (C / 4) * P;
-        float acc = 0.f;
-#pragma unroll
-        for (int c4 = 0; c4 < C / 4; ++c4) {
-          const float4 t = __ldg(dm4 + c4 * P);
-          acc = fmaf(s[4 * c4], t.x, acc);
-          acc = fmaf(s[4 * c4 + 1], t.y, acc);
-          acc = fmaf(s[4 * c4 + 2], t.z, acc);
-          acc = fmaf(s[4 * c4 + 3], t.w, acc);
-        }
-        w[m] = fm(acc, inv_temp);
-        mx = m == 0 ? w[m] : fmaxf(mx, w[m]);
-      }
-      float sum = 0.f;
-#pragma unroll
-      for (int m = 0; m < M; ++m) {
-        w[m] = expf(fsb(w[m], mx));
-        sum = fa(sum, w[m]);
-      }
-      const float inv = __fdiv_rn(1.0f, sum);
-#pragma unroll
-      for (int m = 0; m < M; ++m) w[m] = fm(w[m], inv);
-    }
-    float hd[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) hd[c] = 0.f;
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
-      const float4* dm4 = d4 + (int64_t)m * (C / 4) * P;
-      const float wm = w[m];
-#pragma unroll
-      for (int c4 = 0; c4 < C / 4; ++c4) {
-        const float4 t = __ldg(dm4 + c4 * P);
-        hd[4 * c4] = fmaf(wm, t.x, hd[4 * c4]);
-        hd[4 * c4 + 1] = fmaf(wm, t.y, hd[4 * c4 + 1]);
-        hd[4 * c4 + 2] = fmaf(wm, t.z, hd[4 * c4 + 2]);
-        hd[4 * c4 + 3] = fmaf(wm, t.w, hd[4 * c4 + 3]);
-      }
-    }
-    const float* wo_h = s_wo + h * C * C;
-#pragma unroll
-    for (int k = 0; k < C; ++k) {
-      const float hk = hd[k];
-#pragma unroll
-      for (int c4 = 0; c4 < C / 4; ++c4) {
-        const float4 wv = reinterpret_cast<const float4*>(wo_h + k * C)[c4];
-        out[4 * c4] = fmaf(hk, wv.x, out[4 * c4]);
-        out[4 * c4 + 1] = fmaf(hk, wv.y, out[4 * c4 + 1]);
-        out[4 * c4 + 2] = fmaf(hk, wv.z, out[4 * c4 + 2]);
-        out[4 * c4 + 3] = fmaf(hk, wv.w, out[4 * c4 + 3]);
-      }
-    }
-  }
-  float4* vw = reinterpret_cast<float4*>(V + p * C);
-#pragma unroll
-  for (int k = 0; k < C / 4; ++k) {
-    float4 t = vw[k];
-    t.x = fa(t.x, out[4 * k]);
-    t.y = fa(t.y, out[4 * k + 1]);
-    t.z = fa(t.z, out[4 * k + 2]);
-    t.w = fa(t.w, out[4 * k + 3]);
-    vw[k] = t;
-  }
-}
 
 // Generic-C fallback of the same arithmetic (small channel counts in tests).
 __global__ void attend_generic_kernel(float* V, const float* __restrict__ D, int64_t P, int C,
@@ -1183,12 +948,6 @@ void gather_stack(const float* feats, int M, int Hf, int Wf, int C, const DevCam
                   cudaStream_t st) {
   const bool v4 = C % 4 == 0;
   const int64_t n = (int64_t)L * H * W * M;
-  static const bool tiled = [] {  // LVSG_GATHER=tile: shared-memory windows (gather_tile.cu)
-    const char* e = getenv("LVSG_GATHER");
-    return e && e[0] == 't';
-  }();
-  if (tiled && gather_tile32(feats, M, Hf, Wf, C, cams_dev, rc, depth, L, H, W, deltas, st))
-    return;
   if (C == 32 && (int64_t)M * Hf * Wf * 8 < (int64_t(1) << 31) && n < (int64_t(1) << 31)) {
     launch_k(gather_stack32_kernel, blocks_for(n, 256), 256, 0, st, feats, M, Hf, Wf, cams_dev, rc,
                                                               depth, L, H, W, deltas);
@@ -1209,24 +968,6 @@ void decode_payload(const float* V, int L, int H, int W, int C, const float* w_a
   const int64_t P = (int64_t)L * H * W;
   launch_k(decode_payload_kernel, blocks_for(P, 128), 128, C * (Ca + 2) * sizeof(float), st, 
       V, L, H, W, C, w_appear, Ca, w_sigma, w_depth, act, rc, payload, depth, points);
-}
-void splat(const float* payload, const float* points, int L, int PL, int K, const DevCam* cams_dev,
-           int M, int Hv, int Wv, float* acc, cudaStream_t st) {
-  const int64_t pairs = (int64_t)L * PL * M;
-  if (acc_stride(K) / 4 <= 32 && pairs < (int64_t(1) << 31) &&
-      (int64_t)M * L * Hv * Wv < (int64_t(1) << 31)) {
-    launch_k(splat_coop_kernel, blocks_for(pairs, 256), 256, 0, st, payload, points, L, PL, K, cams_dev, M,
-                                                              Hv, Wv, acc);
-    return;
-  }
-  const int64_t n = pairs * (acc_stride(K) / 4);
-  launch_k(splat_kernel, blocks_for(n, 256), 256, 0, st, payload, points, L, PL, K, cams_dev, M, Hv, Wv,
-                                                   acc);
-}
-void splat_composite(const float* acc, int M, int L, int Hv, int Wv, int K, float* out,
-                     cudaStream_t st) {
-  const int64_t n = (int64_t)M * Hv * Wv * (pay_stride(K) / 4);
-  launch_k(splat_composite_kernel, blocks_for(n, 256), 256, 0, st, acc, M, L, Hv, Wv, K, out);
 }
 
 __global__ void deltas_to_soa_kernel(const float* __restrict__ src, float* __restrict__ dst,
@@ -1253,32 +994,16 @@ void deltas_to_soa(const float* src, float* dst, int64_t P, int M, int C, cudaSt
 }
 void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
             const float* const* wq_heads, const float* wo, const float* gain, int zero_scores,
-            cudaStream_t st) {
+            float* scratch, cudaStream_t st) {
   (void)wq_heads;
-  static const bool simt = [] {
-    const char* e = getenv("LVSG_ATTN");
-    return e && e[0] == 's';  // LVSG_ATTN=simt forces the SIMT kernel
-  }();
-  if (!simt && attend_tc(V, deltas, P, C, M, heads, wq, wo, gain, zero_scores, st)) return;
-  const size_t smem = 2 * size_t(heads) * C * C * sizeof(float);
-  auto launch = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    launch_k(kern, blocks_for(P, 128), 128, smem, st, V, deltas, P, heads, wq, wo, gain, zero_scores);
-  };
-  if (C == 32 && M == 8 && smem <= 200 * 1024) {
-    launch(attend_kernel<32, 8>);
-  } else if (C == 32 && M == 16 && smem <= 200 * 1024) {
-    launch(attend_kernel<32, 16>);
-  } else if (C == 32 && M == 4 && smem <= 200 * 1024) {
-    launch(attend_kernel<32, 4>);
-  } else {
-    // scratch: 4C floats per texel, carved from the caller-visible heap
-    float* scratch = nullptr;
-    cudaMallocAsync(&scratch, size_t(P) * 4 * C * sizeof(float), st);
-    launch_k(attend_generic_kernel, blocks_for(P, 128), 128, 0, st, V, deltas, P, C, M, heads, wq, wo,
-                                                              gain, zero_scores, scratch);
-    cudaFreeAsync(scratch, st);
-  }
+  if (attend_tc(V, deltas, P, C, M, heads, wq, wo, gain, zero_scores, st)) return;
+  // generic fallback: 4C floats of scratch per texel (attend_scratch_floats)
+  if (!scratch) throw CudaError("attend: no arena scratch for the generic kernel");
+  launch_k(attend_generic_kernel, blocks_for(P, 128), 128, 0, st, V, deltas, P, C, M, heads, wq, wo,
+                                                            gain, zero_scores, scratch);
+}
+size_t attend_scratch_floats(int64_t P, int C, int M, int heads) {
+  return attend_tc_supported(C, M, heads) ? 0 : size_t(P) * 4 * C;
 }
 void blend_logits(const float* V, const float* deltas, int64_t P, int C, int M,
                   const float* blend_w, const float* gain, float* logits, cudaStream_t st,

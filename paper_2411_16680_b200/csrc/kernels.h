@@ -27,6 +27,13 @@ __device__ __forceinline__ void pdl_grid_sync() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// Opts `kernel` into `bytes` of dynamic shared memory on the CURRENT device,
+// once per (device, kernel); thread-safe (a process may drive several GPUs
+// and several contexts from several threads).
+void smem_optin(const void* kernel, int bytes);
+// Multiprocessor count of the current device (cached per device).
+int sm_count();
+
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t st, Args... args) {
@@ -121,14 +128,8 @@ void conv3x3_tc(const ConvArgs& a, cudaStream_t st);
 // memory layout, loaded by one bulk copy per CTA.
 constexpr size_t kConvTcWeightBytes = 9 * 4 * 64 * 16;
 void conv3x3_tc_prepare(const ConvArgs& a, void* dst, cudaStream_t st);
-// 1-D Winograd F(2,3) tensor-core conv (conv_wino.cu): same shapes as
-// conv3x3_tc; its weight image holds G g per (xi, dy) (48 KB).
-bool conv3x3_wino_supported(const ConvArgs& a);
-void conv3x3_wino(const ConvArgs& a, cudaStream_t st);
-constexpr size_t kConvWinoWeightBytes = 4 * 3 * 4 * 64 * 16;
-void conv3x3_wino_prepare(const ConvArgs& a, void* dst, cudaStream_t st);
-// Which conv runs: 1 SIMT / stem, 2 direct tensor core, 3 Winograd tensor core
-// (impl: 0 auto = direct tensor core where supported; LVSG_CONV=simt|wino).
+// Which conv runs: 1 SIMT / stem, 2 tensor core (impl: 0 auto = tensor core
+// where supported; LVSG_CONV=simt forces the SIMT kernel).
 int conv3x3_path(const ConvArgs& a, int impl = 0);
 
 // ---- elementwise / layout ------------------------------------------------
@@ -168,11 +169,6 @@ void ray_project(const float* base, int M, int hK, int wK, int Hk, int Wk, const
 void gather_stack(const float* feats, int M, int Hf, int Wf, int C, const DevCam* cams_dev,
                   const DevRayCam& rc, const float* depth, int L, int H, int W, float* deltas,
                   cudaStream_t st);
-// The same for C = 32 with the feature windows staged in shared memory by
-// bulk async copies (gather_tile.cu); false when the shape does not apply.
-bool gather_tile32(const float* feats, int M, int Hf, int Wf, int C, const DevCam* cams_dev,
-                   const DevRayCam& rc, const float* depth, int L, int H, int W, float* deltas,
-                   cudaStream_t st);
 
 // Per-pixel strides of the render-to-input-view buffers, padded to 16 bytes
 // so every row moves as float4 / vector atomics and feeds TMA: the payload
@@ -190,33 +186,30 @@ void decode_payload(const float* V, int L, int H, int W, int C, const float* w_a
                     const float* w_sigma, const float* w_depth, const DepthAct& da,
                     const DevRayCam& rc, float* payload, float* depth, float* points,
                     cudaStream_t st, const float* w_host = nullptr);
-// splat_accumulate (geometry.hpp:230-264) of payload [L*H*W, K] into every
-// view: acc [M, L, Hv, Wv, K+1] (atomics; zeroed by the caller).
-void splat(const float* payload, const float* points, int L, int PL, int K, const DevCam* cams_dev,
-           int M, int Hv, int Wv, float* acc, cudaStream_t st);
-// Deterministic splat + normalise + composite (splat_det.cu): the same
-// result as splat + splat_composite, summed per view pixel in the
-// reference's order (bit-identical from run to run). scratch holds
+// splat_accumulate (geometry.hpp:230-264) + normalise + composite
+// (splat_det.cu): every view pixel sums its taps in the reference's order
+// (bit-identical from run to run). scratch holds
 // splat_det_scratch_ints(L*PL*M, M*L*Hv*Wv) ints.
 size_t splat_det_scratch_ints(int64_t pairs, int64_t bins);
 void splat_det(const float* payload, const float* points, int L, int PL, int K,
                const DevCam* cams_dev, int M, int Hv, int Wv, int* scratch, float* out,
                cudaStream_t st);
-// normalise (splat_project) + over_composite colour and alpha
-// (ldm.hpp:236-243): acc -> out [M, Hv, Wv, K] (K-1 colour + alpha).
-void splat_composite(const float* acc, int M, int L, int Hv, int Wv, int K, float* out,
-                     cudaStream_t st);
 
 // ---- attention / fusion ----------------------------------------------------
 // Δ from the reference layout [P, M, C] (network.hpp:421-436) into the
 // kernels' view-major SoA [M][ceil(C/4)][P][4] (stage entry points).
 void deltas_to_soa(const float* src, float* dst, int64_t P, int M, int C, cudaStream_t st);
-// V += OTM(rms_norm(V), Δ) (attention.hpp:207-252), in place.
+// V += OTM(rms_norm(V), Δ) (attention.hpp:207-252), in place. scratch:
+// attend_scratch_floats(P, C, M, heads) floats of device memory from the
+// caller's arena (the generic fallback's per-texel rows; none for the
+// tensor-core kernel).
 void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
             const float* const* wq_heads, const float* wo, const float* gain, int zero_scores,
-            cudaStream_t st);
-// tcgen05 3xTF32 fused attention (attn_tc.cu): C = 32, h in {1,2,4},
-// M in {4,8,16}; returns false otherwise.
+            float* scratch, cudaStream_t st);
+size_t attend_scratch_floats(int64_t P, int C, int M, int heads);
+// tcgen05 fused attention (attn_tc.cu): C = 32, h in {1,2,4},
+// M in {2,4,8,16}; returns false otherwise.
+bool attend_tc_supported(int C, int M, int heads);
 bool attend_tc(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
                const float* wo, const float* gain, int zero_scores, cudaStream_t st);
 // logits [P, M] = <rms_norm(V,g) W_blend, Δ_m> / sqrt(C) (network.hpp:539-549).

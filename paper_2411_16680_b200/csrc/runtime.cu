@@ -26,7 +26,6 @@
 
 namespace lvsg {
 
-int64_t g_launches = 0;  // incremented by every kernel launcher
 
 namespace {
 
@@ -171,7 +170,7 @@ struct lvsg_ctx {
   lvsg::Buf enc_in, ren_in, rgb, enc_x, enc_t, ray_base;
   std::vector<lvsg::Buf> feats, rays;
   lvsg::Buf splat_scratch;  // deterministic splat: counts, runs, keys, footprints (ints)
-  lvsg::Buf V0, V1, deltas, t1, rinv, uh, ut, uu, payload, depth_in, points, depth_out, acc, fb,
+  lvsg::Buf V0, V1, deltas, t1, rinv, uh, ut, uu, payload, depth_in, points, depth_out, fb,
       fbr, pre_d, pre_s, logits, anchors, ldm_d, ldm_s, ldm_b;
   lvsg::Buf cams_dev;  // DevCam / RayBaseCam tables
   int* bad_flag = nullptr;
@@ -194,7 +193,8 @@ struct lvsg_ctx {
   int64_t L = 0, H = 0, Wd = 0, M = 0;
   lvsg_frustum target{};
   float* V = nullptr;
-  int64_t launches = 0;
+  int64_t launches = 0;      // kernels the last forward / render call launched
+  int64_t launch_total = 0;  // every launch on this context (mark())
 
   // optional per-stage device timing (lvsg_profile_*): one event after each
   // group of launches; consecutive events bound that group's device time
@@ -209,6 +209,7 @@ struct lvsg_ctx {
   std::map<std::tuple<const float*, int, int>, std::unique_ptr<lvsg::Buf>> wimg;
   lvsg::Buf wimg_tmp;  // uncached image for the stage entry points
   lvsg::Buf stage_a, stage_b, stage_c, stage_cams;  // scratch of the per-stage entry points
+  lvsg::Buf attn_scratch;  // generic attention kernel rows (shapes without a tensor-core kernel)
   std::vector<float> stem_host;  // encoder stem weights [32*27] + bias [32] (host copy)
   std::vector<std::vector<float>> rayproj_host;  // per-level ray_proj [32, C] (host copies)
   std::vector<float> blendw_host;                // blend_w [C, C] (host copy)
@@ -227,7 +228,7 @@ thread_local std::string g_create_err;
 // Counts `n` kernel launches under `label`; when profiling, records an event
 // that closes the group on the context stream.
 void mark(lvsg_ctx* c, const char* label, int n) {
-  g_launches += n;
+  c->launch_total += n;  // per context: no shared counter across contexts / threads
   if (!c->prof) return;
   const size_t i = c->prof_labels.size();
   if (i >= c->prof_pool.size()) {
@@ -380,7 +381,7 @@ void ensure_plan(lvsg_ctx* c, int64_t He, int64_t We) {
     c->rays[size_t(k)].ensure(n);
   }
   c->ray_base.ensure(size_t(M * plan.pyramid.back().first * plan.pyramid.back().second * 32));
-  size_t maxV = 0, maxD = 0, maxU = 0, maxAcc = 0, maxFb = 0, maxIn = 0, maxSplat = 0;
+  size_t maxV = 0, maxD = 0, maxU = 0, maxFb = 0, maxIn = 0, maxSplat = 0;
   for (const StepPlan& sp : plan.steps) {
     maxV = std::max({maxV, size_t(sp.in_layers * sp.in_height * sp.in_width),
                      size_t(sp.layers * sp.height * sp.width)});
@@ -388,7 +389,6 @@ void ensure_plan(lvsg_ctx* c, int64_t He, int64_t We) {
     // Δ in the view-major SoA layout [M][ceil(C/4)][P][4]
     maxD = std::max(maxD, size_t(sp.layers * sp.height * sp.width * M * ((C + 3) / 4) * 4));
     maxU = std::max(maxU, size_t(M * sp.feat_h * sp.feat_w));
-    maxAcc = std::max(maxAcc, size_t(M * sp.layers * sp.render_h * sp.render_w * acc_stride(int(Ca) + 1)));
     // deterministic splat over the volume entering the step (at most
     // max(in_layers, layers) x in_height x in_width texels, all views):
     // bins = views x layers x render pixels
@@ -409,7 +409,6 @@ void ensure_plan(lvsg_ctx* c, int64_t He, int64_t We) {
   c->depth_in.ensure(maxIn);
   c->points.ensure(maxIn * 3);
   c->depth_out.ensure(maxV);
-  c->acc.ensure(maxAcc);
   c->splat_scratch.ensure(maxSplat);
   c->fb.ensure(maxFb);
   c->fbr.ensure(maxU * pay_stride(int(Ca) + 1));
@@ -457,16 +456,10 @@ ConvArgs conv_args(int B, int H, int W, int Cin, int Cout, const float* w, const
 void run_conv(lvsg_ctx* c, ConvArgs a, cudaStream_t st, int impl = 0, bool cached = true) {
   const int path = conv3x3_path(a, impl);
   if (path >= 2) {
-    const bool wino = path == 3;
-    const size_t nf = (wino ? kConvWinoWeightBytes : kConvTcWeightBytes) / sizeof(float);
-    auto prepare = [&](void* dst) {
-      if (wino)
-        conv3x3_wino_prepare(a, dst, st);
-      else
-        conv3x3_tc_prepare(a, dst, st);
-    };
+    const size_t nf = kConvTcWeightBytes / sizeof(float);
+    auto prepare = [&](void* dst) { conv3x3_tc_prepare(a, dst, st); };
     if (cached) {
-      auto key = std::make_tuple(a.w, w_cin_of(a), a.w_ci0 + (wino ? (1 << 20) : 0));
+      auto key = std::make_tuple(a.w, w_cin_of(a), a.w_ci0);
       auto it = c->wimg.find(key);
       a.pdl = 1;
       if (it == c->wimg.end()) {
@@ -596,8 +589,11 @@ void update_cnn(lvsg_ctx* c, const StepW& sw, const ConvArgs& stem_in, int M, in
 void fusion(lvsg_ctx* c, float* V, int64_t L, int64_t H, int64_t W, const FusionW& f) {
   const int C = int(c->cfg.channels), M = int(c->cfg.views);
   const int64_t P = L * H * W;
+  // the generic kernel's scratch (none for the tensor-core shapes) grows
+  // the arena once, on the first frame of a plan
+  c->attn_scratch.ensure(attend_scratch_floats(P, C, M, f.heads));
   attend(V, c->deltas.p, P, C, M, f.heads, f.wq, nullptr, f.wo, f.gain, c->cfg.ablate_attention,
-         c->stream);
+         c->attn_scratch.p, c->stream);
   mark(c, "attention", 1);
   for (const MlpW& m : f.mlps) {
     // conv_mlp_residual (attention.hpp:262-267), batched over layers
@@ -779,7 +775,7 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
   const int K = int(cfg.pyramid_levels);
   cudaStream_t st = c->stream;
   const NetW& W = c->W;
-  const int64_t launches0 = g_launches;
+  const int64_t launches0 = c->launch_total;
   if (c->prof) {
     prof_collect(c);
     mark(c, "start", 0);
@@ -865,20 +861,9 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
     if (cfg.ablate_render) {
       CUDA_OK(cudaMemsetAsync(c->fbr.p, 0, size_t(M) * Hf * Wf * PS * sizeof(float), st));
     } else {
-      static const bool atomic_splat = [] {
-        const char* e = getenv("LVSG_SPLAT");
-        return e && e[0] == 'a';  // LVSG_SPLAT=atomic: the fp32-atomics splat (A/B runs)
-      }();
-      if (atomic_splat) {
-        CUDA_OK(cudaMemsetAsync(c->acc.p, 0, size_t(M) * L * Hv * Wv * acc_stride(Kp) * sizeof(float), st));
-        splat(c->payload.p, c->points.p, int(L), int(H * Wd), Kp, cams.rend[s], M, Hv, Wv, c->acc.p, st);
-        splat_composite(c->acc.p, M, int(L), Hv, Wv, Kp, c->fb.p, st);
-        mark(c, "splat", 2);
-      } else {
-        splat_det(c->payload.p, c->points.p, int(L), int(H * Wd), Kp, cams.rend[s], M, Hv, Wv,
-                  reinterpret_cast<int*>(c->splat_scratch.p), c->fb.p, st);
-        mark(c, "splat", 6);
-      }
+      splat_det(c->payload.p, c->points.p, int(L), int(H * Wd), Kp, cams.rend[s], M, Hv, Wv,
+                reinterpret_cast<int*>(c->splat_scratch.p), c->fb.p, st);
+      mark(c, "splat", 6);
       if (sp.doubled) {
         resize_hwc(c->fb.p, c->fbr.p, M, Hv, Wv, PS, Hf, Wf, st);
         mark(c, "misc", 1);
@@ -933,7 +918,7 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
   c->M = M;
   c->target = target;
   c->V = V;
-  c->launches = g_launches - launches0;
+  c->launches = c->launch_total - launches0;
 }
 
 RenderArgs render_args(lvsg_ctx* c, const float* images, int64_t Hr, int64_t Wr,
@@ -1610,7 +1595,7 @@ lvsg_status lvsg_encode_device(lvsg_ctx* c, int64_t views, const float* enc_imag
     cudaStream_t user = static_cast<cudaStream_t>(stream);
     cudaStream_t own = c->stream;
     if (user) c->stream = user;
-    const int64_t launches0 = g_launches;
+    const int64_t launches0 = c->launch_total;
     try {
       if (view1 > view0) encode_views(c, enc_images, enc_h, enc_w, int(view0), int(view1));
       c->pyr_He = enc_h;
@@ -1621,7 +1606,7 @@ lvsg_status lvsg_encode_device(lvsg_ctx* c, int64_t views, const float* enc_imag
       throw;
     }
     c->stream = own;
-    c->launches = g_launches - launches0;
+    c->launches = c->launch_total - launches0;
   });
 }
 
@@ -1660,6 +1645,8 @@ lvsg_status lvsg_pyramid_import(lvsg_ctx* c, int64_t npeers, const uint8_t* hand
     }
     if (c->He <= 0) throw DimError("pyramid exchange: lvsg_pyramid_export first");
     const int64_t K = c->cfg.pyramid_levels;
+    int me = 0;
+    CUDA_OK(cudaGetDevice(&me));
     std::vector<std::vector<float*>> feats;
     for (int64_t q = 0; q < npeers; ++q) {
       std::vector<float*> lv;
@@ -1667,8 +1654,23 @@ lvsg_status lvsg_pyramid_import(lvsg_ctx* c, int64_t npeers, const uint8_t* hand
         cudaIpcMemHandle_t h;
         std::memcpy(&h, handles + (q * K + k) * 64, 64);
         void* p = nullptr;
-        CUDA_OK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+          cudaGetLastError();
+          throw CudaError(std::string("pyramid exchange: peer pyramid not mappable (") +
+                          cudaGetErrorString(e) + "); use the NCCL all-gather");
+        }
         c->peer_maps.push_back(p);
+        // the epilogue stores into this buffer directly: its device must be
+        // this one or a peer this device can write over NVLink
+        cudaPointerAttributes pa{};
+        CUDA_OK(cudaPointerGetAttributes(&pa, p));
+        int ok = 1;
+        if (pa.device != me) CUDA_OK(cudaDeviceCanAccessPeer(&ok, me, pa.device));
+        if (!ok)
+          throw CudaError("pyramid exchange: device " + std::to_string(me) +
+                          " has no peer access to device " + std::to_string(pa.device) +
+                          "; use the NCCL all-gather");
         lv.push_back(static_cast<float*>(p));
       }
       feats.push_back(std::move(lv));
@@ -1816,8 +1818,9 @@ lvsg_status lvsg_stage_attend(lvsg_ctx* c, float* V, const float* deltas, int64_
     const size_t n = size_t(P) * M * ((C + 3) / 4) * 4;
     c->stage_a.ensure(n + 128);
     deltas_to_soa(deltas, c->stage_a.p, P, int(M), C, c->stream);
+    c->attn_scratch.ensure(attend_scratch_floats(P, C, int(M), int(heads)));
     attend(V, c->stage_a.p, P, C, int(M), int(heads), wq, nullptr, wo, gain, zero_scores,
-           c->stream);
+           c->attn_scratch.p, c->stream);
     sync_and_check(c);
   });
 }

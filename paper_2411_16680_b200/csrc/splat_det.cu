@@ -272,186 +272,13 @@ __global__ void __launch_bounds__(288) splat_reduce_composite_kernel(
   reinterpret_cast<float4*>(out)[t * G + g] = make_float4(o[0], o[1], o[2], o[3]);
 }
 
-// The same reduction with one thread per (view m, pixel) holding all NG
-// float4 channel groups (NG = PS/4 compile-time; C = 32 configs: 9): the
-// run is loaded and sorted once per pixel instead of once per channel group,
-// and each entry issues NG independent 16-byte loads of its payload row.
-template <int NG>
-__global__ void __launch_bounds__(128) splat_reduce_px_kernel(
-    const float* __restrict__ payload, int K, int M, int L, int Hv, int Wv,
-    const int* __restrict__ off, const int* __restrict__ cnt, const int2* __restrict__ ent,
-    float* __restrict__ out) {
-  pdl_grid_sync();
-  const int64_t PV = (int64_t)Hv * Wv;
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // (m, pixel)
-  if (t >= (int64_t)M * PV) return;
-  const int64_t pix = t % PV;
-  const int m = int(t / PV);
-  const int Ca = K - 1;
-  const float4* pay4 = reinterpret_cast<const float4*>(payload);
-  float o[NG * 4];
-#pragma unroll
-  for (int c = 0; c < NG * 4; ++c) o[c] = 0.f;
-  for (int l = 0; l < L; ++l) {
-    float acc[NG * 4];
-#pragma unroll
-    for (int c = 0; c < NG * 4; ++c) acc[c] = 0.f;
-    float ws = 0.f;
-    auto add = [&](const int2 en) {
-      const float w = __int_as_float(en.y);
-      const float4* row = pay4 + (int64_t)(en.x >> 2) * NG;
-      float4 v[NG];
-#pragma unroll
-      for (int q = 0; q < NG; ++q) v[q] = __ldg(row + q);
-#pragma unroll
-      for (int q = 0; q < NG; ++q) {
-        acc[4 * q] = fa(acc[4 * q], fm(w, v[q].x));
-        acc[4 * q + 1] = fa(acc[4 * q + 1], fm(w, v[q].y));
-        acc[4 * q + 2] = fa(acc[4 * q + 2], fm(w, v[q].z));
-        acc[4 * q + 3] = fa(acc[4 * q + 3], fm(w, v[q].w));
-      }
-      ws = fa(ws, w);
-    };
-    const int64_t bin = ((int64_t)m * L + l) * PV + pix;
-    const int n = __ldg(cnt + bin), b0 = __ldg(off + bin);
-    if (n <= 4) {
-      int2 e[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) e[k] = k < n ? __ldg(ent + b0 + k) : make_int2(0x7fffffff, 0);
-      sort4(e);
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (k < n) add(e[k]);
-    } else {
-      int last = -1;  // ascending keys by repeated minimum search
-      for (int q = 0; q < n; ++q) {
-        int2 best = make_int2(0x7fffffff, 0);
-        for (int j = 0; j < n; ++j) {
-          const int2 ej = __ldg(ent + b0 + j);
-          if (ej.x > last && ej.x < best.x) best = ej;
-        }
-        last = best.x;
-        add(best);
-      }
-    }
-    // splat_project: * 1/max(wsum, eps); over_composite colour / alpha
-    const float nrm = __fdiv_rn(1.0f, ws > 1e-4f ? ws : 1e-4f);
-    float sa = 0.f;  // acc[Ca] without a dynamic register index
-#pragma unroll
-    for (int c = 0; c < NG * 4; ++c) sa = c == Ca ? acc[c] : sa;
-    const float s = fm(sa, nrm);
-#pragma unroll
-    for (int c = 0; c < NG * 4; ++c) {
-      const float v = c < Ca ? fm(acc[c], nrm) : 1.0f;
-      o[c] = fa(fm(v, s), fm(fsb(1.0f, s), o[c]));
-    }
-  }
-  float4* dst = reinterpret_cast<float4*>(out) + t * NG;
-#pragma unroll
-  for (int q = 0; q < NG; ++q)
-    dst[q] = make_float4(4 * q < K ? o[4 * q] : 0.f, 4 * q + 1 < K ? o[4 * q + 1] : 0.f,
-                         4 * q + 2 < K ? o[4 * q + 2] : 0.f, 4 * q + 3 < K ? o[4 * q + 3] : 0.f);
-}
-
-// One (view m, pixel) per three lanes for NG = 9 (C = 32 configs): lane q of
-// the triple owns channel groups 3q .. 3q+2 (a contiguous 48-byte third of
-// the 144-byte payload row, so the triple's loads coalesce); each warp
-// carries 10 pixels (lanes 30, 31 idle). The alpha channel's sum is taken
-// from the owning lane by a shuffle. Same additions, same order, as
-// splat_reduce_px_kernel.
-__global__ void __launch_bounds__(320, 2) splat_reduce_px3_kernel(
-    const float* __restrict__ payload, int K, int M, int L, int Hv, int Wv,
-    const int* __restrict__ off, const int* __restrict__ cnt, const int2* __restrict__ ent,
-    float* __restrict__ out) {
-  constexpr int NG = 9, NL = 3;  // channel groups per row, per lane
-  pdl_grid_sync();
-  const int64_t PV = (int64_t)Hv * Wv;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int tri = lane / 3, q = lane - tri * 3;
-  const int64_t t = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * 10 + tri;  // (m, pixel)
-  const bool live = lane < 30 && t < (int64_t)M * PV;
-  const int64_t pix = live ? t % PV : 0;
-  const int m = live ? int(t / PV) : 0;
-  const int Ca = K - 1;
-  const int src_lane = tri * 3 + (Ca / 4) / NL;  // the lane owning the alpha channel
-  const float4* pay4 = reinterpret_cast<const float4*>(payload);
-  float o[NL * 4];
-#pragma unroll
-  for (int c = 0; c < NL * 4; ++c) o[c] = 0.f;
-  for (int l = 0; l < L; ++l) {
-    float acc[NL * 4];
-#pragma unroll
-    for (int c = 0; c < NL * 4; ++c) acc[c] = 0.f;
-    float ws = 0.f;
-    auto add = [&](const int2 en) {
-      const float w = __int_as_float(en.y);
-      const float4* row = pay4 + (int64_t)(en.x >> 2) * NG + q * NL;
-      float4 v[NL];
-#pragma unroll
-      for (int k = 0; k < NL; ++k) v[k] = __ldg(row + k);
-#pragma unroll
-      for (int k = 0; k < NL; ++k) {
-        acc[4 * k] = fa(acc[4 * k], fm(w, v[k].x));
-        acc[4 * k + 1] = fa(acc[4 * k + 1], fm(w, v[k].y));
-        acc[4 * k + 2] = fa(acc[4 * k + 2], fm(w, v[k].z));
-        acc[4 * k + 3] = fa(acc[4 * k + 3], fm(w, v[k].w));
-      }
-      ws = fa(ws, w);
-    };
-    if (live) {
-      const int64_t bin = ((int64_t)m * L + l) * PV + pix;
-      const int n = __ldg(cnt + bin), b0 = __ldg(off + bin);
-      if (n <= 4) {
-        int2 e[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) e[k] = k < n ? __ldg(ent + b0 + k) : make_int2(0x7fffffff, 0);
-        sort4(e);
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (k < n) add(e[k]);
-      } else {
-        int last = -1;  // ascending keys by repeated minimum search
-        for (int r = 0; r < n; ++r) {
-          int2 best = make_int2(0x7fffffff, 0);
-          for (int j = 0; j < n; ++j) {
-            const int2 ej = __ldg(ent + b0 + j);
-            if (ej.x > last && ej.x < best.x) best = ej;
-          }
-          last = best.x;
-          add(best);
-        }
-      }
-    }
-    float mine = 0.f;  // this lane's value of channel Ca (if it owns it)
-#pragma unroll
-    for (int c = 0; c < NL * 4; ++c) mine = q * NL * 4 + c == Ca ? acc[c] : mine;
-    const float sa = __shfl_sync(0xffffffffu, mine, live ? src_lane : lane);
-    // splat_project: * 1/max(wsum, eps); over_composite colour / alpha
-    const float nrm = __fdiv_rn(1.0f, ws > 1e-4f ? ws : 1e-4f);
-    const float s = fm(sa, nrm);
-#pragma unroll
-    for (int c = 0; c < NL * 4; ++c) {
-      const float v = q * NL * 4 + c < Ca ? fm(acc[c], nrm) : 1.0f;
-      o[c] = fa(fm(v, s), fm(fsb(1.0f, s), o[c]));
-    }
-  }
-  if (!live) return;
-  float4* dst = reinterpret_cast<float4*>(out) + t * NG + q * NL;
-#pragma unroll
-  for (int k = 0; k < NL; ++k) {
-    const int c0 = q * NL * 4 + 4 * k;
-    dst[k] = make_float4(c0 < K ? o[4 * k] : 0.f, c0 + 1 < K ? o[4 * k + 1] : 0.f,
-                         c0 + 2 < K ? o[4 * k + 2] : 0.f, c0 + 3 < K ? o[4 * k + 3] : 0.f);
-  }
-}
-
 // One thread per (view m, pixel, layer): the run of a layer's bin is summed
 // in parallel across layers (the early steps have 24 layers over small view
 // images, where a thread per pixel walking the layers in sequence left the
 // SMs nearly empty); the normalised values go through shared memory and
 // the back-to-front composite then runs per (pixel, channel group) in the
 // reference's layer order. Same additions, same order, as
-// splat_reduce_px_kernel.
+// splat_reduce_composite_kernel.
 template <int NG>
 __global__ void __launch_bounds__(192) splat_reduce_pl_kernel(
     const float* __restrict__ payload, int K, int M, int L, int Hv, int Wv,
@@ -577,31 +404,12 @@ void splat_det(const float* payload, const float* points, int L, int PL, int K,
   launch_k(splat_fill_kernel, blocks_for(pairs, 256), 256, 0, st, pairs, M, (const int2*)fp_i,
            (const float4*)fp_w, cursor, ent);
   const int G = pay_stride(K) / 4;
-  if (G == 9) {
-    // LVSG_SPLAT_RED (A/B runs): 1 = one thread per pixel walking the layers,
-    // 3 = three lanes per pixel; default: one thread per (pixel, layer)
-    static const int variant = [] {
-      const char* e = getenv("LVSG_SPLAT_RED");
-      return e ? atoi(e) : 0;
-    }();
-    if (variant == 0 && L <= 192) {
-      const int ppb = std::max(1, 192 / L);
-      const size_t smem = size_t(ppb) * L * 36 * sizeof(float);
-      static bool attr = [] {
-        cudaFuncSetAttribute(splat_reduce_pl_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             192 * 36 * 4);
-        return true;
-      }();
-      (void)attr;
-      launch_k(splat_reduce_pl_kernel<9>, blocks_for((int64_t)M * Hv * Wv, ppb), ppb * L, smem, st,
-               payload, K, M, L, Hv, Wv, (const int*)off, (const int*)cnt, (const int2*)ent, out,
-               ppb);
-    } else if (variant != 3)
-      launch_k(splat_reduce_px_kernel<9>, blocks_for((int64_t)M * Hv * Wv, 128), 128, 0, st, payload,
-               K, M, L, Hv, Wv, (const int*)off, (const int*)cnt, (const int2*)ent, out);
-    else
-      launch_k(splat_reduce_px3_kernel, blocks_for((int64_t)M * Hv * Wv, 100), 320, 0, st, payload,
-               K, M, L, Hv, Wv, (const int*)off, (const int*)cnt, (const int2*)ent, out);
+  if (G == 9 && L <= 192) {  // C = 32 configs: one thread per (view pixel, layer)
+    const int ppb = std::max(1, 192 / L);
+    const size_t smem = size_t(ppb) * L * 36 * sizeof(float);
+    smem_optin(reinterpret_cast<const void*>(splat_reduce_pl_kernel<9>), 192 * 36 * 4);
+    launch_k(splat_reduce_pl_kernel<9>, blocks_for((int64_t)M * Hv * Wv, ppb), ppb * L, smem, st,
+             payload, K, M, L, Hv, Wv, (const int*)off, (const int*)cnt, (const int2*)ent, out, ppb);
     return;
   }
   const int ppb = std::max(1, std::min(kRedPixMax, 288 / G));

@@ -49,10 +49,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", nargs="+", default=["c4", "c5"])
     ap.add_argument("--out", default=None)
+    ap.add_argument("--self-runs", type=int, default=0,
+                    help="for each failing frame, re-run the oracle this many times with its "
+                         "inputs moved by one ulp (tests/parity_util.self_sensitivity)")
+    ap.add_argument("--save", default=None, help="directory for per-frame difference maps")
     a = ap.parse_args()
     import paper_2411_16680_b200 as q
     from bindings import Oracle
-    from parity_util import frame_metrics, gate
+    from parity_util import RGB_MAX_ABS, frame_metrics, gate, self_sensitivity
     oracle = Oracle()
     model = None
     fails = 0
@@ -74,6 +78,25 @@ def main():
         m = frame_metrics(oracle, case, rgb, depth, want)
         m["pass"] = gate(m)
         m["gpu_s"], m["oracle_s"] = round(t1 - t0, 2), round(t2 - t1, 2)
+        if not m["pass"] and a.self_runs:
+            gpx = np.abs(rgb - want["rgb"]).max(-1)
+            over = gpx > RGB_MAX_ABS
+            sens = np.zeros_like(over)
+            runs = []
+            maps = {"gpu_dpx": np.where(gpx > 1e-5, gpx, 0)}
+            for k in range(a.self_runs):
+                spx, sfl, _ = self_sensitivity(oracle, case, want, seed=1000 + 17 * k)
+                sens |= spx > 1e-4
+                maps[f"self{k}_dpx"] = np.where(spx > 1e-5, spx, 0)
+                runs.append({"max_abs": float(spx.max()), "px_gt_1e-3": int((spx > RGB_MAX_ABS).sum()),
+                             "px_gt_1e-4": int((spx > 1e-4).sum()), "flip_px": int(sfl.sum())})
+            m["self_runs"] = runs
+            # GPU pixels over the gate inside the reference's own one-ulp
+            # sensitivity region (pixels some perturbed oracle run moves by > 1e-4)
+            m["px_gt_1e-3_in_self_region"] = int((over & sens).sum())
+            if a.save:
+                os.makedirs(a.save, exist_ok=True)
+                np.savez_compressed(os.path.join(a.save, case.name + ".npz"), **maps)
         fails += not m["pass"]
         line = json.dumps(m)
         print(line, flush=True)

@@ -65,3 +65,26 @@ def gate(m):
     tolerance, and nothing above it off the flip pixels."""
     return (m["rgb_max_abs"] <= RGB_MAX_ABS and m["psnr_db"] >= RGB_PSNR_DB
             and m["px_gt_1e-3_unattributed"] == 0)
+
+
+def perturb_ulp(a, seed):
+    """Every element of the f32 array moved by one ulp up or down (random
+    sign, fixed seed): one rounding's worth of noise on the inputs."""
+    a = np.ascontiguousarray(a, np.float32)
+    up = np.random.default_rng(seed).random(a.shape) < 0.5
+    return np.where(up, np.nextafter(a, np.float32(np.inf)),
+                    np.nextafter(a, np.float32(-np.inf))).astype(np.float32)
+
+
+def self_sensitivity(oracle, case, want, seed):
+    """The reference's own conditioning at this frame: the oracle (bit-exact
+    with the reference) re-run with its weights and encoder images each moved
+    by one ulp, compared with its unperturbed frame `want`. Returns the
+    per-pixel max-abs change [Ho, Wo] and the final-render flip mask between
+    the two depth maps."""
+    got = oracle.forward_render(case.cfg, perturb_ulp(case.enc_images, seed), case.enc_cams,
+                                case.ren_images, case.ren_cams, case.target,
+                                perturb_ulp(case.flat(), seed + 1), outputs=("rgb", "depth"))
+    dpx = np.abs(got["rgb"] - want["rgb"]).max(-1)
+    flips = flip_mask(oracle, case.target, case.ren_cams, got["depth"], want["depth"])
+    return dpx, flips, got

@@ -370,16 +370,13 @@ m.close()
 """
 
 
-@pytest.mark.parametrize("env", [{"LVSG_GATHER": "tile"}, {"LVSG_GATHER": "tile1"},
-                                 {"LVSG_SPLAT_RED": "1"}, {"LVSG_SPLAT_RED": "3"},
-                                 {"LVSG_SPLAT": "atomic"}],
-                         ids=["gather_pipelined", "gather_window", "splat_reduce_pixel",
-                              "splat_reduce_3lane", "splat_atomic"])
+@pytest.mark.parametrize("env", [{"LVSG_CONV": "simt"}, {"LVSG_PDL": "0"}],
+                         ids=["conv_simt", "no_pdl"])
 def test_kernel_variants_match_default(tmp_path, env):
-    """The opt-in kernel variants (env-selected, one per process) against the
-    default path on 1/4-scale config 2: the gather windows and the splat
-    reduction layouts are bit-identical by construction; the atomic splat
-    differs only in accumulation order (RGB gate)."""
+    """Environment switches (one per process) against the default path on
+    1/4-scale config 2: the fp32 SIMT conv instead of the tcgen05 split
+    (RGB gate: a different summation) and launches without programmatic
+    dependent launch (bit-identical: only the launch attribute changes)."""
     import os
     import subprocess
     import sys
@@ -388,13 +385,13 @@ def test_kernel_variants_match_default(tmp_path, env):
     for name, extra in (("default", {}), ("variant", env)):
         path = str(tmp_path / f"{name}.npy")
         e = dict(os.environ)
-        for k in ("LVSG_GATHER", "LVSG_SPLAT", "LVSG_SPLAT_RED"):
+        for k in ("LVSG_CONV", "LVSG_PDL"):
             e.pop(k, None)
         e.update(extra)
         subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root, path], env=e, check=True,
                        timeout=600)
         outs[name] = np.load(path)
-    if env.get("LVSG_SPLAT") == "atomic":
+    if "LVSG_CONV" in env:
         assert float(np.abs(outs["default"] - outs["variant"]).max()) <= RGB_MAX_ABS
     else:
         assert np.array_equal(outs["default"].view(np.uint32), outs["variant"].view(np.uint32))
