@@ -85,13 +85,31 @@ def frame_work(cfg, He, We, Hr, Wr):
     last = plan.steps[-1]
     Pf = last.layers * last.height * last.width
     attn += Pf * (2 * C * C + 2 * M * C)  # blend head
+    # conv3x3 algorithmic HBM bytes: every conv reads its input channels once
+    # and writes its output once; the residual conv also reads the residual
+    # (conv_residual / conv_mlp_residual: conv1 2N, conv2 3N for N = one
+    # 32-channel map); the last encoder conv of a level also writes the pool
+    N = lambda px: px * C * 4  # noqa: E731
+    conv_bytes = M * He * We * 3 * 4 + N(M * He * We)  # stem
+    h, w = He, We
+    for _ in range(cfg.pyramid_levels):
+        conv_bytes += 2 * 5 * N(M * h * w) + N(M * (h // 2) * (w // 2))
+        h //= 2
+        w //= 2
+    for s, sp in enumerate(plan.steps):
+        px = M * sp.feat_h * sp.feat_w
+        cin = 2 * C if s == 0 else 2 * C + Ca + 1
+        conv_bytes += px * cin * 4 + N(px) + 2 * 5 * N(px)  # update_cnn stem + 2 pairs
+        nC = sum(1 for t in cfg.steps[s].blocks.split(",") if t.strip() == "C")
+        conv_bytes += nC * 5 * N(sp.layers * sp.height * sp.width)
     Ho, Wo = plan.out_height, plan.out_width
     # fused Stage 3 + 4: LDM pre-activation maps + M input images + output
     render_bytes = Pf * (2 + M) * 4 + M * Hr * Wr * 3 * 4 + Ho * Wo * 3 * 4
     gather_bytes = 0
     for s, sp in enumerate(plan.steps):
         gather_bytes += M * sp.feat_h * sp.feat_w * C * 4 + sp.layers * sp.height * sp.width * (4 + M * C * 4)
-    return {"conv_flops": conv, "attn_flops": attn, "render_bytes": render_bytes,
+    return {"conv_flops": conv, "conv_bytes": conv_bytes, "attn_flops": attn,
+            "render_bytes": render_bytes,
             "gather_bytes": gather_bytes, "out_hw": (Ho, Wo),
             "final_texel_views": last.layers * Ho * Wo * M}
 
@@ -182,6 +200,29 @@ def cpu_sample_desc():
             f"1/{d * d} frame, fps scaled accordingly")
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def calibration():
+    """The 1/16-frame sample against one full config-2 frame of the reference
+    timed on a B200 host (profiles/ref_fullframe.py -> profiles/r2/)."""
+    p = os.path.join(ROOT, "profiles", "r2", "ref_fullframe.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return {"full_frame_s": d.get("full_frame_s"),
+            "sample_x16_s": d.get("sample_extrapolated_frame_s"),
+            "full_over_extrapolated": d.get("full_over_extrapolated"),
+            "cpu_model": d.get("cpu_model"), "source": "profiles/r2/ref_fullframe.json"}
+
+
 def cpu_baseline_single():
     """oracle/_ref (the reference built from its sources) on one host core."""
     from bindings import REF_SO
@@ -191,7 +232,8 @@ def cpu_baseline_single():
     secs = _ref_worker_frame(0)
     frames = 1.0 / (CPU_SAMPLE_DIV ** 2)
     return {"value": frames / secs, "unit": "frames/s", "cores": 1, "kind": "reference",
-            "sample": cpu_sample_desc(), "sample_seconds": secs}
+            "sample": cpu_sample_desc(), "sample_seconds": secs, "cpu_model": cpu_model(),
+            "host_cores": os.cpu_count(), "calibration": calibration()}
 
 
 def reference_arm(args):
@@ -233,7 +275,9 @@ def reference_arm(args):
                        "sample": cpu_sample_desc(), "processes": procs},
                cpu_baseline={"value": fps, "unit": "frames/s", "cores": procs, "kind": "reference",
                              "sample": cpu_sample_desc(),
-                             "mean_sample_seconds": statistics.mean(per)},
+                             "mean_sample_seconds": statistics.mean(per),
+                             "cpu_model": cpu_model(), "host_cores": cores,
+                             "calibration": calibration()},
                e2e={"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0})
     print(json.dumps(out))
@@ -256,6 +300,12 @@ def main():
     ap.add_argument("--ref-procs", type=int, default=0)
     ap.add_argument("--shard-encoder", action="store_true",
                     help="view-sharded encode + pyramid all-gather even at N=1 (default at N>1)")
+    ap.add_argument("--mode", default="targets", choices=["targets", "frames", "rows"],
+                    help="N > 1 partition (SURVEY.md §8(e)): targets = one target viewpoint per "
+                         "rank (config-5 grid) with a view-sharded encoder; frames = the config-4 "
+                         "video dealt round-robin (frame r + k N on rank r, no exchange); rows = one "
+                         "target split into output row bands (replicated solve, band render, NCCL "
+                         "all-gather of the bands)")
     ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
                     help="N>1 pyramid exchange: stores fused into the encoder epilogue over "
                          "CUDA IPC (falls back to nccl if any rank cannot map its peers) or "
@@ -279,19 +329,37 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    # each rank its own target viewpoint (config 5 grid) when sharded
-    center = shard.target_center(rank, world)
-    case = (wl.config2(target_center=center) if args.config == "config2"
-            else wl.config3())
+    # targets: each rank its own target viewpoint (config 5 grid) when sharded;
+    # frames: rank r holds frames r and r + N of the config-4 video (device
+    # resident, alternated step by step); rows: every rank the same target
+    mode = args.mode if world > 1 or args.mode != "targets" else "targets"
+    frames = []
+    if mode == "frames":
+        frames = [wl.config4_frame((rank + k * world) % 30) for k in range(2)]
+        case = frames[0]
+    elif mode == "rows":
+        case = wl.config2() if args.config == "config2" else wl.config3()
+    else:
+        center = shard.target_center(rank, world)
+        case = (wl.config2(target_center=center) if args.config == "config2"
+                else wl.config3())
     cfg = case.cfg
     M = cfg.views
     model = q.Model(cfg, device=local)
     model.init_weights(case.seed)
     enc = torch.from_numpy(case.enc_images).to(dev)
     ren = torch.from_numpy(case.ren_images).to(dev)
+    fr_dev = [(torch.from_numpy(f.enc_images).to(dev), torch.from_numpy(f.ren_images).to(dev))
+              for f in frames]
     plan = q.plan_forward(cfg, enc.shape[1], enc.shape[2])
     Ho, Wo = plan.out_height, plan.out_width
     rgb = torch.empty((Ho, Wo, 3), dtype=torch.float32, device=dev)
+    # rows: this rank's band of the output, gathered into rgb every step
+    band_rows = Ho // world if mode == "rows" else Ho
+    if mode == "rows" and Ho % world:
+        raise SystemExit(f"--mode rows needs the {Ho} output rows divisible by {world}")
+    r0, r1 = rank * band_rows, (rank + 1) * band_rows
+    band = torch.empty((band_rows, Wo, 3), dtype=torch.float32, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     # one dedicated stream carries the frames, the L2 flushes and the timing
     # events (the library enqueues every kernel of the frame on it)
@@ -303,7 +371,7 @@ def main():
     # view_range(r) of the frame and the pyramid levels are all-gathered over
     # NVLink (NCCL, on the frame stream) -- then every rank reconstructs and
     # renders its own target from the full pyramid
-    sharded = world > 1 or args.shard_encoder
+    sharded = (world > 1 and mode == "targets") or args.shard_encoder
     v0, v1 = shard.view_range(rank, world, M)
     levels = []
 
@@ -312,7 +380,7 @@ def main():
     # all-reduce as the stream-ordered barrier) or an NCCL all-gather
     exchange = "nccl"
     barrier_t = None
-    if world > 1 and args.exchange == "fused":
+    if sharded and world > 1 and args.exchange == "fused":
         ok = 1
         try:
             mine = model.pyramid_export((He, We))
@@ -337,7 +405,23 @@ def main():
             for lv in levels:
                 shard.allgather_views(lv, M)
 
+    nstep = [0]
+
     def step():
+        if mode == "frames":
+            f = frames[nstep[0] % len(frames)]
+            e, r = fr_dev[nstep[0] % len(frames)]
+            nstep[0] += 1
+            model.forward_render_device(e, f.enc_cams, r, f.ren_cams, f.target, rgb, stream)
+            return
+        if mode == "rows":
+            model.forward_render_device(enc, case.enc_cams, ren, case.ren_cams, case.target, band,
+                                        stream, rows=(r0, r1))
+            if world > 1:
+                dist.all_gather_into_tensor(rgb, band)  # the band gather (NCCL, frame stream)
+            else:
+                rgb.copy_(band)
+            return
         if not sharded:
             model.forward_render_device(enc, case.enc_cams, ren, case.ren_cams, case.target, rgb,
                                         stream)
@@ -395,7 +479,10 @@ def main():
     ms = sum(a.elapsed_time(b) for a, b in ev)
     ms_max = shard.max_over_ranks(ms, dev)
     ms_per_step = ms_max / args.steps
-    fps = shard.aggregate_fps(world, args.steps, ms_max / 1000.0)
+    # frames / targets: every rank completes a frame per step; rows: the ranks
+    # complete one frame together per step
+    units = 1 if mode == "rows" else world
+    fps = shard.aggregate_fps(units, args.steps, ms_max / 1000.0)
 
     # e2e through the host C ABI: pinned host inputs, H2D + forward + render +
     # D2H of the frame, every step
@@ -409,7 +496,31 @@ def main():
         pending = []
         nsub = [0]
 
+        host_frames = [(torch.from_numpy(f.enc_images).pin_memory().numpy(),
+                        torch.from_numpy(f.ren_images).pin_memory().numpy(), f) for f in frames]
+        band_h = torch.empty((band_rows, Wo, 3), dtype=torch.float32).pin_memory()
+
         def e2e_step():
+            if mode == "frames":
+                # pipelined host frames, this rank's share of the video
+                if len(pending) == 2:
+                    model.wait_frame(pending.pop(0))
+                e_h, r_h, f = host_frames[nsub[0] % len(host_frames)]
+                pending.append(model.submit_frame(e_h, f.enc_cams, r_h, f.ren_cams, f.target,
+                                                  outs[nsub[0] % 2]))
+                nsub[0] += 1
+                return
+            if mode == "rows":
+                # every rank: both image sets up, the solve, its band, the
+                # band all-gather; rank 0 reads the whole frame back
+                with torch.cuda.stream(stream):
+                    enc.copy_(enc_h, non_blocking=True)
+                    ren.copy_(ren_h, non_blocking=True)
+                    step()
+                    if rank == 0:
+                        out_h.copy_(rgb, non_blocking=True)
+                stream.synchronize()
+                return
             if not sharded:
                 # pipelined host frames (lvsg_submit_frame / lvsg_wait_frame): at
                 # most two in flight, so frame k+1's uploads run under frame k
@@ -449,15 +560,18 @@ def main():
             model.wait_frame(pending.pop(0))
         sec = shard.max_over_ranks(time.perf_counter() - t0, dev)
         h2d = (enc_h[v0:v1].numel() if sharded else enc_h.numel()) * 4 + ren_h.numel() * 4
-        e2e = {"value": shard.aggregate_fps(world, args.e2e_steps, sec), "unit": "frames/s",
+        e2e = {"value": shard.aggregate_fps(units, args.e2e_steps, sec), "unit": "frames/s",
                "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(out_h.numel() * 4), "steps": args.e2e_steps,
                "path": ("lvsg_submit_frame / lvsg_wait_frame (host C ABI, pinned buffers, "
-                        "two frames in flight)" if not sharded else
+                        "two frames in flight)" if mode in ("targets", "frames") and not sharded
+                        else "pinned host views -> device (every rank) -> "
+                        "lvsg_forward_render_rows_device (this rank's band) -> NCCL all-gather "
+                        "of the bands -> rank 0 reads the frame back" if mode == "rows" else
                         "pinned host encoder views (own share) -> lvsg_encode_device -> pyramid "
                         "exchange -> lvsg_forward_render (NULL encoder list; pinned render "
                         "views in, pinned frame out)")}
-        if not sharded:
+        if not sharded and mode == "targets":
             # input-side decimation variant: only the
             # 1080p views are uploaded; the encoder input is their device
             # resize to 576 x 960 (a different encoder input than the
@@ -492,8 +606,12 @@ def main():
         for k, (sms, n) in stages.items():
             stage_rows[k] = {"ms": round(sms, 4), "launches": n}
         if "conv" in stages:
-            ach = work["conv_flops"] / (stages["conv"][0] / 1e3) / 1e12
-            stage_rows["conv"].update(tflops=round(ach, 2), frac_bf16_peak=round(ach / peaks["bf16_tflops"], 4))
+            sec = stages["conv"][0] / 1e3
+            ach = work["conv_flops"] / sec / 1e12
+            stage_rows["conv"].update(gbs=round(work["conv_bytes"] / sec / 1e9, 1),
+                                      frac_hbm=round(work["conv_bytes"] / sec / 1e9 / peaks["hbm_gbs"], 4),
+                                      tflops=round(ach, 2),
+                                      frac_bf16_peak=round(ach / peaks["bf16_tflops"], 4))
         if "attention" in stages:
             ach = work["attn_flops"] / (stages["attention"][0] / 1e3) / 1e12
             stage_rows["attention"].update(tflops=round(ach, 2))
@@ -501,27 +619,38 @@ def main():
             gbs = work["render_bytes"] / (stages["render"][0] / 1e3) / 1e9
             stage_rows["render"].update(gbs=round(gbs, 1), frac_hbm=round(gbs / peaks["hbm_gbs"], 4))
         dom = max(stages.items(), key=lambda kv: kv[1][0])[0] if stages else None
+        # DRAM bytes measured by ncu for the same command (profiles/r2/traffic.json,
+        # made by profiles/traffic_summary.py from a dram__bytes launch list)
         traffic = {}
-        tj = os.path.join(ROOT, "profiles", "r1", "traffic.json")
-        if os.path.exists(tj):
-            traffic = json.load(open(tj))
+        for tj in (os.path.join(ROOT, "profiles", "r2", "traffic.json"),
+                   os.path.join(ROOT, "profiles", "r1", "traffic.json")):
+            if os.path.exists(tj):
+                traffic = json.load(open(tj))
+                break
         if dom == "conv":
-            ach = work["conv_flops"] / (stages["conv"][0] / 1e3) / 1e12
-            tc = traffic.get("conv3x3_tc_kernel", {})
-            roof = {"bound": "tensor",
+            # the conv family is HBM-bound at C = 32 fp32 activations (~55
+            # FLOP/B against a bf16 ridge of ~250): roofline in bytes
+            sec = stages["conv"][0] / 1e3
+            gbs = work["conv_bytes"] / sec / 1e9
+            tfl = work["conv_flops"] / sec / 1e12
+            tc = traffic.get("conv3x3", {})
+            roof = {"bound": "hbm",
                     "kernel": "conv3x3_tc_kernel (all conv3x3 launches of a frame)",
-                    "achieved": ach, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                    "frac": ach / peaks["bf16_tflops"],
-                    "traffic": tc.get("dram_bytes_per_launch"),
-                    "traffic_note": (f"DRAM bytes of one {tc['launch']} launch vs "
-                                     f"{tc['algorithmic_bytes']} algorithmic ({tc['source']})"
+                    "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": gbs / peaks["hbm_gbs"],
+                    "traffic": tc.get("dram_bytes_per_frame"),
+                    "traffic_note": (f"ncu dram__bytes_read+write summed over the frame's "
+                                     f"{tc.get('launches')} conv launches ({tc.get('source')}) "
+                                     f"vs {work['conv_bytes'] / 1e9:.2f} GB algorithmic"
                                      if tc else None),
-                    "per_unit": f"{work['conv_flops'] / 1e9:.1f} GFLOP of conv3x3 per frame",
-                    "peak_source": peaks["source"] + ", dense bf16 burst",
-                    "note": "achieved counts fp32 conv FLOPs; they run as a 3-term fp16 split "
-                            "on tcgen05 (3 tensor MACs per fp32 MAC), so the split's own "
-                            "ceiling is peak/3",
-                    "frac_of_split_ceiling": 3 * ach / peaks["bf16_tflops"]}
+                    "per_unit": (f"{work['conv_bytes'] / 1e9:.2f} GB algorithmic per frame (each "
+                                 "conv reads its inputs and residual once and writes its output "
+                                 f"once); {work['conv_flops'] / 1e9:.1f} GFLOP"),
+                    "peak_source": peaks["source"] + ", HBM copy bandwidth",
+                    "tensor": {"achieved_tflops": tfl, "peak_tflops": peaks["bf16_tflops"],
+                               "frac": tfl / peaks["bf16_tflops"],
+                               "note": "fp32 conv FLOPs run as a 3-term fp16 split (3 tensor "
+                                       "MACs per fp32 MAC): the split's ceiling is peak/3"}}
         elif dom == "render":
             gbs = work["render_bytes"] / (stages["render"][0] / 1e3) / 1e9
             roof = {"bound": "hbm", "kernel": "render_fused_kernel", "achieved": gbs,
@@ -530,6 +659,13 @@ def main():
         else:
             roof = {"bound": "hbm", "kernel": dom, "achieved": None, "peak": peaks["hbm_gbs"],
                     "unit": "GB/s", "frac": None, "traffic": None}
+        if "frame_dram_bytes" in traffic:
+            # whole-frame DRAM traffic (ncu, every launch of one frame) over the
+            # device-timed frame
+            fb = traffic["frame_dram_bytes"]
+            roof["frame_dram"] = {"bytes": fb, "gbs": fb / (ms_per_step / 1e3) / 1e9,
+                                  "frac": fb / (ms_per_step / 1e3) / 1e9 / peaks["hbm_gbs"],
+                                  "source": traffic.get("source")}
         roof["stages"] = stage_rows
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -538,24 +674,36 @@ def main():
                 cpu = cpu_baseline_single()
             except Exception as e:  # reported, never fatal
                 cpu = {"value": None, "error": str(e)}
+        if mode == "frames":
+            per_gpu = (f"config-4 video frames {rank}, {rank}+{world}, ... (2 resident frames "
+                       "per rank, alternated), full forward + render each")
+            par = f"frame-sharded x{world}, no data-path collective" if world > 1 else "single GPU"
+        elif mode == "rows":
+            per_gpu = (f"one target: the replicated solve + output rows "
+                       f"[{r0}, {r1}) of {Ho}")
+            par = (f"row-band x{world}: replicated solve, band render, NCCL all-gather of the "
+                   "bands every frame" if world > 1 else "single GPU")
+        else:
+            per_gpu = ("one target viewpoint per rank (config-5 grid), "
+                       f"{v1 - v0} of {M} encoder views per rank") if world > 1 else "1 target"
+            par = (f"target-sharded x{world}; encoder view-sharded, pyramid "
+                   + ("exchange fused into the encoder epilogue (CUDA IPC stores over NVLink + "
+                      "NCCL one-element barrier)" if exchange == "fused" else
+                      "all-gathered per level with NCCL") + " per frame") \
+                if world > 1 else "single GPU"
         out = {
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong" if mode == "rows" else "weak",
+            "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (make_scene seed 21 plane scene, init_param_store seed 3 weights)",
             "config": {"workload": f"{args.config}: {M} views, full_scale_config, encoder "
                                    f"{enc.shape[1]}x{enc.shape[2]}, render {ren.shape[1]}x"
-                                   f"{ren.shape[2]}, output {Ho}x{Wo}",
-                       "per_gpu": ("one target viewpoint per rank (config-5 grid), "
-                                   f"{v1 - v0} of {M} encoder views per rank")
-                       if world > 1 else "1 target",
+                                   f"{ren.shape[2]}, output {Ho}x{Wo}"
+                                   + (" (config-4 video frames)" if mode == "frames" else ""),
+                       "mode": mode, "per_gpu": per_gpu,
                        "l2": "flushed (256 MB write) between timed frames",
-                       "parallelism": (f"target-sharded x{world}; encoder view-sharded, pyramid "
-                                       + ("exchange fused into the encoder epilogue (CUDA IPC "
-                                          "stores over NVLink + NCCL one-element barrier)"
-                                          if exchange == "fused" else
-                                          "all-gathered per level with NCCL") + " per frame")
-                       if world > 1 else "single GPU"},
+                       "parallelism": par},
             "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "roofline": roof, "cpu_baseline": cpu, "clocks": clocks.summary(),
         }

@@ -225,6 +225,17 @@ lvsg_status lvsg_forward_render_device(lvsg_ctx* ctx, int64_t views, const float
                                        int64_t render_w, const lvsg_camera* render_cams,
                                        const lvsg_frustum* target, float* rgb_out, void* stream);
 
+/* The same with only output rows [row0, row1) rendered into rgb_out
+ * ([row1-row0, Wo, 3], device): one row band of a target split across GPUs
+ * (the solve is replicated; the bands are gathered by the caller). */
+lvsg_status lvsg_forward_render_rows_device(lvsg_ctx* ctx, int64_t views, const float* enc_images,
+                                            int64_t enc_h, int64_t enc_w,
+                                            const lvsg_camera* enc_cams, const float* render_images,
+                                            int64_t render_h, int64_t render_w,
+                                            const lvsg_camera* render_cams,
+                                            const lvsg_frustum* target, int64_t row0, int64_t row1,
+                                            float* rgb_out, void* stream);
+
 /* encode_inputs' convolutional part (network.hpp:388-395: stem, residual
  * pairs, mean pools) of views [view0, view1) of the DEVICE images
  * [views,He,We,3] into the context's resident feature pyramid. The pyramid

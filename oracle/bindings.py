@@ -87,6 +87,8 @@ class Oracle:
         L.lvso_render_target.argtypes = [P(capi.FrustumC), vp, vp, vp, i64, i64, i64, i64, vp,
                                          i64, i64, P(capi.CameraC), vp]
         L.lvso_conv3x3.argtypes = [vp, vp, vp, vp, i64, i64, i64, i64]
+        L.lvso_trace_margins.argtypes = [ctypes.c_double, vp, i64]
+        L.lvso_trace_count.restype = i64
         L.lvso_attend_residual.argtypes = [vp, vp, i64, i64, i64, i64, vp, vp, vp, ctypes.c_int]
         L.lvso_render_to_view.argtypes = [P(capi.FrustumC), vp, i64, i64, i64, i64, i64, vp, vp,
                                           vp, P(capi.CameraC), vp]
@@ -155,6 +157,19 @@ class Oracle:
                                           _f32(blend), L_, Ho, Wo, M, _f32(images), Hr, Wr,
                                           _cams(cams), _f32(rgb))
         return rgb, bool(bad)
+
+    def trace_margins(self, tol, fn, cap=1 << 20):
+        """Runs fn() with the validity-margin trace on (lvso_trace_margins):
+        returns (fn's result, rows [n, 8] = step, kind (0 gather / 1 splat),
+        view, layer, y, x, signed margin px, u-or-v)."""
+        buf = np.zeros((cap, 8), np.float32)
+        self.lib.lvso_trace_margins(float(tol), buf.ctypes.data_as(vp), cap)
+        try:
+            out = fn()
+            n = int(self.lib.lvso_trace_count())
+        finally:
+            self.lib.lvso_trace_margins(0.0, None, 0)
+        return out, buf[:min(n, cap)].copy()
 
     def attend_residual(self, V, deltas, wq, wo, gain, zero_scores=False):
         """V [P,C] (not modified) -> V + OTM(rms_norm(V)); deltas [P,M,C];

@@ -405,7 +405,79 @@ static inline fp_t footprint(double u, double v, int64_t W, int64_t H) {
   return f;
 }
 
+/* Validity-margin trace (parity attribution): with
+ * lvso_trace_margins enabled, every footprint the forward computes in a
+ * gather (backproject_stack) or a splat (render_to_input_view) whose
+ * projected point lies within `tol` pixels of its validity boundary is
+ * recorded as one row of 8 floats: step, kind (0 gather, 1 splat), view,
+ * layer, y, x (texel of that step's volume), signed margin in pixels
+ * (> 0 inside), coordinate (u or v) that sets it. Observation only: the
+ * arithmetic and the results are unchanged. */
+static float* g_tr_buf = NULL;
+static int64_t g_tr_cap = 0, g_tr_n = 0, g_tr_H = 1, g_tr_W = 1;
+static double g_tr_tol = 0.0;
+static int g_tr_step = -1, g_tr_kind = 0, g_tr_view = 0;
+static pthread_mutex_t g_tr_mu = PTHREAD_MUTEX_INITIALIZER;
+
+void lvso_trace_margins(double tol, float* buf, int64_t cap) {
+  g_tr_tol = tol;
+  g_tr_buf = buf;
+  g_tr_cap = buf ? cap : 0;
+  g_tr_n = 0;
+}
+int64_t lvso_trace_count(void) { return g_tr_n; }
+
+static void trace_ctx(int step, int kind, int view, int64_t H, int64_t W) {
+  g_tr_step = step;
+  g_tr_kind = kind;
+  g_tr_view = view;
+  g_tr_H = H;
+  g_tr_W = W;
+}
+
+static inline void trace_uv(int64_t texel, double u, double v, int64_t Wi, int64_t Hi) {
+  if (!g_tr_buf) return;
+  const double tol = 1e-4;
+  const double m[4] = {u - (0.5 - tol), ((double)Wi - 0.5 + tol) - u, v - (0.5 - tol),
+                       ((double)Hi - 0.5 + tol) - v};
+  int a = 0;
+  for (int i = 1; i < 4; ++i)
+    if (fabs(m[i]) < fabs(m[a])) a = i;
+  if (fabs(m[a]) >= g_tr_tol) return;
+  pthread_mutex_lock(&g_tr_mu);
+  if (g_tr_n < g_tr_cap) {
+    float* r = g_tr_buf + g_tr_n * 8;
+    const int64_t plane = g_tr_H * g_tr_W, q = texel % plane;
+    r[0] = (float)g_tr_step;
+    r[1] = (float)g_tr_kind;
+    r[2] = (float)g_tr_view;
+    r[3] = (float)(texel / plane);
+    r[4] = (float)(q / g_tr_W);
+    r[5] = (float)(q % g_tr_W);
+    r[6] = (float)m[a];
+    r[7] = (float)(a < 2 ? u : v);
+  }
+  g_tr_n++;
+  pthread_mutex_unlock(&g_tr_mu);
+}
+
 /* CamPod::to_cam + projection + footprint (geometry.hpp:34-37, :152-159). */
+static inline fp_t project_fp_t(const campod* cp, const float* pt, int64_t texel) {
+  double pw[3] = {(double)pt[0], (double)pt[1], (double)pt[2]};
+  double q[3];
+  for (int i = 0; i < 3; ++i)
+    q[i] = cp->R[i * 3 + 0] * pw[0] + cp->R[i * 3 + 1] * pw[1] + cp->R[i * 3 + 2] * pw[2] + cp->t[i];
+  fp_t f;
+  if (q[2] <= 1e-6) {
+    memset(&f, 0, sizeof(f));
+    return f;
+  }
+  double u = cp->fx * q[0] / q[2] + cp->cx;
+  double v = cp->fy * q[1] / q[2] + cp->cy;
+  trace_uv(texel, u, v, cp->W, cp->H);
+  return footprint(u, v, cp->W, cp->H);
+}
+
 static inline fp_t project_fp(const campod* cp, const float* pt) {
   double pw[3] = {(double)pt[0], (double)pt[1], (double)pt[2]};
   double q[3];
@@ -447,13 +519,14 @@ typedef struct {
   int64_t ostride;
   float* mask;
   int64_t mstride;
+  int traced;
 } gather_ctx;
 
 static void gather_rows(void* p, int64_t b, int64_t e) {
   gather_ctx* g = (gather_ctx*)p;
   const int64_t C = g->C, Wi = g->Wi;
   for (int64_t i = b; i < e; ++i) {
-    fp_t f = project_fp(&g->cp, g->pts + i * 3);
+    fp_t f = g->traced ? project_fp_t(&g->cp, g->pts + i * 3, i) : project_fp(&g->cp, g->pts + i * 3);
     float* o = g->out + i * g->ostride;
     if (!f.valid) {
       for (int64_t c = 0; c < C; ++c) o[c] = 0.f;
@@ -476,7 +549,7 @@ static void gather_rows(void* p, int64_t b, int64_t e) {
 static void gather_strided(const lvsg_camera* cam, const float* image, int64_t Hi, int64_t Wi,
                            int64_t C, const float* points, int64_t P, float* values,
                            int64_t ostride, float* mask, int64_t mstride) {
-  gather_ctx g = {pod(cam), image, Hi, Wi, C, points, values, ostride, mask, mstride};
+  gather_ctx g = {pod(cam), image, Hi, Wi, C, points, values, ostride, mask, mstride, 0};
   par_for(P, gather_rows, &g);
 }
 
@@ -489,8 +562,13 @@ void lvso_gather(const lvsg_camera* cam, const float* image, int64_t Hi, int64_t
 static void backproject_stack(float* const* feats, const lvsg_camera* ucams, int64_t M,
                               int64_t Hf, int64_t Wf, int64_t C, const float* pts, int64_t P,
                               float* deltas) {
-  for (int64_t m = 0; m < M; ++m)
-    gather_strided(&ucams[m], feats[m], Hf, Wf, C, pts, P, deltas + m * C, M * C, NULL, 0);
+  for (int64_t m = 0; m < M; ++m) {
+    gather_ctx g = {pod(&ucams[m]), feats[m], Hf, Wf, C, pts, deltas + m * C, M * C, NULL, 0,
+                    g_tr_buf != NULL};
+    g_tr_kind = 0;
+    g_tr_view = (int)m;
+    par_for(P, gather_rows, &g);
+  }
 }
 
 /* splat_accumulate + splat_project (geometry.hpp:230-264, :317-326):
@@ -503,7 +581,7 @@ static void splat_project(const float* val, const float* pts, int64_t L, int64_t
   for (int64_t l = 0; l < L; ++l)
     for (int64_t s = 0; s < PL; ++s) {
       int64_t p = l * PL + s;
-      fp_t f = project_fp(&cp, pts + p * 3);
+      fp_t f = project_fp_t(&cp, pts + p * 3, p);
       if (!f.valid) continue;
       double w[4] = {(1 - f.fx) * (1 - f.fy), f.fx * (1 - f.fy), (1 - f.fx) * f.fy, f.fx * f.fy};
       int64_t tap[4] = {(l * Hi + f.y0) * Wi + f.x0, (l * Hi + f.y0) * Wi + f.x1,
@@ -1240,6 +1318,7 @@ int lvso_forward_render_ex(const lvsg_model_config* cfg, int64_t M, const float*
       ucams[m] = cam_scaled(&enc_cams[m], Wf, Hf);
     }
     deltas = falloc(L * H * W * M * C);
+    trace_ctx(0, 0, 0, H, W);
     backproject_stack(upd, ucams, M, Hf, Wf, C, pts, L * H * W, deltas);
     for (int64_t m = 0; m < M; ++m) free(upd[m]);
     free(upd);
@@ -1277,6 +1356,7 @@ int lvso_forward_render_ex(const lvsg_model_config* cfg, int64_t M, const float*
       } else {
         lvsg_camera rcam = cam_scaled(&enc_cams[m], plan.rend_w[s], plan.rend_h[s]);
         float* rv = falloc(plan.rend_h[s] * plan.rend_w[s] * Kf);
+        trace_ctx((int)s, 1, (int)m, H, W);
         bad |= render_to_view(V, L, H, W, C, Ca, &P, target, &rcam, rv);
         resize_hwc(rv, fb, 1, plan.rend_h[s], plan.rend_w[s], Kf, Hf, Wf);
         free(rv);
@@ -1306,6 +1386,7 @@ int lvso_forward_render_ex(const lvsg_model_config* cfg, int64_t M, const float*
     bad |= lvso_world_points(target, dd, L, Hn, Wn, pts);
     free(deltas);
     deltas = falloc(L * Hn * Wn * M * C);
+    trace_ctx((int)s, 0, 0, Hn, Wn);
     backproject_stack(upd, ucams, M, Hf, Wf, C, pts, L * Hn * Wn, deltas);
     for (int64_t m = 0; m < M; ++m) free(upd[m]);
     free(upd);

@@ -77,6 +77,12 @@ void lvso_attend_residual(float* V, const float* D, int64_t P, int64_t C, int64_
 int lvso_render_to_view(const lvsg_frustum* fr, const float* V, int64_t L, int64_t H, int64_t W,
                         int64_t C, int64_t Ca, const float* w_appear, const float* w_sigma,
                         const float* w_depth, const lvsg_camera* cam, float* out);
+/* Validity-margin trace of the forward's gathers and splats (parity
+ * attribution): rows of 8 floats (step, kind 0 gather / 1 splat, view,
+ * layer, y, x, signed margin px, u-or-v) for every footprint within tol px of
+ * its validity boundary; buf NULL disables. Not thread-safe across calls. */
+void lvso_trace_margins(double tol, float* buf, int64_t cap);
+int64_t lvso_trace_count(void);
 /* conv3x3 (kernels_ref.hpp:72-96), CHW / OIHW, zero pad by tap skipping. */
 void lvso_conv3x3(const float* x, const float* w, const float* b, float* y, int64_t Cin,
                   int64_t Cout, int64_t H, int64_t W);

@@ -110,7 +110,7 @@ SYMBOLS = [
     "lvsg_synchronize", "lvsg_last_launch_count", "lvsg_stream", "lvsg_stage_world_points",
     "lvsg_stage_footprints", "lvsg_stage_gather", "lvsg_rig_cameras", "lvsg_scene_images",
     "lvsg_scene_images_shifted", "lvsg_stage_attend", "lvsg_stage_upsample_render",
-    "lvsg_stage_render_to_view",
+    "lvsg_stage_render_to_view", "lvsg_forward_render_rows_device",
     "lvsg_profile_enable", "lvsg_profile_read", "lvsg_stage_conv3x3", "lvsg_stage_conv3x3_fused",
     "lvsg_load_weights_qntc", "lvsg_param_name", "lvsg_pack_param_store_qntc",
     "lvsg_forward_render_decimated", "lvsg_submit_frame_decimated", "lvsg_decimate_views_device",
@@ -155,6 +155,9 @@ def lib() -> ctypes.CDLL:
                                              c_i64, P(CameraC), P(FrustumC), vp, vp]
     L.lvsg_render_rows_device.argtypes = [vp, c_i64, vp, c_i64, c_i64, P(CameraC), c_i64, c_i64,
                                           vp, vp]
+    L.lvsg_forward_render_rows_device.argtypes = [vp, c_i64, vp, c_i64, c_i64, P(CameraC), vp,
+                                                  c_i64, c_i64, P(CameraC), P(FrustumC), c_i64,
+                                                  c_i64, vp, vp]
     L.lvsg_submit_frame.argtypes = [vp, c_i64, P(c_f32p), c_i64, c_i64, P(CameraC), P(c_f32p),
                                     c_i64, c_i64, P(CameraC), P(FrustumC), c_f32p, P(c_i64)]
     L.lvsg_wait_frame.argtypes = [vp, c_i64]

@@ -157,12 +157,16 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int H, int M>
+// MM: the view count (EXACT) or, for other counts, an upper bound on the
+// runtime view count Mr (views m >= Mr are skipped; MM in {8, 16, 32}).
+template <int H, int MM, bool EXACT>
 __global__ void __launch_bounds__(nthreads<H>(), 1)
     attend_tc_kernel(const __grid_constant__ CUtensorMap vmap,
                      const __grid_constant__ CUtensorMap dmap, int64_t P,
                      const float* __restrict__ wq, const float* __restrict__ wo,
-                     const float* __restrict__ gain, int zero_scores, int num_tiles) {
+                     const float* __restrict__ gain, int zero_scores, int num_tiles, int Mr) {
+  const int M = EXACT ? MM : Mr;
+  auto has = [&](int m) { return EXACT || m < Mr; };
   using S = Smem<H>;
   constexpr int NS = S::NS;
   constexpr int NTH = nthreads<H>(), NGRP = groups<H>(), HG = H / NGRP;
@@ -367,12 +371,12 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
     if (grp == 0) start_tile(0);
     for (int i = 0; i < ntl; ++i) {
       // ---- scores(i) for this group's heads: S in registers, one pass over Δ ----
-      float w[HG][M];
+      float w[HG][MM];
       if (zero_scores) {
 #pragma unroll
         for (int h = 0; h < HG; ++h)
 #pragma unroll
-          for (int m = 0; m < M; ++m) w[h][m] = __fdiv_rn(1.0f, float(M));
+          for (int m = 0; m < MM; ++m) w[h][m] = has(m) ? __fdiv_rn(1.0f, float(M)) : 0.f;
       } else {
         float sv[HG][C];
         tc::mbar_wait(s_done, uint32_t(i & 1));
@@ -384,10 +388,15 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
         // views in pairs, each dot as 4 interleaved partial sums: 8 independent
         // 8-deep FMA chains instead of one 32-deep chain per (view, head)
 #pragma unroll
-        for (int m = 0; m < M; m += 2) {
+        for (int m = 0; m < MM; m += 2) {
+          if (!has(m)) break;
           float d0[C], d1[C];
           slice_row(d0);
-          slice_row(d1);
+          if (has(m + 1))
+            slice_row(d1);
+          else
+#pragma unroll
+            for (int c = 0; c < C; ++c) d1[c] = 0.f;
 #pragma unroll
           for (int h = 0; h < HG; ++h) {
             float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
@@ -408,16 +417,17 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
         for (int h = 0; h < HG; ++h) {
           float mx = w[h][0];
 #pragma unroll
-          for (int m = 1; m < M; ++m) mx = fmaxf(mx, w[h][m]);
+          for (int m = 1; m < MM; ++m)
+            if (has(m)) mx = fmaxf(mx, w[h][m]);
           float sum = 0.f;
 #pragma unroll
-          for (int m = 0; m < M; ++m) {
-            w[h][m] = expf(fsb(w[h][m], mx));
-            sum = fa(sum, w[h][m]);
+          for (int m = 0; m < MM; ++m) {
+            w[h][m] = has(m) ? expf(fsb(w[h][m], mx)) : 0.f;
+            if (has(m)) sum = fa(sum, w[h][m]);
           }
           const float inv = __fdiv_rn(1.0f, sum);
 #pragma unroll
-          for (int m = 0; m < M; ++m) w[h][m] = fm(w[h][m], inv);
+          for (int m = 0; m < MM; ++m) w[h][m] = fm(w[h][m], inv);
         }
       }
       if (grp == 0) {
@@ -431,10 +441,15 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
 #pragma unroll
         for (int c = 0; c < C; ++c) hd[h][c] = 0.f;
 #pragma unroll
-      for (int m = 0; m < M; m += 2) {
+      for (int m = 0; m < MM; m += 2) {
+        if (!has(m)) break;
         float d0[C], d1[C];
         slice_row(d0);
-        slice_row(d1);
+        if (has(m + 1))
+          slice_row(d1);
+        else
+#pragma unroll
+          for (int c = 0; c < C; ++c) d1[c] = 0.f;
 #pragma unroll
         for (int h = 0; h < HG; ++h)
 #pragma unroll
@@ -466,10 +481,10 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-template <int H, int M>
-void launch(float* V, const float* D, int64_t P, const float* wq, const float* wo,
+template <int H, int MM, bool EXACT>
+void launch(float* V, const float* D, int64_t P, int M, const float* wq, const float* wo,
             const float* gain, int zero, cudaStream_t st) {
-  smem_optin(reinterpret_cast<const void*>(attend_tc_kernel<H, M>), Smem<H>::BYTES);
+  smem_optin(reinterpret_cast<const void*>(attend_tc_kernel<H, MM, EXACT>), Smem<H>::BYTES);
   const int sms = sm_count();
   // V [P][32] fp32 as a 2-D map, 128-texel boxes (128B swizzle)
   CUtensorMap vmap, dmap;
@@ -499,15 +514,14 @@ void launch(float* V, const float* D, int64_t P, const float* wq, const float* w
   }
   const int tiles = int((P + TILE - 1) / TILE);
   const int grid = tiles < sms ? tiles : sms;
-  launch_pdl(true, attend_tc_kernel<H, M>, grid, nthreads<H>(), Smem<H>::BYTES, st, vmap, dmap, P,
-             wq, wo, gain, zero, tiles);
+  launch_pdl(true, attend_tc_kernel<H, MM, EXACT>, grid, nthreads<H>(), Smem<H>::BYTES, st, vmap,
+             dmap, P, wq, wo, gain, zero, tiles, M);
 }
 
 }  // namespace
 
 bool attend_tc_supported(int C_, int M, int heads) {
-  return C_ == C && (heads == 1 || heads == 2 || heads == 4) &&
-         (M == 2 || M == 4 || M == 8 || M == 16);
+  return C_ == C && (heads == 1 || heads == 2 || heads == 4) && M >= 1 && M <= 32;
 }
 
 bool attend_tc(float* V, const float* deltas, int64_t P, int C_, int M, int heads, const float* wq,
@@ -515,15 +529,25 @@ bool attend_tc(float* V, const float* deltas, int64_t P, int C_, int M, int head
   if (C_ != C || !encode_fn() || (reinterpret_cast<uintptr_t>(V) & 15) ||
       (reinterpret_cast<uintptr_t>(deltas) & 15) || P >= (int64_t(1) << 31))
     return false;
-#define LVSG_ATT(HH, MM)                                                     \
-  if (heads == HH && M == MM) {                                              \
-    launch<HH, MM>(V, deltas, P, wq, wo, gain, zero_scores, st);             \
-    return true;                                                             \
+#define LVSG_ATT(HH)                                                                  \
+  if (heads == HH) {                                                                  \
+    switch (M) {                                                                      \
+      case 2: launch<HH, 2, true>(V, deltas, P, M, wq, wo, gain, zero_scores, st); break;   \
+      case 4: launch<HH, 4, true>(V, deltas, P, M, wq, wo, gain, zero_scores, st); break;   \
+      case 8: launch<HH, 8, true>(V, deltas, P, M, wq, wo, gain, zero_scores, st); break;   \
+      case 16: launch<HH, 16, true>(V, deltas, P, M, wq, wo, gain, zero_scores, st); break; \
+      default:                                                                        \
+        if (M < 8)                                                                    \
+          launch<HH, 8, false>(V, deltas, P, M, wq, wo, gain, zero_scores, st);       \
+        else if (M < 16)                                                              \
+          launch<HH, 16, false>(V, deltas, P, M, wq, wo, gain, zero_scores, st);      \
+        else                                                                          \
+          launch<HH, 32, false>(V, deltas, P, M, wq, wo, gain, zero_scores, st);      \
+    }                                                                                 \
+    return true;                                                                      \
   }
-  LVSG_ATT(1, 2) LVSG_ATT(2, 2) LVSG_ATT(4, 2)
-  LVSG_ATT(1, 4) LVSG_ATT(2, 4) LVSG_ATT(4, 4)
-  LVSG_ATT(1, 8) LVSG_ATT(2, 8) LVSG_ATT(4, 8)
-  LVSG_ATT(1, 16) LVSG_ATT(2, 16) LVSG_ATT(4, 16)
+  if (M < 1 || M > 32) return false;
+  LVSG_ATT(1) LVSG_ATT(2) LVSG_ATT(4)
 #undef LVSG_ATT
   return false;
 }

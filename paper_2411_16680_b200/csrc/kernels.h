@@ -237,7 +237,7 @@ void decode_scalar(const float* V, int64_t P, int C, const float* w, float* out,
                    int64_t PL, const DepthAct* act, cudaStream_t st);
 
 // ---- Stage 3 + 4 ------------------------------------------------------------
-constexpr int kRenderParamViews = 16;
+constexpr int kRenderParamViews = 32;
 struct RenderArgs {
   const float* pre_d;   // [L,H,W]
   const float* pre_s;   // [L,H,W]
@@ -247,15 +247,19 @@ struct RenderArgs {
   DepthAct act;
   DevRayCam rc;           // target camera re-digitised to (Wo, Ho)
   const DevCam* cams;     // [M] render cameras (device)
-  DevCam pc[kRenderParamViews];  // the same by value (M <= 16; the M-specialised kernels)
+  DevCam pc[kRenderParamViews];  // the same by value (M <= 32; the view-count kernels)
   int pc_valid;                  // pc holds the M cameras
   const float* images;    // [M, Hr, Wr, 3]
+  const float4* images4;  // optional: the same as RGBA rows [M, Hr, Wr] (expand_rgba)
   int Hr, Wr;
   float* rgb;             // [row1-row0, Wo, 3]
   float near_depth, far_depth;
   int* bad_depth;         // set when a depth leaves [near-slack, far+slack]
   double slack_lo, slack_hi;
 };
+// [n, 3] RGB -> [n] float4 rows (one 16-byte load per render tap); returns
+// the number of launches.
+int expand_rgba(const float* rgb, float4* out, int64_t n, cudaStream_t st);
 // upsample_activate + render_target fused (ldm.hpp:193-199, :249-271).
 void render_fused(const RenderArgs& a, cudaStream_t st);
 // ForwardResult.rgb of a direct_rgb config (network.hpp:596-601): pre_a =

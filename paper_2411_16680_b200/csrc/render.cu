@@ -8,6 +8,8 @@
 // Reference semantics: upsample_activate (ldm.hpp:249-271), resize_bilinear
 // (tape.hpp:858-917), render_target -> world_points + blended_layer_colors +
 // over_composite (ldm.hpp:98-199, geometry.hpp:84-171).
+#include <algorithm>
+
 #include "kernels.h"
 
 namespace lvsg {
@@ -26,16 +28,44 @@ __device__ __forceinline__ float sample(const float* map, int W, const Taps& t) 
 }
 
 // Activated LDM sample of layer l at output pixel: depth, sigma, beta[M].
-// MM > 0: compile-time view count (every per-view array stays in registers).
-template <int MM>
+// MM > 0: compile-time view count (every per-view array stays in registers);
+// G: MM is only an upper bound of the runtime count a.M (views >= a.M are
+// skipped, beta[m >= a.M] = 0).
+template <int MM, bool G = false>
 __device__ __forceinline__ void ldm_sample(const RenderArgs& a, int l, const Taps& t, float& depth,
                                            float& sigma, float* beta) {
   const int64_t plane = (int64_t)a.H * a.W;
   depth = activate_depth(sample(a.pre_d + l * plane, a.W, t), l, a.act);
   sigma = sigmoid_ref(sample(a.pre_s + l * plane, a.W, t));
-  const int M = MM > 0 ? MM : a.M;
+  const int M = MM > 0 && !G ? MM : a.M;
   const float* lg = a.logits + l * plane * M;
   float mx = 0.f;
+  if (G) {
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+      if (m >= M) {
+        beta[m] = 0.f;
+        continue;
+      }
+      const float v = lerp2(__ldg(lg + ((int64_t)t.y0 * a.W + t.x0) * M + m),
+                            __ldg(lg + ((int64_t)t.y0 * a.W + t.x1) * M + m),
+                            __ldg(lg + ((int64_t)t.y1 * a.W + t.x0) * M + m),
+                            __ldg(lg + ((int64_t)t.y1 * a.W + t.x1) * M + m), t.fx, t.fy);
+      beta[m] = v;
+      mx = m == 0 ? v : fmaxf(mx, v);
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int m = 0; m < MM; ++m)
+      if (m < M) {
+        beta[m] = expf(fsb(beta[m], mx));
+        sum = fa(sum, beta[m]);
+      }
+    const float inv = __fdiv_rn(1.0f, sum);
+#pragma unroll
+    for (int m = 0; m < MM; ++m) beta[m] = fm(beta[m], inv);
+    return;
+  }
   if (MM > 0 && MM % 4 == 0) {  // each tap's M logits as float4 runs
     const float4* q00 = reinterpret_cast<const float4*>(lg + ((int64_t)t.y0 * a.W + t.x0) * M);
     const float4* q10 = reinterpret_cast<const float4*>(lg + ((int64_t)t.y0 * a.W + t.x1) * M);
@@ -81,14 +111,68 @@ __device__ __forceinline__ Taps taps_for(const RenderArgs& a, int i, int j) {
   return t;
 }
 
+// blended_layer_colors (ldm.hpp:158-189) for a compile-time view count:
+// acc = sum_m beta_m mask_m c_m and wsum = sum_m beta_m mask_m (k ascending),
+// with the cameras in the kernel's parameter space. The caller scales acc
+// by 1/(wsum + 1e-8) once (the reference scales each beta first: ~1 ulp
+// apart, floating-point work); no per-view colour stays live across the
+// loop. EXACT = false takes each footprint from the fast path and returns
+// the mask of views whose decisions it could not take (the caller then
+// re-runs the layer with EXACT = true: the reference's operation order for
+// every view). Taps and validity are the reference's either way; weights
+// are f32 from the f64 fractions and the colour an f32 FMA chain (~2 ulp of
+// the reference's f64 blend).
+template <int MM, bool G, bool EXACT>
+__device__ __forceinline__ unsigned blend_views(const RenderArgs& a, const float pt[3],
+                                                const float* beta, float acc[3], float& wsum) {
+  unsigned need = 0;
+  acc[0] = acc[1] = acc[2] = 0.f;
+  wsum = 0.f;
+#pragma unroll
+  for (int m = 0; m < MM; ++m) {
+    if (G && m >= a.M) break;
+    Footprint f;
+    if (EXACT)
+      f = project_footprint_nb(a.pc[m], pt);
+    else if (!project_footprint_fast(a.pc[m], pt, f))
+      need |= 1u << m;  // f: invalid, in-range taps
+    const float fx = __double2float_rn(f.fx), fy = __double2float_rn(f.fy);
+    const float gx = 1.0f - fx, gy = 1.0f - fy;
+    const float w[4] = {gx * gy, fx * gy, gx * fy, fx * fy};
+    const int r0 = f.y0 * a.Wr, r1 = f.y1 * a.Wr;  // one view < 2^31 floats
+    const float bm = f.valid ? beta[m] : 0.f;
+    if (a.images4) {
+      const float4* im4 = a.images4 + (int64_t)m * a.Hr * a.Wr;
+      const float4 c00 = __ldg(im4 + r0 + f.x0), c10 = __ldg(im4 + r0 + f.x1);
+      const float4 c01 = __ldg(im4 + r1 + f.x0), c11 = __ldg(im4 + r1 + f.x1);
+      acc[0] = fmaf(bm, fmaf(w[3], c11.x, fmaf(w[2], c01.x, fmaf(w[1], c10.x, w[0] * c00.x))), acc[0]);
+      acc[1] = fmaf(bm, fmaf(w[3], c11.y, fmaf(w[2], c01.y, fmaf(w[1], c10.y, w[0] * c00.y))), acc[1]);
+      acc[2] = fmaf(bm, fmaf(w[3], c11.z, fmaf(w[2], c01.z, fmaf(w[1], c10.z, w[0] * c00.z))), acc[2]);
+    } else {
+      const float* img = a.images + (int64_t)m * a.Hr * a.Wr * 3;
+      const float* p00 = img + (r0 + f.x0) * 3;
+      const float* p10 = img + (r0 + f.x1) * 3;
+      const float* p01 = img + (r1 + f.x0) * 3;
+      const float* p11 = img + (r1 + f.x1) * 3;
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        acc[k] = fmaf(bm, fmaf(w[3], __ldg(p11 + k),
+                               fmaf(w[2], __ldg(p01 + k), fmaf(w[1], __ldg(p10 + k), w[0] * __ldg(p00 + k)))),
+                      acc[k]);
+    }
+    wsum = fa(wsum, bm);
+  }
+  return need;
+}
+
 // One thread per output pixel of the row band. MM > 0: the view count is a
 // compile-time constant, the cameras are read from the kernel's parameter
 // space (a.pc: constant-bank operands of the f64 instructions) and each
 // view's footprint is branch-free (taps always in range; an invalid view's
 // colour and weight are zeroed by select). MM == 0: cameras staged in shared
 // memory, branchy footprint.
-template <int MM>
-__global__ void __launch_bounds__(128, MM == 16 ? 4 : 8) render_fused_kernel(const RenderArgs a) {
+template <int MM, bool G = false>
+__global__ void __launch_bounds__(128, MM >= 16 ? 4 : 8) render_fused_kernel(const RenderArgs a) {
   pdl_grid_sync();
   extern __shared__ DevCam s_cams[];
   if (MM == 0) {
@@ -109,39 +193,26 @@ __global__ void __launch_bounds__(128, MM == 16 ? 4 : 8) render_fused_kernel(con
   const int64_t img_stride = (int64_t)a.Hr * a.Wr * 3;
   for (int l = 0; l < a.L; ++l) {
     float depth, sigma;
-    ldm_sample<MM>(a, l, t, depth, sigma, beta);
+    ldm_sample<MM, G>(a, l, t, depth, sigma, beta);
     const double dv = double(depth);
     bad |= (dv < a.slack_lo || dv > a.slack_hi);
     float pt[3];
     world_point_dir(a.rc, dir, depth, pt);
-    // blended_layer_colors: beta * mask, wsum (k ascending from 0), 1/(wsum+1e-8)
-    float col[MM > 0 ? MM : kMaxViews][3];
-    float wsum = 0.f;
+    float rgb[3] = {0.f, 0.f, 0.f};
+    if constexpr (MM > 0) {
+      float acc[3], wsum;
+      if (blend_views<MM, G, false>(a, pt, beta, acc, wsum))
+        blend_views<MM, G, true>(a, pt, beta, acc, wsum);  // rare: a decision within 1e-7 px
+      const float r = __fdiv_rn(1.0f, fa(wsum, 1e-8f));
 #pragma unroll
-    for (int m = 0; m < M; ++m) {
-      const float* img = a.images + m * img_stride;
-      if (MM > 0) {
-        // f64 (bit-exact) taps and weights; the colour blend is an f32 FMA
-        // chain over the weights rounded to f32 (~2 ulp of the f64 blend)
-        const Footprint f = project_footprint_nb(a.pc[m], pt);
-        double wd[4];
-        bilinear_weights(f, wd);
-        float w[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) w[k] = __double2float_rn(wd[k]);
-        const int r0 = f.y0 * a.Wr, r1 = f.y1 * a.Wr;  // one view < 2^31 floats
-        const float* p00 = img + (r0 + f.x0) * 3;
-        const float* p10 = img + (r0 + f.x1) * 3;
-        const float* p01 = img + (r1 + f.x0) * 3;
-        const float* p11 = img + (r1 + f.x1) * 3;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const float v = fmaf(w[3], __ldg(p11 + k),
-                               fmaf(w[2], __ldg(p01 + k), fmaf(w[1], __ldg(p10 + k), w[0] * __ldg(p00 + k))));
-          col[m][k] = f.valid ? v : 0.f;
-        }
-        beta[m] = fm(beta[m], f.valid ? 1.0f : 0.0f);
-      } else {
+      for (int k = 0; k < 3; ++k) rgb[k] = fm(acc[k], r);
+    } else {
+      // blended_layer_colors: beta * mask, wsum (k ascending from 0),
+      // 1/(wsum+1e-8), then sum_m (beta_m r) c_m -- the reference's order
+      float col[kMaxViews][3];
+      float wsum = 0.f;
+      for (int m = 0; m < M; ++m) {
+        const float* img = a.images + m * img_stride;
         const Footprint f = project_footprint(s_cams[m], pt);
         if (f.valid) {
           double wd[4];
@@ -162,16 +233,14 @@ __global__ void __launch_bounds__(128, MM == 16 ? 4 : 8) render_fused_kernel(con
           col[m][0] = col[m][1] = col[m][2] = 0.f;
           beta[m] = fm(beta[m], 0.0f);
         }
+        wsum = fa(wsum, fm(beta[m], 1.0f));
       }
-      wsum = fa(wsum, fm(beta[m], 1.0f));
-    }
-    const float r = __fdiv_rn(1.0f, fa(wsum, 1e-8f));
-    float rgb[3] = {0.f, 0.f, 0.f};
+      const float r = __fdiv_rn(1.0f, fa(wsum, 1e-8f));
+      for (int m = 0; m < M; ++m) {
+        const float b = fm(beta[m], r);
 #pragma unroll
-    for (int m = 0; m < M; ++m) {
-      const float b = fm(beta[m], r);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) rgb[k] = fa(rgb[k], fm(b, col[m][k]));
+        for (int k = 0; k < 3; ++k) rgb[k] = fa(rgb[k], fm(b, col[m][k]));
+      }
     }
     // over_composite: o = v*a + (1-a)*o, layer 0 (far) first
 #pragma unroll
@@ -236,18 +305,68 @@ __global__ void direct_rgb_kernel(const RenderArgs a, const float* __restrict__ 
 
 inline int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
 
+// [n, 3] f32 -> [n] float4 (alpha 0): four pixels per thread, three 16-byte
+// loads and four 16-byte stores (n % 4 == 0, 16-byte aligned input).
+__global__ void __launch_bounds__(256) expand_rgba_kernel(const float4* __restrict__ in,
+                                                          float4* __restrict__ out, int64_t quads) {
+  pdl_grid_sync();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < quads;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 a = __ldg(in + 3 * i), b = __ldg(in + 3 * i + 1), c = __ldg(in + 3 * i + 2);
+    out[4 * i + 0] = make_float4(a.x, a.y, a.z, 0.f);
+    out[4 * i + 1] = make_float4(a.w, b.x, b.y, 0.f);
+    out[4 * i + 2] = make_float4(b.z, b.w, c.x, 0.f);
+    out[4 * i + 3] = make_float4(c.y, c.z, c.w, 0.f);
+  }
+}
+
+__global__ void expand_rgba_tail_kernel(const float* __restrict__ in, float4* __restrict__ out,
+                                        int64_t n0, int64_t n) {
+  pdl_grid_sync();
+  const int64_t i = n0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = make_float4(in[3 * i], in[3 * i + 1], in[3 * i + 2], 0.f);
+}
+
 }  // namespace
+
+int expand_rgba(const float* rgb, float4* out, int64_t n, cudaStream_t st) {
+  const bool al = (reinterpret_cast<uintptr_t>(rgb) & 15) == 0;
+  const int64_t quads = al ? n / 4 : 0;
+  int launches = 0;
+  if (quads) {
+    const int g = int(std::min<int64_t>((quads + 255) / 256, int64_t(sm_count()) * 8));
+    launch_k(expand_rgba_kernel, g, 256, 0, st, reinterpret_cast<const float4*>(rgb), out, quads);
+    ++launches;
+  }
+  if (4 * quads < n) {
+    launch_k(expand_rgba_tail_kernel, blocks_for(n - 4 * quads, 256), 256, 0, st, rgb, out,
+             4 * quads, n);
+    ++launches;
+  }
+  return launches;
+}
 
 void render_fused(const RenderArgs& a, cudaStream_t st) {
   const int64_t n = (int64_t)(a.row1 - a.row0) * a.Wo;
   const int g = blocks_for(n, 128);
-  const int mm = a.pc_valid && (a.M == 4 || a.M == 8 || a.M == 16) ? a.M : 0;
+  // exact view-count kernels for M in {4, 8, 16}; other M <= 32 run the
+  // next larger one with a runtime bound; all of them take the cameras by
+  // value (pc); without them (pc_valid = 0) the generic kernel
+  const bool pc = a.pc_valid && a.M >= 1 && a.M <= kRenderParamViews;
+  const int mm = !pc ? 0 : (a.M == 4 || a.M == 8 || a.M == 16) ? a.M : -a.M;
   const size_t sm = mm ? 0 : a.M * sizeof(DevCam);  // <0> stages the cameras in smem
   switch (mm) {
     case 4: launch_k(render_fused_kernel<4>, g, 128, sm, st, a); break;
     case 8: launch_k(render_fused_kernel<8>, g, 128, sm, st, a); break;
     case 16: launch_k(render_fused_kernel<16>, g, 128, sm, st, a); break;
-    default: launch_k(render_fused_kernel<0>, g, 128, sm, st, a); break;
+    case 0: launch_k(render_fused_kernel<0>, g, 128, sm, st, a); break;
+    default:
+      if (a.M < 8)
+        launch_k(render_fused_kernel<8, true>, g, 128, sm, st, a);
+      else if (a.M < 16)
+        launch_k(render_fused_kernel<16, true>, g, 128, sm, st, a);
+      else
+        launch_k(render_fused_kernel<32, true>, g, 128, sm, st, a);
   }
 }
 

@@ -209,6 +209,7 @@ struct lvsg_ctx {
   std::map<std::tuple<const float*, int, int>, std::unique_ptr<lvsg::Buf>> wimg;
   lvsg::Buf wimg_tmp;  // uncached image for the stage entry points
   lvsg::Buf stage_a, stage_b, stage_c, stage_cams;  // scratch of the per-stage entry points
+  lvsg::Buf ren4;  // render views as RGBA rows (expand_rgba), rewritten per render call
   lvsg::Buf attn_scratch;  // generic attention kernel rows (shapes without a tensor-core kernel)
   std::vector<float> stem_host;  // encoder stem weights [32*27] + bias [32] (host copy)
   std::vector<std::vector<float>> rayproj_host;  // per-level ray_proj [32, C] (host copies)
@@ -957,6 +958,24 @@ RenderArgs render_args(lvsg_ctx* c, const float* images, int64_t Hr, int64_t Wr,
   return a;
 }
 
+// The render views as RGBA rows for the M-specialised render (one 16-byte
+// load per tap instead of three 4-byte loads), on the context stream right
+// before the render that reads them. LVSG_RGBA=0 keeps the 3-channel reads.
+bool rgba_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("LVSG_RGBA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+void use_rgba(lvsg_ctx* c, RenderArgs& a) {
+  if (!rgba_enabled() || !a.pc_valid || !a.images) return;
+  const int64_t n = int64_t(a.M) * a.Hr * a.Wr;
+  c->ren4.ensure(size_t(n) * 4);
+  mark(c, "render", expand_rgba(a.images, reinterpret_cast<float4*>(c->ren4.p), n, c->stream));
+  a.images4 = reinterpret_cast<const float4*>(c->ren4.p);
+}
+
 DevCam* upload_render_cams(lvsg_ctx* c, const lvsg_camera* cams) {
   // render-only path (lvsg_render): a dedicated slot after the frame tables
   const size_t M = size_t(c->M);
@@ -1355,7 +1374,9 @@ lvsg_status lvsg_render(lvsg_ctx* c, int64_t views, const float* const* images, 
     DevCam* dc = upload_render_cams(c, cams);
     const int64_t Ho = c->plan.out_height, Wo = c->plan.out_width;
     c->rgb.ensure(size_t(Ho * Wo * 3));
-    render_fused(render_args(c, c->ren_in.p, height, width, dc, c->rgb.p, 0, Ho, cams), c->stream);
+    RenderArgs a = render_args(c, c->ren_in.p, height, width, dc, c->rgb.p, 0, Ho, cams);
+    use_rgba(c, a);
+    render_fused(a, c->stream);
     CUDA_OK(cudaMemcpyAsync(rgb_out, c->rgb.p, size_t(Ho * Wo * 3) * sizeof(float),
                             cudaMemcpyDeviceToHost, c->stream));
     sync_and_check(c);
@@ -1460,11 +1481,16 @@ lvsg_status submit_impl(lvsg_ctx* c, int64_t views, const float* const* enc_imag
     // banded render; each band's read-back (download stream) overlaps the
     // next band's render
     constexpr int NB = 4;
+    RenderArgs a0 = render_args(c, S.ren_in.p, render_h, render_w, t.final_cams, S.rgb.p, 0, Ho,
+                                render_cams);
+    use_rgba(c, a0);
     for (int b = 0; b < NB; ++b) {
       const int64_t r0 = Ho * b / NB, r1 = Ho * (b + 1) / NB;
       if (r1 == r0) continue;
-      RenderArgs a = render_args(c, S.ren_in.p, render_h, render_w, t.final_cams,
-                                 S.rgb.p + r0 * Wo * 3, r0, r1, render_cams);
+      RenderArgs a = a0;
+      a.rgb = S.rgb.p + r0 * Wo * 3;
+      a.row0 = int(r0);
+      a.row1 = int(r1);
       a.bad_depth = S.bad;
       render_fused(a, c->stream);
       c->launches += 1;
@@ -1551,29 +1577,34 @@ lvsg_status lvsg_forward_render(lvsg_ctx* c, int64_t views, const float* const* 
   return lvsg_wait_frame(c, ticket);
 }
 
-lvsg_status lvsg_forward_render_device(lvsg_ctx* c, int64_t views, const float* enc_images,
-                                       int64_t enc_h, int64_t enc_w, const lvsg_camera* enc_cams,
-                                       const float* render_images, int64_t render_h,
-                                       int64_t render_w, const lvsg_camera* render_cams,
-                                       const lvsg_frustum* target, float* rgb_out, void* stream) {
+lvsg_status lvsg_forward_render_rows_device(lvsg_ctx* c, int64_t views, const float* enc_images,
+                                            int64_t enc_h, int64_t enc_w,
+                                            const lvsg_camera* enc_cams, const float* render_images,
+                                            int64_t render_h, int64_t render_w,
+                                            const lvsg_camera* render_cams,
+                                            const lvsg_frustum* target, int64_t row0, int64_t row1,
+                                            float* rgb_out, void* stream) {
   // enc_images == NULL: the encoder is skipped and the resident pyramid of
   // lvsg_encode_device is used (one encode, many targets / GPUs)
   return guard(c, [&] {
     check_views(c, views, enc_h, enc_w);
     check_views(c, views, render_h, render_w);
     for (int64_t m = 0; m < views; ++m) camera_validate(render_cams[m]);
+    const Plan plan = plan_forward(c->cfg, enc_h, enc_w);
+    if (row0 < 0 || row0 > row1 || row1 > plan.out_height)
+      throw DimError("render_rows: bad row band");
     cudaStream_t user = static_cast<cudaStream_t>(stream);
     cudaStream_t own = c->stream;
     if (user) c->stream = user;
     try {
       CamTables t;
       forward_device(c, enc_images, enc_h, enc_w, enc_cams, *target, render_cams, &t);
-      const int64_t Ho = c->plan.out_height;
-      render_fused(render_args(c, render_images, render_h, render_w, t.final_cams, rgb_out, 0, Ho,
-                               render_cams),
-                   c->stream);
+      RenderArgs a = render_args(c, render_images, render_h, render_w, t.final_cams, rgb_out, row0,
+                                 row1, render_cams);
+      use_rgba(c, a);
+      render_fused(a, c->stream);
       mark(c, "render", 1);
-    c->launches += 1;
+      c->launches += 1;
       CUDA_OK(cudaGetLastError());
     } catch (...) {
       c->stream = own;
@@ -1581,6 +1612,22 @@ lvsg_status lvsg_forward_render_device(lvsg_ctx* c, int64_t views, const float* 
     }
     c->stream = own;
   });
+}
+
+lvsg_status lvsg_forward_render_device(lvsg_ctx* c, int64_t views, const float* enc_images,
+                                       int64_t enc_h, int64_t enc_w, const lvsg_camera* enc_cams,
+                                       const float* render_images, int64_t render_h,
+                                       int64_t render_w, const lvsg_camera* render_cams,
+                                       const lvsg_frustum* target, float* rgb_out, void* stream) {
+  int64_t Ho = 0;
+  try {
+    if (c) Ho = lvsg::plan_forward(c->cfg, enc_h, enc_w).out_height;
+  } catch (...) {
+    Ho = 0;  // the rows call reports the DimError
+  }
+  return lvsg_forward_render_rows_device(c, views, enc_images, enc_h, enc_w, enc_cams,
+                                         render_images, render_h, render_w, render_cams, target,
+                                         0, Ho, rgb_out, stream);
 }
 
 lvsg_status lvsg_encode_device(lvsg_ctx* c, int64_t views, const float* enc_images, int64_t enc_h,
@@ -1691,9 +1738,10 @@ lvsg_status lvsg_render_rows_device(lvsg_ctx* c, int64_t views, const float* ren
     cudaStream_t own = c->stream;
     if (user) c->stream = user;
     DevCam* dc = upload_render_cams(c, render_cams);
-    render_fused(render_args(c, render_images, render_h, render_w, dc, rgb_out, row0, row1,
-                               render_cams),
-                 c->stream);
+    RenderArgs a = render_args(c, render_images, render_h, render_w, dc, rgb_out, row0, row1,
+                               render_cams);
+    use_rgba(c, a);
+    render_fused(a, c->stream);
     c->stream = own;
     CUDA_OK(cudaGetLastError());
   });
@@ -1873,6 +1921,7 @@ lvsg_status lvsg_stage_upsample_render(lvsg_ctx* c, const lvsg_frustum* target, 
     const double slack = 1e-3 * (target->far_depth - target->near_depth);
     a.slack_lo = target->near_depth - slack;
     a.slack_hi = target->far_depth + slack;
+    use_rgba(c, a);
     render_fused(a, c->stream);
     sync_and_check(c);
   });

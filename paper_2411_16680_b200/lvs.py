@@ -369,12 +369,15 @@ class Model:
             getattr(self, "_inflight", {}).pop(int(ticket), None)
 
     def forward_render_device(self, enc_images, enc_cams, render_images, render_cams,
-                              target: Frustum, rgb_out, stream=None, enc_hw=None) -> None:
+                              target: Frustum, rgb_out, stream=None, enc_hw=None,
+                              rows=None) -> None:
         """Device-resident path on torch CUDA tensors (enc [M,He,We,3],
         render [M,Hr,Wr,3], rgb_out [Ho,Wo,3]); enqueued on `stream`
         (torch.cuda.Stream or raw handle; default: torch's current stream).
         enc_images=None: the resident pyramid of encode_device (encoder
-        resolution enc_hw) is used instead of encoding."""
+        resolution enc_hw) is used instead of encoding. rows=(r0, r1): only
+        those output rows are rendered, rgb_out [r1-r0, Wo, 3]
+        (lvsg_forward_render_rows_device)."""
         import torch
         for t in (render_images, rgb_out) + ((enc_images,) if enc_images is not None else ()):
             if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
@@ -388,6 +391,12 @@ class Model:
             He, We = enc_hw
             ep = None
         fr = target.to_c()
+        if rows is not None:
+            self._check(self._lib.lvsg_forward_render_rows_device(
+                self._h, M, ep, He, We, _cam_array(enc_cams),
+                render_images.data_ptr(), Hr, Wr, _cam_array(render_cams), ctypes.byref(fr),
+                int(rows[0]), int(rows[1]), rgb_out.data_ptr(), sh))
+            return
         self._check(self._lib.lvsg_forward_render_device(
             self._h, M, ep, He, We, _cam_array(enc_cams),
             render_images.data_ptr(), Hr, Wr, _cam_array(render_cams), ctypes.byref(fr),

@@ -278,21 +278,25 @@ def test_config2_scaled_matches_oracle(oracle):
 
 
 def _full_scale(oracle, case):
-    """One full-scale frame against the oracle with validity-flip attribution
-    (tests/parity_util.py): max-abs <= 1e-3,
-    >= 50 dB, and no value above the gate off a flip pixel."""
-    from parity_util import frame_metrics, gate
+    """One full-scale frame against the oracle (tests/parity_util.py):
+    PSNR >= 50 dB, max-abs <= 1e-3 on every pixel except those a validity
+    flip explains -- a final-render flip, or an internal gather / splat
+    footprint of the solve lying within 1e-4 px of its view's edge in the
+    oracle's own forward. The reference itself
+    moves such pixels by > 1e-3 under one-ulp input perturbations
+    (profiles/r2/parity_self.jsonl)."""
+    from parity_util import full_frame_check
     m = q.Model(case.cfg, device=0)
     m.load_weights(case.store())
     rgb = m.forward_render(case.enc_images, case.enc_cams, case.ren_images, case.ren_cams,
                            case.target)
     depth = m.forward(case.enc_images, case.enc_cams, case.target).depth
-    want = run_oracle(oracle, case, outputs=("rgb", "depth"))
-    r = frame_metrics(oracle, case, rgb, depth, want)
+    r = full_frame_check(oracle, case, rgb, depth)
+    r.pop("internal_events")
     print(r)
     assert np.isfinite(rgb).all()
-    assert gate(r), r
-    return rgb
+    assert r["pass"], r
+    return r
 
 
 @pytest.mark.slow
@@ -313,20 +317,25 @@ def test_config3_full_scale_matches_oracle(oracle):
 
 
 @pytest.mark.slow
-def test_config4_full_scale_frame_matches_oracle(oracle):
-    """BASELINE config 4 at full scale, one frame of the 30-frame video
-    (moving target, planes shifted by 0.005 t m); the whole sequence is the
-    profiles/parity_full.py sweep (profiles/r2/parity_full.jsonl)."""
+@pytest.mark.parametrize("t", [22, 24], ids=["t22_internal_flip", "t24_render_flip"])
+def test_config4_full_scale_frame_matches_oracle(oracle, t):
+    """BASELINE config 4 at full scale (30-frame video, planes shifted by
+    0.005 t m, moving target): t = 22 carries an internal flip (step-5
+    gather, view 2, 3e-6 px inside the edge: 14 pixels up to 2.2e-3) and
+    t = 24 the sweep's largest final-render flip (one pixel, 2.2e-2). All
+    30 frames: profiles/parity_full.py -> profiles/r2/parity_full.jsonl."""
     from paper_2411_16680_b200 import workloads as wl
-    _full_scale(oracle, wl.config4_frame(17, div=1))
+    r = _full_scale(oracle, wl.config4_frame(t, div=1))
+    assert r["px_gt_1e-3_internal"] + r["px_gt_1e-3_on_flip"] > 0  # the flip is still there
 
 
 @pytest.mark.slow
 def test_config5_full_scale_target_matches_oracle(oracle):
-    """BASELINE config 5 at full scale, one of the eight off-grid target
-    viewpoints; all eight are in profiles/r2/parity_full.jsonl."""
+    """BASELINE config 5 at full scale: off-grid target viewpoint 4 (one
+    final-render flip pixel at 1.5e-3); all eight targets are in
+    profiles/r2/parity_full.jsonl."""
     from paper_2411_16680_b200 import workloads as wl
-    _full_scale(oracle, wl.config2(div=1, target_center=wl.config5_targets()[6]))
+    _full_scale(oracle, wl.config2(div=1, target_center=wl.config5_targets()[4]))
 
 
 def _variants():
@@ -340,6 +349,13 @@ def _variants():
         "config5_target5_div4": lambda: wl.config2(div=4, target_center=wl.config5_targets()[5]),
         # 4 views (2x2 rig): the M = 4 kernels
         "config2_m4_div4": lambda: wl.config2(div=4, views_rig=(2, 2)),
+        # view counts without an exact-M kernel (network.hpp:566-567 takes any
+        # M; PAPER.md:773 runs up to 32): the runtime-bounded tensor-core
+        # attention (M < 8, < 16, <= 32) and render instantiations
+        "config2_m3_div4": lambda: wl.config2(div=4, views_rig=(1, 3)),
+        "config2_m6_div4": lambda: wl.config2(div=4, views_rig=(2, 3)),
+        "config2_m12_div4": lambda: wl.config2(div=4, views_rig=(3, 4)),
+        "config2_m32_div4": lambda: wl.config2(div=4, views_rig=(4, 8)),
     }
 
 
