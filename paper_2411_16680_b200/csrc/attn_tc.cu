@@ -83,7 +83,8 @@ struct Smem {
   static constexpr int NS = (BUDGET - OFF_D) / D_BYTES > 8 ? 8 : (BUDGET - OFF_D) / D_BYTES;
   static constexpr int OFF_BAR = OFF_D + NS * D_BYTES;
   // bars: v_full[NV] v_empty[NV] d_full[NS] d_empty[NS] a_full[2] a_free[2] s_done o_done
-  static constexpr int NBAR = 2 * NV + 2 * NS + 4 + 2;
+  // s_free
+  static constexpr int NBAR = 2 * NV + 2 * NS + 4 + 3;
   static constexpr int BYTES = OFF_BAR + NBAR * 8 + 16;
   static_assert(NS >= 3, "shared memory budget");
 };
@@ -180,6 +181,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
   uint64_t* a_free = a_full + 2;      // [2] MMAs done reading A
   uint64_t* s_done = a_free + 2;      // S ready
   uint64_t* o_done = s_done + 1;      // O ready
+  uint64_t* s_free = o_done + 1;      // every consumer has read S (TMEM S may be rewritten)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + S::NBAR);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   tc::pdl_launch_dependents();
@@ -211,6 +213,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
     }
     tc::mbar_init(s_done, 1);
     tc::mbar_init(o_done, 1);
+    tc::mbar_init(s_free, NCONS * NGRP);
     tc::mbar_init_fence();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, tmem_cols<H>());
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
     }
   } else if (warp == 1) {
     // ---- MMA issuer: S(first); per tile i: S(i+1), then O over the heads ----
-    int u = 0;
+    int u = 0, ns = 0;
     auto next_a = [&]() {
       const int b = u & 1;
       tc::mbar_wait(&a_full[b], uint32_t((u >> 1) & 1));
@@ -257,6 +260,12 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
     };
     auto issue_s = [&]() {
       const int b = next_a();
+      // S lives in one TMEM accumulator: S(j) is written only once every
+      // consumer of both groups has read S(j-1) (with two groups the ring lets
+      // one group run up to NS slices ahead of the other)
+      if (ns > 0) tc::mbar_wait(s_free, uint32_t((ns - 1) & 1));
+      ++ns;
+      tc::fence_after();
       if (tc::elect_one()) {
         mma_split(tmem_s, sb + S::OFF_A + b * A_BYTES, sb + S::OFF_BQ, 32 * H, false);
         tc::commit(s_done);
@@ -377,6 +386,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
         for (int h = 0; h < HG; ++h)
 #pragma unroll
           for (int m = 0; m < MM; ++m) w[h][m] = has(m) ? __fdiv_rn(1.0f, float(M)) : 0.f;
+        tc::mbar_arrive(s_free);
       } else {
         float sv[HG][C];
         tc::mbar_wait(s_done, uint32_t(i & 1));
@@ -385,6 +395,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
         for (int h = 0; h < HG; ++h)
           tmem_split(tmem_s + uint32_t(32 * (grp * HG + h)), 32 * H, sv[h]);
         tc::fence_before();
+        tc::mbar_arrive(s_free);
         // views in pairs, each dot as 4 interleaved partial sums: 8 independent
         // 8-deep FMA chains instead of one 32-deep chain per (view, head)
 #pragma unroll

@@ -248,18 +248,17 @@ struct RenderArgs {
   DevRayCam rc;           // target camera re-digitised to (Wo, Ho)
   const DevCam* cams;     // [M] render cameras (device)
   DevCam pc[kRenderParamViews];  // the same by value (M <= 32; the view-count kernels)
+  FastCam fc[kRenderParamViews];  // ... folded for the fast footprint (fast_cam)
   int pc_valid;                  // pc holds the M cameras
   const float* images;    // [M, Hr, Wr, 3]
-  const float4* images4;  // optional: the same as RGBA rows [M, Hr, Wr] (expand_rgba)
   int Hr, Wr;
   float* rgb;             // [row1-row0, Wo, 3]
   float near_depth, far_depth;
   int* bad_depth;         // set when a depth leaves [near-slack, far+slack]
   double slack_lo, slack_hi;
 };
-// [n, 3] RGB -> [n] float4 rows (one 16-byte load per render tap); returns
-// the number of launches.
-int expand_rgba(const float* rgb, float4* out, int64_t n, cudaStream_t st);
+// The render's folded camera (FastCam, common.cuh) of a DevCam, on the host.
+FastCam fast_cam(const DevCam& d);
 // upsample_activate + render_target fused (ldm.hpp:193-199, :249-271).
 void render_fused(const RenderArgs& a, cudaStream_t st);
 // ForwardResult.rgb of a direct_rgb config (network.hpp:596-601): pre_a =

@@ -134,32 +134,23 @@ __device__ __forceinline__ unsigned blend_views(const RenderArgs& a, const float
     Footprint f;
     if (EXACT)
       f = project_footprint_nb(a.pc[m], pt);
-    else if (!project_footprint_fast(a.pc[m], pt, f))
+    else if (!project_footprint_fast(a.fc[m], pt, f))
       need |= 1u << m;  // f: invalid, in-range taps
     const float fx = __double2float_rn(f.fx), fy = __double2float_rn(f.fy);
     const float gx = 1.0f - fx, gy = 1.0f - fy;
     const float w[4] = {gx * gy, fx * gy, gx * fy, fx * fy};
     const int r0 = f.y0 * a.Wr, r1 = f.y1 * a.Wr;  // one view < 2^31 floats
     const float bm = f.valid ? beta[m] : 0.f;
-    if (a.images4) {
-      const float4* im4 = a.images4 + (int64_t)m * a.Hr * a.Wr;
-      const float4 c00 = __ldg(im4 + r0 + f.x0), c10 = __ldg(im4 + r0 + f.x1);
-      const float4 c01 = __ldg(im4 + r1 + f.x0), c11 = __ldg(im4 + r1 + f.x1);
-      acc[0] = fmaf(bm, fmaf(w[3], c11.x, fmaf(w[2], c01.x, fmaf(w[1], c10.x, w[0] * c00.x))), acc[0]);
-      acc[1] = fmaf(bm, fmaf(w[3], c11.y, fmaf(w[2], c01.y, fmaf(w[1], c10.y, w[0] * c00.y))), acc[1]);
-      acc[2] = fmaf(bm, fmaf(w[3], c11.z, fmaf(w[2], c01.z, fmaf(w[1], c10.z, w[0] * c00.z))), acc[2]);
-    } else {
-      const float* img = a.images + (int64_t)m * a.Hr * a.Wr * 3;
-      const float* p00 = img + (r0 + f.x0) * 3;
-      const float* p10 = img + (r0 + f.x1) * 3;
-      const float* p01 = img + (r1 + f.x0) * 3;
-      const float* p11 = img + (r1 + f.x1) * 3;
+    const float* img = a.images + (int64_t)m * a.Hr * a.Wr * 3;
+    const float* p00 = img + (r0 + f.x0) * 3;
+    const float* p10 = img + (r0 + f.x1) * 3;
+    const float* p01 = img + (r1 + f.x0) * 3;
+    const float* p11 = img + (r1 + f.x1) * 3;
 #pragma unroll
-      for (int k = 0; k < 3; ++k)
-        acc[k] = fmaf(bm, fmaf(w[3], __ldg(p11 + k),
-                               fmaf(w[2], __ldg(p01 + k), fmaf(w[1], __ldg(p10 + k), w[0] * __ldg(p00 + k)))),
-                      acc[k]);
-    }
+    for (int k = 0; k < 3; ++k)
+      acc[k] = fmaf(bm, fmaf(w[3], __ldg(p11 + k),
+                             fmaf(w[2], __ldg(p01 + k), fmaf(w[1], __ldg(p10 + k), w[0] * __ldg(p00 + k)))),
+                    acc[k]);
     wsum = fa(wsum, bm);
   }
   return need;
@@ -305,45 +296,25 @@ __global__ void direct_rgb_kernel(const RenderArgs a, const float* __restrict__ 
 
 inline int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
 
-// [n, 3] f32 -> [n] float4 (alpha 0): four pixels per thread, three 16-byte
-// loads and four 16-byte stores (n % 4 == 0, 16-byte aligned input).
-__global__ void __launch_bounds__(256) expand_rgba_kernel(const float4* __restrict__ in,
-                                                          float4* __restrict__ out, int64_t quads) {
-  pdl_grid_sync();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < quads;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 a = __ldg(in + 3 * i), b = __ldg(in + 3 * i + 1), c = __ldg(in + 3 * i + 2);
-    out[4 * i + 0] = make_float4(a.x, a.y, a.z, 0.f);
-    out[4 * i + 1] = make_float4(a.w, b.x, b.y, 0.f);
-    out[4 * i + 2] = make_float4(b.z, b.w, c.x, 0.f);
-    out[4 * i + 3] = make_float4(c.y, c.z, c.w, 0.f);
-  }
-}
-
-__global__ void expand_rgba_tail_kernel(const float* __restrict__ in, float4* __restrict__ out,
-                                        int64_t n0, int64_t n) {
-  pdl_grid_sync();
-  const int64_t i = n0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) out[i] = make_float4(in[3 * i], in[3 * i + 1], in[3 * i + 2], 0.f);
-}
-
 }  // namespace
 
-int expand_rgba(const float* rgb, float4* out, int64_t n, cudaStream_t st) {
-  const bool al = (reinterpret_cast<uintptr_t>(rgb) & 15) == 0;
-  const int64_t quads = al ? n / 4 : 0;
-  int launches = 0;
-  if (quads) {
-    const int g = int(std::min<int64_t>((quads + 255) / 256, int64_t(sm_count()) * 8));
-    launch_k(expand_rgba_kernel, g, 256, 0, st, reinterpret_cast<const float4*>(rgb), out, quads);
-    ++launches;
+FastCam fast_cam(const DevCam& d) {
+  FastCam c;
+  for (int j = 0; j < 3; ++j) {
+    c.A[0 * 3 + j] = d.fx * d.R[0 * 3 + j] + d.cx * d.R[2 * 3 + j];
+    c.A[1 * 3 + j] = d.fy * d.R[1 * 3 + j] + d.cy * d.R[2 * 3 + j];
+    c.A[2 * 3 + j] = d.R[2 * 3 + j];
   }
-  if (4 * quads < n) {
-    launch_k(expand_rgba_tail_kernel, blocks_for(n - 4 * quads, 256), 256, 0, st, rgb, out,
-             4 * quads, n);
-    ++launches;
-  }
-  return launches;
+  c.b[0] = d.fx * d.t[0] + d.cx * d.t[2];
+  c.b[1] = d.fy * d.t[1] + d.cy * d.t[2];
+  c.b[2] = d.t[2];
+  c.wm = d.wm;
+  c.hm = d.hm;
+  c.hu = d.hu;
+  c.hv = d.hv;
+  c.W = d.W;
+  c.H = d.H;
+  return c;
 }
 
 void render_fused(const RenderArgs& a, cudaStream_t st) {

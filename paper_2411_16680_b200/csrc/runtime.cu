@@ -209,7 +209,6 @@ struct lvsg_ctx {
   std::map<std::tuple<const float*, int, int>, std::unique_ptr<lvsg::Buf>> wimg;
   lvsg::Buf wimg_tmp;  // uncached image for the stage entry points
   lvsg::Buf stage_a, stage_b, stage_c, stage_cams;  // scratch of the per-stage entry points
-  lvsg::Buf ren4;  // render views as RGBA rows (expand_rgba), rewritten per render call
   lvsg::Buf attn_scratch;  // generic attention kernel rows (shapes without a tensor-core kernel)
   std::vector<float> stem_host;  // encoder stem weights [32*27] + bias [32] (host copy)
   std::vector<std::vector<float>> rayproj_host;  // per-level ray_proj [32, C] (host copies)
@@ -944,7 +943,10 @@ RenderArgs render_args(lvsg_ctx* c, const float* images, int64_t Hr, int64_t Wr,
   // the same cameras by value in the kernel's parameter space (constant-bank
   // operands, no per-view shared-memory loads)
   if (host_cams && a.M <= kRenderParamViews) {
-    for (int m = 0; m < a.M; ++m) a.pc[m] = dev_cam(host_cams[m]);
+    for (int m = 0; m < a.M; ++m) {
+      a.pc[m] = dev_cam(host_cams[m]);
+      a.fc[m] = fast_cam(a.pc[m]);
+    }
     a.pc_valid = 1;
   }
   a.images = images;
@@ -956,24 +958,6 @@ RenderArgs render_args(lvsg_ctx* c, const float* images, int64_t Hr, int64_t Wr,
   a.slack_lo = c->target.near_depth - slack;
   a.slack_hi = c->target.far_depth + slack;
   return a;
-}
-
-// The render views as RGBA rows for the M-specialised render (one 16-byte
-// load per tap instead of three 4-byte loads), on the context stream right
-// before the render that reads them. LVSG_RGBA=0 keeps the 3-channel reads.
-bool rgba_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("LVSG_RGBA");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-void use_rgba(lvsg_ctx* c, RenderArgs& a) {
-  if (!rgba_enabled() || !a.pc_valid || !a.images) return;
-  const int64_t n = int64_t(a.M) * a.Hr * a.Wr;
-  c->ren4.ensure(size_t(n) * 4);
-  mark(c, "render", expand_rgba(a.images, reinterpret_cast<float4*>(c->ren4.p), n, c->stream));
-  a.images4 = reinterpret_cast<const float4*>(c->ren4.p);
 }
 
 DevCam* upload_render_cams(lvsg_ctx* c, const lvsg_camera* cams) {
@@ -1375,7 +1359,6 @@ lvsg_status lvsg_render(lvsg_ctx* c, int64_t views, const float* const* images, 
     const int64_t Ho = c->plan.out_height, Wo = c->plan.out_width;
     c->rgb.ensure(size_t(Ho * Wo * 3));
     RenderArgs a = render_args(c, c->ren_in.p, height, width, dc, c->rgb.p, 0, Ho, cams);
-    use_rgba(c, a);
     render_fused(a, c->stream);
     CUDA_OK(cudaMemcpyAsync(rgb_out, c->rgb.p, size_t(Ho * Wo * 3) * sizeof(float),
                             cudaMemcpyDeviceToHost, c->stream));
@@ -1483,7 +1466,6 @@ lvsg_status submit_impl(lvsg_ctx* c, int64_t views, const float* const* enc_imag
     constexpr int NB = 4;
     RenderArgs a0 = render_args(c, S.ren_in.p, render_h, render_w, t.final_cams, S.rgb.p, 0, Ho,
                                 render_cams);
-    use_rgba(c, a0);
     for (int b = 0; b < NB; ++b) {
       const int64_t r0 = Ho * b / NB, r1 = Ho * (b + 1) / NB;
       if (r1 == r0) continue;
@@ -1601,7 +1583,6 @@ lvsg_status lvsg_forward_render_rows_device(lvsg_ctx* c, int64_t views, const fl
       forward_device(c, enc_images, enc_h, enc_w, enc_cams, *target, render_cams, &t);
       RenderArgs a = render_args(c, render_images, render_h, render_w, t.final_cams, rgb_out, row0,
                                  row1, render_cams);
-      use_rgba(c, a);
       render_fused(a, c->stream);
       mark(c, "render", 1);
       c->launches += 1;
@@ -1740,7 +1721,6 @@ lvsg_status lvsg_render_rows_device(lvsg_ctx* c, int64_t views, const float* ren
     DevCam* dc = upload_render_cams(c, render_cams);
     RenderArgs a = render_args(c, render_images, render_h, render_w, dc, rgb_out, row0, row1,
                                render_cams);
-    use_rgba(c, a);
     render_fused(a, c->stream);
     c->stream = own;
     CUDA_OK(cudaGetLastError());
@@ -1910,7 +1890,10 @@ lvsg_status lvsg_stage_upsample_render(lvsg_ctx* c, const lvsg_frustum* target, 
     a.rc = ray_cam(target->camera, Wo, Ho);
     a.cams = reinterpret_cast<const DevCam*>(c->stage_cams.p);
     if (M <= kRenderParamViews) {
-      for (int64_t m = 0; m < M; ++m) a.pc[m] = hc[size_t(m)];
+      for (int64_t m = 0; m < M; ++m) {
+        a.pc[m] = hc[size_t(m)];
+        a.fc[m] = fast_cam(hc[size_t(m)]);
+      }
       a.pc_valid = 1;
     }
     a.images = images;
@@ -1921,7 +1904,6 @@ lvsg_status lvsg_stage_upsample_render(lvsg_ctx* c, const lvsg_frustum* target, 
     const double slack = 1e-3 * (target->far_depth - target->near_depth);
     a.slack_lo = target->near_depth - slack;
     a.slack_hi = target->far_depth + slack;
-    use_rgba(c, a);
     render_fused(a, c->stream);
     sync_and_check(c);
   });
