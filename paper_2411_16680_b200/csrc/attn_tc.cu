@@ -15,10 +15,9 @@
 //
 // Persistent warp-specialised CTA, one per SM, 128-texel tiles:
 //   w0     TMA producer: V tiles (128B-swizzled, 4 buffers, one tile ahead of
-//          the Δ slices) and, per view, the tile's Δ slice [8 channel groups]
-//          [128 texels][16 B] (one 3-D TMA box over the view-major SoA
-//          Δ[m][g][p][4], 512-byte rows) into an NS-deep ring -- twice per tile
-//          (scores, then mix; the second read hits L2)
+//          the Δ slices) and, per view, the tile's Δ slice [128 texels][32]
+//          (one 2-D TMA box over Δ[m][p][32], 128B-swizzled) into an NS-deep
+//          ring -- twice per tile (scores, then mix; the second read hits L2)
 //   w1     MMA issuer (one elected lane; warp-uniform descriptors)
 //   w2-5   consumers (and w6-9 for h >= 2: the heads split over two groups),
 //          thread <-> texel row <-> TMEM lane, software-pipelined
@@ -48,7 +47,7 @@ constexpr int A_LBO = TILE * 16;           // 2 KB: one 8-channel plane of 128 r
 constexpr int A_HALF = NJ * A_LBO;         // 8 KB: hi (or lo') planes
 constexpr int A_BYTES = 2 * A_HALF;        // 16 KB per staging buffer
 constexpr int V_BYTES = TILE * C * 4;      // 16 KB
-constexpr int D_BYTES = NG * TILE * 16;    // one view slice, 16 KB
+constexpr int D_BYTES = TILE * C * 4;      // one view slice [128][32] fp32, 16 KB
 constexpr int NV = 4;                      // V tile buffers
 
 // h >= 2: two consumer groups (warps 2-5, 6-9) split the heads over the same
@@ -87,6 +86,7 @@ struct Smem {
   static constexpr int NBAR = 2 * NV + 2 * NS + 4 + 3;
   static constexpr int BYTES = OFF_BAR + NBAR * 8 + 16;
   static_assert(NS >= 3, "shared memory budget");
+  static_assert(OFF_D % 1024 == 0 && OFF_V % 1024 == 0, "128B-swizzled TMA destinations");
 };
 
 // A[j][row][8 halves] (hi) and A[4 + j][row] (lo') <- x[32] of this row.
@@ -137,14 +137,6 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* map, int c
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
       "[%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(tc::smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* map, int c0, int c1, int c2,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(tc::smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void tma_store_2d(const void* map, uint32_t src, int c0, int c1) {
@@ -238,13 +230,14 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
       load_v(0);
       for (int i = 0; i < ntl; ++i) {
         if (i + 1 < ntl) load_v(i + 1);
-        // one 3-D box per view slice: [8 planes][4 rows of 32 texels][128 floats]
+        // one 2-D box per view slice: rows m P + [128 i, 128 i + 128) of Δ[M P][32]
+        // (rows past P of a view are the next view's, never used; past M P: zero)
         for (int pass = 0; pass < passes; ++pass)
           for (int m = 0; m < M; ++m, ++k) {
             const int sl = k % NS;
             if (k >= NS) tc::mbar_wait(&d_empty[sl], uint32_t((k / NS - 1) & 1));
             tc::mbar_expect_tx(&d_full[sl], D_BYTES);
-            tma_load_3d(sb + S::OFF_D + sl * D_BYTES, &dmap, 0, tile_of(i) * (TILE / 32), m * NG,
+            tma_load_2d(sb + S::OFF_D + sl * D_BYTES, &dmap, 0, int(m * P) + tile_of(i) * TILE,
                         &d_full[sl]);
           }
       }
@@ -313,10 +306,10 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
     auto slice_row = [&](float* dm) {  // this texel's row of the next Δ slice
       const int sl = k % NS;
       tc::mbar_wait(&d_full[sl], uint32_t((k / NS) & 1));
-      const uint8_t* d = smem + S::OFF_D + sl * D_BYTES + row * 16;
+      const uint8_t* d = smem + S::OFF_D + sl * D_BYTES;
 #pragma unroll
       for (int g = 0; g < NG; ++g) {
-        const float4 t = *reinterpret_cast<const float4*>(d + g * TILE * 16);
+        const float4 t = *reinterpret_cast<const float4*>(d + swz(row, g));
         dm[4 * g] = t.x, dm[4 * g + 1] = t.y, dm[4 * g + 2] = t.z, dm[4 * g + 3] = t.w;
       }
       tc::mbar_arrive(&d_empty[sl]);
@@ -512,14 +505,13 @@ void launch(float* V, const float* D, int64_t P, int M, const float* wq, const f
       throw CudaError("attention: V tensor map");
   }
   {
-    // each Δ plane (m, g) as [ceil(P/32) rows][128 floats]; a partial last row
-    // reads past the plane (texels >= P are never used; the buffer has slack)
-    cuuint64_t dims[3] = {128, cuuint64_t((P + 31) / 32), cuuint64_t(M) * NG};
-    cuuint64_t strides[2] = {512, cuuint64_t(P) * 16};
-    cuuint32_t box[3] = {128, TILE / 32, NG};
-    cuuint32_t estr[3] = {1, 1, 1};
-    if (encode_fn()(&dmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(D), dims, strides,
-                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+    // Δ[m][p][32] as one 2-D map [M P rows][32 floats], 128-texel boxes (128B swizzle)
+    cuuint64_t dims[2] = {cuuint64_t(C), cuuint64_t(P) * cuuint64_t(M)};
+    cuuint64_t strides[1] = {cuuint64_t(C) * 4};
+    cuuint32_t box[2] = {cuuint32_t(C), cuuint32_t(TILE)};
+    cuuint32_t estr[2] = {1, 1};
+    if (encode_fn()(&dmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(D), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       throw CudaError("attention: delta tensor map");
   }
@@ -538,7 +530,7 @@ bool attend_tc_supported(int C_, int M, int heads) {
 bool attend_tc(float* V, const float* deltas, int64_t P, int C_, int M, int heads, const float* wq,
                const float* wo, const float* gain, int zero_scores, cudaStream_t st) {
   if (C_ != C || !encode_fn() || (reinterpret_cast<uintptr_t>(V) & 15) ||
-      (reinterpret_cast<uintptr_t>(deltas) & 15) || P >= (int64_t(1) << 31))
+      (reinterpret_cast<uintptr_t>(deltas) & 15) || P * M >= (int64_t(1) << 31))
     return false;
 #define LVSG_ATT(HH)                                                                  \
   if (heads == HH) {                                                                  \

@@ -131,19 +131,17 @@ __global__ void __launch_bounds__(128) blend_logits32_kernel(const float* __rest
     }
   }
   const float inv_temp = __double2float_rn(1.0 / sqrt(double(C)));
-  const float4* d4 = reinterpret_cast<const float4*>(D) + p;  // Δ[m][g][p][4]
   float out[M];
 #pragma unroll
   for (int m = 0; m < M; ++m) {
-    const float4* dm4 = d4 + (int64_t)m * (C / 4) * P;
+    const float* dm = D + ((int64_t)m * P + p) * C;  // Δ[m][p][32]: one 128-byte row
     float acc = 0.f;
 #pragma unroll
-    for (int c4 = 0; c4 < C / 4; ++c4) {
-      const float4 t = __ldg(dm4 + c4 * P);
-      acc = fmaf(q[4 * c4], t.x, acc);
-      acc = fmaf(q[4 * c4 + 1], t.y, acc);
-      acc = fmaf(q[4 * c4 + 2], t.z, acc);
-      acc = fmaf(q[4 * c4 + 3], t.w, acc);
+    for (int c8 = 0; c8 < C / 8; ++c8) {
+      float t[8];
+      ldg256(dm + 8 * c8, t);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc = fmaf(q[8 * c8 + k], t[k], acc);
     }
     out[m] = fm(acc, inv_temp);
   }
@@ -197,13 +195,14 @@ __global__ void __launch_bounds__(128) decode_payload32_kernel(
       acc[4 * c4 + 3] = fmaf(vk, w.w, acc[4 * c4 + 3]);
     }
   }
-  // payload row padded to 36 floats: [a(32), sigma, 0, 0, 0]
-  float4* pay = reinterpret_cast<float4*>(payload + (int64_t)p * (C + 4));
+  // payload row padded to 40 floats (32-byte rows): [a(32), sigma, 0 x 7]
+  float4* pay = reinterpret_cast<float4*>(payload + (int64_t)p * (C + 8));
 #pragma unroll
   for (int c4 = 0; c4 < C / 4; ++c4)
     pay[c4] = make_float4(sigmoid_ref(acc[4 * c4]), sigmoid_ref(acc[4 * c4 + 1]),
                           sigmoid_ref(acc[4 * c4 + 2]), sigmoid_ref(acc[4 * c4 + 3]));
   pay[C / 4] = make_float4(sigmoid_ref(acc[C]), 0.f, 0.f, 0.f);
+  pay[C / 4 + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
   const int q = p / W, j = p - q * W;
   const int l = q / H, i = q - l * H;
   const float d = activate_depth(acc[C + 1], l, act);

@@ -430,8 +430,7 @@ __global__ void __launch_bounds__(128) ray_project32_kernel(const float* __restr
 // One thread per (texel, view); consecutive threads = consecutive texels of
 // one view. The world point and footprint are computed once (f64, bit-exact
 // order); the 4 taps are read as whole channel rows and the result is written
-// in the view-major SoA layout Δ[m][g][p][4] (g = channel group of 4), so the
-// stores here and every Stage-2 read of Δ are fully coalesced.
+// as the texel-view's row of Δ[m][p][C].
 template <bool kVec4>
 __global__ void gather_stack_kernel(const float* __restrict__ feats, int M, int Hf, int Wf, int C,
                                     const DevCam* __restrict__ cams, DevRayCam rc,
@@ -449,9 +448,9 @@ __global__ void gather_stack_kernel(const float* __restrict__ feats, int M, int 
   float pt[3];
   world_point(rc, ii, j, __ldg(depth + p), pt);
   const Footprint f = project_footprint(cams[m], pt);
-  float4* o = reinterpret_cast<float4*>(deltas) + (int64_t)m * G * P + p;
+  float* o = deltas + ((int64_t)m * P + p) * C;
   if (!f.valid) {
-    for (int g = 0; g < G; ++g) o[g * P] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = 0; c < C; ++c) o[c] = 0.f;
     return;
   }
   double w[4];
@@ -467,28 +466,29 @@ __global__ void gather_stack_kernel(const float* __restrict__ feats, int M, int 
       const float4 b = __ldg(reinterpret_cast<const float4*>(i10) + g);
       const float4 c = __ldg(reinterpret_cast<const float4*>(i01) + g);
       const float4 d = __ldg(reinterpret_cast<const float4*>(i11) + g);
-      o[g * P] = make_float4(blend4(w, a.x, b.x, c.x, d.x), blend4(w, a.y, b.y, c.y, d.y),
-                             blend4(w, a.z, b.z, c.z, d.z), blend4(w, a.w, b.w, c.w, d.w));
+      reinterpret_cast<float4*>(o)[g] =
+          make_float4(blend4(w, a.x, b.x, c.x, d.x), blend4(w, a.y, b.y, c.y, d.y),
+                      blend4(w, a.z, b.z, c.z, d.z), blend4(w, a.w, b.w, c.w, d.w));
     }
   } else {
-    for (int g = 0; g < G; ++g) {
-      float v[4];
-      for (int k = 0; k < 4; ++k) {
-        const int c = 4 * g + k;
-        v[k] = c < C ? blend4(w, __ldg(i00 + c), __ldg(i10 + c), __ldg(i01 + c), __ldg(i11 + c)) : 0.f;
-      }
-      o[g * P] = make_float4(v[0], v[1], v[2], v[3]);
-    }
+    for (int c = 0; c < C; ++c) o[c] = blend4(w, __ldg(i00 + c), __ldg(i10 + c), __ldg(i01 + c), __ldg(i11 + c));
   }
 }
 
 // C = 32: each lane computes one (view, texel) footprint as above (f64,
-// bit-exact taps / validity / weights); the 32 footprints of a warp are then
-// consumed by 8-lane groups, lane g of a group loading channel group g of the
-// 4 taps, so one load instruction touches 4 feature rows instead of 32 (the
-// per-lane version is L1-wavefront bound). The 4-tap blend of Δ is an f32 FMA
-// chain over the f64 weights rounded to f32 (within ~2 ulp of the reference's
-// f64 blend; the parity gate is the RGB tolerance).
+// bit-exact taps / validity / weights). The warp's 32 texel-views (32
+// consecutive texels of one output row, mostly) are then consumed by four
+// 8-lane groups, group q taking texel-views 8q .. 8q+7 in order and lane g of
+// the group channel group g (16 bytes) of each 128-byte feature row. Adjacent
+// texels project to adjacent feature cells (about one feature pixel per
+// texel), so a group keeps the previous texel-view's two tap columns in
+// registers: when the cell is the same, or the next one to the right, only
+// the new right column is loaded -- about 2 of the 4 tap rows per
+// texel-view instead of 4, which halves the L1 wavefronts this kernel is
+// bound by. Stores are one 128-byte row of Δ[m][p][32] per texel-view. The
+// 4-tap blend is an f32 FMA chain over the f64 weights rounded to f32
+// (within ~2 ulp of the reference's f64 blend; the parity gate is the RGB
+// tolerance), the same values whichever loads were reused.
 __global__ void __launch_bounds__(256) gather_stack32_kernel(
     const float* __restrict__ feats, int M, int Hf, int Wf, const DevCam* __restrict__ cams,
     DevRayCam rc, const float* __restrict__ depth, int L, int H, int W, float* __restrict__ deltas) {
@@ -521,10 +521,14 @@ __global__ void __launch_bounds__(256) gather_stack32_kernel(
   }
   const float4* f4 = reinterpret_cast<const float4*>(feats);
   float4* o4 = reinterpret_cast<float4*>(deltas);
-  const int g = lane & 7;
+  const int g = lane & 7, q = lane >> 3;
+  // the group's previous texel-view: tap-00 offset and flags (-1: none) and
+  // its left (x0) / right (x1) columns at rows y0 / y1
+  int poff = -1, pfl = 0;
+  float4 l0 = make_float4(0.f, 0.f, 0.f, 0.f), l1 = l0, r0 = l0, r1 = l0;
 #pragma unroll 2
   for (int it = 0; it < 8; ++it) {
-    const int r = 4 * it + (lane >> 3);
+    const int r = 8 * q + it;
     const int rf = __shfl_sync(0xffffffffu, flags, r);
     const int rm = __shfl_sync(0xffffffffu, m, r);
     const int rp = __shfl_sync(0xffffffffu, pl, r);
@@ -536,16 +540,32 @@ __global__ void __launch_bounds__(256) gather_stack32_kernel(
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (rf & 1) {
       const int dx = (rf & 2) ? G : 0, dy = (rf & 4) ? Wf * G : 0;
-      const float4 a = __ldg(f4 + ro);
-      const float4 b = __ldg(f4 + ro + dx);
-      const float4 c = __ldg(f4 + ro + dy);
-      const float4 d = __ldg(f4 + ro + dy + dx);
+      const bool same_rows = poff >= 0 && ((rf ^ pfl) & 4) == 0;
+      if (same_rows && ro == poff) {
+        // the same cell: both columns already in registers
+      } else if (same_rows && ro == poff + G && (pfl & 2) && dx) {
+        // the next cell to the right: the old right column becomes the left
+        l0 = r0;
+        l1 = r1;
+        r0 = __ldg(f4 + ro + dx);
+        r1 = dy ? __ldg(f4 + ro + dy + dx) : r0;
+      } else {
+        l0 = __ldg(f4 + ro);
+        l1 = dy ? __ldg(f4 + ro + dy) : l0;
+        r0 = dx ? __ldg(f4 + ro + dx) : l0;
+        r1 = dx ? (dy ? __ldg(f4 + ro + dy + dx) : r0) : l1;
+      }
+      poff = ro;
+      pfl = rf;
+      const float4 a = l0, b = r0, c = l1, d = r1;
       v.x = fmaf(rw[3], d.x, fmaf(rw[2], c.x, fmaf(rw[1], b.x, rw[0] * a.x)));
       v.y = fmaf(rw[3], d.y, fmaf(rw[2], c.y, fmaf(rw[1], b.y, rw[0] * a.y)));
       v.z = fmaf(rw[3], d.z, fmaf(rw[2], c.z, fmaf(rw[1], b.z, rw[0] * a.z)));
       v.w = fmaf(rw[3], d.w, fmaf(rw[2], c.w, fmaf(rw[1], b.w, rw[0] * a.w)));
+    } else {
+      poff = -1;
     }
-    o4[((int64_t)rm * G + g) * P + rp] = v;
+    o4[((int64_t)rm * P + rp) * G + g] = v;
   }
 }
 
@@ -571,7 +591,7 @@ __global__ void decode_payload_kernel(const float* __restrict__ V, int L, int H,
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= P) return;
   const float* v = V + p * C;
-  float* pay = payload + p * pay_stride(Ca + 1);
+  float* pay = payload + p * payload_stride(Ca + 1);
   // matmul order: k ascending from 0 (kernels_ref.hpp:40-48)
   for (int c = 0; c < Ca + 2; ++c) {
     float acc = 0.f;
@@ -628,7 +648,7 @@ __global__ void attend_generic_kernel(float* V, const float* __restrict__ D, int
       float mx = 0.f;
       for (int m = 0; m < M; ++m) {
         float acc = 0.f;
-        for (int c = 0; c < C; ++c) acc = fmaf(s[c], D[((int64_t)(m * ((C + 3) / 4) + c / 4) * P + p) * 4 + (c & 3)], acc);
+        for (int c = 0; c < C; ++c) acc = fmaf(s[c], D[((int64_t)m * P + p) * C + c], acc);
         w[m] = fm(acc, inv_temp);
         mx = m == 0 ? w[m] : fmaxf(mx, w[m]);
       }
@@ -639,7 +659,7 @@ __global__ void attend_generic_kernel(float* V, const float* __restrict__ D, int
     }
     for (int c = 0; c < C; ++c) {
       float acc = 0.f;
-      for (int m = 0; m < M; ++m) acc = fmaf(w[m], D[((int64_t)(m * ((C + 3) / 4) + c / 4) * P + p) * 4 + (c & 3)], acc);
+      for (int m = 0; m < M; ++m) acc = fmaf(w[m], D[((int64_t)m * P + p) * C + c], acc);
       hd[c] = acc;
     }
     for (int c = 0; c < C; ++c) {
@@ -674,7 +694,7 @@ __global__ void blend_logits_kernel(const float* __restrict__ V, const float* __
   }
   for (int m = 0; m < M; ++m) {
     float acc = 0.f;
-    for (int c = 0; c < Cq; ++c) acc = fmaf(q[c], D[((int64_t)(m * ((C + 3) / 4) + c / 4) * P + p) * 4 + (c & 3)], acc);
+    for (int c = 0; c < Cq; ++c) acc = fmaf(q[c], D[((int64_t)m * P + p) * C + c], acc);
     logits[p * M + m] = fm(acc, inv_temp);
   }
 }
@@ -970,27 +990,24 @@ void decode_payload(const float* V, int L, int H, int W, int C, const float* w_a
       V, L, H, W, C, w_appear, Ca, w_sigma, w_depth, act, rc, payload, depth, points);
 }
 
-__global__ void deltas_to_soa_kernel(const float* __restrict__ src, float* __restrict__ dst,
-                                     int64_t P, int M, int C) {
+__global__ void deltas_to_view_major_kernel(const float* __restrict__ src, float* __restrict__ dst,
+                                            int64_t P, int M, int C) {
   pdl_grid_sync();
-  const int G = (C + 3) / 4;
-  const int64_t n = P * M * G * 4;
+  const int64_t n = P * M * C;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
-    // e enumerates dst: ((m * G + g) * P + p) * 4 + k
-    const int k = int(e & 3);
-    const int64_t r = e >> 2;
+    // e enumerates dst: (m * P + p) * C + c
+    const int c = int(e % C);
+    const int64_t r = e / C;
     const int64_t p = r % P;
-    const int mg = int(r / P);
-    const int g = mg % G, m = mg / G;
-    const int ch = g * 4 + k;
-    dst[e] = ch < C ? src[(p * M + m) * C + ch] : 0.f;
+    const int m = int(r / P);
+    dst[e] = src[(p * M + m) * C + c];
   }
 }
-void deltas_to_soa(const float* src, float* dst, int64_t P, int M, int C, cudaStream_t st) {
-  const int64_t n = P * M * ((C + 3) / 4) * 4;
-  launch_k(deltas_to_soa_kernel, int(std::min<int64_t>((n + 255) / 256, 148 * 16)), 256, 0, st, src,
-           dst, P, M, C);
+void deltas_to_view_major(const float* src, float* dst, int64_t P, int M, int C, cudaStream_t st) {
+  const int64_t n = P * M * C;
+  launch_k(deltas_to_view_major_kernel, int(std::min<int64_t>((n + 255) / 256, 148 * 16)), 256, 0,
+           st, src, dst, P, M, C);
 }
 void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
             const float* const* wq_heads, const float* wo, const float* gain, int zero_scores,

@@ -165,7 +165,9 @@ void ray_project(const float* base, int M, int hK, int wK, int Hk, int Wk, const
 
 // ---- geometry --------------------------------------------------------------
 // Δ[p, m, :] = gather of feats[m] ([M, Hf, Wf, C]) at world_point(p) through
-// cams[m] (backproject_stack, network.hpp:421-436; invalid -> 0).
+// cams[m] (backproject_stack, network.hpp:421-436; invalid -> 0), stored
+// texel-major per view: deltas[m][p][C] (one contiguous C-float row per
+// texel-view; Stage 2 reads 128-texel slices of it with 2-D TMA boxes).
 void gather_stack(const float* feats, int M, int Hf, int Wf, int C, const DevCam* cams_dev,
                   const DevRayCam& rc, const float* depth, int L, int H, int W, float* deltas,
                   cudaStream_t st);
@@ -175,6 +177,9 @@ void gather_stack(const float* feats, int M, int Hf, int Wf, int C, const DevCam
 // and the composited feedback carry K = Ca+1 channels, the splat
 // accumulators K+1 (the bilinear weight sum).
 __host__ __device__ inline int pay_stride(int K) { return (K + 3) & ~3; }
+// Row stride of the splat's input payload [P, K]: 32-byte rows, so the
+// reduction loads each row with 256-bit loads (C = 32: 40 floats).
+__host__ __device__ inline int payload_stride(int K) { return (K + 7) & ~7; }
 __host__ __device__ inline int acc_stride(int K) { return (K + 1 + 3) & ~3; }
 
 // render_to_input_view decode (ldm.hpp:229-235): payload [P, Ca+1] =
@@ -197,8 +202,8 @@ void splat_det(const float* payload, const float* points, int L, int PL, int K,
 
 // ---- attention / fusion ----------------------------------------------------
 // Δ from the reference layout [P, M, C] (network.hpp:421-436) into the
-// kernels' view-major SoA [M][ceil(C/4)][P][4] (stage entry points).
-void deltas_to_soa(const float* src, float* dst, int64_t P, int M, int C, cudaStream_t st);
+// kernels' layout [M][P][C] (texel-major per view; stage entry points).
+void deltas_to_view_major(const float* src, float* dst, int64_t P, int M, int C, cudaStream_t st);
 // V += OTM(rms_norm(V), Δ) (attention.hpp:207-252), in place. scratch:
 // attend_scratch_floats(P, C, M, heads) floats of device memory from the
 // caller's arena (the generic fallback's per-texel rows; none for the

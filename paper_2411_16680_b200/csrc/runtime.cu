@@ -386,8 +386,8 @@ void ensure_plan(lvsg_ctx* c, int64_t He, int64_t We) {
     maxV = std::max({maxV, size_t(sp.in_layers * sp.in_height * sp.in_width),
                      size_t(sp.layers * sp.height * sp.width)});
     maxIn = std::max(maxIn, size_t(sp.layers * sp.in_height * sp.in_width));
-    // Δ in the view-major SoA layout [M][ceil(C/4)][P][4]
-    maxD = std::max(maxD, size_t(sp.layers * sp.height * sp.width * M * ((C + 3) / 4) * 4));
+    // Δ texel-major per view [M][P][C]
+    maxD = std::max(maxD, size_t(sp.layers * sp.height * sp.width * M * C));
     maxU = std::max(maxU, size_t(M * sp.feat_h * sp.feat_w));
     // deterministic splat over the volume entering the step (at most
     // max(in_layers, layers) x in_height x in_width texels, all views):
@@ -405,7 +405,7 @@ void ensure_plan(lvsg_ctx* c, int64_t He, int64_t We) {
   c->uh.ensure(maxU * C);
   c->ut.ensure(maxU * C);
   c->uu.ensure(maxU * C);
-  c->payload.ensure(maxIn * pay_stride(int(Ca) + 1));
+  c->payload.ensure(maxIn * payload_stride(int(Ca) + 1));
   c->depth_in.ensure(maxIn);
   c->points.ensure(maxIn * 3);
   c->depth_out.ensure(maxV);
@@ -1320,18 +1320,13 @@ lvsg_status lvsg_forward(lvsg_ctx* c, int64_t views, const float* const* images,
       d2h(out->blend_logits, c->logits.p, P * M);
       d2h(out->volume, c->V, P * C);
       if (out->deltas) {
-        // device layout: view-major SoA [M][G = ceil(C/4)][P][4] (channels
-        // padded to 4G) -> [L,H,W,M,C]
-        const int64_t G = (C + 3) / 4;
-        std::vector<float> soa(size_t(P * M * G * 4));
-        d2h(soa.data(), c->deltas.p, P * M * G * 4);
+        // device layout: texel-major per view [M][P][C] -> [L,H,W,M,C]
+        std::vector<float> dev(size_t(P * M * C));
+        d2h(dev.data(), c->deltas.p, P * M * C);
         for (int64_t m = 0; m < M; ++m)
-          for (int64_t g = 0; g < G; ++g) {
-            const int64_t n = std::min<int64_t>(4, C - 4 * g);
-            for (int64_t p = 0; p < P; ++p)
-              std::memcpy(out->deltas + (p * M + m) * C + 4 * g,
-                          soa.data() + ((m * G + g) * P + p) * 4, size_t(n) * sizeof(float));
-          }
+          for (int64_t p = 0; p < P; ++p)
+            std::memcpy(out->deltas + (p * M + m) * C, dev.data() + (m * P + p) * C,
+                        size_t(C) * sizeof(float));
       }
       if (out->rgb && c->cfg.direct_rgb) {
         const int64_t Ho = c->plan.out_height, Wo = c->plan.out_width;
@@ -1841,11 +1836,10 @@ lvsg_status lvsg_stage_attend(lvsg_ctx* c, float* V, const float* deltas, int64_
   return guard(c, [&] {
     const int C = int(c->cfg.channels);
     if (P < 1 || M < 1 || heads < 1 || heads > 8) throw DimError("attend_residual: bad shapes");
-    // Δ from the reference layout [P, M, C] into the kernels' view-major SoA
-    // [M][ceil(C/4)][P][4] (+ slack for the attention's partial Δ rows)
-    const size_t n = size_t(P) * M * ((C + 3) / 4) * 4;
+    // Δ from the reference layout [P, M, C] into the kernels' [M][P][C]
+    const size_t n = size_t(P) * M * C;
     c->stage_a.ensure(n + 128);
-    deltas_to_soa(deltas, c->stage_a.p, P, int(M), C, c->stream);
+    deltas_to_view_major(deltas, c->stage_a.p, P, int(M), C, c->stream);
     c->attn_scratch.ensure(attend_scratch_floats(P, C, int(M), int(heads)));
     attend(V, c->stage_a.p, P, C, int(M), int(heads), wq, nullptr, wo, gain, zero_scores,
            c->attn_scratch.p, c->stream);
@@ -1920,7 +1914,7 @@ lvsg_status lvsg_stage_render_to_view(lvsg_ctx* c, const lvsg_frustum* target, c
     if (L < 1 || H < 1 || W < 1 || Ca < 1) throw DimError("render_to_input_view: bad shapes");
     const int64_t P = L * H * W, Hv = cam->height, Wv = cam->width;
     const int K = int(Ca) + 1, PS = pay_stride(K);
-    c->stage_a.ensure(size_t(P) * PS);      // payload
+    c->stage_a.ensure(size_t(P) * payload_stride(K));  // payload
     c->stage_b.ensure(size_t(P) * 4);       // depth + points
     c->stage_c.ensure(size_t(Hv * Wv) * PS + splat_det_scratch_ints(P, L * Hv * Wv));
     float* depth = c->stage_b.p;

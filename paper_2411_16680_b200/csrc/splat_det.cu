@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(288) splat_reduce_composite_kernel(
   const int64_t pix = live ? t % PV : 0;
   const int m = live ? int(t / PV) : 0;
   const int Ca = K - 1, gs = Ca / 4, ks = Ca % 4;
+  const int GP = payload_stride(K) / 4;  // float4 per payload row
   const float4* pay4 = reinterpret_cast<const float4*>(payload);
   float o[4] = {0.f, 0.f, 0.f, 0.f};
   for (int l = 0; l < L; ++l) {
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(288) splat_reduce_composite_kernel(
         float4 v[kRun];
 #pragma unroll
         for (int k = 0; k < kRun; ++k)
-          if (k < n) v[k] = __ldg(pay4 + (int64_t)(e[k].x >> 2) * G + g);
+          if (k < n) v[k] = __ldg(pay4 + (int64_t)(e[k].x >> 2) * GP + g);
 #pragma unroll
         for (int k = 0; k < kRun; ++k)
           if (k < n) add(e[k], v[k]);
@@ -248,7 +249,7 @@ __global__ void __launch_bounds__(288) splat_reduce_composite_kernel(
             if (ej.x > last && ej.x < best.x) best = ej;
           }
           last = best.x;
-          add(best, __ldg(pay4 + (int64_t)(best.x >> 2) * G + g));
+          add(best, __ldg(pay4 + (int64_t)(best.x >> 2) * GP + g));
         }
       }
       if (g == gs) s_sig[lp] = acc[ks];
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(192) splat_reduce_pl_kernel(
   extern __shared__ float s_val[];  // [ppb][L][NG*4]: normalised channels, [Ca] = alpha
   const int64_t PV = (int64_t)Hv * Wv;
   const int Ca = K - 1;
-  const float4* pay4 = reinterpret_cast<const float4*>(payload);
+  const int GP = payload_stride(K) / 4;  // float4 per payload row (>= NG)
   const int64_t t0 = (int64_t)blockIdx.x * ppb;  // first (m, pixel) of the block
   const int lp = threadIdx.x / L, l = threadIdx.x - lp * L;
   const int64_t t = t0 + lp;
@@ -300,18 +301,20 @@ __global__ void __launch_bounds__(192) splat_reduce_pl_kernel(
     for (int c = 0; c < NG * 4; ++c) acc[c] = 0.f;
     float ws = 0.f;
     auto add = [&](const int2 en) {
+      // the payload row (32-byte aligned, payload_stride floats): the first
+      // 32 channels by four 256-bit loads, the rest by 16-byte loads
       const float w = __int_as_float(en.y);
-      const float4* row = pay4 + (int64_t)(en.x >> 2) * NG;
-      float4 v[NG];
+      const float* row = payload + (int64_t)(en.x >> 2) * (4 * GP);
+      float v[NG * 4];
 #pragma unroll
-      for (int q = 0; q < NG; ++q) v[q] = __ldg(row + q);
+      for (int q = 0; q < NG / 2; ++q) ldg256(row + 8 * q, v + 8 * q);
 #pragma unroll
-      for (int q = 0; q < NG; ++q) {
-        acc[4 * q] = fa(acc[4 * q], fm(w, v[q].x));
-        acc[4 * q + 1] = fa(acc[4 * q + 1], fm(w, v[q].y));
-        acc[4 * q + 2] = fa(acc[4 * q + 2], fm(w, v[q].z));
-        acc[4 * q + 3] = fa(acc[4 * q + 3], fm(w, v[q].w));
+      for (int q = 2 * (NG / 2); q < NG; ++q) {
+        const float4 t4 = __ldg(reinterpret_cast<const float4*>(row) + q);
+        v[4 * q] = t4.x, v[4 * q + 1] = t4.y, v[4 * q + 2] = t4.z, v[4 * q + 3] = t4.w;
       }
+#pragma unroll
+      for (int c = 0; c < NG * 4; ++c) acc[c] = fa(acc[c], fm(w, v[c]));
       ws = fa(ws, w);
     };
     const int64_t bin = ((int64_t)m * L + l) * PV + pix;
