@@ -82,8 +82,8 @@ struct Smem {
   static constexpr int NS = (BUDGET - OFF_D) / D_BYTES > 8 ? 8 : (BUDGET - OFF_D) / D_BYTES;
   static constexpr int OFF_BAR = OFF_D + NS * D_BYTES;
   // bars: v_full[NV] v_empty[NV] d_full[NS] d_empty[NS] a_full[2] a_free[2] s_done o_done
-  // s_free
-  static constexpr int NBAR = 2 * NV + 2 * NS + 4 + 3;
+  // s_free w_full
+  static constexpr int NBAR = 2 * NV + 2 * NS + 4 + 4;
   static constexpr int BYTES = OFF_BAR + NBAR * 8 + 16;
   static_assert(NS >= 3, "shared memory budget");
   static_assert(OFF_D % 1024 == 0 && OFF_V % 1024 == 0, "128B-swizzled TMA destinations");
@@ -93,9 +93,9 @@ struct Smem {
 __device__ __forceinline__ void stage_row(uint8_t* a, int row, const float* x) {
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
-    __align__(16) __half h[8], l[8];
+    __align__(16) __half2 h[4], l[4];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) tc::split_f16(x[8 * j + k], h[k], l[k]);
+    for (int k = 0; k < 4; ++k) tc::split_f16x2(x[8 * j + 2 * k], x[8 * j + 2 * k + 1], h[k], l[k]);
     *reinterpret_cast<uint4*>(a + j * A_LBO + row * 16) = *reinterpret_cast<uint4*>(h);
     *reinterpret_cast<uint4*>(a + A_HALF + j * A_LBO + row * 16) = *reinterpret_cast<uint4*>(l);
   }
@@ -157,7 +157,8 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
     attend_tc_kernel(const __grid_constant__ CUtensorMap vmap,
                      const __grid_constant__ CUtensorMap dmap, int64_t P,
                      const float* __restrict__ wq, const float* __restrict__ wo,
-                     const float* __restrict__ gain, int zero_scores, int num_tiles, int Mr) {
+                     const float* __restrict__ gain, int zero_scores, int num_tiles, int Mr,
+                     const uint8_t* __restrict__ wimg) {
   const int M = EXACT ? MM : Mr;
   auto has = [&](int m) { return EXACT || m < Mr; };
   using S = Smem<H>;
@@ -174,6 +175,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
   uint64_t* s_done = a_free + 2;      // S ready
   uint64_t* o_done = s_done + 1;      // O ready
   uint64_t* s_free = o_done + 1;      // every consumer has read S (TMEM S may be rewritten)
+  uint64_t* w_full = s_free + 1;      // pre-split weight image landed (wimg != nullptr)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + S::NBAR);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   tc::pdl_launch_dependents();
@@ -185,11 +187,14 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
   auto tile_of = [&](int i) { return int(blockIdx.x) + i * int(gridDim.x); };
 
   // resident weights: Bq rows n = 32*i + c -> Wq_i[k][c]; Bo_i rows n -> Wo[32i + k][n]
-  stage_weights(smem + S::OFF_BQ, 32 * H, tid, NTH,
-                [&](int n, int k) { return __ldg(wq + ((n >> 5) * C + k) * C + (n & 31)); });
-  for (int h = 0; h < H; ++h)
-    stage_weights(smem + S::OFF_BO + h * S::BO_BYTES, 32, tid, NTH,
-                  [&](int n, int k) { return __ldg(wo + (h * C + k) * C + n); });
+  // (split here unless the context's pre-split image is given: one bulk copy)
+  if (!wimg) {
+    stage_weights(smem + S::OFF_BQ, 32 * H, tid, NTH,
+                  [&](int n, int k) { return __ldg(wq + ((n >> 5) * C + k) * C + (n & 31)); });
+    for (int h = 0; h < H; ++h)
+      stage_weights(smem + S::OFF_BO + h * S::BO_BYTES, 32, tid, NTH,
+                    [&](int n, int k) { return __ldg(wo + (h * C + k) * C + n); });
+  }
   if (tid == 0) {
     for (int k = 0; k < NV; ++k) {
       tc::mbar_init(&v_full[k], 1);
@@ -206,6 +211,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
     tc::mbar_init(s_done, 1);
     tc::mbar_init(o_done, 1);
     tc::mbar_init(s_free, NCONS * NGRP);
+    tc::mbar_init(w_full, 1);
     tc::mbar_init_fence();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, tmem_cols<H>());
@@ -216,6 +222,10 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);  // warp-uniform
   const uint32_t tmem_s = tmem, tmem_o = tmem + 64 * H;
   tc::pdl_wait();  // the prologue above overlaps the previous kernel (weights are static)
+  if (wimg && tid == 0) {
+    tc::mbar_expect_tx(w_full, S::BQ_BYTES + H * S::BO_BYTES);
+    tc::bulk_load(sb + S::OFF_BQ, wimg, S::BQ_BYTES + H * S::BO_BYTES, w_full);
+  }
 
   if (warp == 0) {
     // ---- producer: V(i+1) is issued before tile i's slices ----
@@ -245,6 +255,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
   } else if (warp == 1) {
     // ---- MMA issuer: S(first); per tile i: S(i+1), then O over the heads ----
     int u = 0, ns = 0;
+    if (wimg) tc::mbar_wait(w_full, 0);
     auto next_a = [&]() {
       const int b = u & 1;
       tc::mbar_wait(&a_full[b], uint32_t((u >> 1) & 1));
@@ -487,7 +498,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 template <int H, int MM, bool EXACT>
 void launch(float* V, const float* D, int64_t P, int M, const float* wq, const float* wo,
-            const float* gain, int zero, cudaStream_t st) {
+            const float* gain, int zero, const void* wimg, cudaStream_t st) {
   smem_optin(reinterpret_cast<const void*>(attend_tc_kernel<H, MM, EXACT>), Smem<H>::BYTES);
   const int sms = sm_count();
   // V [P][32] fp32 as a 2-D map, 128-texel boxes (128B swizzle)
@@ -518,34 +529,70 @@ void launch(float* V, const float* D, int64_t P, int M, const float* wq, const f
   const int tiles = int((P + TILE - 1) / TILE);
   const int grid = tiles < sms ? tiles : sms;
   launch_pdl(true, attend_tc_kernel<H, MM, EXACT>, grid, nthreads<H>(), Smem<H>::BYTES, st, vmap,
-             dmap, P, wq, wo, gain, zero, tiles, M);
+             dmap, P, wq, wo, gain, zero, tiles, M, static_cast<const uint8_t*>(wimg));
+}
+
+// The weight image of attend_tc_kernel<H>'s resident B operands, in its
+// shared-memory layout: [Wq hi ; Wq lo'] for all heads, then per head
+// [Wo hi ; Wo lo'] (stage_weights), made once per weight binding.
+template <int H>
+__global__ void attend_tc_weights_kernel(const float* __restrict__ wq, const float* __restrict__ wo,
+                                         uint8_t* out) {
+  pdl_grid_sync();
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  stage_weights(out, 32 * H, tid, nt,
+                [&](int n, int k) { return __ldg(wq + ((n >> 5) * C + k) * C + (n & 31)); });
+  for (int h = 0; h < H; ++h)
+    stage_weights(out + Smem<H>::BQ_BYTES + h * Smem<H>::BO_BYTES, 32, tid, nt,
+                  [&](int n, int k) { return __ldg(wo + (h * C + k) * C + n); });
 }
 
 }  // namespace
+
+size_t attend_tc_weight_bytes(int heads) {
+  switch (heads) {
+    case 1: return Smem<1>::BQ_BYTES + Smem<1>::BO_BYTES;
+    case 2: return Smem<2>::BQ_BYTES + 2 * Smem<2>::BO_BYTES;
+    case 4: return Smem<4>::BQ_BYTES + 4 * Smem<4>::BO_BYTES;
+    default: return 0;
+  }
+}
+
+void attend_tc_prepare(const float* wq, const float* wo, int heads, void* dst, cudaStream_t st) {
+  uint8_t* o = static_cast<uint8_t*>(dst);
+  switch (heads) {
+    case 1: launch_k(attend_tc_weights_kernel<1>, 8, 256, 0, st, wq, wo, o); break;
+    case 2: launch_k(attend_tc_weights_kernel<2>, 8, 256, 0, st, wq, wo, o); break;
+    case 4: launch_k(attend_tc_weights_kernel<4>, 8, 256, 0, st, wq, wo, o); break;
+    default: break;
+  }
+}
 
 bool attend_tc_supported(int C_, int M, int heads) {
   return C_ == C && (heads == 1 || heads == 2 || heads == 4) && M >= 1 && M <= 32;
 }
 
 bool attend_tc(float* V, const float* deltas, int64_t P, int C_, int M, int heads, const float* wq,
-               const float* wo, const float* gain, int zero_scores, cudaStream_t st) {
+               const float* wo, const float* gain, int zero_scores, const void* wimg,
+               cudaStream_t st) {
+  if (wimg && (reinterpret_cast<uintptr_t>(wimg) & 15)) return false;
   if (C_ != C || !encode_fn() || (reinterpret_cast<uintptr_t>(V) & 15) ||
       (reinterpret_cast<uintptr_t>(deltas) & 15) || P * M >= (int64_t(1) << 31))
     return false;
 #define LVSG_ATT(HH)                                                                  \
   if (heads == HH) {                                                                  \
     switch (M) {                                                                      \
-      case 2: launch<HH, 2, true>(V, deltas, P, M, wq, wo, gain, zero_scores, st); break;   \
-      case 4: launch<HH, 4, true>(V, deltas, P, M, wq, wo, gain, zero_scores, st); break;   \
-      case 8: launch<HH, 8, true>(V, deltas, P, M, wq, wo, gain, zero_scores, st); break;   \
-      case 16: launch<HH, 16, true>(V, deltas, P, M, wq, wo, gain, zero_scores, st); break; \
+      case 2: launch<HH, 2, true>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, st); break;   \
+      case 4: launch<HH, 4, true>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, st); break;   \
+      case 8: launch<HH, 8, true>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, st); break;   \
+      case 16: launch<HH, 16, true>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, st); break; \
       default:                                                                        \
         if (M < 8)                                                                    \
-          launch<HH, 8, false>(V, deltas, P, M, wq, wo, gain, zero_scores, st);       \
+          launch<HH, 8, false>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, st);       \
         else if (M < 16)                                                              \
-          launch<HH, 16, false>(V, deltas, P, M, wq, wo, gain, zero_scores, st);      \
+          launch<HH, 16, false>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, st);      \
         else                                                                          \
-          launch<HH, 32, false>(V, deltas, P, M, wq, wo, gain, zero_scores, st);      \
+          launch<HH, 32, false>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, st);      \
     }                                                                                 \
     return true;                                                                      \
   }

@@ -265,9 +265,9 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
           for (int k = 0; k < 8; ++k) v[k] = fm(fm(v[k], rr), g8[k]);
         }
-        __align__(16) __half h[8], l[8];
+        __align__(16) __half2 h[4], l[4];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) tc::split_f16(v[k], h[k], l[k]);
+        for (int k = 0; k < 4; ++k) tc::split_f16x2(v[2 * k], v[2 * k + 1], h[k], l[k]);
         const int off = j * LBO_A + px * 16;  // bytes
         *reinterpret_cast<uint4*>(hi + off) = *reinterpret_cast<uint4*>(h);
         *reinterpret_cast<uint4*>(lo + off) = *reinterpret_cast<uint4*>(l);

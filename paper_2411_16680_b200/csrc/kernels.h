@@ -208,15 +208,21 @@ void deltas_to_view_major(const float* src, float* dst, int64_t P, int M, int C,
 // attend_scratch_floats(P, C, M, heads) floats of device memory from the
 // caller's arena (the generic fallback's per-texel rows; none for the
 // tensor-core kernel).
+// wimg (optional): attend_tc_prepare's image of (wq, wo), 16-byte aligned.
 void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
             const float* const* wq_heads, const float* wo, const float* gain, int zero_scores,
-            float* scratch, cudaStream_t st);
+            float* scratch, const void* wimg, cudaStream_t st);
 size_t attend_scratch_floats(int64_t P, int C, int M, int heads);
 // tcgen05 fused attention (attn_tc.cu): C = 32, h in {1,2,4},
 // M in {2,4,8,16}; returns false otherwise.
 bool attend_tc_supported(int C, int M, int heads);
 bool attend_tc(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
-               const float* wo, const float* gain, int zero_scores, cudaStream_t st);
+               const float* wo, const float* gain, int zero_scores, const void* wimg,
+               cudaStream_t st);
+// The tensor-core attention's pre-split weight image (bytes; 0: no kernel
+// for this head count) and the kernel that makes it.
+size_t attend_tc_weight_bytes(int heads);
+void attend_tc_prepare(const float* wq, const float* wo, int heads, void* dst, cudaStream_t st);
 // logits [P, M] = <rms_norm(V,g) W_blend, Δ_m> / sqrt(C) (network.hpp:539-549).
 void blend_logits(const float* V, const float* deltas, int64_t P, int C, int M,
                   const float* blend_w, const float* gain, float* logits, cudaStream_t st,

@@ -592,8 +592,21 @@ void fusion(lvsg_ctx* c, float* V, int64_t L, int64_t H, int64_t W, const Fusion
   // the generic kernel's scratch (none for the tensor-core shapes) grows
   // the arena once, on the first frame of a plan
   c->attn_scratch.ensure(attend_scratch_floats(P, C, M, f.heads));
+  // the tensor-core kernel's pre-split weight image, made once per binding
+  const void* wimg = nullptr;
+  if (const size_t nb = C == 32 ? attend_tc_weight_bytes(f.heads) : 0) {
+    auto key = std::make_tuple(f.wq, -f.heads, 0);
+    auto it = c->wimg.find(key);
+    if (it == c->wimg.end()) {
+      auto buf = std::make_unique<Buf>();
+      buf->ensure((nb + 3) / 4);
+      attend_tc_prepare(f.wq, f.wo, f.heads, buf->p, c->stream);
+      it = c->wimg.emplace(key, std::move(buf)).first;
+    }
+    wimg = it->second->p;
+  }
   attend(V, c->deltas.p, P, C, M, f.heads, f.wq, nullptr, f.wo, f.gain, c->cfg.ablate_attention,
-         c->attn_scratch.p, c->stream);
+         c->attn_scratch.p, wimg, c->stream);
   mark(c, "attention", 1);
   for (const MlpW& m : f.mlps) {
     // conv_mlp_residual (attention.hpp:262-267), batched over layers
@@ -1842,7 +1855,7 @@ lvsg_status lvsg_stage_attend(lvsg_ctx* c, float* V, const float* deltas, int64_
     deltas_to_view_major(deltas, c->stage_a.p, P, int(M), C, c->stream);
     c->attn_scratch.ensure(attend_scratch_floats(P, C, int(M), int(heads)));
     attend(V, c->stage_a.p, P, C, int(M), int(heads), wq, nullptr, wo, gain, zero_scores,
-           c->attn_scratch.p, c->stream);
+           c->attn_scratch.p, nullptr, c->stream);
     sync_and_check(c);
   });
 }
