@@ -35,6 +35,10 @@
 #include "kernels.h"
 #include "tc.cuh"
 
+#ifndef LVSG_ATT_DEBUG
+#define LVSG_ATT_DEBUG 0
+#endif
+
 namespace lvsg {
 namespace {
 
@@ -254,21 +258,32 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
     }
   } else if (warp == 1) {
     // ---- MMA issuer: S(first); per tile i: S(i+1), then O over the heads ----
-    int u = 0, ns = 0;
+    // A operand stagings in issue order: n(0); per tile i: n(i+1) (group 0),
+    // then heads 0 .. H-1 (head h by group h / HG). One consumer group: two
+    // buffers used alternately; two groups: buffer g belongs to group g, so
+    // every a_free phase a group waits on follows one it waited on itself
+    // (a parity wait is exact only when the waiter is at most one phase
+    // behind -- with shared buffers one group could pass a stale parity of a
+    // buffer whose previous use belonged to the other group)
+    int ca[2] = {0, 0}, ns = 0;
     if (wimg) tc::mbar_wait(w_full, 0);
-    auto next_a = [&]() {
-      const int b = u & 1;
-      tc::mbar_wait(&a_full[b], uint32_t((u >> 1) & 1));
+    auto next_a = [&](int owner) {
+      const int b = NGRP == 1 ? (ca[0] & 1) : owner;
+      const uint32_t ph = NGRP == 1 ? uint32_t((ca[0] >> 1) & 1) : uint32_t(ca[owner] & 1);
+      tc::mbar_wait(&a_full[b], ph);
+      ++ca[NGRP == 1 ? 0 : owner];
+      __syncwarp();
       tc::fence_after();
       return b;
     };
     auto issue_s = [&]() {
-      const int b = next_a();
+      const int b = next_a(0);
       // S lives in one TMEM accumulator: S(j) is written only once every
       // consumer of both groups has read S(j-1) (with two groups the ring lets
       // one group run up to NS slices ahead of the other)
       if (ns > 0) tc::mbar_wait(s_free, uint32_t((ns - 1) & 1));
       ++ns;
+      __syncwarp();
       tc::fence_after();
       if (tc::elect_one()) {
         mma_split(tmem_s, sb + S::OFF_A + b * A_BYTES, sb + S::OFF_BQ, 32 * H, false);
@@ -276,13 +291,12 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
         tc::commit(&a_free[b]);
       }
       __syncwarp();
-      ++u;
     };
     issue_s();
     for (int i = 0; i < ntl; ++i) {
       if (i + 1 < ntl) issue_s();
       for (int h = 0; h < H; ++h) {
-        const int b = next_a();
+        const int b = next_a(h / HG);
         if (tc::elect_one()) {
           mma_split(tmem_o, sb + S::OFF_A + b * A_BYTES, sb + S::OFF_BO + h * S::BO_BYTES, 32,
                     h > 0);
@@ -290,7 +304,6 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
           tc::commit(&a_free[b]);
         }
         __syncwarp();
-        ++u;
       }
     }
   } else {
@@ -303,16 +316,18 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
     const float inv_temp = __double2float_rn(1.0 / sqrt(double(C)));
     const bool storer = warp == 2 && lane == 0;
     int k = 0;
-    // A staging sequence (shared with the MMA issuer): n(0) at 0; in iteration
-    // i, n(i+1) then the H heads of tile i
-    auto u_n = [&](int j) { return j == 0 ? 0 : 1 + (j - 1) * (H + 1); };
-    auto u_h = [&](int i, int h) { return 1 + i * (H + 1) + (i + 1 < ntl ? 1 : 0) + h; };
-    auto stage = [&](int u, const float* x) {  // staging u into buffer u & 1
-      const int b = u & 1;
-      if (u >= 2) tc::mbar_wait(&a_free[b], uint32_t(((u >> 1) - 1) & 1));
+    // A stagings (the MMA issuer consumes them in the same order): group 0
+    // stages n(0), then per tile n(i+1) and its heads; group 1 its heads.
+    // cs counts this group's stagings (see next_a for the buffers).
+    int cs = 0;
+    auto stage = [&](const float* x) {
+      const int b = NGRP == 1 ? (cs & 1) : grp;
+      if (NGRP == 1 ? cs >= 2 : cs >= 1)
+        tc::mbar_wait(&a_free[b], NGRP == 1 ? uint32_t(((cs >> 1) - 1) & 1) : uint32_t((cs - 1) & 1));
       stage_row(smem + S::OFF_A + b * A_BYTES, row, x);
       tc::fence_proxy_async();
       tc::mbar_arrive(&a_full[b]);
+      ++cs;
     };
     auto slice_row = [&](float* dm) {  // this texel's row of the next Δ slice
       const int sl = k % NS;
@@ -323,6 +338,10 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
         const float4 t = *reinterpret_cast<const float4*>(d + swz(row, g));
         dm[4 * g] = t.x, dm[4 * g + 1] = t.y, dm[4 * g + 2] = t.z, dm[4 * g + 3] = t.w;
       }
+      // these generic-proxy reads must be ordered before the TMA (async
+      // proxy) that refills the slot once the last consumer arrives: without
+      // the proxy fence the last arriver's loads can return the next slice
+      tc::fence_proxy_async();
       tc::mbar_arrive(&d_empty[sl]);
       ++k;
     };
@@ -349,7 +368,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
       const float r = __fdiv_rn(1.0f, __fsqrt_rn(fa(__fdiv_rn(ms, float(C)), 1e-6f)));
 #pragma unroll
       for (int c = 0; c < C; ++c) x[c] = fm(fm(x[c], r), __ldg(gain + c));
-      stage(u_n(j), x);
+      stage(x);
     };
     auto finish_tile = [&](int j) {  // V(j) += O(j), TMA store; group 0
       const int vb = j % NV;
@@ -383,6 +402,9 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
 
     if (grp == 0) start_tile(0);
     for (int i = 0; i < ntl; ++i) {
+#if LVSG_ATT_DEBUG & 1
+      if (NGRP > 1) named_sync(2, NCONS * NGRP);  // debug: both groups in lockstep per tile
+#endif
       // ---- scores(i) for this group's heads: S in registers, one pass over Δ ----
       float w[HG][MM];
       if (zero_scores) {
@@ -472,7 +494,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
             hd[h][c] = fmaf(w[h][m + 1], d1[c], fmaf(w[h][m], d0[c], hd[h][c]));
       }
 #pragma unroll
-      for (int h = 0; h < HG; ++h) stage(u_h(i, grp * HG + h), hd[h]);
+      for (int h = 0; h < HG; ++h) stage(hd[h]);
     }
     if (grp == 0) {
       finish_tile(ntl - 1);

@@ -272,8 +272,11 @@ __global__ void __launch_bounds__(NT, 1)
         *reinterpret_cast<uint4*>(hi + off) = *reinterpret_cast<uint4*>(h);
         *reinterpret_cast<uint4*>(lo + off) = *reinterpret_cast<uint4*>(l);
       }
-      tc::mbar_arrive(&raw_empty[r]);
+      // one proxy fence orders this thread's generic reads of the raw box
+      // before the TMA that refills it (WAR across proxies) and its plane
+      // writes before the MMAs that read them
       tc::fence_proxy_async();
+      tc::mbar_arrive(&raw_empty[r]);
       tc::mbar_arrive(&conv_full[b]);
     }
   } else {
@@ -352,6 +355,7 @@ __global__ void __launch_bounds__(NT, 1)
           d0[4 * c4 + 2] = fa(r.z, d0[4 * c4 + 2]);
           d0[4 * c4 + 3] = fa(r.w, d0[4 * c4 + 3]);
         }
+        tc::fence_proxy_async();  // the reads above before the TMA refilling the sub-box
         __syncwarp();
       }
       if (has_res && t + step < num_tiles) res_issue(t + step);
