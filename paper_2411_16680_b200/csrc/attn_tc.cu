@@ -93,8 +93,12 @@ struct Smem {
   static_assert(OFF_D % 1024 == 0 && OFF_V % 1024 == 0, "128B-swizzled TMA destinations");
 };
 
-// A[j][row][8 halves] (hi) and A[4 + j][row] (lo') <- x[32] of this row.
-__device__ __forceinline__ void stage_row(uint8_t* a, int row, const float* x) {
+// A[j][row][8 halves] (hi) and A[4 + j][row] (lo') <- x[32] of this row;
+// returns whether a value overflows the split (tc::split_overflows).
+__device__ __forceinline__ bool stage_row(uint8_t* a, int row, const float* x) {
+  bool ovf = false;
+#pragma unroll
+  for (int c = 0; c < C; ++c) ovf |= tc::split_overflows(x[c]);
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     __align__(16) __half2 h[4], l[4];
@@ -103,19 +107,24 @@ __device__ __forceinline__ void stage_row(uint8_t* a, int row, const float* x) {
     *reinterpret_cast<uint4*>(a + j * A_LBO + row * 16) = *reinterpret_cast<uint4*>(h);
     *reinterpret_cast<uint4*>(a + A_HALF + j * A_LBO + row * 16) = *reinterpret_cast<uint4*>(l);
   }
+  return ovf;
 }
 
 // B rows (K-major interleave): w(n, k) for n < N, hi in rows [0, N), lo' in [N, 2N).
 template <typename F>
-__device__ __forceinline__ void stage_weights(uint8_t* b, int N, int tid, int nt, F w) {
+__device__ __forceinline__ bool stage_weights(uint8_t* b, int N, int tid, int nt, F w) {
   __half* bh = reinterpret_cast<__half*>(b);
+  bool ovf = false;
   for (int e = tid; e < NJ * N * 8; e += nt) {
     const int k8 = e & 7, n = (e >> 3) % N, j = (e >> 3) / N;
     __half hi, lo;
-    tc::split_f16(w(n, 8 * j + k8), hi, lo);
+    const float x = w(n, 8 * j + k8);
+    tc::split_f16(x, hi, lo);
+    ovf |= tc::split_overflows(x);
     bh[(j * 2 * N + n) * 8 + k8] = hi;
     bh[(j * 2 * N + N + n) * 8 + k8] = lo;
   }
+  return ovf;
 }
 
 // D (+)= A * B over K = 32: MMA1 N = 2n into d, MMA2 N = n (lo' x hi) into d + n.
@@ -162,7 +171,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
                      const __grid_constant__ CUtensorMap dmap, int64_t P,
                      const float* __restrict__ wq, const float* __restrict__ wo,
                      const float* __restrict__ gain, int zero_scores, int num_tiles, int Mr,
-                     const uint8_t* __restrict__ wimg) {
+                     const uint8_t* __restrict__ wimg, int* ovf_flag) {
   const int M = EXACT ? MM : Mr;
   auto has = [&](int m) { return EXACT || m < Mr; };
   using S = Smem<H>;
@@ -192,12 +201,13 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
 
   // resident weights: Bq rows n = 32*i + c -> Wq_i[k][c]; Bo_i rows n -> Wo[32i + k][n]
   // (split here unless the context's pre-split image is given: one bulk copy)
+  bool ovf = false;  // an fp16-split operand overflowed (reported once per thread)
   if (!wimg) {
-    stage_weights(smem + S::OFF_BQ, 32 * H, tid, NTH,
-                  [&](int n, int k) { return __ldg(wq + ((n >> 5) * C + k) * C + (n & 31)); });
+    ovf |= stage_weights(smem + S::OFF_BQ, 32 * H, tid, NTH,
+                         [&](int n, int k) { return __ldg(wq + ((n >> 5) * C + k) * C + (n & 31)); });
     for (int h = 0; h < H; ++h)
-      stage_weights(smem + S::OFF_BO + h * S::BO_BYTES, 32, tid, NTH,
-                    [&](int n, int k) { return __ldg(wo + (h * C + k) * C + n); });
+      ovf |= stage_weights(smem + S::OFF_BO + h * S::BO_BYTES, 32, tid, NTH,
+                           [&](int n, int k) { return __ldg(wo + (h * C + k) * C + n); });
   }
   if (tid == 0) {
     for (int k = 0; k < NV; ++k) {
@@ -324,7 +334,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
       const int b = NGRP == 1 ? (cs & 1) : grp;
       if (NGRP == 1 ? cs >= 2 : cs >= 1)
         tc::mbar_wait(&a_free[b], NGRP == 1 ? uint32_t(((cs >> 1) - 1) & 1) : uint32_t((cs - 1) & 1));
-      stage_row(smem + S::OFF_A + b * A_BYTES, row, x);
+      ovf |= stage_row(smem + S::OFF_A + b * A_BYTES, row, x);
       tc::fence_proxy_async();
       tc::mbar_arrive(&a_full[b]);
       ++cs;
@@ -501,6 +511,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
       if (storer) tc::bulk_wait<0>();
     }
   }
+  if (ovf && ovf_flag) atomicOr(ovf_flag, 2);
   tc::fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc(tmem, tmem_cols<H>());
@@ -520,7 +531,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 template <int H, int MM, bool EXACT>
 void launch(float* V, const float* D, int64_t P, int M, const float* wq, const float* wo,
-            const float* gain, int zero, const void* wimg, cudaStream_t st) {
+            const float* gain, int zero, const void* wimg, int* ovf, cudaStream_t st) {
   smem_optin(reinterpret_cast<const void*>(attend_tc_kernel<H, MM, EXACT>), Smem<H>::BYTES);
   const int sms = sm_count();
   // V [P][32] fp32 as a 2-D map, 128-texel boxes (128B swizzle)
@@ -551,7 +562,7 @@ void launch(float* V, const float* D, int64_t P, int M, const float* wq, const f
   const int tiles = int((P + TILE - 1) / TILE);
   const int grid = tiles < sms ? tiles : sms;
   launch_pdl(true, attend_tc_kernel<H, MM, EXACT>, grid, nthreads<H>(), Smem<H>::BYTES, st, vmap,
-             dmap, P, wq, wo, gain, zero, tiles, M, static_cast<const uint8_t*>(wimg));
+             dmap, P, wq, wo, gain, zero, tiles, M, static_cast<const uint8_t*>(wimg), ovf);
 }
 
 // The weight image of attend_tc_kernel<H>'s resident B operands, in its
@@ -559,14 +570,16 @@ void launch(float* V, const float* D, int64_t P, int M, const float* wq, const f
 // [Wo hi ; Wo lo'] (stage_weights), made once per weight binding.
 template <int H>
 __global__ void attend_tc_weights_kernel(const float* __restrict__ wq, const float* __restrict__ wo,
-                                         uint8_t* out) {
+                                         uint8_t* out, int* ovf_flag) {
   pdl_grid_sync();
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
-  stage_weights(out, 32 * H, tid, nt,
-                [&](int n, int k) { return __ldg(wq + ((n >> 5) * C + k) * C + (n & 31)); });
+  bool ovf = stage_weights(out, 32 * H, tid, nt, [&](int n, int k) {
+    return __ldg(wq + ((n >> 5) * C + k) * C + (n & 31));
+  });
   for (int h = 0; h < H; ++h)
-    stage_weights(out + Smem<H>::BQ_BYTES + h * Smem<H>::BO_BYTES, 32, tid, nt,
-                  [&](int n, int k) { return __ldg(wo + (h * C + k) * C + n); });
+    ovf |= stage_weights(out + Smem<H>::BQ_BYTES + h * Smem<H>::BO_BYTES, 32, tid, nt,
+                         [&](int n, int k) { return __ldg(wo + (h * C + k) * C + n); });
+  if (ovf && ovf_flag) atomicOr(ovf_flag, 2);
 }
 
 }  // namespace
@@ -580,12 +593,13 @@ size_t attend_tc_weight_bytes(int heads) {
   }
 }
 
-void attend_tc_prepare(const float* wq, const float* wo, int heads, void* dst, cudaStream_t st) {
+void attend_tc_prepare(const float* wq, const float* wo, int heads, void* dst, int* ovf,
+                       cudaStream_t st) {
   uint8_t* o = static_cast<uint8_t*>(dst);
   switch (heads) {
-    case 1: launch_k(attend_tc_weights_kernel<1>, 8, 256, 0, st, wq, wo, o); break;
-    case 2: launch_k(attend_tc_weights_kernel<2>, 8, 256, 0, st, wq, wo, o); break;
-    case 4: launch_k(attend_tc_weights_kernel<4>, 8, 256, 0, st, wq, wo, o); break;
+    case 1: launch_k(attend_tc_weights_kernel<1>, 8, 256, 0, st, wq, wo, o, ovf); break;
+    case 2: launch_k(attend_tc_weights_kernel<2>, 8, 256, 0, st, wq, wo, o, ovf); break;
+    case 4: launch_k(attend_tc_weights_kernel<4>, 8, 256, 0, st, wq, wo, o, ovf); break;
     default: break;
   }
 }
@@ -595,7 +609,7 @@ bool attend_tc_supported(int C_, int M, int heads) {
 }
 
 bool attend_tc(float* V, const float* deltas, int64_t P, int C_, int M, int heads, const float* wq,
-               const float* wo, const float* gain, int zero_scores, const void* wimg,
+               const float* wo, const float* gain, int zero_scores, const void* wimg, int* ovf,
                cudaStream_t st) {
   if (wimg && (reinterpret_cast<uintptr_t>(wimg) & 15)) return false;
   if (C_ != C || !encode_fn() || (reinterpret_cast<uintptr_t>(V) & 15) ||
@@ -604,17 +618,17 @@ bool attend_tc(float* V, const float* deltas, int64_t P, int C_, int M, int head
 #define LVSG_ATT(HH)                                                                  \
   if (heads == HH) {                                                                  \
     switch (M) {                                                                      \
-      case 2: launch<HH, 2, true>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, st); break;   \
-      case 4: launch<HH, 4, true>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, st); break;   \
-      case 8: launch<HH, 8, true>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, st); break;   \
-      case 16: launch<HH, 16, true>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, st); break; \
+      case 2: launch<HH, 2, true>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, ovf, st); break;   \
+      case 4: launch<HH, 4, true>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, ovf, st); break;   \
+      case 8: launch<HH, 8, true>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, ovf, st); break;   \
+      case 16: launch<HH, 16, true>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, ovf, st); break; \
       default:                                                                        \
         if (M < 8)                                                                    \
-          launch<HH, 8, false>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, st);       \
+          launch<HH, 8, false>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, ovf, st);       \
         else if (M < 16)                                                              \
-          launch<HH, 16, false>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, st);      \
+          launch<HH, 16, false>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, ovf, st);      \
         else                                                                          \
-          launch<HH, 32, false>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, st);      \
+          launch<HH, 32, false>(V, deltas, P, M, wq, wo, gain, zero_scores, wimg, ovf, st);      \
     }                                                                                 \
     return true;                                                                      \
   }

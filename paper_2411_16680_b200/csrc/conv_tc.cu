@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
     for (int k = 0; k < 8; ++k) g8[k] = gain_s[8 * j + k];
     int i = 0;
+    bool ovf = false;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++i) {
       const int r = i % NR, b = i % NP;
       const float* raw = reinterpret_cast<const float*>(smem + OFF_RAW + r * RAW_BYTES);
@@ -268,6 +269,8 @@ __global__ void __launch_bounds__(NT, 1)
         __align__(16) __half2 h[4], l[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) tc::split_f16x2(v[2 * k], v[2 * k + 1], h[k], l[k]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ovf |= tc::split_overflows(v[k]);
         const int off = j * LBO_A + px * 16;  // bytes
         *reinterpret_cast<uint4*>(hi + off) = *reinterpret_cast<uint4*>(h);
         *reinterpret_cast<uint4*>(lo + off) = *reinterpret_cast<uint4*>(l);
@@ -279,6 +282,7 @@ __global__ void __launch_bounds__(NT, 1)
       tc::mbar_arrive(&raw_empty[r]);
       tc::mbar_arrive(&conv_full[b]);
     }
+    if (ovf && a.ovf) atomicOr(a.ovf, 2);
   } else {
     // ---- epilogue: TMEM -> bias / GELU / residual -> swizzled smem -> TMA store ----
     const int ew = warp - 6;   // 0..NEW-1
@@ -422,8 +426,10 @@ __global__ void conv3x3_tc_weights_kernel(const ConvArgs a, __half* out) {
   const int j = rest % NCH, tap = rest / NCH;
   const int co = n & 31, ci = 8 * j + k8;
   __half h, l;
-  tc::split_f16(__ldg(a.w + (co * w_cin_of(a) + a.w_ci0 + ci) * 9 + tap), h, l);
+  const float wv = __ldg(a.w + (co * w_cin_of(a) + a.w_ci0 + ci) * 9 + tap);
+  tc::split_f16(wv, h, l);
   out[e] = n < 32 ? h : l;
+  if (tc::split_overflows(wv) && a.ovf) atomicOr(a.ovf, 2);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {

@@ -494,19 +494,20 @@ __global__ void __launch_bounds__(256) gather_stack32_kernel(
     DevRayCam rc, const float* __restrict__ depth, int L, int H, int W, float* __restrict__ deltas) {
   pdl_grid_sync();
   constexpr int G = 8;
-  const int64_t P = (int64_t)L * H * W;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // grid (texel blocks, views): 32-bit texel indexing (P M < 2^31, checked
+  // by the launcher); a warp = 32 consecutive texels of one view
+  const int P = L * H * W;
+  const int m = blockIdx.y;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  // record: m, p, flags (1 valid | 2 x1>x0 | 4 y1>y0 | 8 past the end), tap 00, weights
-  int m = 0, pl = 0, flags = 8, off = 0;
+  // record: p, flags (1 valid | 2 x1>x0 | 4 y1>y0 | 8 past the end), tap 00, weights
+  int pl = p, flags = 8, off = 0;
   float w[4] = {0.f, 0.f, 0.f, 0.f};
-  if (i < P * M) {
-    m = int(i / P);
-    const int64_t p = i - m * P;
-    pl = int(p);
+  if (p < P) {
     flags = 0;
-    const int j = int(p % W);
-    const int ii = int((p / W) % H);
+    const unsigned pu = unsigned(p);
+    const int j = int(pu % unsigned(W));
+    const int ii = int((pu / unsigned(W)) % unsigned(H));
     float pt[3];
     world_point(rc, ii, j, __ldg(depth + p), pt);
     const Footprint f = project_footprint(cams[m], pt);
@@ -530,7 +531,6 @@ __global__ void __launch_bounds__(256) gather_stack32_kernel(
   for (int it = 0; it < 8; ++it) {
     const int r = 8 * q + it;
     const int rf = __shfl_sync(0xffffffffu, flags, r);
-    const int rm = __shfl_sync(0xffffffffu, m, r);
     const int rp = __shfl_sync(0xffffffffu, pl, r);
     const int ro = __shfl_sync(0xffffffffu, off, r) + g;
     float rw[4];
@@ -541,17 +541,14 @@ __global__ void __launch_bounds__(256) gather_stack32_kernel(
     if (rf & 1) {
       const int dx = (rf & 2) ? G : 0, dy = (rf & 4) ? Wf * G : 0;
       const bool same_rows = poff >= 0 && ((rf ^ pfl) & 4) == 0;
-      if (same_rows && ro == poff) {
-        // the same cell: both columns already in registers
-      } else if (same_rows && ro == poff + G && (pfl & 2) && dx) {
-        // the next cell to the right: the old right column becomes the left
-        l0 = r0;
-        l1 = r1;
-        r0 = __ldg(f4 + ro + dx);
-        r1 = dy ? __ldg(f4 + ro + dy + dx) : r0;
-      } else {
-        l0 = __ldg(f4 + ro);
-        l1 = dy ? __ldg(f4 + ro + dy) : l0;
+      if (!(same_rows && ro == poff)) {  // not the previous cell: new right column
+        if (same_rows && ro == poff + G && (pfl & 2) && dx) {
+          l0 = r0;  // the next cell to the right: the old right column is the left
+          l1 = r1;
+        } else {
+          l0 = __ldg(f4 + ro);
+          l1 = dy ? __ldg(f4 + ro + dy) : l0;
+        }
         r0 = dx ? __ldg(f4 + ro + dx) : l0;
         r1 = dx ? (dy ? __ldg(f4 + ro + dy + dx) : r0) : l1;
       }
@@ -565,7 +562,7 @@ __global__ void __launch_bounds__(256) gather_stack32_kernel(
     } else {
       poff = -1;
     }
-    o4[((int64_t)rm * P + rp) * G + g] = v;
+    o4[((int64_t)m * P + rp) * G + g] = v;
   }
 }
 
@@ -969,8 +966,9 @@ void gather_stack(const float* feats, int M, int Hf, int Wf, int C, const DevCam
   const bool v4 = C % 4 == 0;
   const int64_t n = (int64_t)L * H * W * M;
   if (C == 32 && (int64_t)M * Hf * Wf * 8 < (int64_t(1) << 31) && n < (int64_t(1) << 31)) {
-    launch_k(gather_stack32_kernel, blocks_for(n, 256), 256, 0, st, feats, M, Hf, Wf, cams_dev, rc,
-                                                              depth, L, H, W, deltas);
+    const int64_t P = (int64_t)L * H * W;
+    launch_k(gather_stack32_kernel, dim3(blocks_for(P, 256), M), 256, 0, st, feats, M, Hf, Wf,
+             cams_dev, rc, depth, L, H, W, deltas);
   } else if (v4)
     launch_k(gather_stack_kernel<true>, blocks_for(n, 256), 256, 0, st, feats, M, Hf, Wf, C, cams_dev, rc,
                                                                   depth, L, H, W, deltas);
@@ -1011,9 +1009,9 @@ void deltas_to_view_major(const float* src, float* dst, int64_t P, int M, int C,
 }
 void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
             const float* const* wq_heads, const float* wo, const float* gain, int zero_scores,
-            float* scratch, const void* wimg, cudaStream_t st) {
+            float* scratch, const void* wimg, int* ovf, cudaStream_t st) {
   (void)wq_heads;
-  if (attend_tc(V, deltas, P, C, M, heads, wq, wo, gain, zero_scores, wimg, st)) return;
+  if (attend_tc(V, deltas, P, C, M, heads, wq, wo, gain, zero_scores, wimg, ovf, st)) return;
   // generic fallback: 4C floats of scratch per texel (attend_scratch_floats)
   if (!scratch) throw CudaError("attend: no arena scratch for the generic kernel");
   launch_k(attend_generic_kernel, blocks_for(P, 128), 128, 0, st, V, deltas, P, C, M, heads, wq, wo,

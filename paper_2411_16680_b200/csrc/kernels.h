@@ -113,6 +113,10 @@ struct ConvArgs {
   // them by value in its parameter space, so every FMA reads its weight as
   // a constant-bank operand (no shared-memory weight loads).
   const float* stem_host;
+  // tcgen05 conv only: set bit 2 (atomicOr) when an operand of the fp16
+  // split overflows (|x| >= 65520 rounds to inf in the hi term): the split
+  // would be silently wrong, so the call reports LVSG_ERR_NUMERIC instead
+  int* ovf;
 };
 __host__ __device__ inline int w_cin_of(const ConvArgs& a) { return a.w_cin ? a.w_cin : a.Cin; }
 // Dispatches to the tcgen05 3xTF32 kernel when it applies (Cin = Cout = 32,
@@ -209,20 +213,22 @@ void deltas_to_view_major(const float* src, float* dst, int64_t P, int M, int C,
 // caller's arena (the generic fallback's per-texel rows; none for the
 // tensor-core kernel).
 // wimg (optional): attend_tc_prepare's image of (wq, wo), 16-byte aligned.
+// ovf (optional): bit 2 set when an fp16-split operand overflows (ConvArgs.ovf).
 void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
             const float* const* wq_heads, const float* wo, const float* gain, int zero_scores,
-            float* scratch, const void* wimg, cudaStream_t st);
+            float* scratch, const void* wimg, int* ovf, cudaStream_t st);
 size_t attend_scratch_floats(int64_t P, int C, int M, int heads);
 // tcgen05 fused attention (attn_tc.cu): C = 32, h in {1,2,4},
 // M in {2,4,8,16}; returns false otherwise.
 bool attend_tc_supported(int C, int M, int heads);
 bool attend_tc(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
-               const float* wo, const float* gain, int zero_scores, const void* wimg,
+               const float* wo, const float* gain, int zero_scores, const void* wimg, int* ovf,
                cudaStream_t st);
 // The tensor-core attention's pre-split weight image (bytes; 0: no kernel
 // for this head count) and the kernel that makes it.
 size_t attend_tc_weight_bytes(int heads);
-void attend_tc_prepare(const float* wq, const float* wo, int heads, void* dst, cudaStream_t st);
+void attend_tc_prepare(const float* wq, const float* wo, int heads, void* dst, int* ovf,
+                       cudaStream_t st);
 // logits [P, M] = <rms_norm(V,g) W_blend, Δ_m> / sqrt(C) (network.hpp:539-549).
 void blend_logits(const float* V, const float* deltas, int64_t P, int C, int M,
                   const float* blend_w, const float* gain, float* logits, cudaStream_t st,

@@ -174,6 +174,10 @@ struct lvsg_ctx {
       fbr, pre_d, pre_s, logits, anchors, ldm_d, ldm_s, ldm_b;
   lvsg::Buf cams_dev;  // DevCam / RayBaseCam tables
   int* bad_flag = nullptr;
+  // where the forward's kernels report (atomicOr): bit 1 a depth outside the
+  // frustum (render), bit 2 an fp16-split overflow (tensor-core operands) --
+  // bad_flag, or the pipelined frame slot's flag while its frame is enqueued
+  int* flag = nullptr;
   void* pinned = nullptr;  // camera staging
   size_t pinned_bytes = 0;
   cudaEvent_t staging_done = nullptr;
@@ -454,6 +458,7 @@ ConvArgs conv_args(int B, int H, int W, int Cin, int Cout, const float* w, const
 // from the context cache (cached = true: weights bound to the context) or a
 // fresh one in scratch (stage entry points: arbitrary caller weights).
 void run_conv(lvsg_ctx* c, ConvArgs a, cudaStream_t st, int impl = 0, bool cached = true) {
+  a.ovf = c->flag;
   const int path = conv3x3_path(a, impl);
   if (path >= 2) {
     const size_t nf = kConvTcWeightBytes / sizeof(float);
@@ -600,13 +605,13 @@ void fusion(lvsg_ctx* c, float* V, int64_t L, int64_t H, int64_t W, const Fusion
     if (it == c->wimg.end()) {
       auto buf = std::make_unique<Buf>();
       buf->ensure((nb + 3) / 4);
-      attend_tc_prepare(f.wq, f.wo, f.heads, buf->p, c->stream);
+      attend_tc_prepare(f.wq, f.wo, f.heads, buf->p, c->flag, c->stream);
       it = c->wimg.emplace(key, std::move(buf)).first;
     }
     wimg = it->second->p;
   }
   attend(V, c->deltas.p, P, C, M, f.heads, f.wq, nullptr, f.wo, f.gain, c->cfg.ablate_attention,
-         c->attn_scratch.p, wimg, c->stream);
+         c->attn_scratch.p, wimg, c->flag, c->stream);
   mark(c, "attention", 1);
   for (const MlpW& m : f.mlps) {
     // conv_mlp_residual (attention.hpp:262-267), batched over layers
@@ -1021,6 +1026,17 @@ lvsg_status guard(lvsg_ctx* c, const auto& fn) {
   }
 }
 
+// The device flag's meaning: bit 2 an fp16-split overflow in a tensor-core
+// operand (the result would be silently wrong: NumericError), bit 1 a depth
+// outside the frustum (world_points, geometry.hpp:112-115: DimError).
+[[noreturn]] void throw_flag(int bad) {
+  if (bad & 2)
+    throw NumericError(
+        "fp16 split: a tensor-core operand (conv / attention activation or weight) has |x| >= "
+        "65520, beyond the split's range");
+  throw DimError("world_points: depth outside [near, far]");
+}
+
 void sync_and_check(lvsg_ctx* c) {
   CUDA_OK(cudaGetLastError());
   CUDA_OK(cudaStreamSynchronize(c->stream));
@@ -1029,7 +1045,7 @@ void sync_and_check(lvsg_ctx* c) {
   CUDA_OK(cudaMemcpy(&bad, c->bad_flag, sizeof(int), cudaMemcpyDeviceToHost));
   if (bad) {
     CUDA_OK(cudaMemset(c->bad_flag, 0, sizeof(int)));
-    throw DimError("world_points: depth outside [near, far]");
+    throw_flag(bad);
   }
 }
 
@@ -1042,7 +1058,7 @@ void wait_slot(lvsg_ctx* c, FrameSlot& S) {
   CUDA_OK(cudaMemcpy(&bad, S.bad, sizeof(int), cudaMemcpyDeviceToHost));
   if (bad) {
     CUDA_OK(cudaMemset(S.bad, 0, sizeof(int)));
-    throw DimError("world_points: depth outside [near, far]");
+    throw_flag(bad);
   }
   (void)c;
 }
@@ -1202,6 +1218,7 @@ lvsg_status lvsg_create(const lvsg_model_config* cfg, int32_t device, lvsg_ctx**
     for (cudaEvent_t& e : c->ev_band) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_OK(cudaMalloc(&c->bad_flag, sizeof(int)));
     CUDA_OK(cudaMemset(c->bad_flag, 0, sizeof(int)));
+    c->flag = c->bad_flag;
     c->layout = param_layout(c->cfg);
     c->total_params = 0;
     for (auto& p : c->layout) c->total_params += p.numel();
@@ -1464,8 +1481,16 @@ lvsg_status submit_impl(lvsg_ctx* c, int64_t views, const float* const* enc_imag
     if (enc_images && behind)
       CUDA_OK(cudaStreamWaitEvent(c->stream, S.ev_enc[size_t(views - 1)], 0));
     CamTables t;
-    forward_device(c, enc_images || decimate ? S.enc_in.p : nullptr, enc_h, enc_w, enc_cams_used,
-                   *target, render_cams, &t, enc_images && !behind ? S.ev_enc.data() : nullptr);
+    c->flag = S.bad;  // this frame's kernels report into its slot (read by wait_slot)
+    try {
+      forward_device(c, enc_images || decimate ? S.enc_in.p : nullptr, enc_h, enc_w,
+                     enc_cams_used, *target, render_cams, &t,
+                     enc_images && !behind ? S.ev_enc.data() : nullptr);
+    } catch (...) {
+      c->flag = c->bad_flag;
+      throw;
+    }
+    c->flag = c->bad_flag;
     const int64_t Ho = c->plan.out_height, Wo = c->plan.out_width;
     S.rgb.ensure(size_t(Ho * Wo * 3));
     CUDA_OK(cudaStreamWaitEvent(c->stream, S.ev_ren, 0));
@@ -1855,7 +1880,7 @@ lvsg_status lvsg_stage_attend(lvsg_ctx* c, float* V, const float* deltas, int64_
     deltas_to_view_major(deltas, c->stage_a.p, P, int(M), C, c->stream);
     c->attn_scratch.ensure(attend_scratch_floats(P, C, int(M), int(heads)));
     attend(V, c->stage_a.p, P, C, int(M), int(heads), wq, nullptr, wo, gain, zero_scores,
-           c->attn_scratch.p, nullptr, c->stream);
+           c->attn_scratch.p, nullptr, c->flag, c->stream);
     sync_and_check(c);
   });
 }

@@ -257,6 +257,10 @@ __device__ __forceinline__ void split_f16(float x, __half& hi, __half& lo) {
   lo = __float2half_rn(__fmul_rn(__fsub_rn(x, __half2float(hi)), kF16LoScale));
 }
 
+// |x| from which rn_f16(x) is +-inf: the split's hi term cannot hold x.
+constexpr float kF16SplitMax = 65520.0f;
+__device__ __forceinline__ bool split_overflows(float x) { return fabsf(x) >= kF16SplitMax; }
+
 // split_f16 of two values with packed conversions (F2FP.F16.F32.PACK_AB):
 // bit-identical to two split_f16 calls, fewer instructions.
 __device__ __forceinline__ void split_f16x2(float x0, float x1, __half2& hi, __half2& lo) {

@@ -26,6 +26,12 @@ for step in "$@"; do
         python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1
       echo "ncu rc=$?"
       python profiles/traffic_summary.py gpurun_out/traffic.csv > gpurun_out/traffic.json && head -c 400 gpurun_out/traffic.json ;;
+    fullk:*)
+      rest="${step#fullk:}"; k="${rest%%:*}"; skip="${rest##*:}"
+      timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$k" --launch-skip $skip -c 1 \
+        -o "gpurun_out/full_${k//[^a-zA-Z0-9_]/_}_$skip" -f \
+        python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > "gpurun_out/ncu_full.log" 2>&1
+      echo "ncu full $k skip $skip rc=$?" ;;
     full:*)
       k="${step#full:}"
       timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$k" -c 1 \
@@ -34,3 +40,4 @@ for step in "$@"; do
       echo "ncu full $k rc=$?" ;;
   esac
 done
+# (appended) fullk:<regex>:<skip> -- --set full of the (skip+1)-th matching launch

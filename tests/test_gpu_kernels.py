@@ -89,3 +89,54 @@ def test_conv3x3_fused_options(oracle, model, impl, variant):
     got = y.cpu().numpy()
     err = np.abs(got - want).max()
     assert err <= 3e-5 * max(1.0, np.abs(want).max()), (variant, impl, err)
+
+
+@pytest.mark.parametrize("where", ["input", "weight"])
+def test_fp16_split_overflow_is_numeric_error(model, where):
+    """The tensor-core conv's 3-term fp16 split cannot hold |x| >= 65520 (the
+    hi term rounds to inf): such an operand reports NumericError instead of a
+    silently wrong result; the SIMT conv (impl 1) computes it in fp32, and the
+    context stays usable."""
+    import torch
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((1, 16, 16, 32)).astype(np.float32)
+    w = (rng.standard_normal((32, 32, 3, 3)) / 17.0).astype(np.float32)
+    if where == "input":
+        x[0, 5, 7, 3] = 1.0e5
+    else:
+        w[4, 9, 1, 1] = -7.0e4
+    y = torch.empty((1, 16, 16, 32), dtype=torch.float32, device=dev)
+    t = lambda a: torch.from_numpy(a).to(dev)  # noqa: E731
+    with pytest.raises(q.NumericError):
+        model.stage_conv3x3(t(x), t(w), None, y, impl=2)
+    model.stage_conv3x3(t(x), t(w), None, y, impl=1)  # fp32 SIMT: fine
+    assert torch.isfinite(y).all()
+    x[0, 5, 7, 3] = 0.5
+    w[4, 9, 1, 1] = 0.1
+    model.stage_conv3x3(t(x), t(w), None, y, impl=2)  # the context recovers
+    assert torch.isfinite(y).all()
+
+
+def test_attention_split_overflow_is_numeric_error():
+    """The same guard in the tensor-core attention: a V row whose rms-normed
+    value or a head with |x| >= 65520 in the split operand -> NumericError."""
+    import torch
+    from cases import config1
+    m = q.Model(config1().cfg, device=0)
+    dev = torch.device("cuda:0")
+    rng = np.random.default_rng(6)
+    P_, C, M, H = 4096, 32, 8, 1
+    V = rng.standard_normal((P_, C)).astype(np.float32)
+    D = rng.standard_normal((P_, M, C)).astype(np.float32)
+    wq = (rng.standard_normal((H, C, C)) / np.sqrt(C)).astype(np.float32)
+    wo = (rng.standard_normal((H * C, C)) / np.sqrt(C)).astype(np.float32)
+    g = np.ones(C, np.float32)
+    D[100, 3, :] = 2.0e5  # heads are convex mixes of Δ: this texel's head overflows
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    with pytest.raises(q.NumericError):
+        m.stage_attend(t(V), t(D), t(wq), t(wo), t(g))
+    D[100, 3, :] = 0.25
+    Vt = t(V)
+    m.stage_attend(Vt, t(D), t(wq), t(wo), t(g))
+    assert torch.isfinite(Vt).all()
