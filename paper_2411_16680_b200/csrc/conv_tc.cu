@@ -180,10 +180,16 @@ __global__ void __launch_bounds__(NT, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
+  // a settled weight image (made and synchronised by an earlier call) loads
+  // under the previous kernel's tail; a freshly prepared one after the wait
+  if (a.w_early && tid == 0) {
+    tc::mbar_expect_tx(w_full, W_BYTES);
+    tc::bulk_load(sbase + OFF_W, a.wsplit, W_BYTES, w_full);
+  }
   // everything above overlaps the previous kernel under PDL; global data
   // (inputs, residual, outputs, a freshly prepared weight image) only below
   tc::pdl_wait();
-  if (tid == 0) {
+  if (!a.w_early && tid == 0) {
     tc::mbar_expect_tx(w_full, W_BYTES);
     tc::bulk_load(sbase + OFF_W, a.wsplit, W_BYTES, w_full);
   }

@@ -1009,9 +1009,10 @@ void deltas_to_view_major(const float* src, float* dst, int64_t P, int M, int C,
 }
 void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
             const float* const* wq_heads, const float* wo, const float* gain, int zero_scores,
-            float* scratch, const void* wimg, int* ovf, cudaStream_t st) {
+            float* scratch, const void* wimg, bool wimg_early, int* ovf, cudaStream_t st) {
   (void)wq_heads;
-  if (attend_tc(V, deltas, P, C, M, heads, wq, wo, gain, zero_scores, wimg, ovf, st)) return;
+  if (attend_tc(V, deltas, P, C, M, heads, wq, wo, gain, zero_scores, wimg, wimg_early, ovf, st))
+    return;
   // generic fallback: 4C floats of scratch per texel (attend_scratch_floats)
   if (!scratch) throw CudaError("attend: no arena scratch for the generic kernel");
   launch_k(attend_generic_kernel, blocks_for(P, 128), 128, 0, st, V, deltas, P, C, M, heads, wq, wo,

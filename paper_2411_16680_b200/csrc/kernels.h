@@ -88,6 +88,7 @@ struct ConvArgs {
   int w_cin, w_ci0;
   // tensor-core weight image (conv3x3_tc_prepare) for conv3x3_tc; required there
   const void* wsplit;
+  int w_early;  // the image is settled: bulk-load it before griddepcontrol.wait
   // launch conv3x3_tc with programmatic dependent launch (its prologue overlaps
   // the previous kernel's tail); only when nothing it reads before its grid
   // dependency wait was produced by that kernel
@@ -216,14 +217,14 @@ void deltas_to_view_major(const float* src, float* dst, int64_t P, int M, int C,
 // ovf (optional): bit 2 set when an fp16-split operand overflows (ConvArgs.ovf).
 void attend(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
             const float* const* wq_heads, const float* wo, const float* gain, int zero_scores,
-            float* scratch, const void* wimg, int* ovf, cudaStream_t st);
+            float* scratch, const void* wimg, bool wimg_early, int* ovf, cudaStream_t st);
 size_t attend_scratch_floats(int64_t P, int C, int M, int heads);
 // tcgen05 fused attention (attn_tc.cu): C = 32, h in {1,2,4},
 // M in {2,4,8,16}; returns false otherwise.
 bool attend_tc_supported(int C, int M, int heads);
 bool attend_tc(float* V, const float* deltas, int64_t P, int C, int M, int heads, const float* wq,
-               const float* wo, const float* gain, int zero_scores, const void* wimg, int* ovf,
-               cudaStream_t st);
+               const float* wo, const float* gain, int zero_scores, const void* wimg,
+               bool wimg_early, int* ovf, cudaStream_t st);
 // The tensor-core attention's pre-split weight image (bytes; 0: no kernel
 // for this head count) and the kernel that makes it.
 size_t attend_tc_weight_bytes(int heads);

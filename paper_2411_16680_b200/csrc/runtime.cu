@@ -210,7 +210,15 @@ struct lvsg_ctx {
 
   // tensor-core conv weight images (conv3x3_tc_prepare), keyed by weight
   // tensor and input-channel slice; rebuilt whenever weights are (re)bound
-  std::map<std::tuple<const float*, int, int>, std::unique_ptr<lvsg::Buf>> wimg;
+  // (settled: made by an earlier forward call and synchronised since, so a
+  // kernel may bulk-load it before its griddepcontrol.wait, under the
+  // previous kernel's tail)
+  struct WImg {
+    lvsg::Buf buf;
+    bool settled = false;
+  };
+  std::map<std::tuple<const float*, int, int>, std::unique_ptr<WImg>> wimg;
+  bool wimg_fresh = false;  // an image was made during the current call
   lvsg::Buf wimg_tmp;  // uncached image for the stage entry points
   lvsg::Buf stage_a, stage_b, stage_c, stage_cams;  // scratch of the per-stage entry points
   lvsg::Buf attn_scratch;  // generic attention kernel rows (shapes without a tensor-core kernel)
@@ -454,6 +462,17 @@ ConvArgs conv_args(int B, int H, int W, int Cin, int Cout, const float* w, const
   return a;
 }
 
+// Weight images made during this call become "settled" once the stream has
+// drained them (one synchronisation, on the first frame after a weight
+// binding): from then on kernels may bulk-load them before
+// griddepcontrol.wait, overlapping the previous kernel.
+void settle_images(lvsg_ctx* c) {
+  if (!c->wimg_fresh) return;
+  CUDA_OK(cudaStreamSynchronize(c->stream));
+  for (auto& kv : c->wimg) kv.second->settled = true;
+  c->wimg_fresh = false;
+}
+
 // conv3x3 through the dispatcher; a tensor-core launch gets its weight image
 // from the context cache (cached = true: weights bound to the context) or a
 // fresh one in scratch (stage entry points: arbitrary caller weights).
@@ -468,12 +487,14 @@ void run_conv(lvsg_ctx* c, ConvArgs a, cudaStream_t st, int impl = 0, bool cache
       auto it = c->wimg.find(key);
       a.pdl = 1;
       if (it == c->wimg.end()) {
-        auto buf = std::make_unique<Buf>();
-        buf->ensure(nf);
-        prepare(buf->p);
-        it = c->wimg.emplace(key, std::move(buf)).first;
+        auto img = std::make_unique<lvsg_ctx::WImg>();
+        img->buf.ensure(nf);
+        prepare(img->buf.p);
+        it = c->wimg.emplace(key, std::move(img)).first;
+        c->wimg_fresh = true;
       }
-      a.wsplit = it->second->p;
+      a.wsplit = it->second->buf.p;
+      a.w_early = it->second->settled ? 1 : 0;
     } else {
       c->wimg_tmp.ensure(nf);
       prepare(c->wimg_tmp.p);
@@ -599,19 +620,22 @@ void fusion(lvsg_ctx* c, float* V, int64_t L, int64_t H, int64_t W, const Fusion
   c->attn_scratch.ensure(attend_scratch_floats(P, C, M, f.heads));
   // the tensor-core kernel's pre-split weight image, made once per binding
   const void* wimg = nullptr;
+  bool wimg_early = false;
   if (const size_t nb = C == 32 ? attend_tc_weight_bytes(f.heads) : 0) {
     auto key = std::make_tuple(f.wq, -f.heads, 0);
     auto it = c->wimg.find(key);
     if (it == c->wimg.end()) {
-      auto buf = std::make_unique<Buf>();
-      buf->ensure((nb + 3) / 4);
-      attend_tc_prepare(f.wq, f.wo, f.heads, buf->p, c->flag, c->stream);
-      it = c->wimg.emplace(key, std::move(buf)).first;
+      auto img = std::make_unique<lvsg_ctx::WImg>();
+      img->buf.ensure((nb + 3) / 4);
+      attend_tc_prepare(f.wq, f.wo, f.heads, img->buf.p, c->flag, c->stream);
+      it = c->wimg.emplace(key, std::move(img)).first;
+      c->wimg_fresh = true;
     }
-    wimg = it->second->p;
+    wimg = it->second->buf.p;
+    wimg_early = it->second->settled;
   }
   attend(V, c->deltas.p, P, C, M, f.heads, f.wq, nullptr, f.wo, f.gain, c->cfg.ablate_attention,
-         c->attn_scratch.p, wimg, c->flag, c->stream);
+         c->attn_scratch.p, wimg, wimg_early, c->flag, c->stream);
   mark(c, "attention", 1);
   for (const MlpW& m : f.mlps) {
     // conv_mlp_residual (attention.hpp:262-267), batched over layers
@@ -937,6 +961,7 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
   c->target = target;
   c->V = V;
   c->launches = c->launch_total - launches0;
+  settle_images(c);
 }
 
 RenderArgs render_args(lvsg_ctx* c, const float* images, int64_t Hr, int64_t Wr,
@@ -1668,6 +1693,7 @@ lvsg_status lvsg_encode_device(lvsg_ctx* c, int64_t views, const float* enc_imag
     }
     c->stream = own;
     c->launches = c->launch_total - launches0;
+    settle_images(c);
   });
 }
 
@@ -1880,7 +1906,7 @@ lvsg_status lvsg_stage_attend(lvsg_ctx* c, float* V, const float* deltas, int64_
     deltas_to_view_major(deltas, c->stage_a.p, P, int(M), C, c->stream);
     c->attn_scratch.ensure(attend_scratch_floats(P, C, int(M), int(heads)));
     attend(V, c->stage_a.p, P, C, int(M), int(heads), wq, nullptr, wo, gain, zero_scores,
-           c->attn_scratch.p, nullptr, c->flag, c->stream);
+           c->attn_scratch.p, nullptr, false, c->flag, c->stream);
     sync_and_check(c);
   });
 }
