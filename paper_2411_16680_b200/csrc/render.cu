@@ -123,8 +123,9 @@ __device__ __forceinline__ Taps taps_for(const RenderArgs& a, int i, int j) {
 // are f32 from the f64 fractions and the colour an f32 FMA chain (~2 ulp of
 // the reference's f64 blend).
 template <int MM, bool G, bool EXACT>
-__device__ __forceinline__ unsigned blend_views(const RenderArgs& a, const float pt[3],
-                                                const float* beta, float acc[3], float& wsum) {
+__device__ __forceinline__ unsigned blend_views(const RenderArgs& a, const FastCam* fc,
+                                                const float pt[3], const float* beta, float acc[3],
+                                                float& wsum) {
   unsigned need = 0;
   acc[0] = acc[1] = acc[2] = 0.f;
   wsum = 0.f;
@@ -134,7 +135,7 @@ __device__ __forceinline__ unsigned blend_views(const RenderArgs& a, const float
     Footprint f;
     if (EXACT)
       f = project_footprint_nb(a.pc[m], pt);
-    else if (!project_footprint_fast(a.fc[m], pt, f))
+    else if (!project_footprint_fast(fc[m], pt, f))
       need |= 1u << m;  // f: invalid, in-range taps
     const float fx = __double2float_rn(f.fx), fy = __double2float_rn(f.fy);
     const float gx = 1.0f - fx, gy = 1.0f - fy;
@@ -163,13 +164,15 @@ __device__ __forceinline__ unsigned blend_views(const RenderArgs& a, const float
 // colour and weight are zeroed by select). MM == 0: cameras staged in shared
 // memory, branchy footprint.
 template <int MM, bool G = false>
-__global__ void __launch_bounds__(128, MM >= 16 ? 4 : 8) render_fused_kernel(const RenderArgs a) {
+__global__ void __launch_bounds__(128, MM >= 16 ? 4 : 8)
+    render_fused_kernel(const __grid_constant__ RenderArgs a) {
   pdl_grid_sync();
   extern __shared__ DevCam s_cams[];
   if (MM == 0) {
     for (int m = threadIdx.x; m < a.M; m += blockDim.x) s_cams[m] = a.cams[m];
     __syncthreads();
   }
+  const FastCam* fc = a.fc;  // (shared-memory copies measured slower: 818 vs 782 us)
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int rows = a.row1 - a.row0;
   if (idx >= (int64_t)rows * a.Wo) return;
@@ -192,8 +195,8 @@ __global__ void __launch_bounds__(128, MM >= 16 ? 4 : 8) render_fused_kernel(con
     float rgb[3] = {0.f, 0.f, 0.f};
     if constexpr (MM > 0) {
       float acc[3], wsum;
-      if (blend_views<MM, G, false>(a, pt, beta, acc, wsum))
-        blend_views<MM, G, true>(a, pt, beta, acc, wsum);  // rare: a decision within 1e-7 px
+      if (blend_views<MM, G, false>(a, fc, pt, beta, acc, wsum))
+        blend_views<MM, G, true>(a, fc, pt, beta, acc, wsum);  // rare: a decision within 1e-7 px
       const float r = __fdiv_rn(1.0f, fa(wsum, 1e-8f));
 #pragma unroll
       for (int k = 0; k < 3; ++k) rgb[k] = fm(acc[k], r);

@@ -1,0 +1,16 @@
+#!/bin/bash
+# A/B of one kernel family's serialised time between library builds:
+#   ab_kernel.sh <kernel regex> <lib1> <lib2> ...
+k=$1; shift
+for lib in "$@"; do
+  LVSG_LIB=$lib timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k "regex:$k" --csv \
+    --log-file /tmp/ab.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+  python - "$lib" <<'PY'
+import csv, sys
+lines=[l for l in open('/tmp/ab.csv') if l.startswith('"')]
+rows=list(csv.reader(lines)); h=rows[0]; vi=h.index('Metric Value')
+v=[float(r[vi].replace(',',''))/1e3 for r in rows[1:]]
+n=len(v)//6  # six frames: 3 warm-up + profile + 2 timed (per-frame launch count)
+print(sys.argv[1], 'launches', len(v), 'last-frame us', round(sum(v[-n:]),1) if n else None)
+PY
+done
