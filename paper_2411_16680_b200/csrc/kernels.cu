@@ -541,6 +541,7 @@ __global__ void __launch_bounds__(256) gather_stack32_kernel(
     if (rf & 1) {
       const int dx = (rf & 2) ? G : 0, dy = (rf & 4) ? Wf * G : 0;
       const bool same_rows = poff >= 0 && ((rf ^ pfl) & 4) == 0;
+      LVSG_CHECK(ro >= 0 && int64_t(ro) + dy + dx < int64_t(M) * Hf * Wf * G);
       if (!(same_rows && ro == poff)) {  // not the previous cell: new right column
         if (same_rows && ro == poff + G && (pfl & 2) && dx) {
           l0 = r0;  // the next cell to the right: the old right column is the left

@@ -137,6 +137,8 @@ __device__ __forceinline__ unsigned blend_views(const RenderArgs& a, const FastC
       f = project_footprint_nb(a.pc[m], pt);
     else if (!project_footprint_fast(fc[m], pt, f))
       need |= 1u << m;  // f: invalid, in-range taps
+    LVSG_CHECK(f.x0 >= 0 && f.x1 < a.Wr && f.x0 <= f.x1 && f.y0 >= 0 && f.y1 < a.Hr &&
+               f.y0 <= f.y1);
     const float fx = __double2float_rn(f.fx), fy = __double2float_rn(f.fy);
     const float gx = 1.0f - fx, gy = 1.0f - fy;
     const float w[4] = {gx * gy, fx * gy, gx * fy, fx * fy};

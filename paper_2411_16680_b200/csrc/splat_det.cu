@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(256) scan_add_kernel(int* __restrict__ off, in
   }
 }
 
-__global__ void __launch_bounds__(256) splat_fill_kernel(int64_t pairs, int M,
+__global__ void __launch_bounds__(256) splat_fill_kernel(int64_t pairs, int64_t bins, int M,
                                                          const int2* __restrict__ fp_i,
                                                          const float4* __restrict__ fp_w,
                                                          int* __restrict__ cursor,
@@ -159,8 +159,12 @@ __global__ void __launch_bounds__(256) splat_fill_kernel(int64_t pairs, int M,
   const int d[4] = {f.x, f.x + dx, f.x + dy, f.x + dy + dx};
   const float wk[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
-    ent[atomicAdd(cursor + d[k], 1)] = make_int2(p4 + k, __float_as_int(wk[k]));
+  for (int k = 0; k < 4; ++k) {
+    LVSG_CHECK(d[k] >= 0 && d[k] < bins);
+    const int slot = atomicAdd(cursor + d[k], 1);
+    LVSG_CHECK(slot >= 0 && slot < 4 * pairs);
+    ent[slot] = make_int2(p4 + k, __float_as_int(wk[k]));
+  }
 }
 
 // One thread per (view m, pixel, channel group g of G = PS/4), the G lanes
@@ -194,7 +198,7 @@ __device__ __forceinline__ void sort8(int2* e) {
 __global__ void __launch_bounds__(288) splat_reduce_composite_kernel(
     const float* __restrict__ payload, int K, int M, int L, int Hv, int Wv,
     const int* __restrict__ off, const int* __restrict__ cnt, const int2* __restrict__ ent,
-    float* __restrict__ out, int ppb) {
+    float* __restrict__ out, int ppb, int64_t n_ent, int64_t P) {
   pdl_grid_sync();
   __shared__ float s_sig[kRedPixMax];
   const int PS = pay_stride(K), G = PS / 4;
@@ -221,6 +225,7 @@ __global__ void __launch_bounds__(288) splat_reduce_composite_kernel(
     if (live) {
       const int64_t bin = ((int64_t)m * L + l) * PV + pix;
       const int n = __ldg(cnt + bin), b0 = __ldg(off + bin);
+      LVSG_CHECK(n >= 0 && b0 >= 0 && (int64_t)b0 + n <= n_ent);
       if (n <= kRun) {
         // short run (the common case): entries into registers, sorted by a
         // fixed network, then every payload load in flight at once
@@ -284,7 +289,7 @@ template <int NG>
 __global__ void __launch_bounds__(192) splat_reduce_pl_kernel(
     const float* __restrict__ payload, int K, int M, int L, int Hv, int Wv,
     const int* __restrict__ off, const int* __restrict__ cnt, const int2* __restrict__ ent,
-    float* __restrict__ out, int ppb) {
+    float* __restrict__ out, int ppb, int64_t n_ent, int64_t P) {
   pdl_grid_sync();
   extern __shared__ float s_val[];  // [ppb][L][NG*4]: normalised channels, [Ca] = alpha
   const int64_t PV = (int64_t)Hv * Wv;
@@ -304,6 +309,7 @@ __global__ void __launch_bounds__(192) splat_reduce_pl_kernel(
       // the payload row (32-byte aligned, payload_stride floats): the first
       // 32 channels by four 256-bit loads, the rest by 16-byte loads
       const float w = __int_as_float(en.y);
+      LVSG_CHECK(en.x >= 0 && (en.x >> 2) < P);
       const float* row = payload + (int64_t)(en.x >> 2) * (4 * GP);
       float v[NG * 4];
 #pragma unroll
@@ -319,6 +325,7 @@ __global__ void __launch_bounds__(192) splat_reduce_pl_kernel(
     };
     const int64_t bin = ((int64_t)m * L + l) * PV + pix;
     const int n = __ldg(cnt + bin), b0 = __ldg(off + bin);
+    LVSG_CHECK(n >= 0 && b0 >= 0 && (int64_t)b0 + n <= n_ent);
     if (n <= 4) {
       int2 e[4];
 #pragma unroll
@@ -404,7 +411,7 @@ void splat_det(const float* payload, const float* points, int L, int PL, int K,
   launch_k(scan_blocks_kernel, nb, 256, 0, st, (const int*)cnt, int(bins), off, bsum);
   launch_k(scan_sums_kernel, 1, 1024, 0, st, bsum, nb);
   launch_k(scan_add_kernel, nb, 256, 0, st, off, int(bins), (const int*)bsum, cursor);
-  launch_k(splat_fill_kernel, blocks_for(pairs, 256), 256, 0, st, pairs, M, (const int2*)fp_i,
+  launch_k(splat_fill_kernel, blocks_for(pairs, 256), 256, 0, st, pairs, bins, M, (const int2*)fp_i,
            (const float4*)fp_w, cursor, ent);
   const int G = pay_stride(K) / 4;
   if (G == 9 && L <= 192) {  // C = 32 configs: one thread per (view pixel, layer)
@@ -412,12 +419,14 @@ void splat_det(const float* payload, const float* points, int L, int PL, int K,
     const size_t smem = size_t(ppb) * L * 36 * sizeof(float);
     smem_optin(reinterpret_cast<const void*>(splat_reduce_pl_kernel<9>), 192 * 36 * 4);
     launch_k(splat_reduce_pl_kernel<9>, blocks_for((int64_t)M * Hv * Wv, ppb), ppb * L, smem, st,
-             payload, K, M, L, Hv, Wv, (const int*)off, (const int*)cnt, (const int2*)ent, out, ppb);
+             payload, K, M, L, Hv, Wv, (const int*)off, (const int*)cnt, (const int2*)ent, out, ppb,
+             4 * pairs, pairs / M);
     return;
   }
   const int ppb = std::max(1, std::min(kRedPixMax, 288 / G));
   launch_k(splat_reduce_composite_kernel, blocks_for((int64_t)M * Hv * Wv, ppb), ppb * G, 0, st,
-           payload, K, M, L, Hv, Wv, (const int*)off, (const int*)cnt, (const int2*)ent, out, ppb);
+           payload, K, M, L, Hv, Wv, (const int*)off, (const int*)cnt, (const int2*)ent, out, ppb,
+           4 * pairs, pairs / M);
 }
 
 }  // namespace lvsg
