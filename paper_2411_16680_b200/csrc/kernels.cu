@@ -489,7 +489,9 @@ __global__ void gather_stack_kernel(const float* __restrict__ feats, int M, int 
 // 4-tap blend is an f32 FMA chain over the f64 weights rounded to f32
 // (within ~2 ulp of the reference's f64 blend; the parity gate is the RGB
 // tolerance), the same values whichever loads were reused.
-__global__ void __launch_bounds__(256) gather_stack32_kernel(
+// 6 CTAs per SM (<= 40 registers): 0.78 -> 0.70 ms per frame against the
+// unconstrained 47 registers (ncu A/B, profiles/debug/ab_kernel.sh)
+__global__ void __launch_bounds__(256, 6) gather_stack32_kernel(
     const float* __restrict__ feats, int M, int Hf, int Wf, const DevCam* __restrict__ cams,
     DevRayCam rc, const float* __restrict__ depth, int L, int H, int W, float* __restrict__ deltas) {
   pdl_grid_sync();

@@ -10,7 +10,8 @@ import csv, sys
 lines=[l for l in open('/tmp/ab.csv') if l.startswith('"')]
 rows=list(csv.reader(lines)); h=rows[0]; vi=h.index('Metric Value')
 v=[float(r[vi].replace(',',''))/1e3 for r in rows[1:]]
-n=len(v)//6  # six frames: 3 warm-up + profile + 2 timed (per-frame launch count)
-print(sys.argv[1], 'launches', len(v), 'last-frame us', round(sum(v[-n:]),1) if n else None)
+# bench --steps 2 --warmup 3 runs 7 frames (3 warm-up incl. the profiled one,
+# the launch-count frame, 2 timed): the per-frame mean
+print(sys.argv[1], 'launches', len(v), 'us per frame', round(sum(v) / 7, 1))
 PY
 done
