@@ -226,6 +226,39 @@ __global__ void __launch_bounds__(256) resize_hwc4c_kernel(const float* __restri
   }
 }
 
+// resize_hwc for C = 4G (G = 8 or 9: the 32-channel maps and the padded
+// 36-float feedback rows): one block row per output image row (b, y), its
+// y taps computed once; threads over (x, channel group g), g fastest, the
+// scales divided once per thread (the per-element version spent most of its
+// instructions in f64 divisions and 32-bit index divisions).
+template <int G>
+__global__ void __launch_bounds__(256) resize_hwc4g_kernel(const float* __restrict__ in,
+                                                           float* __restrict__ out, int H, int W,
+                                                           int Ho, int Wo) {
+  pdl_grid_sync();
+  const double sy = dd(double(H), double(Ho)), sx = dd(double(W), double(Wo));
+  const int row = blockIdx.y;  // b * Ho + y
+  const int b = row / Ho, y = row - b * Ho;
+  int y0, y1;
+  float fy;
+  resize_tap_s(y, sy, H, y0, y1, fy);
+  const float4* s4 = reinterpret_cast<const float4*>(in);
+  float4* o4 = reinterpret_cast<float4*>(out) + (int64_t)row * Wo * G;
+  const int r0 = (b * H + y0) * W, r1 = (b * H + y1) * W;
+  for (int e = blockIdx.x * 256 + threadIdx.x; e < Wo * G; e += gridDim.x * 256) {
+    const int x = e / G, g = e - x * G;
+    int x0, x1;
+    float fx;
+    resize_tap_s(x, sx, W, x0, x1, fx);
+    const float4 A = __ldg(s4 + (int64_t)(r0 + x0) * G + g);
+    const float4 Bv = __ldg(s4 + (int64_t)(r0 + x1) * G + g);
+    const float4 Cv = __ldg(s4 + (int64_t)(r1 + x0) * G + g);
+    const float4 D = __ldg(s4 + (int64_t)(r1 + x1) * G + g);
+    o4[e] = make_float4(lerp2(A.x, Bv.x, Cv.x, D.x, fx, fy), lerp2(A.y, Bv.y, Cv.y, D.y, fx, fy),
+                        lerp2(A.z, Bv.z, Cv.z, D.z, fx, fy), lerp2(A.w, Bv.w, Cv.w, D.w, fx, fy));
+  }
+}
+
 // One warp per row: rinv = 1 / sqrt(sum(x^2)/C + 1e-6).
 __global__ void rms_rinv_kernel(const float* x, float* rinv, int64_t rows, int C) {
   pdl_grid_sync();
@@ -921,8 +954,15 @@ void resize_hwc(const float* in, float* out, int B, int H, int W, int C, int Ho,
   if (C % 4 == 0 && al) {
     const int64_t px = (int64_t)B * Ho * Wo;
     const int G = C / 4;
-    if (G >= 4 && G <= 64 && (int64_t)B * H * W * G < (int64_t(1) << 31) &&
-        px * G < (int64_t(1) << 31)) {
+    if ((G == 8 || G == 9) && (int64_t)B * H * W * G < (int64_t(1) << 31) &&
+        px * G < (int64_t(1) << 31) && (int64_t)B * Ho < 65536) {
+      const dim3 grid(unsigned(std::min<int64_t>((int64_t(Wo) * G + 255) / 256, 8)), unsigned(B * Ho));
+      if (G == 8)
+        launch_k(resize_hwc4g_kernel<8>, grid, 256, 0, st, in, out, H, W, Ho, Wo);
+      else
+        launch_k(resize_hwc4g_kernel<9>, grid, 256, 0, st, in, out, H, W, Ho, Wo);
+    } else if (G >= 4 && G <= 64 && (int64_t)B * H * W * G < (int64_t(1) << 31) &&
+               px * G < (int64_t(1) << 31)) {
       const int64_t blocks = (px * G + 255) / 256;
       launch_k(resize_hwc4c_kernel, int(std::min<int64_t>(blocks, 148 * 16)), 256, 0, st, in, out, B,
                H, W, G, Ho, Wo);
