@@ -3,8 +3,10 @@
 #   ab_kernel.sh <kernel regex> <lib1> <lib2> ...
 k=$1; shift
 for lib in "$@"; do
+  rm -f /tmp/ab.csv
   LVSG_LIB=$lib timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k "regex:$k" --csv \
-    --log-file /tmp/ab.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+    --log-file /tmp/ab.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /tmp/ab.log 2>&1 \
+    || { echo "$lib: run failed"; tail -3 /tmp/ab.log; continue; }
   python - "$lib" <<'PY'
 import csv, sys
 lines=[l for l in open('/tmp/ab.csv') if l.startswith('"')]
@@ -12,6 +14,6 @@ rows=list(csv.reader(lines)); h=rows[0]; vi=h.index('Metric Value')
 v=[float(r[vi].replace(',',''))/1e3 for r in rows[1:]]
 # bench --steps 2 --warmup 3 runs 7 frames (3 warm-up incl. the profiled one,
 # the launch-count frame, 2 timed): the per-frame mean
-print(sys.argv[1], 'launches', len(v), 'us per frame', round(sum(v) / 7, 1))
+print(sys.argv[1], 'launches', len(v), 'us per frame', round(sum(v) / 7, 1), 'last', [round(x, 1) for x in v[-16:]])
 PY
 done
