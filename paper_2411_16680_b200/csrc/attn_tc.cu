@@ -35,10 +35,6 @@
 #include "kernels.h"
 #include "tc.cuh"
 
-#ifndef LVSG_ATT_DEBUG
-#define LVSG_ATT_DEBUG 0
-#endif
-
 namespace lvsg {
 namespace {
 
@@ -418,9 +414,6 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
 
     if (grp == 0) start_tile(0);
     for (int i = 0; i < ntl; ++i) {
-#if LVSG_ATT_DEBUG & 1
-      if (NGRP > 1) named_sync(2, NCONS * NGRP);  // debug: both groups in lockstep per tile
-#endif
       // ---- scores(i) for this group's heads: S in registers, one pass over Δ ----
       float w[HG][MM];
       if (zero_scores) {
