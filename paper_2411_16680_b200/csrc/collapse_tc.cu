@@ -1,0 +1,267 @@
+// layer_collapse (network.hpp:440-455) on the sm_100a tensor core, C = 32:
+//
+//   cat = [a | b]                  (the two layers of a pair, K = 64)
+//   h   = gelu(cat W1 + b1)        tcgen05.mma kind::f16, N = 64
+//   out = (a + b) / 2 + (h W2 + b2)  tcgen05.mma kind::f16, N = 32
+//
+// with the conv's / attention's 3-term fp16 split (tc::split_f16: ~2^-22
+// relative error per product, fp32 accumulation in TMEM). Per 64-channel K
+// step pair: MMA1 N = 2n over [Wh ; Wl'] and MMA2 N = n with the lo' rows of
+// the activations; the epilogue forms D[:, c] + 2^-11 D[:, n + c].
+//
+// One 128-texel tile per loop iteration (thread = texel row = TMEM lane):
+// load a, b -> stage [a|b] -> MMA1 -> GELU epilogue -> stage h -> MMA2 ->
+// output epilogue. No warp specialisation: two CTAs per SM (56 KB of shared
+// memory and 256 TMEM columns each) overlap each other's phases. The split
+// weight image is made once per weight binding (collapse_tc_prepare) and
+// arrives by one bulk copy per CTA.
+#include <cuda.h>
+
+#include <algorithm>
+
+#include "host.h"
+#include "kernels.h"
+#include "tc.cuh"
+
+namespace lvsg {
+namespace {
+
+constexpr int C = 32;
+constexpr int K1 = 2 * C;                     // [a | b]
+constexpr int N1 = 2 * C;                     // hidden width
+constexpr int N2 = C;                         // output width
+constexpr int TILE = 128;
+constexpr int NJ = K1 / 8;                    // 8-channel fp16 K chunks (both MMAs: K = 64)
+constexpr int A_LBO = TILE * 16;              // one 8-channel plane of 128 rows
+constexpr int A_HALF = NJ * A_LBO;            // hi (or lo') planes: 16 KB
+constexpr int A_BYTES = 2 * A_HALF;           // 32 KB
+constexpr int W1_BYTES = NJ * 2 * N1 * 16;    // [W1h ; W1l'] per chunk: 16 KB
+constexpr int W2_BYTES = NJ * 2 * N2 * 16;    // 8 KB
+constexpr int OFF_A = 0;
+constexpr int OFF_W1 = OFF_A + A_BYTES;
+constexpr int OFF_W2 = OFF_W1 + W1_BYTES;
+constexpr int OFF_BAR = OFF_W2 + W2_BYTES;
+constexpr int SMEM_USED = OFF_BAR + 4 * 8 + 16;
+// requested dynamic shared memory: caps residency at two CTAs per SM, so the
+// 256-column TMEM allocations of co-resident CTAs always fit (512 columns)
+constexpr int SMEM_BYTES = 96 * 1024;
+constexpr uint32_t TMEM_COLS = 256;           // D1: 128 columns, D2: 64 columns
+static_assert(SMEM_USED <= SMEM_BYTES, "shared memory layout");
+
+// row `row` of the K = 64 A operand <- x[64]; returns a split overflow
+__device__ __forceinline__ bool stage_row64(uint8_t* a, int row, const float* x) {
+  bool ovf = false;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    __align__(16) __half2 h[4], l[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      tc::split_f16x2(x[8 * j + 2 * k], x[8 * j + 2 * k + 1], h[k], l[k]);
+      ovf |= tc::split_overflows(x[8 * j + 2 * k]) | tc::split_overflows(x[8 * j + 2 * k + 1]);
+    }
+    *reinterpret_cast<uint4*>(a + j * A_LBO + row * 16) = *reinterpret_cast<uint4*>(h);
+    *reinterpret_cast<uint4*>(a + A_HALF + j * A_LBO + row * 16) = *reinterpret_cast<uint4*>(l);
+  }
+  return ovf;
+}
+
+// D (=) A * B over K = 64: MMA1 N = 2n into d, MMA2 N = n (lo' x hi) into d + n.
+__device__ __forceinline__ void mma_split64(uint32_t d, uint32_t a, uint32_t b, int n) {
+  const uint32_t id1 = tc::idesc_f16(128, 2 * n), id2 = tc::idesc_f16(128, n);
+  const uint64_t ah = tc::smem_desc(a, A_LBO, 128), al = tc::smem_desc(a + A_HALF, A_LBO, 128);
+  const uint64_t bd = tc::smem_desc(b, 2 * n * 16, 128);
+#pragma unroll
+  for (int s = 0; s < NJ / 2; ++s) {
+    const uint64_t ao = uint64_t((2 * s * A_LBO) >> 4), bo = uint64_t((2 * s * 2 * n * 16) >> 4);
+    tc::mma_f16(d, ah + ao, bd + bo, id1, s > 0 ? 1u : 0u);
+    tc::mma_f16(d + uint32_t(n), al + ao, bd + bo, id2, 1u);
+  }
+}
+
+__device__ __forceinline__ void load_row32(const float* p, float* v) {
+  const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+  for (int k = 0; k < C / 4; ++k) {
+    const float4 t = __ldg(q + k);
+    v[4 * k] = t.x, v[4 * k + 1] = t.y, v[4 * k + 2] = t.z, v[4 * k + 3] = t.w;
+  }
+}
+
+__global__ void __launch_bounds__(TILE, 2)
+    collapse_tc_kernel(const float* __restrict__ V, int L2, int PL, const uint8_t* __restrict__ wimg,
+                       const float* __restrict__ b1, const float* __restrict__ b2,
+                       float* __restrict__ out, int num_tiles, int* ovf_flag) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* w_full = bars;       // weight image landed
+  uint64_t* m1_done = bars + 1;  // h pre-activations in TMEM
+  uint64_t* m2_done = bars + 2;  // outputs in TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  tc::pdl_launch_dependents();
+  if (blockIdx.x >= num_tiles) return;
+  const uint32_t sb = tc::smem_u32(smem);
+  if (tid == 0) {
+    tc::mbar_init(w_full, 1);
+    tc::mbar_init(m1_done, 1);
+    tc::mbar_init(m2_done, 1);
+    tc::mbar_init_fence();
+  }
+  if (warp == 0) tc::tmem_alloc(tmem_slot, TMEM_COLS);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t d1 = tmem, d2 = tmem + 2 * N1;
+  const uint32_t lane_base = uint32_t(warp * 32) << 16;  // warp w reads TMEM lanes 32w..32w+31
+  tc::pdl_wait();
+  if (tid == 0) {
+    tc::mbar_expect_tx(w_full, W1_BYTES + W2_BYTES);
+    tc::bulk_load(sb + OFF_W1, wimg, W1_BYTES + W2_BYTES, w_full);
+  }
+  float bias2[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) bias2[c] = __ldg(b2 + c);
+  tc::mbar_wait(w_full, 0);
+  bool ovf = false;
+  const int64_t total = (int64_t)L2 * PL;
+  int it = 0;
+  for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    const int64_t p = (int64_t)tile * TILE + tid;  // output texel (l, q) = (p / PL, p % PL)
+    const bool valid = p < total;
+    float a[C], b[C];
+    if (valid) {
+      const int64_t l = p / PL, q = p - l * PL;
+      load_row32(V + ((2 * l) * PL + q) * C, a);
+      load_row32(V + ((2 * l + 1) * PL + q) * C, b);
+    } else {
+#pragma unroll
+      for (int c = 0; c < C; ++c) a[c] = b[c] = 0.f;
+    }
+    {
+      float x[K1];
+#pragma unroll
+      for (int c = 0; c < C; ++c) x[c] = a[c], x[C + c] = b[c];
+      ovf |= stage_row64(smem + OFF_A, tid, x);
+    }
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (tid == 0) {
+      mma_split64(d1, sb + OFF_A, sb + OFF_W1, N1);
+      tc::commit(m1_done);
+    }
+    tc::mbar_wait(m1_done, uint32_t(it & 1));
+    tc::fence_after();
+    float h[N1];
+    {
+      float lo[32];
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        tc::tmem_ld32(lane_base + d1 + uint32_t(32 * half), h + 32 * half);
+        tc::tmem_ld32(lane_base + d1 + uint32_t(N1 + 32 * half), lo);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float v = fmaf(lo[c], 1.0f / tc::kF16LoScale, h[32 * half + c]);
+          h[32 * half + c] = gelu_ref(fa(v, __ldg(b1 + 32 * half + c)));
+        }
+      }
+    }
+    // MMA1 has read A (m1_done): restage it with h
+    ovf |= stage_row64(smem + OFF_A, tid, h);
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (tid == 0) {
+      mma_split64(d2, sb + OFF_A, sb + OFF_W2, N2);
+      tc::commit(m2_done);
+    }
+    tc::mbar_wait(m2_done, uint32_t(it & 1));
+    tc::fence_after();
+    float y[C], lo[C];
+    tc::tmem_ld32(lane_base + d2, y);
+    tc::tmem_ld32(lane_base + d2 + uint32_t(N2), lo);
+    if (valid) {
+      float4* o = reinterpret_cast<float4*>(out + p * C);
+#pragma unroll
+      for (int c4 = 0; c4 < C / 4; ++c4) {
+        float v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int c = 4 * c4 + k;
+          const float r = fmaf(lo[c], 1.0f / tc::kF16LoScale, y[c]);
+          v[k] = fa(fm(fa(a[c], b[c]), 0.5f), fa(r, bias2[c]));
+        }
+        o[c4] = make_float4(v[0], v[1], v[2], v[3]);
+      }
+    }
+    // every thread has read D1 / D2 and MMA2 has read A before the next tile
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+  }
+  if (ovf && ovf_flag) atomicOr(ovf_flag, 2);
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, TMEM_COLS);
+}
+
+// The image: [W1h ; W1l'] (rows n = hidden unit, K-major chunks) then
+// [W2h ; W2l'], the layout stage_weights gives the attention (attn_tc.cu).
+__global__ void collapse_tc_weights_kernel(const float* __restrict__ w1,
+                                           const float* __restrict__ w2, uint8_t* out,
+                                           int* ovf_flag) {
+  pdl_grid_sync();
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  __half* bh = reinterpret_cast<__half*>(out);
+  bool ovf = false;
+  if (e < NJ * N1 * 8) {  // W1: w(n, k) = w1[k][n], [2C][2C]
+    const int k8 = e & 7, n = (e >> 3) % N1, j = (e >> 3) / N1;
+    const float x = __ldg(w1 + (8 * j + k8) * N1 + n);
+    __half hi, lo;
+    tc::split_f16(x, hi, lo);
+    ovf = tc::split_overflows(x);
+    bh[(j * 2 * N1 + n) * 8 + k8] = hi;
+    bh[(j * 2 * N1 + N1 + n) * 8 + k8] = lo;
+  } else if (e < NJ * N1 * 8 + NJ * N2 * 8) {  // W2: w(n, k) = w2[k][n], [2C][C]
+    const int f = e - NJ * N1 * 8;
+    const int k8 = f & 7, n = (f >> 3) % N2, j = (f >> 3) / N2;
+    const float x = __ldg(w2 + (8 * j + k8) * N2 + n);
+    __half hi, lo;
+    tc::split_f16(x, hi, lo);
+    ovf = tc::split_overflows(x);
+    __half* b2h = bh + W1_BYTES / 2;
+    b2h[(j * 2 * N2 + n) * 8 + k8] = hi;
+    b2h[(j * 2 * N2 + N2 + n) * 8 + k8] = lo;
+  }
+  if (ovf && ovf_flag) atomicOr(ovf_flag, 2);
+}
+
+}  // namespace
+
+size_t collapse_tc_weight_bytes() { return W1_BYTES + W2_BYTES; }
+
+void collapse_tc_prepare(const float* w1, const float* w2, void* dst, int* ovf, cudaStream_t st) {
+  const int n = NJ * N1 * 8 + NJ * N2 * 8;
+  launch_k(collapse_tc_weights_kernel, (n + 255) / 256, 256, 0, st, w1, w2,
+           static_cast<uint8_t*>(dst), ovf);
+}
+
+bool layer_collapse_tc(const float* V, int L, int64_t PL, int C_, const float* wimg,
+                       const float* b1, const float* b2, float* out, int* ovf, cudaStream_t st) {
+  if (C_ != C || !wimg || (reinterpret_cast<uintptr_t>(wimg) & 15) || (L & 1) ||
+      (reinterpret_cast<uintptr_t>(V) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
+    return false;
+  const int64_t total = (int64_t)(L / 2) * PL;
+  const int64_t tiles = (total + TILE - 1) / TILE;
+  if (tiles >= (int64_t(1) << 31) || PL >= (int64_t(1) << 31)) return false;
+  smem_optin(reinterpret_cast<const void*>(collapse_tc_kernel), SMEM_BYTES);
+  const int grid = int(std::min<int64_t>(tiles, int64_t(sm_count()) * 2));
+  launch_pdl(true, collapse_tc_kernel, grid, TILE, SMEM_BYTES, st, V, L / 2, int(PL),
+             reinterpret_cast<const uint8_t*>(wimg), b1, b2, out, int(tiles), ovf);
+  return true;
+}
+
+}  // namespace lvsg

@@ -237,6 +237,13 @@ void blend_logits(const float* V, const float* deltas, int64_t P, int C, int M,
 // layer_collapse (network.hpp:440-455): V [L,H,W,C] -> out [L/2,H,W,C].
 void layer_collapse(const float* V, int L, int64_t PL, int C, const float* w1, const float* b1,
                     const float* w2, const float* b2, float* out, cudaStream_t st);
+// layer_collapse on tcgen05 (collapse_tc.cu, C = 32): wimg is
+// collapse_tc_prepare's split image of (w1, w2), made once per binding;
+// false when the shape does not apply.
+size_t collapse_tc_weight_bytes();
+void collapse_tc_prepare(const float* w1, const float* w2, void* dst, int* ovf, cudaStream_t st);
+bool layer_collapse_tc(const float* V, int L, int64_t PL, int C, const float* wimg,
+                       const float* b1, const float* b2, float* out, int* ovf, cudaStream_t st);
 // C = 32 specialisations (fast32.cu); return false when the shape differs.
 bool layer_collapse32(const float* V, int L, int64_t PL, int C, const float* w1, const float* b1,
                       const float* w2, const float* b2, float* out, cudaStream_t st);

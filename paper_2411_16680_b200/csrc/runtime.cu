@@ -462,6 +462,16 @@ ConvArgs conv_args(int B, int H, int W, int Cin, int Cout, const float* w, const
   return a;
 }
 
+// LVSG_COLLAPSE=simt keeps the layer-collapse MLP on the fp32 SIMT kernel
+// (A/B and parity comparisons).
+bool collapse_simt() {
+  static const bool on = [] {
+    const char* e = getenv("LVSG_COLLAPSE");
+    return e && e[0] == 's';
+  }();
+  return on;
+}
+
 // Weight images made during this call become "settled" once the stream has
 // drained them (one synchronisation, on the first frame after a weight
 // binding): from then on kernels may bulk-load them before
@@ -886,7 +896,22 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
     const StepPlan& sp = plan.steps[s];
     const StepW& sw = W.steps[s];
     for (const ConvPairW& cw : sw.collapse) {
-      layer_collapse(V, int(L), H * Wd, C, cw.w1, cw.b1, cw.w2, cw.b2, Vs, st);
+      // the tensor-core MLP takes its split weight image from the context cache
+      const float* wimg = nullptr;
+      if (C == 32 && !collapse_simt()) {
+        auto key = std::make_tuple(cw.w1, -1000, 0);
+        auto it = c->wimg.find(key);
+        if (it == c->wimg.end()) {
+          auto img = std::make_unique<lvsg_ctx::WImg>();
+          img->buf.ensure((collapse_tc_weight_bytes() + 3) / 4);
+          collapse_tc_prepare(cw.w1, cw.w2, img->buf.p, c->flag, st);
+          it = c->wimg.emplace(key, std::move(img)).first;
+          c->wimg_fresh = true;
+        }
+        wimg = it->second->buf.p;
+      }
+      if (!wimg || !layer_collapse_tc(V, int(L), H * Wd, C, wimg, cw.b1, cw.b2, Vs, c->flag, st))
+        layer_collapse(V, int(L), H * Wd, C, cw.w1, cw.b1, cw.w2, cw.b2, Vs, st);
       mark(c, "collapse", 1);
       std::swap(V, Vs);
       L /= 2;

@@ -386,13 +386,15 @@ m.close()
 """
 
 
-@pytest.mark.parametrize("env", [{"LVSG_CONV": "simt"}, {"LVSG_PDL": "0"}],
-                         ids=["conv_simt", "no_pdl"])
+@pytest.mark.parametrize("env", [{"LVSG_CONV": "simt"}, {"LVSG_COLLAPSE": "simt"},
+                                 {"LVSG_PDL": "0"}],
+                         ids=["conv_simt", "collapse_simt", "no_pdl"])
 def test_kernel_variants_match_default(tmp_path, env):
     """Environment switches (one per process) against the default path on
-    1/4-scale config 2: the fp32 SIMT conv instead of the tcgen05 split
-    (RGB gate: a different summation) and launches without programmatic
-    dependent launch (bit-identical: only the launch attribute changes)."""
+    1/4-scale config 2: the fp32 SIMT conv or layer-collapse MLP instead of
+    the tcgen05 split (RGB gate: a different summation) and launches without
+    programmatic dependent launch (bit-identical: only the launch attribute
+    changes)."""
     import os
     import subprocess
     import sys
@@ -401,13 +403,13 @@ def test_kernel_variants_match_default(tmp_path, env):
     for name, extra in (("default", {}), ("variant", env)):
         path = str(tmp_path / f"{name}.npy")
         e = dict(os.environ)
-        for k in ("LVSG_CONV", "LVSG_PDL"):
+        for k in ("LVSG_CONV", "LVSG_COLLAPSE", "LVSG_PDL"):
             e.pop(k, None)
         e.update(extra)
         subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root, path], env=e, check=True,
                        timeout=600)
         outs[name] = np.load(path)
-    if "LVSG_CONV" in env:
+    if "LVSG_CONV" in env or "LVSG_COLLAPSE" in env:
         assert float(np.abs(outs["default"] - outs["variant"]).max()) <= RGB_MAX_ABS
     else:
         assert np.array_equal(outs["default"].view(np.uint32), outs["variant"].view(np.uint32))
