@@ -48,11 +48,13 @@ constexpr int SMEM_BYTES = 96 * 1024;
 constexpr uint32_t TMEM_COLS = 256;           // D1: 128 columns, D2: 64 columns
 static_assert(SMEM_USED <= SMEM_BYTES, "shared memory layout");
 
-// row `row` of the K = 64 A operand <- x[64]; returns a split overflow
-__device__ __forceinline__ bool stage_row64(uint8_t* a, int row, const float* x) {
+// row `row` of a K = 8 NJK A operand (planes of A_LBO bytes; lo' planes at
+// `half` bytes) <- x[8 NJK]; returns whether a value overflows the split
+template <int NJK>
+__device__ __forceinline__ bool stage_row_k(uint8_t* a, int half, int row, const float* x) {
   bool ovf = false;
 #pragma unroll
-  for (int j = 0; j < NJ; ++j) {
+  for (int j = 0; j < NJK; ++j) {
     __align__(16) __half2 h[4], l[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -60,22 +62,29 @@ __device__ __forceinline__ bool stage_row64(uint8_t* a, int row, const float* x)
       ovf |= tc::split_overflows(x[8 * j + 2 * k]) | tc::split_overflows(x[8 * j + 2 * k + 1]);
     }
     *reinterpret_cast<uint4*>(a + j * A_LBO + row * 16) = *reinterpret_cast<uint4*>(h);
-    *reinterpret_cast<uint4*>(a + A_HALF + j * A_LBO + row * 16) = *reinterpret_cast<uint4*>(l);
+    *reinterpret_cast<uint4*>(a + half + j * A_LBO + row * 16) = *reinterpret_cast<uint4*>(l);
   }
   return ovf;
 }
+__device__ __forceinline__ bool stage_row64(uint8_t* a, int row, const float* x) {
+  return stage_row_k<NJ>(a, A_HALF, row, x);
+}
 
-// D (=) A * B over K = 64: MMA1 N = 2n into d, MMA2 N = n (lo' x hi) into d + n.
-__device__ __forceinline__ void mma_split64(uint32_t d, uint32_t a, uint32_t b, int n) {
+// D (=) A * B over K = 8 NJK: MMA1 N = 2n into d, MMA2 N = n (lo' x hi) into d + n.
+template <int NJK>
+__device__ __forceinline__ void mma_split_k(uint32_t d, uint32_t a, int half, uint32_t b, int n) {
   const uint32_t id1 = tc::idesc_f16(128, 2 * n), id2 = tc::idesc_f16(128, n);
-  const uint64_t ah = tc::smem_desc(a, A_LBO, 128), al = tc::smem_desc(a + A_HALF, A_LBO, 128);
+  const uint64_t ah = tc::smem_desc(a, A_LBO, 128), al = tc::smem_desc(a + half, A_LBO, 128);
   const uint64_t bd = tc::smem_desc(b, 2 * n * 16, 128);
 #pragma unroll
-  for (int s = 0; s < NJ / 2; ++s) {
+  for (int s = 0; s < NJK / 2; ++s) {
     const uint64_t ao = uint64_t((2 * s * A_LBO) >> 4), bo = uint64_t((2 * s * 2 * n * 16) >> 4);
     tc::mma_f16(d, ah + ao, bd + bo, id1, s > 0 ? 1u : 0u);
     tc::mma_f16(d + uint32_t(n), al + ao, bd + bo, id2, 1u);
   }
+}
+__device__ __forceinline__ void mma_split64(uint32_t d, uint32_t a, uint32_t b, int n) {
+  mma_split_k<NJ>(d, a, A_HALF, b, n);
 }
 
 __device__ __forceinline__ void load_row32(const float* p, float* v) {
@@ -239,7 +248,148 @@ __global__ void collapse_tc_weights_kernel(const float* __restrict__ w1,
   if (ovf && ovf_flag) atomicOr(ovf_flag, 2);
 }
 
+// ---- ray encodings: rays_k = resize_bilinear(base -> Hk x Wk) @ ray_proj ----
+// (network.hpp:397-413). The A operand is each pixel's resized 32-channel
+// base row (the resize's exact taps, its f32 lerps); one split GEMM, N = 32.
+constexpr int RNJ = C / 8;                       // K = 32
+constexpr int R_AHALF = RNJ * A_LBO;             // 8 KB
+constexpr int R_ABYTES = 2 * R_AHALF;            // 16 KB
+constexpr int R_WBYTES = RNJ * 2 * C * 16;       // 4 KB
+constexpr int R_OFF_W = R_ABYTES;
+constexpr int R_OFF_BAR = R_OFF_W + R_WBYTES;
+constexpr int R_SMEM = R_OFF_BAR + 2 * 8 + 16;
+
+__global__ void __launch_bounds__(TILE, 4)
+    ray_project_tc_kernel(const float* __restrict__ base, int M, int hK, int wK, int Hk, int Wk,
+                          const uint8_t* __restrict__ wimg, float* __restrict__ out,
+                          int num_tiles, int* ovf_flag) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + R_OFF_BAR);
+  uint64_t* w_full = bars;
+  uint64_t* m_done = bars + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  tc::pdl_launch_dependents();
+  if (blockIdx.x >= num_tiles) return;
+  const uint32_t sb = tc::smem_u32(smem);
+  if (tid == 0) {
+    tc::mbar_init(w_full, 1);
+    tc::mbar_init(m_done, 1);
+    tc::mbar_init_fence();
+  }
+  if (warp == 0) tc::tmem_alloc(tmem_slot, 64);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t lane_base = uint32_t(warp * 32) << 16;
+  tc::pdl_wait();
+  if (tid == 0) {
+    tc::mbar_expect_tx(w_full, R_WBYTES);
+    tc::bulk_load(sb + R_OFF_W, wimg, R_WBYTES, w_full);
+  }
+  const double sy = dd(double(hK), double(Hk)), sx = dd(double(wK), double(Wk));
+  tc::mbar_wait(w_full, 0);
+  bool ovf = false;
+  const int n = M * Hk * Wk;
+  int it = 0;
+  for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    const int i = tile * TILE + tid;
+    float f[C];
+    if (i < n) {
+      const int q = i / Wk, x = i - q * Wk;
+      const int m = q / Hk, y = q - m * Hk;
+      const float4* b = reinterpret_cast<const float4*>(base + (int64_t)m * hK * wK * C);
+      int y0, y1, x0, x1;
+      float fy, fx;
+      resize_tap_s(y, sy, hK, y0, y1, fy);
+      resize_tap_s(x, sx, wK, x0, x1, fx);
+#pragma unroll
+      for (int g = 0; g < C / 4; ++g) {
+        const float4 A = __ldg(b + (y0 * wK + x0) * 8 + g);
+        const float4 B = __ldg(b + (y0 * wK + x1) * 8 + g);
+        const float4 Cc = __ldg(b + (y1 * wK + x0) * 8 + g);
+        const float4 D = __ldg(b + (y1 * wK + x1) * 8 + g);
+        f[4 * g] = lerp2(A.x, B.x, Cc.x, D.x, fx, fy);
+        f[4 * g + 1] = lerp2(A.y, B.y, Cc.y, D.y, fx, fy);
+        f[4 * g + 2] = lerp2(A.z, B.z, Cc.z, D.z, fx, fy);
+        f[4 * g + 3] = lerp2(A.w, B.w, Cc.w, D.w, fx, fy);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < C; ++c) f[c] = 0.f;
+    }
+    ovf |= stage_row_k<RNJ>(smem, R_AHALF, tid, f);
+    tc::fence_proxy_async();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (tid == 0) {
+      mma_split_k<RNJ>(tmem, sb, R_AHALF, sb + R_OFF_W, C);
+      tc::commit(m_done);
+    }
+    tc::mbar_wait(m_done, uint32_t(it & 1));
+    tc::fence_after();
+    float y[C], lo[C];
+    tc::tmem_ld32(lane_base + tmem, y);
+    tc::tmem_ld32(lane_base + tmem + uint32_t(C), lo);
+    if (i < n) {
+      float4* o = reinterpret_cast<float4*>(out + (int64_t)i * C);
+#pragma unroll
+      for (int c4 = 0; c4 < C / 4; ++c4)
+        o[c4] = make_float4(fmaf(lo[4 * c4], 1.0f / tc::kF16LoScale, y[4 * c4]),
+                            fmaf(lo[4 * c4 + 1], 1.0f / tc::kF16LoScale, y[4 * c4 + 1]),
+                            fmaf(lo[4 * c4 + 2], 1.0f / tc::kF16LoScale, y[4 * c4 + 2]),
+                            fmaf(lo[4 * c4 + 3], 1.0f / tc::kF16LoScale, y[4 * c4 + 3]));
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+  }
+  if (ovf && ovf_flag) atomicOr(ovf_flag, 2);
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 64);
+}
+
+// ray_proj [32 in][32 out] -> [Wh ; Wl'] image (rows n = output channel).
+__global__ void ray_tc_weights_kernel(const float* __restrict__ proj, uint8_t* out, int* ovf_flag) {
+  pdl_grid_sync();
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= RNJ * C * 8) return;
+  const int k8 = e & 7, n = (e >> 3) % C, j = (e >> 3) / C;
+  const float x = __ldg(proj + (8 * j + k8) * C + n);
+  __half hi, lo;
+  tc::split_f16(x, hi, lo);
+  __half* bh = reinterpret_cast<__half*>(out);
+  bh[(j * 2 * C + n) * 8 + k8] = hi;
+  bh[(j * 2 * C + C + n) * 8 + k8] = lo;
+  if (tc::split_overflows(x) && ovf_flag) atomicOr(ovf_flag, 2);
+}
+
 }  // namespace
+
+size_t ray_tc_weight_bytes() { return R_WBYTES; }
+
+void ray_tc_prepare(const float* proj, void* dst, int* ovf, cudaStream_t st) {
+  launch_k(ray_tc_weights_kernel, (RNJ * C * 8 + 255) / 256, 256, 0, st, proj,
+           static_cast<uint8_t*>(dst), ovf);
+}
+
+bool ray_project_tc(const float* base, int M, int hK, int wK, int Hk, int Wk, const float* wimg,
+                    float* out, int* ovf, cudaStream_t st) {
+  const int64_t n = (int64_t)M * Hk * Wk;
+  if (!wimg || (reinterpret_cast<uintptr_t>(wimg) & 15) || (reinterpret_cast<uintptr_t>(out) & 15) ||
+      (reinterpret_cast<uintptr_t>(base) & 15) || n >= (int64_t(1) << 31) ||
+      (int64_t)M * hK * wK * C >= (int64_t(1) << 31))
+    return false;
+  const int tiles = int((n + TILE - 1) / TILE);
+  smem_optin(reinterpret_cast<const void*>(ray_project_tc_kernel), R_SMEM);
+  const int grid = std::min(tiles, sm_count() * 4);
+  launch_pdl(false, ray_project_tc_kernel, grid, TILE, R_SMEM, st, base, M, hK, wK, Hk, Wk,
+             reinterpret_cast<const uint8_t*>(wimg), out, tiles, ovf);
+  return true;
+}
 
 size_t collapse_tc_weight_bytes() { return W1_BYTES + W2_BYTES; }
 

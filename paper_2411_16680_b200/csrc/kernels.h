@@ -244,6 +244,12 @@ size_t collapse_tc_weight_bytes();
 void collapse_tc_prepare(const float* w1, const float* w2, void* dst, int* ovf, cudaStream_t st);
 bool layer_collapse_tc(const float* V, int L, int64_t PL, int C, const float* wimg,
                        const float* b1, const float* b2, float* out, int* ovf, cudaStream_t st);
+// rays_k = resize(base) @ ray_proj on tcgen05 (collapse_tc.cu, C = 32);
+// wimg: ray_tc_prepare's split image of ray_proj [32, 32].
+size_t ray_tc_weight_bytes();
+void ray_tc_prepare(const float* proj, void* dst, int* ovf, cudaStream_t st);
+bool ray_project_tc(const float* base, int M, int hK, int wK, int Hk, int Wk, const float* wimg,
+                    float* out, int* ovf, cudaStream_t st);
 // C = 32 specialisations (fast32.cu); return false when the shape differs.
 bool layer_collapse32(const float* V, int L, int64_t PL, int C, const float* w1, const float* b1,
                       const float* w2, const float* b2, float* out, cudaStream_t st);

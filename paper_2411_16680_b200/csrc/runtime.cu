@@ -462,8 +462,8 @@ ConvArgs conv_args(int B, int H, int W, int Cin, int Cout, const float* w, const
   return a;
 }
 
-// LVSG_COLLAPSE=simt keeps the layer-collapse MLP on the fp32 SIMT kernel
-// (A/B and parity comparisons).
+// LVSG_COLLAPSE=simt keeps the per-texel MLPs (layer collapse, ray
+// projection) on the fp32 SIMT kernels (A/B and parity comparisons).
 bool collapse_simt() {
   static const bool on = [] {
     const char* e = getenv("LVSG_COLLAPSE");
@@ -859,10 +859,26 @@ void forward_device(lvsg_ctx* c, const float* enc, int64_t He, int64_t We,
       ray_base(cams.ray, ra, c->ray_base.p, st);
       mark(c, "misc", 1);
       for (int k = 0; k < K; ++k) {
-        ray_project(c->ray_base.p, M, hK, wK, int(plan.pyramid[size_t(k)].first),
-                    int(plan.pyramid[size_t(k)].second), W.ray_proj[size_t(k)], C,
-                    c->rays[size_t(k)].p, st,
-                    k < int(c->rayproj_host.size()) ? c->rayproj_host[size_t(k)].data() : nullptr);
+        const int Hk = int(plan.pyramid[size_t(k)].first), Wk = int(plan.pyramid[size_t(k)].second);
+        // C = 32: the 32 x 32 projection as a tcgen05 GEMM (collapse_tc.cu)
+        const float* wimg = nullptr;
+        if (C == 32 && !collapse_simt()) {
+          auto key = std::make_tuple(W.ray_proj[size_t(k)], -2000, 0);
+          auto it = c->wimg.find(key);
+          if (it == c->wimg.end()) {
+            auto img = std::make_unique<lvsg_ctx::WImg>();
+            img->buf.ensure((ray_tc_weight_bytes() + 3) / 4);
+            ray_tc_prepare(W.ray_proj[size_t(k)], img->buf.p, c->flag, st);
+            it = c->wimg.emplace(key, std::move(img)).first;
+            c->wimg_fresh = true;
+          }
+          wimg = it->second->buf.p;
+        }
+        if (!wimg || !ray_project_tc(c->ray_base.p, M, hK, wK, Hk, Wk, wimg, c->rays[size_t(k)].p,
+                                     c->flag, st))
+          ray_project(c->ray_base.p, M, hK, wK, Hk, Wk, W.ray_proj[size_t(k)], C,
+                      c->rays[size_t(k)].p, st,
+                      k < int(c->rayproj_host.size()) ? c->rayproj_host[size_t(k)].data() : nullptr);
         mark(c, "misc", 1);
       }
     }
