@@ -342,14 +342,28 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        float y_ = fmaf(d1[c], 1.0f / tc::kF16LoScale, d0[c]);
-        if constexpr (kAlpha) {
-          float s = 0.f;
+      for (int c = 0; c < 32; ++c) d0[c] = fmaf(d1[c], 1.0f / tc::kF16LoScale, d0[c]);
+      if constexpr (kAlpha) {
+        // the folded channel's 9 taps for 4 output channels per step, the
+        // weights as 16-byte broadcasts (taps ascending per channel)
 #pragma unroll
-          for (int tap = 0; tap < 9; ++tap) s = fmaf(al[tap], walpha_s[tap * 32 + c], s);
-          y_ = fa(y_, s);
+        for (int c4 = 0; c4 < 8; ++c4) {
+          float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+            const float4 w = reinterpret_cast<const float4*>(walpha_s + tap * 32)[c4];
+            s4[0] = fmaf(al[tap], w.x, s4[0]);
+            s4[1] = fmaf(al[tap], w.y, s4[1]);
+            s4[2] = fmaf(al[tap], w.z, s4[2]);
+            s4[3] = fmaf(al[tap], w.w, s4[3]);
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) d0[4 * c4 + k] = fa(d0[4 * c4 + k], s4[k]);
         }
+      }
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        float y_ = d0[c];
         if (a.bias) y_ = fa(y_, bias_s[c]);
         if (a.gelu) y_ = gelu_ref(y_);
         d0[c] = y_;
