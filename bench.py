@@ -498,9 +498,70 @@ def main():
 
         host_frames = [(torch.from_numpy(f.enc_images).pin_memory().numpy(),
                         torch.from_numpy(f.ren_images).pin_memory().numpy(), f) for f in frames]
-        band_h = torch.empty((band_rows, Wo, 3), dtype=torch.float32).pin_memory()
+
+        # rows / view-sharded targets: the same two-frames-in-flight pipeline
+        # as lvsg_submit_frame, built from the device entry points -- frame
+        # k+1's uploads (own stream) run under frame k's solve, frame k's
+        # read-back (own stream) under frame k+1's; two device slots of the
+        # uploaded images and of the frame, released by a host wait on the
+        # read-back of frame k-1 before frame k+1 is enqueued
+        piped = mode == "rows" or sharded
+        if piped:
+            h2d_s = torch.cuda.Stream(device=dev)
+            d2h_s = torch.cuda.Stream(device=dev)
+            enc_d = [enc, torch.empty_like(enc)]
+            ren_d = [ren, torch.empty_like(ren)]
+            rgb_d = [rgb, torch.empty_like(rgb)]
+            outs_t = [out_h, torch.empty_like(out_h).pin_memory()]
+            up_ev = [torch.cuda.Event(), torch.cuda.Event()]
+            done_ev = [torch.cuda.Event(), torch.cuda.Event()]
+            slot_busy = [False, False]
+
+        def piped_step():
+            s = nsub[0] % 2
+            nsub[0] += 1
+            if slot_busy[s]:
+                done_ev[s].synchronize()  # frame k-1 (this slot) read back: slot free
+            with torch.cuda.stream(h2d_s):
+                if mode == "rows":
+                    enc_d[s].copy_(enc_h, non_blocking=True)
+                else:
+                    enc_d[s][v0:v1].copy_(enc_h[v0:v1], non_blocking=True)
+                ren_d[s].copy_(ren_h, non_blocking=True)
+                up_ev[s].record(h2d_s)
+            with torch.cuda.stream(stream):
+                stream.wait_event(up_ev[s])
+                if mode == "rows":
+                    model.forward_render_device(enc_d[s], case.enc_cams, ren_d[s], case.ren_cams,
+                                                case.target, band, stream, rows=(r0, r1))
+                    if world > 1:
+                        dist.all_gather_into_tensor(rgb_d[s], band)
+                    else:
+                        rgb_d[s].copy_(band)
+                else:
+                    if exchange == "fused":
+                        dist.all_reduce(barrier_t)  # no rank still reads the pyramid
+                    model.encode_device(enc_d[s], v0, v1, stream)
+                    exchange_levels()
+                    model.forward_render_device(None, case.enc_cams, ren_d[s], case.ren_cams,
+                                                case.target, rgb_d[s], stream, enc_hw=(He, We))
+                d2h_s.wait_stream(stream)
+            with torch.cuda.stream(d2h_s):
+                if rank == 0 or mode != "rows":
+                    outs_t[s].copy_(rgb_d[s], non_blocking=True)
+                done_ev[s].record(d2h_s)
+            slot_busy[s] = True
+
+        def piped_drain():
+            for s in range(2):
+                if slot_busy[s]:
+                    done_ev[s].synchronize()
+                    slot_busy[s] = False
 
         def e2e_step():
+            if piped:
+                piped_step()
+                return
             if mode == "frames":
                 # pipelined host frames, this rank's share of the video
                 if len(pending) == 2:
@@ -510,44 +571,20 @@ def main():
                                                   outs[nsub[0] % 2]))
                 nsub[0] += 1
                 return
-            if mode == "rows":
-                # every rank: both image sets up, the solve, its band, the
-                # band all-gather; rank 0 reads the whole frame back
-                with torch.cuda.stream(stream):
-                    enc.copy_(enc_h, non_blocking=True)
-                    ren.copy_(ren_h, non_blocking=True)
-                    step()
-                    if rank == 0:
-                        out_h.copy_(rgb, non_blocking=True)
-                stream.synchronize()
-                return
-            if not sharded:
-                # pipelined host frames (lvsg_submit_frame / lvsg_wait_frame): at
-                # most two in flight, so frame k+1's uploads run under frame k
-                if len(pending) == 2:
-                    model.wait_frame(pending.pop(0))
-                pending.append(model.submit_frame(e_np, case.enc_cams, r_np, case.ren_cams,
-                                                  case.target, outs[nsub[0] % 2]))
-                nsub[0] += 1
-                return
-            # this rank's encoder views up and encoded, the shares
-            # all-gathered (on the frame stream), then the host C ABI with a
-            # NULL encoder list: render views uploaded under the forward pass,
-            # the frame read back in bands
-            with torch.cuda.stream(stream):
-                enc[v0:v1].copy_(enc_h[v0:v1], non_blocking=True)
-                if exchange == "fused":
-                    dist.all_reduce(barrier_t)
-                model.encode_device(enc, v0, v1, stream)
-                exchange_levels()
-            stream.synchronize()
-            model.forward_render(None, case.enc_cams, r_np, case.ren_cams, case.target, out=o_np,
-                                 enc_hw=(He, We))
+            # pipelined host frames (lvsg_submit_frame / lvsg_wait_frame): at
+            # most two in flight, so frame k+1's uploads run under frame k
+            if len(pending) == 2:
+                model.wait_frame(pending.pop(0))
+            pending.append(model.submit_frame(e_np, case.enc_cams, r_np, case.ren_cams,
+                                              case.target, outs[nsub[0] % 2]))
+            nsub[0] += 1
 
         for _ in range(3):  # warm-up: both frame slots allocate their buffers
             e2e_step()
         while pending:
             model.wait_frame(pending.pop(0))
+        if piped:
+            piped_drain()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -558,19 +595,24 @@ def main():
                 print(f"e2e step {time.perf_counter() - t0:.4f}", file=sys.stderr)
         while pending:
             model.wait_frame(pending.pop(0))
+        if piped:
+            piped_drain()
         sec = shard.max_over_ranks(time.perf_counter() - t0, dev)
         h2d = (enc_h[v0:v1].numel() if sharded else enc_h.numel()) * 4 + ren_h.numel() * 4
+        d2h = out_h.numel() * 4 if (rank == 0 or mode != "rows") else 0
         e2e = {"value": shard.aggregate_fps(units, args.e2e_steps, sec), "unit": "frames/s",
                "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(out_h.numel() * 4), "steps": args.e2e_steps,
+               "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps,
                "path": ("lvsg_submit_frame / lvsg_wait_frame (host C ABI, pinned buffers, "
-                        "two frames in flight)" if mode in ("targets", "frames") and not sharded
-                        else "pinned host views -> device (every rank) -> "
+                        "two frames in flight)" if not piped
+                        else "pinned host views -> device (every rank, upload stream) -> "
                         "lvsg_forward_render_rows_device (this rank's band) -> NCCL all-gather "
-                        "of the bands -> rank 0 reads the frame back" if mode == "rows" else
-                        "pinned host encoder views (own share) -> lvsg_encode_device -> pyramid "
-                        "exchange -> lvsg_forward_render (NULL encoder list; pinned render "
-                        "views in, pinned frame out)")}
+                        "of the bands -> rank 0 reads the frame back (read-back stream); two "
+                        "frames in flight" if mode == "rows" else
+                        "pinned host views (own encoder share + render views, upload stream) "
+                        "-> lvsg_encode_device -> pyramid exchange -> "
+                        "lvsg_forward_render_device (resident pyramid) -> pinned frame "
+                        "(read-back stream); two frames in flight")}
         if not sharded and mode == "targets":
             # input-side decimation variant: only the
             # 1080p views are uploaded; the encoder input is their device

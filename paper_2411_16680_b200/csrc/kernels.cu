@@ -1045,6 +1045,26 @@ __global__ void deltas_to_view_major_kernel(const float* __restrict__ src, float
     dst[e] = src[(p * M + m) * C + c];
   }
 }
+__global__ void copy_pinned_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                   size_t bytes, int vec) {
+  pdl_grid_sync();  // the previous frame's kernels may still read dst
+  const size_t n16 = vec ? bytes / 16 : 0;
+  const size_t t = blockIdx.x * size_t(blockDim.x) + threadIdx.x, nt = size_t(gridDim.x) * blockDim.x;
+  for (size_t i = t; i < n16; i += nt)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  for (size_t i = n16 * 16 + t; i < bytes; i += nt) dst[i] = src[i];
+}
+void copy_from_pinned(void* dst, const void* pinned_src, size_t bytes, cudaStream_t st) {
+  if (!bytes) return;
+  void* src = nullptr;
+  if (cudaHostGetDevicePointer(&src, const_cast<void*>(pinned_src), 0) != cudaSuccess)
+    throw CudaError("copy_from_pinned: source is not mapped pinned memory");
+  const int vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  const int blocks = int(std::min<size_t>((bytes / 16 + 255) / 256 + 1, 16));
+  launch_k(copy_pinned_kernel, blocks, 256, 0, st, static_cast<const uint8_t*>(src),
+           static_cast<uint8_t*>(dst), bytes, vec);
+}
+
 void deltas_to_view_major(const float* src, float* dst, int64_t P, int M, int C, cudaStream_t st) {
   const int64_t n = P * M * C;
   launch_k(deltas_to_view_major_kernel, int(std::min<int64_t>((n + 255) / 256, 148 * 16)), 256, 0,

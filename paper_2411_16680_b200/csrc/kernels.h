@@ -209,6 +209,10 @@ void splat_det(const float* payload, const float* points, int L, int PL, int K,
 // Δ from the reference layout [P, M, C] (network.hpp:421-436) into the
 // kernels' layout [M][P][C] (texel-major per view; stage entry points).
 void deltas_to_view_major(const float* src, float* dst, int64_t P, int M, int C, cudaStream_t st);
+// Stream-ordered copy of `bytes` from pinned (device-mapped) host memory by a
+// kernel rather than a copy engine: a small per-frame table then never queues
+// behind a bulk image upload on another stream.
+void copy_from_pinned(void* dst, const void* pinned_src, size_t bytes, cudaStream_t st);
 // V += OTM(rms_norm(V), Δ) (attention.hpp:207-252), in place. scratch:
 // attend_scratch_floats(P, C, M, heads) floats of device memory from the
 // caller's arena (the generic fallback's per-texel rows; none for the

@@ -725,7 +725,10 @@ CamTables upload_cams(lvsg_ctx* c, const lvsg_camera* enc_cams, const lvsg_frust
   }
   t.ray = reinterpret_cast<RayBaseCam*>(dev + off);
   off += size_t(M) * sizeof(RayBaseCam);
-  CUDA_OK(cudaMemcpyAsync(dev, host, off, cudaMemcpyHostToDevice, c->stream));
+  // by a kernel, not a copy engine: on the compute stream a memcpy would
+  // queue behind a bulk upload of the next frame's images (another stream)
+  copy_from_pinned(dev, host, off, c->stream);
+  mark(c, "misc", 1);
   CUDA_OK(cudaEventRecord(c->staging_done, c->stream));
   return t;
 }
@@ -1053,7 +1056,8 @@ DevCam* upload_render_cams(lvsg_ctx* c, const lvsg_camera* cams) {
   DevCam* h = reinterpret_cast<DevCam*>(static_cast<char*>(c->pinned) + off);
   for (size_t m = 0; m < M; ++m) h[m] = dev_cam(cams[m]);
   DevCam* d = reinterpret_cast<DevCam*>(reinterpret_cast<char*>(c->cams_dev.p) + off);
-  CUDA_OK(cudaMemcpyAsync(d, h, M * sizeof(DevCam), cudaMemcpyHostToDevice, c->stream));
+  copy_from_pinned(d, h, M * sizeof(DevCam), c->stream);
+  mark(c, "misc", 1);
   CUDA_OK(cudaEventRecord(c->staging_done, c->stream));
   return d;
 }
