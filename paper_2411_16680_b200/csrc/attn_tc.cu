@@ -82,8 +82,8 @@ struct Smem {
   static constexpr int NS = (BUDGET - OFF_D) / D_BYTES > 8 ? 8 : (BUDGET - OFF_D) / D_BYTES;
   static constexpr int OFF_BAR = OFF_D + NS * D_BYTES;
   // bars: v_full[NV] v_empty[NV] d_full[NS] d_empty[NS] a_full[2] a_free[2] s_done o_done
-  // s_free w_full
-  static constexpr int NBAR = 2 * NV + 2 * NS + 4 + 4;
+  // s_free w_full o_free
+  static constexpr int NBAR = 2 * NV + 2 * NS + 4 + 5;
   static constexpr int BYTES = OFF_BAR + NBAR * 8 + 16;
   static_assert(NS >= 3, "shared memory budget");
   static_assert(OFF_D % 1024 == 0 && OFF_V % 1024 == 0, "128B-swizzled TMA destinations");
@@ -148,6 +148,21 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* map, int c
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(tc::smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_2d(const void* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+#ifndef LVSG_ATT_PF
+#define LVSG_ATT_PF 1
+#endif
+#ifndef LVSG_ATT_PFPOS
+#define LVSG_ATT_PFPOS 1
+#endif
+#ifndef LVSG_ATT_PFMIN
+#define LVSG_ATT_PFMIN 4
+#endif
 __device__ __forceinline__ void tma_store_2d(const void* map, uint32_t src, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -185,6 +200,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
   uint64_t* o_done = s_done + 1;      // O ready
   uint64_t* s_free = o_done + 1;      // every consumer has read S (TMEM S may be rewritten)
   uint64_t* w_full = s_free + 1;      // pre-split weight image landed (wimg != nullptr)
+  uint64_t* o_free = w_full + 1;      // the finishing group has read O (TMEM O may be rewritten)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + S::NBAR);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   tc::pdl_launch_dependents();
@@ -222,6 +238,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
     tc::mbar_init(o_done, 1);
     tc::mbar_init(s_free, NCONS * NGRP);
     tc::mbar_init(w_full, 1);
+    tc::mbar_init(o_free, NCONS);
     tc::mbar_init_fence();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, tmem_cols<H>());
@@ -258,7 +275,12 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
         if (i + 1 < ntl) load_v(i + 1);
         // one 2-D box per view slice: rows m P + [128 i, 128 i + 128) of Δ[M P][32]
         // (rows past P of a view are the next view's, never used; past M P: zero)
-        for (int pass = 0; pass < passes; ++pass)
+        for (int pass = 0; pass < passes; ++pass) {
+          // the next tile's Δ slices into L2 (CTAs with a few tiles
+          // excepted): its first (scores) pass then waits on L2, not HBM
+          if (LVSG_ATT_PF > 0 && pass == LVSG_ATT_PFPOS && ntl > LVSG_ATT_PFMIN && i + 1 < ntl)
+            for (int m = 0; m < M; ++m)
+              tma_prefetch_2d(&dmap, 0, int(m * P) + tile_of(i + 1) * TILE);
           for (int m = 0; m < M; ++m, ++k) {
             const int sl = k % NS;
             if (k >= NS) tc::mbar_wait(&d_empty[sl], uint32_t((k / NS - 1) & 1));
@@ -266,6 +288,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
             tma_load_2d(sb + S::OFF_D + sl * D_BYTES, &dmap, 0, int(m * P) + tile_of(i) * TILE,
                         &d_full[sl]);
           }
+        }
       }
     }
   } else if (warp == 1) {
@@ -309,6 +332,12 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
       if (i + 1 < ntl) issue_s();
       for (int h = 0; h < H; ++h) {
         const int b = next_a(h / HG);
+        if (NGRP == 2 && h == 0 && i > 0) {
+          // two groups: group 1 reads O(i-1) (finish_tile) while group 0
+          // already stages head 0 of tile i; O(i) overwrites it only after
+          tc::mbar_wait(o_free, uint32_t((i - 1) & 1));
+          tc::fence_after();
+        }
         if (tc::elect_one()) {
           mma_split(tmem_o, sb + S::OFF_A + b * A_BYTES, sb + S::OFF_BO + h * S::BO_BYTES, 32,
                     h > 0);
@@ -326,7 +355,11 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
     const int row = q * 32 + lane;  // texel row of the tile == TMEM lane
     const uint32_t lane_base = uint32_t(q * 32) << 16;
     const float inv_temp = __double2float_rn(1.0 / sqrt(double(C)));
-    const bool storer = warp == 2 && lane == 0;
+    // two groups: group 0 starts tiles (rms-norm, n staging) and group 1
+    // finishes them (O + V, TMA store), so neither group runs behind the
+    // other on the Δ ring the two share
+    const int fin_grp = NGRP - 1;
+    const bool storer = warp == 2 + 4 * fin_grp && lane == 0;
     int k = 0;
     // A stagings (the MMA issuer consumes them in the same order): group 0
     // stages n(0), then per tile n(i+1) and its heads; group 1 its heads.
@@ -382,14 +415,18 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
       for (int c = 0; c < C; ++c) x[c] = fm(fm(x[c], r), __ldg(gain + c));
       stage(x);
     };
-    auto finish_tile = [&](int j) {  // V(j) += O(j), TMA store; group 0
+    auto finish_tile = [&](int j) {  // V(j) += O(j), TMA store; group fin_grp
       const int vb = j % NV;
       uint8_t* vt = smem + S::OFF_V + vb * V_BYTES;
+      // the finishing group's own acquire of the V tile (group 0 waited for
+      // it in start_tile; the buffer is refilled only after this store)
+      if (NGRP == 2) tc::mbar_wait(&v_full[vb], uint32_t((j / NV) & 1));
       tc::mbar_wait(o_done, uint32_t(j & 1));
       tc::fence_after();
       float o[C];
       tmem_split(tmem_o, 32, o);
       tc::fence_before();
+      if (NGRP == 2) tc::mbar_arrive(o_free);
 #pragma unroll
       for (int c4 = 0; c4 < 8; ++c4) {
         float4* pv = reinterpret_cast<float4*>(vt + swz(row, c4));
@@ -476,10 +513,8 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
           for (int m = 0; m < MM; ++m) w[h][m] = fm(w[h][m], inv);
         }
       }
-      if (grp == 0) {
-        if (i > 0) finish_tile(i - 1);
-        if (i + 1 < ntl) start_tile(i + 1);
-      }
+      if (grp == fin_grp && i > 0) finish_tile(i - 1);
+      if (grp == 0 && i + 1 < ntl) start_tile(i + 1);
       // ---- mix(i): this group's heads in one pass over Δ ----
       float hd[HG][C];
 #pragma unroll
@@ -505,7 +540,7 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
 #pragma unroll
       for (int h = 0; h < HG; ++h) stage(hd[h]);
     }
-    if (grp == 0) {
+    if (grp == fin_grp) {
       finish_tile(ntl - 1);
       if (storer) tc::bulk_wait<0>();
     }

@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(TILE, 2)
   uint64_t* m1_done = bars + 1;  // h pre-activations in TMEM
   uint64_t* m2_done = bars + 2;  // outputs in TMEM
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = tid >> 5;
   tc::pdl_launch_dependents();
   if (blockIdx.x >= num_tiles) return;
   const uint32_t sb = tc::smem_u32(smem);
