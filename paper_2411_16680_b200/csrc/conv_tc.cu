@@ -123,6 +123,21 @@ __device__ __forceinline__ uint32_t swz(int r, int c4) {
 // kPool: 0 none, 1 the fused mean pool, 2 the pool also stored into peer
 // GPUs' pyramids (the fused exchange; its own instantiation so the common
 // pool path carries no peer code)
+#ifdef LVSG_TIMELINE
+constexpr int kTlSlots = 1024;
+__device__ unsigned long long g_conv_tl[kTlSlots][4];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CONV_TL(k, op)                                                          \
+  if (a.tl_slot > 0 && a.tl_slot <= kTlSlots && threadIdx.x == 0)               \
+    op(&g_conv_tl[a.tl_slot - 1][k], gtime());
+#else
+#define CONV_TL(k, op)
+#endif
+
 template <bool kAlpha, int kPool>
 __global__ void __launch_bounds__(NT, 1)
     conv3x3_tc_kernel(const __grid_constant__ CUtensorMap xmap,
@@ -146,6 +161,7 @@ __global__ void __launch_bounds__(NT, 1)
 
   tc::pdl_launch_dependents();
   if (blockIdx.x >= num_tiles) return;
+  CONV_TL(0, atomicMin)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t sbase = tc::smem_u32(smem);
   if (tid == 0 && (sbase & 1023u)) __trap();  // swizzle atoms need 1 KB alignment
@@ -189,6 +205,7 @@ __global__ void __launch_bounds__(NT, 1)
   // everything above overlaps the previous kernel under PDL; global data
   // (inputs, residual, outputs, a freshly prepared weight image) only below
   tc::pdl_wait();
+  CONV_TL(1, atomicMin)
   if (!a.w_early && tid == 0) {
     tc::mbar_expect_tx(w_full, W_BYTES);
     tc::bulk_load(sbase + OFF_W, a.wsplit, W_BYTES, w_full);
@@ -433,6 +450,10 @@ __global__ void __launch_bounds__(NT, 1)
   }
   tc::fence_before();
   __syncthreads();
+  CONV_TL(2, atomicMax)
+#ifdef LVSG_TIMELINE
+  if (a.tl_slot > 0 && a.tl_slot <= kTlSlots && tid == 0) atomicAdd(&g_conv_tl[a.tl_slot - 1][3], 1ull);
+#endif
   if (warp == 1) tc::tmem_dealloc(tmem, TMEM_COLS);
 }
 
@@ -535,6 +556,28 @@ void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
   if (a.alpha && a.pool_out) throw CudaError("conv3x3_tc: alpha and pool together are not built");
   if (cudaLaunchKernelEx(&cfg, kern, xmap, omap, rmap, a, tiles) != cudaSuccess)
     throw CudaError("conv3x3_tc: launch failed");
+}
+
+void conv_timeline_reset() {
+#ifdef LVSG_TIMELINE
+  static unsigned long long init[kTlSlots][4];
+  for (int i = 0; i < kTlSlots; ++i) {
+    init[i][0] = init[i][1] = ~0ull;
+    init[i][2] = init[i][3] = 0;
+  }
+  cudaMemcpyToSymbol(g_conv_tl, init, sizeof(init));
+#endif
+}
+int conv_timeline_read(unsigned long long* out, int slots) {
+#ifdef LVSG_TIMELINE
+  const int n = slots < kTlSlots ? slots : kTlSlots;
+  cudaMemcpyFromSymbol(out, g_conv_tl, size_t(n) * 4 * sizeof(unsigned long long));
+  return n;
+#else
+  (void)out;
+  (void)slots;
+  return -1;
+#endif
 }
 
 }  // namespace lvsg

@@ -118,7 +118,14 @@ struct ConvArgs {
   // split overflows (|x| >= 65520 rounds to inf in the hi term): the split
   // would be silently wrong, so the call reports LVSG_ERR_NUMERIC instead
   int* ovf;
+  // debug builds with LVSG_TIMELINE: 1-based slot of this launch in the conv
+  // timeline (globaltimer at entry / after the grid dependency wait / exit)
+  int tl_slot;
 };
+// LVSG_TIMELINE builds: reset / read the conv timeline ([slot][4]: entry,
+// ready, exit, CTAs); other builds: no-op / -1
+void conv_timeline_reset();
+int conv_timeline_read(unsigned long long* out, int slots);
 __host__ __device__ inline int w_cin_of(const ConvArgs& a) { return a.w_cin ? a.w_cin : a.Cin; }
 // Dispatches to the tcgen05 3xTF32 kernel when it applies (Cin = Cout = 32,
 // one 16-byte-aligned source), else to the fp32 SIMT kernel. impl: 0 auto,

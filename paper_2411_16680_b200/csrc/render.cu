@@ -9,6 +9,7 @@
 // (tape.hpp:858-917), render_target -> world_points + blended_layer_colors +
 // over_composite (ldm.hpp:98-199, geometry.hpp:84-171).
 #include <algorithm>
+#include <cfloat>
 
 #include "kernels.h"
 
@@ -319,6 +320,23 @@ FastCam fast_cam(const DevCam& d) {
   c.hv = d.hv;
   c.W = d.W;
   c.H = d.H;
+  // f32 decision bounds (kDecisionEpsF): the f32 roundings of the f64
+  // bounds, moved by the band. Views wider or taller than 8192 px: nothing
+  // is clearly inside or outside, every decision takes the exact path.
+  const double lo = 0.5 - 1e-4, e = double(kDecisionEpsF);
+  if (d.W > 8192 || d.H > 8192) {
+    c.in_lo = FLT_MAX;
+    c.in_u = c.in_v = -FLT_MAX;
+    c.out_lo = -FLT_MAX;
+    c.out_u = c.out_v = FLT_MAX;
+    return c;
+  }
+  c.in_lo = float(lo + e);
+  c.in_u = float(d.hu - e);
+  c.in_v = float(d.hv - e);
+  c.out_lo = float(lo - e);
+  c.out_u = float(d.hu + e);
+  c.out_v = float(d.hv + e);
   return c;
 }
 

@@ -203,6 +203,7 @@ struct lvsg_ctx {
   // optional per-stage device timing (lvsg_profile_*): one event after each
   // group of launches; consecutive events bound that group's device time
   bool prof = false;
+  int tl_next = -1;  // conv timeline (LVSG_TIMELINE debug builds): next slot, -1 off
   std::vector<cudaEvent_t> prof_pool;
   std::vector<const char*> prof_labels;
   std::vector<int> prof_counts;
@@ -488,6 +489,7 @@ void settle_images(lvsg_ctx* c) {
 // fresh one in scratch (stage entry points: arbitrary caller weights).
 void run_conv(lvsg_ctx* c, ConvArgs a, cudaStream_t st, int impl = 0, bool cached = true) {
   a.ovf = c->flag;
+  if (c->tl_next >= 0) a.tl_slot = ++c->tl_next;
   const int path = conv3x3_path(a, impl);
   if (path >= 2) {
     const size_t nf = kConvTcWeightBytes / sizeof(float);
@@ -1836,6 +1838,27 @@ lvsg_status lvsg_synchronize(lvsg_ctx* c) {
 }
 
 int64_t lvsg_last_launch_count(const lvsg_ctx* c) { return c ? c->launches : 0; }
+
+// Debug hook (not in the public header): cmd 0 resets and starts the conv
+// timeline, 1 copies `n` slots [entry, ready, exit, CTAs] (globaltimer ns)
+// into buf and returns the slot count through *n, 2 stops it. Builds without
+// LVSG_TIMELINE report *n = -1.
+extern "C" lvsg_status lvsg_debug_conv_timeline(lvsg_ctx* c, int32_t cmd, unsigned long long* buf,
+                                                int32_t* n) {
+  return guard(c, [&] {
+    if (cmd == 0) {
+      CUDA_OK(cudaStreamSynchronize(c->stream));
+      lvsg::conv_timeline_reset();
+      c->tl_next = 0;
+    } else if (cmd == 1) {
+      CUDA_OK(cudaDeviceSynchronize());
+      const int got = lvsg::conv_timeline_read(buf, std::min(*n, c->tl_next));
+      *n = got < 0 ? -1 : got;
+    } else {
+      c->tl_next = -1;
+    }
+  });
+}
 
 lvsg_status lvsg_profile_enable(lvsg_ctx* c, int32_t on) {
   return guard(c, [&] {
