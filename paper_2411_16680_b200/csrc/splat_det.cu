@@ -334,6 +334,14 @@ __global__ void __launch_bounds__(192) splat_reduce_pl_kernel(
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         if (k < n) add(e[k]);
+    } else if (n <= 8) {  // the sorting network again, in registers
+      int2 e[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) e[k] = k < n ? __ldg(ent + b0 + k) : make_int2(0x7fffffff, 0);
+      sort8(e);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < n) add(e[k]);
     } else {
       int last = -1;  // ascending keys by repeated minimum search
       for (int r = 0; r < n; ++r) {
