@@ -524,6 +524,9 @@ __global__ void gather_stack_kernel(const float* __restrict__ feats, int M, int 
 // tolerance), the same values whichever loads were reused.
 // 6 CTAs per SM (<= 40 registers): 0.78 -> 0.70 ms per frame against the
 // unconstrained 47 registers (ncu A/B, profiles/debug/ab_kernel.sh)
+#ifndef LVSG_GATHER_CS
+#define LVSG_GATHER_CS 1
+#endif
 __global__ void __launch_bounds__(256, 6) gather_stack32_kernel(
     const float* __restrict__ feats, int M, int Hf, int Wf, const DevCam* __restrict__ cams,
     DevRayCam rc, const float* __restrict__ depth, int L, int H, int W, float* __restrict__ deltas) {
@@ -598,7 +601,13 @@ __global__ void __launch_bounds__(256, 6) gather_stack32_kernel(
     } else {
       poff = -1;
     }
+#if LVSG_GATHER_CS
+    // evict-first: the 128 B rows stream past L2 without pushing out the
+    // feature level the next warps still sample
+    __stcs(o4 + ((int64_t)m * P + rp) * G + g, v);
+#else
     o4[((int64_t)m * P + rp) * G + g] = v;
+#endif
   }
 }
 
