@@ -296,7 +296,7 @@ def main():
     ap.add_argument("--config", default="config2", choices=["config2", "config3"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--ref-procs", type=int, default=0)
     ap.add_argument("--shard-encoder", action="store_true",
                     help="view-sharded encode + pyramid all-gather even at N=1 (default at N>1)")
