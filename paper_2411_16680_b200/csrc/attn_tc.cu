@@ -330,9 +330,12 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
     issue_s();
     for (int i = 0; i < ntl; ++i) {
       if (i + 1 < ntl) issue_s();
-      for (int h = 0; h < H; ++h) {
+      // heads alternate between the groups (two groups: 0, HG, 1, HG + 1,
+      // ...), so neither group's first staging waits behind the other's last
+      for (int k = 0; k < H; ++k) {
+        const int h = NGRP == 2 ? (k & 1) * HG + (k >> 1) : k;
         const int b = next_a(h / HG);
-        if (NGRP == 2 && h == 0 && i > 0) {
+        if (NGRP == 2 && k == 0 && i > 0) {
           // two groups: group 1 reads O(i-1) (finish_tile) while group 0
           // already stages head 0 of tile i; O(i) overwrites it only after
           tc::mbar_wait(o_free, uint32_t((i - 1) & 1));
@@ -340,8 +343,8 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
         }
         if (tc::elect_one()) {
           mma_split(tmem_o, sb + S::OFF_A + b * A_BYTES, sb + S::OFF_BO + h * S::BO_BYTES, 32,
-                    h > 0);
-          if (h == H - 1) tc::commit(o_done);
+                    k > 0);
+          if (k == H - 1) tc::commit(o_done);
           tc::commit(&a_free[b]);
         }
         __syncwarp();

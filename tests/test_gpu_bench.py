@@ -37,3 +37,21 @@ def test_bench_json_contract():
     assert d["gpu_launches"] >= 100 * d["steps"]
     c = d["clocks"]
     assert "sm_mhz" in c and "reasons" in c
+
+
+@pytest.mark.parametrize("mode", [["--mode", "rows"], ["--shard-encoder"], ["--mode", "frames"]])
+def test_bench_other_partitions_single_gpu(mode):
+    """The N > 1 partitions' code paths at N = 1 (rows: the band render and
+    the band gather; --shard-encoder: encode_device + the NULL-encoder
+    forward; frames: the config-4 video): one valid JSON line each, with the
+    pipelined e2e (upload / read-back streams, two frames in flight)."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "2",
+                          "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "4"] + mode,
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] >= 100 * d["steps"]
