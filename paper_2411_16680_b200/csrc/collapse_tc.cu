@@ -16,6 +16,9 @@
 // weight image is made once per weight binding (collapse_tc_prepare) and
 // arrives by one bulk copy per CTA.
 #include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
 
 #include <algorithm>
 
@@ -255,13 +258,23 @@ constexpr int RNJ = C / 8;                       // K = 32
 constexpr int R_AHALF = RNJ * A_LBO;             // 8 KB
 constexpr int R_ABYTES = 2 * R_AHALF;            // 16 KB
 constexpr int R_WBYTES = RNJ * 2 * C * 16;       // 4 KB
-constexpr int R_OFF_W = R_ABYTES;
+constexpr int R_OUT_BYTES = TILE * C * 4;        // one 128B-swizzled output tile, 16 KB
+constexpr int R_OFF_OUT = 0;                     // two staging tiles (1 KB aligned)
+constexpr int R_OFF_A = 2 * R_OUT_BYTES;
+constexpr int R_OFF_W = R_OFF_A + R_ABYTES;
 constexpr int R_OFF_BAR = R_OFF_W + R_WBYTES;
 constexpr int R_SMEM = R_OFF_BAR + 2 * 8 + 16;
 
+__device__ __forceinline__ uint32_t swz128(int r, int c4) {  // 128B-swizzled [rows][128 B]
+  return uint32_t(r * 128 + ((c4 ^ (r & 7)) << 4));
+}
+
+// One 128-pixel tile per iteration: resize taps -> split A -> MMA -> the
+// rows through a 128B-swizzled staging tile (two, alternating) and one TMA
+// store (the per-thread 128-byte row stores were a third of the kernel).
 __global__ void __launch_bounds__(TILE, 4)
-    ray_project_tc_kernel(const float* __restrict__ base, int M, int hK, int wK, int Hk, int Wk,
-                          const uint8_t* __restrict__ wimg, float* __restrict__ out,
+    ray_project_tc_kernel(const __grid_constant__ CUtensorMap omap, const float* __restrict__ base,
+                          int M, int hK, int wK, int Hk, int Wk, const uint8_t* __restrict__ wimg,
                           int num_tiles, int* ovf_flag) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + R_OFF_BAR);
@@ -272,6 +285,7 @@ __global__ void __launch_bounds__(TILE, 4)
   tc::pdl_launch_dependents();
   if (blockIdx.x >= num_tiles) return;
   const uint32_t sb = tc::smem_u32(smem);
+  if (tid == 0 && (sb & 1023u)) __trap();  // swizzle atoms need 1 KB alignment
   if (tid == 0) {
     tc::mbar_init(w_full, 1);
     tc::mbar_init(m_done, 1);
@@ -295,37 +309,52 @@ __global__ void __launch_bounds__(TILE, 4)
   int it = 0;
   for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
     const int i = tile * TILE + tid;
-    float f[C];
-    if (i < n) {
+    // this thread's pixel: taps and fractions once; the loads cooperatively,
+    // 8 lanes per pixel with one 16-byte channel group each (a tap's
+    // 128-byte base row is one coalesced request)
+    int r00 = 0, r01 = 0, r10 = 0, r11 = 0;
+    float fy = 0.f, fx = 0.f;
+    const bool live = i < n;
+    if (live) {
       const int q = i / Wk, x = i - q * Wk;
       const int m = q / Hk, y = q - m * Hk;
-      const float4* b = reinterpret_cast<const float4*>(base + (int64_t)m * hK * wK * C);
       int y0, y1, x0, x1;
-      float fy, fx;
       resize_tap_s(y, sy, hK, y0, y1, fy);
       resize_tap_s(x, sx, wK, x0, x1, fx);
-#pragma unroll
-      for (int g = 0; g < C / 4; ++g) {
-        const float4 A = __ldg(b + (y0 * wK + x0) * 8 + g);
-        const float4 B = __ldg(b + (y0 * wK + x1) * 8 + g);
-        const float4 Cc = __ldg(b + (y1 * wK + x0) * 8 + g);
-        const float4 D = __ldg(b + (y1 * wK + x1) * 8 + g);
-        f[4 * g] = lerp2(A.x, B.x, Cc.x, D.x, fx, fy);
-        f[4 * g + 1] = lerp2(A.y, B.y, Cc.y, D.y, fx, fy);
-        f[4 * g + 2] = lerp2(A.z, B.z, Cc.z, D.z, fx, fy);
-        f[4 * g + 3] = lerp2(A.w, B.w, Cc.w, D.w, fx, fy);
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < C; ++c) f[c] = 0.f;
+      const int mb = m * hK * wK;
+      r00 = mb + y0 * wK + x0;
+      r01 = mb + y0 * wK + x1;
+      r10 = mb + y1 * wK + x0;
+      r11 = mb + y1 * wK + x1;
     }
-    ovf |= stage_row_k<RNJ>(smem, R_AHALF, tid, f);
+    const int lane = tid & 31, wbase = tid & ~31, g = lane & 7;
+    const float4* b4 = reinterpret_cast<const float4*>(base);
+#pragma unroll 4
+    for (int k = 0; k < 8; ++k) {
+      const int src = 4 * k + (lane >> 3);
+      const int s00 = __shfl_sync(0xffffffffu, r00, src), s01 = __shfl_sync(0xffffffffu, r01, src);
+      const int s10 = __shfl_sync(0xffffffffu, r10, src), s11 = __shfl_sync(0xffffffffu, r11, src);
+      const float sfy = __shfl_sync(0xffffffffu, fy, src), sfx = __shfl_sync(0xffffffffu, fx, src);
+      const float4 A = __ldg(b4 + s00 * 8 + g), B = __ldg(b4 + s01 * 8 + g);
+      const float4 Cc = __ldg(b4 + s10 * 8 + g), D = __ldg(b4 + s11 * 8 + g);
+      const float4 v = make_float4(lerp2(A.x, B.x, Cc.x, D.x, sfx, sfy), lerp2(A.y, B.y, Cc.y, D.y, sfx, sfy),
+                                   lerp2(A.z, B.z, Cc.z, D.z, sfx, sfy), lerp2(A.w, B.w, Cc.w, D.w, sfx, sfy));
+      __align__(8) __half2 h[2], l[2];
+      tc::split_f16x2(v.x, v.y, h[0], l[0]);
+      tc::split_f16x2(v.z, v.w, h[1], l[1]);
+      ovf |= tc::split_overflows(v.x) | tc::split_overflows(v.y) | tc::split_overflows(v.z) |
+             tc::split_overflows(v.w);
+      const int o = R_OFF_A + (g >> 1) * A_LBO + (wbase + src) * 16 + (g & 1) * 8;
+      *reinterpret_cast<uint2*>(smem + o) = *reinterpret_cast<uint2*>(h);
+      *reinterpret_cast<uint2*>(smem + R_AHALF + o) = *reinterpret_cast<uint2*>(l);
+    }
     tc::fence_proxy_async();
     tc::fence_before();
+    if (tid == 0) tc::bulk_wait_read<1>();  // staging tile (it & 1) read out by its store
     __syncthreads();
     tc::fence_after();
     if (tid == 0) {
-      mma_split_k<RNJ>(tmem, sb, R_AHALF, sb + R_OFF_W, C);
+      mma_split_k<RNJ>(tmem, sb + R_OFF_A, R_AHALF, sb + R_OFF_W, C);
       tc::commit(m_done);
     }
     tc::mbar_wait(m_done, uint32_t(it & 1));
@@ -333,19 +362,28 @@ __global__ void __launch_bounds__(TILE, 4)
     float y[C], lo[C];
     tc::tmem_ld32(lane_base + tmem, y);
     tc::tmem_ld32(lane_base + tmem + uint32_t(C), lo);
-    if (i < n) {
-      float4* o = reinterpret_cast<float4*>(out + (int64_t)i * C);
+    uint8_t* ot = smem + R_OFF_OUT + (it & 1) * R_OUT_BYTES;
 #pragma unroll
-      for (int c4 = 0; c4 < C / 4; ++c4)
-        o[c4] = make_float4(fmaf(lo[4 * c4], 1.0f / tc::kF16LoScale, y[4 * c4]),
-                            fmaf(lo[4 * c4 + 1], 1.0f / tc::kF16LoScale, y[4 * c4 + 1]),
-                            fmaf(lo[4 * c4 + 2], 1.0f / tc::kF16LoScale, y[4 * c4 + 2]),
-                            fmaf(lo[4 * c4 + 3], 1.0f / tc::kF16LoScale, y[4 * c4 + 3]));
-    }
+    for (int c4 = 0; c4 < C / 4; ++c4)
+      *reinterpret_cast<float4*>(ot + swz128(tid, c4)) =
+          make_float4(fmaf(lo[4 * c4], 1.0f / tc::kF16LoScale, y[4 * c4]),
+                      fmaf(lo[4 * c4 + 1], 1.0f / tc::kF16LoScale, y[4 * c4 + 1]),
+                      fmaf(lo[4 * c4 + 2], 1.0f / tc::kF16LoScale, y[4 * c4 + 2]),
+                      fmaf(lo[4 * c4 + 3], 1.0f / tc::kF16LoScale, y[4 * c4 + 3]));
+    tc::fence_proxy_async();  // generic staging writes before the TMA store reads them
     tc::fence_before();
-    __syncthreads();
+    __syncthreads();          // also: TMEM read and A consumed before the next tile's MMA
     tc::fence_after();
+    if (tid == 0) {
+      asm volatile(
+          "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+              reinterpret_cast<uint64_t>(&omap)),
+          "r"(sb + R_OFF_OUT + (it & 1) * R_OUT_BYTES), "r"(0), "r"(tile * TILE)
+          : "memory");
+      tc::bulk_commit();
+    }
   }
+  if (tid == 0) tc::bulk_wait<0>();
   if (ovf && ovf_flag) atomicOr(ovf_flag, 2);
   tc::fence_before();
   __syncthreads();
@@ -376,18 +414,41 @@ void ray_tc_prepare(const float* proj, void* dst, int* ovf, cudaStream_t st) {
            static_cast<uint8_t*>(dst), ovf);
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
 bool ray_project_tc(const float* base, int M, int hK, int wK, int Hk, int Wk, const float* wimg,
                     float* out, int* ovf, cudaStream_t st) {
   const int64_t n = (int64_t)M * Hk * Wk;
   if (!wimg || (reinterpret_cast<uintptr_t>(wimg) & 15) || (reinterpret_cast<uintptr_t>(out) & 15) ||
       (reinterpret_cast<uintptr_t>(base) & 15) || n >= (int64_t(1) << 31) ||
-      (int64_t)M * hK * wK * C >= (int64_t(1) << 31))
+      (int64_t)M * hK * wK * C >= (int64_t(1) << 31) || !encode_fn())
+    return false;
+  // out [n][32] fp32 as a 2-D map, 128-pixel boxes, 128B swizzle
+  CUtensorMap omap;
+  std::memset(&omap, 0, sizeof(omap));
+  cuuint64_t dims[2] = {cuuint64_t(C), cuuint64_t(n)};
+  cuuint64_t strides[1] = {cuuint64_t(C) * 4};
+  cuuint32_t box[2] = {cuuint32_t(C), cuuint32_t(TILE)};
+  cuuint32_t estr[2] = {1, 1};
+  if (encode_fn()(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, out, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return false;
   const int tiles = int((n + TILE - 1) / TILE);
   smem_optin(reinterpret_cast<const void*>(ray_project_tc_kernel), R_SMEM);
   const int grid = std::min(tiles, sm_count() * 4);
-  launch_pdl(false, ray_project_tc_kernel, grid, TILE, R_SMEM, st, base, M, hK, wK, Hk, Wk,
-             reinterpret_cast<const uint8_t*>(wimg), out, tiles, ovf);
+  launch_pdl(false, ray_project_tc_kernel, grid, TILE, R_SMEM, st, omap, base, M, hK, wK, Hk, Wk,
+             reinterpret_cast<const uint8_t*>(wimg), tiles, ovf);
   return true;
 }
 
