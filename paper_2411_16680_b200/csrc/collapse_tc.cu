@@ -40,14 +40,18 @@ constexpr int A_HALF = NJ * A_LBO;            // hi (or lo') planes: 16 KB
 constexpr int A_BYTES = 2 * A_HALF;           // 32 KB
 constexpr int W1_BYTES = NJ * 2 * N1 * 16;    // [W1h ; W1l'] per chunk: 16 KB
 constexpr int W2_BYTES = NJ * 2 * N2 * 16;    // 8 KB
+constexpr int ROW_TILE = TILE * C * 4;         // one 128B-swizzled [128][32] fp32 tile, 16 KB
 constexpr int OFF_A = 0;
 constexpr int OFF_W1 = OFF_A + A_BYTES;
 constexpr int OFF_W2 = OFF_W1 + W1_BYTES;
-constexpr int OFF_BAR = OFF_W2 + W2_BYTES;
+constexpr int OFF_IN = OFF_W2 + W2_BYTES;     // TMA path: the a and b row tiles (1 KB aligned)
+constexpr int OFF_OUT = OFF_IN + 2 * ROW_TILE;  // TMA path: the output staging tile
+constexpr int OFF_BAR = OFF_OUT + ROW_TILE;
 constexpr int SMEM_USED = OFF_BAR + 4 * 8 + 16;
+static_assert(OFF_IN % 1024 == 0 && OFF_OUT % 1024 == 0, "swizzled staging alignment");
 // requested dynamic shared memory: caps residency at two CTAs per SM, so the
 // 256-column TMEM allocations of co-resident CTAs always fit (512 columns)
-constexpr int SMEM_BYTES = 96 * 1024;
+constexpr int SMEM_BYTES = 110 * 1024;
 constexpr uint32_t TMEM_COLS = 256;           // D1: 128 columns, D2: 64 columns
 static_assert(SMEM_USED <= SMEM_BYTES, "shared memory layout");
 
@@ -99,8 +103,33 @@ __device__ __forceinline__ void load_row32(const float* p, float* v) {
   }
 }
 
+__device__ __forceinline__ uint32_t swz128(int r, int c4) {  // 128B-swizzled [rows][128 B]
+  return uint32_t(r * 128 + ((c4 ^ (r & 7)) << 4));
+}
+__device__ __forceinline__ void tma_load_rows(uint32_t dst, const CUtensorMap* map, int row,
+                                              uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(row), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_rows(const CUtensorMap* map, uint32_t src, int row) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(0), "r"(row)
+               : "memory");
+}
+
+// kTma (PL a multiple of 128: a tile's texels are 128 consecutive rows of
+// one layer pair): the a and b rows of the next tile arrive by two TMA boxes
+// while this tile computes, and the output leaves through a 128B-swizzled
+// staging tile and one TMA store; otherwise per-thread row loads / stores.
+template <bool kTma>
 __global__ void __launch_bounds__(TILE, 2)
-    collapse_tc_kernel(const float* __restrict__ V, int L2, int PL, const uint8_t* __restrict__ wimg,
+    collapse_tc_kernel(const __grid_constant__ CUtensorMap vmap,
+                       const __grid_constant__ CUtensorMap omap, const float* __restrict__ V,
+                       int L2, int PL, const uint8_t* __restrict__ wimg,
                        const float* __restrict__ b1, const float* __restrict__ b2,
                        float* __restrict__ out, int num_tiles, int* ovf_flag) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -108,6 +137,7 @@ __global__ void __launch_bounds__(TILE, 2)
   uint64_t* w_full = bars;       // weight image landed
   uint64_t* m1_done = bars + 1;  // h pre-activations in TMEM
   uint64_t* m2_done = bars + 2;  // outputs in TMEM
+  uint64_t* in_full = bars + 3;  // kTma: the tile's a / b rows landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4);
   const int tid = threadIdx.x, warp = tid >> 5;
   tc::pdl_launch_dependents();
@@ -117,6 +147,7 @@ __global__ void __launch_bounds__(TILE, 2)
     tc::mbar_init(w_full, 1);
     tc::mbar_init(m1_done, 1);
     tc::mbar_init(m2_done, 1);
+    tc::mbar_init(in_full, 1);
     tc::mbar_init_fence();
   }
   if (warp == 0) tc::tmem_alloc(tmem_slot, TMEM_COLS);
@@ -134,6 +165,15 @@ __global__ void __launch_bounds__(TILE, 2)
   float bias2[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) bias2[c] = __ldg(b2 + c);
+  // kTma: rows of layer 2l (a) and 2l + 1 (b) for output tile t
+  auto load_in = [&](int t) {
+    const int row0 = t * TILE;  // output texel row; PL % TILE == 0
+    const int l = row0 / PL, q0 = row0 - l * PL;
+    tc::mbar_expect_tx(in_full, 2 * ROW_TILE);
+    tma_load_rows(sb + OFF_IN, &vmap, (2 * l) * PL + q0, in_full);
+    tma_load_rows(sb + OFF_IN + ROW_TILE, &vmap, (2 * l + 1) * PL + q0, in_full);
+  };
+  if (kTma && tid == 0) load_in(blockIdx.x);
   tc::mbar_wait(w_full, 0);
   bool ovf = false;
   const int64_t total = (int64_t)L2 * PL;
@@ -142,7 +182,16 @@ __global__ void __launch_bounds__(TILE, 2)
     const int64_t p = (int64_t)tile * TILE + tid;  // output texel (l, q) = (p / PL, p % PL)
     const bool valid = p < total;
     float a[C], b[C];
-    if (valid) {
+    if (kTma) {
+      tc::mbar_wait(in_full, uint32_t(it & 1));
+#pragma unroll
+      for (int c4 = 0; c4 < C / 4; ++c4) {
+        const float4 ta = *reinterpret_cast<const float4*>(smem + OFF_IN + swz128(tid, c4));
+        const float4 tb = *reinterpret_cast<const float4*>(smem + OFF_IN + ROW_TILE + swz128(tid, c4));
+        a[4 * c4] = ta.x, a[4 * c4 + 1] = ta.y, a[4 * c4 + 2] = ta.z, a[4 * c4 + 3] = ta.w;
+        b[4 * c4] = tb.x, b[4 * c4 + 1] = tb.y, b[4 * c4 + 2] = tb.z, b[4 * c4 + 3] = tb.w;
+      }
+    } else if (valid) {
       const int64_t l = p / PL, q = p - l * PL;
       load_row32(V + ((2 * l) * PL + q) * C, a);
       load_row32(V + ((2 * l + 1) * PL + q) * C, b);
@@ -156,11 +205,12 @@ __global__ void __launch_bounds__(TILE, 2)
       for (int c = 0; c < C; ++c) x[c] = a[c], x[C + c] = b[c];
       ovf |= stage_row64(smem + OFF_A, tid, x);
     }
-    tc::fence_proxy_async();
+    tc::fence_proxy_async();  // also orders the row-tile reads before their TMA refill
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     if (tid == 0) {
+      if (kTma && tile + int(gridDim.x) < num_tiles) load_in(tile + gridDim.x);
       mma_split64(d1, sb + OFF_A, sb + OFF_W1, N1);
       tc::commit(m1_done);
     }
@@ -184,6 +234,7 @@ __global__ void __launch_bounds__(TILE, 2)
     ovf |= stage_row64(smem + OFF_A, tid, h);
     tc::fence_proxy_async();
     tc::fence_before();
+    if (kTma && tid == 0) tc::bulk_wait_read<0>();  // the previous tile's store left the staging tile
     __syncthreads();
     tc::fence_after();
     if (tid == 0) {
@@ -195,7 +246,7 @@ __global__ void __launch_bounds__(TILE, 2)
     float y[C], lo[C];
     tc::tmem_ld32(lane_base + d2, y);
     tc::tmem_ld32(lane_base + d2 + uint32_t(N2), lo);
-    if (valid) {
+    if (kTma || valid) {
       float4* o = reinterpret_cast<float4*>(out + p * C);
 #pragma unroll
       for (int c4 = 0; c4 < C / 4; ++c4) {
@@ -206,14 +257,23 @@ __global__ void __launch_bounds__(TILE, 2)
           const float r = fmaf(lo[c], 1.0f / tc::kF16LoScale, y[c]);
           v[k] = fa(fm(fa(a[c], b[c]), 0.5f), fa(r, bias2[c]));
         }
-        o[c4] = make_float4(v[0], v[1], v[2], v[3]);
+        if (kTma)
+          *reinterpret_cast<float4*>(smem + OFF_OUT + swz128(tid, c4)) = make_float4(v[0], v[1], v[2], v[3]);
+        else
+          o[c4] = make_float4(v[0], v[1], v[2], v[3]);
       }
     }
+    if (kTma) tc::fence_proxy_async();  // staging writes before the TMA store reads them
     // every thread has read D1 / D2 and MMA2 has read A before the next tile
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
+    if (kTma && tid == 0) {
+      tma_store_rows(&omap, sb + OFF_OUT, tile * TILE);
+      tc::bulk_commit();
+    }
   }
+  if (kTma && tid == 0) tc::bulk_wait<0>();
   if (ovf && ovf_flag) atomicOr(ovf_flag, 2);
   tc::fence_before();
   __syncthreads();
@@ -265,9 +325,6 @@ constexpr int R_OFF_W = R_OFF_A + R_ABYTES;
 constexpr int R_OFF_BAR = R_OFF_W + R_WBYTES;
 constexpr int R_SMEM = R_OFF_BAR + 2 * 8 + 16;
 
-__device__ __forceinline__ uint32_t swz128(int r, int c4) {  // 128B-swizzled [rows][128 B]
-  return uint32_t(r * 128 + ((c4 ^ (r & 7)) << 4));
-}
 
 // One 128-pixel tile per iteration: resize taps -> split A -> MMA -> the
 // rows through a 128B-swizzled staging tile (two, alternating) and one TMA
@@ -468,10 +525,33 @@ bool layer_collapse_tc(const float* V, int L, int64_t PL, int C_, const float* w
   const int64_t total = (int64_t)(L / 2) * PL;
   const int64_t tiles = (total + TILE - 1) / TILE;
   if (tiles >= (int64_t(1) << 31) || PL >= (int64_t(1) << 31)) return false;
-  smem_optin(reinterpret_cast<const void*>(collapse_tc_kernel), SMEM_BYTES);
   const int grid = int(std::min<int64_t>(tiles, int64_t(sm_count()) * 2));
-  launch_pdl(true, collapse_tc_kernel, grid, TILE, SMEM_BYTES, st, V, L / 2, int(PL),
-             reinterpret_cast<const uint8_t*>(wimg), b1, b2, out, int(tiles), ovf);
+  // the TMA path: every tile inside one layer pair, rows addressable by
+  // 32-bit box coordinates
+  CUtensorMap vmap, omap;
+  std::memset(&vmap, 0, sizeof(vmap));
+  std::memset(&omap, 0, sizeof(omap));
+  bool tma = PL % TILE == 0 && (int64_t)L * PL < (int64_t(1) << 31) && encode_fn() != nullptr;
+  auto rows_map = [&](CUtensorMap* m, const float* ptr, int64_t rows) {
+    cuuint64_t dims[2] = {cuuint64_t(C), cuuint64_t(rows)};
+    cuuint64_t strides[1] = {cuuint64_t(C) * 4};
+    cuuint32_t box[2] = {cuuint32_t(C), cuuint32_t(TILE)};
+    cuuint32_t estr[2] = {1, 1};
+    return encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides,
+                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  if (tma) tma = rows_map(&vmap, V, (int64_t)L * PL) && rows_map(&omap, out, total);
+  if (tma) {
+    smem_optin(reinterpret_cast<const void*>(collapse_tc_kernel<true>), SMEM_BYTES);
+    launch_pdl(true, collapse_tc_kernel<true>, grid, TILE, SMEM_BYTES, st, vmap, omap, V, L / 2,
+               int(PL), reinterpret_cast<const uint8_t*>(wimg), b1, b2, out, int(tiles), ovf);
+  } else {
+    smem_optin(reinterpret_cast<const void*>(collapse_tc_kernel<false>), SMEM_BYTES);
+    launch_pdl(true, collapse_tc_kernel<false>, grid, TILE, SMEM_BYTES, st, vmap, omap, V, L / 2,
+               int(PL), reinterpret_cast<const uint8_t*>(wimg), b1, b2, out, int(tiles), ovf);
+  }
   return true;
 }
 
