@@ -234,9 +234,10 @@ __global__ void __launch_bounds__(256) resize_hwc4c_kernel(const float* __restri
 template <int G>
 __global__ void __launch_bounds__(256) resize_hwc4g_kernel(const float* __restrict__ in,
                                                            float* __restrict__ out, int H, int W,
-                                                           int Ho, int Wo) {
+                                                           int Ho, int Wo, double sy, double sx) {
   pdl_grid_sync();
-  const double sy = dd(double(H), double(Ho)), sx = dd(double(W), double(Wo));
+  // sy, sx = dd(H, Ho), dd(W, Wo), divided once on the host (IEEE binary64,
+  // the same value as the device's __ddiv_rn)
   const int row = blockIdx.y;  // b * Ho + y
   const int b = row / Ho, y = row - b * Ho;
   int y0, y1;
@@ -965,11 +966,14 @@ void resize_hwc(const float* in, float* out, int B, int H, int W, int C, int Ho,
     const int G = C / 4;
     if ((G == 8 || G == 9) && (int64_t)B * H * W * G < (int64_t(1) << 31) &&
         px * G < (int64_t(1) << 31) && (int64_t)B * Ho < 65536) {
-      const dim3 grid(unsigned(std::min<int64_t>((int64_t(Wo) * G + 255) / 256, 8)), unsigned(B * Ho));
+      // a few blocks per row, each thread several (x, g) elements: the per-
+      // thread row setup is amortised
+      const dim3 grid(unsigned(std::min<int64_t>((int64_t(Wo) * G + 1023) / 1024, 8)), unsigned(B * Ho));
+      const double sy = double(H) / double(Ho), sx = double(W) / double(Wo);
       if (G == 8)
-        launch_k(resize_hwc4g_kernel<8>, grid, 256, 0, st, in, out, H, W, Ho, Wo);
+        launch_k(resize_hwc4g_kernel<8>, grid, 256, 0, st, in, out, H, W, Ho, Wo, sy, sx);
       else
-        launch_k(resize_hwc4g_kernel<9>, grid, 256, 0, st, in, out, H, W, Ho, Wo);
+        launch_k(resize_hwc4g_kernel<9>, grid, 256, 0, st, in, out, H, W, Ho, Wo, sy, sx);
     } else if (G >= 4 && G <= 64 && (int64_t)B * H * W * G < (int64_t(1) << 31) &&
                px * G < (int64_t(1) << 31)) {
       const int64_t blocks = (px * G + 255) / 256;
