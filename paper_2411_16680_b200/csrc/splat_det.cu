@@ -38,7 +38,8 @@ __global__ void __launch_bounds__(256) splat_count_kernel(const float* __restric
                                                           const DevCam* __restrict__ cams, int M,
                                                           int Hv, int Wv, int* __restrict__ cnt,
                                                           int2* __restrict__ fp_i,
-                                                          float4* __restrict__ fp_w) {
+                                                          float4* __restrict__ fp_w,
+                                                          int4* __restrict__ rank) {
   pdl_grid_sync();
   const int64_t P = (int64_t)L * PL;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // pair (p, m), m fastest
@@ -59,10 +60,14 @@ __global__ void __launch_bounds__(256) splat_count_kernel(const float* __restric
   fp_i[i] = make_int2(d0, dx | (dy << 1));
   fp_w[i] = make_float4(__double2float_rn(wd[0]), __double2float_rn(wd[1]),
                         __double2float_rn(wd[2]), __double2float_rn(wd[3]));
-  atomicAdd(cnt + d0, 1);
-  atomicAdd(cnt + d0 + dx, 1);
-  atomicAdd(cnt + d0 + dy, 1);
-  atomicAdd(cnt + d0 + dy + dx, 1);
+  // each tap's position in its bin's run (the count before it): the fill
+  // then writes entry slots without a second round of atomics
+  int4 r;
+  r.x = atomicAdd(cnt + d0, 1);
+  r.y = atomicAdd(cnt + d0 + dx, 1);
+  r.z = atomicAdd(cnt + d0 + dy, 1);
+  r.w = atomicAdd(cnt + d0 + dy + dx, 1);
+  rank[i] = r;
 }
 
 // exclusive scan, pass 1: per-block scan of kScanBlock counts (in place into
@@ -125,28 +130,24 @@ __global__ void __launch_bounds__(1024) scan_sums_kernel(int* __restrict__ block
   }
 }
 
-// pass 3: add each block's base; the result doubles as the fill cursor
+// pass 3: add each block's base
 __global__ void __launch_bounds__(256) scan_add_kernel(int* __restrict__ off, int n,
-                                                       const int* __restrict__ block_sum,
-                                                       int* __restrict__ cursor) {
+                                                       const int* __restrict__ block_sum) {
   pdl_grid_sync();
   const int base = blockIdx.x * kScanBlock;
   const int add = block_sum[blockIdx.x];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int i = base + threadIdx.x + 256 * k;
-    if (i < n) {
-      const int o = off[i] + add;
-      off[i] = o;
-      cursor[i] = o;
-    }
+    if (i < n) off[i] += add;
   }
 }
 
 __global__ void __launch_bounds__(256) splat_fill_kernel(int64_t pairs, int64_t bins, int M,
                                                          const int2* __restrict__ fp_i,
                                                          const float4* __restrict__ fp_w,
-                                                         int* __restrict__ cursor,
+                                                         const int4* __restrict__ rank,
+                                                         const int* __restrict__ off,
                                                          int2* __restrict__ ent) {
   pdl_grid_sync();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -154,14 +155,16 @@ __global__ void __launch_bounds__(256) splat_fill_kernel(int64_t pairs, int64_t 
   const int2 f = fp_i[i];
   if (f.x < 0) return;
   const float4 w = fp_w[i];
+  const int4 r = rank[i];
   const int p4 = int(i / M) * 4;
   const int dx = f.y & 1, dy = f.y >> 1;
   const int d[4] = {f.x, f.x + dx, f.x + dy, f.x + dy + dx};
+  const int rk[4] = {r.x, r.y, r.z, r.w};
   const float wk[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     LVSG_CHECK(d[k] >= 0 && d[k] < bins);
-    const int slot = atomicAdd(cursor + d[k], 1);
+    const int slot = __ldg(off + d[k]) + rk[k];
     LVSG_CHECK(slot >= 0 && slot < 4 * pairs);
     ent[slot] = make_int2(p4 + k, __float_as_int(wk[k]));
   }
@@ -392,9 +395,9 @@ inline int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
 
 size_t splat_det_scratch_ints(int64_t pairs, int64_t bins) {
   const int64_t nb = (bins + kScanBlock - 1) / kScanBlock;
-  // cnt, off, cursor [bins]; block sums; entries (int2) [4 pairs]; fp_i
-  // (int2) and fp_w (float4) [pairs]
-  return size_t(3 * bins + nb + 8 * pairs + 2 * pairs + 4 * pairs + 16);
+  // cnt, off [bins]; block sums; entries (int2) [4 pairs]; fp_i (int2),
+  // fp_w (float4) and tap ranks (int4) [pairs]
+  return size_t(2 * bins + nb + 8 * pairs + 2 * pairs + 4 * pairs + 4 * pairs + 16);
 }
 
 void splat_det(const float* payload, const float* points, int L, int PL, int K,
@@ -405,22 +408,22 @@ void splat_det(const float* payload, const float* points, int L, int PL, int K,
   const int nb = int((bins + kScanBlock - 1) / kScanBlock);
   int* cnt = scratch;
   int* off = cnt + bins;
-  int* cursor = off + bins;
-  int* bsum = cursor + bins;
-  // 16-byte alignment for the int2 / float4 records
+  int* bsum = off + bins;
+  // 16-byte alignment for the int2 / float4 / int4 records
   uintptr_t a = reinterpret_cast<uintptr_t>(bsum + nb);
   a = (a + 15) & ~uintptr_t(15);
   float4* fp_w = reinterpret_cast<float4*>(a);
-  int2* ent = reinterpret_cast<int2*>(fp_w + pairs);
+  int4* rank = reinterpret_cast<int4*>(fp_w + pairs);
+  int2* ent = reinterpret_cast<int2*>(rank + pairs);
   int2* fp_i = ent + 4 * pairs;
   cudaMemsetAsync(cnt, 0, size_t(bins) * sizeof(int), st);  // errors surface at the caller's check
   launch_k(splat_count_kernel, blocks_for(pairs, 256), 256, 0, st, points, L, PL, cams_dev, M, Hv,
-           Wv, cnt, fp_i, fp_w);
+           Wv, cnt, fp_i, fp_w, rank);
   launch_k(scan_blocks_kernel, nb, 256, 0, st, (const int*)cnt, int(bins), off, bsum);
   launch_k(scan_sums_kernel, 1, 1024, 0, st, bsum, nb);
-  launch_k(scan_add_kernel, nb, 256, 0, st, off, int(bins), (const int*)bsum, cursor);
+  launch_k(scan_add_kernel, nb, 256, 0, st, off, int(bins), (const int*)bsum);
   launch_k(splat_fill_kernel, blocks_for(pairs, 256), 256, 0, st, pairs, bins, M, (const int2*)fp_i,
-           (const float4*)fp_w, cursor, ent);
+           (const float4*)fp_w, (const int4*)rank, (const int*)off, ent);
   const int G = pay_stride(K) / 4;
   if (G == 9 && L <= 192) {  // C = 32 configs: one thread per (view pixel, layer)
     const int ppb = std::max(1, 192 / L);
