@@ -9,11 +9,13 @@
 // pixels):
 //   1. splat_count: one thread per (texel, view) pair computes the f64
 //      footprint once (the gather's rule), stores it (dest of tap 0, tap
-//      offsets, f32 weights) and counts each valid tap into its bin;
+//      offsets, f32 weights) and counts each valid tap into its bin, keeping
+//      the count before it (the tap's rank in the bin);
 //   2. a three-pass exclusive scan of the bin counts gives each bin its run
 //      in the entry array;
-//   3. splat_fill: each valid tap appends (key p*4+k, f32 weight) to its
-//      bin's run (slot order inside a run is arbitrary);
+//   3. splat_fill: each valid tap writes (key p*4+k, f32 weight) to slot
+//      off[bin] + rank of its bin's run (slot order inside a run is
+//      arbitrary);
 //   4. splat_reduce_composite: one thread per (view pixel, 4-channel group)
 //      sorts, layer by layer, its bin's run by key (= the reference's (s, k)
 //      order; short runs in registers), accumulates the payload rows,
