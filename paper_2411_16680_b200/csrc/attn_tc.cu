@@ -485,17 +485,21 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
             for (int c = 0; c < C; ++c) d1[c] = 0.f;
 #pragma unroll
           for (int h = 0; h < HG; ++h) {
-            float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
+            // 4 interleaved partial sums per dot as two packed f32x2 pairs
+            // (FFMA2: the same per-lane roundings and order)
+            float2 a0[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+            float2 a1[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
             for (int c = 0; c < C; c += 4) {
 #pragma unroll
-              for (int r = 0; r < 4; ++r) {
-                a0[r] = fmaf(sv[h][c + r], d0[c + r], a0[r]);
-                a1[r] = fmaf(sv[h][c + r], d1[c + r], a1[r]);
+              for (int r = 0; r < 2; ++r) {
+                const float2 s2 = make_float2(sv[h][c + 2 * r], sv[h][c + 2 * r + 1]);
+                a0[r] = __ffma2_rn(s2, make_float2(d0[c + 2 * r], d0[c + 2 * r + 1]), a0[r]);
+                a1[r] = __ffma2_rn(s2, make_float2(d1[c + 2 * r], d1[c + 2 * r + 1]), a1[r]);
               }
             }
-            w[h][m] = fm(fa(fa(a0[0], a0[1]), fa(a0[2], a0[3])), inv_temp);
-            w[h][m + 1] = fm(fa(fa(a1[0], a1[1]), fa(a1[2], a1[3])), inv_temp);
+            w[h][m] = fm(fa(fa(a0[0].x, a0[0].y), fa(a0[1].x, a0[1].y)), inv_temp);
+            w[h][m + 1] = fm(fa(fa(a1[0].x, a1[0].y), fa(a1[1].x, a1[1].y)), inv_temp);
           }
         }
         // softmax over views (tape.hpp:390-404: max, exp(x - max), sum, * 1/sum)
@@ -535,10 +539,15 @@ __global__ void __launch_bounds__(nthreads<H>(), 1)
 #pragma unroll
           for (int c = 0; c < C; ++c) d1[c] = 0.f;
 #pragma unroll
-        for (int h = 0; h < HG; ++h)
+        for (int h = 0; h < HG; ++h) {
+          const float2 wa = make_float2(w[h][m], w[h][m]), wb = make_float2(w[h][m + 1], w[h][m + 1]);
 #pragma unroll
-          for (int c = 0; c < C; ++c)
-            hd[h][c] = fmaf(w[h][m + 1], d1[c], fmaf(w[h][m], d0[c], hd[h][c]));
+          for (int c = 0; c < C; c += 2) {
+            float2 t = __ffma2_rn(wa, make_float2(d0[c], d0[c + 1]), make_float2(hd[h][c], hd[h][c + 1]));
+            t = __ffma2_rn(wb, make_float2(d1[c], d1[c + 1]), t);
+            hd[h][c] = t.x, hd[h][c + 1] = t.y;
+          }
+        }
       }
 #pragma unroll
       for (int h = 0; h < HG; ++h) stage(hd[h]);

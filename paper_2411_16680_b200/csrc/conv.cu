@@ -243,6 +243,9 @@ __global__ void __launch_bounds__(128) conv3x3_stem_kernel(const ConvArgs a,
 // constant-bank weight feeds two FMAs and the two pixels share 8 of their
 // 12 tap columns. Requires an even W (pairs never straddle a row or an
 // image); same per-pixel arithmetic and order as the one-pixel kernel.
+#ifndef LVSG_STEM_FFMA2
+#define LVSG_STEM_FFMA2 1
+#endif
 __global__ void __launch_bounds__(128) conv3x3_stem3x2_kernel(const ConvArgs a,
                                                               const __grid_constant__ StemParam pw) {
   pdl_grid_sync();
@@ -277,6 +280,34 @@ __global__ void __launch_bounds__(128) conv3x3_stem3x2_kernel(const ConvArgs a,
         for (int ci = 0; ci < 3; ++ci) xin[dy][cx][ci] = ok ? __ldg(p + ci) : 0.f;
       }
     float acc0[32], acc1[32];
+#if LVSG_STEM_FFMA2
+    // packed f32x2 FMAs over channel pairs (sm_100 FFMA2: two IEEE fmas per
+    // instruction, the same roundings): half the FMA instructions
+    float2 a0[16], a1[16];
+#pragma unroll
+    for (int c2 = 0; c2 < 16; ++c2) a0[c2] = a1[c2] = make_float2(pw.b[2 * c2], pw.b[2 * c2 + 1]);
+#pragma unroll
+    for (int ci = 0; ci < 3; ++ci)
+#pragma unroll
+      for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+          const int k = ci * 9 + dy * 3 + dx;
+          const float2 x0 = make_float2(xin[dy][dx][ci], xin[dy][dx][ci]);
+          const float2 x1 = make_float2(xin[dy][dx + 1][ci], xin[dy][dx + 1][ci]);
+#pragma unroll
+          for (int c2 = 0; c2 < 16; ++c2) {
+            const float2 w = make_float2(pw.w[k * 32 + 2 * c2], pw.w[k * 32 + 2 * c2 + 1]);
+            a0[c2] = __ffma2_rn(x0, w, a0[c2]);
+            a1[c2] = __ffma2_rn(x1, w, a1[c2]);
+          }
+        }
+#pragma unroll
+    for (int c2 = 0; c2 < 16; ++c2) {
+      acc0[2 * c2] = a0[c2].x, acc0[2 * c2 + 1] = a0[c2].y;
+      acc1[2 * c2] = a1[c2].x, acc1[2 * c2 + 1] = a1[c2].y;
+    }
+#else
 #pragma unroll
     for (int c = 0; c < 32; ++c) acc0[c] = acc1[c] = pw.b[c];
 #pragma unroll
@@ -293,6 +324,7 @@ __global__ void __launch_bounds__(128) conv3x3_stem3x2_kernel(const ConvArgs a,
             acc1[c] = fmaf(x1, pw.w[k * 32 + c], acc1[c]);
           }
         }
+#endif
 #pragma unroll
     for (int c4 = 0; c4 < 8; ++c4) {
       const int p0 = 2 * t, p1 = 2 * t + 1;

@@ -114,22 +114,25 @@ __global__ void __launch_bounds__(128) blend_logits32_kernel(const float* __rest
   const float r = __fdiv_rn(1.0f, __fsqrt_rn(fa(__fdiv_rn(ms, float(C)), 1e-6f)));
 #pragma unroll
   for (int k = 0; k < C; ++k) n[k] = fm(fm(n[k], r), __ldg(gain + k));
+  // q = n W_blend as packed f32x2 FMAs over output-channel pairs (FFMA2,
+  // the same per-lane roundings)
+  float2 q2[C / 2];
 #pragma unroll
-  for (int c = 0; c < C; ++c) q[c] = 0.f;
+  for (int c = 0; c < C / 2; ++c) q2[c] = make_float2(0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < C; ++k) {
-    const float nk = n[k];
+    const float2 nk = make_float2(n[k], n[k]);
 #pragma unroll
     for (int c4 = 0; c4 < C / 4; ++c4) {
       const float4 w = PW ? make_float4(pw.w[k * C + 4 * c4], pw.w[k * C + 4 * c4 + 1],
                                         pw.w[k * C + 4 * c4 + 2], pw.w[k * C + 4 * c4 + 3])
                           : reinterpret_cast<const float4*>(s_bw + k * C)[c4];
-      q[4 * c4] = fmaf(nk, w.x, q[4 * c4]);
-      q[4 * c4 + 1] = fmaf(nk, w.y, q[4 * c4 + 1]);
-      q[4 * c4 + 2] = fmaf(nk, w.z, q[4 * c4 + 2]);
-      q[4 * c4 + 3] = fmaf(nk, w.w, q[4 * c4 + 3]);
+      q2[2 * c4] = __ffma2_rn(nk, make_float2(w.x, w.y), q2[2 * c4]);
+      q2[2 * c4 + 1] = __ffma2_rn(nk, make_float2(w.z, w.w), q2[2 * c4 + 1]);
     }
   }
+#pragma unroll
+  for (int c = 0; c < C / 2; ++c) q[2 * c] = q2[c].x, q[2 * c + 1] = q2[c].y;
   const float inv_temp = __double2float_rn(1.0 / sqrt(double(C)));
   float out[M];
 #pragma unroll
@@ -179,22 +182,25 @@ __global__ void __launch_bounds__(128) decode_payload32_kernel(
   if (p >= P) return;
   float v[C], acc[KW];
   load_row(V + p * C, v);
+  // packed f32x2 FMAs over output-channel pairs (sm_100 FFMA2: the same
+  // per-lane roundings as fmaf), the input channel broadcast
+  float2 acc2[KW / 2];
 #pragma unroll
-  for (int c = 0; c < KW; ++c) acc[c] = 0.f;
+  for (int c = 0; c < KW / 2; ++c) acc2[c] = make_float2(0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < C; ++k) {
-    const float vk = v[k];
+    const float2 vk = make_float2(v[k], v[k]);
 #pragma unroll
     for (int c4 = 0; c4 < KW / 4; ++c4) {
       const float4 w = PW ? make_float4(pw.w[k * KW + 4 * c4], pw.w[k * KW + 4 * c4 + 1],
                                         pw.w[k * KW + 4 * c4 + 2], pw.w[k * KW + 4 * c4 + 3])
                           : reinterpret_cast<const float4*>(s_w + k * KW)[c4];
-      acc[4 * c4] = fmaf(vk, w.x, acc[4 * c4]);
-      acc[4 * c4 + 1] = fmaf(vk, w.y, acc[4 * c4 + 1]);
-      acc[4 * c4 + 2] = fmaf(vk, w.z, acc[4 * c4 + 2]);
-      acc[4 * c4 + 3] = fmaf(vk, w.w, acc[4 * c4 + 3]);
+      acc2[2 * c4] = __ffma2_rn(vk, make_float2(w.x, w.y), acc2[2 * c4]);
+      acc2[2 * c4 + 1] = __ffma2_rn(vk, make_float2(w.z, w.w), acc2[2 * c4 + 1]);
     }
   }
+#pragma unroll
+  for (int c = 0; c < KW / 2; ++c) acc[2 * c] = acc2[c].x, acc[2 * c + 1] = acc2[c].y;
   // payload row padded to 40 floats (32-byte rows): [a(32), sigma, 0 x 7]
   float4* pay = reinterpret_cast<float4*>(payload + (int64_t)p * (C + 8));
 #pragma unroll
