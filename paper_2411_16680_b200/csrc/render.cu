@@ -17,6 +17,9 @@ namespace lvsg {
 namespace {
 
 constexpr int kMaxViews = 32;
+#ifndef LVSG_RENDER_X2
+#define LVSG_RENDER_X2 1
+#endif
 
 struct Taps {
   int y0, y1, x0, x1;
@@ -142,7 +145,6 @@ __device__ __forceinline__ unsigned blend_views(const RenderArgs& a, const FastC
                f.y0 <= f.y1);
     const float fx = __double2float_rn(f.fx), fy = __double2float_rn(f.fy);
     const float gx = 1.0f - fx, gy = 1.0f - fy;
-    const float w[4] = {gx * gy, fx * gy, gx * fy, fx * fy};
     const int r0 = f.y0 * a.Wr, r1 = f.y1 * a.Wr;  // one view < 2^31 floats
     const float bm = f.valid ? beta[m] : 0.f;
     const float* img = a.images + (int64_t)m * a.Hr * a.Wr * 3;
@@ -150,11 +152,31 @@ __device__ __forceinline__ unsigned blend_views(const RenderArgs& a, const FastC
     const float* p10 = img + (r0 + f.x1) * 3;
     const float* p01 = img + (r1 + f.x0) * 3;
     const float* p11 = img + (r1 + f.x1) * 3;
+#if LVSG_RENDER_X2
+    // red and green as packed f32x2 ops (sm_100 FMUL2 / FFMA2: the same
+    // per-lane roundings as the scalar chain blue keeps; frames
+    // bit-identical). The resize lerps stay scalar: ptxas contracts a packed
+    // mul.rn.f32x2 feeding an add.rn.f32x2 into one FFMA2, which would change
+    // their (uncontracted, tape.hpp:890-894) rounding
+    const float2 wa = __fmul2_rn(make_float2(gx, fx), make_float2(gy, gy));  // w00, w10
+    const float2 wb = __fmul2_rn(make_float2(gx, fx), make_float2(fy, fy));  // w01, w11
+    float2 t = __fmul2_rn(make_float2(wa.x, wa.x), make_float2(__ldg(p00), __ldg(p00 + 1)));
+    t = __ffma2_rn(make_float2(wa.y, wa.y), make_float2(__ldg(p10), __ldg(p10 + 1)), t);
+    t = __ffma2_rn(make_float2(wb.x, wb.x), make_float2(__ldg(p01), __ldg(p01 + 1)), t);
+    t = __ffma2_rn(make_float2(wb.y, wb.y), make_float2(__ldg(p11), __ldg(p11 + 1)), t);
+    const float2 rg = __ffma2_rn(make_float2(bm, bm), t, make_float2(acc[0], acc[1]));
+    acc[0] = rg.x, acc[1] = rg.y;
+    acc[2] = fmaf(bm, fmaf(wb.y, __ldg(p11 + 2),
+                           fmaf(wb.x, __ldg(p01 + 2), fmaf(wa.y, __ldg(p10 + 2), wa.x * __ldg(p00 + 2)))),
+                  acc[2]);
+#else
+    const float w[4] = {gx * gy, fx * gy, gx * fy, fx * fy};
 #pragma unroll
     for (int k = 0; k < 3; ++k)
       acc[k] = fmaf(bm, fmaf(w[3], __ldg(p11 + k),
                              fmaf(w[2], __ldg(p01 + k), fmaf(w[1], __ldg(p10 + k), w[0] * __ldg(p00 + k)))),
                     acc[k]);
+#endif
     wsum = fa(wsum, bm);
   }
   return need;
