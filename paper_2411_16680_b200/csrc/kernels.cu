@@ -595,10 +595,18 @@ __global__ void __launch_bounds__(256, 6) gather_stack32_kernel(
       poff = ro;
       pfl = rf;
       const float4 a = l0, b = r0, c = l1, d = r1;
-      v.x = fmaf(rw[3], d.x, fmaf(rw[2], c.x, fmaf(rw[1], b.x, rw[0] * a.x)));
-      v.y = fmaf(rw[3], d.y, fmaf(rw[2], c.y, fmaf(rw[1], b.y, rw[0] * a.y)));
-      v.z = fmaf(rw[3], d.z, fmaf(rw[2], c.z, fmaf(rw[1], b.z, rw[0] * a.z)));
-      v.w = fmaf(rw[3], d.w, fmaf(rw[2], c.w, fmaf(rw[1], b.w, rw[0] * a.w)));
+      // the 4-tap chain on channel pairs (packed f32x2 ops: the same per-lane
+      // roundings as fmaf / the product)
+      const float2 w0 = make_float2(rw[0], rw[0]), w1 = make_float2(rw[1], rw[1]);
+      const float2 w2 = make_float2(rw[2], rw[2]), w3 = make_float2(rw[3], rw[3]);
+      float2 xy = __fmul2_rn(w0, make_float2(a.x, a.y)), zw = __fmul2_rn(w0, make_float2(a.z, a.w));
+      xy = __ffma2_rn(w1, make_float2(b.x, b.y), xy);
+      zw = __ffma2_rn(w1, make_float2(b.z, b.w), zw);
+      xy = __ffma2_rn(w2, make_float2(c.x, c.y), xy);
+      zw = __ffma2_rn(w2, make_float2(c.z, c.w), zw);
+      xy = __ffma2_rn(w3, make_float2(d.x, d.y), xy);
+      zw = __ffma2_rn(w3, make_float2(d.z, d.w), zw);
+      v = make_float4(xy.x, xy.y, zw.x, zw.y);
     } else {
       poff = -1;
     }
