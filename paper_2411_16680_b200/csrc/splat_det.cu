@@ -179,6 +179,9 @@ __global__ void __launch_bounds__(256) splat_fill_kernel(int64_t pairs, int64_t 
 // shared through shared memory for the composite. ppb pixels per block
 // (<= kRedPixMax, blockDim = ppb * G <= 288).
 constexpr int kRedPixMax = 64;
+#ifndef LVSG_SPLAT_PL3
+#define LVSG_SPLAT_PL3 3  // lanes per (view pixel, layer) in splat_reduce_pl3 (0: off)
+#endif
 constexpr int kRun = 8;  // runs up to this long are sorted in registers
 
 __device__ __forceinline__ void cswap(int2& a, int2& b) {
@@ -391,6 +394,110 @@ __global__ void __launch_bounds__(192) splat_reduce_pl_kernel(
   }
 }
 
+// The same reduction with three lanes per (view pixel, layer): each lane
+// sums 12 of the 36 payload channels (three 16-byte loads per entry), so a
+// warp's loads of an entry's row are one contiguous 144-byte run instead of
+// 32 lanes each fetching its own row. The run is sorted by each of the three
+// lanes (the same network), and every channel is accumulated in the same
+// sorted order as splat_reduce_pl_kernel: identical sums.
+template <int NL>
+__global__ void __launch_bounds__(192) splat_reduce_pl3_kernel(
+    const float* __restrict__ payload, int K, int M, int L, int Hv, int Wv,
+    const int* __restrict__ off, const int* __restrict__ cnt, const int2* __restrict__ ent,
+    float* __restrict__ out, int ppb, int64_t n_ent, int64_t P) {
+  pdl_grid_sync();
+  constexpr int NG = 9, CL = 36 / NL, NQ = CL / 4;  // 36 channels, CL per lane
+  extern __shared__ float s_val[];  // [ppb][L][36]: normalised channels, [Ca] = alpha
+  const int64_t PV = (int64_t)Hv * Wv;
+  const int Ca = K - 1;
+  const int GP = payload_stride(K) / 4;  // float4 per payload row
+  const int64_t t0 = (int64_t)blockIdx.x * ppb;
+  const int part = threadIdx.x % NL, bt = threadIdx.x / NL;
+  const int lp = bt / L, l = bt - lp * L;
+  const int64_t t = t0 + lp;
+  if (lp < ppb && t < (int64_t)M * PV) {
+    const int64_t pix = t % PV;
+    const int m = int(t / PV);
+    float acc[CL];
+#pragma unroll
+    for (int c = 0; c < CL; ++c) acc[c] = 0.f;
+    float ws = 0.f;
+    auto add = [&](const int2 en) {
+      const float w = __int_as_float(en.y);
+      LVSG_CHECK(en.x >= 0 && (en.x >> 2) < P);
+      const float4* row = reinterpret_cast<const float4*>(payload) + (int64_t)(en.x >> 2) * GP + NQ * part;
+      float v[CL];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const float4 t4 = __ldg(row + q);
+        v[4 * q] = t4.x, v[4 * q + 1] = t4.y, v[4 * q + 2] = t4.z, v[4 * q + 3] = t4.w;
+      }
+#pragma unroll
+      for (int c = 0; c < CL; ++c) acc[c] = fa(acc[c], fm(w, v[c]));
+      ws = fa(ws, w);
+    };
+    const int64_t bin = ((int64_t)m * L + l) * PV + pix;
+    const int n = __ldg(cnt + bin), b0 = __ldg(off + bin);
+    LVSG_CHECK(n >= 0 && b0 >= 0 && (int64_t)b0 + n <= n_ent);
+    if (n <= 4) {
+      int2 e[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) e[k] = k < n ? __ldg(ent + b0 + k) : make_int2(0x7fffffff, 0);
+      sort4(e);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k < n) add(e[k]);
+    } else if (n <= 8) {
+      int2 e[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) e[k] = k < n ? __ldg(ent + b0 + k) : make_int2(0x7fffffff, 0);
+      sort8(e);
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < n) add(e[k]);
+    } else {
+      int last = -1;  // ascending keys by repeated minimum search
+      for (int r = 0; r < n; ++r) {
+        int2 best = make_int2(0x7fffffff, 0);
+        for (int j = 0; j < n; ++j) {
+          const int2 ej = __ldg(ent + b0 + j);
+          if (ej.x > last && ej.x < best.x) best = ej;
+        }
+        last = best.x;
+        add(best);
+      }
+    }
+    const float nrm = __fdiv_rn(1.0f, ws > 1e-4f ? ws : 1e-4f);
+    float4* dst = reinterpret_cast<float4*>(s_val + ((int64_t)lp * L + l) * NG * 4) + NQ * part;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+      dst[q] = make_float4(fm(acc[4 * q], nrm), fm(acc[4 * q + 1], nrm), fm(acc[4 * q + 2], nrm),
+                           fm(acc[4 * q + 3], nrm));
+  }
+  __syncthreads();
+  // over_composite colour / alpha, layer 0 (far) first
+  for (int u = threadIdx.x; u < ppb * NG; u += blockDim.x) {
+    const int p = u / NG, g = u - p * NG;
+    const int64_t tt = t0 + p;
+    if (tt >= (int64_t)M * PV) break;
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int ll = 0; ll < L; ++ll) {
+      const float* vv = s_val + ((int64_t)p * L + ll) * NG * 4;
+      const float s = vv[Ca];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = 4 * g + k;
+        const float v = c < Ca ? vv[c] : 1.0f;
+        o[k] = fa(fm(v, s), fm(fsb(1.0f, s), o[k]));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (4 * g + k >= K) o[k] = 0.f;
+    reinterpret_cast<float4*>(out)[tt * NG + g] = make_float4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 inline int blocks_for(int64_t n, int t) { return int((n + t - 1) / t); }
 
 }  // namespace
@@ -427,6 +534,15 @@ void splat_det(const float* payload, const float* points, int L, int PL, int K,
   launch_k(splat_fill_kernel, blocks_for(pairs, 256), 256, 0, st, pairs, bins, M, (const int2*)fp_i,
            (const float4*)fp_w, (const int4*)rank, (const int*)off, ent);
   const int G = pay_stride(K) / 4;
+  if (G == 9 && L <= 192 / LVSG_SPLAT_PL3 && LVSG_SPLAT_PL3) {  // C = 32: lanes per (view pixel, layer)
+    constexpr int NL = LVSG_SPLAT_PL3 > 0 ? LVSG_SPLAT_PL3 : 1;
+    const int ppb = std::max(1, 192 / NL / L);
+    const size_t smem = size_t(ppb) * L * 36 * sizeof(float);
+    launch_k(splat_reduce_pl3_kernel<NL>, blocks_for((int64_t)M * Hv * Wv, ppb), NL * ppb * L, smem, st,
+             payload, K, M, L, Hv, Wv, (const int*)off, (const int*)cnt, (const int2*)ent, out, ppb,
+             4 * pairs, pairs / M);
+    return;
+  }
   if (G == 9 && L <= 192) {  // C = 32 configs: one thread per (view pixel, layer)
     const int ppb = std::max(1, 192 / L);
     const size_t smem = size_t(ppb) * L * 36 * sizeof(float);
