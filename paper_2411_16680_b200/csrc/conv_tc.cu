@@ -74,7 +74,9 @@ constexpr int OFF_RAW = OFF_W + W_BYTES;
 constexpr int OFF_PLANES = OFF_RAW + NR * RAW_BYTES;
 constexpr int OFF_SMALL = OFF_PLANES + NP * PLANES_BYTES;  // rms[192], bias[32], gain[32], walpha[288]
 constexpr int OFF_BAR = OFF_SMALL + (256 + 288) * 4;
-constexpr int NBAR = 2 * NR + 2 * NP + 2 * NA + NEW + 1;
+constexpr int NAL = 8;  // kAlpha: ring of per-tile alpha halos [180] (in the unused residual area)
+constexpr int NBAR = 2 * NR + 2 * NP + 2 * NA + NEW + 1 + NAL;
+static_assert(NAL * HALO_PX * 4 <= NEW * SUB_BYTES, "alpha halos fit the residual staging");
 constexpr int SMEM_BYTES = OFF_BAR + NBAR * 8 + 16;
 constexpr int NT = 64 + 128 + 128 * EPW;
 constexpr uint32_t TMEM_COLS = 64 * NA;
@@ -157,6 +159,7 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* acc_empty = mma_done + NA;       // [NA] accumulator drained
   uint64_t* res_full = acc_empty + NA;       // [NEW] residual sub-box landed
   uint64_t* w_full = res_full + NEW;         // weight image landed
+  uint64_t* alpha_full = w_full + 1;         // [NAL] kAlpha: a tile's alpha halo in smem
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
 
   tc::pdl_launch_dependents();
@@ -189,6 +192,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
     for (int k = 0; k < NEW; ++k) tc::mbar_init(&res_full[k], 1);
     tc::mbar_init(w_full, 1);
+    for (int k = 0; k < NAL; ++k) tc::mbar_init(&alpha_full[k], NCONV);
     tc::mbar_init_fence();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, TMEM_COLS);
@@ -265,6 +269,20 @@ __global__ void __launch_bounds__(NT, 1)
       const float* raw = reinterpret_cast<const float*>(smem + OFF_RAW + r * RAW_BYTES);
       uint8_t* hi = smem + OFF_PLANES + b * PLANES_BYTES;
       uint8_t* lo = hi + HALF_BYTES;
+      // kAlpha: this tile's halo of the folded alpha channel, loaded before the
+      // conversion (its latency overlaps it) and kept in smem for the epilogue
+      float alv[2] = {0.f, 0.f};
+      if constexpr (kAlpha) {
+        const TileCoord c = tile_coord(t, a.H, a.W);
+        const float* ab = a.alpha + (long long)c.b * a.alpha_bstride;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int e = ct + q * NCONV;
+          const int yy = c.y0 - 1 + e / HWD, xx = c.x0 - 1 + e % HWD;
+          if (e < HALO_PX && yy >= 0 && yy < a.H && xx >= 0 && xx < a.W)
+            alv[q] = __ldg(ab + ((long long)yy * a.W + xx) * a.alpha_pstride);
+        }
+      }
       tc::mbar_wait(&raw_full[r], uint32_t((i / NR) & 1));
       if (i >= NP) tc::mbar_wait(&planes_empty[b], uint32_t((i / NP - 1) & 1));
       for (int e = ct; e < ((LVSG_CONV_PROBE & 4) ? 0 : HALO_PX * NCH); e += NCONV) {
@@ -304,6 +322,16 @@ __global__ void __launch_bounds__(NT, 1)
       tc::fence_proxy_async();
       tc::mbar_arrive(&raw_empty[r]);
       tc::mbar_arrive(&conv_full[b]);
+      if constexpr (kAlpha) {
+        // slot i % NAL: its previous tile (i - NAL) left the epilogue before
+        // this converter could reach tile i (planes_empty of i - 2 needs the
+        // accumulator of i - 6, drained after i - 8 by the same warpgroup)
+        float* sa = reinterpret_cast<float*>(smem + OFF_RES) + (i % NAL) * HALO_PX;
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          if (ct + q * NCONV < HALO_PX) sa[ct + q * NCONV] = alv[q];
+        tc::mbar_arrive(&alpha_full[i % NAL]);
+      }
     }
     if (ovf && a.ovf) atomicOr(a.ovf, 2);
   } else {
@@ -346,17 +374,13 @@ __global__ void __launch_bounds__(NT, 1)
       const TileCoord tt = tile_coord(t, a.H, a.W);
       const bool valid = sub_valid(tt);
       float al[9];
-      if constexpr (kAlpha) {  // the folded single-channel input: its 9 taps here
+      if constexpr (kAlpha) {  // the folded single-channel input: its 9 taps, from the halo
         const int row = q * 32 + lane;  // tile row m <-> pixel (y0 + m/8, x0 + m%8)
-        const int py = tt.y0 + (row >> 3), px = tt.x0 + (row & 7);
-        const float* ab = a.alpha + (long long)tt.b * a.alpha_bstride;
+        tc::mbar_wait(&alpha_full[i % NAL], uint32_t((i / NAL) & 1));
+        const float* sa = reinterpret_cast<const float*>(smem + OFF_RES) + (i % NAL) * HALO_PX;
 #pragma unroll
-        for (int tap = 0; tap < 9; ++tap) {
-          const int yy = py + tap / 3 - 1, xx = px + tap % 3 - 1;
-          al[tap] = (yy >= 0 && yy < a.H && xx >= 0 && xx < a.W)
-                        ? __ldg(ab + ((long long)yy * a.W + xx) * a.alpha_pstride)
-                        : 0.f;
-        }
+        for (int tap = 0; tap < 9; ++tap)
+          al[tap] = sa[((row >> 3) + tap / 3) * HWD + (row & 7) + tap % 3];  // zero outside
       }
 #pragma unroll
       for (int c = 0; c < 32; ++c) d0[c] = fmaf(d1[c], 1.0f / tc::kF16LoScale, d0[c]);
@@ -365,15 +389,16 @@ __global__ void __launch_bounds__(NT, 1)
         // weights as 16-byte broadcasts (taps ascending per channel)
 #pragma unroll
         for (int c4 = 0; c4 < 8; ++c4) {
-          float s4[4] = {0.f, 0.f, 0.f, 0.f};
+          // packed f32x2 FMAs (FFMA2: the same per-lane roundings as fmaf)
+          float2 s01 = make_float2(0.f, 0.f), s23 = make_float2(0.f, 0.f);
 #pragma unroll
           for (int tap = 0; tap < 9; ++tap) {
             const float4 w = reinterpret_cast<const float4*>(walpha_s + tap * 32)[c4];
-            s4[0] = fmaf(al[tap], w.x, s4[0]);
-            s4[1] = fmaf(al[tap], w.y, s4[1]);
-            s4[2] = fmaf(al[tap], w.z, s4[2]);
-            s4[3] = fmaf(al[tap], w.w, s4[3]);
+            const float2 a2 = make_float2(al[tap], al[tap]);
+            s01 = __ffma2_rn(a2, make_float2(w.x, w.y), s01);
+            s23 = __ffma2_rn(a2, make_float2(w.z, w.w), s23);
           }
+          const float s4[4] = {s01.x, s01.y, s23.x, s23.y};
 #pragma unroll
           for (int k = 0; k < 4; ++k) d0[4 * c4 + k] = fa(d0[4 * c4 + k], s4[k]);
         }
@@ -554,6 +579,8 @@ void conv3x3_tc(const ConvArgs& a, cudaStream_t st) {
                                               : conv3x3_tc_kernel<false, 0>;
   smem_optin(reinterpret_cast<const void*>(kern), SMEM_BYTES);
   if (a.alpha && a.pool_out) throw CudaError("conv3x3_tc: alpha and pool together are not built");
+  // the alpha halos live in the residual staging area
+  if (a.alpha && a.resid) throw CudaError("conv3x3_tc: alpha and a residual together are not built");
   if (cudaLaunchKernelEx(&cfg, kern, xmap, omap, rmap, a, tiles) != cudaSuccess)
     throw CudaError("conv3x3_tc: launch failed");
 }
