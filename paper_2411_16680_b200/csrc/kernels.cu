@@ -913,27 +913,30 @@ __global__ void stage_gather_kernel(DevCam cam, const float* image, int Hi, int 
 
 // resize_hwc for RGB (the input-side decimation of the views): one thread
 // per output pixel, taps computed once for its three channels.
-__global__ void resize_rgb_kernel(const float* __restrict__ in, float* __restrict__ out, int B,
-                                  int H, int W, int Ho, int Wo) {
+// 3-channel resize (the input-side decimation), one block row per output
+// image row (b, y): the y taps once per thread, scales divided on the host,
+// 32-bit index math (the caller checks the sizes)
+__global__ void __launch_bounds__(256) resize_rgb_kernel(const float* __restrict__ in,
+                                                         float* __restrict__ out, int H, int W,
+                                                         int Ho, int Wo, double sy, double sx) {
   pdl_grid_sync();
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= (int64_t)B * Ho * Wo) return;
-  const int x = int(i % Wo);
-  const int64_t t = i / Wo;
-  const int y = int(t % Ho);
-  const int b = int(t / Ho);
-  int y0, y1, x0, x1;
-  float fy, fx;
-  resize_tap(y, H, Ho, y0, y1, fy);
-  resize_tap(x, W, Wo, x0, x1, fx);
-  const float* s = in + (int64_t)b * H * W * 3;
-  const float* p00 = s + ((int64_t)y0 * W + x0) * 3;
-  const float* p10 = s + ((int64_t)y0 * W + x1) * 3;
-  const float* p01 = s + ((int64_t)y1 * W + x0) * 3;
-  const float* p11 = s + ((int64_t)y1 * W + x1) * 3;
+  const int row = blockIdx.y;  // b * Ho + y
+  const int b = row / Ho, y = row - b * Ho;
+  int y0, y1;
+  float fy;
+  resize_tap_s(y, sy, H, y0, y1, fy);
+  const float* s0 = in + ((int64_t)b * H + y0) * W * 3;
+  const float* s1 = in + ((int64_t)b * H + y1) * W * 3;
+  float* o = out + (int64_t)row * Wo * 3;
+  for (int x = blockIdx.x * 256 + threadIdx.x; x < Wo; x += gridDim.x * 256) {
+    int x0, x1;
+    float fx;
+    resize_tap_s(x, sx, W, x0, x1, fx);
 #pragma unroll
-  for (int c = 0; c < 3; ++c)
-    out[i * 3 + c] = lerp2(__ldg(p00 + c), __ldg(p10 + c), __ldg(p01 + c), __ldg(p11 + c), fx, fy);
+    for (int c = 0; c < 3; ++c)
+      o[x * 3 + c] = lerp2(__ldg(s0 + x0 * 3 + c), __ldg(s0 + x1 * 3 + c), __ldg(s1 + x0 * 3 + c),
+                           __ldg(s1 + x1 * 3 + c), fx, fy);
+  }
 }
 
 }  // namespace
@@ -993,9 +996,12 @@ void resize_hwc(const float* in, float* out, int B, int H, int W, int C, int Ho,
     return;
   }
   if (C == 3) {
-    launch_k(resize_rgb_kernel, blocks_for((int64_t)B * Ho * Wo, 256), 256, 0, st, in, out, B, H, W,
-             Ho, Wo);
-    return;
+    if ((int64_t)B * Ho < 65536 && (int64_t)W * 3 < (int64_t(1) << 31)) {
+      const dim3 grid(unsigned(std::min<int64_t>((Wo + 255) / 256, 8)), unsigned(B * Ho));
+      launch_k(resize_rgb_kernel, grid, 256, 0, st, in, out, H, W, Ho, Wo,
+               double(H) / double(Ho), double(W) / double(Wo));
+      return;
+    }
   }
   launch_k(resize_hwc_kernel, blocks_for(n, 256), 256, 0, st, in, out, B, H, W, C, Ho, Wo);
 }
