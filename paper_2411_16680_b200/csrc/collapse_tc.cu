@@ -224,9 +224,12 @@ __global__ void __launch_bounds__(TILE, 2)
         tc::tmem_ld32(lane_base + d1 + uint32_t(32 * half), h + 32 * half);
         tc::tmem_ld32(lane_base + d1 + uint32_t(N1 + 32 * half), lo);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const float v = fmaf(lo[c], 1.0f / tc::kF16LoScale, h[32 * half + c]);
-          h[32 * half + c] = gelu_ref(fa(v, __ldg(b1 + 32 * half + c)));
+        for (int c = 0; c < 32; c += 2) {
+          const float v0 = fmaf(lo[c], 1.0f / tc::kF16LoScale, h[32 * half + c]);
+          const float v1 = fmaf(lo[c + 1], 1.0f / tc::kF16LoScale, h[32 * half + c + 1]);
+          const float2 g = gelu2_ref(make_float2(fa(v0, __ldg(b1 + 32 * half + c)),
+                                                 fa(v1, __ldg(b1 + 32 * half + c + 1))));
+          h[32 * half + c] = g.x, h[32 * half + c + 1] = g.y;
         }
       }
     }

@@ -47,6 +47,9 @@
 #define LVSG_CONV_PROBE 0
 #endif
 
+#ifndef LVSG_GELU2
+#define LVSG_GELU2 1
+#endif
 namespace lvsg {
 namespace {
 
@@ -404,11 +407,19 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        float y_ = d0[c];
-        if (a.bias) y_ = fa(y_, bias_s[c]);
-        if (a.gelu) y_ = gelu_ref(y_);
-        d0[c] = y_;
+      for (int c = 0; c < 32; ++c)
+        if (a.bias) d0[c] = fa(d0[c], bias_s[c]);
+      if (a.gelu) {
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+#if LVSG_GELU2
+          const float2 g2 = gelu2_ref(make_float2(d0[c], d0[c + 1]));
+          d0[c] = g2.x, d0[c + 1] = g2.y;
+#else
+          d0[c] = gelu_ref(d0[c]);
+          d0[c + 1] = gelu_ref(d0[c + 1]);
+#endif
+        }
       }
       if (has_res && valid) {
         tc::mbar_wait(&res_full[ew], rph);
