@@ -386,7 +386,12 @@ __global__ void __launch_bounds__(NT, 1)
           al[tap] = sa[((row >> 3) + tap / 3) * HWD + (row & 7) + tap % 3];  // zero outside
       }
 #pragma unroll
-      for (int c = 0; c < 32; ++c) d0[c] = fmaf(d1[c], 1.0f / tc::kF16LoScale, d0[c]);
+      for (int c = 0; c < 32; c += 2) {  // D[:, c] + 2^-11 D[:, 32 + c], packed (FFMA2)
+        const float2 s = __ffma2_rn(make_float2(d1[c], d1[c + 1]),
+                                    make_float2(1.0f / tc::kF16LoScale, 1.0f / tc::kF16LoScale),
+                                    make_float2(d0[c], d0[c + 1]));
+        d0[c] = s.x, d0[c + 1] = s.y;
+      }
       if constexpr (kAlpha) {
         // the folded channel's 9 taps for 4 output channels per step, the
         // weights as 16-byte broadcasts (taps ascending per channel)
@@ -406,9 +411,13 @@ __global__ void __launch_bounds__(NT, 1)
           for (int k = 0; k < 4; ++k) d0[4 * c4 + k] = fa(d0[4 * c4 + k], s4[k]);
         }
       }
+      if (a.bias) {
 #pragma unroll
-      for (int c = 0; c < 32; ++c)
-        if (a.bias) d0[c] = fa(d0[c], bias_s[c]);
+        for (int c = 0; c < 32; c += 2) {  // packed adds (FADD2); nothing multiplies into them
+          const float2 s = __fadd2_rn(make_float2(d0[c], d0[c + 1]), make_float2(bias_s[c], bias_s[c + 1]));
+          d0[c] = s.x, d0[c + 1] = s.y;
+        }
+      }
       if (a.gelu) {
 #pragma unroll
         for (int c = 0; c < 32; c += 2) {
