@@ -528,6 +528,10 @@ __global__ void gather_stack_kernel(const float* __restrict__ feats, int M, int 
 #ifndef LVSG_GATHER_CS
 #define LVSG_GATHER_CS 1
 #endif
+#ifndef LVSG_GATHER_UNROLL
+#define LVSG_GATHER_UNROLL 8
+#endif
+constexpr int kGatherUnroll = LVSG_GATHER_UNROLL;
 __global__ void __launch_bounds__(256, 6) gather_stack32_kernel(
     const float* __restrict__ feats, int M, int Hf, int Wf, const DevCam* __restrict__ cams,
     DevRayCam rc, const float* __restrict__ depth, int L, int H, int W, float* __restrict__ deltas) {
@@ -566,7 +570,7 @@ __global__ void __launch_bounds__(256, 6) gather_stack32_kernel(
   // its left (x0) / right (x1) columns at rows y0 / y1
   int poff = -1, pfl = 0;
   float4 l0 = make_float4(0.f, 0.f, 0.f, 0.f), l1 = l0, r0 = l0, r1 = l0;
-#pragma unroll 2
+#pragma unroll kGatherUnroll
   for (int it = 0; it < 8; ++it) {
     const int r = 8 * q + it;
     const int rf = __shfl_sync(0xffffffffu, flags, r);
