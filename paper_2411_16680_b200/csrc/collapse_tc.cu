@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(TILE, 4)
     }
     const int lane = tid & 31, wbase = tid & ~31, g = lane & 7;
     const float4* b4 = reinterpret_cast<const float4*>(base);
-#pragma unroll 4
+#pragma unroll 8
     for (int k = 0; k < 8; ++k) {
       const int src = 4 * k + (lane >> 3);
       const int s00 = __shfl_sync(0xffffffffu, r00, src), s01 = __shfl_sync(0xffffffffu, r01, src);
